@@ -1,0 +1,502 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into or called by the product.
+//
+// Thin extern "C" driver over the UNMODIFIED reference C++ implementation
+// (/root/reference/proj/include + src/*.cpp, compiled in place by
+// oracle/Makefile into oracle/_ref/libttref.so).  It exists so that
+//   * tests/ can pin the C restatement (oracle/tt_oracle.c) and the CUDA
+//     path against the reference's own forward_bags / backward_bags /
+//     sgd_step / lookup_row / LfuCache on identical inputs,
+//   * tests/golden/ fixtures are produced by the reference's own RNG,
+//     initializer and Zipf sampler (libstdc++-specific streams), and
+//   * bench.py's cpu_baseline / --impl reference arm times the reference's
+//     own OpenMP CPU path.
+// Nothing here re-implements reference arithmetic: every call forwards to
+// the reference symbol named in its comment.
+#include <omp.h>
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "ttrec/data.hpp"
+#include "ttrec/embedding_ops.hpp"
+#include "ttrec/embedding_stats.hpp"
+#include "ttrec/initializer.hpp"
+#include "ttrec/lfu_cache.hpp"
+#include "ttrec/shape_plan.hpp"
+#include "ttrec/tt_table.hpp"
+
+using namespace ttrec;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+struct RefTable {
+  int dtype = 0;  // 0 f32, 1 f64
+  std::unique_ptr<TtTable<float>> f;
+  std::unique_ptr<TtTable<double>> d;
+  const ShapePlan& plan() const { return dtype ? d->plan() : f->plan(); }
+};
+
+struct RefCtx {
+  int dtype = 0;
+  ForwardContext<float> f;
+  ForwardContext<double> d;
+};
+
+IndexBatch make_batch(const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                      const double* w, int pooling) {
+  IndexBatch b;
+  b.indices.assign(idx, idx + L);
+  b.offsets.assign(off, off + B + 1);
+  if (w) b.weights.assign(w, w + L);
+  b.pooling = pooling ? Pooling::Mean : Pooling::Sum;
+  return b;
+}
+
+ShapePlan plan_from(int64_t rows, int64_t emb, int d, const int64_t* rf, const int64_t* cf,
+                    const int64_t* rk) {
+  ShapePlan p;
+  p.num_rows = rows;
+  p.emb_dim = emb;
+  p.tt_dim = d;
+  p.row_factors.assign(rf, rf + d);
+  p.col_factors.assign(cf, cf + d);
+  p.ranks.assign(rk, rk + d + 1);
+  return p;
+}
+
+template <class T>
+TtTable<T>& tab(RefTable* t);
+template <>
+TtTable<float>& tab<float>(RefTable* t) { return *t->f; }
+template <>
+TtTable<double>& tab<double>(RefTable* t) { return *t->d; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ttrec::plan_shapes (shape_plan.cpp:142-169).  rf_in/cf_in may be null.
+int ref_plan_shapes(int64_t rows, int64_t emb, int d, int64_t rank, const int64_t* rf_in,
+                    const int64_t* cf_in, int64_t* rf_out, int64_t* cf_out, int64_t* rk_out,
+                    int64_t* padded, int64_t* params, int64_t* reduction) {
+  return guarded([&] {
+    std::optional<std::vector<index_t>> rf, cf;
+    if (rf_in) rf = std::vector<index_t>(rf_in, rf_in + d);
+    if (cf_in) cf = std::vector<index_t>(cf_in, cf_in + d);
+    ShapePlan p = plan_shapes(rows, emb, d, rank, rf, cf);
+    std::memcpy(rf_out, p.row_factors.data(), sizeof(int64_t) * d);
+    std::memcpy(cf_out, p.col_factors.data(), sizeof(int64_t) * d);
+    std::memcpy(rk_out, p.ranks.data(), sizeof(int64_t) * (d + 1));
+    *padded = p.padded_rows();
+    *params = p.parameter_count();
+    *reduction = p.memory_reduction();
+  });
+}
+
+// ttrec::decompose_index (shape_plan.cpp:171-185)
+int ref_decompose_index(int64_t flat, const int64_t* radices, int n, int64_t* out) {
+  return guarded([&] {
+    auto v = decompose_index(flat, std::span<const index_t>(radices, n));
+    std::memcpy(out, v.data(), sizeof(int64_t) * n);
+  });
+}
+
+int ref_table_create(int64_t rows, int64_t emb, int d, const int64_t* rf, const int64_t* cf,
+                     const int64_t* rk, int dtype, const char* name, void** out) {
+  return guarded([&] {
+    auto* t = new RefTable;
+    t->dtype = dtype;
+    ShapePlan p = plan_from(rows, emb, d, rf, cf, rk);
+    if (dtype)
+      t->d = std::make_unique<TtTable<double>>(p, name);
+    else
+      t->f = std::make_unique<TtTable<float>>(p, name);
+    *out = t;
+  });
+}
+
+void ref_table_destroy(void* t) { delete static_cast<RefTable*>(t); }
+
+int64_t ref_core_size(void* h, int k) {
+  auto* t = static_cast<RefTable*>(h);
+  return t->dtype ? (int64_t)t->d->core(k).size() : (int64_t)t->f->core(k).size();
+}
+
+// Raw bytes of TtTable::core(k) (tt_table.hpp:43-44), (m_k, R_{k-1}, n_k, R_k) layout.
+void ref_set_core(void* h, int k, const void* src) {
+  auto* t = static_cast<RefTable*>(h);
+  if (t->dtype) {
+    auto c = t->d->core(k);
+    std::memcpy(c.data(), src, c.size() * sizeof(double));
+    t->d->mark_mutated();
+  } else {
+    auto c = t->f->core(k);
+    std::memcpy(c.data(), src, c.size() * sizeof(float));
+    t->f->mark_mutated();
+  }
+}
+
+void ref_get_core(void* h, int k, void* dst) {
+  auto* t = static_cast<RefTable*>(h);
+  if (t->dtype) {
+    auto c = t->d->core(k);
+    std::memcpy(dst, c.data(), c.size() * sizeof(double));
+  } else {
+    auto c = t->f->core(k);
+    std::memcpy(dst, c.data(), c.size() * sizeof(float));
+  }
+}
+
+// ttrec::init_tt_cores(table, InitSpec::sampled_gaussian(), seed) (initializer.hpp:143-154)
+int ref_init_sampled_gaussian(void* h, uint64_t seed) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    if (t->dtype)
+      init_tt_cores(*t->d, InitSpec::sampled_gaussian(), seed);
+    else
+      init_tt_cores(*t->f, InitSpec::sampled_gaussian(), seed);
+  });
+}
+
+// oracle_helpers.hpp:55-62 fill_cores: Rng::derive(seed,k).normal()*scale per core
+void ref_fill_cores_normal(void* h, uint64_t seed, double scale) {
+  auto* t = static_cast<RefTable*>(h);
+  const int d = t->plan().tt_dim;
+  for (int k = 0; k < d; ++k) {
+    Rng rng = Rng::derive(seed, static_cast<uint64_t>(k));
+    if (t->dtype)
+      for (double& v : t->d->core(k)) v = scale * rng.normal();
+    else
+      for (float& v : t->f->core(k)) v = static_cast<float>(scale * rng.normal());
+  }
+  if (t->dtype)
+    t->d->mark_mutated();
+  else
+    t->f->mark_mutated();
+}
+
+void ref_set_threads(int n) { omp_set_num_threads(n); }
+int ref_max_threads() { return omp_get_max_threads(); }
+
+// ttrec::forward_bags (embedding_ops.hpp:159-253).  *ctx_out receives a
+// context usable by ref_backward; free with ref_ctx_destroy.
+int ref_forward(void* h, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                const double* w, int pooling, int64_t micro_batch, int save, void* out,
+                void** ctx_out) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    IndexBatch b = make_batch(idx, L, off, B, w, pooling);
+    auto* ctx = new RefCtx;
+    ctx->dtype = t->dtype;
+    if (t->dtype) {
+      auto r = forward_bags(*t->d, b, micro_batch, save != 0);
+      std::memcpy(out, r.output.data(), r.output.size() * sizeof(double));
+      ctx->d = std::move(r.context);
+    } else {
+      auto r = forward_bags(*t->f, b, micro_batch, save != 0);
+      std::memcpy(out, r.output.data(), r.output.size() * sizeof(float));
+      ctx->f = std::move(r.context);
+    }
+    if (ctx_out)
+      *ctx_out = ctx;
+    else
+      delete ctx;
+  });
+}
+
+void ref_ctx_destroy(void* c) { delete static_cast<RefCtx*>(c); }
+
+// ttrec::backward_bags (embedding_ops.hpp:260-358).  grads[k] receives core k's
+// dense gradient (same layout and size as the core).
+int ref_backward(void* h, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                 const double* w, int pooling, void* c, const void* grad, int64_t grad_len,
+                 void** grads) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    auto* ctx = static_cast<RefCtx*>(c);
+    IndexBatch b = make_batch(idx, L, off, B, w, pooling);
+    if (t->dtype) {
+      auto g = backward_bags(*t->d, b, ctx->d,
+                             std::span<const double>((const double*)grad, grad_len));
+      for (size_t k = 0; k < g.cores.size(); ++k)
+        std::memcpy(grads[k], g.cores[k].data(), g.cores[k].size() * sizeof(double));
+    } else {
+      auto g = backward_bags(*t->f, b, ctx->f,
+                             std::span<const float>((const float*)grad, grad_len));
+      for (size_t k = 0; k < g.cores.size(); ++k)
+        std::memcpy(grads[k], g.cores[k].data(), g.cores[k].size() * sizeof(float));
+    }
+  });
+}
+
+// ttrec::ref::forward_bags (embedding_ops.hpp:382-423), serial.
+int ref_serial_forward(void* h, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                       const double* w, int pooling, void* out) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    IndexBatch b = make_batch(idx, L, off, B, w, pooling);
+    if (t->dtype) {
+      auto o = ref::forward_bags(*t->d, b);
+      std::memcpy(out, o.data(), o.size() * sizeof(double));
+    } else {
+      auto o = ref::forward_bags(*t->f, b);
+      std::memcpy(out, o.data(), o.size() * sizeof(float));
+    }
+  });
+}
+
+// ttrec::ref::backward_bags (embedding_ops.hpp:426-490), serial.
+int ref_serial_backward(void* h, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                        const double* w, int pooling, const void* grad, int64_t grad_len,
+                        void** grads) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    IndexBatch b = make_batch(idx, L, off, B, w, pooling);
+    if (t->dtype) {
+      auto g = ref::backward_bags(*t->d, b,
+                                  std::span<const double>((const double*)grad, grad_len));
+      for (size_t k = 0; k < g.cores.size(); ++k)
+        std::memcpy(grads[k], g.cores[k].data(), g.cores[k].size() * sizeof(double));
+    } else {
+      auto g = ref::backward_bags(*t->f, b,
+                                  std::span<const float>((const float*)grad, grad_len));
+      for (size_t k = 0; k < g.cores.size(); ++k)
+        std::memcpy(grads[k], g.cores[k].data(), g.cores[k].size() * sizeof(float));
+    }
+  });
+}
+
+// ttrec::sgd_step (embedding_ops.hpp:361-376) with caller-supplied grads.
+int ref_sgd(void* h, const void* const* grads, double lr) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    const int d = t->plan().tt_dim;
+    if (t->dtype) {
+      auto g = CoreGradients<double>::zeros_like(*t->d);
+      for (int k = 0; k < d; ++k)
+        std::memcpy(g.cores[k].data(), grads[k], g.cores[k].size() * sizeof(double));
+      sgd_step(*t->d, g, lr);
+    } else {
+      auto g = CoreGradients<float>::zeros_like(*t->f);
+      for (int k = 0; k < d; ++k)
+        std::memcpy(g.cores[k].data(), grads[k], g.cores[k].size() * sizeof(float));
+      sgd_step(*t->f, g, lr);
+    }
+  });
+}
+
+// ttrec::lookup_row (embedding_ops.hpp:120-152)
+int ref_lookup_row(void* h, int64_t row, void* out) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    if (t->dtype) {
+      auto v = lookup_row(*t->d, row);
+      std::memcpy(out, v.data(), v.size() * sizeof(double));
+    } else {
+      auto v = lookup_row(*t->f, row);
+      std::memcpy(out, v.data(), v.size() * sizeof(float));
+    }
+  });
+}
+
+// ttrec::reconstruct_full (tt_table.hpp:104-146): dense oracle sharing no code with the chain.
+int ref_reconstruct_full(void* h, void* out) {
+  return guarded([&] {
+    auto* t = static_cast<RefTable*>(h);
+    if (t->dtype) {
+      auto v = reconstruct_full(*t->d);
+      std::memcpy(out, v.data(), v.size() * sizeof(double));
+    } else {
+      auto v = reconstruct_full(*t->f);
+      std::memcpy(out, v.data(), v.size() * sizeof(float));
+    }
+  });
+}
+
+void ref_stats_reset() { EmbeddingStats::reset(); }
+uint64_t ref_stats_rows() { return EmbeddingStats::tt_rows_computed(); }
+
+// ---- reference RNG / data streams (rng.hpp, data.cpp) -------------------
+
+void ref_rng_normal(uint64_t seed, int64_t n, double* out) {
+  Rng rng(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = rng.normal();
+}
+
+void ref_rng_uniform_int(uint64_t seed, int64_t lo, int64_t hi, int64_t n, int64_t* out) {
+  Rng rng(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = rng.uniform_int(lo, hi);
+}
+
+// oracle_helpers.hpp:65-77 random_batch; offsets has room for bags+1, indices/weights
+// for bags*max_size.  Returns the lookup count.
+int64_t ref_random_batch(uint64_t seed, int64_t rows, int64_t bags, int64_t min_size,
+                         int64_t max_size, int weighted, int64_t* idx, int64_t* off,
+                         double* w) {
+  Rng rng(seed);
+  int64_t n = 0;
+  off[0] = 0;
+  for (int64_t b = 0; b < bags; ++b) {
+    const int64_t sz = rng.uniform_int(min_size, max_size + 1);
+    for (int64_t t = 0; t < sz; ++t) idx[n++] = rng.uniform_int(0, rows);
+    off[b + 1] = n;
+  }
+  if (weighted)
+    for (int64_t t = 0; t < n; ++t) w[t] = rng.uniform(-2.0, 2.0);
+  return n;
+}
+
+// ZipfianSampler + generate_zipfian_batch (data.cpp:8-47) with Rng(seed).
+int ref_zipf_batch(int64_t population, double exponent, uint64_t seed, int64_t bags,
+                   int64_t pooling_factor, int64_t* idx, int64_t* off) {
+  return guarded([&] {
+    ZipfianSampler zs(population, exponent);
+    Rng rng(seed);
+    IndexBatch b = generate_zipfian_batch(zs, rng, bags, pooling_factor);
+    std::memcpy(idx, b.indices.data(), b.indices.size() * sizeof(int64_t));
+    std::memcpy(off, b.offsets.data(), b.offsets.size() * sizeof(int64_t));
+  });
+}
+
+// ---- LFU cache (lfu_cache.hpp / lfu_cache.cpp) ----------------------------
+
+struct RefCache {
+  std::unique_ptr<LfuCache<float>> c;
+  CachePartition last;
+};
+
+int ref_cache_create(int64_t capacity, int64_t emb, int64_t refresh, void** out) {
+  return guarded([&] {
+    auto* rc = new RefCache;
+    rc->c = std::make_unique<LfuCache<float>>(capacity, emb, refresh);
+    *out = rc;
+  });
+}
+void ref_cache_destroy(void* c) { delete static_cast<RefCache*>(c); }
+int64_t ref_cache_default_capacity(int64_t rows) {
+  return LfuCache<float>::default_capacity(rows);
+}
+
+// LfuCache::record_and_partition (lfu_cache.hpp:187-219).  Sizes of the two
+// parts are returned; fetch them with ref_cache_last_partition.
+int ref_cache_record_and_partition(void* c, const int64_t* idx, int64_t L, const int64_t* off,
+                                   int64_t B, const double* w, int pooling, int64_t* n_cached,
+                                   int64_t* n_tt) {
+  return guarded([&] {
+    auto* rc = static_cast<RefCache*>(c);
+    rc->last = rc->c->record_and_partition(make_batch(idx, L, off, B, w, pooling));
+    *n_cached = rc->last.cached.num_lookups();
+    *n_tt = rc->last.tt.num_lookups();
+  });
+}
+
+void ref_cache_last_partition(void* c, int64_t* cached_slots, int64_t* cached_rows,
+                              int64_t* cached_off, int64_t* tt_idx, int64_t* tt_off) {
+  auto* rc = static_cast<RefCache*>(c);
+  const auto& p = rc->last;
+  std::memcpy(cached_slots, p.cached.indices.data(), p.cached.indices.size() * 8);
+  std::memcpy(cached_rows, p.cached_rows.data(), p.cached_rows.size() * 8);
+  std::memcpy(cached_off, p.cached.offsets.data(), p.cached.offsets.size() * 8);
+  std::memcpy(tt_idx, p.tt.indices.data(), p.tt.indices.size() * 8);
+  std::memcpy(tt_off, p.tt.offsets.data(), p.tt.offsets.size() * 8);
+}
+
+void ref_cache_record(void* c, const int64_t* idx, int64_t L) {
+  IndexBatch b;
+  b.indices.assign(idx, idx + L);
+  b.offsets = {0, L};
+  static_cast<RefCache*>(c)->c->record(b);
+}
+
+int ref_cache_warmup_finalize(void* c, void* t) {
+  return guarded([&] {
+    static_cast<RefCache*>(c)->c->warmup_finalize(*static_cast<RefTable*>(t)->f);
+  });
+}
+
+int ref_cache_refresh(void* c, void* t, double* drift) {
+  return guarded([&] {
+    *drift = static_cast<RefCache*>(c)->c->refresh(*static_cast<RefTable*>(t)->f);
+  });
+}
+
+int64_t ref_cache_hot_rows(void* c, int64_t* out) {
+  auto rows = static_cast<RefCache*>(c)->c->hot_rows();
+  if (out) std::memcpy(out, rows.data(), rows.size() * 8);
+  return (int64_t)rows.size();
+}
+
+int64_t ref_cache_slot_of(void* c, int64_t row) {
+  return static_cast<RefCache*>(c)->c->slot_of(row);
+}
+
+void ref_cache_row_values(void* c, int64_t slot, float* out) {
+  auto v = static_cast<RefCache*>(c)->c->row_values(slot);
+  std::memcpy(out, v.data(), v.size() * sizeof(float));
+}
+
+double ref_cache_hit_rate(void* c) { return static_cast<RefCache*>(c)->c->hit_rate(); }
+
+uint64_t ref_cache_freq(void* c, int64_t row) {
+  return static_cast<RefCache*>(c)->c->freq().count(row);
+}
+
+int64_t ref_cache_top_k(void* c, int64_t k, int64_t* out) {
+  auto v = static_cast<RefCache*>(c)->c->freq().top_k(static_cast<size_t>(k));
+  std::memcpy(out, v.data(), v.size() * 8);
+  return (int64_t)v.size();
+}
+
+// ---- CPU baseline timing: the reference's own OpenMP path -----------------
+// One step = forward_bags(save=true) + backward_bags + sgd_step, fp32, the
+// sequence SURVEY.md §8(d) / BASELINE.md §3 specifies.  Returns the median
+// seconds per step over `reps` (after one warm-up step).
+double ref_time_step(void* h, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                     const float* grad, double lr, int reps, int threads) {
+  auto* t = static_cast<RefTable*>(h);
+  if (threads > 0) omp_set_num_threads(threads);
+  IndexBatch b = make_batch(idx, L, off, B, nullptr, 0);
+  std::span<const float> g(grad, static_cast<size_t>(B) * t->f->cols());
+  auto step = [&] {
+    auto r = forward_bags(*t->f, b, kDefaultMicroBatch, true);
+    auto gr = backward_bags(*t->f, b, r.context, g);
+    sgd_step(*t->f, gr, lr);
+  };
+  step();
+  std::vector<double> ts;
+  for (int i = 0; i < reps; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    step();
+    ts.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+  std::sort(ts.begin(), ts.end());
+  return ts.empty() ? 0.0 : ts[ts.size() / 2];
+}
+
+}  // extern "C"
