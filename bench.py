@@ -1,0 +1,429 @@
+"""TT-EmbeddingBag fwd+bwd+SGD throughput (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config cfg2]
+
+One step = forward_bags(save) + backward_bags + sgd_step over one batch of
+the configuration's synthetic index stream (cfg2 = BASELINE configs[1]:
+10,131,227 x 16, R=32, 65,536 bags x 1 index, Zipf(1.05)).  Per GPU the batch
+is fixed (weak scaling); N>1 runs one process per GPU (torchrun) and sums the
+dense core gradients with an NCCL allreduce before the identical SGD.
+
+Timing: W untimed warm-up steps, then K steps, each replayed from a CUDA graph
+of the whole step and bracketed by CUDA events on the table's stream; L2 is
+flushed (256 MiB write) before every timed step and the flush is outside the
+events.  Multi-GPU: barrier + synchronize around the timed region and the max
+over ranks.  `e2e` repeats the step through the reference-facing host C-ABI
+calls (host buffers, H2D of indices/offsets/grad_out and D2H of the pooled
+output inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TT-EmbeddingBag fwd+bwd indices/sec (11M×16, rank 32, batch 64K) at 1/2/4/8 GPU"
+
+CONFIGS = {
+    # name: rows, emb, row_factors, col_factors, rank, bags, pooling_factor, zipf exponent
+    "cfg1": dict(rows=1000000, emb=16, rf=[100, 100, 100], cf=[2, 2, 4], rank=16, bags=4096,
+                 pf=1, zipf=0.0,
+                 desc="1M rows (100x100x100), dim 16 (2x2x4), R=16, 4096 bags x 1, uniform"),
+    "cfg2": dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32, bags=65536,
+                 pf=1, zipf=1.05,
+                 desc="10,131,227 rows (200x220x250), dim 16 (2x2x4), R=32, 65,536 bags x 1, "
+                      "Zipf(1.05), fwd+bwd+SGD"),
+    "cfg2u": dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32, bags=65536,
+                  pf=1, zipf=0.0, desc="cfg2 shape with uniform indices"),
+    "cfg3": dict(rows=40000000, emb=64, rf=[200, 200, 1000], cf=[4, 4, 4], rank=64, bags=65536,
+                 pf=32, zipf=0.0,
+                 desc="40M rows (200x200x1000), dim 64 (4x4x4), R=64, 65,536 bags x 32, uniform"),
+}
+LR = 0.01
+
+
+def flops_per_lookup(rf, cf, ranks):
+    """F_fwd = 2*sum_{k>=1} prefix[k-1]*R_k*n_k*R_{k+1}; F_bwd = 2*F_fwd."""
+    d = len(rf)
+    pre = [int(np.prod(cf[: k + 1])) for k in range(d)]
+    f = sum(2 * pre[k - 1] * ranks[k] * cf[k] * ranks[k + 1] for k in range(1, d))
+    return 3 * f
+
+
+def bytes_per_step(L, B, N, params):
+    """Algorithmic HBM bytes per step: indices + offsets read twice (fwd, bwd),
+    pooled output written, grad_out read, cores read + written once."""
+    return 2 * 8 * L + 2 * 8 * (B + 1) + 4 * B * N + 4 * B * N + 2 * 4 * params
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def make_inputs(cfg, seed, tt):
+    if cfg["zipf"] > 0:
+        b = tt.generate_zipfian_batch(cfg["rows"], cfg["zipf"], seed, cfg["bags"], cfg["pf"])
+        idx, off = b.indices, b.offsets
+    else:
+        idx = tt.uniform_indices(cfg["rows"], seed, cfg["bags"] * cfg["pf"])
+        off = np.arange(0, cfg["bags"] * cfg["pf"] + 1, cfg["pf"], dtype=np.int64)
+    g = np.random.default_rng(seed + 1000).standard_normal((cfg["bags"], cfg["emb"]))
+    return idx, off, g.astype(np.float32)
+
+
+def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0):
+    """The reference's own OpenMP CPU step (oracle/_ref, compiled from the
+    reference sources) on this host's cores; falls back to the C restatement."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    threads = os.cpu_count() or 1
+    plan = pyoracle.Plan(cfg["rows"], cfg["emb"], cfg["rf"], cfg["cf"],
+                         [1] + [cfg["rank"]] * (len(cfg["rf"]) - 1) + [1])
+    L = len(idx)
+    if pyoracle.ref_available():
+        ref = pyoracle.RefImpl()
+        t = ref.table(plan, np.float32, "cpu")
+        t.init_sampled_gaussian(1)
+        first = t.time_step(idx, off, grad, LR, reps=1, threads=threads)
+        reps = int(max(3, min(50, budget_s / max(first, 1e-6))))
+        sec = t.time_step(idx, off, grad, LR, reps=reps, threads=threads)
+        kind = "reference"
+    else:
+        orc = pyoracle.Oracle()
+        rng = np.random.default_rng(0)
+        cores = [rng.standard_normal(plan.core_size(k)).astype(np.float32) * 0.3
+                 for k in range(plan.tt_dim)]
+        ts = [orc.time_step(plan, cores, idx, off, grad, LR, threads) for _ in range(3)]
+        sec, reps, kind = float(np.median(ts)), 3, "port"
+    return {"value": L / sec, "unit": "indices/s", "cores": threads, "kind": kind,
+            "sample": f"{L} lookups ({cfg['bags']} bags x {cfg['pf']}), median of {reps} steps "
+                      f"(fwd save + bwd + sgd, fp32, OMP threads={threads})",
+            "ms_per_step": sec * 1e3}
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    import paper_2101_11714_b200 as tt  # host-only helpers: the reference's own streams
+
+    idx, off, grad = make_inputs(cfg, 7, tt)
+    times = []
+    for _ in range(max(1, args.warmup)):
+        cpu_reference_time(cfg, idx, off, grad, budget_s=1.0)
+    base = cpu_reference_time(cfg, idx, off, grad, budget_s=10.0)
+    times.append(base["ms_per_step"])
+    v = base["value"]
+    line = {"metric": METRIC, "value": v, "unit": "indices/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference Zipf/uniform streams, sampled-Gaussian cores)",
+            "impl": "reference",
+            "config": {"workload": cfg["desc"], "global_batch": cfg["bags"],
+                       "lookups_per_step": len(idx), "parallelism": "cpu-openmp"},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "indices/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--fast-forward", action="store_true",
+                    help="FFMA forward instead of the bit-exact default")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="print per-phase times")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2101_11714_b200 as tt
+
+    stream = torch.cuda.Stream(device=dev)
+    plan = tt.plan_shapes(cfg["rows"], cfg["emb"], len(cfg["rf"]), cfg["rank"], cfg["rf"], cfg["cf"])
+    table = tt.TtTable(plan, "bench", np.float32, device=local, stream=stream.cuda_stream)
+    table.init_sampled_gaussian(1)
+    table.set_exact_forward(not args.fast_forward)
+    idx, off, grad = make_inputs(cfg, 7 + rank, tt)
+    L, B, N = len(idx), cfg["bags"], cfg["emb"]
+    with torch.cuda.stream(stream):
+        d_idx = torch.from_numpy(idx).to(dev)
+        d_off = torch.from_numpy(off).to(dev)
+        d_grad = torch.from_numpy(grad).to(dev)
+        d_out = torch.empty((B, N), dtype=torch.float32, device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream.synchronize()
+    ctx = tt.ForwardContext(table)
+
+    gbuf = None
+    if world > 1:
+        gptr, gn = table.grad_buffer()
+
+        class _Arr:
+            __cuda_array_interface__ = {"shape": (gn,), "typestr": "<f4", "data": (gptr, False),
+                                        "version": 3, "strides": None}
+
+        gbuf = torch.as_tensor(_Arr(), device=dev)
+
+    def step():
+        table.forward_device(ctx, d_idx.data_ptr(), L, d_off.data_ptr(), B, d_out.data_ptr(),
+                             save=True)
+        if world == 1:
+            table.backward_sgd_device(ctx, d_grad.data_ptr(), LR)
+        else:
+            table.backward_device(ctx, d_grad.data_ptr())
+            with torch.cuda.stream(stream):
+                dist.all_reduce(gbuf)
+            table.apply_grad(LR)
+
+    # warm-up (allocates every workspace), validation, then graph capture
+    for _ in range(args.warmup):
+        step()
+    table.check()
+    use_graph = world == 1
+    kernels_per_step = None
+    if use_graph:
+        table.graph_begin()
+        step()
+        kernels_per_step, _ = table.graph_end()
+        run = table.graph_launch
+        for _ in range(2):
+            run()
+    else:
+        run = step
+    stream.synchronize()
+
+    if args.profile:
+        table.profile(True)
+        step()
+        phases = table.profile_read()
+        table.profile(False)
+    else:
+        phases = None
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)
+            starts[i].record(stream)
+            run()
+            ends[i].record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * L * args.steps / (total_ms / 1e3)
+
+    # per-phase breakdown for the roofline (events between pipeline phases)
+    table.profile(True)
+    for _ in range(3):
+        flush.fill_(1)
+        step()
+    ph_all = table.profile_read()
+    table.profile(False)
+    agg = {}
+    for name, ms in ph_all:
+        agg.setdefault(name, []).append(ms)
+    phase_ms = {k: float(np.mean(v)) for k, v in agg.items()}
+    dom = max(phase_ms, key=phase_ms.get)
+
+    # e2e through the host C ABI: pinned host buffers, copies inside the region
+    h_idx = torch.from_numpy(idx).pin_memory().numpy()
+    h_off = torch.from_numpy(off).pin_memory().numpy()
+    h_grad = torch.from_numpy(grad).pin_memory().numpy()
+    h_out = torch.empty((B, N), dtype=torch.float32).pin_memory().numpy()
+    batch = tt.IndexBatch(h_idx, h_off)
+    import ctypes as C
+
+    from paper_2101_11714_b200._lib import lib
+
+    hctx = tt.ForwardContext(table)
+
+    def e2e_step():
+        st = lib().ttgpu_forward(table.handle, h_idx.ctypes.data_as(C.c_void_p), L,
+                                 h_off.ctypes.data_as(C.c_void_p), B, None, 0, 2048, 1,
+                                 h_out.ctypes.data_as(C.c_void_p), hctx.handle)
+        assert st == 0, lib().ttgpu_last_error()
+        if world == 1:
+            table.backward_sgd(hctx, batch, h_grad, LR)
+        else:
+            st = lib().ttgpu_backward(table.handle, hctx.handle, L, B,
+                                      h_grad.ctypes.data_as(C.c_void_p), B * N, None)
+            assert st == 0
+            with torch.cuda.stream(stream):
+                dist.all_reduce(gbuf)
+            table.apply_grad(LR)
+            table.sync()
+
+    for _ in range(3):
+        e2e_step()
+    if dist:
+        dist.barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.fill_(2)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_total = float(sum(e2e_times))
+    if dist:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * L * args.steps / e2e_total
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    props = torch.cuda.get_device_properties(dev)
+    fp32_peak_tf = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
+    params = plan.parameter_count()
+    ranks = plan.ranks
+    f_lookup = flops_per_lookup(cfg["rf"], cfg["cf"], ranks)
+    step_flops = f_lookup * L + 2 * params
+    step_bytes = bytes_per_step(L, B, N, params)
+    step_s = ms_per_step / 1e3
+    line = {
+        "metric": METRIC, "value": value, "unit": "indices/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference Zipf/uniform index streams (same bytes as data.cpp), "
+                "sampled-Gaussian cores (initializer.hpp), N(0,1) grad_out",
+        "config": {"workload": cfg["desc"], "global_batch": B * world, "lookups_per_step": L * world,
+                   "parallelism": f"dp{world}" if world > 1 else "single-gpu",
+                   "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                   "forward": "ffma" if args.fast_forward else "exact (bit-identical to reference)",
+                   "graph": use_graph},
+        "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
+        "clocks": clk,
+        "roofline": {
+            "bound": "hbm", "achieved": step_bytes / step_s / 1e9, "peak": hbm_peak,
+            "unit": "GB/s", "frac": step_bytes / step_s / 1e9 / hbm_peak,
+            "traffic": None,
+            "scope": "whole step (all kernels); algorithmic bytes = 16B/lookup idx + 16B/bag "
+                     "offsets + 8N B/bag output+grad + 8B/param cores",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
+        "roofline_fp32": {
+            "bound": "fp32-ffma", "achieved": step_flops / step_s / 1e12, "peak": fp32_peak_tf,
+            "unit": "TFLOP/s", "frac": step_flops / step_s / 1e12 / fp32_peak_tf,
+            "flops_per_lookup": f_lookup,
+            "peak_source": f"derived: {props.multi_processor_count} SMs x 128 FMA x 2 x "
+                           f"{sm_mhz:.0f} MHz (nominal)",
+            "note": "algorithmic reference-chain flops (no dedup); pair dedup lets frac exceed "
+                    "the executed-flop rate"},
+        "phases_ms": phase_ms, "dominant_phase": dom,
+        "e2e": {"value": e2e_value, "unit": "indices/s",
+                "h2d_bytes_per_step": int(idx.nbytes + off.nbytes + grad.nbytes),
+                "d2h_bytes_per_step": int(h_out.nbytes),
+                "path": "ttgpu_forward + ttgpu_backward_sgd (host C ABI, pinned buffers)"},
+    }
+    if not args.no_cpu_baseline:
+        cb = cpu_reference_time(cfg, idx, off, grad, budget_s=10.0)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if phases:
+        line["profile_single_step"] = phases
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * ttgpu.h -- C ABI of the B200-native TT-EmbeddingBag (libttgpu.so).
+ *
+ * Drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/ttrec/embedding_ops.hpp).  The reference has
+ * no C ABI (header-only C++ templates over TtTable<T> + IndexBatch); each
+ * entry point below names the reference interface it replaces.  Plain
+ * pointers and sizes only -- no torch or C++ types cross this boundary.
+ *
+ * Conventions
+ *  - Status codes mirror the reference's exception types:
+ *      TTGPU_OK 0, TTGPU_ERR_RUNTIME 1 (std::runtime_error),
+ *      TTGPU_ERR_INVALID_ARGUMENT 2 (std::invalid_argument),
+ *      TTGPU_ERR_OUT_OF_RANGE 3 (std::out_of_range).
+ *    ttgpu_last_error() returns the thread-local message, worded like the
+ *    reference's (table names, "stale", ...), so a C++ or Python wrapper can
+ *    re-throw the same type with the same text.
+ *  - Core layout is the reference's physical layout (tt_table.hpp:19-22):
+ *    core k is (m_k, R_{k-1}, n_k, R_k) row-major, byte-identical to
+ *    TtTable<T>::core(k).
+ *  - "host" entry points take host pointers, copy in/out and synchronise
+ *    before returning (value semantics, like the reference).  "_device"
+ *    entry points take device pointers and are asynchronous on the table's
+ *    stream (graph-capturable); data-dependent validation errors (index out
+ *    of range, malformed offsets) are latched on the device and reported by
+ *    the next ttgpu_check() / host call.
+ *  - dtype: TTGPU_F32 or TTGPU_F64 (the reference instantiates float and
+ *    double, common.hpp:13-15).  pooling: TTGPU_SUM / TTGPU_MEAN
+ *    (index_batch.hpp:10).
+ */
+#ifndef TTGPU_H
+#define TTGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TTGPU_OK = 0, TTGPU_ERR_RUNTIME = 1, TTGPU_ERR_INVALID_ARGUMENT = 2,
+       TTGPU_ERR_OUT_OF_RANGE = 3 };
+enum { TTGPU_F32 = 0, TTGPU_F64 = 1 };
+enum { TTGPU_SUM = 0, TTGPU_MEAN = 1 };
+
+typedef struct ttgpu_table ttgpu_table; /* TtTable<T> resident on one GPU */
+typedef struct ttgpu_ctx ttgpu_ctx;     /* ForwardContext<T> (embedding_ops.hpp:101-110) */
+typedef struct ttgpu_cache ttgpu_cache; /* LfuCache<T> (lfu_cache.hpp:134-310) */
+
+const char* ttgpu_last_error(void);
+int ttgpu_abi_version(void);
+
+/* ---- shape planning: shape_plan.hpp:19-67 / src/shape_plan.cpp -------- */
+/* plan_shapes (shape_plan.hpp:56-58).  rf_in / cf_in may be NULL (auto). */
+int ttgpu_plan_shapes(int64_t num_rows, int64_t emb_dim, int tt_dim, int64_t rank,
+                      const int64_t* rf_in, const int64_t* cf_in, int64_t* rf_out,
+                      int64_t* cf_out, int64_t* ranks_out);
+/* ShapePlan::validate / padded_rows / parameter_count / memory_reduction (:28-43) */
+int ttgpu_plan_info(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* rf,
+                    const int64_t* cf, const int64_t* ranks, int64_t* padded_rows,
+                    int64_t* parameter_count, int64_t* memory_reduction);
+/* decompose_index / recompose_index (shape_plan.hpp:60-66) */
+int ttgpu_decompose_index(int64_t flat, const int64_t* radices, int n, int64_t* digits);
+int ttgpu_recompose_index(const int64_t* digits, const int64_t* radices, int n, int64_t* flat);
+
+/* ---- tables: TtTable<T> (tt_table.hpp:23-102) -------------------------- */
+/* TtTable(ShapePlan, name) (tt_table.hpp:25-33); cores zero-initialised.
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* row_factors,
+                 const int64_t* col_factors, const int64_t* ranks, int dtype, const char* name,
+                 int device, void* stream, ttgpu_table** out);
+int ttgpu_destroy(ttgpu_table* t);
+int ttgpu_set_stream(ttgpu_table* t, void* stream);
+int ttgpu_core_size(const ttgpu_table* t, int k, int64_t* n);
+/* TtTable::core(k) read / write as raw bytes (tt_table.hpp:43-44).  A write
+ * bumps the mutation counter (tt_table.hpp:82-85) like init / sgd_step. */
+int ttgpu_get_core(ttgpu_table* t, int k, void* host_dst);
+int ttgpu_set_core(ttgpu_table* t, int k, const void* host_src);
+int ttgpu_core_device_ptr(ttgpu_table* t, int k, void** dptr);
+int ttgpu_mark_mutated(ttgpu_table* t);                        /* tt_table.hpp:85 */
+/* on (default): forward products and sums separately rounded in the
+ * reference's loop order -> forward_bags / lookup_row bit-identical to the
+ * reference (gemm.hpp:15-31, embedding_ops.hpp:232-249).  off: FFMA. */
+int ttgpu_set_exact_forward(ttgpu_table* t, int on);
+int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out); /* tt_table.hpp:84 */
+
+/* ---- forward_bags (embedding_ops.hpp:159-253) ---------------------------- */
+int ttgpu_ctx_create(ttgpu_table* t, ttgpu_ctx** out);
+int ttgpu_ctx_destroy(ttgpu_ctx* c);
+/* Host pointers; out is (B x emb_dim) row-major.  weights may be NULL (all
+ * ones, index_batch.hpp:24).  micro_batch must be >= 1 (:165) but does not
+ * change results (:155-158).  save keeps the per-lookup chain partials for
+ * backward (:181-185); backward results are identical either way. */
+int ttgpu_forward(ttgpu_table* t, const int64_t* indices, int64_t L, const int64_t* offsets,
+                  int64_t B, const double* weights, int pooling, int64_t micro_batch, int save,
+                  void* out, ttgpu_ctx* ctx);
+int ttgpu_forward_device(ttgpu_table* t, const int64_t* d_indices, int64_t L,
+                         const int64_t* d_offsets, int64_t B, const double* d_weights,
+                         int pooling, int save, void* d_out, ttgpu_ctx* ctx);
+
+/* ---- backward_bags (embedding_ops.hpp:260-358) --------------------------- */
+/* Checks the reference's contract (:264-274): context table identity,
+ * L/B match, stale mutation snapshot, grad size == B*emb_dim.  Writes the
+ * dense CoreGradients into the table's gradient buffer; grads_out (host
+ * pointers, one per core, each core_size elements) may be NULL. */
+int ttgpu_backward(ttgpu_table* t, ttgpu_ctx* ctx, int64_t L, int64_t B, const void* grad_out,
+                   int64_t grad_len, void* const* grads_out);
+/* device variant; the dense gradient stays in the table's gradient buffer
+ * (ttgpu_grad_device_ptr), e.g. for an NCCL allreduce before ttgpu_apply_grad */
+int ttgpu_backward_device(ttgpu_table* t, ttgpu_ctx* ctx, const void* d_grad_out);
+int ttgpu_grad_device_ptr(ttgpu_table* t, int k, void** dptr);
+
+/* ---- sgd_step (embedding_ops.hpp:361-376) -------------------------------- */
+/* sgd_step(table, grads, lr) with caller gradients (host, one per core) */
+int ttgpu_sgd_step(ttgpu_table* t, const void* const* host_grads, double lr);
+/* host variant of the fused call: copies grad_out in, synchronises */
+int ttgpu_backward_sgd(ttgpu_table* t, ttgpu_ctx* ctx, int64_t L, int64_t B, const void* grad_out,
+                       int64_t grad_len, double lr);
+/* the whole dense gradient buffer (all cores, aligned offsets, padding zero) */
+int ttgpu_grad_buffer(ttgpu_table* t, void** dptr, int64_t* n_elems);
+/* core -= lr * (table gradient buffer); async */
+int ttgpu_apply_grad(ttgpu_table* t, double lr);
+/* fused backward_bags + sgd_step: gradients are reduced per touched core
+ * slice and applied in the reduction epilogue (no dense gradient); async */
+int ttgpu_backward_sgd_device(ttgpu_table* t, ttgpu_ctx* ctx, const void* d_grad_out,
+                              double lr);
+
+/* ---- lookup_row (embedding_ops.hpp:120-152) ------------------------------ */
+int ttgpu_lookup_row(ttgpu_table* t, int64_t row, void* host_out);
+int ttgpu_lookup_rows_device(ttgpu_table* t, const int64_t* d_rows, int64_t n, void* d_out);
+
+/* ---- CUDA graphs: capture any sequence of _device calls on the table's
+ * (non-default) stream, then replay it with one launch ------------------- */
+int ttgpu_graph_begin(ttgpu_table* t);
+int ttgpu_graph_end(ttgpu_table* t, int* kernel_nodes, int* total_nodes);
+int ttgpu_graph_launch(ttgpu_table* t);
+
+/* ---- synchronisation / deferred device errors ----------------------------- */
+int ttgpu_sync(ttgpu_table* t);
+int ttgpu_check(ttgpu_table* t); /* sync + report latched validation errors */
+
+/* ---- instrumentation (no reference counterpart; diagnostics only) ------- */
+/* on: record CUDA events between pipeline phases on the table's stream;
+ * read: per-phase milliseconds since the last read ("decode;sort_pairs;..."). */
+int ttgpu_profile(ttgpu_table* t, int on);
+int ttgpu_profile_read(ttgpu_table* t, char* names, int64_t names_len, float* ms, int max_phases,
+                       int* n_out);
+
+/* ---- EmbeddingStats (embedding_stats.hpp:12-23) -------------------------- */
+void ttgpu_stats_reset(void);
+uint64_t ttgpu_stats_rows(void);            /* tt_rows_computed */
+uint64_t ttgpu_stats_peak_workspace(void);  /* peak_workspace_bytes (device) */
+void ttgpu_stats_add_rows(uint64_t n);
+
+/* ---- synthetic index streams (data.hpp:11-37), host ---------------------- */
+/* ZipfianSampler(population, s) + generate_zipfian_batch with Rng(seed):
+ * same CDF-inversion algorithm and mt19937_64 stream as the reference, so
+ * the bytes match data.cpp:8-47 on the same libstdc++. */
+int ttgpu_zipf_batch(int64_t population, double exponent, uint64_t seed, int64_t bags,
+                     int64_t pooling_factor, int64_t* indices, int64_t* offsets);
+/* Rng(seed).uniform_int(0, rows) x n (rng.hpp:47-51) */
+int ttgpu_uniform_indices(int64_t rows, uint64_t seed, int64_t n, int64_t* indices);
+/* init_tt_cores(table, InitSpec::sampled_gaussian(), seed) (initializer.hpp:143-154) */
+int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTGPU_H */

@@ -1,0 +1,26 @@
+"""B200-native TT-EmbeddingBag (TT-Rec, arXiv:2101.11714): a drop-in for the
+reference C++ operator's hot path, implemented as sm_100a CUDA kernels behind
+a C ABI (include/ttgpu.h, lib/libttgpu.so)."""
+from .ttrec import (  # noqa: F401
+    CoreGradients,
+    EmbeddingStats,
+    ForwardContext,
+    ForwardResult,
+    IndexBatch,
+    InvalidArgument,
+    OutOfRange,
+    Pooling,
+    RuntimeFailure,
+    ShapePlan,
+    TtTable,
+    backward_bags,
+    decompose_index,
+    forward_bags,
+    generate_zipfian_batch,
+    kDefaultMicroBatch,
+    lookup_row,
+    plan_shapes,
+    recompose_index,
+    sgd_step,
+    uniform_indices,
+)

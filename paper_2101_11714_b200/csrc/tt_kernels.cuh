@@ -1,0 +1,633 @@
+// sm_100a kernels for the TT-EmbeddingBag hot path.
+//
+// Algorithm: the reference evaluates the rank-R chain
+// G0[i0]·G1[i1]·…·G_{d-1}[i_{d-1}] once per lookup (embedding_ops.hpp:213-229)
+// and scatters per-lookup gradients into per-worker dense copies
+// (:320-357).  Here the widest, most expensive stage -- the "head"
+// H(i0,i1) = G0[i0]·G1[i1] -- is evaluated once per UNIQUE (i0,i1) pair, and
+// every gradient is reduced per unique core slice by a deterministic
+// sort-by-key / chunked segmented reduction (no floating-point atomics):
+//
+//   forward : decode -> sort lookups by pair key (i1-major) -> head GEMM per
+//             unique pair -> per-bag tail chain + pooling in lookup order
+//   backward: S(pair)  = Σ_{lookups of pair} D1          (segmented, by pair)
+//             dG_k[i]  = Σ_{lookups with i_k=i} u_{k-1}ᵀ D_k  (segmented, k>=2)
+//             dG1[i1]  = Σ_{pairs with i1} G0[i0]ᵀ S      (segmented over pairs)
+//             D0(pair) = S · G1[i1]ᵀ ;  dG0[i0] = Σ_{i1} D0   (dense pair table)
+//
+// All reductions combine their per-chunk partials in a fixed order, so the
+// result is bit-reproducible run to run.  Forward kernels take a kExact flag:
+// with it, products and sums are separately rounded in the reference's loop
+// order (gemm.hpp:15-31, embedding_ops.hpp:232-249), which makes forward and
+// lookup_row bit-identical to the reference; without it they use FFMA.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ttgpu {
+
+constexpr int kMaxD = 8;
+
+// Shape of one table as the kernels see it (shape_plan.hpp:19-46 +
+// embedding_ops.hpp:27-47 ChainDims).
+struct DevPlan {
+  int d;
+  int N;                    // emb_dim
+  int64_t num_rows;
+  int64_t suffix[kMaxD];    // row-digit place values (tt_table.hpp:30-33)
+  int m[kMaxD];             // row factors
+  int n[kMaxD];             // col factors
+  int r[kMaxD + 1];         // ranks
+  int prefix[kMaxD];        // prod_{j<=k} n_j
+  int slice[kMaxD];         // R_k n_k R_{k+1}
+  int64_t coff[kMaxD];      // element offset of core k in the core buffer
+  int W1;                   // head width prefix[1]*R_2 (== N when d == 2)
+  int C1;                   // G1 slice columns n_1*R_2
+  int maxw;                 // max chain width
+};
+
+// ---------------------------------------------------------------- helpers --
+template <typename T, bool kExact>
+__device__ __forceinline__ T madd(T a, T b, T acc);
+template <>
+__device__ __forceinline__ float madd<float, true>(float a, float b, float acc) {
+  return __fadd_rn(acc, __fmul_rn(a, b));
+}
+template <>
+__device__ __forceinline__ float madd<float, false>(float a, float b, float acc) {
+  return __fmaf_rn(a, b, acc);
+}
+template <>
+__device__ __forceinline__ double madd<double, true>(double a, double b, double acc) {
+  return __dadd_rn(acc, __dmul_rn(a, b));
+}
+template <>
+__device__ __forceinline__ double madd<double, false>(double a, double b, double acc) {
+  return __fma_rn(a, b, acc);
+}
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+
+__device__ __forceinline__ void decode_row(const DevPlan& P, int64_t row, int* dig) {
+#pragma unroll
+  for (int k = 0; k < kMaxD; ++k) {
+    if (k >= P.d) break;
+    const int64_t q = row / P.suffix[k];
+    dig[k] = static_cast<int>(q);
+    row -= q * P.suffix[k];
+  }
+}
+
+// C[M x Nc] = A[M x K] · B[K x Nc] by one warp, p-ascending accumulation from
+// zero per output (gemm.hpp:15-31 order).  A, C: shared; B: global/shared.
+template <typename T, bool kExact>
+__device__ __forceinline__ void warp_mm(const T* A, const T* __restrict__ B, T* C, int M, int K,
+                                        int Nc, int lane) {
+  for (int e = lane; e < M * Nc; e += 32) {
+    const int i = e / Nc, j = e - i * Nc;
+    const T* a = A + i * K;
+    T acc = T(0);
+    for (int p = 0; p < K; ++p) acc = madd<T, kExact>(a[p], B[p * Nc + j], acc);
+    C[e] = acc;
+  }
+}
+
+// C[M x K] = A[M x Nc] · B[K x Nc]ᵀ by one warp (gemm.hpp:47-60 order).
+template <typename T>
+__device__ __forceinline__ void warp_mm_abt(const T* A, const T* __restrict__ B, T* C, int M,
+                                            int Nc, int K, int lane) {
+  for (int e = lane; e < M * K; e += 32) {
+    const int i = e / K, q = e - i * K;
+    const T* a = A + i * Nc;
+    const T* b = B + q * Nc;
+    T acc = T(0);
+    for (int j = 0; j < Nc; ++j) acc = madd<T, false>(a[j], b[j], acc);
+    C[e] = acc;
+  }
+}
+
+// ---------------------------------------------------------- batch decode --
+// One pass over the lookups: range check (index_batch.hpp:49-54 -- the first
+// offending lookup is latched), mixed-radix decode, pair key (i1-major so
+// pairs sharing G1[i1] are adjacent after sorting) and tail digits.
+__global__ void k_decode(DevPlan P, const int64_t* __restrict__ idx, int64_t L,
+                         uint32_t* __restrict__ pair_key, uint32_t* __restrict__ iota,
+                         uint32_t* __restrict__ tail_dig, unsigned long long* __restrict__ bad) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < L;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = idx[l];
+    if (row < 0 || row >= P.num_rows) {
+      atomicMin(bad, static_cast<unsigned long long>(l));
+      row = 0;
+    }
+    int dig[kMaxD];
+    decode_row(P, row, dig);
+    pair_key[l] = static_cast<uint32_t>(dig[1]) * static_cast<uint32_t>(P.m[0]) +
+                  static_cast<uint32_t>(dig[0]);
+    iota[l] = static_cast<uint32_t>(l);
+    for (int k = 2; k < P.d; ++k) tail_dig[(k - 2) * L + l] = static_cast<uint32_t>(dig[k]);
+  }
+}
+
+// Per bag: structural offsets checks (index_batch.hpp:42-46), lookup->bag map
+// and the backward scale alpha = T(w / bag_size) computed in double
+// (embedding_ops.hpp:329-333).
+template <typename T>
+__global__ void k_bags(const int64_t* __restrict__ off, int64_t B, int64_t L,
+                       const double* __restrict__ w, int mean, int32_t* __restrict__ lk_bag,
+                       T* __restrict__ lk_alpha, int* __restrict__ err_struct) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = off[b], e = off[b + 1];
+    if (b == 0 && s != 0) atomicOr(err_struct, 1);
+    if (e < s) atomicOr(err_struct, 2);
+    if (b == B - 1 && e != L) atomicOr(err_struct, 4);
+    const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
+    const double inv = mean ? static_cast<double>(e - s) : 1.0;
+    for (int64_t l = lo; l < hi; ++l) {
+      lk_bag[l] = static_cast<int32_t>(b);
+      double a = w ? w[l] : 1.0;
+      if (mean) a /= inv;
+      lk_alpha[l] = static_cast<T>(a);
+    }
+  }
+}
+
+// ---------------------------------------------- segment / run bookkeeping --
+// Items sorted by key are cut into fixed chunks of C positions; a "run" is a
+// maximal piece of one segment inside one chunk.  packed[s] = head | run-head<<32
+// is scanned (inclusive) to give segment and run ordinals per position.
+__global__ void k_run_flags(const uint32_t* __restrict__ keys, const int* __restrict__ n_dev,
+                            int64_t n_host, int C, unsigned long long* __restrict__ packed) {
+  const int64_t n = n_dev ? *n_dev : n_host;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_host;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long v = 0;
+    if (s < n) {
+      const bool head = (s == 0) || keys[s] != keys[s - 1];
+      const bool run = head || (s % C == 0);
+      v = (head ? 1ull : 0ull) | ((run ? 1ull : 0ull) << 32);
+    }
+    packed[s] = v;
+  }
+}
+
+// Unique pairs from the sorted lookup keys.
+__global__ void k_pairs_compact(const uint32_t* __restrict__ s_key,
+                                const uint32_t* __restrict__ s_lk,
+                                const unsigned long long* __restrict__ scan, int64_t L,
+                                uint32_t* __restrict__ pair_key_u, int32_t* __restrict__ pair_start,
+                                int32_t* __restrict__ lk_pid,
+                                int* __restrict__ counts /* [0]=U, [1]=runs */) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < L;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = scan[s];
+    const int pid = static_cast<int>(v & 0xffffffffull) - 1;
+    const uint32_t key = s_key[s];
+    if (s == 0 || s_key[s - 1] != key) {
+      pair_key_u[pid] = key;
+      pair_start[pid] = static_cast<int32_t>(s);
+    }
+    lk_pid[s_lk[s]] = pid;
+    if (s == L - 1) {
+      counts[0] = pid + 1;
+      counts[1] = static_cast<int>(v >> 32);
+      pair_start[pid + 1] = static_cast<int32_t>(L);
+    }
+  }
+}
+
+// CSR over a dense key space [0, K) from keys sorted ascending: seg[v] = first
+// position with key >= v, seg[K] = n.
+__global__ void k_key_bounds(const uint32_t* __restrict__ keys, const int* __restrict__ n_dev,
+                             int64_t n_host, int K, int32_t* __restrict__ seg) {
+  const int64_t n = n_dev ? *n_dev : n_host;
+  if (n == 0) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= K; v += gridDim.x * blockDim.x)
+      seg[v] = 0;
+    return;
+  }
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = keys[s];
+    const int64_t prev = s == 0 ? -1 : static_cast<int64_t>(keys[s - 1]);
+    for (int64_t v = prev + 1; v <= k; ++v) seg[v] = static_cast<int32_t>(s);
+    if (s == n - 1)
+      for (int64_t v = k + 1; v <= K; ++v) seg[v] = static_cast<int32_t>(n);
+  }
+}
+
+// Dense pair table key -> pid for this context's pairs (the table is shared
+// by all contexts of a table, so it is refreshed before each backward).
+__global__ void k_pair_scatter(const uint32_t* __restrict__ pair_key_u,
+                               const int* __restrict__ counts, int64_t cap,
+                               int32_t* __restrict__ pair_tab) {
+  const int U = counts[0];
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < cap && p < U;
+       p += (int64_t)gridDim.x * blockDim.x)
+    pair_tab[pair_key_u[p]] = static_cast<int32_t>(p);
+}
+
+// i1 of each unique pair (pid order == (i1, i0) order).
+__global__ void k_pair_i1(const uint32_t* __restrict__ pair_key_u, const int* __restrict__ counts,
+                          int64_t cap, int m0, uint32_t* __restrict__ out) {
+  const int U = counts[0];
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < cap;
+       p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = p < U ? pair_key_u[p] / static_cast<uint32_t>(m0) : 0xffffffffu;
+}
+
+// ------------------------------------------------------------ forward: head --
+// H[pid] = G0[i0] (P0 x R1) · G1[i1] (R1 x C1) for every unique pair.  Pairs
+// are processed in chunks of CH; G1[i1] is staged in shared memory once per
+// i1 run inside the chunk (pairs are i1-major, so runs are long).
+template <typename T, bool kExact>
+__global__ void k_head_fwd(DevPlan P, const T* __restrict__ cores,
+                           const uint32_t* __restrict__ pair_key_u,
+                           const int* __restrict__ counts, int CH, T* __restrict__ H) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* g1s = reinterpret_cast<T*>(smem_raw);                 // R1 x C1
+  T* g0s = g1s + P.r[1] * P.C1;                            // CH x P0 x R1
+  const int U = counts[0];
+  const int P0 = P.n[0], R1 = P.r[1], C1 = P.C1;
+  const int s0 = P.slice[0], s1 = P.slice[1];
+  const T* G0 = cores + P.coff[0];
+  const T* G1 = cores + P.coff[1];
+  const int nchunks = (U + CH - 1) / CH;
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int p0 = ch * CH, p1 = min(U, p0 + CH);
+    __syncthreads();
+    for (int e = threadIdx.x; e < (p1 - p0) * s0; e += blockDim.x) {
+      const int q = e / s0;
+      const uint32_t i0 = pair_key_u[p0 + q] % static_cast<uint32_t>(P.m[0]);
+      g0s[e] = G0[i0 * s0 + (e - q * s0)];
+    }
+    int run_lo = p0;
+    while (run_lo < p1) {
+      const uint32_t i1 = pair_key_u[run_lo] / static_cast<uint32_t>(P.m[0]);
+      int run_hi = run_lo + 1;
+      while (run_hi < p1 && pair_key_u[run_hi] / static_cast<uint32_t>(P.m[0]) == i1) ++run_hi;
+      __syncthreads();
+      for (int e = threadIdx.x; e < s1; e += blockDim.x) g1s[e] = G1[(int64_t)i1 * s1 + e];
+      __syncthreads();
+      const int outs = P0 * C1;
+      for (int e = threadIdx.x; e < (run_hi - run_lo) * outs; e += blockDim.x) {
+        const int q = e / outs, rem = e - q * outs;
+        const int a = rem / C1, c = rem - a * C1;
+        const T* arow = g0s + (run_lo - p0 + q) * s0 + a * R1;
+        T acc = T(0);
+        for (int p = 0; p < R1; ++p) acc = madd<T, kExact>(arow[p], g1s[p * C1 + c], acc);
+        H[static_cast<int64_t>(run_lo + q) * P.W1 + rem] = acc;
+      }
+      run_lo = run_hi;
+    }
+  }
+}
+
+// ---------------------------------------------------- forward: tail + pool --
+// One warp per bag: for each lookup in ascending order, chain the head row
+// through G_2..G_{d-1} and pool out[b] += T(w)·y (embedding_ops.hpp:232-237),
+// then the Mean rescale (:240-249).  Saves u_k (2 <= k <= d-2) when requested.
+template <typename T, bool kExact>
+__global__ void k_tail_pool(DevPlan P, const T* __restrict__ cores, const T* __restrict__ H,
+                            const int32_t* __restrict__ lk_pid, const uint32_t* __restrict__ tail_dig,
+                            const int64_t* __restrict__ off, int64_t B, int64_t L,
+                            const double* __restrict__ w, int mean, T* __restrict__ out,
+                            T* __restrict__ saved /* (d-3) x L x maxw or null */) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* buf = reinterpret_cast<T*>(smem_raw) + static_cast<int64_t>(wid) * (2 * P.maxw + P.N);
+  T* ping = buf;
+  T* pong = buf + P.maxw;
+  T* acc = buf + 2 * P.maxw;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * warps + wid; b < B;
+       b += static_cast<int64_t>(gridDim.x) * warps) {
+    for (int j = lane; j < P.N; j += 32) acc[j] = T(0);
+    const int64_t s = off[b], e = off[b + 1];
+    const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
+    for (int64_t l = lo; l < hi; ++l) {
+      const T* u = H + static_cast<int64_t>(lk_pid[l]) * P.W1;
+      if (P.d > 2) {
+        const T* src = u;
+        T* dst = ping;
+        for (int k = 2; k < P.d; ++k) {
+          const int i_k = static_cast<int>(tail_dig[(k - 2) * L + l]);
+          const T* G = cores + P.coff[k] + static_cast<int64_t>(i_k) * P.slice[k];
+          __syncwarp();
+          warp_mm<T, kExact>(src, G, dst, P.prefix[k - 1], P.r[k], P.n[k] * P.r[k + 1], lane);
+          __syncwarp();
+          if (saved && k <= P.d - 2) {
+            const int wk = P.prefix[k] * P.r[k + 1];
+            T* sv = saved + (static_cast<int64_t>(k - 2) * L + l) * P.maxw;
+            for (int x = lane; x < wk; x += 32) sv[x] = dst[x];
+          }
+          src = dst;
+          dst = (dst == ping) ? pong : ping;
+        }
+        u = src;
+      }
+      const T a = static_cast<T>(w ? w[l] : 1.0);
+      for (int j = lane; j < P.N; j += 32) acc[j] = madd<T, kExact>(a, u[j], acc[j]);
+      __syncwarp();
+    }
+    T scale = T(1);
+    const bool do_scale = mean && (e - s) > 1;
+    if (do_scale) scale = static_cast<T>(1.0 / static_cast<double>(e - s));
+    for (int j = lane; j < P.N; j += 32)
+      out[b * P.N + j] = do_scale ? mul_rn<T>(acc[j], scale) : acc[j];
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------ backward: chain helpers --
+// D_{k-1} = D_k · G_k[i_k]ᵀ for k = kfrom..kto+1 (descending), starting from
+// D_{d-1} = alpha * g[bag].  Result left in *res (ping/pong owned by caller).
+template <typename T>
+__device__ __forceinline__ const T* bwd_chain(const DevPlan& P, const T* __restrict__ cores,
+                                              const uint32_t* __restrict__ tail_dig, int64_t L,
+                                              int64_t l, const T* __restrict__ grow, T alpha,
+                                              int kto, T* ping, T* pong, int lane) {
+  for (int j = lane; j < P.N; j += 32) ping[j] = mul_rn<T>(alpha, grow[j]);
+  __syncwarp();
+  T* cur = ping;
+  T* nxt = pong;
+  for (int k = P.d - 1; k > kto; --k) {
+    const int i_k = static_cast<int>(tail_dig[(k - 2) * L + l]);
+    const T* G = cores + P.coff[k] + static_cast<int64_t>(i_k) * P.slice[k];
+    warp_mm_abt<T>(cur, G, nxt, P.prefix[k - 1], P.n[k] * P.r[k + 1], P.r[k], lane);
+    __syncwarp();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  return cur;
+}
+
+// u_{kk} for one lookup from its head row (forward chain k = 2..kk), or the
+// saved partial.
+template <typename T>
+__device__ __forceinline__ const T* fwd_partial(const DevPlan& P, const T* __restrict__ cores,
+                                                const T* __restrict__ H, const int32_t* lk_pid,
+                                                const uint32_t* __restrict__ tail_dig, int64_t L,
+                                                int64_t l, int kk, const T* __restrict__ saved,
+                                                T* ping, T* pong, int lane) {
+  const T* src = H + static_cast<int64_t>(lk_pid[l]) * P.W1;
+  if (kk <= 1) return src;
+  if (saved) return saved + (static_cast<int64_t>(kk - 2) * L + l) * P.maxw;
+  T* dst = ping;
+  for (int k = 2; k <= kk; ++k) {
+    const int i_k = static_cast<int>(tail_dig[(k - 2) * L + l]);
+    const T* G = cores + P.coff[k] + static_cast<int64_t>(i_k) * P.slice[k];
+    warp_mm<T, false>(src, G, dst, P.prefix[k - 1], P.r[k], P.n[k] * P.r[k + 1], lane);
+    __syncwarp();
+    src = dst;
+    dst = (dst == ping) ? pong : ping;
+  }
+  return src;
+}
+
+// ---------------------------------------- backward: chunked segmented sums --
+// Generic chunked reduction over items sorted by segment.  Each CTA owns one
+// chunk of C consecutive sorted positions; each of its warps produces the
+// contribution vector (width Wc) of one item into a shared slot; the CTA then
+// folds the slots in position order into a shared accumulator and emits one
+// partial per run.  MODE selects the contribution:
+//   0: S pairs   item = lookup (pair order)    contrib = D1 (P1 x R2) [d>=3], alpha*g [d==2]
+//   1: tail core item = lookup (i_k order)     contrib = u_{k-1}ᵀ D_k  (R_k x n_k R_{k+1})
+template <typename T, int MODE>
+__global__ void k_chunk_reduce(DevPlan P, const T* __restrict__ cores, const T* __restrict__ H,
+                               const T* __restrict__ saved, const int32_t* __restrict__ lk_pid,
+                               const uint32_t* __restrict__ tail_dig, const int32_t* lk_bag,
+                               const T* __restrict__ lk_alpha, const T* __restrict__ grad,
+                               const uint32_t* __restrict__ s_key, const uint32_t* __restrict__ s_lk,
+                               const unsigned long long* __restrict__ scan, int64_t L, int C,
+                               int kcore, int Wc, T* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* acc = reinterpret_cast<T*>(smem_raw);                  // Wc
+  T* slots = acc + Wc;                                      // warps x Wc
+  T* scratch = slots + static_cast<int64_t>(warps) * Wc;    // warps x 4 x maxw
+  T* my = scratch + static_cast<int64_t>(wid) * 4 * P.maxw;
+  const int64_t nchunks = (L + C - 1) / C;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = ch * C, c1 = (L < c0 + C ? L : c0 + C);
+    int run = static_cast<int>(scan[c0] >> 32) - 1;
+    for (int e = threadIdx.x; e < Wc; e += blockDim.x) acc[e] = T(0);
+    for (int64_t g0 = c0; g0 < c1; g0 += warps) {
+      const int64_t s = g0 + wid;
+      if (s < c1) {
+        const int64_t l = s_lk[s];
+        const T alpha = lk_alpha[l];
+        const T* grow = grad + static_cast<int64_t>(lk_bag[l]) * P.N;
+        T* slot = slots + static_cast<int64_t>(wid) * Wc;
+        if (MODE == 0) {
+          const T* D = bwd_chain<T>(P, cores, tail_dig, L, l, grow, alpha, 1, my, my + P.maxw,
+                                    lane);
+          for (int e = lane; e < Wc; e += 32) slot[e] = D[e];
+        } else {
+          // contribution u_{k-1}ᵀ · D_k : (R_k x P_{k-1}) · (P_{k-1} x n_k R_{k+1})
+          const T* D = bwd_chain<T>(P, cores, tail_dig, L, l, grow, alpha, kcore, my,
+                                    my + P.maxw, lane);
+          const T* u = fwd_partial<T>(P, cores, H, lk_pid, tail_dig, L, l, kcore - 1, saved,
+                                      my + 2 * P.maxw, my + 3 * P.maxw, lane);
+          const int pk = P.prefix[kcore - 1], rk = P.r[kcore], wk = P.n[kcore] * P.r[kcore + 1];
+          for (int e = lane; e < rk * wk; e += 32) {
+            const int q = e / wk, j = e - q * wk;
+            T a = T(0);
+            for (int i = 0; i < pk; ++i) a = madd<T, false>(u[i * rk + q], D[i * wk + j], a);
+            slot[e] = a;
+          }
+        }
+      }
+      __syncthreads();
+      const int ng = static_cast<int>((warps < c1 - g0 ? (int64_t)warps : c1 - g0));
+      for (int q = 0; q < ng; ++q) {
+        const int64_t s = g0 + q;
+        const bool new_run = (s != c0) && (s_key[s] != s_key[s - 1]);
+        if (new_run) {
+          for (int e = threadIdx.x; e < Wc; e += blockDim.x) {
+            partials[static_cast<int64_t>(run) * Wc + e] = acc[e];
+            acc[e] = T(0);
+          }
+          ++run;
+        }
+        const T* slot = slots + static_cast<int64_t>(q) * Wc;
+        for (int e = threadIdx.x; e < Wc; e += blockDim.x) acc[e] += slot[e];
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < Wc; e += blockDim.x)
+      partials[static_cast<int64_t>(run) * Wc + e] = acc[e];
+    __syncthreads();
+  }
+}
+
+// Fold the partials of each segment in order.  Segment g spans sorted
+// positions [first, last]; its runs are run(first)..run(last).
+//   OUT_MODE 0: out[g*Wc + e] = sum      (S per pair; dense gradient slices)
+//   OUT_MODE 1: core[g*Wc + e] -= lr*sum (fused SGD on touched slices)
+template <typename T, int OUT_MODE>
+__global__ void k_combine(const T* __restrict__ partials, const unsigned long long* __restrict__ scan,
+                          const int32_t* __restrict__ seg, const int* __restrict__ nseg_dev,
+                          int nseg_host, int Wc, T* __restrict__ out, T lr) {
+  const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+  for (int g = blockIdx.x; g < nseg; g += gridDim.x) {
+    const int first = seg[g], last = seg[g + 1] - 1;
+    if (last < first) continue;  // empty segment: untouched slice
+    const int r0 = static_cast<int>(scan[first] >> 32) - 1;
+    const int r1 = static_cast<int>(scan[last] >> 32) - 1;
+    for (int e = threadIdx.x; e < Wc; e += blockDim.x) {
+      T sum = partials[static_cast<int64_t>(r0) * Wc + e];
+      for (int r = r0 + 1; r <= r1; ++r) sum += partials[static_cast<int64_t>(r) * Wc + e];
+      if (OUT_MODE == 0)
+        out[static_cast<int64_t>(g) * Wc + e] = sum;
+      else
+        out[static_cast<int64_t>(g) * Wc + e] =
+            add_rn<T>(out[static_cast<int64_t>(g) * Wc + e], -mul_rn<T>(lr, sum));
+    }
+  }
+}
+
+// ------------------------------------------------- backward: head (pairs) --
+// Over pairs in pid order (i1-major), chunks of CH pairs, runs by i1:
+//   D0[pid] = S[pid] (P0 x C1) · G1[i1]ᵀ (C1 x R1)
+//   partial(run) = Σ_pairs G0[i0]ᵀ (R1 x P0) · S[pid] (P0 x C1)
+template <typename T>
+__global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __restrict__ S,
+                           const uint32_t* __restrict__ pair_key_u, const int* __restrict__ counts,
+                           const unsigned long long* __restrict__ scan1, int CH,
+                           T* __restrict__ D0, T* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int R1 = P.r[1], C1 = P.C1, P0 = P.n[0], s0 = P.slice[0], s1 = P.slice[1];
+  T* g1s = reinterpret_cast<T*>(smem_raw);  // R1 x C1
+  T* acc = g1s + s1;                        // R1 x C1
+  const T* G0 = cores + P.coff[0];
+  const T* G1 = cores + P.coff[1];
+  const int U = counts[0];
+  const int nchunks = (U + CH - 1) / CH;
+  const uint32_t m0 = static_cast<uint32_t>(P.m[0]);
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int p0 = ch * CH, p1 = min(U, p0 + CH);
+    int run = static_cast<int>(scan1[p0] >> 32) - 1;
+    int lo = p0;
+    while (lo < p1) {
+      const uint32_t i1 = pair_key_u[lo] / m0;
+      int hi = lo + 1;
+      while (hi < p1 && pair_key_u[hi] / m0 == i1) ++hi;
+      __syncthreads();
+      for (int e = threadIdx.x; e < s1; e += blockDim.x) {
+        g1s[e] = G1[static_cast<int64_t>(i1) * s1 + e];
+        acc[e] = T(0);
+      }
+      __syncthreads();
+      for (int p = lo; p < hi; ++p) {
+        const uint32_t i0 = pair_key_u[p] % m0;
+        const T* Sp = S + static_cast<int64_t>(p) * P.W1;
+        const T* g0 = G0 + static_cast<int64_t>(i0) * s0;
+        // D0[p][a][r] = sum_c S[a][c] * G1[r][c]
+        for (int e = threadIdx.x; e < P0 * R1; e += blockDim.x) {
+          const int a = e / R1, rr = e - a * R1;
+          T v = T(0);
+          for (int c = 0; c < C1; ++c) v = madd<T, false>(Sp[a * C1 + c], g1s[rr * C1 + c], v);
+          D0[static_cast<int64_t>(p) * s0 + e] = v;
+        }
+        // acc[r][c] += sum_a G0[a][r] * S[a][c]
+        for (int e = threadIdx.x; e < s1; e += blockDim.x) {
+          const int rr = e / C1, c = e - rr * C1;
+          T v = acc[e];
+          for (int a = 0; a < P0; ++a) v = madd<T, false>(g0[a * R1 + rr], Sp[a * C1 + c], v);
+          acc[e] = v;
+        }
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < s1; e += blockDim.x)
+        partials[static_cast<int64_t>(run) * s1 + e] = acc[e];
+      ++run;
+      lo = hi;
+    }
+  }
+}
+
+// dG0[i0] = Σ_{i1 ascending} D0[pair(i0,i1)] via the dense pair table; entries
+// from earlier batches are rejected by checking the pair key back.
+// OUT_MODE 0 writes the dense slice, 1 applies SGD to touched slices.
+template <typename T, int OUT_MODE>
+__global__ void k_head_g0(DevPlan P, const T* __restrict__ D0, const int32_t* __restrict__ pair_tab,
+                          const uint32_t* __restrict__ pair_key_u, const int* __restrict__ counts,
+                          T* __restrict__ out, T lr) {
+  const int U = counts[0];
+  const int s0 = P.slice[0], m0 = P.m[0], m1 = P.m[1];
+  for (int i0 = blockIdx.x; i0 < m0; i0 += gridDim.x) {
+    for (int e = threadIdx.x; e < s0; e += blockDim.x) {
+      T sum = T(0);
+      bool touched = false;
+      for (int i1 = 0; i1 < m1; ++i1) {
+        const uint32_t key = static_cast<uint32_t>(i1) * static_cast<uint32_t>(m0) + i0;
+        const int pid = pair_tab[key];
+        if (pid < 0 || pid >= U || pair_key_u[pid] != key) continue;
+        sum += D0[static_cast<int64_t>(pid) * s0 + e];
+        touched = true;
+      }
+      if (OUT_MODE == 0)
+        out[static_cast<int64_t>(i0) * s0 + e] = sum;
+      else if (touched)
+        out[static_cast<int64_t>(i0) * s0 + e] =
+            add_rn<T>(out[static_cast<int64_t>(i0) * s0 + e], -mul_rn<T>(lr, sum));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ misc --
+// sgd_step element update c -= T(lr) * g, separately rounded like the
+// reference's `c[i] -= step * g[i]` (embedding_ops.hpp:372-373).
+template <typename T>
+__global__ void k_sgd(T* __restrict__ c, const T* __restrict__ g, int64_t n, T step) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c[i] = add_rn<T>(c[i], -mul_rn<T>(step, g[i]));
+}
+
+// lookup_row for a list of rows (embedding_ops.hpp:120-152), one warp per row,
+// bit-identical to the reference (kExact).  Rows are pre-validated on the host
+// or latched into *bad.
+template <typename T>
+__global__ void k_lookup_rows(DevPlan P, const T* __restrict__ cores, const int64_t* __restrict__ rows,
+                              int64_t n, T* __restrict__ out, unsigned long long* bad) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* ping = reinterpret_cast<T*>(smem_raw) + static_cast<int64_t>(wid) * 2 * P.maxw;
+  T* pong = ping + P.maxw;
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * warps + wid; q < n;
+       q += static_cast<int64_t>(gridDim.x) * warps) {
+    int64_t row = rows[q];
+    if (row < 0 || row >= P.num_rows) {
+      if (lane == 0 && bad) atomicMin(bad, static_cast<unsigned long long>(q));
+      row = 0;
+    }
+    int dig[kMaxD];
+    decode_row(P, row, dig);
+    const T* src = cores + P.coff[0] + static_cast<int64_t>(dig[0]) * P.slice[0];
+    T* dst = ping;
+    for (int k = 1; k < P.d; ++k) {
+      const T* G = cores + P.coff[k] + static_cast<int64_t>(dig[k]) * P.slice[k];
+      T* target = (k == P.d - 1) ? out + q * P.N : dst;
+      warp_mm<T, true>(src, G, target, P.prefix[k - 1], P.r[k], P.n[k] * P.r[k + 1], lane);
+      __syncwarp();
+      src = target;
+      dst = (dst == ping) ? pong : ping;
+    }
+  }
+}
+
+}  // namespace ttgpu

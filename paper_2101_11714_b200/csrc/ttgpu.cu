@@ -1,0 +1,1112 @@
+// Host side of the B200 TT-EmbeddingBag: the device-resident table
+// (TtTable<T> equivalent), forward contexts, the launch pipeline and the C ABI
+// declared in include/ttgpu.h.  See tt_kernels.cuh for the algorithm.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/ttgpu.h"
+#include "shape_plan.hpp"
+#include "tt_kernels.cuh"
+
+namespace ttgpu {
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_rows{0};
+std::atomic<uint64_t> g_ws_cur{0};
+std::atomic<uint64_t> g_ws_peak{0};
+
+template <class... A>
+std::string cat(const A&... a) {
+  std::ostringstream os;
+  (os << ... << a);
+  return os.str();
+}
+
+struct Error : std::exception {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw Error(code, m); }
+void require_arg(bool ok, const std::string& m) {
+  if (!ok) fail(TTGPU_ERR_INVALID_ARGUMENT, m);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TTGPU_ERR_RUNTIME, cat("CUDA error in ", what, ": ", cudaGetErrorString(e)));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TTGPU_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return TTGPU_ERR_OUT_OF_RANGE;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return TTGPU_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TTGPU_ERR_RUNTIME;
+  }
+}
+
+void ws_add(uint64_t b) {
+  const uint64_t cur = g_ws_cur.fetch_add(b) + b;
+  uint64_t peak = g_ws_peak.load();
+  while (cur > peak && !g_ws_peak.compare_exchange_weak(peak, cur)) {
+  }
+}
+void ws_sub(uint64_t b) { g_ws_cur.fetch_sub(b); }
+
+// Growable device buffer; only reallocates when a call needs more.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) {
+      cudaFree(p);
+      ws_sub(cap);
+    }
+    bytes = std::max<size_t>(bytes, 256);
+    CK(cudaMalloc(&p, bytes));
+    cap = bytes;
+    ws_add(cap);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    if (p) {
+      cudaFree(p);
+      ws_sub(cap);
+    }
+  }
+};
+
+constexpr int kTailChunk = 32;   // lookups per CTA in the lookup-level reductions
+constexpr int kHeadChunk = 32;   // pairs per CTA in the head kernels
+constexpr int kThreads = 256;
+
+int bits_for(uint64_t n) {  // bits needed to represent values < n
+  int b = 0;
+  while (b < 64 && (1ull << b) < n) ++b;
+  return std::max(b, 1);
+}
+
+}  // namespace
+}  // namespace ttgpu
+
+using namespace ttgpu;
+
+struct ttgpu_table {
+  ShapePlan plan;
+  std::string name;
+  int dtype = TTGPU_F32;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t esz = 4;
+  DevPlan dp{};
+  int64_t total = 0;         // total core elements (with alignment padding)
+  DevBuf cores, grads, pair_tab, errs, lk_rows, lk_out;
+  uint64_t generation = 0;
+  bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
+  // optional phase timing (CUDA events between pipeline phases)
+  bool prof = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  std::vector<cudaEvent_t> ev_pool;
+  void mark(const char* name) {
+    if (!prof) return;
+    cudaEvent_t e;
+    if (ev_pool.empty()) {
+      cudaEventCreate(&e);
+    } else {
+      e = ev_pool.back();
+      ev_pool.pop_back();
+    }
+    cudaEventRecord(e, stream);
+    marks.emplace_back(name, e);
+  }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  ~ttgpu_table() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto& m : marks) cudaEventDestroy(m.second);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
+  // latched device errors: [0]=first bad lookup, [1]=its value, [2]=struct flags
+  unsigned long long* d_bad() { return errs.as<unsigned long long>(); }
+  int* d_struct() { return reinterpret_cast<int*>(errs.as<unsigned long long>() + 2); }
+};
+
+struct ttgpu_ctx {
+  ttgpu_table* table = nullptr;
+  uint64_t snapshot = 0;
+  bool valid = false;
+  int64_t L = 0, B = 0;
+  int pooling = 0;
+  bool save = false;
+  bool has_w = false;
+  // host-API staging
+  DevBuf h_idx, h_off, h_w, h_out, h_grad;
+  // forward state
+  DevBuf pair_key, iota, s_key, s_lk, tail_dig, lk_bag, lk_alpha, lk_pid, flags, pair_scan,
+      pair_key_u, pair_start, counts, H, saved, cub_tmp;
+  const double* w_dev = nullptr;
+  // backward state
+  DevBuf s_dkey, s_dlk, dscan, dseg, pair_i1, scan1, seg1, S, D0, partS, partK, part1;
+  size_t cub_bytes = 0;
+};
+
+namespace ttgpu {
+namespace {
+
+DevPlan make_devplan(const ShapePlan& p, std::vector<int64_t>& coff, int64_t& total) {
+  DevPlan d{};
+  d.d = p.tt_dim;
+  d.N = static_cast<int>(p.emb_dim);
+  d.num_rows = p.num_rows;
+  int64_t suf = 1;
+  for (int k = p.tt_dim - 1; k >= 0; --k) {
+    d.suffix[k] = suf;
+    suf *= p.row_factors[k];
+  }
+  int pre = 1;
+  int64_t off = 0;
+  coff.resize(p.tt_dim);
+  d.maxw = 0;
+  for (int k = 0; k < p.tt_dim; ++k) {
+    d.m[k] = static_cast<int>(p.row_factors[k]);
+    d.n[k] = static_cast<int>(p.col_factors[k]);
+    d.r[k] = static_cast<int>(p.ranks[k]);
+    pre *= d.n[k];
+    d.prefix[k] = pre;
+    d.slice[k] = static_cast<int>(p.slice_size(k));
+    d.coff[k] = off;
+    coff[k] = off;
+    off += (p.core_size(k) + 63) / 64 * 64;  // 256 B alignment per core (f32)
+    d.maxw = std::max<int>(d.maxw, pre * static_cast<int>(p.ranks[k + 1]));
+  }
+  d.r[p.tt_dim] = 1;
+  d.W1 = d.prefix[1] * d.r[2];
+  d.C1 = d.n[1] * d.r[2];
+  total = off;
+  return d;
+}
+
+void check_supported(const ShapePlan& p) {
+  for (int k = 0; k < p.tt_dim; ++k)
+    require_arg(p.row_factors[k] < (1ll << 31) && p.ranks[k + 1] < (1 << 16) &&
+                    p.col_factors[k] < (1 << 16),
+                "plan dimension too large for the GPU kernels");
+  require_arg(static_cast<uint64_t>(p.row_factors[0]) * static_cast<uint64_t>(p.row_factors[1]) <
+                  (1ull << 31),
+              "m_0 * m_1 must be < 2^31 for the GPU pair table");
+  int64_t pre = 1, maxw = 0;
+  for (int k = 0; k < p.tt_dim; ++k) {
+    pre *= p.col_factors[k];
+    maxw = std::max<int64_t>(maxw, pre * p.ranks[k + 1]);
+  }
+  require_arg(maxw <= (1 << 16), "chain width too large for the GPU kernels");
+}
+
+int grid_for(int64_t work, int per_block, int num_sms, int waves = 8) {
+  const int64_t g = (work + per_block - 1) / per_block;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, int64_t(num_sms) * waves)));
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024)
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(bytes)));
+}
+
+int warps_fitting(size_t per_warp, size_t fixed, size_t limit, int want) {
+  int w = want;
+  while (w > 1 && fixed + per_warp * w > limit) --w;
+  if (fixed + per_warp * w > 227 * 1024) fail(TTGPU_ERR_INVALID_ARGUMENT, "plan too large for shared memory");
+  return w;
+}
+
+template <typename T>
+T* core_ptr(ttgpu_table* t, int k) {
+  return t->cores.as<T>() + t->dp.coff[k];
+}
+
+// ------------------------------------------------------------- forward ---
+template <typename T>
+void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, const int64_t* off,
+                  int64_t B, const double* w, int pooling, bool save, T* out, bool exact) {
+  const DevPlan& P = t->dp;
+  cudaStream_t st = t->stream;
+  const int d = P.d;
+  c->table = t;
+  c->snapshot = t->generation;
+  c->L = L;
+  c->B = B;
+  c->pooling = pooling;
+  c->save = save && d >= 4;
+  c->has_w = w != nullptr;
+  c->w_dev = w;
+  c->valid = true;
+  g_rows.fetch_add(static_cast<uint64_t>(L));
+  if (B == 0) return;
+  if (L == 0) {
+    CK(cudaMemsetAsync(out, 0, sizeof(T) * B * P.N, st));
+    // still validate the offsets structure
+    c->lk_bag.ensure(4);
+    c->lk_alpha.ensure(sizeof(T));
+    k_bags<T><<<grid_for(B, kThreads, t->num_sms), kThreads, 0, st>>>(
+        off, B, 0, w, pooling, c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), t->d_struct());
+    CK(cudaGetLastError());
+    return;
+  }
+  const int64_t m01 = static_cast<int64_t>(P.m[0]) * P.m[1];
+  const int64_t ucap = std::min<int64_t>(L, m01);
+  c->pair_key.ensure(4 * L);
+  c->iota.ensure(4 * L);
+  c->s_key.ensure(4 * L);
+  c->s_lk.ensure(4 * L);
+  c->tail_dig.ensure(4 * L * std::max(1, d - 2));
+  c->lk_bag.ensure(4 * L);
+  c->lk_alpha.ensure(sizeof(T) * L);
+  c->lk_pid.ensure(4 * L);
+  c->flags.ensure(8 * L);
+  c->pair_scan.ensure(8 * L);
+  c->pair_key_u.ensure(4 * ucap);
+  c->pair_start.ensure(4 * (ucap + 1));
+  c->counts.ensure(64);
+  c->H.ensure(sizeof(T) * ucap * P.W1);
+  if (c->save) c->saved.ensure(sizeof(T) * (d - 3) * L * P.maxw);
+  // CUB scratch (sized for the largest sort/scan we run on L items)
+  {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, c->pair_key.as<uint32_t>(), c->s_key.as<uint32_t>(),
+                                    c->iota.as<uint32_t>(), c->s_lk.as<uint32_t>(), L, 0, 32, st);
+    cub::DeviceScan::InclusiveSum(nullptr, b, c->flags.as<unsigned long long>(),
+                                  c->pair_scan.as<unsigned long long>(), L, st);
+    c->cub_bytes = std::max(a, b);
+    c->cub_tmp.ensure(c->cub_bytes);
+  }
+  const int gL = grid_for(L, kThreads, t->num_sms);
+  t->mark("fwd_begin");
+  k_decode<<<gL, kThreads, 0, st>>>(P, idx, L, c->pair_key.as<uint32_t>(), c->iota.as<uint32_t>(),
+                                    c->tail_dig.as<uint32_t>(), t->d_bad());
+  k_bags<T><<<grid_for(B, kThreads, t->num_sms), kThreads, 0, st>>>(
+      off, B, L, w, pooling, c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), t->d_struct());
+  t->mark("decode");
+  size_t tb = c->cub_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tb, c->pair_key.as<uint32_t>(),
+                                     c->s_key.as<uint32_t>(), c->iota.as<uint32_t>(),
+                                     c->s_lk.as<uint32_t>(), L, 0, bits_for(m01), st));
+  t->mark("sort_pairs");
+  k_run_flags<<<gL, kThreads, 0, st>>>(c->s_key.as<uint32_t>(), nullptr, L, kTailChunk,
+                                       c->flags.as<unsigned long long>());
+  tb = c->cub_bytes;
+  CK(cub::DeviceScan::InclusiveSum(c->cub_tmp.p, tb, c->flags.as<unsigned long long>(),
+                                   c->pair_scan.as<unsigned long long>(), L, st));
+  k_pairs_compact<<<gL, kThreads, 0, st>>>(
+      c->s_key.as<uint32_t>(), c->s_lk.as<uint32_t>(), c->pair_scan.as<unsigned long long>(), L,
+      c->pair_key_u.as<uint32_t>(), c->pair_start.as<int32_t>(), c->lk_pid.as<int32_t>(),
+      c->counts.as<int>());
+  t->mark("pairs_compact");
+  // head GEMM per unique pair
+  {
+    const size_t smem = sizeof(T) * (P.slice[1] + static_cast<size_t>(kHeadChunk) * P.slice[0]);
+    auto kern = exact ? k_head_fwd<T, true> : k_head_fwd<T, false>;
+    set_smem(kern, smem);
+    const int g = grid_for(ucap, kHeadChunk, t->num_sms, 4);
+    kern<<<g, kThreads, smem, st>>>(P, t->cores.as<T>(), c->pair_key_u.as<uint32_t>(),
+                                    c->counts.as<int>(), kHeadChunk, c->H.as<T>());
+  }
+  t->mark("head_fwd");
+  // tail chain + pooling per bag
+  {
+    const size_t per_warp = sizeof(T) * (2 * P.maxw + P.N);
+    const int warps = warps_fitting(per_warp, 0, 96 * 1024, 8);
+    const size_t smem = per_warp * warps;
+    auto kern = exact ? k_tail_pool<T, true> : k_tail_pool<T, false>;
+    set_smem(kern, smem);
+    kern<<<grid_for(B, warps, t->num_sms), warps * 32, smem, st>>>(
+        P, t->cores.as<T>(), c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
+        off, B, L, w, pooling, out, c->save ? c->saved.as<T>() : nullptr);
+  }
+  t->mark("tail_pool");
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ backward ---
+// mode 0: dense gradient into t->grads; mode 1: fused SGD (lr) on touched slices.
+template <typename T>
+void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double lr) {
+  const DevPlan& P = t->dp;
+  cudaStream_t st = t->stream;
+  const int d = P.d;
+  const int64_t L = c->L;
+  T* cores = t->cores.as<T>();
+  T* grads = t->grads.as<T>();
+  if (mode == 0) CK(cudaMemsetAsync(grads, 0, sizeof(T) * t->total, st));
+  if (L == 0 || c->B == 0) return;
+  const int64_t m01 = static_cast<int64_t>(P.m[0]) * P.m[1];
+  const int64_t ucap = std::min<int64_t>(L, m01);
+  const int gL = grid_for(L, kThreads, t->num_sms);
+  const T tlr = static_cast<T>(lr);
+  // ---- tail-digit orderings (k >= 2)
+  const int ntail = std::max(0, d - 2);
+  if (ntail) {
+    c->s_dkey.ensure(4 * L * ntail);
+    c->s_dlk.ensure(4 * L * ntail);
+    c->dscan.ensure(8 * L * ntail);
+    int64_t segsz = 0;
+    for (int k = 2; k < d; ++k) segsz += P.m[k] + 1;
+    c->dseg.ensure(4 * segsz);
+  }
+  // ---- pair ordering by i1
+  c->pair_i1.ensure(4 * L);
+  c->scan1.ensure(8 * L);
+  c->seg1.ensure(4 * (P.m[1] + 1));
+  c->S.ensure(sizeof(T) * ucap * P.W1);
+  c->D0.ensure(sizeof(T) * ucap * P.slice[0]);
+  const int64_t nchunksL = (L + kTailChunk - 1) / kTailChunk;
+  c->partS.ensure(sizeof(T) * (nchunksL + ucap + 1) * P.W1);
+  int64_t partk = 0;
+  for (int k = 2; k < d; ++k)
+    partk = std::max<int64_t>(partk, (nchunksL + std::min<int64_t>(L, P.m[k]) + 1) * P.slice[k]);
+  c->partK.ensure(sizeof(T) * std::max<int64_t>(partk, 1));
+  c->part1.ensure(sizeof(T) * ((ucap + kHeadChunk - 1) / kHeadChunk + std::min<int64_t>(ucap, P.m[1]) + 1) *
+                  P.slice[1]);
+
+  t->mark("bwd_begin");
+  int64_t segoff = 0;
+  for (int k = 2; k < d; ++k) {
+    const int j = k - 2;
+    uint32_t* dk = c->tail_dig.as<uint32_t>() + j * L;
+    uint32_t* sk = c->s_dkey.as<uint32_t>() + j * L;
+    uint32_t* sl = c->s_dlk.as<uint32_t>() + j * L;
+    unsigned long long* sc = c->dscan.as<unsigned long long>() + j * L;
+    int32_t* seg = c->dseg.as<int32_t>() + segoff;
+    size_t tb = c->cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tb, dk, sk, c->iota.as<uint32_t>(), sl, L, 0,
+                                       bits_for(P.m[k]), st));
+    k_run_flags<<<gL, kThreads, 0, st>>>(sk, nullptr, L, kTailChunk, c->flags.as<unsigned long long>());
+    tb = c->cub_bytes;
+    CK(cub::DeviceScan::InclusiveSum(c->cub_tmp.p, tb, c->flags.as<unsigned long long>(), sc, L, st));
+    k_key_bounds<<<gL, kThreads, 0, st>>>(sk, nullptr, L, P.m[k], seg);
+    segoff += P.m[k] + 1;
+  }
+  k_pair_scatter<<<gL, kThreads, 0, st>>>(c->pair_key_u.as<uint32_t>(), c->counts.as<int>(), ucap,
+                                          t->pair_tab.as<int32_t>());
+  k_pair_i1<<<gL, kThreads, 0, st>>>(c->pair_key_u.as<uint32_t>(), c->counts.as<int>(), L, P.m[0],
+                                     c->pair_i1.as<uint32_t>());
+  k_run_flags<<<gL, kThreads, 0, st>>>(c->pair_i1.as<uint32_t>(), c->counts.as<int>(), L, kHeadChunk,
+                                       c->flags.as<unsigned long long>());
+  {
+    size_t tb = c->cub_bytes;
+    CK(cub::DeviceScan::InclusiveSum(c->cub_tmp.p, tb, c->flags.as<unsigned long long>(),
+                                     c->scan1.as<unsigned long long>(), L, st));
+  }
+  k_key_bounds<<<gL, kThreads, 0, st>>>(c->pair_i1.as<uint32_t>(), c->counts.as<int>(), L, P.m[1],
+                                        c->seg1.as<int32_t>());
+
+  t->mark("bwd_prep");
+  // ---- S(pair) = sum of D1 over the pair's lookups
+  {
+    const int Wc = P.W1;
+    const size_t per_warp = sizeof(T) * (Wc + 4 * static_cast<size_t>(P.maxw));
+    const int warps = warps_fitting(per_warp, sizeof(T) * Wc, 100 * 1024, 8);
+    const size_t smem = sizeof(T) * Wc + per_warp * warps;
+    auto kern = k_chunk_reduce<T, 0>;
+    set_smem(kern, smem);
+    kern<<<grid_for(nchunksL, 1, t->num_sms, 4), warps * 32, smem, st>>>(
+        P, cores, c->H.as<T>(), nullptr, c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
+        c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad, c->s_key.as<uint32_t>(),
+        c->s_lk.as<uint32_t>(), c->pair_scan.as<unsigned long long>(), L, kTailChunk, 1, Wc,
+        c->partS.as<T>());
+    k_combine<T, 0><<<grid_for(ucap, 1, t->num_sms, 8), 128, 0, st>>>(
+        c->partS.as<T>(), c->pair_scan.as<unsigned long long>(), c->pair_start.as<int32_t>(),
+        c->counts.as<int>(), 0, Wc, c->S.as<T>(), T(0));
+  }
+  t->mark("bwd_S");
+  // ---- tail cores k >= 2 (the fused in-place update is only safe when no
+  //      later kernel reads core k, i.e. d == 3)
+  const bool fuse_tail = (mode == 1 && d == 3);
+  segoff = 0;
+  for (int k = 2; k < d; ++k) {
+    const int j = k - 2;
+    const int Wc = P.slice[k];
+    const size_t per_warp = sizeof(T) * (Wc + 4 * static_cast<size_t>(P.maxw));
+    const int warps = warps_fitting(per_warp, sizeof(T) * Wc, 100 * 1024, 8);
+    const size_t smem = sizeof(T) * Wc + per_warp * warps;
+    auto kern = k_chunk_reduce<T, 1>;
+    set_smem(kern, smem);
+    kern<<<grid_for(nchunksL, 1, t->num_sms, 4), warps * 32, smem, st>>>(
+        P, cores, c->H.as<T>(), c->save ? c->saved.as<T>() : nullptr, c->lk_pid.as<int32_t>(),
+        c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad,
+        c->s_dkey.as<uint32_t>() + j * L, c->s_dlk.as<uint32_t>() + j * L,
+        c->dscan.as<unsigned long long>() + j * L, L, kTailChunk, k, Wc, c->partK.as<T>());
+    T* dst = fuse_tail ? cores + P.coff[k] : grads + P.coff[k];
+    if (fuse_tail)
+      k_combine<T, 1><<<grid_for(P.m[k], 1, t->num_sms, 8), 128, 0, st>>>(
+          c->partK.as<T>(), c->dscan.as<unsigned long long>() + j * L, c->dseg.as<int32_t>() + segoff,
+          nullptr, P.m[k], Wc, dst, tlr);
+    else
+      k_combine<T, 0><<<grid_for(P.m[k], 1, t->num_sms, 8), 128, 0, st>>>(
+          c->partK.as<T>(), c->dscan.as<unsigned long long>() + j * L, c->dseg.as<int32_t>() + segoff,
+          nullptr, P.m[k], Wc, dst, T(0));
+    segoff += P.m[k] + 1;
+  }
+  t->mark("bwd_tail");
+  // ---- head: D0 per pair, dG1 partials per i1 run
+  {
+    const size_t smem = sizeof(T) * 2 * static_cast<size_t>(P.slice[1]);
+    if (smem > 227 * 1024) fail(TTGPU_ERR_INVALID_ARGUMENT, "G1 slice too large for shared memory");
+    auto kern = k_head_bwd<T>;
+    set_smem(kern, smem);
+    kern<<<grid_for(ucap, kHeadChunk, t->num_sms, 2), kThreads, smem, st>>>(
+        P, cores, c->S.as<T>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
+        c->scan1.as<unsigned long long>(), kHeadChunk, c->D0.as<T>(), c->part1.as<T>());
+  }
+  t->mark("bwd_head");
+  const bool fuse_head = (mode == 1);
+  if (fuse_head)
+    k_combine<T, 1><<<grid_for(P.m[1], 1, t->num_sms, 8), 256, 0, st>>>(
+        c->part1.as<T>(), c->scan1.as<unsigned long long>(), c->seg1.as<int32_t>(), nullptr, P.m[1],
+        P.slice[1], cores + P.coff[1], tlr);
+  else
+    k_combine<T, 0><<<grid_for(P.m[1], 1, t->num_sms, 8), 256, 0, st>>>(
+        c->part1.as<T>(), c->scan1.as<unsigned long long>(), c->seg1.as<int32_t>(), nullptr, P.m[1],
+        P.slice[1], grads + P.coff[1], T(0));
+  t->mark("bwd_head_combine");
+  if (fuse_head)
+    k_head_g0<T, 1><<<grid_for(P.m[0], 1, t->num_sms, 8), 128, 0, st>>>(
+        P, c->D0.as<T>(), t->pair_tab.as<int32_t>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
+        cores + P.coff[0], tlr);
+  else
+    k_head_g0<T, 0><<<grid_for(P.m[0], 1, t->num_sms, 8), 128, 0, st>>>(
+        P, c->D0.as<T>(), t->pair_tab.as<int32_t>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
+        grads + P.coff[0], T(0));
+  t->mark("bwd_g0");
+  // fused mode with d >= 4: tail slices were written densely; apply them now
+  if (mode == 1 && !fuse_tail && d >= 4) {
+    for (int k = 2; k < d; ++k) {
+      const int64_t n = P.slice[k] * static_cast<int64_t>(P.m[k]);
+      k_sgd<T><<<grid_for(n, kThreads, t->num_sms), kThreads, 0, st>>>(cores + P.coff[k],
+                                                                       grads + P.coff[k], n, tlr);
+    }
+  }
+  CK(cudaGetLastError());
+}
+
+void check_ctx(ttgpu_table* t, ttgpu_ctx* c) {
+  require_arg(c != nullptr && c->valid, "forward context is empty (run forward first)");
+  require_arg(c->table == t, "forward context belongs to a different table");
+  require_arg(c->snapshot == t->generation,
+              cat("stale forward context for table '", t->name,
+                  "': cores changed since the forward pass"));
+}
+
+void raise_latched(ttgpu_table* t, const int64_t* host_idx) {
+  unsigned long long h[3];
+  CK(cudaMemcpyAsync(h, t->errs.p, sizeof(h), cudaMemcpyDeviceToHost, t->stream));
+  CK(cudaStreamSynchronize(t->stream));
+  const int sflags = static_cast<int>(h[2] & 0xffffffffu);
+  if (sflags == 0 && h[0] == ULLONG_MAX) return;
+  // reset the latch before reporting
+  unsigned long long init[3] = {ULLONG_MAX, 0, 0};
+  CK(cudaMemcpyAsync(t->errs.p, init, sizeof(init), cudaMemcpyHostToDevice, t->stream));
+  CK(cudaStreamSynchronize(t->stream));
+  if (sflags & 1) fail(TTGPU_ERR_INVALID_ARGUMENT, "offsets must start at 0");
+  if (sflags & 2) fail(TTGPU_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing");
+  if (sflags & 4) fail(TTGPU_ERR_INVALID_ARGUMENT, "offsets end does not match the index count");
+  const int64_t pos = static_cast<int64_t>(h[0]);
+  if (host_idx)
+    throw std::out_of_range(cat("index ", host_idx[pos], " out of range [0, ", t->plan.num_rows,
+                                ") for table '", t->name, "'"));
+  throw std::out_of_range(cat("index at lookup ", pos, " out of range [0, ", t->plan.num_rows,
+                              ") for table '", t->name, "'"));
+}
+
+// Host-side structural validation with the reference's messages
+// (index_batch.hpp:41-56); index range is checked on the device.
+void validate_host(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* off, int64_t B) {
+  require_arg(off != nullptr && off[0] == 0, "offsets must start at 0");
+  for (int64_t b = 0; b < B; ++b) require_arg(off[b] <= off[b + 1], "offsets must be non-decreasing");
+  require_arg(off[B] == L, cat("offsets end at ", off[B], " but there are ", L, " indices"));
+  (void)idx;
+  (void)t;
+}
+
+}  // namespace
+}  // namespace ttgpu
+
+// =========================================================================
+//                                 C ABI
+// =========================================================================
+extern "C" {
+
+const char* ttgpu_last_error(void) { return g_last_error.c_str(); }
+int ttgpu_abi_version(void) { return 1; }
+
+int ttgpu_plan_shapes(int64_t num_rows, int64_t emb_dim, int tt_dim, int64_t rank,
+                      const int64_t* rf_in, const int64_t* cf_in, int64_t* rf_out, int64_t* cf_out,
+                      int64_t* ranks_out) {
+  return guarded([&] {
+    ShapePlan p = plan_shapes(num_rows, emb_dim, tt_dim, rank, rf_in, cf_in);
+    std::copy(p.row_factors.begin(), p.row_factors.end(), rf_out);
+    std::copy(p.col_factors.begin(), p.col_factors.end(), cf_out);
+    std::copy(p.ranks.begin(), p.ranks.end(), ranks_out);
+  });
+}
+
+int ttgpu_plan_info(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* rf,
+                    const int64_t* cf, const int64_t* ranks, int64_t* padded, int64_t* params,
+                    int64_t* reduction) {
+  return guarded([&] {
+    require_arg(tt_dim >= kMinTtDim && tt_dim <= kMaxTtDim,
+                cat("tt_dim must be in [", kMinTtDim, ", ", kMaxTtDim, "], got ", tt_dim));
+    ShapePlan p;
+    p.num_rows = num_rows;
+    p.emb_dim = emb_dim;
+    p.tt_dim = tt_dim;
+    p.row_factors.assign(rf, rf + tt_dim);
+    p.col_factors.assign(cf, cf + tt_dim);
+    p.ranks.assign(ranks, ranks + tt_dim + 1);
+    p.validate();
+    if (padded) *padded = p.padded_rows();
+    if (params) *params = p.parameter_count();
+    if (reduction) *reduction = p.memory_reduction();
+  });
+}
+
+int ttgpu_decompose_index(int64_t flat, const int64_t* radices, int n, int64_t* digits) {
+  return guarded([&] {
+    auto v = decompose_index(flat, radices, n);
+    std::copy(v.begin(), v.end(), digits);
+  });
+}
+
+int ttgpu_recompose_index(const int64_t* digits, const int64_t* radices, int n, int64_t* flat) {
+  return guarded([&] { *flat = recompose_index(digits, radices, n); });
+}
+
+int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* rf,
+                 const int64_t* cf, const int64_t* ranks, int dtype, const char* name, int device,
+                 void* stream, ttgpu_table** out) {
+  return guarded([&] {
+    require_arg(dtype == TTGPU_F32 || dtype == TTGPU_F64, "dtype must be TTGPU_F32 or TTGPU_F64");
+    require_arg(tt_dim >= kMinTtDim && tt_dim <= kMaxTtDim,
+                cat("tt_dim must be in [", kMinTtDim, ", ", kMaxTtDim, "], got ", tt_dim));
+    auto t = std::make_unique<ttgpu_table>();
+    t->plan.num_rows = num_rows;
+    t->plan.emb_dim = emb_dim;
+    t->plan.tt_dim = tt_dim;
+    t->plan.row_factors.assign(rf, rf + tt_dim);
+    t->plan.col_factors.assign(cf, cf + tt_dim);
+    t->plan.ranks.assign(ranks, ranks + tt_dim + 1);
+    t->plan.validate();
+    check_supported(t->plan);
+    t->name = name ? name : "tt-table";
+    t->dtype = dtype;
+    t->esz = dtype == TTGPU_F64 ? 8 : 4;
+    t->device = device;
+    t->stream = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, device));
+    std::vector<int64_t> coff;
+    t->dp = make_devplan(t->plan, coff, t->total);
+    t->cores.ensure(t->esz * t->total);
+    t->grads.ensure(t->esz * t->total);
+    CK(cudaMemsetAsync(t->cores.p, 0, t->esz * t->total, t->stream));
+    CK(cudaMemsetAsync(t->grads.p, 0, t->esz * t->total, t->stream));
+    const int64_t m01 = static_cast<int64_t>(t->dp.m[0]) * t->dp.m[1];
+    t->pair_tab.ensure(4 * m01);
+    CK(cudaMemsetAsync(t->pair_tab.p, 0xff, 4 * m01, t->stream));
+    t->errs.ensure(3 * sizeof(unsigned long long));
+    unsigned long long init[3] = {ULLONG_MAX, 0, 0};
+    CK(cudaMemcpyAsync(t->errs.p, init, sizeof(init), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    *out = t.release();
+  });
+}
+
+int ttgpu_destroy(ttgpu_table* t) {
+  return guarded([&] {
+    if (t) {
+      cudaStreamSynchronize(t->stream);
+      delete t;
+    }
+  });
+}
+
+int ttgpu_set_stream(ttgpu_table* t, void* stream) {
+  return guarded([&] { t->stream = static_cast<cudaStream_t>(stream); });
+}
+
+int ttgpu_core_size(const ttgpu_table* t, int k, int64_t* n) {
+  return guarded([&] {
+    require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
+    *n = t->plan.core_size(k);
+  });
+}
+
+int ttgpu_get_core(ttgpu_table* t, int k, void* dst) {
+  return guarded([&] {
+    require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
+    CK(cudaMemcpyAsync(dst, static_cast<char*>(t->cores.p) + t->esz * t->dp.coff[k],
+                       t->esz * t->plan.core_size(k), cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int ttgpu_set_core(ttgpu_table* t, int k, const void* src) {
+  return guarded([&] {
+    require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
+    CK(cudaMemcpyAsync(static_cast<char*>(t->cores.p) + t->esz * t->dp.coff[k], src,
+                       t->esz * t->plan.core_size(k), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    ++t->generation;
+  });
+}
+
+int ttgpu_core_device_ptr(ttgpu_table* t, int k, void** p) {
+  return guarded([&] {
+    require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
+    *p = static_cast<char*>(t->cores.p) + t->esz * t->dp.coff[k];
+  });
+}
+
+int ttgpu_grad_device_ptr(ttgpu_table* t, int k, void** p) {
+  return guarded([&] {
+    require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
+    *p = static_cast<char*>(t->grads.p) + t->esz * t->dp.coff[k];
+  });
+}
+
+int ttgpu_set_exact_forward(ttgpu_table* t, int on) {
+  return guarded([&] { t->exact = on != 0; });
+}
+
+int ttgpu_mark_mutated(ttgpu_table* t) {
+  return guarded([&] { ++t->generation; });
+}
+
+int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out) {
+  return guarded([&] { *out = t->generation; });
+}
+
+int ttgpu_ctx_create(ttgpu_table* t, ttgpu_ctx** out) {
+  return guarded([&] {
+    auto* c = new ttgpu_ctx;
+    c->table = t;
+    *out = c;
+  });
+}
+
+int ttgpu_ctx_destroy(ttgpu_ctx* c) {
+  return guarded([&] {
+    if (c && c->table) cudaStreamSynchronize(c->table->stream);
+    delete c;
+  });
+}
+
+int ttgpu_forward(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                  const double* w, int pooling, int64_t micro_batch, int save, void* out,
+                  ttgpu_ctx* c) {
+  return guarded([&] {
+    require_arg(c != nullptr, "forward needs a context");
+    require_arg(L >= 0 && B >= 0, "negative batch size");
+    validate_host(t, idx, L, off, B);
+    require_arg(micro_batch >= 1, cat("micro_batch must be positive, got ", micro_batch));
+    c->valid = false;
+    c->h_idx.ensure(8 * std::max<int64_t>(L, 1));
+    c->h_off.ensure(8 * (B + 1));
+    c->h_out.ensure(t->esz * std::max<int64_t>(B * t->plan.emb_dim, 1));
+    CK(cudaMemcpyAsync(c->h_idx.p, idx, 8 * L, cudaMemcpyHostToDevice, t->stream));
+    CK(cudaMemcpyAsync(c->h_off.p, off, 8 * (B + 1), cudaMemcpyHostToDevice, t->stream));
+    const double* dw = nullptr;
+    if (w && L > 0) {
+      c->h_w.ensure(8 * L);
+      CK(cudaMemcpyAsync(c->h_w.p, w, 8 * L, cudaMemcpyHostToDevice, t->stream));
+      dw = c->h_w.as<double>();
+    }
+    if (t->dtype == TTGPU_F64)
+      forward_impl<double>(t, c, c->h_idx.as<int64_t>(), L, c->h_off.as<int64_t>(), B, dw,
+                           pooling, save != 0, c->h_out.as<double>(), t->exact);
+    else
+      forward_impl<float>(t, c, c->h_idx.as<int64_t>(), L, c->h_off.as<int64_t>(), B, dw, pooling,
+                          save != 0, c->h_out.as<float>(), t->exact);
+    if (B > 0)
+      CK(cudaMemcpyAsync(out, c->h_out.p, t->esz * B * t->plan.emb_dim, cudaMemcpyDeviceToHost,
+                         t->stream));
+    try {
+      raise_latched(t, idx);
+    } catch (...) {
+      c->valid = false;
+      throw;
+    }
+  });
+}
+
+int ttgpu_forward_device(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* off,
+                         int64_t B, const double* w, int pooling, int save, void* out,
+                         ttgpu_ctx* c) {
+  return guarded([&] {
+    require_arg(c != nullptr, "forward needs a context");
+    require_arg(L >= 0 && B >= 0, "negative batch size");
+    if (t->dtype == TTGPU_F64)
+      forward_impl<double>(t, c, idx, L, off, B, w, pooling, save != 0, static_cast<double*>(out),
+                           t->exact);
+    else
+      forward_impl<float>(t, c, idx, L, off, B, w, pooling, save != 0, static_cast<float*>(out),
+                          t->exact);
+  });
+}
+
+int ttgpu_backward(ttgpu_table* t, ttgpu_ctx* c, int64_t L, int64_t B, const void* grad,
+                   int64_t grad_len, void* const* grads_out) {
+  return guarded([&] {
+    check_ctx(t, c);
+    require_arg(c->L == L && c->B == B,
+                cat("forward context does not match this batch (", c->L, "/", c->B, " vs ", L, "/",
+                    B, ")"));
+    require_arg(grad_len == B * t->plan.emb_dim,
+                cat("grad_output has ", grad_len, " elements, expected ", B * t->plan.emb_dim));
+    c->h_grad.ensure(t->esz * std::max<int64_t>(grad_len, 1));
+    if (grad_len > 0)
+      CK(cudaMemcpyAsync(c->h_grad.p, grad, t->esz * grad_len, cudaMemcpyHostToDevice, t->stream));
+    if (t->dtype == TTGPU_F64)
+      backward_impl<double>(t, c, c->h_grad.as<double>(), 0, 0.0);
+    else
+      backward_impl<float>(t, c, c->h_grad.as<float>(), 0, 0.0);
+    if (grads_out)
+      for (int k = 0; k < t->plan.tt_dim; ++k)
+        if (grads_out[k])
+          CK(cudaMemcpyAsync(grads_out[k], static_cast<char*>(t->grads.p) + t->esz * t->dp.coff[k],
+                             t->esz * t->plan.core_size(k), cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int ttgpu_backward_device(ttgpu_table* t, ttgpu_ctx* c, const void* grad) {
+  return guarded([&] {
+    check_ctx(t, c);
+    if (t->dtype == TTGPU_F64)
+      backward_impl<double>(t, c, static_cast<const double*>(grad), 0, 0.0);
+    else
+      backward_impl<float>(t, c, static_cast<const float*>(grad), 0, 0.0);
+  });
+}
+
+int ttgpu_backward_sgd_device(ttgpu_table* t, ttgpu_ctx* c, const void* grad, double lr) {
+  return guarded([&] {
+    check_ctx(t, c);
+    if (t->dtype == TTGPU_F64)
+      backward_impl<double>(t, c, static_cast<const double*>(grad), 1, lr);
+    else
+      backward_impl<float>(t, c, static_cast<const float*>(grad), 1, lr);
+    ++t->generation;
+  });
+}
+
+int ttgpu_backward_sgd(ttgpu_table* t, ttgpu_ctx* c, int64_t L, int64_t B, const void* grad,
+                       int64_t grad_len, double lr) {
+  return guarded([&] {
+    check_ctx(t, c);
+    require_arg(c->L == L && c->B == B,
+                cat("forward context does not match this batch (", c->L, "/", c->B, " vs ", L, "/",
+                    B, ")"));
+    require_arg(grad_len == B * t->plan.emb_dim,
+                cat("grad_output has ", grad_len, " elements, expected ", B * t->plan.emb_dim));
+    c->h_grad.ensure(t->esz * std::max<int64_t>(grad_len, 1));
+    if (grad_len > 0)
+      CK(cudaMemcpyAsync(c->h_grad.p, grad, t->esz * grad_len, cudaMemcpyHostToDevice, t->stream));
+    if (t->dtype == TTGPU_F64)
+      backward_impl<double>(t, c, c->h_grad.as<double>(), 1, lr);
+    else
+      backward_impl<float>(t, c, c->h_grad.as<float>(), 1, lr);
+    ++t->generation;
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int ttgpu_grad_buffer(ttgpu_table* t, void** ptr, int64_t* n) {
+  return guarded([&] {
+    *ptr = t->grads.p;
+    *n = t->total;
+  });
+}
+
+int ttgpu_graph_begin(ttgpu_table* t) {
+  return guarded([&] {
+    require_arg(t->stream != nullptr, "graph capture needs a non-default stream (ttgpu_set_stream)");
+    CK(cudaStreamBeginCapture(t->stream, cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+int ttgpu_graph_end(ttgpu_table* t, int* kernel_nodes, int* total_nodes) {
+  return guarded([&] {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamEndCapture(t->stream, &g));
+    if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
+    if (t->graph) cudaGraphDestroy(t->graph);
+    t->graph = g;
+    CK(cudaGraphInstantiate(&t->graph_exec, g, 0));
+    size_t n = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (n) CK(cudaGraphGetNodes(g, nodes.data(), &n));
+    int kn = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      CK(cudaGraphNodeGetType(nd, &ty));
+      if (ty == cudaGraphNodeTypeKernel) ++kn;
+    }
+    if (kernel_nodes) *kernel_nodes = kn;
+    if (total_nodes) *total_nodes = static_cast<int>(n);
+  });
+}
+
+int ttgpu_graph_launch(ttgpu_table* t) {
+  return guarded([&] {
+    require_arg(t->graph_exec != nullptr, "no captured graph");
+    CK(cudaGraphLaunch(t->graph_exec, t->stream));
+  });
+}
+
+int ttgpu_apply_grad(ttgpu_table* t, double lr) {
+  return guarded([&] {
+    for (int k = 0; k < t->plan.tt_dim; ++k) {
+      const int64_t n = t->plan.core_size(k);
+      if (n == 0) continue;
+      const int g = grid_for(n, kThreads, t->num_sms);
+      if (t->dtype == TTGPU_F64)
+        k_sgd<double><<<g, kThreads, 0, t->stream>>>(t->cores.as<double>() + t->dp.coff[k],
+                                                     t->grads.as<double>() + t->dp.coff[k], n,
+                                                     static_cast<double>(lr));
+      else
+        k_sgd<float><<<g, kThreads, 0, t->stream>>>(t->cores.as<float>() + t->dp.coff[k],
+                                                    t->grads.as<float>() + t->dp.coff[k], n,
+                                                    static_cast<float>(lr));
+    }
+    CK(cudaGetLastError());
+    ++t->generation;
+  });
+}
+
+int ttgpu_sgd_step(ttgpu_table* t, const void* const* host_grads, double lr) {
+  return guarded([&] {
+    require_arg(host_grads != nullptr, "gradient core count mismatch");
+    for (int k = 0; k < t->plan.tt_dim; ++k) {
+      require_arg(host_grads[k] != nullptr, cat("gradient shape mismatch on core ", k));
+      CK(cudaMemcpyAsync(static_cast<char*>(t->grads.p) + t->esz * t->dp.coff[k], host_grads[k],
+                         t->esz * t->plan.core_size(k), cudaMemcpyHostToDevice, t->stream));
+    }
+    const int st = ttgpu_apply_grad(t, lr);
+    if (st) fail(st, g_last_error);
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int ttgpu_lookup_rows_device(ttgpu_table* t, const int64_t* rows, int64_t n, void* out) {
+  return guarded([&] {
+    if (n <= 0) return;
+    const DevPlan& P = t->dp;
+    const size_t per_warp = t->esz * 2 * P.maxw;
+    const int warps = warps_fitting(per_warp, 0, 64 * 1024, 8);
+    const int g = grid_for(n, warps, t->num_sms);
+    if (t->dtype == TTGPU_F64) {
+      set_smem(k_lookup_rows<double>, per_warp * warps);
+      k_lookup_rows<double><<<g, warps * 32, per_warp * warps, t->stream>>>(
+          P, t->cores.as<double>(), rows, n, static_cast<double*>(out), t->d_bad());
+    } else {
+      set_smem(k_lookup_rows<float>, per_warp * warps);
+      k_lookup_rows<float><<<g, warps * 32, per_warp * warps, t->stream>>>(
+          P, t->cores.as<float>(), rows, n, static_cast<float*>(out), t->d_bad());
+    }
+    CK(cudaGetLastError());
+    g_rows.fetch_add(static_cast<uint64_t>(n));
+  });
+}
+
+int ttgpu_lookup_row(ttgpu_table* t, int64_t row, void* out) {
+  return guarded([&] {
+    if (row < 0 || row >= t->plan.num_rows)
+      throw std::out_of_range(cat("index ", row, " out of range [0, ", t->plan.num_rows,
+                                  ") for table '", t->name, "'"));
+    DevBuf& r = t->lk_rows;
+    DevBuf& o = t->lk_out;
+    r.ensure(8);
+    o.ensure(t->esz * t->plan.emb_dim);
+    CK(cudaMemcpyAsync(r.p, &row, 8, cudaMemcpyHostToDevice, t->stream));
+    const int st = ttgpu_lookup_rows_device(t, r.as<int64_t>(), 1, o.p);
+    if (st) fail(st, g_last_error);
+    CK(cudaMemcpyAsync(out, o.p, t->esz * t->plan.emb_dim, cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int ttgpu_profile(ttgpu_table* t, int on) {
+  return guarded([&] {
+    CK(cudaStreamSynchronize(t->stream));
+    for (auto& m : t->marks) t->ev_pool.push_back(m.second);
+    t->marks.clear();
+    t->prof = on != 0;
+  });
+}
+
+int ttgpu_profile_read(ttgpu_table* t, char* names, int64_t names_len, float* ms, int max_phases,
+                       int* n_out) {
+  return guarded([&] {
+    CK(cudaStreamSynchronize(t->stream));
+    std::string all;
+    int n = 0;
+    for (size_t i = 1; i < t->marks.size() && n < max_phases; ++i) {
+      const std::string& nm = t->marks[i].first;
+      if (nm == "fwd_begin" || nm == "bwd_begin") continue;
+      float v = 0;
+      CK(cudaEventElapsedTime(&v, t->marks[i - 1].second, t->marks[i].second));
+      ms[n++] = v;
+      all += nm;
+      all += ';';
+    }
+    if (names && names_len > 0) {
+      std::strncpy(names, all.c_str(), static_cast<size_t>(names_len - 1));
+      names[names_len - 1] = 0;
+    }
+    *n_out = n;
+    for (auto& m : t->marks) t->ev_pool.push_back(m.second);
+    t->marks.clear();
+  });
+}
+
+int ttgpu_sync(ttgpu_table* t) {
+  return guarded([&] { CK(cudaStreamSynchronize(t->stream)); });
+}
+
+int ttgpu_check(ttgpu_table* t) {
+  return guarded([&] { raise_latched(t, nullptr); });
+}
+
+void ttgpu_stats_reset(void) {
+  g_rows.store(0);
+  g_ws_peak.store(g_ws_cur.load());
+}
+uint64_t ttgpu_stats_rows(void) { return g_rows.load(); }
+uint64_t ttgpu_stats_peak_workspace(void) { return g_ws_peak.load(); }
+void ttgpu_stats_add_rows(uint64_t n) { g_rows.fetch_add(n); }
+
+// ---- synthetic streams: same algorithms and libstdc++ engines as the
+// reference (rng.hpp:10-51, data.cpp:8-47, initializer.hpp:95-154) -------
+namespace {
+constexpr uint64_t splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+}  // namespace
+
+int ttgpu_zipf_batch(int64_t population, double s, uint64_t seed, int64_t bags, int64_t pf,
+                     int64_t* indices, int64_t* offsets) {
+  return guarded([&] {
+    require_arg(population >= 1, cat("population must be positive, got ", population));
+    require_arg(s >= 0, cat("exponent must be non-negative, got ", s));
+    require_arg(bags >= 0, "num_bags must be non-negative");
+    require_arg(pf >= 1, cat("pooling_factor must be >= 1, got ", pf));
+    std::vector<double> cdf(population);
+    double acc = 0.0;
+    for (int64_t r = 0; r < population; ++r) {
+      acc += std::pow(static_cast<double>(r + 1), -s);
+      cdf[r] = acc;
+    }
+    const double inv = 1.0 / acc;
+    for (double& c : cdf) c *= inv;
+    cdf.back() = 1.0;
+    std::mt19937_64 eng(splitmix(seed));
+    std::uniform_real_distribution<double> unit(0.0, 1.0);
+    int64_t n = 0;
+    offsets[0] = 0;
+    for (int64_t b = 0; b < bags; ++b) {
+      for (int64_t p = 0; p < pf; ++p) {
+        const double u = unit(eng);
+        auto it = std::upper_bound(cdf.begin(), cdf.end(), u);
+        if (it == cdf.end()) --it;
+        indices[n++] = static_cast<int64_t>(it - cdf.begin());
+      }
+      offsets[b + 1] = n;
+    }
+  });
+}
+
+int ttgpu_uniform_indices(int64_t rows, uint64_t seed, int64_t n, int64_t* out) {
+  return guarded([&] {
+    require_arg(rows >= 1, "rows must be positive");
+    std::mt19937_64 eng(splitmix(seed));
+    for (int64_t i = 0; i < n; ++i)
+      out[i] = static_cast<int64_t>(
+          std::uniform_int_distribution<uint64_t>(0, static_cast<uint64_t>(rows - 1))(eng));
+  });
+}
+
+int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
+  return guarded([&] {
+    // InitSpec::sampled_gaussian(): threshold 2, target 1/(3N), MomentMatched
+    const int d = t->plan.tt_dim;
+    const double thr = 2.0;
+    const double v = 1.0 / (3.0 * static_cast<double>(t->plan.emb_dim));
+    const double root = std::pow(v, 1.0 / (2.0 * d));
+    const double phi = std::exp(-0.5 * thr * thr) / std::sqrt(2.0 * M_PI);
+    const double q = 0.5 * std::erfc(thr / std::sqrt(2.0));
+    const double scale = root / std::sqrt(1.0 + thr * phi / q);
+    for (int k = 0; k < d; ++k) {
+      std::mt19937_64 eng(0);
+      eng.seed(splitmix(splitmix(seed) ^ splitmix(static_cast<uint64_t>(k) ^ 0xD1B54A32D192ED03ull)));
+      std::normal_distribution<double> nd(0.0, 1.0);
+      const int64_t n = t->plan.core_size(k);
+      std::vector<double> vals(n);
+      for (int64_t i = 0; i < n; ++i) {
+        double x = 0;
+        int attempt = 0;
+        for (; attempt < 10000; ++attempt) {
+          x = nd(eng);
+          if (std::abs(x) > thr) break;
+        }
+        if (attempt == 10000) fail(TTGPU_ERR_RUNTIME, "sampled init: no accepted draw");
+        vals[i] = x * scale;
+      }
+      if (t->dtype == TTGPU_F64) {
+        if (ttgpu_set_core(t, k, vals.data())) fail(TTGPU_ERR_RUNTIME, g_last_error);
+      } else {
+        std::vector<float> f(vals.begin(), vals.end());
+        if (ttgpu_set_core(t, k, f.data())) fail(TTGPU_ERR_RUNTIME, g_last_error);
+      }
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,413 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on identical
+inputs.  Mirrors the reference's kernel tests (test_embedding_ops.cpp:44-353,
+acceptance.cpp criteria 2/3) plus the BASELINE configs.
+
+Tolerances (BASELINE.json north_star): forward rel 1e-5, gradients rel 1e-4
+(scaled_max_err, oracle_helpers.hpp:43-53).  With exact forward (the default)
+forward_bags and lookup_row are additionally required to be BIT-identical to
+the oracle, which is itself bit-identical to the reference.
+"""
+import numpy as np
+import pytest
+
+import paper_2101_11714_b200 as tt
+from helpers import CFG2, CFG3, cfg1, scaled_max_err, small_cases
+from pyoracle import Oracle, Plan, RefImpl, ref_available
+
+pytestmark = pytest.mark.gpu
+
+FWD_TOL = 1e-5
+GRAD_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def as_oplan(p: tt.ShapePlan) -> Plan:
+    return Plan(p.num_rows, p.emb_dim, p.row_factors, p.col_factors, p.ranks)
+
+
+def to_tt(p: Plan) -> tt.ShapePlan:
+    return tt.ShapePlan(p.num_rows, p.emb_dim, p.tt_dim, list(p.row_factors), list(p.col_factors),
+                        list(p.ranks))
+
+
+def make_table(plan, dtype, seed, name="t", scale=1.0):
+    t = tt.TtTable(plan, name, dtype)
+    rng = np.random.default_rng(seed)
+    cores = [(rng.standard_normal(plan.core_size(k)) * scale).astype(dtype)
+             for k in range(plan.tt_dim)]
+    t.set_cores(cores)
+    return t, cores
+
+
+def random_batch(rng, rows, bags, lo, hi, weighted, pooling):
+    sizes = rng.integers(lo, hi + 1, bags)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    idx = rng.integers(0, rows, int(off[-1])).astype(np.int64)
+    w = rng.uniform(-2, 2, len(idx)) if weighted else None
+    return tt.IndexBatch(idx, off, w, pooling)
+
+
+def small_plan(rng):
+    d = int(rng.integers(2, 5))
+    rank = int(rng.integers(1, 9))
+    rows = int(rng.integers(10, 300))
+    return tt.plan_shapes(rows, 16, d, rank, None, [2, 2, 2, 2] if d == 4 else None), rows
+
+
+# ------------------------------------------------------------ goldens ----
+def test_golden_small_cases():
+    """Reference-generated cases: forward bit-exact, grads within tolerance,
+    sgd_step with the reference's gradients bit-exact."""
+    for c in small_cases():
+        p = to_tt(c["plan"])
+        t = tt.TtTable(p, "golden", c["dtype"])
+        t.set_cores(c["cores"])
+        b = tt.IndexBatch(c["idx"], c["off"], c["w"], tt.Pooling(c["pooling"]))
+        res = tt.forward_bags(t, b)
+        assert np.array_equal(res.output, c["fwd"])
+        g = tt.backward_bags(t, b, res.context, c["grad_out"])
+        tol = 1e-12 if c["dtype"] == np.float64 else GRAD_TOL
+        for k in range(p.tt_dim):
+            assert scaled_max_err(g.cores[k], c["grads"][k]) <= tol
+        tt.sgd_step(t, tt.CoreGradients(c["grads"]), 0.05)
+        for k in range(p.tt_dim):
+            assert np.array_equal(t.core(k), c["after"][k])
+
+
+def test_golden_cfg1():
+    """BASELINE configs[0] (1M rows, R=16, 4096 uniform) from the reference."""
+    plan, z = cfg1()
+    p = to_tt(plan)
+    t = tt.TtTable(p, "cfg1")
+    t.set_cores([z[f"core{k}"] for k in range(3)])
+    b = tt.IndexBatch(z["idx"], z["off"])
+    res = tt.forward_bags(t, b, save_intermediates=True)
+    assert np.array_equal(res.output, z["fwd"])
+    g = tt.backward_bags(t, b, res.context, z["grad_out"])
+    for k in range(3):
+        assert scaled_max_err(g.cores[k], z[f"grad{k}"]) <= GRAD_TOL
+    for r, want in zip(z["rows"], z["lookup"]):
+        assert np.array_equal(tt.lookup_row(t, int(r)), want)
+
+
+# ------------------------------------------- test_embedding_ops.cpp ports --
+def test_lookup_row_matches_oracle_and_bounds(orc):
+    rng = np.random.default_rng(101)
+    for trial in range(10):
+        p, rows = small_plan(rng)
+        for dt in (np.float32, np.float64):
+            t, cores = make_table(p, dt, 500 + trial, "lk")
+            for r in rng.integers(0, rows, 20):
+                assert np.array_equal(tt.lookup_row(t, int(r)),
+                                      orc.lookup_row(as_oplan(p), cores, int(r)))
+    t = tt.TtTable(tt.plan_shapes(50, 16, 3, 2), "bounds")
+    with pytest.raises(tt.OutOfRange, match="bounds"):
+        tt.lookup_row(t, 50)
+    with pytest.raises(tt.OutOfRange):
+        tt.lookup_row(t, -1)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_forward_random_plans(orc, exact):
+    rng = np.random.default_rng(202)
+    for trial in range(30):
+        p, rows = small_plan(rng)
+        pooling = tt.Pooling.Mean if trial % 3 == 0 else tt.Pooling.Sum
+        b = random_batch(rng, rows, int(rng.integers(1, 24)), 0, 8, trial % 2 == 1, pooling)
+        for dt in (np.float32, np.float64):
+            t, cores = make_table(p, dt, 900 + trial, "fw")
+            t.set_exact_forward(exact)
+            got = tt.forward_bags(t, b, int(rng.integers(1, 64))).output
+            want = orc.forward(as_oplan(p), cores, b.indices, b.offsets, b.weights, int(pooling))
+            if exact:
+                assert np.array_equal(got, want)
+            else:
+                tol = 1e-12 if dt == np.float64 else FWD_TOL
+                assert scaled_max_err(got, want) <= tol
+
+
+def test_forward_independent_of_micro_batch():
+    rng = np.random.default_rng(303)
+    p = tt.plan_shapes(500, 16, 3, 8)
+    t, _ = make_table(p, np.float32, 3)
+    b = random_batch(rng, 500, 64, 0, 12, True, tt.Pooling.Mean)
+    base = tt.forward_bags(t, b, tt.kDefaultMicroBatch).output
+    for mb in (1, 2, 3, 7, 61, 4096):
+        assert np.array_equal(base, tt.forward_bags(t, b, mb).output)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_backward_random_plans(orc, dtype):
+    rng = np.random.default_rng(404)
+    for trial in range(24):
+        p, rows = small_plan(rng)
+        pooling = tt.Pooling.Mean if trial % 2 else tt.Pooling.Sum
+        t, cores = make_table(p, dtype, 40 + trial)
+        b = random_batch(rng, rows, 16, 0, 6, trial % 3 == 0, pooling)
+        g = rng.standard_normal((b.num_bags(), 16)).astype(dtype)
+        res = tt.forward_bags(t, b, 7, trial % 2 == 0)
+        got = tt.backward_bags(t, b, res.context, g)
+        want = orc.backward(as_oplan(p), cores, b.indices, b.offsets, g, b.weights, int(pooling))
+        tol = 1e-11 if dtype == np.float64 else GRAD_TOL
+        for k in range(p.tt_dim):
+            assert scaled_max_err(got.cores[k], want[k]) <= tol, (trial, k)
+
+
+def test_saved_and_recomputed_backward_bitwise():
+    rng = np.random.default_rng(404)
+    for trial in range(6):
+        p, rows = small_plan(rng)
+        t, _ = make_table(p, np.float32, 40 + trial)
+        b = random_batch(rng, rows, 16, 0, 6, trial % 2 == 0, tt.Pooling.Sum)
+        g = rng.standard_normal((b.num_bags(), 16)).astype(np.float32)
+        saved = tt.forward_bags(t, b, 7, True)
+        recomputed = tt.forward_bags(t, b, 7, False)
+        assert np.array_equal(saved.output, recomputed.output)
+        gs = tt.backward_bags(t, b, saved.context, g)
+        gr = tt.backward_bags(t, b, recomputed.context, g)
+        for k in range(p.tt_dim):
+            assert np.array_equal(gs.cores[k], gr.cores[k])
+
+
+def test_backward_deterministic():
+    rng = np.random.default_rng(7)
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t, _ = make_table(p, np.float32, 1, scale=0.2)
+    b = tt.generate_zipfian_batch(p.num_rows, 1.05, 11, 8192, 1)
+    g = rng.standard_normal((8192, 16)).astype(np.float32)
+    r1 = tt.forward_bags(t, b)
+    a = tt.backward_bags(t, b, r1.context, g)
+    r2 = tt.forward_bags(t, b)
+    c = tt.backward_bags(t, b, r2.context, g)
+    assert np.array_equal(r1.output, r2.output)
+    for k in range(3):
+        assert np.array_equal(a.cores[k], c.cores[k])
+
+
+def test_backward_finite_differences():
+    # test_embedding_ops.cpp:169-205 in f64 on the GPU
+    rng = np.random.default_rng(606)
+    for trial in range(8):
+        d = int(rng.integers(2, 5))
+        cols = [2, 2, 2, 1] if d == 4 else None
+        p = tt.plan_shapes(int(rng.integers(8, 60)), 8, d, int(rng.integers(1, 5)), None, cols)
+        t, cores = make_table(p, np.float64, 60 + trial)
+        pooling = tt.Pooling.Sum if trial % 2 == 0 else tt.Pooling.Mean
+        b = random_batch(rng, p.num_rows, 6, 0, 4, trial % 3 == 0, pooling)
+        g = rng.standard_normal((b.num_bags(), p.emb_dim))
+        res = tt.forward_bags(t, b, 5, trial % 2 == 0)
+        grads = tt.backward_bags(t, b, res.context, g)
+
+        def loss(cs):
+            t.set_cores(cs)
+            return float((tt.forward_bags(t, b).output * g).sum())
+
+        h = 1e-6
+        for _ in range(12):
+            k = int(rng.integers(0, d))
+            i = int(rng.integers(0, cores[k].size))
+            up = [c.copy() for c in cores]
+            dn = [c.copy() for c in cores]
+            up[k][i] += h
+            dn[k][i] -= h
+            fd = (loss(up) - loss(dn)) / (2 * h)
+            an = grads.cores[k][i]
+            assert abs(fd - an) <= 1e-6 * max(1.0, abs(fd), abs(an))
+        t.set_cores(cores)
+
+
+def test_gradients_linear_in_upstream():
+    rng = np.random.default_rng(707)
+    p = tt.plan_shapes(80, 16, 3, 4)
+    t, _ = make_table(p, np.float64, 12)
+    b = random_batch(rng, 80, 10, 1, 4, False, tt.Pooling.Sum)
+    g1 = rng.standard_normal((10, 16))
+    g2 = rng.standard_normal((10, 16))
+    ctx = tt.forward_bags(t, b).context
+    b1 = tt.backward_bags(t, b, ctx, g1)
+    b2 = tt.backward_bags(t, b, ctx, g2)
+    bs = tt.backward_bags(t, b, ctx, g1 + g2)
+    for k in range(3):
+        assert scaled_max_err(b1.cores[k] + b2.cores[k], bs.cores[k]) <= 1e-12
+
+
+def test_one_param_per_core_exact_sgd_and_stale():
+    p = tt.plan_shapes(1, 1, 2, 1, [1, 1], [1, 1])
+    t = tt.TtTable(p, "one", np.float64)
+    t.set_core(0, [3.0])
+    t.set_core(1, [5.0])
+    b = tt.IndexBatch.singles([0])
+    fwd = tt.forward_bags(t, b)
+    assert fwd.output[0, 0] == 15.0
+    g = tt.backward_bags(t, b, fwd.context, [1.0])
+    assert g.cores[0][0] == 5.0 and g.cores[1][0] == 3.0
+    tt.sgd_step(t, g, 0.1)
+    assert t.core(0)[0] == pytest.approx(2.5) and t.core(1)[0] == pytest.approx(4.7)
+    with pytest.raises(tt.InvalidArgument, match="stale"):
+        tt.backward_bags(t, b, fwd.context, [1.0])
+
+
+def test_empty_bags_and_batches(orc):
+    p = tt.plan_shapes(40, 16, 3, 2)
+    t, cores = make_table(p, np.float32, 9)
+    empty = tt.IndexBatch(pooling=tt.Pooling.Mean)
+    r = tt.forward_bags(t, empty)
+    assert r.output.shape == (0, 16)
+    g = tt.backward_bags(t, empty, r.context, np.zeros(0, np.float32))
+    assert g.total_elements() == p.parameter_count()
+    assert all(np.all(c == 0) for c in g.cores)
+    mixed = tt.IndexBatch([1, 2, 3], [0, 2, 2, 3], None, tt.Pooling.Mean)
+    out = tt.forward_bags(t, mixed).output
+    assert np.all(out[1] == 0)
+    assert np.array_equal(out, orc.forward(as_oplan(p), cores, [1, 2, 3], [0, 2, 2, 3], None, 1))
+    # all bags empty, lookups zero
+    allempty = tt.IndexBatch(np.zeros(0, np.int64), [0, 0, 0], None, tt.Pooling.Mean)
+    r = tt.forward_bags(t, allempty)
+    assert np.all(r.output == 0)
+    g = tt.backward_bags(t, allempty, r.context, np.ones((2, 16), np.float32))
+    assert all(np.all(c == 0) for c in g.cores)
+
+
+def test_invalid_inputs_rejected():
+    p = tt.plan_shapes(40, 16, 3, 2)
+    a, _ = make_table(p, np.float32, 1, "alpha")
+    bt, _ = make_table(p, np.float32, 2, "beta")
+    batch = tt.IndexBatch.singles([0, 1, 2])
+    fwd = tt.forward_bags(a, batch)
+    grad = np.ones((3, 16), np.float32)
+    with pytest.raises(tt.InvalidArgument):
+        tt.backward_bags(bt, batch, fwd.context, grad)
+    with pytest.raises(tt.InvalidArgument):
+        tt.backward_bags(a, tt.IndexBatch.singles([0, 1]), fwd.context, grad)
+    with pytest.raises(tt.InvalidArgument):
+        tt.backward_bags(a, batch, fwd.context, np.ones(3, np.float32))
+    with pytest.raises(tt.InvalidArgument):
+        tt.forward_bags(a, batch, 0)
+    with pytest.raises(tt.OutOfRange, match="alpha"):
+        tt.forward_bags(a, tt.IndexBatch.singles([40]))
+    with pytest.raises(tt.OutOfRange, match="alpha"):
+        tt.forward_bags(a, tt.IndexBatch.singles([0, 5, -3]))
+    with pytest.raises(tt.InvalidArgument):
+        tt.forward_bags(a, tt.IndexBatch([0, 1], [0, 2, 1]))
+    # the table keeps working after a rejected batch
+    assert np.array_equal(tt.forward_bags(a, batch).output, fwd.output)
+
+
+def test_row_counter():
+    p = tt.plan_shapes(300, 16, 3, 8)
+    t, _ = make_table(p, np.float32, 21)
+    rng = np.random.default_rng(909)
+    b = random_batch(rng, 300, 128, 2, 6, False, tt.Pooling.Sum)
+    tt.EmbeddingStats.reset()
+    fwd = tt.forward_bags(t, b, 32)
+    assert tt.EmbeddingStats.tt_rows_computed() == b.num_lookups()
+    tt.backward_bags(t, b, fwd.context, np.ones((128, 16), np.float32))
+    assert tt.EmbeddingStats.tt_rows_computed() == b.num_lookups()
+    tt.lookup_row(t, 5)
+    assert tt.EmbeddingStats.tt_rows_computed() == b.num_lookups() + 1
+    assert tt.EmbeddingStats.peak_workspace_bytes() > 0
+
+
+# ----------------------------------------------------- BASELINE configs --
+def test_cfg2_full_batch(orc):
+    """configs[1]: 10,131,227 x 16, R=32, 65,536 x 1 Zipf(1.05), fwd+bwd+SGD."""
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t = tt.TtTable(p, "cfg2")
+    t.init_sampled_gaussian(1)
+    cores = t.cores()
+    b = tt.generate_zipfian_batch(p.num_rows, 1.05, 7, 65536, 1)
+    rng = np.random.default_rng(2)
+    g = rng.standard_normal((65536, 16)).astype(np.float32)
+    res = tt.forward_bags(t, b, save_intermediates=True)
+    op = as_oplan(p)
+    assert np.array_equal(res.output, orc.forward(op, cores, b.indices, b.offsets))
+    grads = tt.backward_bags(t, b, res.context, g)
+    want = orc.backward(op, cores, b.indices, b.offsets, g)
+    for k in range(3):
+        assert scaled_max_err(grads.cores[k], want[k]) <= GRAD_TOL
+    tt.sgd_step(t, grads, 0.01)
+    orc.sgd(op, cores, grads.cores, 0.01)
+    for k in range(3):
+        assert np.array_equal(t.core(k), cores[k])
+
+
+@pytest.mark.parametrize("exponent", [0.0, 1.05, 1.2])
+def test_fused_device_step_matches_oracle(orc, exponent):
+    """The bench path: device API, fused backward+SGD, vs oracle fwd+bwd+sgd."""
+    import torch
+
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t = tt.TtTable(p, "cfg2dev")
+    t.init_sampled_gaussian(1)
+    cores = t.cores()
+    b = tt.generate_zipfian_batch(p.num_rows, exponent, 5, 16384, 1)
+    g = np.random.default_rng(3).standard_normal((16384, 16)).astype(np.float32)
+    dev = torch.device("cuda:0")
+    idx = torch.from_numpy(b.indices).to(dev)
+    off = torch.from_numpy(b.offsets).to(dev)
+    gd = torch.from_numpy(g).to(dev)
+    out = torch.empty((16384, 16), dtype=torch.float32, device=dev)
+    ctx = tt.ForwardContext(t)
+    t.set_exact_forward(False)
+    t.forward_device(ctx, idx.data_ptr(), 16384, off.data_ptr(), 16384, out.data_ptr())
+    t.backward_sgd_device(ctx, gd.data_ptr(), 0.01)
+    t.check()
+    op = as_oplan(p)
+    want_out = orc.forward(op, cores, b.indices, b.offsets)
+    assert scaled_max_err(out.cpu().numpy(), want_out) <= FWD_TOL
+    want_g = orc.backward(op, cores, b.indices, b.offsets, g)
+    orc.sgd(op, cores, want_g, 0.01)
+    for k in range(3):
+        # updated cores: the gradient tolerance scaled by lr
+        assert scaled_max_err(t.core(k), cores[k]) <= GRAD_TOL * 0.01 + 1e-7
+
+
+def test_cfg3_subsample(orc):
+    """configs[2] shape (40M rows, dim 64 = 4x4x4, R=64, P=32) on 256 bags."""
+    p = tt.plan_shapes(40000000, 64, 3, 64, [200, 200, 1000], [4, 4, 4])
+    t, cores = make_table(p, np.float32, 5, "cfg3", scale=0.1)
+    rng = np.random.default_rng(8)
+    idx = rng.integers(0, p.num_rows, 256 * 32).astype(np.int64)
+    off = np.arange(0, 256 * 32 + 1, 32, dtype=np.int64)
+    b = tt.IndexBatch(idx, off)
+    g = rng.standard_normal((256, 64)).astype(np.float32)
+    res = tt.forward_bags(t, b)
+    op = as_oplan(p)
+    assert np.array_equal(res.output, orc.forward(op, cores, idx, off))
+    grads = tt.backward_bags(t, b, res.context, g)
+    want = orc.backward(op, cores, idx, off, g)
+    for k in range(3):
+        assert scaled_max_err(grads.cores[k], want[k]) <= GRAD_TOL
+
+
+def test_skewed_segments_large_runs(orc):
+    """Every lookup on one row (a single huge pair / i2 segment) and a mix."""
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t, cores = make_table(p, np.float32, 6, scale=0.2)
+    rng = np.random.default_rng(4)
+    for idx in (np.zeros(20000, np.int64), np.full(5000, 10131226, np.int64),
+                np.concatenate([np.zeros(7000, np.int64), rng.integers(0, 300, 3000)])):
+        off = np.arange(len(idx) + 1, dtype=np.int64)
+        g = rng.standard_normal((len(idx), 16)).astype(np.float32)
+        b = tt.IndexBatch(idx, off)
+        res = tt.forward_bags(t, b)
+        grads = tt.backward_bags(t, b, res.context, g)
+        want = orc.backward(as_oplan(p), cores, idx, off, g)
+        for k in range(3):
+            assert scaled_max_err(grads.cores[k], want[k]) <= GRAD_TOL
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_init_matches_reference_initializer():
+    ref = RefImpl()
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t = tt.TtTable(p, "init")
+    t.init_sampled_gaussian(1)
+    r = ref.table(as_oplan(p), np.float32, "init")
+    r.init_sampled_gaussian(1)
+    for a, b in zip(t.cores(), r.get_cores()):
+        assert np.array_equal(a, b)
