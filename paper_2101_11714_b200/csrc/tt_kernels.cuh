@@ -381,7 +381,7 @@ __device__ __forceinline__ const T* fwd_partial(const DevPlan& P, const T* __res
                                                 const T* __restrict__ H, const int32_t* lk_pid,
                                                 const uint32_t* __restrict__ tail_dig, int64_t L,
                                                 int64_t l, int kk, const T* __restrict__ saved,
-                                                T* ping, T* pong, int lane) {
+                                                T* ping, T* pong, int lane, bool exact) {
   const T* src = H + static_cast<int64_t>(lk_pid[l]) * P.W1;
   if (kk <= 1) return src;
   if (saved) return saved + (static_cast<int64_t>(kk - 2) * L + l) * P.maxw;
@@ -389,7 +389,11 @@ __device__ __forceinline__ const T* fwd_partial(const DevPlan& P, const T* __res
   for (int k = 2; k <= kk; ++k) {
     const int i_k = static_cast<int>(tail_dig[(k - 2) * L + l]);
     const T* G = cores + P.coff[k] + static_cast<int64_t>(i_k) * P.slice[k];
-    warp_mm<T, false>(src, G, dst, P.prefix[k - 1], P.r[k], P.n[k] * P.r[k + 1], lane);
+    // same rounding as the forward that produced (or would have saved) it
+    if (exact)
+      warp_mm<T, true>(src, G, dst, P.prefix[k - 1], P.r[k], P.n[k] * P.r[k + 1], lane);
+    else
+      warp_mm<T, false>(src, G, dst, P.prefix[k - 1], P.r[k], P.n[k] * P.r[k + 1], lane);
     __syncwarp();
     src = dst;
     dst = (dst == ping) ? pong : ping;
@@ -412,7 +416,7 @@ __global__ void k_chunk_reduce(DevPlan P, const T* __restrict__ cores, const T* 
                                const T* __restrict__ lk_alpha, const T* __restrict__ grad,
                                const uint32_t* __restrict__ s_key, const uint32_t* __restrict__ s_lk,
                                const unsigned long long* __restrict__ scan, int64_t L, int C,
-                               int kcore, int Wc, T* __restrict__ partials) {
+                               int kcore, int Wc, T* __restrict__ partials, bool exact) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* acc = reinterpret_cast<T*>(smem_raw);                  // Wc
@@ -440,7 +444,7 @@ __global__ void k_chunk_reduce(DevPlan P, const T* __restrict__ cores, const T* 
           const T* D = bwd_chain<T>(P, cores, tail_dig, L, l, grow, alpha, kcore, my,
                                     my + P.maxw, lane);
           const T* u = fwd_partial<T>(P, cores, H, lk_pid, tail_dig, L, l, kcore - 1, saved,
-                                      my + 2 * P.maxw, my + 3 * P.maxw, lane);
+                                      my + 2 * P.maxw, my + 3 * P.maxw, lane, exact);
           const int pk = P.prefix[kcore - 1], rk = P.r[kcore], wk = P.n[kcore] * P.r[kcore + 1];
           for (int e = lane; e < rk * wk; e += 32) {
             const int q = e / wk, j = e - q * wk;

@@ -171,6 +171,7 @@ struct ttgpu_ctx {
   int pooling = 0;
   bool save = false;
   bool has_w = false;
+  bool exact = true;  // rounding mode of the forward that filled this context
   // host-API staging
   DevBuf h_idx, h_off, h_w, h_out, h_grad;
   // forward state
@@ -271,6 +272,7 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
   c->B = B;
   c->pooling = pooling;
   c->save = save && d >= 4;
+  c->exact = exact;
   c->has_w = w != nullptr;
   c->w_dev = w;
   c->valid = true;
@@ -446,7 +448,7 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
         P, cores, c->H.as<T>(), nullptr, c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
         c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad, c->s_key.as<uint32_t>(),
         c->s_lk.as<uint32_t>(), c->pair_scan.as<unsigned long long>(), L, kTailChunk, 1, Wc,
-        c->partS.as<T>());
+        c->partS.as<T>(), c->exact);
     k_combine<T, 0><<<grid_for(ucap, 1, t->num_sms, 8), 128, 0, st>>>(
         c->partS.as<T>(), c->pair_scan.as<unsigned long long>(), c->pair_start.as<int32_t>(),
         c->counts.as<int>(), 0, Wc, c->S.as<T>(), T(0));
@@ -468,7 +470,8 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
         P, cores, c->H.as<T>(), c->save ? c->saved.as<T>() : nullptr, c->lk_pid.as<int32_t>(),
         c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad,
         c->s_dkey.as<uint32_t>() + j * L, c->s_dlk.as<uint32_t>() + j * L,
-        c->dscan.as<unsigned long long>() + j * L, L, kTailChunk, k, Wc, c->partK.as<T>());
+        c->dscan.as<unsigned long long>() + j * L, L, kTailChunk, k, Wc, c->partK.as<T>(),
+        c->exact);
     T* dst = fuse_tail ? cores + P.coff[k] : grads + P.coff[k];
     if (fuse_tail)
       k_combine<T, 1><<<grid_for(P.m[k], 1, t->num_sms, 8), 128, 0, st>>>(
