@@ -8,7 +8,7 @@ LIB      := $(PKG)/lib/libttgpu.so
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -shared -Xptxas -v
 SRCS     := $(CSRC)/ttgpu.cu $(CSRC)/shape_plan.cpp
-HDRS     := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) include/ttgpu.h
+HDRS     := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/*.inl) include/ttgpu.h
 
 .PHONY: all lib oracle clean
 all: lib oracle

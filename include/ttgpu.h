@@ -81,6 +81,11 @@ int ttgpu_mark_mutated(ttgpu_table* t);                        /* tt_table.hpp:8
  * reference's loop order -> forward_bags / lookup_row bit-identical to the
  * reference (gemm.hpp:15-31, embedding_ops.hpp:232-249).  off: FFMA. */
 int ttgpu_set_exact_forward(ttgpu_table* t, int on);
+/* 3-core float tables with a compiled shape use the specialised fast path
+ * (kind >= 0); on=1 forces the generic pipeline instead (used by tests to
+ * cross-check the two implementations). */
+int ttgpu_set_generic_path(ttgpu_table* t, int on);
+int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind);
 int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out); /* tt_table.hpp:84 */
 
 /* ---- forward_bags (embedding_ops.hpp:159-253) ---------------------------- */

@@ -1,0 +1,195 @@
+// Host launch code for the 3-core fast path (fast3.cuh).  Included by ttgpu.cu
+// after the table/context definitions.
+namespace ttgpu {
+
+struct F3Bufs {
+  DevBuf key, d0, d2, hist, perm, tiles, tile_base, ntiles, Hbuf, y, slotpos, tile_i0, tile_nslots,
+      part1, part2, mask2, D0, tab0;
+  f3::Geo geo{};
+  int max_tiles = 0;
+  int kind = -1;  // instantiation index
+};
+
+void f3_free(F3Bufs* f) { delete f; }
+
+namespace {
+
+constexpr int kF3TL = 2048;  // lookups per histogram / scatter CTA
+
+f3::Geo make_geo(const ttgpu_table* t) {
+  f3::Geo g{};
+  const DevPlan& P = t->dp;
+  g.m0 = P.m[0];
+  g.m1 = P.m[1];
+  g.m2 = P.m[2];
+  g.m12 = static_cast<uint32_t>(P.m[1]) * static_cast<uint32_t>(P.m[2]);
+  g.blk = std::min(64, P.m[2]);
+  g.nblk = (P.m[2] + g.blk - 1) / g.blk;
+  g.K = g.nblk * P.m[1];
+  g.num_rows = P.num_rows;
+  g.coff0 = P.coff[0];
+  g.coff1 = P.coff[1];
+  g.coff2 = P.coff[2];
+  return g;
+}
+
+template <class D>
+struct F3Runner {
+  static size_t fwd_smem(const f3::Geo& g) { return f3::FwdSmem<D>::bytes(g.m0); }
+  static size_t bwd_smem(const f3::Geo& g) { return f3::BwdSmem<D>::bytes(g.m0, g.blk); }
+
+  static void forward(ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L, const int64_t* off,
+                      int64_t B, const double* w, int pooling, float* out, bool exact,
+                      int32_t* lk_bag, float* alpha) {
+    cudaStream_t st = t->stream;
+    f3::Geo& g = f.geo;
+    g = make_geo(t);
+    const int NT = static_cast<int>((L + kF3TL - 1) / kF3TL);
+    f.max_tiles = static_cast<int>((L + D::TT - 1) / D::TT) + g.K;
+    f.key.ensure(4 * L);
+    f.d0.ensure(2 * L);
+    f.d2.ensure(2 * L);
+    f.hist.ensure(4 * static_cast<size_t>(g.K) * NT);
+    f.perm.ensure(4 * L);
+    f.tiles.ensure(sizeof(f3::Tile) * f.max_tiles);
+    f.tile_base.ensure(4 * (g.K + 1));
+    f.ntiles.ensure(16);
+    f.Hbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
+    f.y.ensure(4 * static_cast<size_t>(L) * D::N);
+    f.slotpos.ensure(2 * L);
+    f.tile_i0.ensure(2 * L);
+    f.tile_nslots.ensure(4 * f.max_tiles);
+    const int gb = std::max(NT, grid_for(B, 512, t->num_sms, 4));
+    t->mark("fwd_begin");
+    f3::f3_hist<float><<<gb, 512, 4 * g.K, st>>>(
+        g, idx, L, kF3TL, NT, off, B, w, pooling, f.key.as<uint32_t>(), f.d0.as<uint16_t>(),
+        f.d2.as<uint16_t>(), lk_bag, alpha, f.hist.as<uint32_t>(), t->d_bad(), t->d_struct());
+    t->mark("hist");
+    f3::f3_scan<<<1, 1024, 0, st>>>(g, NT, D::TT, L, f.hist.as<uint32_t>(), f.tile_base.as<int32_t>(),
+                                    f.tiles.as<f3::Tile>(), f.ntiles.as<int>());
+    t->mark("scan");
+    {
+      const size_t sm = 4 * 8 * static_cast<size_t>(g.K);
+      set_smem(f3::f3_scatter, sm);
+      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.key.as<uint32_t>(), L, kF3TL, NT,
+                                          f.hist.as<uint32_t>(), f.perm.as<uint32_t>());
+    }
+    t->mark("scatter");
+    {
+      const size_t sm = fwd_smem(g);
+      auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
+      set_smem(kern, sm);
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::kThreads, sm);
+      const int grid = std::max(1, std::min(f.max_tiles, t->num_sms * std::max(occ, 1)));
+      kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles.as<f3::Tile>(),
+                                           f.ntiles.as<int>(), f.perm.as<uint32_t>(),
+                                           f.d0.as<uint16_t>(), f.d2.as<uint16_t>(),
+                                           f.Hbuf.as<float>(), f.y.as<float>(),
+                                           f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
+                                           f.tile_nslots.as<int>());
+    }
+    t->mark("f3_fwd");
+    {
+      auto kern = exact ? f3::f3_pool<D::N, true> : f3::f3_pool<D::N, false>;
+      kern<<<grid_for(B * (D::N / 4), 256, t->num_sms, 8), 256, 0, st>>>(
+          off, B, L, w, pooling, f.y.as<float>(), out);
+    }
+    t->mark("pool");
+    CK(cudaGetLastError());
+  }
+
+  static void backward(ttgpu_table* t, F3Bufs& f, const float* grad, int mode, float lr,
+                       const int32_t* lk_bag, const float* alpha, int64_t L) {
+    cudaStream_t st = t->stream;
+    const f3::Geo& g = f.geo;
+    f.part1.ensure(4 * static_cast<size_t>(f.max_tiles) * D::S1);
+    f.part2.ensure(4 * static_cast<size_t>(f.max_tiles) * g.blk * D::S2);
+    f.mask2.ensure(8 * static_cast<size_t>(f.max_tiles));
+    f.D0.ensure(4 * static_cast<size_t>(L) * D::S0);
+    f.tab0.ensure(4 * static_cast<size_t>(g.m0) * f.max_tiles);
+    t->mark("bwd_begin");
+    {
+      const size_t sm = bwd_smem(g);
+      auto kern = f3::f3_bwd<D>;
+      set_smem(kern, sm);
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::kThreads, sm);
+      const int grid = std::max(1, std::min(f.max_tiles, t->num_sms * std::max(occ, 1)));
+      kern<<<grid, f3::kThreads, sm, st>>>(
+          g, t->cores.as<float>(), f.tiles.as<f3::Tile>(), f.ntiles.as<int>(),
+          f.perm.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad, f.Hbuf.as<float>(),
+          f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(),
+          f.part1.as<float>(), f.part2.as<float>(), f.mask2.as<unsigned long long>(),
+          f.D0.as<float>(), f.tab0.as<int>(), f.max_tiles);
+    }
+    t->mark("f3_bwd");
+    {
+      const size_t sm = 4 * (static_cast<size_t>(f.max_tiles) + 8) + 4 * 2 * f3::kThreads;
+      auto kern = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
+      set_smem(kern, sm);
+      kern<<<g.m0 + g.m1 + g.m2, f3::kThreads, sm, st>>>(
+          g, t->cores.as<float>(), t->grads.as<float>(), f.tiles.as<f3::Tile>(), f.ntiles.as<int>(),
+          f.tile_base.as<int32_t>(), f.part1.as<float>(), f.part2.as<float>(),
+          f.mask2.as<unsigned long long>(), f.D0.as<float>(), f.tab0.as<int>(), f.max_tiles, lr);
+    }
+    t->mark("f3_combine");
+    CK(cudaGetLastError());
+  }
+};
+
+// instantiation table: (P0, R1, N1, R2, N2, TT)
+using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 128>;
+using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 128>;
+using F3_R32 = f3::Dims<2, 32, 2, 32, 4, 64>;
+using F3_R64 = f3::Dims<2, 64, 2, 64, 4, 64>;
+
+template <class D>
+bool dims_match(const DevPlan& P) {
+  return P.n[0] == D::P0 && P.r[1] == D::R1 && P.n[1] == D::N1 && P.r[2] == D::R2 &&
+         P.n[2] == D::N2 && P.r[3] == 1;
+}
+
+// Which fast-path instantiation serves this table (-1: generic path).
+int f3_kind(const ttgpu_table* t) {
+  const DevPlan& P = t->dp;
+  if (t->dtype != TTGPU_F32 || P.d != 3) return -1;
+  if (P.m[0] >= 65536 || P.m[1] >= 65536 || P.m[2] >= 65536) return -1;
+  if (P.num_rows >= (1ll << 32) || static_cast<int64_t>(P.m[0]) * P.m[1] * P.m[2] >= (1ll << 32))
+    return -1;
+  const int blk = std::min(64, P.m[2]);
+  const int64_t K = static_cast<int64_t>((P.m[2] + blk - 1) / blk) * P.m[1];
+  if (K > 6144 || P.m[0] > 8192) return -1;
+  if (dims_match<F3_R8>(P)) return 0;
+  if (dims_match<F3_R16>(P)) return 1;
+  if (dims_match<F3_R32>(P)) return 2;
+  if (dims_match<F3_R64>(P)) return 3;
+  return -1;
+}
+
+void f3_forward(int kind, ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L,
+                const int64_t* off, int64_t B, const double* w, int pooling, float* out, bool exact,
+                int32_t* lk_bag, float* alpha) {
+  f.kind = kind;
+  switch (kind) {
+    case 0: F3Runner<F3_R8>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
+    case 1: F3Runner<F3_R16>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
+    case 2: F3Runner<F3_R32>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
+    case 3: F3Runner<F3_R64>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
+    default: fail(TTGPU_ERR_RUNTIME, "bad fast-path kind");
+  }
+}
+
+void f3_backward(ttgpu_table* t, F3Bufs& f, const float* grad, int mode, float lr,
+                 const int32_t* lk_bag, const float* alpha, int64_t L) {
+  switch (f.kind) {
+    case 0: F3Runner<F3_R8>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
+    case 1: F3Runner<F3_R16>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
+    case 2: F3Runner<F3_R32>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
+    case 3: F3Runner<F3_R64>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
+    default: fail(TTGPU_ERR_RUNTIME, "bad fast-path kind");
+  }
+}
+
+}  // namespace
+}  // namespace ttgpu

@@ -14,11 +14,13 @@
 #include <random>
 #include <sstream>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/ttgpu.h"
 #include "shape_plan.hpp"
 #include "tt_kernels.cuh"
+#include "fast3.cuh"
 
 namespace ttgpu {
 namespace {
@@ -134,6 +136,7 @@ struct ttgpu_table {
   DevBuf cores, grads, pair_tab, errs, lk_rows, lk_out;
   uint64_t generation = 0;
   bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
+  bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
   // optional phase timing (CUDA events between pipeline phases)
   bool prof = false;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
@@ -163,7 +166,17 @@ struct ttgpu_table {
   int* d_struct() { return reinterpret_cast<int*>(errs.as<unsigned long long>() + 2); }
 };
 
+namespace ttgpu {
+struct F3Bufs;
+void f3_free(F3Bufs*);
+}  // namespace ttgpu
+
 struct ttgpu_ctx {
+  ~ttgpu_ctx() {
+    if (f3) ttgpu::f3_free(f3);
+  }
+  ttgpu::F3Bufs* f3 = nullptr;  // fast-path state (3-core tables)
+  bool fast = false;
   ttgpu_table* table = nullptr;
   uint64_t snapshot = 0;
   bool valid = false;
@@ -259,6 +272,14 @@ T* core_ptr(ttgpu_table* t, int k) {
   return t->cores.as<T>() + t->dp.coff[k];
 }
 
+}  // namespace
+}  // namespace ttgpu
+
+#include "fast3_host.inl"
+
+namespace ttgpu {
+namespace {
+
 // ------------------------------------------------------------- forward ---
 template <typename T>
 void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, const int64_t* off,
@@ -287,6 +308,19 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
         off, B, 0, w, pooling, c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), t->d_struct());
     CK(cudaGetLastError());
     return;
+  }
+  c->fast = false;
+  if constexpr (std::is_same_v<T, float>) {
+    const int kind = f3_kind(t);
+    if (kind >= 0 && !t->force_generic) {
+      if (!c->f3) c->f3 = new F3Bufs;
+      c->lk_bag.ensure(4 * L);
+      c->lk_alpha.ensure(sizeof(T) * L);
+      f3_forward(kind, t, *c->f3, idx, L, off, B, w, pooling, out, exact, c->lk_bag.as<int32_t>(),
+                 c->lk_alpha.as<float>());
+      c->fast = true;
+      return;
+    }
   }
   const int64_t m01 = static_cast<int64_t>(P.m[0]) * P.m[1];
   const int64_t ucap = std::min<int64_t>(L, m01);
@@ -372,6 +406,13 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   const int64_t L = c->L;
   T* cores = t->cores.as<T>();
   T* grads = t->grads.as<T>();
+  if constexpr (std::is_same_v<T, float>) {
+    if (c->fast && L > 0 && c->B > 0) {
+      f3_backward(t, *c->f3, grad, mode, static_cast<float>(lr), c->lk_bag.as<int32_t>(),
+                  c->lk_alpha.as<float>(), L);
+      return;
+    }
+  }
   if (mode == 0) CK(cudaMemsetAsync(grads, 0, sizeof(T) * t->total, st));
   if (L == 0 || c->B == 0) return;
   const int64_t m01 = static_cast<int64_t>(P.m[0]) * P.m[1];
@@ -708,6 +749,14 @@ int ttgpu_grad_device_ptr(ttgpu_table* t, int k, void** p) {
     require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
     *p = static_cast<char*>(t->grads.p) + t->esz * t->dp.coff[k];
   });
+}
+
+int ttgpu_set_generic_path(ttgpu_table* t, int on) {
+  return guarded([&] { t->force_generic = on != 0; });
+}
+
+int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind) {
+  return guarded([&] { *kind = t->force_generic ? -1 : f3_kind(t); });
 }
 
 int ttgpu_set_exact_forward(ttgpu_table* t, int on) {

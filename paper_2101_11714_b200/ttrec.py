@@ -276,6 +276,14 @@ class TtTable:
     def mark_mutated(self):
         _raise(lib().ttgpu_mark_mutated(self.handle))
 
+    def set_generic_path(self, on: bool):
+        _raise(lib().ttgpu_set_generic_path(self.handle, int(bool(on))))
+
+    def fast_path_kind(self) -> int:
+        k = C.c_int()
+        _raise(lib().ttgpu_fast_path_kind(self.handle, C.byref(k)))
+        return k.value
+
     def set_exact_forward(self, on: bool):
         _raise(lib().ttgpu_set_exact_forward(self.handle, int(bool(on))))
 

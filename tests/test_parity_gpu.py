@@ -413,3 +413,54 @@ def test_init_matches_reference_initializer():
     r.init_sampled_gaussian(1)
     for a, b in zip(t.cores(), r.get_cores()):
         assert np.array_equal(a, b)
+
+
+# ------------------------------------------------ specialised 3-core path --
+@pytest.mark.parametrize("rank", [8, 16, 32, 64])
+@pytest.mark.parametrize("exponent", [0.0, 1.2])
+def test_fast_path_vs_oracle_and_generic(orc, rank, exponent):
+    """The compiled-shape fast path (tile counting sort, smem partials) against
+    the oracle and against the generic pipeline on the same inputs; multi-hot,
+    weighted, Mean-pooled bags with empties."""
+    p = tt.plan_shapes(10131227, 16, 3, rank, [200, 220, 250], [2, 2, 4])
+    t, cores = make_table(p, np.float32, rank, "fast", scale=0.3)
+    assert t.fast_path_kind() >= 0
+    rng = np.random.default_rng(rank)
+    base = tt.generate_zipfian_batch(p.num_rows, exponent, 3, 3000, 3)
+    sizes = rng.integers(0, 6, 3000)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    idx = np.resize(base.indices, int(off[-1])).astype(np.int64)
+    w = rng.uniform(-2, 2, len(idx))
+    b = tt.IndexBatch(idx, off, w, tt.Pooling.Mean)
+    g = rng.standard_normal((3000, 16)).astype(np.float32)
+    op = as_oplan(p)
+    res = tt.forward_bags(t, b)
+    assert np.array_equal(res.output, orc.forward(op, cores, idx, off, w, 1))
+    got = tt.backward_bags(t, b, res.context, g)
+    want = orc.backward(op, cores, idx, off, g, w, 1)
+    for k in range(3):
+        assert scaled_max_err(got.cores[k], want[k]) <= GRAD_TOL
+    t.set_generic_path(True)
+    assert t.fast_path_kind() == -1
+    res2 = tt.forward_bags(t, b)
+    assert np.array_equal(res2.output, res.output)
+    got2 = tt.backward_bags(t, b, res2.context, g)
+    for k in range(3):
+        assert scaled_max_err(got.cores[k], got2.cores[k]) <= GRAD_TOL
+
+
+def test_fast_path_fused_sgd_equals_dense_then_sgd():
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    a, cores = make_table(p, np.float32, 9, "a", scale=0.3)
+    b_, _ = make_table(p, np.float32, 9, "b", scale=0.3)
+    batch = tt.generate_zipfian_batch(p.num_rows, 1.05, 9, 20000, 1)
+    g = np.random.default_rng(9).standard_normal((20000, 16)).astype(np.float32)
+    ra = tt.forward_bags(a, batch)
+    grads = tt.backward_bags(a, batch, ra.context, g)
+    tt.sgd_step(a, grads, 0.01)
+    rb = tt.forward_bags(b_, batch)
+    b_.backward_sgd(rb.context, batch, g, 0.01)
+    for k in range(3):
+        assert np.array_equal(a.core(k), b_.core(k))
+    with pytest.raises(tt.InvalidArgument, match="stale"):
+        b_.backward_sgd(rb.context, batch, g, 0.01)
