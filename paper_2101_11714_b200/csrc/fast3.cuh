@@ -52,6 +52,7 @@ struct Dims {
   static constexpr int C1P = C1 + 1;
   static_assert(N2 == 4, "fast path expects n_2 == 4 (float4 rows)");
   static_assert(C1 % 4 == 0, "C1 must be a multiple of 4");
+  static_assert((C1 & (C1 - 1)) == 0, "C1 must be a power of two (rotated D0 reads)");
 };
 
 constexpr int kThreads = 256;
@@ -63,6 +64,38 @@ __device__ __forceinline__ float4 madd4(float a, float4 b, float4 acc) {
   acc.z = madd<float, kExact>(a, b.z, acc.z);
   acc.w = madd<float, kExact>(a, b.w, acc.w);
   return acc;
+}
+
+// ---- TMA bulk copies (cp.async.bulk, sm_90+/sm_100a) with mbarrier completion
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arrive (count 1) and raise the expected transaction bytes of the current phase
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy; bytes % 16 == 0, both addresses 16-byte aligned
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -101,9 +134,10 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total, int* sm /* >= 
 }
 
 // ------------------------------------------------------------- f3_hist ---
-template <typename T>
+// TL = 512 * LPT lookups per CTA (LPT lookups per thread, loads batched).
+template <typename T, int LPT>
 __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict__ idx, int64_t L,
-                                               int TL, int NT, const int64_t* __restrict__ off,
+                                               int NT, const int64_t* __restrict__ off,
                                                int64_t B, const double* __restrict__ w, int mean,
                                                uint32_t* __restrict__ key, uint16_t* __restrict__ d0,
                                                uint16_t* __restrict__ d2, int32_t* __restrict__ lk_bag,
@@ -116,11 +150,19 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
   const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31;
   if (tile < NT) {
-    for (int i = threadIdx.x; i < TL; i += blockDim.x) {  // TL % blockDim == 0: warp-uniform
-      const int64_t l = static_cast<int64_t>(tile) * TL + i;
+    int64_t rows[LPT];
+    const int64_t base = static_cast<int64_t>(tile) * 512 * LPT + threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int64_t l = base + q * 512;
+      rows[q] = l < L ? idx[l] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int64_t l = base + q * 512;
       uint32_t k = 0xffffffffu;
       if (l < L) {
-        int64_t row = idx[l];
+        int64_t row = rows[q];
         if (row < 0 || row >= g.num_rows) {
           atomicMin(bad, static_cast<unsigned long long>(l));
           row = 0;
@@ -141,8 +183,9 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
   }
   __syncthreads();
   if (tile < NT)
-    for (int k = threadIdx.x; k < g.K; k += blockDim.x) hist[static_cast<int64_t>(k) * NT + tile] = shist[k];
-  // bags (grid-stride over all CTAs)
+    for (int k = threadIdx.x; k < g.K; k += blockDim.x)
+      hist[static_cast<int64_t>(k) * NT + tile] = shist[k];
+  // bags (grid-stride over all CTAs): offsets checks, lookup->bag, backward alpha
   for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < B;
        b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = off[b], e = off[b + 1];
@@ -161,42 +204,50 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
 }
 
 // ------------------------------------------------------------- f3_scan ---
-// One CTA of 1024 threads.  hist (K x NT, key-major) becomes exclusive offsets.
+// One CTA of 1024 threads; the (K x NT, key-major) histogram is staged in
+// shared memory with coalesced loads, scanned there, and written back as
+// exclusive offsets.  Also emits the tile list (buckets cut into <= TT).
 __global__ void __launch_bounds__(1024) f3_scan(Geo g, int NT, int TT, int64_t L,
                                                 uint32_t* __restrict__ hist,
                                                 int32_t* __restrict__ tile_base,
                                                 Tile* __restrict__ tiles, int* __restrict__ ntiles) {
   using Scan = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
+  extern __shared__ uint32_t sh[];  // n entries
   const int n = g.K * NT;
+  const int tid = threadIdx.x;
+#pragma unroll 8
+  for (int i = tid; i < n; i += 1024) sh[i] = hist[i];
+  __syncthreads();
   const int per = (n + 1023) / 1024;
-  const int lo = min(n, static_cast<int>(threadIdx.x) * per), hi = min(n, lo + per);
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
   uint32_t s = 0;
-  for (int i = lo; i < hi; ++i) s += hist[i];
+  for (int i = lo; i < hi; ++i) s += sh[i];
   uint32_t ex;
   Scan(tmp).ExclusiveSum(s, ex);
-  __syncthreads();
   for (int i = lo; i < hi; ++i) {
-    const uint32_t c = hist[i];
-    hist[i] = ex;
+    const uint32_t c = sh[i];
+    sh[i] = ex;
     ex += c;
   }
   __syncthreads();
+#pragma unroll 8
+  for (int i = tid; i < n; i += 1024) hist[i] = sh[i];
   // tiles per bucket
   const int perk = (g.K + 1023) / 1024;
-  const int klo = min(g.K, static_cast<int>(threadIdx.x) * perk), khi = min(g.K, klo + perk);
+  const int klo = min(g.K, tid * perk), khi = min(g.K, klo + perk);
   uint32_t nt = 0;
   for (int k = klo; k < khi; ++k) {
-    const uint32_t bs = hist[static_cast<int64_t>(k) * NT];
-    const uint32_t be = k + 1 < g.K ? hist[static_cast<int64_t>(k + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t bs = sh[k * NT];
+    const uint32_t be = k + 1 < g.K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
     nt += (be - bs + TT - 1) / TT;
   }
   uint32_t tex;
   __syncthreads();
   Scan(tmp).ExclusiveSum(nt, tex);
   for (int k = klo; k < khi; ++k) {
-    const uint32_t bs = hist[static_cast<int64_t>(k) * NT];
-    const uint32_t be = k + 1 < g.K ? hist[static_cast<int64_t>(k + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t bs = sh[k * NT];
+    const uint32_t be = k + 1 < g.K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
     tile_base[k] = static_cast<int32_t>(tex);
     for (uint32_t st = bs; st < be; st += TT) {
       Tile t;
@@ -207,14 +258,15 @@ __global__ void __launch_bounds__(1024) f3_scan(Geo g, int NT, int TT, int64_t L
       tiles[tex++] = t;
     }
   }
-  if (threadIdx.x == 1023) {
+  if (tid == 1023) {
     tile_base[g.K] = static_cast<int32_t>(tex);
     *ntiles = static_cast<int>(tex);
   }
 }
 
 // ---------------------------------------------------------- f3_scatter ---
-// Stable scatter: 8 warps per CTA, each owning TL/8 consecutive lookups.
+// Stable scatter: 8 warps per CTA, each owning TL/8 consecutive lookups,
+// keys loaded 8 rounds at a time.
 __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restrict__ key, int64_t L,
                                                   int TL, int NT, const uint32_t* __restrict__ hoff,
                                                   uint32_t* __restrict__ perm) {
@@ -226,16 +278,25 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restr
   uint32_t* my = wc + static_cast<int64_t>(wid) * g.K;
   for (int k = lane; k < g.K; k += 32) my[k] = 0;
   __syncwarp();
-  for (int r = 0; r < per; r += 32) {
-    const int64_t l = base + r + lane;
-    const uint32_t k = l < L ? key[l] : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    if (k != 0xffffffffu && lane == __ffs(peers) - 1) my[k] += __popc(peers);
-    __syncwarp();
+  for (int r0 = 0; r0 < per; r0 += 256) {
+    uint32_t ks[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t l = base + r0 + q * 32 + lane;
+      ks[q] = (r0 + q * 32 < per && l < L) ? key[l] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t k = ks[q];
+      const unsigned peers = __match_any_sync(0xffffffffu, k);
+      if (k != 0xffffffffu && lane == __ffs(peers) - 1) my[k] += __popc(peers);
+      __syncwarp();
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < g.K; k += blockDim.x) {
     uint32_t run = hoff[static_cast<int64_t>(k) * NT + tile];
+#pragma unroll
     for (int w = 0; w < 8; ++w) {
       const uint32_t c = wc[static_cast<int64_t>(w) * g.K + k];
       wc[static_cast<int64_t>(w) * g.K + k] = run;
@@ -244,36 +305,50 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restr
   }
   __syncthreads();
   const unsigned lt = lanemask_lt();
-  for (int r = 0; r < per; r += 32) {
-    const int64_t l = base + r + lane;
-    const uint32_t k = l < L ? key[l] : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    uint32_t pos = 0;
-    if (k != 0xffffffffu) pos = my[k] + __popc(peers & lt);
-    __syncwarp();
-    if (k != 0xffffffffu) {
-      perm[pos] = static_cast<uint32_t>(l);
-      if (lane == __ffs(peers) - 1) my[k] += __popc(peers);
+  for (int r0 = 0; r0 < per; r0 += 256) {
+    uint32_t ks[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t l = base + r0 + q * 32 + lane;
+      ks[q] = (r0 + q * 32 < per && l < L) ? key[l] : 0xffffffffu;
     }
-    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t k = ks[q];
+      const int64_t l = base + r0 + q * 32 + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, k);
+      uint32_t pos = 0;
+      if (k != 0xffffffffu) pos = my[k] + __popc(peers & lt);
+      __syncwarp();
+      if (k != 0xffffffffu) {
+        perm[pos] = static_cast<uint32_t>(l);
+        if (lane == __ffs(peers) - 1) my[k] += __popc(peers);
+      }
+      __syncwarp();
+    }
   }
 }
 
 // --------------------------------------------------------- smem layouts ---
+// Row strides padded by 4 floats keep TMA destinations 16-byte aligned.
 template <class D>
 struct FwdSmem {
-  // floats: G1s[S1] | Hs[TT*W1P] | G0s[TT*S0P] | G2s[TT*S2P] ; ints after
+  // floats: G1s[S1] | Hs[TT*W1P] | G0s[TT*S0P] | G2s[TT*S2P] ; then 2 mbarriers + ints
+  static constexpr int W1P = D::W1 + 1;
+  static constexpr int S0P = D::S0 + 4;
   static __host__ __device__ size_t floats() {
-    return D::S1 + static_cast<size_t>(D::TT) * (D::W1P + D::S0P + D::S2P);
+    size_t f = D::S1 + static_cast<size_t>(D::TT) * (W1P + S0P + D::S2P);
+    return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes(int m0) {
-    return floats() * 4 + sizeof(int) * (static_cast<size_t>(m0) + 5 * D::TT + 40);
+    return floats() * 4 + 16 + sizeof(int) * (static_cast<size_t>(m0) + 5 * D::TT + 40);
   }
 };
 
 // ------------------------------------------------------------- f3_fwd ----
-// Per tile: stage G1[i1]; dedup i0 -> slots (numbered by ascending i0 -> the
-// same numbering in backward); H(slot); y per lookup.  Saves H, slot maps.
+// Per tile: TMA G1[i1] (issued first, overlaps the index gathers); dedup i0
+// -> slots (ascending i0, the numbering backward reuses); TMA the slot G0
+// rows and the lookups' G2 slices; H(slot) = G0·G1; y = H·G2 per lookup.
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
@@ -285,12 +360,14 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint16_t* __restrict__ slot_of_pos,
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots) {
-  extern __shared__ __align__(16) float sm[];
+  using SM = FwdSmem<D>;
+  extern __shared__ __align__(128) float sm[];
   float* G1s = sm;
   float* Hs = G1s + D::S1;
-  float* G0s = Hs + D::TT * D::W1P;
-  float* G2s = G0s + D::TT * D::S0P;
-  int* flags = reinterpret_cast<int*>(G2s + D::TT * D::S2P);
+  float* G0s = Hs + D::TT * SM::W1P;
+  float* G2s = G0s + D::TT * SM::S0P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM::floats());
+  int* flags = reinterpret_cast<int*>(bars + 2);
   int* lk_l = flags + g.m0;
   int* lk_i0 = lk_l + D::TT;
   int* lk_i2 = lk_i0 + D::TT;
@@ -302,28 +379,33 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
   const int tid = threadIdx.x;
-  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  for (int i = tid; i < g.m0; i += kThreads) flags[i] = 0;
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int t = blockIdx.x; t < nt; t += gridDim.x, phase ^= 1u) {
     const Tile tl = tiles[t];
     const int i1 = tl.key % g.m1;
     const int ntl = tl.end - tl.start;
-    {
-      const float4* src = reinterpret_cast<const float4*>(G1 + static_cast<int64_t>(i1) * D::S1);
-      for (int e = tid; e < D::S1 / 4; e += kThreads) reinterpret_cast<float4*>(G1s)[e] = src[e];
+    if (tid == 0) {
+      // smem last touched by generic-proxy accesses; order them before the TMA writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect(&bars[0], D::S1 * 4);
+      tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, &bars[0]);
     }
-    for (int i = tid; i < g.m0; i += kThreads) flags[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < ntl; i += kThreads) {
-      const int l = static_cast<int>(perm[tl.start + i]);
-      lk_l[i] = l;
+    if (tid < ntl) {
+      const int l = static_cast<int>(perm[tl.start + tid]);
       const int i0 = d0[l];
-      lk_i0[i] = i0;
       const int i2 = d2[l];
-      lk_i2[i] = i2;
+      lk_l[tid] = l;
+      lk_i0[tid] = i0;
+      lk_i2[tid] = i2;
       flags[i0] = 1;
-      // stage G2[i2] (float4 rows, padded stride)
     }
     __syncthreads();
-    // slot numbering: ascending i0 (deterministic)
     int nslots;
     {
       const int per = (g.m0 + kThreads - 1) / kThreads;
@@ -335,37 +417,43 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         if (flags[i]) {
           slot_i0[ex] = i;
           flags[i] = ex++;
-        } else {
-          flags[i] = -1;
         }
       }
     }
+    if (tid == 0) mbar_arrive_expect(&bars[1], (nslots * D::S0 + ntl * D::S2) * 4);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    for (int i = tid; i < ntl; i += kThreads) lk_slot[i] = flags[lk_i0[i]];
-    for (int e = tid; e < nslots * D::S0; e += kThreads) {
-      const int s = e / D::S0, q = e - s * D::S0;
-      G0s[s * D::S0P + q] = G0[static_cast<int64_t>(slot_i0[s]) * D::S0 + q];
+    if (tid < nslots)
+      tma_load(G0s + tid * SM::S0P, G0 + static_cast<int64_t>(slot_i0[tid]) * D::S0, D::S0 * 4,
+               &bars[1]);
+    if (tid < ntl) {
+      tma_load(G2s + tid * D::S2P, G2 + static_cast<int64_t>(lk_i2[tid]) * D::S2, D::S2 * 4,
+               &bars[1]);
+      const int s = flags[lk_i0[tid]];
+      lk_slot[tid] = s;
+      slot_of_pos[tl.start + tid] = static_cast<uint16_t>(s);
     }
-    for (int e = tid; e < ntl * (D::S2 / 4); e += kThreads) {
-      const int i = e / (D::S2 / 4), q = e - i * (D::S2 / 4);
-      reinterpret_cast<float4*>(G2s + i * D::S2P)[q] =
-          reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2)[q];
-    }
+    if (tid < nslots) tile_i0[tl.start + tid] = static_cast<uint16_t>(slot_i0[tid]);
+    if (tid == 0) tile_nslots[t] = nslots;
+    mbar_wait(&bars[0], phase);
+    mbar_wait(&bars[1], phase);
+    // flags back to 0 for the next tile (only the entries this tile set)
     __syncthreads();
+    if (tid < nslots) flags[slot_i0[tid]] = 0;
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
     for (int q = tid; q < nslots * D::C4; q += kThreads) {
       const int s = q / D::C4, c4 = q - s * D::C4;
       float4 acc[D::P0];
 #pragma unroll
       for (int a = 0; a < D::P0; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* g0 = G0s + s * D::S0P;
+      const float* g0 = G0s + s * SM::S0P;
 #pragma unroll 8
       for (int p = 0; p < D::R1; ++p) {
         const float4 b = reinterpret_cast<const float4*>(G1s + p * D::C1)[c4];
 #pragma unroll
         for (int a = 0; a < D::P0; ++a) acc[a] = madd4<float, kExact>(g0[a * D::R1 + p], b, acc[a]);
       }
-      float* hrow = Hs + s * D::W1P;
+      float* hrow = Hs + s * SM::W1P;
       float* hg = Hbuf + static_cast<int64_t>(tl.start + s) * D::W1;
 #pragma unroll
       for (int a = 0; a < D::P0; ++a) {
@@ -377,14 +465,11 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         reinterpret_cast<float4*>(hg + c)[0] = acc[a];
       }
     }
-    for (int s = tid; s < nslots; s += kThreads) tile_i0[tl.start + s] = static_cast<uint16_t>(slot_i0[s]);
-    for (int i = tid; i < ntl; i += kThreads) slot_of_pos[tl.start + i] = static_cast<uint16_t>(lk_slot[i]);
-    if (tid == 0) tile_nslots[t] = nslots;
     __syncthreads();
     // y = H(slot) (P1 x R2) · G2[i2] (R2 x N2): thread -> (lookup, row a)
     for (int q = tid; q < ntl * D::P1; q += kThreads) {
       const int i = q / D::P1, a = q - i * D::P1;
-      const float* hrow = Hs + lk_slot[i] * D::W1P + a * D::R2;
+      const float* hrow = Hs + lk_slot[i] * SM::W1P + a * D::R2;
       const float4* g2 = reinterpret_cast<const float4*>(G2s + i * D::S2P);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
@@ -427,18 +512,26 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
 // -------------------------------------------------------------- f3_bwd ---
 template <class D>
 struct BwdSmem {
-  // floats: G1s[R1*C1P] | A[TT*W1P] (H then S) | Bq[max(BLK*S2, TT*S2P)] (P2 then G2s)
-  //         | D2s[TT*N] | G0s[TT*S0P] ; ints after
+  // floats: G1s[S1] | A[TT*W1] (H, then S) | P2[BLK*S2] | G2s[TT*S2P] | Gr[TT*N]
+  //         | G0s[TT*S0P] ; then mbarrier + u64 mask + ints
+  static constexpr int S0P = D::S0 + 4;
   static __host__ __device__ size_t floats(int blk) {
-    const size_t b1 = static_cast<size_t>(blk) * D::S2, b2 = static_cast<size_t>(D::TT) * D::S2P;
-    return static_cast<size_t>(D::R1) * D::C1P + static_cast<size_t>(D::TT) * D::W1P +
-           (b1 > b2 ? b1 : b2) + static_cast<size_t>(D::TT) * (D::N + D::S0P);
+    size_t f = static_cast<size_t>(D::S1) + static_cast<size_t>(D::TT) * D::W1 +
+               static_cast<size_t>(blk) * D::S2 +
+               static_cast<size_t>(D::TT) * (D::S2P + D::N + S0P);
+    return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes(int m0, int blk) {
-    return floats(blk) * 4 + sizeof(int) * (static_cast<size_t>(m0) + 4 * D::TT + 8);
+    (void)m0;
+    return floats(blk) * 4 + 16 + sizeof(int) * (5 * static_cast<size_t>(D::TT) + 8);
   }
 };
 
+// Each CTA owns a contiguous range of tiles.  Consecutive tiles of the same
+// bucket keep accumulating the dG1 partial (registers) and the dG2 partial
+// (smem); one partial per (CTA, bucket run) is flushed, stored at the run's
+// first tile (has1 / mask2 mark it).  D0 accumulates per (CTA, i0) in a
+// CTA-private global block.  Everything is folded later in fixed order.
 template <class D>
 __global__ void __launch_bounds__(kThreads) f3_bwd(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
@@ -447,259 +540,348 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
     const float* __restrict__ alpha, const float* __restrict__ grad,
     const float* __restrict__ Hbuf, const uint16_t* __restrict__ slot_of_pos,
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
-    float* __restrict__ part1, float* __restrict__ part2, unsigned long long* __restrict__ mask2,
-    float* __restrict__ D0buf, int* __restrict__ tab0, int tab_stride) {
-  extern __shared__ __align__(16) float sm[];
-  float* G1s = sm;                                   // R1 x C1P
-  float* A = G1s + D::R1 * D::C1P;                   // TT x W1P  (H, then S)
-  float* Bq = A + D::TT * D::W1P;                    // P2 (BLK x S2), then G2s (TT x S2P)
-  const int bq = (g.blk * D::S2 > D::TT * D::S2P) ? g.blk * D::S2 : D::TT * D::S2P;
-  float* D2s = Bq + bq;                              // TT x N
-  float* G0s = D2s + D::TT * D::N;                   // TT x S0P
-  int* slotmap = reinterpret_cast<int*>(G0s + D::TT * D::S0P);  // m0
-  int* lk_slot = slotmap + g.m0;
+    float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ part2,
+    unsigned long long* __restrict__ mask2, float* __restrict__ D0acc,
+    unsigned char* __restrict__ d0mask) {
+  using SM = BwdSmem<D>;
+  extern __shared__ __align__(128) float sm[];
+  float* G1s = sm;                                   // R1 x C1 (contiguous, TMA)
+  float* A = G1s + D::S1;                            // TT x W1  (H rows via TMA, then S)
+  float* Bq = A + D::TT * D::W1;                     // dG2 partial, BLK x S2
+  const int p2sz = g.blk * D::S2;
+  float* G2s = Bq + p2sz;                            // TT x S2P
+  float* Gr = G2s + D::TT * D::S2P;                  // TT x N   (raw grad rows)
+  float* G0s = Gr + D::TT * D::N;                    // TT x S0P
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats(g.blk));
+  unsigned long long* tmask = reinterpret_cast<unsigned long long*>(bar + 1);
+  int* lk_slot = reinterpret_cast<int*>(tmask + 1);
   int* lk_i2 = lk_slot + D::TT;
-  int* lk_l = lk_i2 + D::TT;
-  int* slot_i0 = lk_l + D::TT;
-  unsigned long long* tmask = reinterpret_cast<unsigned long long*>(slot_i0 + D::TT + 2);
+  int* lk_bg = lk_i2 + D::TT;
+  float* lk_al = reinterpret_cast<float*>(lk_bg + D::TT);
+  int* slot_i0 = reinterpret_cast<int*>(lk_al + D::TT);
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
   const int tid = threadIdx.x;
-  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+  const int t_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nt / gridDim.x);
+  const int t_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nt / gridDim.x);
+  float* d0acc = D0acc + static_cast<int64_t>(blockIdx.x) * g.m0 * D::S0;
+  unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
+  if (tid == 0) mbar_init(bar, 1);
+  for (int e = tid; e < g.m0 * D::S0; e += kThreads) d0acc[e] = 0.f;
+  for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
+  constexpr int PER = D::S1 / kThreads > 0 ? D::S1 / kThreads : 1;
+  float acc1[PER];
+#pragma unroll
+  for (int x = 0; x < PER; ++x) acc1[x] = 0.f;
+  int run_start = t_lo;
+  for (int e = tid; e < p2sz; e += kThreads) Bq[e] = 0.f;
+  if (tid == 0) *tmask = 0ull;
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int t = t_lo; t < t_hi; ++t, phase ^= 1u) {
     const Tile tl = tiles[t];
     const int i1 = tl.key % g.m1;
     const int i2base = (tl.key / g.m1) * g.blk;
     const int ntl = tl.end - tl.start;
     const int nslots = tile_nslots[t];
-    for (int e = tid; e < D::S1; e += kThreads) {
-      const int r = e / D::C1, c = e - r * D::C1;
-      G1s[r * D::C1P + c] = G1[static_cast<int64_t>(i1) * D::S1 + e];
+    if (tid < ntl) {
+      const int l = static_cast<int>(perm[tl.start + tid]);
+      lk_slot[tid] = slot_of_pos[tl.start + tid];
+      const int i2 = d2[l];
+      const int bg = lk_bag[l];
+      lk_i2[tid] = i2;
+      lk_bg[tid] = bg;
+      lk_al[tid] = alpha[l];
+      atomicOr(tmask, 1ull << (i2 - i2base));
     }
-    for (int i = tid; i < g.m0; i += kThreads) slotmap[i] = -1;
-    for (int e = tid; e < g.blk * D::S2; e += kThreads) Bq[e] = 0.f;
-    if (tid == 0) *tmask = 0ull;
-    for (int i = tid; i < ntl; i += kThreads) {
-      const int l = static_cast<int>(perm[tl.start + i]);
-      lk_l[i] = l;
-      lk_i2[i] = d2[l];
-      lk_slot[i] = slot_of_pos[tl.start + i];
-    }
+    if (tid < nslots) slot_i0[tid] = tile_i0[tl.start + tid];
+    if (tid == 0)
+      mbar_arrive_expect(bar, (D::S1 + nslots * (D::W1 + D::S0) + ntl * (D::S2 + D::N)) * 4);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    for (int s = tid; s < nslots; s += kThreads) {
-      const int i0 = tile_i0[tl.start + s];
-      slot_i0[s] = i0;
-      slotmap[i0] = s;
+    if (tid == 0) tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, bar);
+    if (tid < nslots) {
+      tma_load(A + tid * D::W1, Hbuf + static_cast<int64_t>(tl.start + tid) * D::W1, D::W1 * 4, bar);
+      tma_load(G0s + tid * SM::S0P, G0 + static_cast<int64_t>(slot_i0[tid]) * D::S0, D::S0 * 4, bar);
     }
-    for (int e = tid; e < ntl * D::N; e += kThreads) {
-      const int i = e / D::N, j = e - i * D::N;
-      const int l = lk_l[i];
-      D2s[e] = __fmul_rn(alpha[l], grad[static_cast<int64_t>(lk_bag[l]) * D::N + j]);
+    if (tid < ntl) {
+      tma_load(G2s + tid * D::S2P, G2 + static_cast<int64_t>(lk_i2[tid]) * D::S2, D::S2 * 4, bar);
+      tma_load(Gr + tid * D::N, grad + static_cast<int64_t>(lk_bg[tid]) * D::N, D::N * 4, bar);
     }
-    for (int e = tid; e < nslots * D::W1; e += kThreads) {
-      const int s = e / D::W1, q = e - s * D::W1;
-      A[s * D::W1P + q] = Hbuf[static_cast<int64_t>(tl.start + s) * D::W1 + q];
-    }
-    __syncthreads();
-    // dG2 partial: slice j = i2 - i2base, element e = (r, j2); groups split lookups by i2 parity
+    mbar_wait(bar, phase);
+    // dG2 partial (accumulates over the bucket run): slice j = i2 - i2base,
+    // element e = (r, j2); slices split between thread groups by j parity
     {
       constexpr int NG = kThreads / D::S2 > 0 ? kThreads / D::S2 : 1;
-      const int e = tid % D::S2, grp = tid / D::S2;
-      if (grp < NG) {
+      for (int e0 = tid; e0 < D::S2 * NG; e0 += kThreads) {
+        const int e = e0 % D::S2, grp = e0 / D::S2;
         const int r = e / D::N2, j2 = e - r * D::N2;
         for (int i = 0; i < ntl; ++i) {
           const int j = lk_i2[i] - i2base;
           if (j % NG != grp) continue;
-          const float* hrow = A + lk_slot[i] * D::W1P + r;
-          const float* d = D2s + i * D::N + j2;
+          const float* hrow = A + lk_slot[i] * D::W1 + r;
+          const float* gr = Gr + i * D::N + j2;
+          const float al = lk_al[i];
           float v = Bq[j * D::S2 + e];
 #pragma unroll
-          for (int a = 0; a < D::P1; ++a) v = __fmaf_rn(hrow[a * D::R2], d[a * D::N2], v);
+          for (int a = 0; a < D::P1; ++a)
+            v = __fmaf_rn(hrow[a * D::R2], __fmul_rn(al, gr[a * D::N2]), v);
           Bq[j * D::S2 + e] = v;
         }
       }
-      for (int i = tid; i < ntl; i += kThreads) atomicOr(tmask, 1ull << (lk_i2[i] - i2base));
     }
     __syncthreads();
-    const unsigned long long tm = *tmask;
-    for (int e = tid; e < g.blk * D::S2; e += kThreads) {
-      const int j = e / D::S2;
-      if ((tm >> j) & 1ull) part2[static_cast<int64_t>(t) * g.blk * D::S2 + e] = Bq[e];
-    }
-    if (tid == 0) mask2[t] = tm;
+    for (int e = tid; e < nslots * D::W1; e += kThreads) A[e] = 0.f;
     __syncthreads();
-    // stage G2 slices (reuse Bq) and zero S (reuse A)
-    for (int e = tid; e < ntl * (D::S2 / 4); e += kThreads) {
-      const int i = e / (D::S2 / 4), q = e - i * (D::S2 / 4);
-      reinterpret_cast<float4*>(Bq + i * D::S2P)[q] =
-          reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2)[q];
-    }
-    for (int e = tid; e < nslots * D::W1P; e += kThreads) A[e] = 0.f;
-    __syncthreads();
-    // S(slot) += D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2); element e = (a, r); groups by slot parity
+    // S(slot) += D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2); element e = (a, r); slot-parity groups
     {
       constexpr int NG = kThreads / D::W1 > 0 ? kThreads / D::W1 : 1;
       for (int e0 = tid; e0 < D::W1 * NG; e0 += kThreads) {
         const int e = e0 % D::W1, grp = e0 / D::W1;
         const int a = e / D::R2, r = e - a * D::R2;
+        float acc = 0.f;
+        int cur = -1;
         for (int i = 0; i < ntl; ++i) {
           const int s = lk_slot[i];
           if (s % NG != grp) continue;
-          const float4 gv = reinterpret_cast<const float4*>(Bq + i * D::S2P)[r];
-          const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
-          float v = __fmul_rn(dv.x, gv.x);
-          v = __fmaf_rn(dv.y, gv.y, v);
-          v = __fmaf_rn(dv.z, gv.z, v);
-          v = __fmaf_rn(dv.w, gv.w, v);
-          A[s * D::W1P + e] += v;
+          if (s != cur) {
+            if (cur >= 0) A[cur * D::W1 + e] += acc;
+            acc = 0.f;
+            cur = s;
+          }
+          const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2P)[r];
+          const float4 gw = reinterpret_cast<const float4*>(Gr + i * D::N)[a];
+          const float al = lk_al[i];
+          float v = __fmul_rn(__fmul_rn(al, gw.x), gv.x);
+          v = __fmaf_rn(__fmul_rn(al, gw.y), gv.y, v);
+          v = __fmaf_rn(__fmul_rn(al, gw.z), gv.z, v);
+          v = __fmaf_rn(__fmul_rn(al, gw.w), gv.w, v);
+          acc += v;
         }
+        if (cur >= 0) A[cur * D::W1 + e] += acc;
       }
-    }
-    for (int e = tid; e < nslots * D::S0; e += kThreads) {
-      const int s = e / D::S0, q = e - s * D::S0;
-      G0s[s * D::S0P + q] = G0[static_cast<int64_t>(slot_i0[s]) * D::S0 + q];
     }
     __syncthreads();
-    // dG1 partial (R1 x C1) = Σ_slots G0[i0]ᵀ (R1 x P0) · S (P0 x C1)
+    // dG1 partial += Σ_slots G0[i0]ᵀ (R1 x P0) · S (P0 x C1)
     {
-      constexpr int PER = D::S1 / kThreads > 0 ? D::S1 / kThreads : 1;
-      for (int e0 = tid * PER; e0 < D::S1; e0 += kThreads * PER) {
+      const int e0 = tid * PER;
+      if (e0 < D::S1) {
         const int r1 = e0 / D::C1, c0 = e0 - r1 * D::C1;
-        float acc[PER];
-#pragma unroll
-        for (int x = 0; x < PER; ++x) acc[x] = 0.f;
         for (int s = 0; s < nslots; ++s) {
-          const float* srow = A + s * D::W1P;
+          const float* srow = A + s * D::W1;
 #pragma unroll
           for (int a = 0; a < D::P0; ++a) {
-            const float gv = G0s[s * D::S0P + a * D::R1 + r1];
+            const float gv = G0s[s * SM::S0P + a * D::R1 + r1];
 #pragma unroll
-            for (int x = 0; x < PER; ++x) acc[x] = __fmaf_rn(gv, srow[a * D::C1 + c0 + x], acc[x]);
+            for (int x = 0; x < PER; ++x) acc1[x] = __fmaf_rn(gv, srow[a * D::C1 + c0 + x], acc1[x]);
           }
         }
-        float* dst = part1 + static_cast<int64_t>(t) * D::S1 + e0;
-#pragma unroll
-        for (int x = 0; x < PER; ++x) dst[x] = acc[x];
       }
     }
-    // D0(slot) (P0 x R1) = S (P0 x C1) · G1[i1]ᵀ (C1 x R1)
+    // D0(slot) (P0 x R1) = S (P0 x C1) · G1[i1]ᵀ (C1 x R1), into smem scratch (reuse G2s)
+    float* d0tmp = G2s;
     for (int q = tid; q < nslots * D::S0; q += kThreads) {
       const int s = q / D::S0, e = q - s * D::S0;
       const int a = e / D::R1, r1 = e - a * D::R1;
-      const float* srow = A + s * D::W1P + a * D::C1;
-      const float* grow = G1s + r1 * D::C1P;
+      const float* srow = A + s * D::W1 + a * D::C1;
+      const float* grow = G1s + r1 * D::C1;
       float v = 0.f;
+      // rotated column order: lanes with different r1 hit different banks
 #pragma unroll 8
-      for (int c = 0; c < D::C1; ++c) v = __fmaf_rn(srow[c], grow[c], v);
-      D0buf[static_cast<int64_t>(tl.start + s) * D::S0 + e] = v;
+      for (int k = 0; k < D::C1; ++k) {
+        const int c = (k + r1) & (D::C1 - 1);
+        v = __fmaf_rn(srow[c], grow[c], v);
+      }
+      d0tmp[q] = v;
     }
-    for (int i0 = tid; i0 < g.m0; i0 += kThreads)
-      tab0[static_cast<int64_t>(i0) * tab_stride + t] = slotmap[i0];
+    __syncthreads();
+    // batched read-modify-write of this CTA's private D0 accumulator
+    {
+      constexpr int U = 4;
+      for (int q0 = tid; q0 < nslots * D::S0; q0 += kThreads * U) {
+        float cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = q0 + u * kThreads;
+          if (q < nslots * D::S0) {
+            const int s = q / D::S0, e = q - s * D::S0;
+            cur[u] = d0acc[slot_i0[s] * D::S0 + e];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = q0 + u * kThreads;
+          if (q < nslots * D::S0) {
+            const int s = q / D::S0, e = q - s * D::S0;
+            d0acc[slot_i0[s] * D::S0 + e] = cur[u] + d0tmp[q];
+            if (e == 0) d0m[slot_i0[s]] = 1;
+          }
+        }
+      }
+    }
+    // end of a bucket run (or of this CTA's range): flush the run partials
+    const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
+    if (tid == 0) {
+      has1[t] = (t == run_start) ? 1 : 0;
+      if (t != run_start) mask2[t] = 0ull;
+    }
+    __syncthreads();
+    if (last) {
+      const int e0 = tid * PER;
+      if (e0 < D::S1) {
+        float* dst = part1 + static_cast<int64_t>(run_start) * D::S1 + e0;
+#pragma unroll
+        for (int x = 0; x < PER; ++x) {
+          dst[x] = acc1[x];
+          acc1[x] = 0.f;
+        }
+      }
+      const unsigned long long tm = *tmask;
+      for (int e = tid; e < p2sz; e += kThreads) {
+        const int j = e / D::S2;
+        if ((tm >> j) & 1ull) part2[static_cast<int64_t>(run_start) * p2sz + e] = Bq[e];
+        Bq[e] = 0.f;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        mask2[run_start] = tm;
+        *tmask = 0ull;
+      }
+      run_start = t + 1;
+    }
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------- f3_combine ---
-// CTA roles: [0, m1) dG1 slices, [m1, m1+m2) dG2 slices, [m1+m2, +m0) dG0.
-// MODE 0: dense gradient write (zeros for untouched slices); 1: SGD in place.
+// Fixed-order list reductions.  One CTA per (output slice, 128-column chunk):
+// 8 warps take candidate list positions w, w+8, ...; lanes own float4
+// columns; the warp sums are folded in warp order.  Roles by blockIdx:
+//   [0, m1*C1c)            dG1[i1]   candidates: tiles of buckets (blk, i1), has1
+//   [.., + m2*C2c)         dG2[i2]   candidates: tiles of blk(i2) buckets, mask2 bit
+//   [.., + m0*C0c)         dG0[i0]   candidates: bwd CTAs, d0mask
+// MODE 0 writes dense gradients (zeros if untouched), 1 applies SGD in place.
+template <int W>
+__device__ __forceinline__ void fold_store(float4 v, bool touched, float* red, float* out_core,
+                                           float* out_grad, int col4, int mode, float lr,
+                                           int* touched_sm) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  reinterpret_cast<float4*>(red)[wid * 32 + lane] = v;
+  if (touched) atomicOr(touched_sm, 1);
+  __syncthreads();
+  if (wid == 0 && col4 < W / 4) {
+    float4 s = reinterpret_cast<float4*>(red)[lane];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      const float4 q = reinterpret_cast<float4*>(red)[w * 32 + lane];
+      s.x += q.x;
+      s.y += q.y;
+      s.z += q.z;
+      s.w += q.w;
+    }
+    if (mode == 0) {
+      reinterpret_cast<float4*>(out_grad)[col4] = s;
+    } else if (*touched_sm) {
+      float4 c = reinterpret_cast<float4*>(out_core)[col4];
+      c.x = __fadd_rn(c.x, -__fmul_rn(lr, s.x));
+      c.y = __fadd_rn(c.y, -__fmul_rn(lr, s.y));
+      c.z = __fadd_rn(c.z, -__fmul_rn(lr, s.z));
+      c.w = __fadd_rn(c.w, -__fmul_rn(lr, s.w));
+      reinterpret_cast<float4*>(out_core)[col4] = c;
+    }
+  }
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
 template <class D, int MODE>
 __global__ void __launch_bounds__(kThreads) f3_combine(
-    Geo g, float* __restrict__ cores, float* __restrict__ grads, const Tile* __restrict__ tiles,
-    const int* __restrict__ ntiles, const int32_t* __restrict__ tile_base,
-    const float* __restrict__ part1, const float* __restrict__ part2,
-    const unsigned long long* __restrict__ mask2, const float* __restrict__ D0buf,
-    const int* __restrict__ tab0, int tab_stride, float lr) {
-  extern __shared__ int lst[];  // compacted (tile, slot) lists
-  __shared__ int cnt_sm[40];
-  const int tid = threadIdx.x;
-  const int nt = *ntiles;
-  const int bid = blockIdx.x;
-  if (bid < g.m1) {
-    const int i1 = bid;
-    for (int e = tid; e < D::S1; e += kThreads) {
-      float sum = 0.f;
-      bool touched = false;
-      for (int b = 0; b < g.nblk; ++b) {
-        const int key = b * g.m1 + i1;
-        for (int t = tile_base[key]; t < tile_base[key + 1]; ++t) {
-          sum += part1[static_cast<int64_t>(t) * D::S1 + e];
+    Geo g, float* __restrict__ cores, float* __restrict__ grads, const int* __restrict__ ntiles,
+    const int32_t* __restrict__ tile_base, const float* __restrict__ part1,
+    const int* __restrict__ has1, const float* __restrict__ part2,
+    const unsigned long long* __restrict__ mask2, const float* __restrict__ D0acc,
+    const unsigned char* __restrict__ d0mask, int nbwd, float lr) {
+  __shared__ __align__(16) float red[kThreads * 4];
+  __shared__ int touched_sm;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
+  if (threadIdx.x == 0) touched_sm = 0;
+  __syncthreads();
+  int bid = blockIdx.x;
+  float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (bid < g.m1 * C1c) {
+    const int i1 = bid / C1c, ch = bid - i1 * C1c;
+    const int col4 = ch * 32 + lane;
+    const bool colok = col4 < D::S1 / 4;
+    float4 a0 = z, a1 = z;
+    bool touched = false;
+    for (int b = 0; b < g.nblk; ++b) {
+      const int key = b * g.m1 + i1;
+      const int t0 = tile_base[key], t1 = tile_base[key + 1];
+      // warp w takes the tiles with t % 8 == w (a fixed, input-determined split)
+      for (int t = t0 + ((wid - t0) % 8 + 8) % 8; t < t1; t += 8) {
+        if (has1[t]) {
           touched = true;
+          if (colok) add4((t & 8) ? a1 : a0,
+                          reinterpret_cast<const float4*>(part1 + static_cast<int64_t>(t) * D::S1)[col4]);
         }
       }
-      const int64_t o = g.coff1 + static_cast<int64_t>(i1) * D::S1 + e;
-      if (MODE == 0)
-        grads[o] = sum;
-      else if (touched)
-        cores[o] = __fadd_rn(cores[o], -__fmul_rn(lr, sum));
     }
+    add4(a0, a1);
+    fold_store<D::S1>(a0, touched, red, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
+                      grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, col4, MODE, lr,
+                      &touched_sm);
     return;
   }
-  if (bid < g.m1 + g.m2) {
-    const int i2 = bid - g.m1;
+  bid -= g.m1 * C1c;
+  if (bid < g.m2 * C2c) {
+    const int i2 = bid / C2c, ch = bid - i2 * C2c;
     const int b = i2 / g.blk, j = i2 - b * g.blk;
+    const int col4 = ch * 32 + lane;
+    const bool colok = col4 < D::S2 / 4;
     const int t0 = tile_base[b * g.m1], t1 = tile_base[b * g.m1 + g.m1];
-    // compact the tiles that touched slice j, in tile order
-    int n = 0;
-    for (int base = t0; base < t1; base += kThreads) {
-      const int t = base + tid;
-      const int f = (t < t1) && ((mask2[t] >> j) & 1ull);
-      int tot;
-      const int pos = block_excl_scan(f, &tot, cnt_sm);
-      if (f) lst[n + pos] = t;
-      n += tot;
+    float4 a0 = z, a1 = z;
+    bool touched = false;
+    const int p2sz = g.blk * D::S2;
+    for (int t = t0 + wid; t < t1; t += 8) {
+      if ((mask2[t] >> j) & 1ull) {
+        touched = true;
+        if (colok)
+          add4(((t - t0) & 8) ? a1 : a0,
+               reinterpret_cast<const float4*>(part2 + static_cast<int64_t>(t) * p2sz + j * D::S2)[col4]);
+      }
     }
-    __syncthreads();
-    constexpr int NG = kThreads / D::S2 > 0 ? kThreads / D::S2 : 1;
-    float* red = reinterpret_cast<float*>(lst + n + 4);
-    const int e = tid % D::S2, grp = tid / D::S2;
-    float sum = 0.f;
-    if (grp < NG)
-      for (int k = grp; k < n; k += NG)
-        sum += part2[(static_cast<int64_t>(lst[k]) * g.blk + j) * D::S2 + e];
-    if (grp < NG) red[grp * D::S2 + e] = sum;
-    __syncthreads();
-    if (tid < D::S2) {
-      float s = red[tid];
-      for (int q = 1; q < NG; ++q) s += red[q * D::S2 + tid];
-      const int64_t o = g.coff2 + static_cast<int64_t>(i2) * D::S2 + tid;
-      if (MODE == 0)
-        grads[o] = s;
-      else if (n > 0)
-        cores[o] = __fadd_rn(cores[o], -__fmul_rn(lr, s));
-    }
+    add4(a0, a1);
+    fold_store<D::S2>(a0, touched, red, cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
+                      grads + g.coff2 + static_cast<int64_t>(i2) * D::S2, col4, MODE, lr,
+                      &touched_sm);
     return;
   }
-  const int i0 = bid - g.m1 - g.m2;
+  bid -= g.m2 * C2c;
+  const int i0 = bid / C0c, ch = bid - i0 * C0c;
   if (i0 >= g.m0) return;
-  int n = 0;
-  const int* row = tab0 + static_cast<int64_t>(i0) * tab_stride;
-  for (int base = 0; base < nt; base += kThreads) {
-    const int t = base + tid;
-    const int s = t < nt ? row[t] : -1;
-    int tot;
-    const int pos = block_excl_scan(s >= 0 ? 1 : 0, &tot, cnt_sm);
-    if (s >= 0) lst[n + pos] = tiles[t].start + s;
-    n += tot;
+  const int col4 = ch * 32 + lane;
+  const bool colok = col4 < D::S0 / 4;
+  float4 a0 = z, a1 = z;
+  bool touched = false;
+  for (int c = wid; c < nbwd; c += 8) {
+    if (d0mask[static_cast<int64_t>(c) * g.m0 + i0]) {
+      touched = true;
+      if (colok)
+        add4((c & 8) ? a1 : a0,
+             reinterpret_cast<const float4*>(D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0)[col4]);
+    }
   }
-  __syncthreads();
-  constexpr int NG = kThreads / D::S0 > 0 ? kThreads / D::S0 : 1;
-  float* red = reinterpret_cast<float*>(lst + n + 4);
-  const int e = tid % D::S0, grp = tid / D::S0;
-  float sum = 0.f;
-  if (grp < NG)
-    for (int k = grp; k < n; k += NG) sum += D0buf[static_cast<int64_t>(lst[k]) * D::S0 + e];
-  if (grp < NG) red[grp * D::S0 + e] = sum;
-  __syncthreads();
-  if (tid < D::S0) {
-    float s = red[tid];
-    for (int q = 1; q < NG; ++q) s += red[q * D::S0 + tid];
-    const int64_t o = g.coff0 + static_cast<int64_t>(i0) * D::S0 + tid;
-    if (MODE == 0)
-      grads[o] = s;
-    else if (n > 0)
-      cores[o] = __fadd_rn(cores[o], -__fmul_rn(lr, s));
-  }
+  add4(a0, a1);
+  fold_store<D::S0>(a0, touched, red, cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
+                    grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, col4, MODE, lr,
+                    &touched_sm);
 }
 
 }  // namespace f3

@@ -4,7 +4,7 @@ namespace ttgpu {
 
 struct F3Bufs {
   DevBuf key, d0, d2, hist, perm, tiles, tile_base, ntiles, Hbuf, y, slotpos, tile_i0, tile_nslots,
-      part1, part2, mask2, D0, tab0;
+      part1, has1, part2, mask2, D0acc, d0mask;
   f3::Geo geo{};
   int max_tiles = 0;
   int kind = -1;  // instantiation index
@@ -14,7 +14,25 @@ void f3_free(F3Bufs* f) { delete f; }
 
 namespace {
 
-constexpr int kF3TL = 2048;  // lookups per histogram / scatter CTA
+constexpr int kF3MaxHist = 48 * 1024;  // (key x CTA) histogram entries the 1-CTA scan stages
+
+// lookups per hist/scatter CTA: 512 * LPT, LPT in {4, 8, 16, 32}; 0 = infeasible
+int f3_lpt(int64_t L, int K) {
+  for (int lpt = 4; lpt <= 32; lpt *= 2) {
+    const int64_t nt = (L + 512 * lpt - 1) / (512 * lpt);
+    if (nt * K <= kF3MaxHist) return lpt;
+  }
+  return 0;
+}
+
+template <int LPT>
+void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const int64_t* idx,
+                 int64_t L, int NT, const int64_t* off, int64_t B, const double* w, int pooling,
+                 F3Bufs& f, int32_t* lk_bag, float* alpha, ttgpu_table* t) {
+  f3::f3_hist<float, LPT><<<grid, 512, smem, st>>>(
+      g, idx, L, NT, off, B, w, pooling, f.key.as<uint32_t>(), f.d0.as<uint16_t>(),
+      f.d2.as<uint16_t>(), lk_bag, alpha, f.hist.as<uint32_t>(), t->d_bad(), t->d_struct());
+}
 
 f3::Geo make_geo(const ttgpu_table* t) {
   f3::Geo g{};
@@ -44,7 +62,10 @@ struct F3Runner {
     cudaStream_t st = t->stream;
     f3::Geo& g = f.geo;
     g = make_geo(t);
-    const int NT = static_cast<int>((L + kF3TL - 1) / kF3TL);
+    const int lpt = f3_lpt(L, g.K);
+    if (lpt == 0) fail(TTGPU_ERR_RUNTIME, "batch too large for the fast path histogram");
+    const int TL = 512 * lpt;
+    const int NT = static_cast<int>((L + TL - 1) / TL);
     f.max_tiles = static_cast<int>((L + D::TT - 1) / D::TT) + g.K;
     f.key.ensure(4 * L);
     f.d0.ensure(2 * L);
@@ -61,17 +82,25 @@ struct F3Runner {
     f.tile_nslots.ensure(4 * f.max_tiles);
     const int gb = std::max(NT, grid_for(B, 512, t->num_sms, 4));
     t->mark("fwd_begin");
-    f3::f3_hist<float><<<gb, 512, 4 * g.K, st>>>(
-        g, idx, L, kF3TL, NT, off, B, w, pooling, f.key.as<uint32_t>(), f.d0.as<uint16_t>(),
-        f.d2.as<uint16_t>(), lk_bag, alpha, f.hist.as<uint32_t>(), t->d_bad(), t->d_struct());
+    switch (lpt) {
+      case 4: launch_hist<4>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      case 8: launch_hist<8>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      case 16: launch_hist<16>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      default: launch_hist<32>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+    }
     t->mark("hist");
-    f3::f3_scan<<<1, 1024, 0, st>>>(g, NT, D::TT, L, f.hist.as<uint32_t>(), f.tile_base.as<int32_t>(),
-                                    f.tiles.as<f3::Tile>(), f.ntiles.as<int>());
+    {
+      const size_t sm = 4 * static_cast<size_t>(g.K) * NT;
+      set_smem(f3::f3_scan, sm);
+      f3::f3_scan<<<1, 1024, sm, st>>>(g, NT, D::TT, L, f.hist.as<uint32_t>(),
+                                       f.tile_base.as<int32_t>(), f.tiles.as<f3::Tile>(),
+                                       f.ntiles.as<int>());
+    }
     t->mark("scan");
     {
       const size_t sm = 4 * 8 * static_cast<size_t>(g.K);
       set_smem(f3::f3_scatter, sm);
-      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.key.as<uint32_t>(), L, kF3TL, NT,
+      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.key.as<uint32_t>(), L, TL, NT,
                                           f.hist.as<uint32_t>(), f.perm.as<uint32_t>());
     }
     t->mark("scatter");
@@ -103,35 +132,34 @@ struct F3Runner {
                        const int32_t* lk_bag, const float* alpha, int64_t L) {
     cudaStream_t st = t->stream;
     const f3::Geo& g = f.geo;
+    const size_t sm = bwd_smem(g);
+    auto kern = f3::f3_bwd<D>;
+    set_smem(kern, sm);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::kThreads, sm);
+    const int grid = std::max(1, std::min(f.max_tiles, t->num_sms * std::max(occ, 1)));
     f.part1.ensure(4 * static_cast<size_t>(f.max_tiles) * D::S1);
+    f.has1.ensure(4 * static_cast<size_t>(f.max_tiles));
     f.part2.ensure(4 * static_cast<size_t>(f.max_tiles) * g.blk * D::S2);
     f.mask2.ensure(8 * static_cast<size_t>(f.max_tiles));
-    f.D0.ensure(4 * static_cast<size_t>(L) * D::S0);
-    f.tab0.ensure(4 * static_cast<size_t>(g.m0) * f.max_tiles);
+    f.D0acc.ensure(4 * static_cast<size_t>(grid) * g.m0 * D::S0);
+    f.d0mask.ensure(static_cast<size_t>(grid) * g.m0);
     t->mark("bwd_begin");
-    {
-      const size_t sm = bwd_smem(g);
-      auto kern = f3::f3_bwd<D>;
-      set_smem(kern, sm);
-      int occ = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::kThreads, sm);
-      const int grid = std::max(1, std::min(f.max_tiles, t->num_sms * std::max(occ, 1)));
-      kern<<<grid, f3::kThreads, sm, st>>>(
-          g, t->cores.as<float>(), f.tiles.as<f3::Tile>(), f.ntiles.as<int>(),
-          f.perm.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad, f.Hbuf.as<float>(),
-          f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(),
-          f.part1.as<float>(), f.part2.as<float>(), f.mask2.as<unsigned long long>(),
-          f.D0.as<float>(), f.tab0.as<int>(), f.max_tiles);
-    }
+    kern<<<grid, f3::kThreads, sm, st>>>(
+        g, t->cores.as<float>(), f.tiles.as<f3::Tile>(), f.ntiles.as<int>(), f.perm.as<uint32_t>(),
+        f.d2.as<uint16_t>(), lk_bag, alpha, grad, f.Hbuf.as<float>(), f.slotpos.as<uint16_t>(),
+        f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(), f.part1.as<float>(), f.has1.as<int>(),
+        f.part2.as<float>(), f.mask2.as<unsigned long long>(), f.D0acc.as<float>(),
+        f.d0mask.as<unsigned char>());
     t->mark("f3_bwd");
     {
-      const size_t sm = 4 * (static_cast<size_t>(f.max_tiles) + 8) + 4 * 2 * f3::kThreads;
-      auto kern = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
-      set_smem(kern, sm);
-      kern<<<g.m0 + g.m1 + g.m2, f3::kThreads, sm, st>>>(
-          g, t->cores.as<float>(), t->grads.as<float>(), f.tiles.as<f3::Tile>(), f.ntiles.as<int>(),
-          f.tile_base.as<int32_t>(), f.part1.as<float>(), f.part2.as<float>(),
-          f.mask2.as<unsigned long long>(), f.D0.as<float>(), f.tab0.as<int>(), f.max_tiles, lr);
+      constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
+      auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
+      ck<<<g.m1 * C1c + g.m2 * C2c + g.m0 * C0c, f3::kThreads, 0, st>>>(
+          g, t->cores.as<float>(), t->grads.as<float>(), f.ntiles.as<int>(),
+          f.tile_base.as<int32_t>(), f.part1.as<float>(), f.has1.as<int>(), f.part2.as<float>(),
+          f.mask2.as<unsigned long long>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>(),
+          grid, lr);
     }
     t->mark("f3_combine");
     CK(cudaGetLastError());
@@ -142,7 +170,7 @@ struct F3Runner {
 using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 128>;
 using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 128>;
 using F3_R32 = f3::Dims<2, 32, 2, 32, 4, 64>;
-using F3_R64 = f3::Dims<2, 64, 2, 64, 4, 64>;
+using F3_R64 = f3::Dims<2, 64, 2, 64, 4, 32>;
 
 template <class D>
 bool dims_match(const DevPlan& P) {
@@ -166,6 +194,8 @@ int f3_kind(const ttgpu_table* t) {
   if (dims_match<F3_R64>(P)) return 3;
   return -1;
 }
+
+bool f3_feasible(const ttgpu_table* t, int64_t L) { return f3_lpt(L, make_geo(t).K) > 0; }
 
 void f3_forward(int kind, ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L,
                 const int64_t* off, int64_t B, const double* w, int pooling, float* out, bool exact,

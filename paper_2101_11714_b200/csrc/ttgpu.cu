@@ -312,7 +312,7 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
   c->fast = false;
   if constexpr (std::is_same_v<T, float>) {
     const int kind = f3_kind(t);
-    if (kind >= 0 && !t->force_generic) {
+    if (kind >= 0 && !t->force_generic && f3_feasible(t, L)) {
       if (!c->f3) c->f3 = new F3Bufs;
       c->lk_bag.ensure(4 * L);
       c->lk_alpha.ensure(sizeof(T) * L);
