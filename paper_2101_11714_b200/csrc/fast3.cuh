@@ -245,22 +245,36 @@ __global__ void __launch_bounds__(1024) f3_scan(Geo g, int NT, int TT, int64_t L
   uint32_t tex;
   __syncthreads();
   Scan(tmp).ExclusiveSum(nt, tex);
+  uint32_t* tb = sh + n;  // K + 1 tile bases
   for (int k = klo; k < khi; ++k) {
     const uint32_t bs = sh[k * NT];
     const uint32_t be = k + 1 < g.K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
+    tb[k] = tex;
     tile_base[k] = static_cast<int32_t>(tex);
-    for (uint32_t st = bs; st < be; st += TT) {
-      Tile t;
-      t.key = k;
-      t.start = static_cast<int>(st);
-      t.end = static_cast<int>(min(be, st + TT));
-      t.pad = 0;
-      tiles[tex++] = t;
-    }
+    tex += (be - bs + TT - 1) / TT;
   }
   if (tid == 1023) {
+    tb[g.K] = tex;
     tile_base[g.K] = static_cast<int32_t>(tex);
     *ntiles = static_cast<int>(tex);
+  }
+  __syncthreads();
+  // one thread per tile: find its bucket by binary search over the tile bases
+  const uint32_t total = tb[g.K];
+  for (uint32_t t = tid; t < total; t += 1024) {
+    int lo = 0, hi = g.K;  // invariant: tb[lo] <= t < tb[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (tb[mid] <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t bs = sh[lo * NT];
+    const uint32_t be = lo + 1 < g.K ? sh[(lo + 1) * NT] : static_cast<uint32_t>(L);
+    Tile tl;
+    tl.key = lo;
+    tl.start = static_cast<int>(bs + (t - tb[lo]) * TT);
+    tl.end = static_cast<int>(min(be, bs + (t - tb[lo] + 1) * TT));
+    tl.pad = 0;
+    tiles[t] = tl;
   }
 }
 
@@ -330,14 +344,12 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restr
 }
 
 // --------------------------------------------------------- smem layouts ---
-// Row strides padded by 4 floats keep TMA destinations 16-byte aligned.
 template <class D>
 struct FwdSmem {
-  // floats: G1s[S1] | Hs[TT*W1P] | G0s[TT*S0P] | G2s[TT*S2P] ; then 2 mbarriers + ints
-  static constexpr int W1P = D::W1 + 1;
-  static constexpr int S0P = D::S0 + 4;
+  // floats: G1s[S1] (TMA) | Hs[TT*W1P] | G0s[TT*S0] ; then mbarrier + ints
+  static constexpr int W1P = D::W1 + 1;  // odd: lookups of different slots hit different banks
   static __host__ __device__ size_t floats() {
-    size_t f = D::S1 + static_cast<size_t>(D::TT) * (W1P + S0P + D::S2P);
+    size_t f = D::S1 + static_cast<size_t>(D::TT) * (W1P + D::S0);
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes(int m0) {
@@ -347,8 +359,8 @@ struct FwdSmem {
 
 // ------------------------------------------------------------- f3_fwd ----
 // Per tile: TMA G1[i1] (issued first, overlaps the index gathers); dedup i0
-// -> slots (ascending i0, the numbering backward reuses); TMA the slot G0
-// rows and the lookups' G2 slices; H(slot) = G0·G1; y = H·G2 per lookup.
+// -> slots (ascending i0, the numbering backward reuses); H(slot) = G0·G1
+// with G1 from smem; y = H·G2[i2] per lookup (G2 rows straight from L1/L2).
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
@@ -365,9 +377,8 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   float* G1s = sm;
   float* Hs = G1s + D::S1;
   float* G0s = Hs + D::TT * SM::W1P;
-  float* G2s = G0s + D::TT * SM::S0P;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM::floats());
-  int* flags = reinterpret_cast<int*>(bars + 2);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());
+  int* flags = reinterpret_cast<int*>(bar + 2);
   int* lk_l = flags + g.m0;
   int* lk_i0 = lk_l + D::TT;
   int* lk_i2 = lk_i0 + D::TT;
@@ -379,10 +390,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-  }
+  if (tid == 0) mbar_init(bar, 1);
   for (int i = tid; i < g.m0; i += kThreads) flags[i] = 0;
   __syncthreads();
   uint32_t phase = 0;
@@ -391,10 +399,10 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     const int i1 = tl.key % g.m1;
     const int ntl = tl.end - tl.start;
     if (tid == 0) {
-      // smem last touched by generic-proxy accesses; order them before the TMA writes
+      // smem last touched by generic-proxy accesses; order them before the TMA write
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect(&bars[0], D::S1 * 4);
-      tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, &bars[0]);
+      mbar_arrive_expect(bar, D::S1 * 4);
+      tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, bar);
     }
     if (tid < ntl) {
       const int l = static_cast<int>(perm[tl.start + tid]);
@@ -420,33 +428,43 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         }
       }
     }
-    if (tid == 0) mbar_arrive_expect(&bars[1], (nslots * D::S0 + ntl * D::S2) * 4);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (tid < nslots)
-      tma_load(G0s + tid * SM::S0P, G0 + static_cast<int64_t>(slot_i0[tid]) * D::S0, D::S0 * 4,
-               &bars[1]);
     if (tid < ntl) {
-      tma_load(G2s + tid * D::S2P, G2 + static_cast<int64_t>(lk_i2[tid]) * D::S2, D::S2 * 4,
-               &bars[1]);
       const int s = flags[lk_i0[tid]];
       lk_slot[tid] = s;
       slot_of_pos[tl.start + tid] = static_cast<uint16_t>(s);
     }
     if (tid < nslots) tile_i0[tl.start + tid] = static_cast<uint16_t>(slot_i0[tid]);
     if (tid == 0) tile_nslots[t] = nslots;
-    mbar_wait(&bars[0], phase);
-    mbar_wait(&bars[1], phase);
-    // flags back to 0 for the next tile (only the entries this tile set)
+    // G0 rows of the slots (independent loads, batched)
+    {
+      constexpr int U = 8;
+      for (int e0 = tid; e0 < nslots * D::S0; e0 += kThreads * U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kThreads;
+          v[u] = 0.f;
+          if (e < nslots * D::S0) {
+            const int s = e / D::S0;
+            v[u] = __ldg(G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (e0 + u * kThreads < nslots * D::S0) G0s[e0 + u * kThreads] = v[u];
+      }
+    }
     __syncthreads();
-    if (tid < nslots) flags[slot_i0[tid]] = 0;
+    if (tid < nslots) flags[slot_i0[tid]] = 0;  // ready for the next tile
+    mbar_wait(bar, phase);
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
     for (int q = tid; q < nslots * D::C4; q += kThreads) {
       const int s = q / D::C4, c4 = q - s * D::C4;
       float4 acc[D::P0];
 #pragma unroll
       for (int a = 0; a < D::P0; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* g0 = G0s + s * SM::S0P;
+      const float* g0 = G0s + s * D::S0;
 #pragma unroll 8
       for (int p = 0; p < D::R1; ++p) {
         const float4 b = reinterpret_cast<const float4*>(G1s + p * D::C1)[c4];
@@ -470,10 +488,10 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     for (int q = tid; q < ntl * D::P1; q += kThreads) {
       const int i = q / D::P1, a = q - i * D::P1;
       const float* hrow = Hs + lk_slot[i] * SM::W1P + a * D::R2;
-      const float4* g2 = reinterpret_cast<const float4*>(G2s + i * D::S2P);
+      const float4* g2 = reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-      for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
+      for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], __ldg(g2 + r), acc);
       reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
     }
     __syncthreads();
@@ -512,13 +530,12 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
 // -------------------------------------------------------------- f3_bwd ---
 template <class D>
 struct BwdSmem {
-  // floats: G1s[S1] | A[TT*W1] (H, then S) | P2[BLK*S2] | G2s[TT*S2P] | Gr[TT*N]
-  //         | G0s[TT*S0P] ; then mbarrier + u64 mask + ints
-  static constexpr int S0P = D::S0 + 4;
+  // floats: G1t[C1*R1P] (G1 slice transposed) | S[TT*W1] | P2[BLK*S2] | G0s[TT*S0]
+  //         | d0tmp[TT*S0] ; then u64 mask + ints
+  static constexpr int R1P = D::R1 + 4;
   static __host__ __device__ size_t floats(int blk) {
-    size_t f = static_cast<size_t>(D::S1) + static_cast<size_t>(D::TT) * D::W1 +
-               static_cast<size_t>(blk) * D::S2 +
-               static_cast<size_t>(D::TT) * (D::S2P + D::N + S0P);
+    size_t f = static_cast<size_t>(D::C1) * R1P + static_cast<size_t>(D::TT) * D::W1 +
+               static_cast<size_t>(blk) * D::S2 + 2 * static_cast<size_t>(D::TT) * D::S0;
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes(int m0, int blk) {
@@ -531,7 +548,10 @@ struct BwdSmem {
 // bucket keep accumulating the dG1 partial (registers) and the dG2 partial
 // (smem); one partial per (CTA, bucket run) is flushed, stored at the run's
 // first tile (has1 / mask2 mark it).  D0 accumulates per (CTA, i0) in a
-// CTA-private global block.  Everything is folded later in fixed order.
+// CTA-private global block.  Within a tile, warp w owns the dG2 slices
+// j = w (mod 8) and the slots s = w (mod 8): each warp walks the tile's
+// lookups in order and updates only what it owns, so every accumulation
+// happens in one fixed order (deterministic) with no atomics.
 template <class D>
 __global__ void __launch_bounds__(kThreads) f3_bwd(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
@@ -544,16 +564,15 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
     unsigned long long* __restrict__ mask2, float* __restrict__ D0acc,
     unsigned char* __restrict__ d0mask) {
   using SM = BwdSmem<D>;
+  constexpr int NW = kThreads / 32;
   extern __shared__ __align__(128) float sm[];
-  float* G1s = sm;                                   // R1 x C1 (contiguous, TMA)
-  float* A = G1s + D::S1;                            // TT x W1  (H rows via TMA, then S)
-  float* Bq = A + D::TT * D::W1;                     // dG2 partial, BLK x S2
+  float* G1t = sm;                                   // C1 x R1P
+  float* S = G1t + D::C1 * SM::R1P;                  // TT x W1
+  float* P2 = S + D::TT * D::W1;                     // BLK x S2
   const int p2sz = g.blk * D::S2;
-  float* G2s = Bq + p2sz;                            // TT x S2P
-  float* Gr = G2s + D::TT * D::S2P;                  // TT x N   (raw grad rows)
-  float* G0s = Gr + D::TT * D::N;                    // TT x S0P
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats(g.blk));
-  unsigned long long* tmask = reinterpret_cast<unsigned long long*>(bar + 1);
+  float* G0s = P2 + p2sz;                            // TT x S0
+  float* d0tmp = G0s + D::TT * D::S0;                // TT x S0
+  unsigned long long* tmask = reinterpret_cast<unsigned long long*>(sm + SM::floats(g.blk));
   int* lk_slot = reinterpret_cast<int*>(tmask + 1);
   int* lk_i2 = lk_slot + D::TT;
   int* lk_bg = lk_i2 + D::TT;
@@ -563,24 +582,24 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int t_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nt / gridDim.x);
   const int t_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nt / gridDim.x);
   float* d0acc = D0acc + static_cast<int64_t>(blockIdx.x) * g.m0 * D::S0;
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
-  if (tid == 0) mbar_init(bar, 1);
   for (int e = tid; e < g.m0 * D::S0; e += kThreads) d0acc[e] = 0.f;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
-  constexpr int PER = D::S1 / kThreads > 0 ? D::S1 / kThreads : 1;
-  float acc1[PER];
+  // dG1 partial: thread owns (r1, 4 consecutive columns) items, float4 each
+  constexpr int ITEMS1 = D::R1 * D::C4;
+  constexpr int PER1 = (ITEMS1 + kThreads - 1) / kThreads;
+  float4 acc1[PER1];
 #pragma unroll
-  for (int x = 0; x < PER; ++x) acc1[x] = 0.f;
+  for (int x = 0; x < PER1; ++x) acc1[x] = make_float4(0.f, 0.f, 0.f, 0.f);
   int run_start = t_lo;
-  for (int e = tid; e < p2sz; e += kThreads) Bq[e] = 0.f;
+  for (int e = tid; e < p2sz; e += kThreads) P2[e] = 0.f;
   if (tid == 0) *tmask = 0ull;
   __syncthreads();
-  uint32_t phase = 0;
-  for (int t = t_lo; t < t_hi; ++t, phase ^= 1u) {
+  for (int t = t_lo; t < t_hi; ++t) {
     const Tile tl = tiles[t];
     const int i1 = tl.key % g.m1;
     const int i2base = (tl.key / g.m1) * g.blk;
@@ -590,111 +609,141 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
       const int l = static_cast<int>(perm[tl.start + tid]);
       lk_slot[tid] = slot_of_pos[tl.start + tid];
       const int i2 = d2[l];
-      const int bg = lk_bag[l];
       lk_i2[tid] = i2;
-      lk_bg[tid] = bg;
+      lk_bg[tid] = lk_bag[l];
       lk_al[tid] = alpha[l];
       atomicOr(tmask, 1ull << (i2 - i2base));
     }
     if (tid < nslots) slot_i0[tid] = tile_i0[tl.start + tid];
-    if (tid == 0)
-      mbar_arrive_expect(bar, (D::S1 + nslots * (D::W1 + D::S0) + ntl * (D::S2 + D::N)) * 4);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, bar);
-    if (tid < nslots) {
-      tma_load(A + tid * D::W1, Hbuf + static_cast<int64_t>(tl.start + tid) * D::W1, D::W1 * 4, bar);
-      tma_load(G0s + tid * SM::S0P, G0 + static_cast<int64_t>(slot_i0[tid]) * D::S0, D::S0 * 4, bar);
-    }
-    if (tid < ntl) {
-      tma_load(G2s + tid * D::S2P, G2 + static_cast<int64_t>(lk_i2[tid]) * D::S2, D::S2 * 4, bar);
-      tma_load(Gr + tid * D::N, grad + static_cast<int64_t>(lk_bg[tid]) * D::N, D::N * 4, bar);
-    }
-    mbar_wait(bar, phase);
-    // dG2 partial (accumulates over the bucket run): slice j = i2 - i2base,
-    // element e = (r, j2); slices split between thread groups by j parity
+    // G1[i1] transposed into smem (c-major, padded rows): coalesced, batched loads
     {
-      constexpr int NG = kThreads / D::S2 > 0 ? kThreads / D::S2 : 1;
-      for (int e0 = tid; e0 < D::S2 * NG; e0 += kThreads) {
-        const int e = e0 % D::S2, grp = e0 / D::S2;
-        const int r = e / D::N2, j2 = e - r * D::N2;
-        for (int i = 0; i < ntl; ++i) {
-          const int j = lk_i2[i] - i2base;
-          if (j % NG != grp) continue;
-          const float* hrow = A + lk_slot[i] * D::W1 + r;
-          const float* gr = Gr + i * D::N + j2;
-          const float al = lk_al[i];
-          float v = Bq[j * D::S2 + e];
+      constexpr int U = (D::S1 / kThreads) > 8 ? 8 : (D::S1 / kThreads > 0 ? D::S1 / kThreads : 1);
+      const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
+      for (int e0 = tid; e0 < D::S1; e0 += kThreads * U) {
+        float v[U];
 #pragma unroll
-          for (int a = 0; a < D::P1; ++a)
-            v = __fmaf_rn(hrow[a * D::R2], __fmul_rn(al, gr[a * D::N2]), v);
-          Bq[j * D::S2 + e] = v;
+        for (int u = 0; u < U; ++u) v[u] = e0 + u * kThreads < D::S1 ? __ldg(src + e0 + u * kThreads) : 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kThreads;
+          if (e < D::S1) {
+            const int r = e / D::C1, c = e - r * D::C1;
+            G1t[c * SM::R1P + r] = v[u];
+          }
         }
       }
     }
     __syncthreads();
-    for (int e = tid; e < nslots * D::W1; e += kThreads) A[e] = 0.f;
-    __syncthreads();
-    // S(slot) += D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2); element e = (a, r); slot-parity groups
     {
-      constexpr int NG = kThreads / D::W1 > 0 ? kThreads / D::W1 : 1;
-      for (int e0 = tid; e0 < D::W1 * NG; e0 += kThreads) {
-        const int e = e0 % D::W1, grp = e0 / D::W1;
-        const int a = e / D::R2, r = e - a * D::R2;
-        float acc = 0.f;
-        int cur = -1;
-        for (int i = 0; i < ntl; ++i) {
-          const int s = lk_slot[i];
-          if (s % NG != grp) continue;
-          if (s != cur) {
-            if (cur >= 0) A[cur * D::W1 + e] += acc;
-            acc = 0.f;
-            cur = s;
+      constexpr int U = 8;
+      for (int e0 = tid; e0 < nslots * D::S0; e0 += kThreads * U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kThreads;
+          v[u] = 0.f;
+          if (e < nslots * D::S0) {
+            const int s = e / D::S0;
+            v[u] = __ldg(G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0));
           }
-          const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2P)[r];
-          const float4 gw = reinterpret_cast<const float4*>(Gr + i * D::N)[a];
-          const float al = lk_al[i];
-          float v = __fmul_rn(__fmul_rn(al, gw.x), gv.x);
-          v = __fmaf_rn(__fmul_rn(al, gw.y), gv.y, v);
-          v = __fmaf_rn(__fmul_rn(al, gw.z), gv.z, v);
-          v = __fmaf_rn(__fmul_rn(al, gw.w), gv.w, v);
-          acc += v;
         }
-        if (cur >= 0) A[cur * D::W1 + e] += acc;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (e0 + u * kThreads < nslots * D::S0) G0s[e0 + u * kThreads] = v[u];
+      }
+    }
+    for (int e = tid; e < nslots * D::W1; e += kThreads) S[e] = 0.f;
+    __syncthreads();
+    // dG2 (warp owns slices j = w mod NW) and S (warp owns slots s = w mod NW);
+    // lane owns rank column r.  D2 = alpha * grad row, recomputed per use.
+    for (int i = 0; i < ntl; ++i) {
+      const int j = lk_i2[i] - i2base;
+      const int s = lk_slot[i];
+      const bool own_j = (j % NW) == wid, own_s = (s % NW) == wid;
+      if (!own_j && !own_s) continue;
+      const float al = lk_al[i];
+      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bg[i]) * D::N);
+      float4 d[D::P1];
+#pragma unroll
+      for (int a = 0; a < D::P1; ++a) {
+        const float4 gv = __ldg(grow + a);
+        d[a] = make_float4(__fmul_rn(al, gv.x), __fmul_rn(al, gv.y), __fmul_rn(al, gv.z),
+                           __fmul_rn(al, gv.w));
+      }
+      for (int r = lane; r < D::R2; r += 32) {
+        if (own_j) {
+          // P2[j][r][:] += Σ_a H[a][r] · D2[a][:]
+          const float* hrow = Hbuf + static_cast<int64_t>(tl.start + s) * D::W1 + r;
+          float h[D::P1];
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) h[a] = __ldg(hrow + a * D::R2);
+          float4* p = reinterpret_cast<float4*>(P2 + j * D::S2 + r * D::N2);
+          float4 v = *p;
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) {
+            v.x = __fmaf_rn(h[a], d[a].x, v.x);
+            v.y = __fmaf_rn(h[a], d[a].y, v.y);
+            v.z = __fmaf_rn(h[a], d[a].z, v.z);
+            v.w = __fmaf_rn(h[a], d[a].w, v.w);
+          }
+          *p = v;
+        }
+        if (own_s) {
+          // S[s][a][r] += Σ_j2 D2[a][j2] · G2[i2][r][j2]
+          const float4 gv = __ldg(reinterpret_cast<const float4*>(
+              G2 + static_cast<int64_t>(lk_i2[i]) * D::S2) + r);
+          float* srow = S + s * D::W1 + r;
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) {
+            float v = __fmul_rn(d[a].x, gv.x);
+            v = __fmaf_rn(d[a].y, gv.y, v);
+            v = __fmaf_rn(d[a].z, gv.z, v);
+            v = __fmaf_rn(d[a].w, gv.w, v);
+            srow[a * D::R2] += v;
+          }
+        }
       }
     }
     __syncthreads();
     // dG1 partial += Σ_slots G0[i0]ᵀ (R1 x P0) · S (P0 x C1)
-    {
-      const int e0 = tid * PER;
-      if (e0 < D::S1) {
-        const int r1 = e0 / D::C1, c0 = e0 - r1 * D::C1;
+#pragma unroll
+    for (int x = 0; x < PER1; ++x) {
+      const int item = tid + x * kThreads;
+      if (item < ITEMS1) {
+        const int r1 = item / D::C4, c4 = item - r1 * D::C4;
+        float4 a4 = acc1[x];
         for (int s = 0; s < nslots; ++s) {
-          const float* srow = A + s * D::W1;
 #pragma unroll
           for (int a = 0; a < D::P0; ++a) {
-            const float gv = G0s[s * SM::S0P + a * D::R1 + r1];
-#pragma unroll
-            for (int x = 0; x < PER; ++x) acc1[x] = __fmaf_rn(gv, srow[a * D::C1 + c0 + x], acc1[x]);
+            const float gv = G0s[s * D::S0 + a * D::R1 + r1];
+            const float4 sv = reinterpret_cast<const float4*>(S + s * D::W1 + a * D::C1)[c4];
+            a4.x = __fmaf_rn(gv, sv.x, a4.x);
+            a4.y = __fmaf_rn(gv, sv.y, a4.y);
+            a4.z = __fmaf_rn(gv, sv.z, a4.z);
+            a4.w = __fmaf_rn(gv, sv.w, a4.w);
           }
         }
+        acc1[x] = a4;
       }
     }
-    // D0(slot) (P0 x R1) = S (P0 x C1) · G1[i1]ᵀ (C1 x R1), into smem scratch (reuse G2s)
-    float* d0tmp = G2s;
-    for (int q = tid; q < nslots * D::S0; q += kThreads) {
-      const int s = q / D::S0, e = q - s * D::S0;
-      const int a = e / D::R1, r1 = e - a * D::R1;
-      const float* srow = A + s * D::W1 + a * D::C1;
-      const float* grow = G1s + r1 * D::C1;
-      float v = 0.f;
-      // rotated column order: lanes with different r1 hit different banks
+    // D0(slot) (P0 x R1) = S (P0 x C1) · G1[i1]ᵀ: item (slot, a, 4 r1) over c
+    {
+      constexpr int R4 = D::R1 / 4;
+      for (int q = tid; q < nslots * D::P0 * R4; q += kThreads) {
+        const int sa = q / R4, r4 = q - sa * R4;
+        const float* srow = S + (sa / D::P0) * D::W1 + (sa % D::P0) * D::C1;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-      for (int k = 0; k < D::C1; ++k) {
-        const int c = (k + r1) & (D::C1 - 1);
-        v = __fmaf_rn(srow[c], grow[c], v);
+        for (int c = 0; c < D::C1; ++c) {
+          const float sv = srow[c];
+          const float4 gt = reinterpret_cast<const float4*>(G1t + c * SM::R1P)[r4];
+          v.x = __fmaf_rn(sv, gt.x, v.x);
+          v.y = __fmaf_rn(sv, gt.y, v.y);
+          v.z = __fmaf_rn(sv, gt.z, v.z);
+          v.w = __fmaf_rn(sv, gt.w, v.w);
+        }
+        reinterpret_cast<float4*>(d0tmp + sa * D::R1)[r4] = v;
       }
-      d0tmp[q] = v;
     }
     __syncthreads();
     // batched read-modify-write of this CTA's private D0 accumulator
@@ -729,20 +778,19 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
     }
     __syncthreads();
     if (last) {
-      const int e0 = tid * PER;
-      if (e0 < D::S1) {
-        float* dst = part1 + static_cast<int64_t>(run_start) * D::S1 + e0;
 #pragma unroll
-        for (int x = 0; x < PER; ++x) {
-          dst[x] = acc1[x];
-          acc1[x] = 0.f;
+      for (int x = 0; x < PER1; ++x) {
+        const int item = tid + x * kThreads;
+        if (item < ITEMS1) {
+          reinterpret_cast<float4*>(part1 + static_cast<int64_t>(run_start) * D::S1)[item] = acc1[x];
+          acc1[x] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
       const unsigned long long tm = *tmask;
       for (int e = tid; e < p2sz; e += kThreads) {
         const int j = e / D::S2;
-        if ((tm >> j) & 1ull) part2[static_cast<int64_t>(run_start) * p2sz + e] = Bq[e];
-        Bq[e] = 0.f;
+        if ((tm >> j) & 1ull) part2[static_cast<int64_t>(run_start) * p2sz + e] = P2[e];
+        P2[e] = 0.f;
       }
       __syncthreads();
       if (tid == 0) {
@@ -757,29 +805,58 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
 
 // ---------------------------------------------------------- f3_combine ---
 // Fixed-order list reductions.  One CTA per (output slice, 128-column chunk):
-// 8 warps take candidate list positions w, w+8, ...; lanes own float4
-// columns; the warp sums are folded in warp order.  Roles by blockIdx:
+// warp w scans candidate chunks of 32 (w, w+8, ...), ballots the live
+// candidates, and sums their rows 4 loads at a time (lanes own float4
+// columns); warp sums are folded in warp order.  Roles by blockIdx:
 //   [0, m1*C1c)            dG1[i1]   candidates: tiles of buckets (blk, i1), has1
 //   [.., + m2*C2c)         dG2[i2]   candidates: tiles of blk(i2) buckets, mask2 bit
 //   [.., + m0*C0c)         dG0[i0]   candidates: bwd CTAs, d0mask
 // MODE 0 writes dense gradients (zeros if untouched), 1 applies SGD in place.
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// Sum rows row_of(k) (float4 column col4) over the set bits k of `live`
+// (relative to cand0), 4 independent loads in flight.
+template <class RowFn>
+__device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, bool colok, RowFn row_of,
+                                         float4& acc) {
+  while (live) {
+    int idx[4];
+    int n = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      idx[u] = -1;
+      if (live) {
+        idx[u] = cand0 + __ffs(live) - 1;
+        live &= live - 1;
+        ++n;
+      }
+    }
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = (idx[u] >= 0 && colok) ? __ldg(reinterpret_cast<const float4*>(row_of(idx[u])) + col4)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) add4(acc, v[u]);
+  }
+}
+
 template <int W>
-__device__ __forceinline__ void fold_store(float4 v, bool touched, float* red, float* out_core,
+__device__ __forceinline__ void fold_store(float4 v, bool touched, float4* red, float* out_core,
                                            float* out_grad, int col4, int mode, float lr,
                                            int* touched_sm) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  reinterpret_cast<float4*>(red)[wid * 32 + lane] = v;
+  red[wid * 32 + lane] = v;
   if (touched) atomicOr(touched_sm, 1);
   __syncthreads();
   if (wid == 0 && col4 < W / 4) {
-    float4 s = reinterpret_cast<float4*>(red)[lane];
-    for (int w = 1; w < kThreads / 32; ++w) {
-      const float4 q = reinterpret_cast<float4*>(red)[w * 32 + lane];
-      s.x += q.x;
-      s.y += q.y;
-      s.z += q.z;
-      s.w += q.w;
-    }
+    float4 s = red[lane];
+    for (int w = 1; w < kThreads / 32; ++w) add4(s, red[w * 32 + lane]);
     if (mode == 0) {
       reinterpret_cast<float4*>(out_grad)[col4] = s;
     } else if (*touched_sm) {
@@ -793,13 +870,6 @@ __device__ __forceinline__ void fold_store(float4 v, bool touched, float* red, f
   }
 }
 
-__device__ __forceinline__ void add4(float4& a, const float4 b) {
-  a.x += b.x;
-  a.y += b.y;
-  a.z += b.z;
-  a.w += b.w;
-}
-
 template <class D, int MODE>
 __global__ void __launch_bounds__(kThreads) f3_combine(
     Geo g, float* __restrict__ cores, float* __restrict__ grads, const int* __restrict__ ntiles,
@@ -807,34 +877,32 @@ __global__ void __launch_bounds__(kThreads) f3_combine(
     const int* __restrict__ has1, const float* __restrict__ part2,
     const unsigned long long* __restrict__ mask2, const float* __restrict__ D0acc,
     const unsigned char* __restrict__ d0mask, int nbwd, float lr) {
-  __shared__ __align__(16) float red[kThreads * 4];
+  __shared__ float4 red[kThreads];
   __shared__ int touched_sm;
+  constexpr int NW = kThreads / 32;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
   if (threadIdx.x == 0) touched_sm = 0;
   __syncthreads();
   int bid = blockIdx.x;
-  float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool touched = false;
   if (bid < g.m1 * C1c) {
     const int i1 = bid / C1c, ch = bid - i1 * C1c;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S1 / 4;
-    float4 a0 = z, a1 = z;
-    bool touched = false;
+    auto row = [&](int t) { return part1 + static_cast<int64_t>(t) * D::S1; };
     for (int b = 0; b < g.nblk; ++b) {
       const int key = b * g.m1 + i1;
       const int t0 = tile_base[key], t1 = tile_base[key + 1];
-      // warp w takes the tiles with t % 8 == w (a fixed, input-determined split)
-      for (int t = t0 + ((wid - t0) % 8 + 8) % 8; t < t1; t += 8) {
-        if (has1[t]) {
-          touched = true;
-          if (colok) add4((t & 8) ? a1 : a0,
-                          reinterpret_cast<const float4*>(part1 + static_cast<int64_t>(t) * D::S1)[col4]);
-        }
+      for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
+        const int t = c0 + lane;
+        const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has1[t] != 0);
+        touched |= live != 0;
+        sum_live(live, c0, col4, colok, row, acc);
       }
     }
-    add4(a0, a1);
-    fold_store<D::S1>(a0, touched, red, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
+    fold_store<D::S1>(acc, touched, red, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
                       grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, col4, MODE, lr,
                       &touched_sm);
     return;
@@ -846,19 +914,15 @@ __global__ void __launch_bounds__(kThreads) f3_combine(
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S2 / 4;
     const int t0 = tile_base[b * g.m1], t1 = tile_base[b * g.m1 + g.m1];
-    float4 a0 = z, a1 = z;
-    bool touched = false;
     const int p2sz = g.blk * D::S2;
-    for (int t = t0 + wid; t < t1; t += 8) {
-      if ((mask2[t] >> j) & 1ull) {
-        touched = true;
-        if (colok)
-          add4(((t - t0) & 8) ? a1 : a0,
-               reinterpret_cast<const float4*>(part2 + static_cast<int64_t>(t) * p2sz + j * D::S2)[col4]);
-      }
+    auto row = [&](int t) { return part2 + static_cast<int64_t>(t) * p2sz + j * D::S2; };
+    for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
+      const int t = c0 + lane;
+      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && ((mask2[t] >> j) & 1ull));
+      touched |= live != 0;
+      sum_live(live, c0, col4, colok, row, acc);
     }
-    add4(a0, a1);
-    fold_store<D::S2>(a0, touched, red, cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
+    fold_store<D::S2>(acc, touched, red, cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
                       grads + g.coff2 + static_cast<int64_t>(i2) * D::S2, col4, MODE, lr,
                       &touched_sm);
     return;
@@ -868,18 +932,15 @@ __global__ void __launch_bounds__(kThreads) f3_combine(
   if (i0 >= g.m0) return;
   const int col4 = ch * 32 + lane;
   const bool colok = col4 < D::S0 / 4;
-  float4 a0 = z, a1 = z;
-  bool touched = false;
-  for (int c = wid; c < nbwd; c += 8) {
-    if (d0mask[static_cast<int64_t>(c) * g.m0 + i0]) {
-      touched = true;
-      if (colok)
-        add4((c & 8) ? a1 : a0,
-             reinterpret_cast<const float4*>(D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0)[col4]);
-    }
+  auto row = [&](int c) { return D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0; };
+  for (int c0 = wid * 32; c0 < nbwd; c0 += NW * 32) {
+    const int c = c0 + lane;
+    const unsigned live =
+        __ballot_sync(0xffffffffu, c < nbwd && d0mask[static_cast<int64_t>(c) * g.m0 + i0] != 0);
+    touched |= live != 0;
+    sum_live(live, c0, col4, colok, row, acc);
   }
-  add4(a0, a1);
-  fold_store<D::S0>(a0, touched, red, cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
+  fold_store<D::S0>(acc, touched, red, cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
                     grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, col4, MODE, lr,
                     &touched_sm);
 }

@@ -90,7 +90,7 @@ struct F3Runner {
     }
     t->mark("hist");
     {
-      const size_t sm = 4 * static_cast<size_t>(g.K) * NT;
+      const size_t sm = 4 * (static_cast<size_t>(g.K) * NT + g.K + 1);
       set_smem(f3::f3_scan, sm);
       f3::f3_scan<<<1, 1024, sm, st>>>(g, NT, D::TT, L, f.hist.as<uint32_t>(),
                                        f.tile_base.as<int32_t>(), f.tiles.as<f3::Tile>(),
