@@ -1,18 +1,18 @@
 // Fast path for 3-core tables (every BASELINE config): compile-time TT shape,
-// 7 kernels per fwd+bwd+SGD step, deterministic, no floating-point atomics.
+// 8 kernels per fwd+bwd+SGD step, deterministic, no floating-point atomics.
 //
-//   f3_hist    decode + validate + per-CTA histogram of the tile key
-//              key = (i2 / BLK) * m1 + i1, lookup->bag map and backward alpha
-//   f3_scan    one CTA: exclusive scan of the (key, CTA) histogram, bucket
-//              tile list (buckets cut into tiles of <= TT lookups)
-//   f3_scatter stable counting-sort scatter (warp match_any ranks)
-//   f3_fwd     per tile: G1[i1] staged in smem once, tile-local dedup of i0
-//              ("slots"), H(slot) = G0[i0]·G1[i1], y = H·G2[i2] per lookup
-//   f3_pool    per bag, lookup order: out = Σ T(w)·y (Mean rescale)
-//   f3_bwd     per tile: dG2 partial (BLK i2 slices in smem), S(slot) = Σ D1,
-//              dG1 partial = Σ G0ᵀ S, D0(slot) = S·G1ᵀ
-//   f3_combine fixed-order folds of the tile partials per core slice, fused
-//              with the SGD update (or a dense gradient write)
+//   f3_hist     decode + validate; per-CTA histograms of two sort keys
+//               (k1 = i1, k2 = i2); lookup->bag map and backward alpha
+//   f3_scan     2 CTAs (one per key): exclusive scan of the (key, CTA)
+//               histogram; tile lists (each key bucket cut into tiles)
+//   f3_scatter  stable counting-sort scatter of both keys (warp match_any)
+//   f3_fwd      per i1-tile: G1[i1] staged in smem by TMA once; tile-local
+//               dedup of i0 ("slots"); H(slot) = G0[i0]·G1[i1]; y = H·G2[i2]
+//   f3_pool     per bag, lookup order: out = Σ T(w)·y (Mean rescale)
+//   f3_bwd1     per i1-tile: S(slot) = Σ D1, dG1 += Σ G0ᵀS, D0(slot) = S·G1ᵀ
+//   f3_bwd2     per i2-tile: dG2 += Σ H(lookup)ᵀ D2 (H rows saved by f3_fwd)
+//   f3_combine  fixed-order folds of the partials per core slice, fused with
+//               the SGD update (or a dense gradient write)
 //
 // Reference semantics: embedding_ops.hpp:159-376.  In exact mode the forward
 // keeps the reference's per-element operation order (separately rounded
@@ -29,10 +29,7 @@ namespace f3 {
 
 struct Geo {
   int m0, m1, m2;
-  uint32_t m12;   // m1 * m2
-  int blk;        // i2 block size (<= 64)
-  int nblk;       // ceil(m2 / blk)
-  int K;          // nblk * m1 tile keys
+  uint32_t m12;  // m1 * m2
   int64_t num_rows;
   int64_t coff0, coff1, coff2;
 };
@@ -46,13 +43,10 @@ struct Dims {
   static constexpr int P0 = P0_, R1 = R1_, N1 = N1_, R2 = R2_, N2 = N2_, TT = TT_;
   static constexpr int C1 = N1 * R2, S0 = P0 * R1, S1 = R1 * C1, P1 = P0 * N1;
   static constexpr int W1 = P1 * R2, S2 = R2 * N2, N = P1 * N2, C4 = C1 / 4;
-  static constexpr int W1P = W1 + 1;  // odd slot strides: conflict-free across slots
-  static constexpr int S0P = S0 + 1;
-  static constexpr int S2P = S2 + 4;  // 16 B pad: float4 rows land in distinct bank groups
-  static constexpr int C1P = C1 + 1;
+  static constexpr int TT2 = 64;  // lookups per i2-tile (f3_bwd2)
   static_assert(N2 == 4, "fast path expects n_2 == 4 (float4 rows)");
-  static_assert(C1 % 4 == 0, "C1 must be a multiple of 4");
-  static_assert((C1 & (C1 - 1)) == 0, "C1 must be a power of two (rotated D0 reads)");
+  static_assert(C1 % 4 == 0 && R1 % 4 == 0, "C1 and R1 must be multiples of 4");
+  static_assert(TT <= 256, "tile must fit one lookup per thread");
 };
 
 constexpr int kThreads = 256;
@@ -64,6 +58,13 @@ __device__ __forceinline__ float4 madd4(float a, float4 b, float4 acc) {
   acc.z = madd<float, kExact>(a, b.z, acc.z);
   acc.w = madd<float, kExact>(a, b.w, acc.w);
   return acc;
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
 }
 
 // ---- TMA bulk copies (cp.async.bulk, sm_90+/sm_100a) with mbarrier completion
@@ -133,19 +134,38 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total, int* sm /* >= 
   return r;
 }
 
+// Copy `n` floats (element e at dst[e]) whose source is src_of(e); U loads in flight.
+template <int U, class SrcFn>
+__device__ __forceinline__ void gather_to_smem(float* dst, int n, SrcFn src_of) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += kThreads * U) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      v[u] = e < n ? __ldg(src_of(e)) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * kThreads < n) dst[e0 + u * kThreads] = v[u];
+  }
+}
+
 // ------------------------------------------------------------- f3_hist ---
-// TL = 512 * LPT lookups per CTA (LPT lookups per thread, loads batched).
+// 512 * LPT lookups per CTA (LPT lookups per thread, loads batched).
 template <typename T, int LPT>
 __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict__ idx, int64_t L,
                                                int NT, const int64_t* __restrict__ off,
                                                int64_t B, const double* __restrict__ w, int mean,
-                                               uint32_t* __restrict__ key, uint16_t* __restrict__ d0,
+                                               uint16_t* __restrict__ d0, uint16_t* __restrict__ d1,
                                                uint16_t* __restrict__ d2, int32_t* __restrict__ lk_bag,
-                                               T* __restrict__ alpha, uint32_t* __restrict__ hist,
+                                               T* __restrict__ alpha, uint32_t* __restrict__ hist1,
+                                               uint32_t* __restrict__ hist2,
                                                unsigned long long* __restrict__ bad,
                                                int* __restrict__ errs) {
-  extern __shared__ uint32_t shist[];
-  for (int k = threadIdx.x; k < g.K; k += blockDim.x) shist[k] = 0;
+  extern __shared__ uint32_t shist[];  // m1 + m2
+  uint32_t* sh1 = shist;
+  uint32_t* sh2 = shist + g.m1;
+  for (int k = threadIdx.x; k < g.m1 + g.m2; k += blockDim.x) shist[k] = 0;
   __syncthreads();
   const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -160,7 +180,7 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       const int64_t l = base + q * 512;
-      uint32_t k = 0xffffffffu;
+      uint32_t k1 = 0xffffffffu, k2 = 0xffffffffu;
       if (l < L) {
         int64_t row = rows[q];
         if (row < 0 || row >= g.num_rows) {
@@ -172,19 +192,23 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
         const uint32_t rem = r - i0 * g.m12;
         const uint32_t i1 = rem / static_cast<uint32_t>(g.m2);
         const uint32_t i2 = rem - i1 * static_cast<uint32_t>(g.m2);
-        k = (i2 / static_cast<uint32_t>(g.blk)) * static_cast<uint32_t>(g.m1) + i1;
-        key[l] = k;
         d0[l] = static_cast<uint16_t>(i0);
+        d1[l] = static_cast<uint16_t>(i1);
         d2[l] = static_cast<uint16_t>(i2);
+        k1 = i1;
+        k2 = i2;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, k);
-      if (k != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&shist[k], __popc(peers));
+      unsigned peers = __match_any_sync(0xffffffffu, k1);
+      if (k1 != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&sh1[k1], __popc(peers));
+      peers = __match_any_sync(0xffffffffu, k2);
+      if (k2 != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&sh2[k2], __popc(peers));
     }
   }
   __syncthreads();
-  if (tile < NT)
-    for (int k = threadIdx.x; k < g.K; k += blockDim.x)
-      hist[static_cast<int64_t>(k) * NT + tile] = shist[k];
+  if (tile < NT) {
+    for (int k = threadIdx.x; k < g.m1; k += blockDim.x) hist1[static_cast<int64_t>(k) * NT + tile] = sh1[k];
+    for (int k = threadIdx.x; k < g.m2; k += blockDim.x) hist2[static_cast<int64_t>(k) * NT + tile] = sh2[k];
+  }
   // bags (grid-stride over all CTAs): offsets checks, lookup->bag, backward alpha
   for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < B;
        b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -204,20 +228,28 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
 }
 
 // ------------------------------------------------------------- f3_scan ---
-// One CTA of 1024 threads; the (K x NT, key-major) histogram is staged in
-// shared memory with coalesced loads, scanned there, and written back as
-// exclusive offsets.  Also emits the tile list (buckets cut into <= TT).
-__global__ void __launch_bounds__(1024) f3_scan(Geo g, int NT, int TT, int64_t L,
-                                                uint32_t* __restrict__ hist,
-                                                int32_t* __restrict__ tile_base,
-                                                Tile* __restrict__ tiles, int* __restrict__ ntiles) {
+// CTA 0 handles key 1 (K = m1), CTA 1 key 2 (K = m2).  The (K x NT,
+// key-major) histogram is staged in smem, scanned there and written back as
+// exclusive offsets; each bucket is cut into tiles of <= TT lookups, one
+// thread per tile finding its bucket by binary search.
+struct ScanArgs {
+  uint32_t* hist;
+  int32_t* tile_base;  // K + 1
+  Tile* tiles;
+  int* ntiles;
+  int K, TT;
+};
+
+__global__ void __launch_bounds__(1024) f3_scan(ScanArgs a1, ScanArgs a2, int NT, int64_t L) {
   using Scan = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
-  extern __shared__ uint32_t sh[];  // n entries
-  const int n = g.K * NT;
+  extern __shared__ uint32_t sh[];
+  const ScanArgs& A = blockIdx.x == 0 ? a1 : a2;
+  const int K = A.K, TT = A.TT;
+  const int n = K * NT;
   const int tid = threadIdx.x;
 #pragma unroll 8
-  for (int i = tid; i < n; i += 1024) sh[i] = hist[i];
+  for (int i = tid; i < n; i += 1024) sh[i] = A.hist[i];
   __syncthreads();
   const int per = (n + 1023) / 1024;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
@@ -232,14 +264,13 @@ __global__ void __launch_bounds__(1024) f3_scan(Geo g, int NT, int TT, int64_t L
   }
   __syncthreads();
 #pragma unroll 8
-  for (int i = tid; i < n; i += 1024) hist[i] = sh[i];
-  // tiles per bucket
-  const int perk = (g.K + 1023) / 1024;
-  const int klo = min(g.K, tid * perk), khi = min(g.K, klo + perk);
+  for (int i = tid; i < n; i += 1024) A.hist[i] = sh[i];
+  const int perk = (K + 1023) / 1024;
+  const int klo = min(K, tid * perk), khi = min(K, klo + perk);
   uint32_t nt = 0;
   for (int k = klo; k < khi; ++k) {
     const uint32_t bs = sh[k * NT];
-    const uint32_t be = k + 1 < g.K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t be = k + 1 < K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
     nt += (be - bs + TT - 1) / TT;
   }
   uint32_t tex;
@@ -248,49 +279,47 @@ __global__ void __launch_bounds__(1024) f3_scan(Geo g, int NT, int TT, int64_t L
   uint32_t* tb = sh + n;  // K + 1 tile bases
   for (int k = klo; k < khi; ++k) {
     const uint32_t bs = sh[k * NT];
-    const uint32_t be = k + 1 < g.K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t be = k + 1 < K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
     tb[k] = tex;
-    tile_base[k] = static_cast<int32_t>(tex);
+    A.tile_base[k] = static_cast<int32_t>(tex);
     tex += (be - bs + TT - 1) / TT;
   }
   if (tid == 1023) {
-    tb[g.K] = tex;
-    tile_base[g.K] = static_cast<int32_t>(tex);
-    *ntiles = static_cast<int>(tex);
+    tb[K] = tex;
+    A.tile_base[K] = static_cast<int32_t>(tex);
+    *A.ntiles = static_cast<int>(tex);
   }
   __syncthreads();
-  // one thread per tile: find its bucket by binary search over the tile bases
-  const uint32_t total = tb[g.K];
+  const uint32_t total = tb[K];
   for (uint32_t t = tid; t < total; t += 1024) {
-    int lo = 0, hi = g.K;  // invariant: tb[lo] <= t < tb[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (tb[mid] <= t) lo = mid; else hi = mid;
+    int lo2 = 0, hi2 = K;  // invariant: tb[lo2] <= t < tb[hi2]
+    while (hi2 - lo2 > 1) {
+      const int mid = (lo2 + hi2) >> 1;
+      if (tb[mid] <= t) lo2 = mid; else hi2 = mid;
     }
-    const uint32_t bs = sh[lo * NT];
-    const uint32_t be = lo + 1 < g.K ? sh[(lo + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t bs = sh[lo2 * NT];
+    const uint32_t be = lo2 + 1 < K ? sh[(lo2 + 1) * NT] : static_cast<uint32_t>(L);
     Tile tl;
-    tl.key = lo;
-    tl.start = static_cast<int>(bs + (t - tb[lo]) * TT);
-    tl.end = static_cast<int>(min(be, bs + (t - tb[lo] + 1) * TT));
+    tl.key = lo2;
+    tl.start = static_cast<int>(bs + (t - tb[lo2]) * TT);
+    tl.end = static_cast<int>(min(be, bs + (t - tb[lo2] + 1) * TT));
     tl.pad = 0;
-    tiles[t] = tl;
+    A.tiles[t] = tl;
   }
 }
 
 // ---------------------------------------------------------- f3_scatter ---
-// Stable scatter: 8 warps per CTA, each owning TL/8 consecutive lookups,
-// keys loaded 8 rounds at a time.
-__global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restrict__ key, int64_t L,
-                                                  int TL, int NT, const uint32_t* __restrict__ hoff,
-                                                  uint32_t* __restrict__ perm) {
-  extern __shared__ uint32_t wc[];  // 8 x K
+// Stable scatter of one key: 8 warps per CTA, each owning TL/8 consecutive
+// lookups, keys loaded 8 rounds at a time.  Run for key 1 then key 2.
+__device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, int K, int64_t L,
+                                            int TL, int NT, const uint32_t* __restrict__ hoff,
+                                            uint32_t* __restrict__ perm, uint32_t* wc) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int per = TL / 8;
   const int64_t base = static_cast<int64_t>(tile) * TL + static_cast<int64_t>(wid) * per;
-  uint32_t* my = wc + static_cast<int64_t>(wid) * g.K;
-  for (int k = lane; k < g.K; k += 32) my[k] = 0;
+  uint32_t* my = wc + static_cast<int64_t>(wid) * K;
+  for (int k = lane; k < K; k += 32) my[k] = 0;
   __syncwarp();
   for (int r0 = 0; r0 < per; r0 += 256) {
     uint32_t ks[8];
@@ -308,12 +337,12 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restr
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < g.K; k += blockDim.x) {
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
     uint32_t run = hoff[static_cast<int64_t>(k) * NT + tile];
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      const uint32_t c = wc[static_cast<int64_t>(w) * g.K + k];
-      wc[static_cast<int64_t>(w) * g.K + k] = run;
+      const uint32_t c = wc[static_cast<int64_t>(w) * K + k];
+      wc[static_cast<int64_t>(w) * K + k] = run;
       run += c;
     }
   }
@@ -341,9 +370,21 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint32_t* __restr
       __syncwarp();
     }
   }
+  __syncthreads();
 }
 
-// --------------------------------------------------------- smem layouts ---
+__global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restrict__ d1,
+                                                  const uint16_t* __restrict__ d2, int64_t L,
+                                                  int TL, int NT, const uint32_t* __restrict__ hoff1,
+                                                  const uint32_t* __restrict__ hoff2,
+                                                  uint32_t* __restrict__ perm1,
+                                                  uint32_t* __restrict__ perm2) {
+  extern __shared__ uint32_t wc[];  // 8 x max(m1, m2)
+  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc);
+  scatter_one(d2, g.m2, L, TL, NT, hoff2, perm2, wc);
+}
+
+// ------------------------------------------------------------- f3_fwd ----
 template <class D>
 struct FwdSmem {
   // floats: G1s[S1] (TMA) | Hs[TT*W1P] | G0s[TT*S0] ; then mbarrier + ints
@@ -357,10 +398,10 @@ struct FwdSmem {
   }
 };
 
-// ------------------------------------------------------------- f3_fwd ----
-// Per tile: TMA G1[i1] (issued first, overlaps the index gathers); dedup i0
-// -> slots (ascending i0, the numbering backward reuses); H(slot) = G0·G1
-// with G1 from smem; y = H·G2[i2] per lookup (G2 rows straight from L1/L2).
+// Per i1-tile: TMA G1[i1] (issued first, overlaps the index gathers); dedup
+// i0 -> slots (numbered by ascending i0; backward reuses the numbering);
+// H(slot) = G0·G1; y = H·G2[i2] per lookup.  Saves H rows and, per lookup,
+// the H row index (hloc) for f3_bwd2.
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
@@ -369,6 +410,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    const uint16_t* __restrict__ d0,
                                                    const uint16_t* __restrict__ d2,
                                                    float* __restrict__ Hbuf, float* __restrict__ y,
+                                                   uint32_t* __restrict__ hloc,
                                                    uint16_t* __restrict__ slot_of_pos,
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots) {
@@ -396,7 +438,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < nt; t += gridDim.x, phase ^= 1u) {
     const Tile tl = tiles[t];
-    const int i1 = tl.key % g.m1;
+    const int i1 = tl.key;
     const int ntl = tl.end - tl.start;
     if (tid == 0) {
       // smem last touched by generic-proxy accesses; order them before the TMA write
@@ -433,28 +475,14 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
       const int s = flags[lk_i0[tid]];
       lk_slot[tid] = s;
       slot_of_pos[tl.start + tid] = static_cast<uint16_t>(s);
+      hloc[lk_l[tid]] = static_cast<uint32_t>(tl.start + s);
     }
     if (tid < nslots) tile_i0[tl.start + tid] = static_cast<uint16_t>(slot_i0[tid]);
     if (tid == 0) tile_nslots[t] = nslots;
-    // G0 rows of the slots (independent loads, batched)
-    {
-      constexpr int U = 8;
-      for (int e0 = tid; e0 < nslots * D::S0; e0 += kThreads * U) {
-        float v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * kThreads;
-          v[u] = 0.f;
-          if (e < nslots * D::S0) {
-            const int s = e / D::S0;
-            v[u] = __ldg(G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (e0 + u * kThreads < nslots * D::S0) G0s[e0 + u * kThreads] = v[u];
-      }
-    }
+    gather_to_smem<8>(G0s, nslots * D::S0, [&](int e) {
+      const int s = e / D::S0;
+      return G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0);
+    });
     __syncthreads();
     if (tid < nslots) flags[slot_i0[tid]] = 0;  // ready for the next tile
     mbar_wait(bar, phase);
@@ -527,57 +555,50 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
   }
 }
 
-// -------------------------------------------------------------- f3_bwd ---
+// ------------------------------------------------------------ f3_bwd1 ----
 template <class D>
-struct BwdSmem {
-  // floats: G1t[C1*R1P] (G1 slice transposed) | S[TT*W1] | P2[BLK*S2] | G0s[TT*S0]
-  //         | d0tmp[TT*S0] ; then u64 mask + ints
+struct Bwd1Smem {
+  // floats: G1t[C1*R1P] (G1 slice transposed) | S[TT*W1] | G2s[TT*S2] | D2s[TT*N]
+  //         | G0s[TT*S0] | d0tmp[TT*S0] ; then ints
   static constexpr int R1P = D::R1 + 4;
-  static __host__ __device__ size_t floats(int blk) {
-    size_t f = static_cast<size_t>(D::C1) * R1P + static_cast<size_t>(D::TT) * D::W1 +
-               static_cast<size_t>(blk) * D::S2 + 2 * static_cast<size_t>(D::TT) * D::S0;
+  static __host__ __device__ size_t floats() {
+    size_t f = static_cast<size_t>(D::C1) * R1P +
+               static_cast<size_t>(D::TT) * (D::W1 + D::S2 + D::N + 2 * D::S0);
     return (f + 3) / 4 * 4;
   }
-  static __host__ __device__ size_t bytes(int m0, int blk) {
-    (void)m0;
-    return floats(blk) * 4 + 16 + sizeof(int) * (5 * static_cast<size_t>(D::TT) + 8);
+  static __host__ __device__ size_t bytes() {
+    return floats() * 4 + sizeof(int) * (3 * static_cast<size_t>(D::TT) + 8);
   }
 };
 
-// Each CTA owns a contiguous range of tiles.  Consecutive tiles of the same
-// bucket keep accumulating the dG1 partial (registers) and the dG2 partial
-// (smem); one partial per (CTA, bucket run) is flushed, stored at the run's
-// first tile (has1 / mask2 mark it).  D0 accumulates per (CTA, i0) in a
-// CTA-private global block.  Within a tile, warp w owns the dG2 slices
-// j = w (mod 8) and the slots s = w (mod 8): each warp walks the tile's
-// lookups in order and updates only what it owns, so every accumulation
-// happens in one fixed order (deterministic) with no atomics.
+// Each CTA owns a contiguous range of i1-tiles.  Consecutive tiles of the
+// same i1 keep accumulating the dG1 partial in registers; one partial per
+// (CTA, i1 run) is flushed at the run's first tile (has1 marks it).  D0
+// accumulates per (CTA, i0) in a CTA-private global block.  In the S phase
+// warp w owns the (slot, 32-column chunk) pairs o = w, w+8, ... and walks the
+// tile's lookups in order: a fixed accumulation order, no atomics.
 template <class D>
-__global__ void __launch_bounds__(kThreads) f3_bwd(
+__global__ void __launch_bounds__(kThreads) f3_bwd1(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
     const int* __restrict__ ntiles, const uint32_t* __restrict__ perm,
     const uint16_t* __restrict__ d2, const int32_t* __restrict__ lk_bag,
     const float* __restrict__ alpha, const float* __restrict__ grad,
-    const float* __restrict__ Hbuf, const uint16_t* __restrict__ slot_of_pos,
-    const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
-    float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ part2,
-    unsigned long long* __restrict__ mask2, float* __restrict__ D0acc,
-    unsigned char* __restrict__ d0mask) {
-  using SM = BwdSmem<D>;
+    const uint16_t* __restrict__ slot_of_pos, const uint16_t* __restrict__ tile_i0,
+    const int* __restrict__ tile_nslots, float* __restrict__ part1, int* __restrict__ has1,
+    float* __restrict__ D0acc, unsigned char* __restrict__ d0mask) {
+  using SM = Bwd1Smem<D>;
   constexpr int NW = kThreads / 32;
+  constexpr int CH = (D::R2 + 31) / 32;  // 32-column chunks per (slot, row)
   extern __shared__ __align__(128) float sm[];
   float* G1t = sm;                                   // C1 x R1P
   float* S = G1t + D::C1 * SM::R1P;                  // TT x W1
-  float* P2 = S + D::TT * D::W1;                     // BLK x S2
-  const int p2sz = g.blk * D::S2;
-  float* G0s = P2 + p2sz;                            // TT x S0
+  float* G2s = S + D::TT * D::W1;                    // TT x S2
+  float* D2s = G2s + D::TT * D::S2;                  // TT x N (alpha * grad rows)
+  float* G0s = D2s + D::TT * D::N;                   // TT x S0
   float* d0tmp = G0s + D::TT * D::S0;                // TT x S0
-  unsigned long long* tmask = reinterpret_cast<unsigned long long*>(sm + SM::floats(g.blk));
-  int* lk_slot = reinterpret_cast<int*>(tmask + 1);
+  int* lk_slot = reinterpret_cast<int*>(sm + SM::floats());
   int* lk_i2 = lk_slot + D::TT;
-  int* lk_bg = lk_i2 + D::TT;
-  float* lk_al = reinterpret_cast<float*>(lk_bg + D::TT);
-  int* slot_i0 = reinterpret_cast<int*>(lk_al + D::TT);
+  int* slot_i0 = lk_i2 + D::TT;
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
@@ -589,36 +610,59 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0 * D::S0; e += kThreads) d0acc[e] = 0.f;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
-  // dG1 partial: thread owns (r1, 4 consecutive columns) items, float4 each
   constexpr int ITEMS1 = D::R1 * D::C4;
   constexpr int PER1 = (ITEMS1 + kThreads - 1) / kThreads;
   float4 acc1[PER1];
 #pragma unroll
   for (int x = 0; x < PER1; ++x) acc1[x] = make_float4(0.f, 0.f, 0.f, 0.f);
   int run_start = t_lo;
-  for (int e = tid; e < p2sz; e += kThreads) P2[e] = 0.f;
-  if (tid == 0) *tmask = 0ull;
-  __syncthreads();
   for (int t = t_lo; t < t_hi; ++t) {
     const Tile tl = tiles[t];
-    const int i1 = tl.key % g.m1;
-    const int i2base = (tl.key / g.m1) * g.blk;
+    const int i1 = tl.key;
     const int ntl = tl.end - tl.start;
     const int nslots = tile_nslots[t];
+    int my_l = 0;
     if (tid < ntl) {
-      const int l = static_cast<int>(perm[tl.start + tid]);
+      my_l = static_cast<int>(perm[tl.start + tid]);
       lk_slot[tid] = slot_of_pos[tl.start + tid];
-      const int i2 = d2[l];
-      lk_i2[tid] = i2;
-      lk_bg[tid] = lk_bag[l];
-      lk_al[tid] = alpha[l];
-      atomicOr(tmask, 1ull << (i2 - i2base));
+      lk_i2[tid] = d2[my_l];
     }
     if (tid < nslots) slot_i0[tid] = tile_i0[tl.start + tid];
-    // G1[i1] transposed into smem (c-major, padded rows): coalesced, batched loads
+    __syncthreads();  // also: the previous tile's smem reads are done
+    // stage: D2 = alpha * grad rows, G2 slices, G1 transposed, G0 rows
+    if (tid < ntl) {
+      const float al = alpha[my_l];
+      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bag[my_l]) * D::N);
+      float4 gv[D::N / 4];
+#pragma unroll
+      for (int q = 0; q < D::N / 4; ++q) gv[q] = __ldg(grow + q);
+#pragma unroll
+      for (int q = 0; q < D::N / 4; ++q)
+        reinterpret_cast<float4*>(D2s + tid * D::N)[q] =
+            make_float4(__fmul_rn(al, gv[q].x), __fmul_rn(al, gv[q].y), __fmul_rn(al, gv[q].z),
+                        __fmul_rn(al, gv[q].w));
+    }
     {
-      constexpr int U = (D::S1 / kThreads) > 8 ? 8 : (D::S1 / kThreads > 0 ? D::S1 / kThreads : 1);
+      constexpr int Q = D::S2 / 4;
+      for (int e0 = tid; e0 < ntl * Q; e0 += kThreads * 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * kThreads;
+          if (e < ntl * Q) {
+            const int i = e / Q;
+            v[u] = __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2) +
+                         (e - i * Q));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * kThreads < ntl * Q) reinterpret_cast<float4*>(G2s)[e0 + u * kThreads] = v[u];
+      }
+    }
+    {
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
+      constexpr int U = 8;
       for (int e0 = tid; e0 < D::S1; e0 += kThreads * U) {
         float v[U];
 #pragma unroll
@@ -633,79 +677,38 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
         }
       }
     }
+    gather_to_smem<8>(G0s, nslots * D::S0, [&](int e) {
+      const int s = e / D::S0;
+      return G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0);
+    });
     __syncthreads();
-    {
-      constexpr int U = 8;
-      for (int e0 = tid; e0 < nslots * D::S0; e0 += kThreads * U) {
-        float v[U];
+    // S(slot) = Σ_lookups D1, D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2): warp owns
+    // (slot, chunk) pairs; lane owns the rank column r; rows a in registers
+    for (int o = wid; o < nslots * CH; o += NW) {
+      const int s = o / CH, r = (o - s * CH) * 32 + lane;
+      float acc[D::P1];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * kThreads;
-          v[u] = 0.f;
-          if (e < nslots * D::S0) {
-            const int s = e / D::S0;
-            v[u] = __ldg(G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (e0 + u * kThreads < nslots * D::S0) G0s[e0 + u * kThreads] = v[u];
-      }
-    }
-    for (int e = tid; e < nslots * D::W1; e += kThreads) S[e] = 0.f;
-    __syncthreads();
-    // dG2 (warp owns slices j = w mod NW) and S (warp owns slots s = w mod NW);
-    // lane owns rank column r.  D2 = alpha * grad row, recomputed per use.
-    for (int i = 0; i < ntl; ++i) {
-      const int j = lk_i2[i] - i2base;
-      const int s = lk_slot[i];
-      const bool own_j = (j % NW) == wid, own_s = (s % NW) == wid;
-      if (!own_j && !own_s) continue;
-      const float al = lk_al[i];
-      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bg[i]) * D::N);
-      float4 d[D::P1];
-#pragma unroll
-      for (int a = 0; a < D::P1; ++a) {
-        const float4 gv = __ldg(grow + a);
-        d[a] = make_float4(__fmul_rn(al, gv.x), __fmul_rn(al, gv.y), __fmul_rn(al, gv.z),
-                           __fmul_rn(al, gv.w));
-      }
-      for (int r = lane; r < D::R2; r += 32) {
-        if (own_j) {
-          // P2[j][r][:] += Σ_a H[a][r] · D2[a][:]
-          const float* hrow = Hbuf + static_cast<int64_t>(tl.start + s) * D::W1 + r;
-          float h[D::P1];
-#pragma unroll
-          for (int a = 0; a < D::P1; ++a) h[a] = __ldg(hrow + a * D::R2);
-          float4* p = reinterpret_cast<float4*>(P2 + j * D::S2 + r * D::N2);
-          float4 v = *p;
+      for (int a = 0; a < D::P1; ++a) acc[a] = 0.f;
+      if (r < D::R2) {
+        for (int i = 0; i < ntl; ++i) {
+          if (lk_slot[i] != s) continue;
+          const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2)[r];
 #pragma unroll
           for (int a = 0; a < D::P1; ++a) {
-            v.x = __fmaf_rn(h[a], d[a].x, v.x);
-            v.y = __fmaf_rn(h[a], d[a].y, v.y);
-            v.z = __fmaf_rn(h[a], d[a].z, v.z);
-            v.w = __fmaf_rn(h[a], d[a].w, v.w);
+            const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
+            float v = __fmul_rn(dv.x, gv.x);
+            v = __fmaf_rn(dv.y, gv.y, v);
+            v = __fmaf_rn(dv.z, gv.z, v);
+            v = __fmaf_rn(dv.w, gv.w, v);
+            acc[a] += v;
           }
-          *p = v;
         }
-        if (own_s) {
-          // S[s][a][r] += Σ_j2 D2[a][j2] · G2[i2][r][j2]
-          const float4 gv = __ldg(reinterpret_cast<const float4*>(
-              G2 + static_cast<int64_t>(lk_i2[i]) * D::S2) + r);
-          float* srow = S + s * D::W1 + r;
 #pragma unroll
-          for (int a = 0; a < D::P1; ++a) {
-            float v = __fmul_rn(d[a].x, gv.x);
-            v = __fmaf_rn(d[a].y, gv.y, v);
-            v = __fmaf_rn(d[a].z, gv.z, v);
-            v = __fmaf_rn(d[a].w, gv.w, v);
-            srow[a * D::R2] += v;
-          }
-        }
+        for (int a = 0; a < D::P1; ++a) S[s * D::W1 + a * D::R2 + r] = acc[a];
       }
     }
     __syncthreads();
-    // dG1 partial += Σ_slots G0[i0]ᵀ (R1 x P0) · S (P0 x C1)
+    // dG1 partial += Σ_slots G0[i0]ᵀ (R1 x P0) · S (P0 x C1): item (r1, 4 columns)
 #pragma unroll
     for (int x = 0; x < PER1; ++x) {
       const int item = tid + x * kThreads;
@@ -770,13 +773,9 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
         }
       }
     }
-    // end of a bucket run (or of this CTA's range): flush the run partials
+    // end of an i1 run (or of this CTA's range): flush the dG1 partial
     const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
-    if (tid == 0) {
-      has1[t] = (t == run_start) ? 1 : 0;
-      if (t != run_start) mask2[t] = 0ull;
-    }
-    __syncthreads();
+    if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
     if (last) {
 #pragma unroll
       for (int x = 0; x < PER1; ++x) {
@@ -786,17 +785,93 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
           acc1[x] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-      const unsigned long long tm = *tmask;
-      for (int e = tid; e < p2sz; e += kThreads) {
-        const int j = e / D::S2;
-        if ((tm >> j) & 1ull) part2[static_cast<int64_t>(run_start) * p2sz + e] = P2[e];
-        P2[e] = 0.f;
+      run_start = t + 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------ f3_bwd2 ----
+// Per i2-tile (<= TT2 lookups with the same i2): dG2 contribution
+// Σ_l H(l)ᵀ (R2 x P1) · D2_l (P1 x N2).  4 warps split the lookups
+// (l = w, w+4, ...), lanes own rank columns (float4 over j2); warp sums are
+// folded in warp order.  Consecutive tiles of the same i2 in a CTA's range
+// accumulate; one partial per run (has2 marks its first tile).
+template <class D>
+__global__ void __launch_bounds__(128) f3_bwd2(
+    Geo g, const Tile* __restrict__ tiles, const int* __restrict__ ntiles,
+    const uint32_t* __restrict__ perm, const uint32_t* __restrict__ hloc,
+    const int32_t* __restrict__ lk_bag, const float* __restrict__ alpha,
+    const float* __restrict__ grad, const float* __restrict__ Hbuf, float* __restrict__ part2,
+    int* __restrict__ has2) {
+  constexpr int NW = 4;
+  constexpr int CH = (D::R2 + 31) / 32;
+  __shared__ float4 red[NW][CH * 32];
+  __shared__ int hl[D::TT2], bg[D::TT2];
+  __shared__ float al[D::TT2];
+  const int nt = *ntiles;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int t_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nt / gridDim.x);
+  const int t_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nt / gridDim.x);
+  float4 acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int run_start = t_lo;
+  for (int t = t_lo; t < t_hi; ++t) {
+    const Tile tl = tiles[t];
+    const int ntl = tl.end - tl.start;
+    if (tid < ntl) {
+      const int l = static_cast<int>(perm[tl.start + tid]);
+      hl[tid] = static_cast<int>(hloc[l]);
+      bg[tid] = lk_bag[l];
+      al[tid] = alpha[l];
+    }
+    __syncthreads();
+    for (int i = wid; i < ntl; i += NW) {
+      const float a0 = al[i];
+      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bg[i]) * D::N);
+      const float* hrow = Hbuf + static_cast<int64_t>(hl[i]) * D::W1;
+      float4 d[D::P1];
+#pragma unroll
+      for (int a = 0; a < D::P1; ++a) {
+        const float4 gv = __ldg(grow + a);
+        d[a] = make_float4(__fmul_rn(a0, gv.x), __fmul_rn(a0, gv.y), __fmul_rn(a0, gv.z),
+                           __fmul_rn(a0, gv.w));
       }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int r = c * 32 + lane;
+        if (r < D::R2) {
+          float h[D::P1];
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) h[a] = __ldg(hrow + a * D::R2 + r);
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) {
+            acc[c].x = __fmaf_rn(h[a], d[a].x, acc[c].x);
+            acc[c].y = __fmaf_rn(h[a], d[a].y, acc[c].y);
+            acc[c].z = __fmaf_rn(h[a], d[a].z, acc[c].z);
+            acc[c].w = __fmaf_rn(h[a], d[a].w, acc[c].w);
+          }
+        }
+      }
+    }
+    const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
+    if (tid == 0) has2[t] = (t == run_start) ? 1 : 0;
+    if (last) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) red[wid][c * 32 + lane] = acc[c];
       __syncthreads();
-      if (tid == 0) {
-        mask2[run_start] = tm;
-        *tmask = 0ull;
+      if (wid == 0) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int r = c * 32 + lane;
+          float4 s = red[0][c * 32 + lane];
+          for (int w = 1; w < NW; ++w) add4(s, red[w][c * 32 + lane]);
+          if (r < D::R2)
+            reinterpret_cast<float4*>(part2 + static_cast<int64_t>(run_start) * D::S2)[r] = s;
+        }
       }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       run_start = t + 1;
     }
     __syncthreads();
@@ -808,32 +883,21 @@ __global__ void __launch_bounds__(kThreads) f3_bwd(
 // warp w scans candidate chunks of 32 (w, w+8, ...), ballots the live
 // candidates, and sums their rows 4 loads at a time (lanes own float4
 // columns); warp sums are folded in warp order.  Roles by blockIdx:
-//   [0, m1*C1c)            dG1[i1]   candidates: tiles of buckets (blk, i1), has1
-//   [.., + m2*C2c)         dG2[i2]   candidates: tiles of blk(i2) buckets, mask2 bit
-//   [.., + m0*C0c)         dG0[i0]   candidates: bwd CTAs, d0mask
+//   [0, m1*C1c)      dG1[i1]   candidates: i1-tiles of bucket i1, has1
+//   [.., + m2*C2c)   dG2[i2]   candidates: i2-tiles of bucket i2, has2
+//   [.., + m0*C0c)   dG0[i0]   candidates: f3_bwd1 CTAs, d0mask
 // MODE 0 writes dense gradients (zeros if untouched), 1 applies SGD in place.
-__device__ __forceinline__ void add4(float4& a, const float4 b) {
-  a.x += b.x;
-  a.y += b.y;
-  a.z += b.z;
-  a.w += b.w;
-}
-
-// Sum rows row_of(k) (float4 column col4) over the set bits k of `live`
-// (relative to cand0), 4 independent loads in flight.
 template <class RowFn>
 __device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, bool colok, RowFn row_of,
                                          float4& acc) {
   while (live) {
     int idx[4];
-    int n = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       idx[u] = -1;
       if (live) {
         idx[u] = cand0 + __ffs(live) - 1;
         live &= live - 1;
-        ++n;
       }
     }
     float4 v[4];
@@ -872,11 +936,11 @@ __device__ __forceinline__ void fold_store(float4 v, bool touched, float4* red, 
 
 template <class D, int MODE>
 __global__ void __launch_bounds__(kThreads) f3_combine(
-    Geo g, float* __restrict__ cores, float* __restrict__ grads, const int* __restrict__ ntiles,
-    const int32_t* __restrict__ tile_base, const float* __restrict__ part1,
-    const int* __restrict__ has1, const float* __restrict__ part2,
-    const unsigned long long* __restrict__ mask2, const float* __restrict__ D0acc,
-    const unsigned char* __restrict__ d0mask, int nbwd, float lr) {
+    Geo g, float* __restrict__ cores, float* __restrict__ grads,
+    const int32_t* __restrict__ tile_base1, const int32_t* __restrict__ tile_base2,
+    const float* __restrict__ part1, const int* __restrict__ has1,
+    const float* __restrict__ part2, const int* __restrict__ has2,
+    const float* __restrict__ D0acc, const unsigned char* __restrict__ d0mask, int nbwd, float lr) {
   __shared__ float4 red[kThreads];
   __shared__ int touched_sm;
   constexpr int NW = kThreads / 32;
@@ -892,15 +956,12 @@ __global__ void __launch_bounds__(kThreads) f3_combine(
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S1 / 4;
     auto row = [&](int t) { return part1 + static_cast<int64_t>(t) * D::S1; };
-    for (int b = 0; b < g.nblk; ++b) {
-      const int key = b * g.m1 + i1;
-      const int t0 = tile_base[key], t1 = tile_base[key + 1];
-      for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
-        const int t = c0 + lane;
-        const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has1[t] != 0);
-        touched |= live != 0;
-        sum_live(live, c0, col4, colok, row, acc);
-      }
+    const int t0 = tile_base1[i1], t1 = tile_base1[i1 + 1];
+    for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
+      const int t = c0 + lane;
+      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has1[t] != 0);
+      touched |= live != 0;
+      sum_live(live, c0, col4, colok, row, acc);
     }
     fold_store<D::S1>(acc, touched, red, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
                       grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, col4, MODE, lr,
@@ -910,15 +971,13 @@ __global__ void __launch_bounds__(kThreads) f3_combine(
   bid -= g.m1 * C1c;
   if (bid < g.m2 * C2c) {
     const int i2 = bid / C2c, ch = bid - i2 * C2c;
-    const int b = i2 / g.blk, j = i2 - b * g.blk;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S2 / 4;
-    const int t0 = tile_base[b * g.m1], t1 = tile_base[b * g.m1 + g.m1];
-    const int p2sz = g.blk * D::S2;
-    auto row = [&](int t) { return part2 + static_cast<int64_t>(t) * p2sz + j * D::S2; };
+    auto row = [&](int t) { return part2 + static_cast<int64_t>(t) * D::S2; };
+    const int t0 = tile_base2[i2], t1 = tile_base2[i2 + 1];
     for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
       const int t = c0 + lane;
-      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && ((mask2[t] >> j) & 1ull));
+      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has2[t] != 0);
       touched |= live != 0;
       sum_live(live, c0, col4, colok, row, acc);
     }

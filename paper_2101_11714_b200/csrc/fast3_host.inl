@@ -3,10 +3,10 @@
 namespace ttgpu {
 
 struct F3Bufs {
-  DevBuf key, d0, d2, hist, perm, tiles, tile_base, ntiles, Hbuf, y, slotpos, tile_i0, tile_nslots,
-      part1, has1, part2, mask2, D0acc, d0mask;
+  DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, tiles1, tiles2, tile_base1, tile_base2, ntiles,
+      Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask;
   f3::Geo geo{};
-  int max_tiles = 0;
+  int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
 };
 
@@ -25,15 +25,6 @@ int f3_lpt(int64_t L, int K) {
   return 0;
 }
 
-template <int LPT>
-void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const int64_t* idx,
-                 int64_t L, int NT, const int64_t* off, int64_t B, const double* w, int pooling,
-                 F3Bufs& f, int32_t* lk_bag, float* alpha, ttgpu_table* t) {
-  f3::f3_hist<float, LPT><<<grid, 512, smem, st>>>(
-      g, idx, L, NT, off, B, w, pooling, f.key.as<uint32_t>(), f.d0.as<uint16_t>(),
-      f.d2.as<uint16_t>(), lk_bag, alpha, f.hist.as<uint32_t>(), t->d_bad(), t->d_struct());
-}
-
 f3::Geo make_geo(const ttgpu_table* t) {
   f3::Geo g{};
   const DevPlan& P = t->dp;
@@ -41,9 +32,6 @@ f3::Geo make_geo(const ttgpu_table* t) {
   g.m1 = P.m[1];
   g.m2 = P.m[2];
   g.m12 = static_cast<uint32_t>(P.m[1]) * static_cast<uint32_t>(P.m[2]);
-  g.blk = std::min(64, P.m[2]);
-  g.nblk = (P.m[2] + g.blk - 1) / g.blk;
-  g.K = g.nblk * P.m[1];
   g.num_rows = P.num_rows;
   g.coff0 = P.coff[0];
   g.coff1 = P.coff[1];
@@ -51,70 +39,93 @@ f3::Geo make_geo(const ttgpu_table* t) {
   return g;
 }
 
+template <int LPT>
+void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const int64_t* idx,
+                 int64_t L, int NT, const int64_t* off, int64_t B, const double* w, int pooling,
+                 F3Bufs& f, int32_t* lk_bag, float* alpha, ttgpu_table* t) {
+  f3::f3_hist<float, LPT><<<grid, 512, smem, st>>>(
+      g, idx, L, NT, off, B, w, pooling, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
+      f.d2.as<uint16_t>(), lk_bag, alpha, f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
+      t->d_bad(), t->d_struct());
+}
+
+template <class K>
+int grid_occ(K kern, int threads, size_t smem, int num_sms, int cap) {
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  return std::max(1, std::min(cap, num_sms * std::max(occ, 1)));
+}
+
 template <class D>
 struct F3Runner {
-  static size_t fwd_smem(const f3::Geo& g) { return f3::FwdSmem<D>::bytes(g.m0); }
-  static size_t bwd_smem(const f3::Geo& g) { return f3::BwdSmem<D>::bytes(g.m0, g.blk); }
-
   static void forward(ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L, const int64_t* off,
                       int64_t B, const double* w, int pooling, float* out, bool exact,
                       int32_t* lk_bag, float* alpha) {
     cudaStream_t st = t->stream;
     f3::Geo& g = f.geo;
     g = make_geo(t);
-    const int lpt = f3_lpt(L, g.K);
+    const int Kmax = std::max(g.m1, g.m2);
+    const int lpt = f3_lpt(L, Kmax);
     if (lpt == 0) fail(TTGPU_ERR_RUNTIME, "batch too large for the fast path histogram");
     const int TL = 512 * lpt;
     const int NT = static_cast<int>((L + TL - 1) / TL);
-    f.max_tiles = static_cast<int>((L + D::TT - 1) / D::TT) + g.K;
-    f.key.ensure(4 * L);
+    f.max_tiles1 = static_cast<int>((L + D::TT - 1) / D::TT) + g.m1;
+    f.max_tiles2 = static_cast<int>((L + D::TT2 - 1) / D::TT2) + g.m2;
     f.d0.ensure(2 * L);
+    f.d1.ensure(2 * L);
     f.d2.ensure(2 * L);
-    f.hist.ensure(4 * static_cast<size_t>(g.K) * NT);
-    f.perm.ensure(4 * L);
-    f.tiles.ensure(sizeof(f3::Tile) * f.max_tiles);
-    f.tile_base.ensure(4 * (g.K + 1));
+    f.hist1.ensure(4 * static_cast<size_t>(g.m1) * NT);
+    f.hist2.ensure(4 * static_cast<size_t>(g.m2) * NT);
+    f.perm1.ensure(4 * L);
+    f.perm2.ensure(4 * L);
+    f.tiles1.ensure(sizeof(f3::Tile) * f.max_tiles1);
+    f.tiles2.ensure(sizeof(f3::Tile) * f.max_tiles2);
+    f.tile_base1.ensure(4 * (g.m1 + 1));
+    f.tile_base2.ensure(4 * (g.m2 + 1));
     f.ntiles.ensure(16);
     f.Hbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
     f.y.ensure(4 * static_cast<size_t>(L) * D::N);
+    f.hloc.ensure(4 * L);
     f.slotpos.ensure(2 * L);
     f.tile_i0.ensure(2 * L);
-    f.tile_nslots.ensure(4 * f.max_tiles);
+    f.tile_nslots.ensure(4 * f.max_tiles1);
     const int gb = std::max(NT, grid_for(B, 512, t->num_sms, 4));
     t->mark("fwd_begin");
+    const size_t hs = 4 * static_cast<size_t>(g.m1 + g.m2);
     switch (lpt) {
-      case 4: launch_hist<4>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      case 8: launch_hist<8>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      case 16: launch_hist<16>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      default: launch_hist<32>(gb, 4 * g.K, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      case 4: launch_hist<4>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      case 8: launch_hist<8>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      case 16: launch_hist<16>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      default: launch_hist<32>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
     }
     t->mark("hist");
     {
-      const size_t sm = 4 * (static_cast<size_t>(g.K) * NT + g.K + 1);
+      f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tile_base1.as<int32_t>(), f.tiles1.as<f3::Tile>(),
+                      f.ntiles.as<int>(), g.m1, D::TT};
+      f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tile_base2.as<int32_t>(), f.tiles2.as<f3::Tile>(),
+                      f.ntiles.as<int>() + 1, g.m2, D::TT2};
+      const size_t sm = 4 * (static_cast<size_t>(Kmax) * NT + Kmax + 1);
       set_smem(f3::f3_scan, sm);
-      f3::f3_scan<<<1, 1024, sm, st>>>(g, NT, D::TT, L, f.hist.as<uint32_t>(),
-                                       f.tile_base.as<int32_t>(), f.tiles.as<f3::Tile>(),
-                                       f.ntiles.as<int>());
+      f3::f3_scan<<<2, 1024, sm, st>>>(a1, a2, NT, L);
     }
     t->mark("scan");
     {
-      const size_t sm = 4 * 8 * static_cast<size_t>(g.K);
+      const size_t sm = 4 * 8 * static_cast<size_t>(Kmax);
       set_smem(f3::f3_scatter, sm);
-      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.key.as<uint32_t>(), L, TL, NT,
-                                          f.hist.as<uint32_t>(), f.perm.as<uint32_t>());
+      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.d1.as<uint16_t>(), f.d2.as<uint16_t>(), L, TL, NT,
+                                          f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
+                                          f.perm1.as<uint32_t>(), f.perm2.as<uint32_t>());
     }
     t->mark("scatter");
     {
-      const size_t sm = fwd_smem(g);
+      const size_t sm = f3::FwdSmem<D>::bytes(g.m0);
       auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
       set_smem(kern, sm);
-      int occ = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::kThreads, sm);
-      const int grid = std::max(1, std::min(f.max_tiles, t->num_sms * std::max(occ, 1)));
-      kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles.as<f3::Tile>(),
-                                           f.ntiles.as<int>(), f.perm.as<uint32_t>(),
+      const int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
+      kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
+                                           f.ntiles.as<int>(), f.perm1.as<uint32_t>(),
                                            f.d0.as<uint16_t>(), f.d2.as<uint16_t>(),
-                                           f.Hbuf.as<float>(), f.y.as<float>(),
+                                           f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
                                            f.tile_nslots.as<int>());
     }
@@ -132,34 +143,36 @@ struct F3Runner {
                        const int32_t* lk_bag, const float* alpha, int64_t L) {
     cudaStream_t st = t->stream;
     const f3::Geo& g = f.geo;
-    const size_t sm = bwd_smem(g);
-    auto kern = f3::f3_bwd<D>;
-    set_smem(kern, sm);
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::kThreads, sm);
-    const int grid = std::max(1, std::min(f.max_tiles, t->num_sms * std::max(occ, 1)));
-    f.part1.ensure(4 * static_cast<size_t>(f.max_tiles) * D::S1);
-    f.has1.ensure(4 * static_cast<size_t>(f.max_tiles));
-    f.part2.ensure(4 * static_cast<size_t>(f.max_tiles) * g.blk * D::S2);
-    f.mask2.ensure(8 * static_cast<size_t>(f.max_tiles));
-    f.D0acc.ensure(4 * static_cast<size_t>(grid) * g.m0 * D::S0);
-    f.d0mask.ensure(static_cast<size_t>(grid) * g.m0);
+    const size_t sm1 = f3::Bwd1Smem<D>::bytes();
+    auto k1 = f3::f3_bwd1<D>;
+    set_smem(k1, sm1);
+    const int grid1 = grid_occ(k1, f3::kThreads, sm1, t->num_sms, f.max_tiles1);
+    const int grid2 = grid_occ(f3::f3_bwd2<D>, 128, 0, t->num_sms, f.max_tiles2);
+    f.part1.ensure(4 * static_cast<size_t>(f.max_tiles1) * D::S1);
+    f.has1.ensure(4 * static_cast<size_t>(f.max_tiles1));
+    f.part2.ensure(4 * static_cast<size_t>(f.max_tiles2) * D::S2);
+    f.has2.ensure(4 * static_cast<size_t>(f.max_tiles2));
+    f.D0acc.ensure(4 * static_cast<size_t>(grid1) * g.m0 * D::S0);
+    f.d0mask.ensure(static_cast<size_t>(grid1) * g.m0);
     t->mark("bwd_begin");
-    kern<<<grid, f3::kThreads, sm, st>>>(
-        g, t->cores.as<float>(), f.tiles.as<f3::Tile>(), f.ntiles.as<int>(), f.perm.as<uint32_t>(),
-        f.d2.as<uint16_t>(), lk_bag, alpha, grad, f.Hbuf.as<float>(), f.slotpos.as<uint16_t>(),
+    k1<<<grid1, f3::kThreads, sm1, st>>>(
+        g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.perm1.as<uint32_t>(),
+        f.d2.as<uint16_t>(), lk_bag, alpha, grad, f.slotpos.as<uint16_t>(),
         f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(), f.part1.as<float>(), f.has1.as<int>(),
-        f.part2.as<float>(), f.mask2.as<unsigned long long>(), f.D0acc.as<float>(),
-        f.d0mask.as<unsigned char>());
-    t->mark("f3_bwd");
+        f.D0acc.as<float>(), f.d0mask.as<unsigned char>());
+    t->mark("f3_bwd1");
+    f3::f3_bwd2<D><<<grid2, 128, 0, st>>>(g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
+                                          f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag,
+                                          alpha, grad, f.Hbuf.as<float>(), f.part2.as<float>(),
+                                          f.has2.as<int>());
+    t->mark("f3_bwd2");
     {
       constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
       auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
       ck<<<g.m1 * C1c + g.m2 * C2c + g.m0 * C0c, f3::kThreads, 0, st>>>(
-          g, t->cores.as<float>(), t->grads.as<float>(), f.ntiles.as<int>(),
-          f.tile_base.as<int32_t>(), f.part1.as<float>(), f.has1.as<int>(), f.part2.as<float>(),
-          f.mask2.as<unsigned long long>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>(),
-          grid, lr);
+          g, t->cores.as<float>(), t->grads.as<float>(), f.tile_base1.as<int32_t>(),
+          f.tile_base2.as<int32_t>(), f.part1.as<float>(), f.has1.as<int>(), f.part2.as<float>(),
+          f.has2.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>(), grid1, lr);
     }
     t->mark("f3_combine");
     CK(cudaGetLastError());
@@ -167,9 +180,9 @@ struct F3Runner {
 };
 
 // instantiation table: (P0, R1, N1, R2, N2, TT)
-using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 128>;
-using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 128>;
-using F3_R32 = f3::Dims<2, 32, 2, 32, 4, 64>;
+using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 64>;
+using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 64>;
+using F3_R32 = f3::Dims<2, 32, 2, 32, 4, 32>;
 using F3_R64 = f3::Dims<2, 64, 2, 64, 4, 32>;
 
 template <class D>
@@ -185,9 +198,7 @@ int f3_kind(const ttgpu_table* t) {
   if (P.m[0] >= 65536 || P.m[1] >= 65536 || P.m[2] >= 65536) return -1;
   if (P.num_rows >= (1ll << 32) || static_cast<int64_t>(P.m[0]) * P.m[1] * P.m[2] >= (1ll << 32))
     return -1;
-  const int blk = std::min(64, P.m[2]);
-  const int64_t K = static_cast<int64_t>((P.m[2] + blk - 1) / blk) * P.m[1];
-  if (K > 6144 || P.m[0] > 8192) return -1;
+  if (std::max(P.m[1], P.m[2]) > 6144 || P.m[0] > 8192) return -1;
   if (dims_match<F3_R8>(P)) return 0;
   if (dims_match<F3_R16>(P)) return 1;
   if (dims_match<F3_R32>(P)) return 2;
@@ -195,7 +206,10 @@ int f3_kind(const ttgpu_table* t) {
   return -1;
 }
 
-bool f3_feasible(const ttgpu_table* t, int64_t L) { return f3_lpt(L, make_geo(t).K) > 0; }
+bool f3_feasible(const ttgpu_table* t, int64_t L) {
+  const f3::Geo g = make_geo(t);
+  return L < (1ll << 31) && f3_lpt(L, std::max(g.m1, g.m2)) > 0;
+}
 
 void f3_forward(int kind, ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L,
                 const int64_t* off, int64_t B, const double* w, int pooling, float* out, bool exact,
