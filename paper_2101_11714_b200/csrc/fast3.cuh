@@ -387,21 +387,24 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
 // ------------------------------------------------------------- f3_fwd ----
 template <class D>
 struct FwdSmem {
-  // floats: G1s[S1] (TMA) | Hs[TT*W1P] | G0s[TT*S0] ; then mbarrier + ints
-  static constexpr int W1P = D::W1 + 1;  // odd: lookups of different slots hit different banks
+  // floats: G1s[S1] (TMA) | Hs[TT*HSP] | G0s[TT*S0P] | G2s[TT*S2P] ; then mbarrier + ints
+  static constexpr int R2P = D::R2 + 1;          // padded H rows: (slot, row) -> distinct banks
+  static constexpr int HSP = D::P1 * R2P + 1;    // odd slot stride
+  static constexpr int S0P = D::S0 + 1;
+  static constexpr int S2P = D::S2 + 4;          // lookups' float4 rows in distinct bank groups
   static __host__ __device__ size_t floats() {
-    size_t f = D::S1 + static_cast<size_t>(D::TT) * (W1P + D::S0);
+    size_t f = D::S1 + static_cast<size_t>(D::TT) * (HSP + S0P + S2P);
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes(int m0) {
-    return floats() * 4 + 16 + sizeof(int) * (static_cast<size_t>(m0) + 5 * D::TT + 40);
+    return floats() * 4 + 16 + sizeof(int) * (static_cast<size_t>(m0) + 6 * D::TT + 16);
   }
 };
 
-// Per i1-tile: TMA G1[i1] (issued first, overlaps the index gathers); dedup
-// i0 -> slots (numbered by ascending i0; backward reuses the numbering);
-// H(slot) = G0·G1; y = H·G2[i2] per lookup.  Saves H rows and, per lookup,
-// the H row index (hloc) for f3_bwd2.
+// Per i1-tile: TMA G1[i1] (issued first, overlaps the index gathers); slots =
+// distinct i0 numbered by first occurrence in the tile (warp ballots; the
+// numbering backward reuses); H(slot) = G0·G1; y = H·G2[i2] per lookup.
+// Saves H rows and, per lookup, the H row index (hloc) for f3_bwd2.
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
@@ -415,25 +418,28 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots) {
   using SM = FwdSmem<D>;
+  constexpr int TW = (D::TT + 31) / 32;  // warps holding tile lookups
   extern __shared__ __align__(128) float sm[];
   float* G1s = sm;
   float* Hs = G1s + D::S1;
-  float* G0s = Hs + D::TT * SM::W1P;
+  float* G0s = Hs + D::TT * SM::HSP;
+  float* G2s = G0s + D::TT * SM::S0P;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());
-  int* flags = reinterpret_cast<int*>(bar + 2);
-  int* lk_l = flags + g.m0;
+  int* first = reinterpret_cast<int*>(bar + 2);  // m0: first tile position of each i0
+  int* lk_l = first + g.m0;
   int* lk_i0 = lk_l + D::TT;
   int* lk_i2 = lk_i0 + D::TT;
   int* lk_slot = lk_i2 + D::TT;
   int* slot_i0 = lk_slot + D::TT;
-  int* scr = slot_i0 + D::TT;  // 40 ints scan scratch
+  int* slot_at = slot_i0 + D::TT;  // slot id of a first-occurrence position
+  int* wcnt = slot_at + D::TT;     // 16
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) mbar_init(bar, 1);
-  for (int i = tid; i < g.m0; i += kThreads) flags[i] = 0;
+  for (int i = tid; i < g.m0; i += kThreads) first[i] = 0x7fffffff;
   __syncthreads();
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < nt; t += gridDim.x, phase ^= 1u) {
@@ -446,45 +452,87 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
       mbar_arrive_expect(bar, D::S1 * 4);
       tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, bar);
     }
+    int my_i0 = -1;
     if (tid < ntl) {
       const int l = static_cast<int>(perm[tl.start + tid]);
-      const int i0 = d0[l];
-      const int i2 = d2[l];
+      my_i0 = d0[l];
       lk_l[tid] = l;
-      lk_i0[tid] = i0;
-      lk_i2[tid] = i2;
-      flags[i0] = 1;
+      lk_i0[tid] = my_i0;
+      lk_i2[tid] = d2[l];
+      atomicMin(&first[my_i0], tid);
     }
     __syncthreads();
-    int nslots;
-    {
-      const int per = (g.m0 + kThreads - 1) / kThreads;
-      const int lo = min(g.m0, tid * per), hi = min(g.m0, lo + per);
-      int c = 0;
-      for (int i = lo; i < hi; ++i) c += flags[i];
-      int ex = block_excl_scan(c, &nslots, scr);
-      for (int i = lo; i < hi; ++i) {
-        if (flags[i]) {
-          slot_i0[ex] = i;
-          flags[i] = ex++;
-        }
-      }
+    const bool is_first = tid < ntl && first[my_i0] == tid;
+    const unsigned fb = __ballot_sync(0xffffffffu, is_first);
+    if (wid < TW && lane == 0) wcnt[wid] = __popc(fb);
+    __syncthreads();
+    int base = 0, nslots = 0;
+#pragma unroll
+    for (int w = 0; w < TW; ++w) {
+      base += (w < wid) ? wcnt[w] : 0;
+      nslots += wcnt[w];
+    }
+    if (is_first) {
+      const int s = base + __popc(fb & lanemask_lt());
+      slot_i0[s] = my_i0;
+      slot_at[tid] = s;
+      tile_i0[tl.start + s] = static_cast<uint16_t>(my_i0);
     }
     __syncthreads();
     if (tid < ntl) {
-      const int s = flags[lk_i0[tid]];
+      const int s = slot_at[first[my_i0]];
       lk_slot[tid] = s;
       slot_of_pos[tl.start + tid] = static_cast<uint16_t>(s);
       hloc[lk_l[tid]] = static_cast<uint32_t>(tl.start + s);
     }
-    if (tid < nslots) tile_i0[tl.start + tid] = static_cast<uint16_t>(slot_i0[tid]);
     if (tid == 0) tile_nslots[t] = nslots;
-    gather_to_smem<8>(G0s, nslots * D::S0, [&](int e) {
-      const int s = e / D::S0;
-      return G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0);
-    });
+    // G0 rows of the slots and G2 slices of the lookups (independent loads, batched)
+    {
+      constexpr int U = 8;
+      for (int e0 = tid; e0 < nslots * D::S0; e0 += kThreads * U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kThreads;
+          v[u] = 0.f;
+          if (e < nslots * D::S0) {
+            const int s = e / D::S0;
+            v[u] = __ldg(G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kThreads;
+          if (e < nslots * D::S0) {
+            const int s = e / D::S0;
+            G0s[s * SM::S0P + (e - s * D::S0)] = v[u];
+          }
+        }
+      }
+      constexpr int Q = D::S2 / 4;
+      for (int e0 = tid; e0 < ntl * Q; e0 += kThreads * 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * kThreads;
+          if (e < ntl * Q) {
+            const int i = e / Q;
+            v[u] = __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2) +
+                         (e - i * Q));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * kThreads;
+          if (e < ntl * Q) {
+            const int i = e / Q;
+            reinterpret_cast<float4*>(G2s + i * SM::S2P)[e - i * Q] = v[u];
+          }
+        }
+      }
+    }
     __syncthreads();
-    if (tid < nslots) flags[slot_i0[tid]] = 0;  // ready for the next tile
+    if (tid < ntl && is_first) first[my_i0] = 0x7fffffff;  // ready for the next tile
     mbar_wait(bar, phase);
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
     for (int q = tid; q < nslots * D::C4; q += kThreads) {
@@ -492,22 +540,24 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
       float4 acc[D::P0];
 #pragma unroll
       for (int a = 0; a < D::P0; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* g0 = G0s + s * D::S0;
+      const float* g0 = G0s + s * SM::S0P;
 #pragma unroll 8
       for (int p = 0; p < D::R1; ++p) {
         const float4 b = reinterpret_cast<const float4*>(G1s + p * D::C1)[c4];
 #pragma unroll
         for (int a = 0; a < D::P0; ++a) acc[a] = madd4<float, kExact>(g0[a * D::R1 + p], b, acc[a]);
       }
-      float* hrow = Hs + s * SM::W1P;
+      float* hs = Hs + s * SM::HSP;
       float* hg = Hbuf + static_cast<int64_t>(tl.start + s) * D::W1;
 #pragma unroll
       for (int a = 0; a < D::P0; ++a) {
-        const int c = a * D::C1 + c4 * 4;
-        hrow[c] = acc[a].x;
-        hrow[c + 1] = acc[a].y;
-        hrow[c + 2] = acc[a].z;
-        hrow[c + 3] = acc[a].w;
+        const int c = a * D::C1 + c4 * 4;  // = (row, r) in the (P1 x R2) view
+        const float v4[4] = {acc[a].x, acc[a].y, acc[a].z, acc[a].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int row = (c + u) / D::R2, r = (c + u) - row * D::R2;
+          hs[row * SM::R2P + r] = v4[u];
+        }
         reinterpret_cast<float4*>(hg + c)[0] = acc[a];
       }
     }
@@ -515,11 +565,11 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     // y = H(slot) (P1 x R2) · G2[i2] (R2 x N2): thread -> (lookup, row a)
     for (int q = tid; q < ntl * D::P1; q += kThreads) {
       const int i = q / D::P1, a = q - i * D::P1;
-      const float* hrow = Hs + lk_slot[i] * SM::W1P + a * D::R2;
-      const float4* g2 = reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2);
+      const float* hrow = Hs + lk_slot[i] * SM::HSP + a * SM::R2P;
+      const float4* g2 = reinterpret_cast<const float4*>(G2s + i * SM::S2P);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-      for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], __ldg(g2 + r), acc);
+      for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
       reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
     }
     __syncthreads();
@@ -556,14 +606,28 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
 }
 
 // ------------------------------------------------------------ f3_bwd1 ----
+// dG1 micro-GEMM geometry: NQ output groups x KG slot-row groups = 8 warps;
+// each lane owns a 4 (r1) x CB (c) register block.
+template <class D>
+struct G1Blk {
+  static constexpr int NQ = D::S1 > 32 * 64 ? D::S1 / (32 * 64) : 1;  // <= 64 accumulators/lane
+  static constexpr int KG = 8 / NQ;
+  static constexpr int QS = D::S1 / NQ;  // outputs per group
+  static constexpr int RB = 4;
+  static constexpr int RG = D::R1 / RB;  // r1 groups
+  static constexpr int CB = QS / (32 * RB);
+  static_assert(NQ * KG == 8 && CB >= 1 && CB % 4 == 0 || CB < 4, "bad dG1 blocking");
+};
+
 template <class D>
 struct Bwd1Smem {
-  // floats: G1t[C1*R1P] (G1 slice transposed) | S[TT*W1] | G2s[TT*S2] | D2s[TT*N]
-  //         | G0s[TT*S0] | d0tmp[TT*S0] ; then ints
+  // floats: G1t[C1*R1P] | S[TT*W1] ([kappa][c]) | ST[C1*KP] ([c][kappa]) | G2s[TT*S2]
+  //         | D2s[TT*N] | G0s[TT*S0] ; then ints
   static constexpr int R1P = D::R1 + 4;
+  static constexpr int KP = D::P0 * D::TT + 4;
   static __host__ __device__ size_t floats() {
-    size_t f = static_cast<size_t>(D::C1) * R1P +
-               static_cast<size_t>(D::TT) * (D::W1 + D::S2 + D::N + 2 * D::S0);
+    size_t f = static_cast<size_t>(D::C1) * (R1P + KP) +
+               static_cast<size_t>(D::TT) * (D::W1 + D::S2 + D::N + D::S0);
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes() {
@@ -572,11 +636,12 @@ struct Bwd1Smem {
 };
 
 // Each CTA owns a contiguous range of i1-tiles.  Consecutive tiles of the
-// same i1 keep accumulating the dG1 partial in registers; one partial per
-// (CTA, i1 run) is flushed at the run's first tile (has1 marks it).  D0
-// accumulates per (CTA, i0) in a CTA-private global block.  In the S phase
-// warp w owns the (slot, 32-column chunk) pairs o = w, w+8, ... and walks the
-// tile's lookups in order: a fixed accumulation order, no atomics.
+// same i1 keep accumulating the dG1 partial in registers (warp = (output
+// group, slot-row group)); one partial row per (CTA, i1 run, row group) is
+// flushed at the run's first tile (has1 marks it).  D0 accumulates per
+// (CTA, i0) in a CTA-private global block.  S phase: warp w owns the (slot,
+// 32-column chunk) pairs o = w, w+8, ... and walks the tile's lookups in
+// order -- a fixed accumulation order, no atomics.
 template <class D>
 __global__ void __launch_bounds__(kThreads) f3_bwd1(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
@@ -587,15 +652,16 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
     const int* __restrict__ tile_nslots, float* __restrict__ part1, int* __restrict__ has1,
     float* __restrict__ D0acc, unsigned char* __restrict__ d0mask) {
   using SM = Bwd1Smem<D>;
+  using GB = G1Blk<D>;
   constexpr int NW = kThreads / 32;
   constexpr int CH = (D::R2 + 31) / 32;  // 32-column chunks per (slot, row)
   extern __shared__ __align__(128) float sm[];
-  float* G1t = sm;                                   // C1 x R1P
-  float* S = G1t + D::C1 * SM::R1P;                  // TT x W1
+  float* G1t = sm;                                   // C1 x R1P   (G1 slice transposed)
+  float* ST = G1t + D::C1 * SM::R1P;                 // C1 x KP    (S transposed)
+  float* S = ST + D::C1 * SM::KP;                    // TT*P0 x C1 (S rows kappa = (slot, a0))
   float* G2s = S + D::TT * D::W1;                    // TT x S2
   float* D2s = G2s + D::TT * D::S2;                  // TT x N (alpha * grad rows)
-  float* G0s = D2s + D::TT * D::N;                   // TT x S0
-  float* d0tmp = G0s + D::TT * D::S0;                // TT x S0
+  float* G0s = D2s + D::TT * D::N;                   // TT*P0 x R1 (rows kappa)
   int* lk_slot = reinterpret_cast<int*>(sm + SM::floats());
   int* lk_i2 = lk_slot + D::TT;
   int* slot_i0 = lk_i2 + D::TT;
@@ -610,11 +676,15 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0 * D::S0; e += kThreads) d0acc[e] = 0.f;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
-  constexpr int ITEMS1 = D::R1 * D::C4;
-  constexpr int PER1 = (ITEMS1 + kThreads - 1) / kThreads;
-  float4 acc1[PER1];
+  // dG1 register block: warp -> (q = output group, kg = slot-row group)
+  const int q = wid / GB::KG, kg = wid - q * GB::KG;
+  const int r1b = (lane % GB::RG) * GB::RB;                      // 4 rows of r1
+  const int cb = q * (GB::QS / D::R1) + (lane / GB::RG) * GB::CB;  // CB columns
+  float acc1[GB::RB][GB::CB];
 #pragma unroll
-  for (int x = 0; x < PER1; ++x) acc1[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < GB::RB; ++i)
+#pragma unroll
+    for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
   int run_start = t_lo;
   for (int t = t_lo; t < t_hi; ++t) {
     const Tile tl = tiles[t];
@@ -635,12 +705,12 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
       const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bag[my_l]) * D::N);
       float4 gv[D::N / 4];
 #pragma unroll
-      for (int q = 0; q < D::N / 4; ++q) gv[q] = __ldg(grow + q);
+      for (int k = 0; k < D::N / 4; ++k) gv[k] = __ldg(grow + k);
 #pragma unroll
-      for (int q = 0; q < D::N / 4; ++q)
-        reinterpret_cast<float4*>(D2s + tid * D::N)[q] =
-            make_float4(__fmul_rn(al, gv[q].x), __fmul_rn(al, gv[q].y), __fmul_rn(al, gv[q].z),
-                        __fmul_rn(al, gv[q].w));
+      for (int k = 0; k < D::N / 4; ++k)
+        reinterpret_cast<float4*>(D2s + tid * D::N)[k] =
+            make_float4(__fmul_rn(al, gv[k].x), __fmul_rn(al, gv[k].y), __fmul_rn(al, gv[k].z),
+                        __fmul_rn(al, gv[k].w));
     }
     {
       constexpr int Q = D::S2 / 4;
@@ -683,7 +753,8 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
     });
     __syncthreads();
     // S(slot) = Σ_lookups D1, D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2): warp owns
-    // (slot, chunk) pairs; lane owns the rank column r; rows a in registers
+    // (slot, chunk) pairs; lane owns the rank column r; rows a in registers.
+    // Written twice: rows kappa = (slot, a0) x c and transposed c x kappa.
     for (int o = wid; o < nslots * CH; o += NW) {
       const int s = o / CH, r = (o - s * CH) * 32 + lane;
       float acc[D::P1];
@@ -704,86 +775,93 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
           }
         }
 #pragma unroll
-        for (int a = 0; a < D::P1; ++a) S[s * D::W1 + a * D::R2 + r] = acc[a];
+        for (int a = 0; a < D::P1; ++a) {
+          const int kappa = s * D::P0 + a / D::N1, c = (a % D::N1) * D::R2 + r;
+          S[kappa * D::C1 + c] = acc[a];
+          ST[c * SM::KP + kappa] = acc[a];
+        }
       }
     }
     __syncthreads();
-    // dG1 partial += Σ_slots G0[i0]ᵀ (R1 x P0) · S (P0 x C1): item (r1, 4 columns)
-#pragma unroll
-    for (int x = 0; x < PER1; ++x) {
-      const int item = tid + x * kThreads;
-      if (item < ITEMS1) {
-        const int r1 = item / D::C4, c4 = item - r1 * D::C4;
-        float4 a4 = acc1[x];
-        for (int s = 0; s < nslots; ++s) {
-#pragma unroll
-          for (int a = 0; a < D::P0; ++a) {
-            const float gv = G0s[s * D::S0 + a * D::R1 + r1];
-            const float4 sv = reinterpret_cast<const float4*>(S + s * D::W1 + a * D::C1)[c4];
-            a4.x = __fmaf_rn(gv, sv.x, a4.x);
-            a4.y = __fmaf_rn(gv, sv.y, a4.y);
-            a4.z = __fmaf_rn(gv, sv.z, a4.z);
-            a4.w = __fmaf_rn(gv, sv.w, a4.w);
-          }
-        }
-        acc1[x] = a4;
-      }
-    }
-    // D0(slot) (P0 x R1) = S (P0 x C1) · G1[i1]ᵀ: item (slot, a, 4 r1) over c
+    // dG1 partial += Σ_kappa G0[kappa][r1] (x) S[kappa][c]: warp covers the
+    // kappa rows = kg (mod KG) of its output group; 4 x CB outer products
     {
-      constexpr int R4 = D::R1 / 4;
-      for (int q = tid; q < nslots * D::P0 * R4; q += kThreads) {
-        const int sa = q / R4, r4 = q - sa * R4;
-        const float* srow = S + (sa / D::P0) * D::W1 + (sa % D::P0) * D::C1;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-        for (int c = 0; c < D::C1; ++c) {
-          const float sv = srow[c];
-          const float4 gt = reinterpret_cast<const float4*>(G1t + c * SM::R1P)[r4];
-          v.x = __fmaf_rn(sv, gt.x, v.x);
-          v.y = __fmaf_rn(sv, gt.y, v.y);
-          v.z = __fmaf_rn(sv, gt.z, v.z);
-          v.w = __fmaf_rn(sv, gt.w, v.w);
+      const int nk = nslots * D::P0;
+      for (int kap = kg; kap < nk; kap += GB::KG) {
+        const float4 av = reinterpret_cast<const float4*>(G0s + kap * D::R1)[r1b / 4];
+        const float a4[4] = {av.x, av.y, av.z, av.w};
+        float bv[GB::CB];
+#pragma unroll
+        for (int j = 0; j < GB::CB; j += 4) {
+          const float4 b = reinterpret_cast<const float4*>(S + kap * D::C1 + cb)[j / 4];
+          bv[j] = b.x;
+          bv[j + 1] = b.y;
+          bv[j + 2] = b.z;
+          bv[j + 3] = b.w;
         }
-        reinterpret_cast<float4*>(d0tmp + sa * D::R1)[r4] = v;
+#pragma unroll
+        for (int i = 0; i < GB::RB; ++i)
+#pragma unroll
+          for (int j = 0; j < GB::CB; ++j) acc1[i][j] = __fmaf_rn(a4[i], bv[j], acc1[i][j]);
       }
     }
-    __syncthreads();
-    // batched read-modify-write of this CTA's private D0 accumulator
+    // D0[kappa][r1] = Σ_c ST[c][kappa] · G1t[c][r1], 8 r1 per lane, rows
+    // distributed over warps; accumulated straight into the CTA's D0 block
     {
-      constexpr int U = 4;
-      for (int q0 = tid; q0 < nslots * D::S0; q0 += kThreads * U) {
-        float cur[U];
+      constexpr int LR = D::R1 / 8;             // lanes per row
+      constexpr int RPW = 32 / LR;              // rows per warp pass
+      const int nk = nslots * D::P0;
+      const int rsub = lane / LR, rb = (lane % LR) * 8;
+      for (int k0 = wid * RPW; k0 < nk; k0 += NW * RPW) {
+        const int kap = k0 + rsub;
+        if (kap < nk) {
+          float v[8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int q = q0 + u * kThreads;
-          if (q < nslots * D::S0) {
-            const int s = q / D::S0, e = q - s * D::S0;
-            cur[u] = d0acc[slot_i0[s] * D::S0 + e];
+          for (int j = 0; j < 8; ++j) v[j] = 0.f;
+#pragma unroll 4
+          for (int c = 0; c < D::C1; ++c) {
+            const float sv = ST[c * SM::KP + kap];
+            const float4 g0 = reinterpret_cast<const float4*>(G1t + c * SM::R1P + rb)[0];
+            const float4 g1 = reinterpret_cast<const float4*>(G1t + c * SM::R1P + rb)[1];
+            v[0] = __fmaf_rn(sv, g0.x, v[0]);
+            v[1] = __fmaf_rn(sv, g0.y, v[1]);
+            v[2] = __fmaf_rn(sv, g0.z, v[2]);
+            v[3] = __fmaf_rn(sv, g0.w, v[3]);
+            v[4] = __fmaf_rn(sv, g1.x, v[4]);
+            v[5] = __fmaf_rn(sv, g1.y, v[5]);
+            v[6] = __fmaf_rn(sv, g1.z, v[6]);
+            v[7] = __fmaf_rn(sv, g1.w, v[7]);
           }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int q = q0 + u * kThreads;
-          if (q < nslots * D::S0) {
-            const int s = q / D::S0, e = q - s * D::S0;
-            d0acc[slot_i0[s] * D::S0 + e] = cur[u] + d0tmp[q];
-            if (e == 0) d0m[slot_i0[s]] = 1;
-          }
+          const int s = kap / D::P0, a0 = kap - s * D::P0, i0 = slot_i0[s];
+          float4* dst = reinterpret_cast<float4*>(d0acc + i0 * D::S0 + a0 * D::R1 + rb);
+          float4 c0 = dst[0], c1 = dst[1];
+          c0.x += v[0];
+          c0.y += v[1];
+          c0.z += v[2];
+          c0.w += v[3];
+          c1.x += v[4];
+          c1.y += v[5];
+          c1.z += v[6];
+          c1.w += v[7];
+          dst[0] = c0;
+          dst[1] = c1;
+          if (a0 == 0 && rb == 0) d0m[i0] = 1;
         }
       }
     }
-    // end of an i1 run (or of this CTA's range): flush the dG1 partial
+    // end of an i1 run (or of this CTA's range): flush the dG1 partial rows
     const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
     if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
     if (last) {
+      float* dst = part1 + (static_cast<int64_t>(run_start) * GB::KG + kg) * D::S1;
 #pragma unroll
-      for (int x = 0; x < PER1; ++x) {
-        const int item = tid + x * kThreads;
-        if (item < ITEMS1) {
-          reinterpret_cast<float4*>(part1 + static_cast<int64_t>(run_start) * D::S1)[item] = acc1[x];
-          acc1[x] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+      for (int i = 0; i < GB::RB; ++i) {
+#pragma unroll
+        for (int j = 0; j < GB::CB; j += 4)
+          reinterpret_cast<float4*>(dst + (r1b + i) * D::C1 + cb + j)[0] =
+              make_float4(acc1[i][j], acc1[i][j + 1], acc1[i][j + 2], acc1[i][j + 3]);
+#pragma unroll
+        for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
       }
       run_start = t + 1;
     }
@@ -793,9 +871,10 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
 // ------------------------------------------------------------ f3_bwd2 ----
 // Per i2-tile (<= TT2 lookups with the same i2): dG2 contribution
 // Σ_l H(l)ᵀ (R2 x P1) · D2_l (P1 x N2).  4 warps split the lookups
-// (l = w, w+4, ...), lanes own rank columns (float4 over j2); warp sums are
-// folded in warp order.  Consecutive tiles of the same i2 in a CTA's range
-// accumulate; one partial per run (has2 marks its first tile).
+// (l = w, w+4, ...), 4 lookups' loads in flight per warp; lanes own rank
+// columns (float4 over j2); warp sums are folded in warp order.  Consecutive
+// tiles of the same i2 in a CTA's range accumulate; one partial per run
+// (has2 marks its first tile).
 template <class D>
 __global__ void __launch_bounds__(128) f3_bwd2(
     Geo g, const Tile* __restrict__ tiles, const int* __restrict__ ntiles,
@@ -803,7 +882,7 @@ __global__ void __launch_bounds__(128) f3_bwd2(
     const int32_t* __restrict__ lk_bag, const float* __restrict__ alpha,
     const float* __restrict__ grad, const float* __restrict__ Hbuf, float* __restrict__ part2,
     int* __restrict__ has2) {
-  constexpr int NW = 4;
+  constexpr int NW = 4, U = 4;
   constexpr int CH = (D::R2 + 31) / 32;
   __shared__ float4 red[NW][CH * 32];
   __shared__ int hl[D::TT2], bg[D::TT2];
@@ -826,30 +905,40 @@ __global__ void __launch_bounds__(128) f3_bwd2(
       al[tid] = alpha[l];
     }
     __syncthreads();
-    for (int i = wid; i < ntl; i += NW) {
-      const float a0 = al[i];
-      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bg[i]) * D::N);
-      const float* hrow = Hbuf + static_cast<int64_t>(hl[i]) * D::W1;
-      float4 d[D::P1];
+    for (int i0 = wid * U; i0 < ntl; i0 += NW * U) {
+      float4 d[U][D::P1];
+      float h[U][CH][D::P1];
 #pragma unroll
-      for (int a = 0; a < D::P1; ++a) {
-        const float4 gv = __ldg(grow + a);
-        d[a] = make_float4(__fmul_rn(a0, gv.x), __fmul_rn(a0, gv.y), __fmul_rn(a0, gv.z),
-                           __fmul_rn(a0, gv.w));
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u;
+        if (i < ntl) {
+          const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bg[i]) * D::N);
+          const float* hrow = Hbuf + static_cast<int64_t>(hl[i]) * D::W1;
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) d[u][a] = __ldg(grow + a);
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int a = 0; a < D::P1; ++a)
+              h[u][c][a] = (c * 32 + lane < D::R2) ? __ldg(hrow + a * D::R2 + c * 32 + lane) : 0.f;
+        }
       }
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int r = c * 32 + lane;
-        if (r < D::R2) {
-          float h[D::P1];
-#pragma unroll
-          for (int a = 0; a < D::P1; ++a) h[a] = __ldg(hrow + a * D::R2 + r);
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u;
+        if (i < ntl) {
+          const float a0 = al[i];
 #pragma unroll
           for (int a = 0; a < D::P1; ++a) {
-            acc[c].x = __fmaf_rn(h[a], d[a].x, acc[c].x);
-            acc[c].y = __fmaf_rn(h[a], d[a].y, acc[c].y);
-            acc[c].z = __fmaf_rn(h[a], d[a].z, acc[c].z);
-            acc[c].w = __fmaf_rn(h[a], d[a].w, acc[c].w);
+            const float4 dv = make_float4(__fmul_rn(a0, d[u][a].x), __fmul_rn(a0, d[u][a].y),
+                                          __fmul_rn(a0, d[u][a].z), __fmul_rn(a0, d[u][a].w));
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              acc[c].x = __fmaf_rn(h[u][c][a], dv.x, acc[c].x);
+              acc[c].y = __fmaf_rn(h[u][c][a], dv.y, acc[c].y);
+              acc[c].z = __fmaf_rn(h[u][c][a], dv.z, acc[c].z);
+              acc[c].w = __fmaf_rn(h[u][c][a], dv.w, acc[c].w);
+            }
           }
         }
       }
@@ -879,13 +968,13 @@ __global__ void __launch_bounds__(128) f3_bwd2(
 }
 
 // ---------------------------------------------------------- f3_combine ---
-// Fixed-order list reductions.  One CTA per (output slice, 128-column chunk):
-// warp w scans candidate chunks of 32 (w, w+8, ...), ballots the live
-// candidates, and sums their rows 4 loads at a time (lanes own float4
-// columns); warp sums are folded in warp order.  Roles by blockIdx:
-//   [0, m1*C1c)      dG1[i1]   candidates: i1-tiles of bucket i1, has1
-//   [.., + m2*C2c)   dG2[i2]   candidates: i2-tiles of bucket i2, has2
-//   [.., + m0*C0c)   dG0[i0]   candidates: f3_bwd1 CTAs, d0mask
+// Fixed-order list reductions, one WARP per (output slice, 128-column
+// chunk) task: the warp scans its candidates 32 at a time, ballots the live
+// ones and sums their rows 4 loads at a time (lanes own float4 columns).
+// No block barriers.  Task ranges:
+//   [0, m1*C1c)      dG1[i1]   candidates: i1-tiles of bucket i1 (has1), KG rows each
+//   [.., + m2*C2c)   dG2[i2]   candidates: i2-tiles of bucket i2 (has2)
+//   [.., + m0*C0c)   dG0[i0]   candidates: f3_bwd1 CTAs (d0mask)
 // MODE 0 writes dense gradients (zeros if untouched), 1 applies SGD in place.
 template <class RowFn>
 __device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, bool colok, RowFn row_of,
@@ -910,27 +999,18 @@ __device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, boo
   }
 }
 
-template <int W>
-__device__ __forceinline__ void fold_store(float4 v, bool touched, float4* red, float* out_core,
-                                           float* out_grad, int col4, int mode, float lr,
-                                           int* touched_sm) {
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  red[wid * 32 + lane] = v;
-  if (touched) atomicOr(touched_sm, 1);
-  __syncthreads();
-  if (wid == 0 && col4 < W / 4) {
-    float4 s = red[lane];
-    for (int w = 1; w < kThreads / 32; ++w) add4(s, red[w * 32 + lane]);
-    if (mode == 0) {
-      reinterpret_cast<float4*>(out_grad)[col4] = s;
-    } else if (*touched_sm) {
-      float4 c = reinterpret_cast<float4*>(out_core)[col4];
-      c.x = __fadd_rn(c.x, -__fmul_rn(lr, s.x));
-      c.y = __fadd_rn(c.y, -__fmul_rn(lr, s.y));
-      c.z = __fadd_rn(c.z, -__fmul_rn(lr, s.z));
-      c.w = __fadd_rn(c.w, -__fmul_rn(lr, s.w));
-      reinterpret_cast<float4*>(out_core)[col4] = c;
-    }
+__device__ __forceinline__ void store_slice(float4 s, bool touched, float* out_core, float* out_grad,
+                                            int col4, bool colok, int mode, float lr) {
+  if (!colok) return;
+  if (mode == 0) {
+    reinterpret_cast<float4*>(out_grad)[col4] = s;
+  } else if (touched) {
+    float4 c = reinterpret_cast<float4*>(out_core)[col4];
+    c.x = __fadd_rn(c.x, -__fmul_rn(lr, s.x));
+    c.y = __fadd_rn(c.y, -__fmul_rn(lr, s.y));
+    c.z = __fadd_rn(c.z, -__fmul_rn(lr, s.z));
+    c.w = __fadd_rn(c.w, -__fmul_rn(lr, s.w));
+    reinterpret_cast<float4*>(out_core)[col4] = c;
   }
 }
 
@@ -941,67 +1021,63 @@ __global__ void __launch_bounds__(kThreads) f3_combine(
     const float* __restrict__ part1, const int* __restrict__ has1,
     const float* __restrict__ part2, const int* __restrict__ has2,
     const float* __restrict__ D0acc, const unsigned char* __restrict__ d0mask, int nbwd, float lr) {
-  __shared__ float4 red[kThreads];
-  __shared__ int touched_sm;
-  constexpr int NW = kThreads / 32;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  using GB = G1Blk<D>;
+  const int lane = threadIdx.x & 31;
   constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
-  if (threadIdx.x == 0) touched_sm = 0;
-  __syncthreads();
-  int bid = blockIdx.x;
+  int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   bool touched = false;
-  if (bid < g.m1 * C1c) {
-    const int i1 = bid / C1c, ch = bid - i1 * C1c;
+  if (task < g.m1 * C1c) {
+    const int i1 = task / C1c, ch = task - i1 * C1c;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S1 / 4;
-    auto row = [&](int t) { return part1 + static_cast<int64_t>(t) * D::S1; };
     const int t0 = tile_base1[i1], t1 = tile_base1[i1 + 1];
-    for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
+    for (int c0 = t0; c0 < t1; c0 += 32) {
       const int t = c0 + lane;
       const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has1[t] != 0);
       touched |= live != 0;
-      sum_live(live, c0, col4, colok, row, acc);
+#pragma unroll
+      for (int kg = 0; kg < GB::KG; ++kg) {
+        auto row = [&](int tt) { return part1 + (static_cast<int64_t>(tt) * GB::KG + kg) * D::S1; };
+        sum_live(live, c0, col4, colok, row, acc);
+      }
     }
-    fold_store<D::S1>(acc, touched, red, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
-                      grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, col4, MODE, lr,
-                      &touched_sm);
+    store_slice(acc, touched, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
+                grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, col4, colok, MODE, lr);
     return;
   }
-  bid -= g.m1 * C1c;
-  if (bid < g.m2 * C2c) {
-    const int i2 = bid / C2c, ch = bid - i2 * C2c;
+  task -= g.m1 * C1c;
+  if (task < g.m2 * C2c) {
+    const int i2 = task / C2c, ch = task - i2 * C2c;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S2 / 4;
-    auto row = [&](int t) { return part2 + static_cast<int64_t>(t) * D::S2; };
+    auto row = [&](int tt) { return part2 + static_cast<int64_t>(tt) * D::S2; };
     const int t0 = tile_base2[i2], t1 = tile_base2[i2 + 1];
-    for (int c0 = t0 + wid * 32; c0 < t1; c0 += NW * 32) {
+    for (int c0 = t0; c0 < t1; c0 += 32) {
       const int t = c0 + lane;
       const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has2[t] != 0);
       touched |= live != 0;
       sum_live(live, c0, col4, colok, row, acc);
     }
-    fold_store<D::S2>(acc, touched, red, cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
-                      grads + g.coff2 + static_cast<int64_t>(i2) * D::S2, col4, MODE, lr,
-                      &touched_sm);
+    store_slice(acc, touched, cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
+                grads + g.coff2 + static_cast<int64_t>(i2) * D::S2, col4, colok, MODE, lr);
     return;
   }
-  bid -= g.m2 * C2c;
-  const int i0 = bid / C0c, ch = bid - i0 * C0c;
+  task -= g.m2 * C2c;
+  const int i0 = task / C0c, ch = task - i0 * C0c;
   if (i0 >= g.m0) return;
   const int col4 = ch * 32 + lane;
   const bool colok = col4 < D::S0 / 4;
   auto row = [&](int c) { return D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0; };
-  for (int c0 = wid * 32; c0 < nbwd; c0 += NW * 32) {
+  for (int c0 = 0; c0 < nbwd; c0 += 32) {
     const int c = c0 + lane;
     const unsigned live =
         __ballot_sync(0xffffffffu, c < nbwd && d0mask[static_cast<int64_t>(c) * g.m0 + i0] != 0);
     touched |= live != 0;
     sum_live(live, c0, col4, colok, row, acc);
   }
-  fold_store<D::S0>(acc, touched, red, cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
-                    grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, col4, MODE, lr,
-                    &touched_sm);
+  store_slice(acc, touched, cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
+              grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, col4, colok, MODE, lr);
 }
 
 }  // namespace f3

@@ -16,9 +16,10 @@ namespace {
 
 constexpr int kF3MaxHist = 48 * 1024;  // (key x CTA) histogram entries the 1-CTA scan stages
 
-// lookups per hist/scatter CTA: 512 * LPT, LPT in {4, 8, 16, 32}; 0 = infeasible
+// lookups per hist/scatter CTA: 512 * LPT, LPT in {1, 2, ..., 32}; 0 = infeasible.
+// The smallest LPT (most CTAs) whose histogram still fits the 1-CTA scan.
 int f3_lpt(int64_t L, int K) {
-  for (int lpt = 4; lpt <= 32; lpt *= 2) {
+  for (int lpt = 1; lpt <= 32; lpt *= 2) {
     const int64_t nt = (L + 512 * lpt - 1) / (512 * lpt);
     if (nt * K <= kF3MaxHist) return lpt;
   }
@@ -93,6 +94,8 @@ struct F3Runner {
     t->mark("fwd_begin");
     const size_t hs = 4 * static_cast<size_t>(g.m1 + g.m2);
     switch (lpt) {
+      case 1: launch_hist<1>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+      case 2: launch_hist<2>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
       case 4: launch_hist<4>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
       case 8: launch_hist<8>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
       case 16: launch_hist<16>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
@@ -148,7 +151,7 @@ struct F3Runner {
     set_smem(k1, sm1);
     const int grid1 = grid_occ(k1, f3::kThreads, sm1, t->num_sms, f.max_tiles1);
     const int grid2 = grid_occ(f3::f3_bwd2<D>, 128, 0, t->num_sms, f.max_tiles2);
-    f.part1.ensure(4 * static_cast<size_t>(f.max_tiles1) * D::S1);
+    f.part1.ensure(4 * static_cast<size_t>(f.max_tiles1) * f3::G1Blk<D>::KG * D::S1);
     f.has1.ensure(4 * static_cast<size_t>(f.max_tiles1));
     f.part2.ensure(4 * static_cast<size_t>(f.max_tiles2) * D::S2);
     f.has2.ensure(4 * static_cast<size_t>(f.max_tiles2));
@@ -169,7 +172,8 @@ struct F3Runner {
     {
       constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
       auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
-      ck<<<g.m1 * C1c + g.m2 * C2c + g.m0 * C0c, f3::kThreads, 0, st>>>(
+      const int tasks = g.m1 * C1c + g.m2 * C2c + g.m0 * C0c;  // one warp each
+      ck<<<(tasks * 32 + f3::kThreads - 1) / f3::kThreads, f3::kThreads, 0, st>>>(
           g, t->cores.as<float>(), t->grads.as<float>(), f.tile_base1.as<int32_t>(),
           f.tile_base2.as<int32_t>(), f.part1.as<float>(), f.has1.as<int>(), f.part2.as<float>(),
           f.has2.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>(), grid1, lr);
