@@ -234,59 +234,72 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
 // thread per tile finding its bucket by binary search.
 struct ScanArgs {
   uint32_t* hist;
-  int32_t* tile_base;  // K + 1
+  int32_t* tile_base;   // K + 1
+  int32_t* group_base;  // K + 1: combine groups of <= kGroup tiles per bucket (>= 1 each)
   Tile* tiles;
   int* ntiles;
   int K, TT;
 };
 
+constexpr int kGroup = 16;  // combine: candidate tiles per warp task
+
+__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }  // bank-conflict-free chunks
+
 __global__ void __launch_bounds__(1024) f3_scan(ScanArgs a1, ScanArgs a2, int NT, int64_t L) {
   using Scan = cub::BlockScan<uint32_t, 1024>;
   __shared__ typename Scan::TempStorage tmp;
-  extern __shared__ uint32_t sh[];
+  extern __shared__ uint32_t sh[];  // spad(n) histogram entries, then K + 1 tile bases
   const ScanArgs& A = blockIdx.x == 0 ? a1 : a2;
   const int K = A.K, TT = A.TT;
   const int n = K * NT;
   const int tid = threadIdx.x;
 #pragma unroll 8
-  for (int i = tid; i < n; i += 1024) sh[i] = A.hist[i];
+  for (int i = tid; i < n; i += 1024) sh[spad(i)] = A.hist[i];
   __syncthreads();
   const int per = (n + 1023) / 1024;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   uint32_t s = 0;
-  for (int i = lo; i < hi; ++i) s += sh[i];
+  for (int i = lo; i < hi; ++i) s += sh[spad(i)];
   uint32_t ex;
   Scan(tmp).ExclusiveSum(s, ex);
   for (int i = lo; i < hi; ++i) {
-    const uint32_t c = sh[i];
-    sh[i] = ex;
+    const uint32_t c = sh[spad(i)];
+    sh[spad(i)] = ex;
     ex += c;
   }
   __syncthreads();
 #pragma unroll 8
-  for (int i = tid; i < n; i += 1024) A.hist[i] = sh[i];
+  for (int i = tid; i < n; i += 1024) A.hist[i] = sh[spad(i)];
   const int perk = (K + 1023) / 1024;
   const int klo = min(K, tid * perk), khi = min(K, klo + perk);
-  uint32_t nt = 0;
+  uint32_t nt = 0, ng = 0;
   for (int k = klo; k < khi; ++k) {
-    const uint32_t bs = sh[k * NT];
-    const uint32_t be = k + 1 < K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
-    nt += (be - bs + TT - 1) / TT;
+    const uint32_t bs = sh[spad(k * NT)];
+    const uint32_t be = k + 1 < K ? sh[spad((k + 1) * NT)] : static_cast<uint32_t>(L);
+    const uint32_t tk = (be - bs + TT - 1) / TT;
+    nt += tk;
+    ng += tk > kGroup ? (tk + kGroup - 1) / kGroup : 1;
   }
-  uint32_t tex;
+  uint32_t tex, gex;
   __syncthreads();
   Scan(tmp).ExclusiveSum(nt, tex);
-  uint32_t* tb = sh + n;  // K + 1 tile bases
+  __syncthreads();
+  Scan(tmp).ExclusiveSum(ng, gex);
+  uint32_t* tb = sh + spad(n) + 1;  // K + 1 tile bases
   for (int k = klo; k < khi; ++k) {
-    const uint32_t bs = sh[k * NT];
-    const uint32_t be = k + 1 < K ? sh[(k + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t bs = sh[spad(k * NT)];
+    const uint32_t be = k + 1 < K ? sh[spad((k + 1) * NT)] : static_cast<uint32_t>(L);
+    const uint32_t tk = (be - bs + TT - 1) / TT;
     tb[k] = tex;
     A.tile_base[k] = static_cast<int32_t>(tex);
-    tex += (be - bs + TT - 1) / TT;
+    A.group_base[k] = static_cast<int32_t>(gex);
+    tex += tk;
+    gex += tk > kGroup ? (tk + kGroup - 1) / kGroup : 1;
   }
   if (tid == 1023) {
     tb[K] = tex;
     A.tile_base[K] = static_cast<int32_t>(tex);
+    A.group_base[K] = static_cast<int32_t>(gex);
     *A.ntiles = static_cast<int>(tex);
   }
   __syncthreads();
@@ -297,8 +310,8 @@ __global__ void __launch_bounds__(1024) f3_scan(ScanArgs a1, ScanArgs a2, int NT
       const int mid = (lo2 + hi2) >> 1;
       if (tb[mid] <= t) lo2 = mid; else hi2 = mid;
     }
-    const uint32_t bs = sh[lo2 * NT];
-    const uint32_t be = lo2 + 1 < K ? sh[(lo2 + 1) * NT] : static_cast<uint32_t>(L);
+    const uint32_t bs = sh[spad(lo2 * NT)];
+    const uint32_t be = lo2 + 1 < K ? sh[spad((lo2 + 1) * NT)] : static_cast<uint32_t>(L);
     Tile tl;
     tl.key = lo2;
     tl.start = static_cast<int>(bs + (t - tb[lo2]) * TT);
@@ -610,13 +623,13 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
 // each lane owns a 4 (r1) x CB (c) register block.
 template <class D>
 struct G1Blk {
-  static constexpr int NQ = D::S1 > 32 * 64 ? D::S1 / (32 * 64) : 1;  // <= 64 accumulators/lane
-  static constexpr int KG = 8 / NQ;
-  static constexpr int QS = D::S1 / NQ;  // outputs per group
-  static constexpr int RB = 4;
-  static constexpr int RG = D::R1 / RB;  // r1 groups
-  static constexpr int CB = QS / (32 * RB);
-  static_assert(NQ * KG == 8 && CB >= 1 && CB % 4 == 0 || CB < 4, "bad dG1 blocking");
+  // dG1 (R1 x C1) += Σ_kappa G0[kappa][r1] (x) S[kappa][c]: warp w owns the
+  // columns [w*CB, (w+1)*CB), lane owns RB rows of r1; every warp walks all kappa
+  static constexpr int RB = D::R1 > 32 ? D::R1 / 32 : 1;
+  static constexpr int LANES = D::R1 / RB;  // active lanes
+  static constexpr int CB = D::C1 / 8;
+  static constexpr int KG = 1;              // partial rows per run
+  static_assert(D::C1 % 8 == 0 && LANES <= 32, "bad dG1 blocking");
 };
 
 template <class D>
@@ -676,10 +689,10 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0 * D::S0; e += kThreads) d0acc[e] = 0.f;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
-  // dG1 register block: warp -> (q = output group, kg = slot-row group)
-  const int q = wid / GB::KG, kg = wid - q * GB::KG;
-  const int r1b = (lane % GB::RG) * GB::RB;                      // 4 rows of r1
-  const int cb = q * (GB::QS / D::R1) + (lane / GB::RG) * GB::CB;  // CB columns
+  // dG1 register block: warp -> CB columns, lane -> RB rows
+  const int cb = wid * GB::CB;
+  const int r1b = lane * GB::RB;
+  const bool lane_on = lane < GB::LANES;
   float acc1[GB::RB][GB::CB];
 #pragma unroll
   for (int i = 0; i < GB::RB; ++i)
@@ -783,26 +796,31 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
       }
     }
     __syncthreads();
-    // dG1 partial += Σ_kappa G0[kappa][r1] (x) S[kappa][c]: warp covers the
-    // kappa rows = kg (mod KG) of its output group; 4 x CB outer products
-    {
+    // dG1 partial += Σ_kappa G0[kappa][r1] (x) S[kappa][c] (outer products)
+    if (lane_on) {
       const int nk = nslots * D::P0;
-      for (int kap = kg; kap < nk; kap += GB::KG) {
-        const float4 av = reinterpret_cast<const float4*>(G0s + kap * D::R1)[r1b / 4];
-        const float a4[4] = {av.x, av.y, av.z, av.w};
-        float bv[GB::CB];
+      for (int kap = 0; kap < nk; ++kap) {
+        float a[GB::RB];
 #pragma unroll
-        for (int j = 0; j < GB::CB; j += 4) {
-          const float4 b = reinterpret_cast<const float4*>(S + kap * D::C1 + cb)[j / 4];
-          bv[j] = b.x;
-          bv[j + 1] = b.y;
-          bv[j + 2] = b.z;
-          bv[j + 3] = b.w;
+        for (int i = 0; i < GB::RB; ++i) a[i] = G0s[kap * D::R1 + r1b + i];
+        float bv[GB::CB];
+        if constexpr (GB::CB % 4 == 0) {
+#pragma unroll
+          for (int j = 0; j < GB::CB; j += 4) {
+            const float4 b = reinterpret_cast<const float4*>(S + kap * D::C1 + cb)[j / 4];
+            bv[j] = b.x;
+            bv[j + 1] = b.y;
+            bv[j + 2] = b.z;
+            bv[j + 3] = b.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < GB::CB; ++j) bv[j] = S[kap * D::C1 + cb + j];
         }
 #pragma unroll
         for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
-          for (int j = 0; j < GB::CB; ++j) acc1[i][j] = __fmaf_rn(a4[i], bv[j], acc1[i][j]);
+          for (int j = 0; j < GB::CB; ++j) acc1[i][j] = __fmaf_rn(a[i], bv[j], acc1[i][j]);
       }
     }
     // D0[kappa][r1] = Σ_c ST[c][kappa] · G1t[c][r1], 8 r1 per lane, rows
@@ -853,15 +871,14 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
     const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
     if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
     if (last) {
-      float* dst = part1 + (static_cast<int64_t>(run_start) * GB::KG + kg) * D::S1;
+      float* dst = part1 + static_cast<int64_t>(run_start) * D::S1;
 #pragma unroll
       for (int i = 0; i < GB::RB; ++i) {
 #pragma unroll
-        for (int j = 0; j < GB::CB; j += 4)
-          reinterpret_cast<float4*>(dst + (r1b + i) * D::C1 + cb + j)[0] =
-              make_float4(acc1[i][j], acc1[i][j + 1], acc1[i][j + 2], acc1[i][j + 3]);
-#pragma unroll
-        for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
+        for (int j = 0; j < GB::CB; ++j) {
+          if (lane_on) dst[(r1b + i) * D::C1 + cb + j] = acc1[i][j];
+          acc1[i][j] = 0.f;
+        }
       }
       run_start = t + 1;
     }
@@ -1014,70 +1031,134 @@ __device__ __forceinline__ void store_slice(float4 s, bool touched, float* out_c
   }
 }
 
+struct CombineArgs {
+  const int32_t *tile_base1, *tile_base2, *group_base1, *group_base2;
+  const float *part1, *part2, *D0acc;
+  const int *has1, *has2;
+  const unsigned char* d0mask;
+  float* gpart;        // one 128-column chunk per warp task
+  int* gtouch;         // per warp task
+  int* counters;       // per (slice, chunk); zero between launches
+  int maxg1, maxg2, nbwd;
+};
+
+// Warp task (role, slice, group, chunk).  A slice's candidate list is cut into
+// groups of <= kGroup; each group is summed by its own warp.  Single-group
+// slices are applied directly; otherwise the last warp to finish (atomic
+// counter) folds the group partials in group order -- deterministic.
+template <int W>
+__device__ __forceinline__ void finish_task(float4 acc, bool touched, int task_first, int ng, int gi,
+                                            int ch, int nch, int* counter, const CombineArgs& A,
+                                            float* core, float* grad, int mode, float lr) {
+  const int lane = threadIdx.x & 31;
+  const int col4 = ch * 32 + lane;
+  const bool colok = col4 < W / 4;
+  if (ng == 1) {
+    store_slice(acc, touched, core, grad, col4, colok, mode, lr);
+    return;
+  }
+  const int task = task_first + gi * nch + ch;
+  reinterpret_cast<float4*>(A.gpart + static_cast<int64_t>(task) * 128)[lane] = acc;
+  if (lane == 0) A.gtouch[task] = touched ? 1 : 0;
+  __threadfence();
+  int prev = 0;
+  if (lane == 0) prev = atomicAdd(counter, 1);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != ng - 1) return;
+  __threadfence();
+  float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool any = false;
+  for (int q = 0; q < ng; ++q) {
+    const int tq = task_first + q * nch + ch;
+    add4(sum, __ldcg(reinterpret_cast<const float4*>(A.gpart + static_cast<int64_t>(tq) * 128) + lane));
+    any |= __ldcg(A.gtouch + tq) != 0;
+  }
+  store_slice(sum, any, core, grad, col4, colok, mode, lr);
+  if (lane == 0) *counter = 0;  // ready for the next launch
+}
+
+__device__ __forceinline__ int find_slice(const int32_t* base, int K, int x) {
+  int lo = 0, hi = K;  // base[lo] <= x < base[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (base[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 template <class D, int MODE>
-__global__ void __launch_bounds__(kThreads) f3_combine(
-    Geo g, float* __restrict__ cores, float* __restrict__ grads,
-    const int32_t* __restrict__ tile_base1, const int32_t* __restrict__ tile_base2,
-    const float* __restrict__ part1, const int* __restrict__ has1,
-    const float* __restrict__ part2, const int* __restrict__ has2,
-    const float* __restrict__ D0acc, const unsigned char* __restrict__ d0mask, int nbwd, float lr) {
-  using GB = G1Blk<D>;
+__global__ void __launch_bounds__(kThreads) f3_combine(Geo g, float* __restrict__ cores,
+                                                       float* __restrict__ grads, CombineArgs A,
+                                                       float lr) {
   const int lane = threadIdx.x & 31;
   constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
   int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   bool touched = false;
-  if (task < g.m1 * C1c) {
-    const int i1 = task / C1c, ch = task - i1 * C1c;
+  if (task < A.maxg1 * C1c) {
+    const int gidx = task / C1c, ch = task - gidx * C1c;
+    if (gidx >= A.group_base1[g.m1]) return;
+    const int i1 = find_slice(A.group_base1, g.m1, gidx);
+    const int gfirst = A.group_base1[i1], ng = A.group_base1[i1 + 1] - gfirst, gi = gidx - gfirst;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S1 / 4;
-    const int t0 = tile_base1[i1], t1 = tile_base1[i1 + 1];
+    auto row = [&](int t) { return A.part1 + static_cast<int64_t>(t) * D::S1; };
+    const int t0 = A.tile_base1[i1] + gi * kGroup;
+    const int t1 = min(A.tile_base1[i1 + 1], t0 + kGroup);
     for (int c0 = t0; c0 < t1; c0 += 32) {
       const int t = c0 + lane;
-      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has1[t] != 0);
-      touched |= live != 0;
-#pragma unroll
-      for (int kg = 0; kg < GB::KG; ++kg) {
-        auto row = [&](int tt) { return part1 + (static_cast<int64_t>(tt) * GB::KG + kg) * D::S1; };
-        sum_live(live, c0, col4, colok, row, acc);
-      }
-    }
-    store_slice(acc, touched, cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
-                grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, col4, colok, MODE, lr);
-    return;
-  }
-  task -= g.m1 * C1c;
-  if (task < g.m2 * C2c) {
-    const int i2 = task / C2c, ch = task - i2 * C2c;
-    const int col4 = ch * 32 + lane;
-    const bool colok = col4 < D::S2 / 4;
-    auto row = [&](int tt) { return part2 + static_cast<int64_t>(tt) * D::S2; };
-    const int t0 = tile_base2[i2], t1 = tile_base2[i2 + 1];
-    for (int c0 = t0; c0 < t1; c0 += 32) {
-      const int t = c0 + lane;
-      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && has2[t] != 0);
+      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && A.has1[t] != 0);
       touched |= live != 0;
       sum_live(live, c0, col4, colok, row, acc);
     }
-    store_slice(acc, touched, cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
-                grads + g.coff2 + static_cast<int64_t>(i2) * D::S2, col4, colok, MODE, lr);
+    finish_task<D::S1>(acc, touched, gfirst * C1c, ng, gi, ch, C1c, A.counters + i1 * C1c + ch, A,
+                       cores + g.coff1 + static_cast<int64_t>(i1) * D::S1,
+                       grads + g.coff1 + static_cast<int64_t>(i1) * D::S1, MODE, lr);
     return;
   }
-  task -= g.m2 * C2c;
-  const int i0 = task / C0c, ch = task - i0 * C0c;
-  if (i0 >= g.m0) return;
+  task -= A.maxg1 * C1c;
+  if (task < A.maxg2 * C2c) {
+    const int gidx = task / C2c, ch = task - gidx * C2c;
+    if (gidx >= A.group_base2[g.m2]) return;
+    const int i2 = find_slice(A.group_base2, g.m2, gidx);
+    const int gfirst = A.group_base2[i2], ng = A.group_base2[i2 + 1] - gfirst, gi = gidx - gfirst;
+    const int col4 = ch * 32 + lane;
+    const bool colok = col4 < D::S2 / 4;
+    auto row = [&](int t) { return A.part2 + static_cast<int64_t>(t) * D::S2; };
+    const int t0 = A.tile_base2[i2] + gi * kGroup;
+    const int t1 = min(A.tile_base2[i2 + 1], t0 + kGroup);
+    for (int c0 = t0; c0 < t1; c0 += 32) {
+      const int t = c0 + lane;
+      const unsigned live = __ballot_sync(0xffffffffu, t < t1 && A.has2[t] != 0);
+      touched |= live != 0;
+      sum_live(live, c0, col4, colok, row, acc);
+    }
+    finish_task<D::S2>(acc, touched, A.maxg1 * C1c + gfirst * C2c, ng, gi, ch, C2c,
+                       A.counters + g.m1 * C1c + i2 * C2c + ch, A,
+                       cores + g.coff2 + static_cast<int64_t>(i2) * D::S2,
+                       grads + g.coff2 + static_cast<int64_t>(i2) * D::S2, MODE, lr);
+    return;
+  }
+  task -= A.maxg2 * C2c;
+  const int ng0 = (A.nbwd + kGroup - 1) / kGroup;
+  const int gidx = task / C0c, ch = task - gidx * C0c;
+  if (gidx >= g.m0 * ng0) return;
+  const int i0 = gidx / ng0, gi = gidx - i0 * ng0;
   const int col4 = ch * 32 + lane;
   const bool colok = col4 < D::S0 / 4;
-  auto row = [&](int c) { return D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0; };
-  for (int c0 = 0; c0 < nbwd; c0 += 32) {
+  auto row = [&](int c) { return A.D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0; };
+  const int c0 = gi * kGroup, c1 = min(A.nbwd, c0 + kGroup);
+  {
     const int c = c0 + lane;
     const unsigned live =
-        __ballot_sync(0xffffffffu, c < nbwd && d0mask[static_cast<int64_t>(c) * g.m0 + i0] != 0);
+        __ballot_sync(0xffffffffu, c < c1 && A.d0mask[static_cast<int64_t>(c) * g.m0 + i0] != 0);
     touched |= live != 0;
     sum_live(live, c0, col4, colok, row, acc);
   }
-  store_slice(acc, touched, cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
-              grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, col4, colok, MODE, lr);
+  finish_task<D::S0>(acc, touched, A.maxg1 * C1c + A.maxg2 * C2c + i0 * ng0 * C0c, ng0, gi, ch, C0c,
+                     A.counters + g.m1 * C1c + g.m2 * C2c + i0 * C0c + ch, A,
+                     cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
+                     grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, MODE, lr);
 }
 
 }  // namespace f3

@@ -4,7 +4,8 @@ namespace ttgpu {
 
 struct F3Bufs {
   DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, tiles1, tiles2, tile_base1, tile_base2, ntiles,
-      Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask;
+      Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
+      group_base1, group_base2, gpart, gtouch, counters;
   f3::Geo geo{};
   int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
@@ -83,6 +84,8 @@ struct F3Runner {
     f.tiles2.ensure(sizeof(f3::Tile) * f.max_tiles2);
     f.tile_base1.ensure(4 * (g.m1 + 1));
     f.tile_base2.ensure(4 * (g.m2 + 1));
+    f.group_base1.ensure(4 * (g.m1 + 1));
+    f.group_base2.ensure(4 * (g.m2 + 1));
     f.ntiles.ensure(16);
     f.Hbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
     f.y.ensure(4 * static_cast<size_t>(L) * D::N);
@@ -103,11 +106,12 @@ struct F3Runner {
     }
     t->mark("hist");
     {
-      f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tile_base1.as<int32_t>(), f.tiles1.as<f3::Tile>(),
-                      f.ntiles.as<int>(), g.m1, D::TT};
-      f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tile_base2.as<int32_t>(), f.tiles2.as<f3::Tile>(),
-                      f.ntiles.as<int>() + 1, g.m2, D::TT2};
-      const size_t sm = 4 * (static_cast<size_t>(Kmax) * NT + Kmax + 1);
+      f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tile_base1.as<int32_t>(), f.group_base1.as<int32_t>(),
+                      f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), g.m1, D::TT};
+      f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tile_base2.as<int32_t>(), f.group_base2.as<int32_t>(),
+                      f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, g.m2, D::TT2};
+      const size_t n = static_cast<size_t>(Kmax) * NT;
+      const size_t sm = 4 * (n + n / 32 + 2 + Kmax + 1);
       set_smem(f3::f3_scan, sm);
       f3::f3_scan<<<2, 1024, sm, st>>>(a1, a2, NT, L);
     }
@@ -171,12 +175,35 @@ struct F3Runner {
     t->mark("f3_bwd2");
     {
       constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
+      f3::CombineArgs A{};
+      A.tile_base1 = f.tile_base1.as<int32_t>();
+      A.tile_base2 = f.tile_base2.as<int32_t>();
+      A.group_base1 = f.group_base1.as<int32_t>();
+      A.group_base2 = f.group_base2.as<int32_t>();
+      A.part1 = f.part1.as<float>();
+      A.part2 = f.part2.as<float>();
+      A.D0acc = f.D0acc.as<float>();
+      A.has1 = f.has1.as<int>();
+      A.has2 = f.has2.as<int>();
+      A.d0mask = f.d0mask.as<unsigned char>();
+      A.maxg1 = g.m1 + (f.max_tiles1 + f3::kGroup - 1) / f3::kGroup;
+      A.maxg2 = g.m2 + (f.max_tiles2 + f3::kGroup - 1) / f3::kGroup;
+      A.nbwd = grid1;
+      const int ng0 = (grid1 + f3::kGroup - 1) / f3::kGroup;
+      const int tasks = A.maxg1 * C1c + A.maxg2 * C2c + g.m0 * ng0 * C0c;  // one warp each
+      const int ncnt = g.m1 * C1c + g.m2 * C2c + g.m0 * C0c;
+      if (f.counters.cap < 4 * static_cast<size_t>(ncnt)) {
+        f.counters.ensure(4 * static_cast<size_t>(ncnt));
+        CK(cudaMemsetAsync(f.counters.p, 0, f.counters.cap, st));
+      }
+      f.gpart.ensure(4 * 128 * static_cast<size_t>(tasks));
+      f.gtouch.ensure(4 * static_cast<size_t>(tasks));
+      A.gpart = f.gpart.as<float>();
+      A.gtouch = f.gtouch.as<int>();
+      A.counters = f.counters.as<int>();
       auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
-      const int tasks = g.m1 * C1c + g.m2 * C2c + g.m0 * C0c;  // one warp each
       ck<<<(tasks * 32 + f3::kThreads - 1) / f3::kThreads, f3::kThreads, 0, st>>>(
-          g, t->cores.as<float>(), t->grads.as<float>(), f.tile_base1.as<int32_t>(),
-          f.tile_base2.as<int32_t>(), f.part1.as<float>(), f.has1.as<int>(), f.part2.as<float>(),
-          f.has2.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>(), grid1, lr);
+          g, t->cores.as<float>(), t->grads.as<float>(), A, lr);
     }
     t->mark("f3_combine");
     CK(cudaGetLastError());
