@@ -882,6 +882,7 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
       }
       run_start = t + 1;
     }
+    __syncthreads();  // the next tile overwrites slot_i0 / lk_* still read above
   }
 }
 
