@@ -46,7 +46,7 @@ struct Dims {
   static constexpr int TT2 = 64;  // lookups per i2-tile (f3_bwd2)
   static_assert(N2 == 4, "fast path expects n_2 == 4 (float4 rows)");
   static_assert(C1 % 4 == 0 && R1 % 4 == 0, "C1 and R1 must be multiples of 4");
-  static_assert(TT <= 256, "tile must fit one lookup per thread");
+  static_assert(TT <= 32, "a tile's lookups must fit one warp (slot ballots / match_any)");
 };
 
 constexpr int kThreads = 256;
@@ -634,17 +634,17 @@ struct G1Blk {
 
 template <class D>
 struct Bwd1Smem {
-  // floats: G1t[C1*R1P] | S[TT*W1] ([kappa][c]) | ST[C1*KP] ([c][kappa]) | G2s[TT*S2]
-  //         | D2s[TT*N] | G0s[TT*S0] ; then ints
+  // floats: G1t[C1*R1P] | ST[C1*KP] ([c][kappa]) | S[TT*W1] ([kappa][c]) | G2s[TT*S2]
+  //         | D2s[TT*N] | G0s[TT*S0] | D1b[TT*W1] ; then ints
   static constexpr int R1P = D::R1 + 4;
   static constexpr int KP = D::P0 * D::TT + 4;
   static __host__ __device__ size_t floats() {
     size_t f = static_cast<size_t>(D::C1) * (R1P + KP) +
-               static_cast<size_t>(D::TT) * (D::W1 + D::S2 + D::N + D::S0);
+               static_cast<size_t>(D::TT) * (2 * D::W1 + D::S2 + D::N + D::S0);
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes() {
-    return floats() * 4 + sizeof(int) * (3 * static_cast<size_t>(D::TT) + 8);
+    return floats() * 4 + sizeof(int) * (6 * static_cast<size_t>(D::TT) + 8);
   }
 };
 
@@ -675,9 +675,12 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
   float* G2s = S + D::TT * D::W1;                    // TT x S2
   float* D2s = G2s + D::TT * D::S2;                  // TT x N (alpha * grad rows)
   float* G0s = D2s + D::TT * D::N;                   // TT*P0 x R1 (rows kappa)
+  float* D1b = G0s + D::TT * D::S0;                  // TT x W1 (per-lookup D1)
   int* lk_slot = reinterpret_cast<int*>(sm + SM::floats());
   int* lk_i2 = lk_slot + D::TT;
   int* slot_i0 = lk_i2 + D::TT;
+  int* members = slot_i0 + D::TT;   // tile positions sorted by slot (stable)
+  int* sstart = members + D::TT;    // nslots + 1 member-list starts
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
@@ -765,35 +768,56 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
       return G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0);
     });
     __syncthreads();
-    // S(slot) = Σ_lookups D1, D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2): warp owns
-    // (slot, chunk) pairs; lane owns the rank column r; rows a in registers.
-    // Written twice: rows kappa = (slot, a0) x c and transposed c x kappa.
-    for (int o = wid; o < nslots * CH; o += NW) {
-      const int s = o / CH, r = (o - s * CH) * 32 + lane;
-      float acc[D::P1];
+    // per-lookup D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2): warp w takes lookups
+    // w, w+8, ...; lane owns the rank column r.  Warp 0 also builds the slot
+    // member lists (positions sorted by slot, stable) with one match_any.
+    if (wid == 0) {
+      const int sl = lane < ntl ? lk_slot[lane] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, sl);
+      int cnt = 0;
+      if (lane < nslots) cnt = 0;
+      // count of each slot -> exclusive starts (nslots <= 32: one lane per slot)
+      const unsigned lt = lanemask_lt();
+      if (sl >= 0 && (peers & lt) == 0) sstart[sl] = __popc(peers);  // leader stores the count
+      __syncwarp();
+      cnt = lane < nslots ? sstart[lane] : 0;
+      int inc = cnt;
 #pragma unroll
-      for (int a = 0; a < D::P1; ++a) acc[a] = 0.f;
-      if (r < D::R2) {
-        for (int i = 0; i < ntl; ++i) {
-          if (lk_slot[i] != s) continue;
-          const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2)[r];
-#pragma unroll
-          for (int a = 0; a < D::P1; ++a) {
-            const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
-            float v = __fmul_rn(dv.x, gv.x);
-            v = __fmaf_rn(dv.y, gv.y, v);
-            v = __fmaf_rn(dv.z, gv.z, v);
-            v = __fmaf_rn(dv.w, gv.w, v);
-            acc[a] += v;
-          }
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      __syncwarp();
+      if (lane < nslots) sstart[lane] = inc - cnt;
+      if (lane == 31) sstart[nslots] = inc;  // total = ntl (lanes >= nslots add 0)
+      __syncwarp();
+      if (sl >= 0) members[sstart[sl] + __popc(peers & lt)] = lane;
+    }
+    for (int i = wid; i < ntl; i += NW) {
+      for (int r = lane; r < D::R2; r += 32) {
+        const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2)[r];
 #pragma unroll
         for (int a = 0; a < D::P1; ++a) {
-          const int kappa = s * D::P0 + a / D::N1, c = (a % D::N1) * D::R2 + r;
-          S[kappa * D::C1 + c] = acc[a];
-          ST[c * SM::KP + kappa] = acc[a];
+          const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
+          float v = __fmul_rn(dv.x, gv.x);
+          v = __fmaf_rn(dv.y, gv.y, v);
+          v = __fmaf_rn(dv.z, gv.z, v);
+          v = __fmaf_rn(dv.w, gv.w, v);
+          D1b[i * D::W1 + a * D::R2 + r] = v;
         }
       }
+    }
+    __syncthreads();
+    // S(slot)[e] = Σ over the slot's lookups in tile order; written twice:
+    // rows kappa = (slot, a0) x c, and transposed c x kappa
+    for (int q = tid; q < nslots * D::W1; q += kThreads) {
+      const int sl = q / D::W1, e = q - sl * D::W1;
+      float acc = 0.f;
+      for (int j = sstart[sl]; j < sstart[sl + 1]; ++j) acc += D1b[members[j] * D::W1 + e];
+      const int a = e / D::R2, r = e - a * D::R2;
+      const int kappa = sl * D::P0 + a / D::N1, c = (a % D::N1) * D::R2 + r;
+      S[kappa * D::C1 + c] = acc;
+      ST[c * SM::KP + kappa] = acc;
     }
     __syncthreads();
     // dG1 partial += Σ_kappa G0[kappa][r1] (x) S[kappa][c] (outer products)

@@ -211,8 +211,8 @@ struct F3Runner {
 };
 
 // instantiation table: (P0, R1, N1, R2, N2, TT)
-using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 64>;
-using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 64>;
+using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 32>;
+using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 32>;
 using F3_R32 = f3::Dims<2, 32, 2, 32, 4, 32>;
 using F3_R64 = f3::Dims<2, 64, 2, 64, 4, 32>;
 
