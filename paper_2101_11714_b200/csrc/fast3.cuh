@@ -634,13 +634,14 @@ struct G1Blk {
 
 template <class D>
 struct Bwd1Smem {
-  // floats: G1t[C1*R1P] | ST[C1*KP] ([c][kappa]) | S[TT*W1] ([kappa][c]) | G2s[TT*S2]
-  //         | D2s[TT*N] | G0s[TT*S0] | D1b[TT*W1] ; then ints
+  // floats: G1t[C1*R1P] | ST[C1*KP] (S transposed, [c][kappa]) | G2s[TT*S2] (G2 rows,
+  //         overwritten in place by D1) | D2s[TT*N] | G0s[TT*S0] ; then ints
   static constexpr int R1P = D::R1 + 4;
   static constexpr int KP = D::P0 * D::TT + 4;
+  static_assert(D::S2 == D::W1, "D1 reuses the G2 row storage");
   static __host__ __device__ size_t floats() {
     size_t f = static_cast<size_t>(D::C1) * (R1P + KP) +
-               static_cast<size_t>(D::TT) * (2 * D::W1 + D::S2 + D::N + D::S0);
+               static_cast<size_t>(D::TT) * (D::S2 + D::N + D::S0);
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes() {
@@ -671,11 +672,10 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
   extern __shared__ __align__(128) float sm[];
   float* G1t = sm;                                   // C1 x R1P   (G1 slice transposed)
   float* ST = G1t + D::C1 * SM::R1P;                 // C1 x KP    (S transposed)
-  float* S = ST + D::C1 * SM::KP;                    // TT*P0 x C1 (S rows kappa = (slot, a0))
-  float* G2s = S + D::TT * D::W1;                    // TT x S2
+  float* G2s = ST + D::C1 * SM::KP;                  // TT x S2, then D1 in place
   float* D2s = G2s + D::TT * D::S2;                  // TT x N (alpha * grad rows)
   float* G0s = D2s + D::TT * D::N;                   // TT*P0 x R1 (rows kappa)
-  float* D1b = G0s + D::TT * D::S0;                  // TT x W1 (per-lookup D1)
+  float* D1b = G2s;                                  // TT x W1 (per-lookup D1, in place)
   int* lk_slot = reinterpret_cast<int*>(sm + SM::floats());
   int* lk_i2 = lk_slot + D::TT;
   int* slot_i0 = lk_i2 + D::TT;
@@ -794,29 +794,41 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
       if (sl >= 0) members[sstart[sl] + __popc(peers & lt)] = lane;
     }
     for (int i = wid; i < ntl; i += NW) {
-      for (int r = lane; r < D::R2; r += 32) {
-        const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2)[r];
+      float dout[D::R2 / 32 > 0 ? D::R2 / 32 : 1][D::P1];
 #pragma unroll
-        for (int a = 0; a < D::P1; ++a) {
-          const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
-          float v = __fmul_rn(dv.x, gv.x);
-          v = __fmaf_rn(dv.y, gv.y, v);
-          v = __fmaf_rn(dv.z, gv.z, v);
-          v = __fmaf_rn(dv.w, gv.w, v);
-          D1b[i * D::W1 + a * D::R2 + r] = v;
+      for (int rr = 0; rr < (D::R2 + 31) / 32; ++rr) {
+        const int r = rr * 32 + lane;
+        if (r < D::R2) {
+          const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2)[r];
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) {
+            const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
+            float v = __fmul_rn(dv.x, gv.x);
+            v = __fmaf_rn(dv.y, gv.y, v);
+            v = __fmaf_rn(dv.z, gv.z, v);
+            v = __fmaf_rn(dv.w, gv.w, v);
+            dout[rr][a] = v;
+          }
         }
+      }
+      __syncwarp();  // every lane has read its G2 row before the row is overwritten
+#pragma unroll
+      for (int rr = 0; rr < (D::R2 + 31) / 32; ++rr) {
+        const int r = rr * 32 + lane;
+        if (r < D::R2)
+#pragma unroll
+          for (int a = 0; a < D::P1; ++a) D1b[i * D::W1 + a * D::R2 + r] = dout[rr][a];
       }
     }
     __syncthreads();
-    // S(slot)[e] = Σ over the slot's lookups in tile order; written twice:
-    // rows kappa = (slot, a0) x c, and transposed c x kappa
+    // S(slot)[e] = Σ over the slot's lookups in tile order, stored transposed
+    // (c x kappa): read by dG1 (warp-uniform broadcasts) and D0
     for (int q = tid; q < nslots * D::W1; q += kThreads) {
       const int sl = q / D::W1, e = q - sl * D::W1;
       float acc = 0.f;
       for (int j = sstart[sl]; j < sstart[sl + 1]; ++j) acc += D1b[members[j] * D::W1 + e];
       const int a = e / D::R2, r = e - a * D::R2;
       const int kappa = sl * D::P0 + a / D::N1, c = (a % D::N1) * D::R2 + r;
-      S[kappa * D::C1 + c] = acc;
       ST[c * SM::KP + kappa] = acc;
     }
     __syncthreads();
@@ -828,19 +840,8 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
 #pragma unroll
         for (int i = 0; i < GB::RB; ++i) a[i] = G0s[kap * D::R1 + r1b + i];
         float bv[GB::CB];
-        if constexpr (GB::CB % 4 == 0) {
 #pragma unroll
-          for (int j = 0; j < GB::CB; j += 4) {
-            const float4 b = reinterpret_cast<const float4*>(S + kap * D::C1 + cb)[j / 4];
-            bv[j] = b.x;
-            bv[j + 1] = b.y;
-            bv[j + 2] = b.z;
-            bv[j + 3] = b.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < GB::CB; ++j) bv[j] = S[kap * D::C1 + cb + j];
-        }
+        for (int j = 0; j < GB::CB; ++j) bv[j] = ST[(cb + j) * SM::KP + kap];
 #pragma unroll
         for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
