@@ -59,6 +59,27 @@ def flops_per_lookup(rf, cf, ranks):
     return 3 * f
 
 
+def kernel_work(name, rf, cf, ranks, L, B, N, params):
+    """Algorithmic work of one launch of a fast-path kernel (SURVEY §8(d) per-lookup
+    figures, reference chain, no dedup): (flops, hbm_bytes).  3-core chain:
+    fwd  H = G0[i0]·G1[i1] (2·n0·R1·n1R2), y = H·G2[i2] (2·n0n1·R2·n2)
+    bwd1 D1 = D2·G2ᵀ (2·n0n1·n2·R2), dG1 += G0ᵀ·D1 and D0 = D1·G1ᵀ (2·n0·R1·n1R2 each)
+    bwd2 dG2 += Hᵀ·D2 (2·n0n1·R2·n2)."""
+    n0, n1, n2 = cf
+    R1, R2 = ranks[1], ranks[2]
+    head = 2 * n0 * R1 * n1 * R2
+    tail = 2 * n0 * n1 * R2 * n2
+    idx_b = 8 * L
+    table = {
+        "f3_fwd": (L * (head + tail), idx_b + 4 * L * N),
+        "f3_bwd1": (L * (tail + 2 * head), idx_b + 4 * B * N),
+        "f3_bwd2": (L * tail, idx_b + 4 * B * N),
+        "f3_combine": (2 * params, 3 * 4 * params),
+        "pool": (2 * L * N, 4 * L * N + 8 * (B + 1) + 4 * B * N),
+    }
+    return table.get(name)
+
+
 def bytes_per_step(L, B, N, params):
     """Algorithmic HBM bytes per step: indices + offsets read twice (fwd, bwd),
     pooled output written, grad_out read, cores read + written once."""
@@ -302,16 +323,27 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * L * args.steps / (total_ms / 1e3)
 
-    # per-phase breakdown for the roofline (events between pipeline phases)
+    # Per-kernel times for the roofline: the same step re-captured with CUDA event
+    # nodes between its kernels (external event records inside the graph), launched
+    # under the same conditions as the timed region (L2 flushed before each step).
     table.profile(True)
-    for _ in range(3):
-        flush.fill_(1)
-        step()
-    ph_all = table.profile_read()
-    table.profile(False)
     agg = {}
-    for name, ms in ph_all:
-        agg.setdefault(name, []).append(ms)
+    if use_graph:
+        table.graph_begin()
+        step()
+        table.graph_end()
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)
+            table.graph_launch()
+            for name, ms in table.profile_read():
+                agg.setdefault(name, []).append(ms)
+    else:
+        for i in range(3):
+            flush.fill_(1)
+            step()
+            for name, ms in table.profile_read():
+                agg.setdefault(name, []).append(ms)
+    table.profile(False)
     phase_ms = {k: float(np.mean(v)) for k, v in agg.items()}
     dom = max(phase_ms, key=phase_ms.get)
 
@@ -375,12 +407,51 @@ def main():
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     props = torch.cuda.get_device_properties(dev)
     fp32_peak_tf = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
+    fp32_src = (f"derived: {props.multi_processor_count} SMs x 128 FFMA/clk x 2 x {sm_mhz:.0f} "
+                f"MHz (no measured FP32 figure)")
+    try:  # measured by tools/ffma_peak.cu on a B200 of this pool
+        fp = json.load(open(os.path.join(ROOT, "profiles", "fp32_peak.json")))
+        fp32_peak_tf = float(fp["fp32_tflops"])
+        fp32_src = "profiles/fp32_peak.json (measured, tools/ffma_peak.cu: " + fp["how"] + ")"
+    except Exception:  # noqa: BLE001
+        pass
     params = plan.parameter_count()
     ranks = plan.ranks
     f_lookup = flops_per_lookup(cfg["rf"], cfg["cf"], ranks)
     step_flops = f_lookup * L + 2 * params
     step_bytes = bytes_per_step(L, B, N, params)
     step_s = ms_per_step / 1e3
+    # dominant kernel: algorithmic work per launch / its event-timed duration
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json")))
+    except Exception:  # noqa: BLE001
+        ncu = {}
+    work = kernel_work(dom, cfg["rf"], cfg["cf"], ranks, L, B, N, params)
+    dom_s = phase_ms[dom] / 1e3
+    traffic = ncu.get(args.config, {}).get(dom, {}).get("dram_bytes")
+    if work:
+        fl, by = work
+        roofline = {"bound": "fp32", "kernel": dom, "achieved": fl / dom_s / 1e12,
+                    "peak": fp32_peak_tf, "unit": "TFLOP/s", "frac": fl / dom_s / 1e12 / fp32_peak_tf,
+                    "traffic": traffic, "flops_per_launch": fl, "launch_ms": phase_ms[dom],
+                    "peak_source": fp32_src,
+                    "note": "FP32 CUDA-core FFMA chain (no tensor-core path: the reference's fp32 "
+                            "arithmetic order is kept); algorithmic flops, reference chain without "
+                            "dedup; traffic = ncu dram read+write bytes per launch "
+                            "(profiles/ncu_kernels.json)"}
+        roofline_hbm = {"bound": "hbm", "kernel": dom, "achieved": by / dom_s / 1e9,
+                        "peak": hbm_peak, "unit": "GB/s", "frac": by / dom_s / 1e9 / hbm_peak,
+                        "traffic": traffic, "bytes_per_launch": by,
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        roofline = {"bound": "fp32", "kernel": "whole step", "achieved": step_flops / step_s / 1e12,
+                    "peak": fp32_peak_tf, "unit": "TFLOP/s",
+                    "frac": step_flops / step_s / 1e12 / fp32_peak_tf, "traffic": None,
+                    "peak_source": fp32_src}
+        roofline_hbm = {"bound": "hbm", "kernel": "whole step", "achieved": step_bytes / step_s / 1e9,
+                        "peak": hbm_peak, "unit": "GB/s",
+                        "frac": step_bytes / step_s / 1e9 / hbm_peak, "traffic": None,
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     line = {
         "metric": METRIC, "value": value, "unit": "indices/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -394,21 +465,16 @@ def main():
                    "graph": use_graph},
         "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
         "clocks": clk,
-        "roofline": {
-            "bound": "hbm", "achieved": step_bytes / step_s / 1e9, "peak": hbm_peak,
-            "unit": "GB/s", "frac": step_bytes / step_s / 1e9 / hbm_peak,
-            "traffic": None,
-            "scope": "whole step (all kernels); algorithmic bytes = 16B/lookup idx + 16B/bag "
-                     "offsets + 8N B/bag output+grad + 8B/param cores",
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
-        "roofline_fp32": {
+        "roofline": roofline,
+        "roofline_hbm": roofline_hbm,
+        "roofline_step": {
             "bound": "fp32-ffma", "achieved": step_flops / step_s / 1e12, "peak": fp32_peak_tf,
             "unit": "TFLOP/s", "frac": step_flops / step_s / 1e12 / fp32_peak_tf,
-            "flops_per_lookup": f_lookup,
-            "peak_source": f"derived: {props.multi_processor_count} SMs x 128 FMA x 2 x "
-                           f"{sm_mhz:.0f} MHz (nominal)",
-            "note": "algorithmic reference-chain flops (no dedup); pair dedup lets frac exceed "
-                    "the executed-flop rate"},
+            "flops_per_lookup": f_lookup, "hbm_GBs": step_bytes / step_s / 1e9,
+            "hbm_frac": step_bytes / step_s / 1e9 / hbm_peak,
+            "scope": "whole timed step (all kernels), algorithmic reference-chain flops (no dedup); "
+                     "hbm bytes = 16B/lookup idx + 16B/bag offsets + 8N B/bag output+grad + "
+                     "8B/param cores", "peak_source": fp32_src},
         "phases_ms": phase_ms, "dominant_phase": dom,
         "e2e": {"value": e2e_value, "unit": "indices/s",
                 "h2d_bytes_per_step": int(idx.nbytes + off.nbytes + grad.nbytes),

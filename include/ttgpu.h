@@ -145,7 +145,10 @@ int ttgpu_check(ttgpu_table* t); /* sync + report latched validation errors */
 
 /* ---- instrumentation (no reference counterpart; diagnostics only) ------- */
 /* on: record CUDA events between pipeline phases on the table's stream;
- * read: per-phase milliseconds since the last read ("decode;sort_pairs;..."). */
+ * read: per-phase milliseconds since the last read ("decode;sort_pairs;...").
+ * Marks recorded while a graph is being captured (profile on before
+ * ttgpu_graph_begin) become event nodes of that graph: read after each
+ * ttgpu_graph_launch gives that launch's per-kernel times. */
 int ttgpu_profile(ttgpu_table* t, int on);
 int ttgpu_profile_read(ttgpu_table* t, char* names, int64_t names_len, float* ms, int max_phases,
                        int* n_out);

@@ -619,45 +619,59 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
 }
 
 // ------------------------------------------------------------ f3_bwd1 ----
-// dG1 micro-GEMM geometry: NQ output groups x KG slot-row groups = 8 warps;
-// each lane owns a 4 (r1) x CB (c) register block.
+// Register blocking of the two per-tile micro-GEMMs.  Both contract over the
+// tile's kappa = (slot, a0) rows, padded to a multiple of 4 so that the
+// transposed S (ST[c][kappa]) yields 4 kappas per float4 load:
+//   dG1 (R1 x C1) += G0sᵀ · S : thread = RB r1 x CB c, kappa in quads
+//   D0  (kappa x R1) = S · G1ᵀ : thread = 4 kappa x RB0 r1, c in sequence
 template <class D>
 struct G1Blk {
-  // dG1 (R1 x C1) += Σ_kappa G0[kappa][r1] (x) S[kappa][c]: warp w owns the
-  // columns [w*CB, (w+1)*CB), lane owns RB rows of r1; every warp walks all kappa
-  static constexpr int RB = D::R1 > 32 ? D::R1 / 32 : 1;
-  static constexpr int LANES = D::R1 / RB;  // active lanes
-  static constexpr int CB = D::C1 / 8;
-  static constexpr int KG = 1;              // partial rows per run
-  static_assert(D::C1 % 8 == 0 && LANES <= 32, "bad dG1 blocking");
+  static constexpr int RB = D::R1 >= 64 ? 4 : 2;
+  static constexpr int CB = D::R1 >= 64 ? 8 : 4;
+  static constexpr int TR = D::R1 / RB;  // dG1 threads along r1
+  static constexpr int TC = D::C1 / CB;  // dG1 threads along c
+  static constexpr int RB0 = D::R1 >= 64 ? 4 : 2;
+  static constexpr int TR0 = D::R1 / RB0;  // D0 threads along r1
+  static constexpr int KG = 1;             // dG1 partial rows per (CTA, i1 run)
+  static constexpr int CHUNK = D::TT / (kThreads / 32);  // slot-sorted positions per warp (D1)
+  static_assert(TR * TC <= kThreads && TR0 * (D::P0 * D::TT / 4) <= kThreads, "bad blocking");
+  static_assert(D::C1 % CB == 0 && D::R1 % RB == 0 && D::TT % (kThreads / 32) == 0, "bad blocking");
 };
 
 template <class D>
 struct Bwd1Smem {
-  // floats: G1t[C1*R1P] | ST[C1*KP] (S transposed, [c][kappa]) | G2s[TT*S2] (G2 rows,
-  //         overwritten in place by D1) | D2s[TT*N] | G0s[TT*S0] ; then ints
+  // floats: G1t[C1*R1P] | ST[C1*KP] (S transposed, [c][kappa]) | G2s[TT*S2] (G2 rows;
+  //         then split-slot D1 partials in place) | D2s[TT*N] | G0s[KP*R1] ; then ints
   static constexpr int R1P = D::R1 + 4;
   static constexpr int KP = D::P0 * D::TT + 4;
-  static_assert(D::S2 == D::W1, "D1 reuses the G2 row storage");
+  static constexpr int NI = 8 * D::TT + 16 + 256;  // + D0 first-touch bitmap (m0 <= 8192)
+  static_assert(D::S2 == D::W1, "D1 partials reuse the G2 row storage");
+  static_assert((D::P0 * D::TT) % 4 == 0, "kappa quads");
   static __host__ __device__ size_t floats() {
     size_t f = static_cast<size_t>(D::C1) * (R1P + KP) +
-               static_cast<size_t>(D::TT) * (D::S2 + D::N + D::S0);
+               static_cast<size_t>(D::TT) * (D::S2 + D::N) + static_cast<size_t>(KP) * D::R1;
     return (f + 3) / 4 * 4;
   }
-  static __host__ __device__ size_t bytes() {
-    return floats() * 4 + sizeof(int) * (6 * static_cast<size_t>(D::TT) + 8);
-  }
+  static __host__ __device__ size_t bytes() { return floats() * 4 + sizeof(int) * NI; }
 };
 
-// Each CTA owns a contiguous range of i1-tiles.  Consecutive tiles of the
-// same i1 keep accumulating the dG1 partial in registers (warp = (output
-// group, slot-row group)); one partial row per (CTA, i1 run, row group) is
-// flushed at the run's first tile (has1 marks it).  D0 accumulates per
-// (CTA, i0) in a CTA-private global block.  S phase: warp w owns the (slot,
-// 32-column chunk) pairs o = w, w+8, ... and walks the tile's lookups in
-// order -- a fixed accumulation order, no atomics.
+// Each CTA owns a contiguous range of i1-tiles.  Consecutive tiles of the same
+// i1 keep accumulating the dG1 partial in registers; one partial per (CTA, i1
+// run) is flushed at the run's first tile (has1 marks it).  D0 accumulates per
+// (CTA, i0) in a CTA-private global block (stored on first touch, d0mask marks
+// it for the combine).  Per tile:
+//   warp 0  publishes the tile's positions (prefetched during the previous
+//           tile), sorts them by slot (match_any) and marks the slots whose
+//           member range crosses a warp chunk;
+//   stage   D2 rows, G2 rows, G1 slice (transposed), G0 rows (kappa-major);
+//   D1      warp w walks the slot-sorted positions [w*CHUNK, (w+1)*CHUNK):
+//           D1 = D2·G2ᵀ per lookup, summed per slot in registers in tile
+//           order; whole slots go straight to ST, split slots leave one
+//           partial per chunk which a short fold adds in chunk order;
+//   GEMMs   dG1 += G0sᵀ·S and D0 = S·G1ᵀ.
+// Every sum has a fixed order: the result is bitwise reproducible.
 template <class D>
-__global__ void __launch_bounds__(kThreads) f3_bwd1(
+__global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 4 : 1) f3_bwd1(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
     const int* __restrict__ ntiles, const uint32_t* __restrict__ perm,
     const uint16_t* __restrict__ d2, const int32_t* __restrict__ lk_bag,
@@ -667,20 +681,23 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
     float* __restrict__ D0acc, unsigned char* __restrict__ d0mask) {
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
-  constexpr int NW = kThreads / 32;
-  constexpr int CH = (D::R2 + 31) / 32;  // 32-column chunks per (slot, row)
+  constexpr int CH = (D::R2 + 31) / 32;  // rank columns per lane
+  constexpr int KP = SM::KP;
   extern __shared__ __align__(128) float sm[];
-  float* G1t = sm;                                   // C1 x R1P   (G1 slice transposed)
-  float* ST = G1t + D::C1 * SM::R1P;                 // C1 x KP    (S transposed)
-  float* G2s = ST + D::C1 * SM::KP;                  // TT x S2, then D1 in place
-  float* D2s = G2s + D::TT * D::S2;                  // TT x N (alpha * grad rows)
-  float* G0s = D2s + D::TT * D::N;                   // TT*P0 x R1 (rows kappa)
-  float* D1b = G2s;                                  // TT x W1 (per-lookup D1, in place)
+  float* G1t = sm;                        // C1 x R1P
+  float* ST = G1t + D::C1 * SM::R1P;      // C1 x KP
+  float* G2s = ST + D::C1 * KP;           // TT x S2
+  float* D2s = G2s + D::TT * D::S2;       // TT x N (alpha * grad rows)
+  float* G0s = D2s + D::TT * D::N;        // KP x R1 (rows kappa)
   int* lk_slot = reinterpret_cast<int*>(sm + SM::floats());
   int* lk_i2 = lk_slot + D::TT;
   int* slot_i0 = lk_i2 + D::TT;
-  int* members = slot_i0 + D::TT;   // tile positions sorted by slot (stable)
-  int* sstart = members + D::TT;    // nslots + 1 member-list starts
+  int* members = slot_i0 + D::TT;  // tile positions sorted by slot (stable)
+  int* sstart = members + D::TT;   // TT + 1
+  int* d0first = sstart + D::TT + 1;
+  int* splitl = d0first + D::TT;
+  int* misc = splitl + D::TT;      // [0] nsplit [1] i1 [2] ntl [3] nslots [4] next i1
+  unsigned* d0bits = reinterpret_cast<unsigned*>(misc + 16);
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
@@ -690,12 +707,31 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
   const int t_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nt / gridDim.x);
   float* d0acc = D0acc + static_cast<int64_t>(blockIdx.x) * g.m0 * D::S0;
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
-  for (int e = tid; e < g.m0 * D::S0; e += kThreads) d0acc[e] = 0.f;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
-  // dG1 register block: warp -> CB columns, lane -> RB rows
-  const int cb = wid * GB::CB;
-  const int r1b = lane * GB::RB;
-  const bool lane_on = lane < GB::LANES;
+  for (int e = tid; e < 256; e += kThreads) d0bits[e] = 0u;
+  // warp 0: the current tile's per-position indices, and the next tile's in flight
+  Tile c_d{}, n_d{};
+  int c_ns = 0, c_l = 0, c_sl = 0, c_i0 = 0, c_i2 = 0, c_bag = 0;
+  float c_al = 0.f;
+  int n_ns = 0, n_l = 0, n_sl = 0, n_i0 = 0, n_i2 = 0, n_bag = 0;
+  float n_al = 0.f;
+  if (wid == 0 && t_lo < t_hi) {
+    c_d = tiles[t_lo];
+    c_ns = tile_nslots[t_lo];
+    if (lane < c_d.end - c_d.start) {
+      c_l = static_cast<int>(perm[c_d.start + lane]);
+      c_sl = slot_of_pos[c_d.start + lane];
+      c_i0 = tile_i0[c_d.start + lane];
+      c_i2 = d2[c_l];
+      c_al = alpha[c_l];
+      c_bag = lk_bag[c_l];
+    }
+    if (t_lo + 1 < t_hi) n_d = tiles[t_lo + 1];
+  }
+  __syncthreads();  // d0bits / d0m cleared
+  // dG1 register block
+  const int r0 = (tid % GB::TR) * GB::RB, cb0 = (tid / GB::TR) * GB::CB;
+  const bool g1_on = tid < GB::TR * GB::TC;
   float acc1[GB::RB][GB::CB];
 #pragma unroll
   for (int i = 0; i < GB::RB; ++i)
@@ -703,30 +739,66 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
     for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
   int run_start = t_lo;
   for (int t = t_lo; t < t_hi; ++t) {
-    const Tile tl = tiles[t];
-    const int i1 = tl.key;
-    const int ntl = tl.end - tl.start;
-    const int nslots = tile_nslots[t];
-    int my_l = 0;
-    if (tid < ntl) {
-      my_l = static_cast<int>(perm[tl.start + tid]);
-      lk_slot[tid] = slot_of_pos[tl.start + tid];
-      lk_i2[tid] = d2[my_l];
+    if (wid == 0) {
+      // publish tile t: positions, slot member lists, split slots, D0 first touches
+      const int ntl = c_d.end - c_d.start;
+      const bool on = lane < ntl;
+      const int sl = on ? c_sl : -1;
+      if (on) {
+        lk_slot[lane] = sl;
+        lk_i2[lane] = c_i2;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, sl);
+      const unsigned lt = lanemask_lt();
+      if (sl >= 0 && (peers & lt) == 0) sstart[sl] = __popc(peers);  // slot leader: count
+      __syncwarp();
+      const int cnt = lane < c_ns ? sstart[lane] : 0;
+      int inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int ex = inc - cnt;
+      const int base = __shfl_sync(0xffffffffu, ex, sl >= 0 ? sl : 0);
+      __syncwarp();
+      if (sl >= 0) members[base + __popc(peers & lt)] = lane;
+      bool split = false;
+      if (lane < c_ns) {
+        sstart[lane] = ex;
+        split = (ex / GB::CHUNK) != ((ex + cnt - 1) / GB::CHUNK);
+        slot_i0[lane] = c_i0;
+        const unsigned bit = 1u << (c_i0 & 31);
+        const unsigned old = atomicOr(d0bits + (c_i0 >> 5), bit);
+        d0first[lane] = (old & bit) ? 0 : 1;
+        if (!(old & bit)) d0m[c_i0] = 1;
+      }
+      const unsigned sb = __ballot_sync(0xffffffffu, split);
+      if (split) splitl[__popc(sb & lt)] = lane;
+      if (lane == 0) {
+        sstart[c_ns] = ntl;
+        misc[0] = __popc(sb);
+        misc[1] = c_d.key;
+        misc[2] = ntl;
+        misc[3] = c_ns;
+        misc[4] = (t + 1 < t_hi) ? n_d.key : -1;
+      }
     }
-    if (tid < nslots) slot_i0[tid] = tile_i0[tl.start + tid];
-    __syncthreads();  // also: the previous tile's smem reads are done
-    // stage: D2 = alpha * grad rows, G2 slices, G1 transposed, G0 rows
-    if (tid < ntl) {
-      const float al = alpha[my_l];
-      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bag[my_l]) * D::N);
+    __syncthreads();
+    const int i1 = misc[1], ntl = misc[2], nslots = misc[3], nsplit = misc[0];
+    const bool last = misc[4] != i1;
+    const int nk = nslots * D::P0, nk4 = (nk + 3) & ~3;
+    // ---- stage
+    if (wid == 0 && lane < ntl) {
+      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(c_bag) * D::N);
       float4 gv[D::N / 4];
 #pragma unroll
       for (int k = 0; k < D::N / 4; ++k) gv[k] = __ldg(grow + k);
 #pragma unroll
       for (int k = 0; k < D::N / 4; ++k)
-        reinterpret_cast<float4*>(D2s + tid * D::N)[k] =
-            make_float4(__fmul_rn(al, gv[k].x), __fmul_rn(al, gv[k].y), __fmul_rn(al, gv[k].z),
-                        __fmul_rn(al, gv[k].w));
+        reinterpret_cast<float4*>(D2s + lane * D::N)[k] =
+            make_float4(__fmul_rn(c_al, gv[k].x), __fmul_rn(c_al, gv[k].y),
+                        __fmul_rn(c_al, gv[k].z), __fmul_rn(c_al, gv[k].w));
     }
     {
       constexpr int Q = D::S2 / 4;
@@ -748,7 +820,7 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
     }
     {
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
-      constexpr int U = 8;
+      constexpr int U = (D::S1 + kThreads - 1) / kThreads < 8 ? (D::S1 + kThreads - 1) / kThreads : 8;
       for (int e0 = tid; e0 < D::S1; e0 += kThreads * U) {
         float v[U];
 #pragma unroll
@@ -763,151 +835,193 @@ __global__ void __launch_bounds__(kThreads) f3_bwd1(
         }
       }
     }
-    gather_to_smem<8>(G0s, nslots * D::S0, [&](int e) {
+    gather_to_smem<8>(G0s, nk * D::R1, [&](int e) {
       const int s = e / D::S0;
       return G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0);
     });
-    __syncthreads();
-    // per-lookup D1 = D2 (P1 x N2) · G2[i2]ᵀ (N2 x R2): warp w takes lookups
-    // w, w+8, ...; lane owns the rank column r.  Warp 0 also builds the slot
-    // member lists (positions sorted by slot, stable) with one match_any.
-    if (wid == 0) {
-      const int sl = lane < ntl ? lk_slot[lane] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, sl);
-      int cnt = 0;
-      if (lane < nslots) cnt = 0;
-      // count of each slot -> exclusive starts (nslots <= 32: one lane per slot)
-      const unsigned lt = lanemask_lt();
-      if (sl >= 0 && (peers & lt) == 0) sstart[sl] = __popc(peers);  // leader stores the count
-      __syncwarp();
-      cnt = lane < nslots ? sstart[lane] : 0;
-      int inc = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      __syncwarp();
-      if (lane < nslots) sstart[lane] = inc - cnt;
-      if (lane == 31) sstart[nslots] = inc;  // total = ntl (lanes >= nslots add 0)
-      __syncwarp();
-      if (sl >= 0) members[sstart[sl] + __popc(peers & lt)] = lane;
+    for (int e = tid; e < (nk4 - nk) * D::R1; e += kThreads) G0s[nk * D::R1 + e] = 0.f;
+    for (int e = tid; e < (nk4 - nk) * D::C1; e += kThreads) {
+      const int c = e / (nk4 - nk);
+      ST[c * KP + nk + (e - c * (nk4 - nk))] = 0.f;
     }
-    for (int i = wid; i < ntl; i += NW) {
-      float dout[D::R2 / 32 > 0 ? D::R2 / 32 : 1][D::P1];
+    if (wid == 0 && t + 1 < t_hi) {  // prefetch tile t+1 (stage 1: positions)
+      n_ns = tile_nslots[t + 1];
+      if (lane < n_d.end - n_d.start) {
+        n_l = static_cast<int>(perm[n_d.start + lane]);
+        n_sl = slot_of_pos[n_d.start + lane];
+        n_i0 = tile_i0[n_d.start + lane];
+      }
+    }
+    __syncthreads();
+    // ---- D1 per lookup, summed per slot along the slot-sorted positions
+    {
+      const int j0 = wid * GB::CHUNK;
+      const int j1 = j0 + GB::CHUNK < ntl ? j0 + GB::CHUNK : ntl;
+      float acc[CH][D::P1];
+      int run_p = j0;
+      for (int j = j0; j < j1; ++j) {
+        const int m = members[j];
+        const int sl = lk_slot[m];
+        const bool first = j == j0 || lk_slot[members[j - 1]] != sl;
+        if (first) run_p = j;
 #pragma unroll
-      for (int rr = 0; rr < (D::R2 + 31) / 32; ++rr) {
-        const int r = rr * 32 + lane;
-        if (r < D::R2) {
-          const float4 gv = reinterpret_cast<const float4*>(G2s + i * D::S2)[r];
+        for (int rr = 0; rr < CH; ++rr) {
+          const int r = rr * 32 + lane;
+          if (r < D::R2) {
+            const float4 gv = reinterpret_cast<const float4*>(G2s + m * D::S2)[r];
 #pragma unroll
-          for (int a = 0; a < D::P1; ++a) {
-            const float4 dv = reinterpret_cast<const float4*>(D2s + i * D::N)[a];
-            float v = __fmul_rn(dv.x, gv.x);
-            v = __fmaf_rn(dv.y, gv.y, v);
-            v = __fmaf_rn(dv.z, gv.z, v);
-            v = __fmaf_rn(dv.w, gv.w, v);
-            dout[rr][a] = v;
+            for (int a = 0; a < D::P1; ++a) {
+              const float4 dv = reinterpret_cast<const float4*>(D2s + m * D::N)[a];
+              float v = __fmul_rn(dv.x, gv.x);
+              v = __fmaf_rn(dv.y, gv.y, v);
+              v = __fmaf_rn(dv.z, gv.z, v);
+              v = __fmaf_rn(dv.w, gv.w, v);
+              acc[rr][a] = first ? v : acc[rr][a] + v;
+            }
+          }
+        }
+        const bool end = j + 1 == j1 || lk_slot[members[j + 1]] != sl;
+        if (end) {
+          const bool whole = sstart[sl] >= j0 && sstart[sl + 1] <= j1;
+          __syncwarp();  // the partial row (this warp's, already consumed) may be overwritten
+#pragma unroll
+          for (int rr = 0; rr < CH; ++rr) {
+            const int r = rr * 32 + lane;
+            if (r < D::R2) {
+#pragma unroll
+              for (int a = 0; a < D::P1; ++a) {
+                if (whole)
+                  ST[((a % D::N1) * D::R2 + r) * KP + sl * D::P0 + a / D::N1] = acc[rr][a];
+                else
+                  G2s[members[run_p] * D::S2 + a * D::R2 + r] = acc[rr][a];
+              }
+            }
           }
         }
       }
-      __syncwarp();  // every lane has read its G2 row before the row is overwritten
-#pragma unroll
-      for (int rr = 0; rr < (D::R2 + 31) / 32; ++rr) {
-        const int r = rr * 32 + lane;
-        if (r < D::R2)
-#pragma unroll
-          for (int a = 0; a < D::P1; ++a) D1b[i * D::W1 + a * D::R2 + r] = dout[rr][a];
+    }
+    if (wid == 0 && t + 1 < t_hi) {  // prefetch tile t+1 (stage 2: per-lookup data)
+      if (lane < n_d.end - n_d.start) {
+        n_i2 = d2[n_l];
+        n_al = alpha[n_l];
+        n_bag = lk_bag[n_l];
       }
     }
     __syncthreads();
-    // S(slot)[e] = Σ over the slot's lookups in tile order, stored transposed
-    // (c x kappa): read by dG1 (warp-uniform broadcasts) and D0
-    for (int q = tid; q < nslots * D::W1; q += kThreads) {
-      const int sl = q / D::W1, e = q - sl * D::W1;
-      float acc = 0.f;
-      for (int j = sstart[sl]; j < sstart[sl + 1]; ++j) acc += D1b[members[j] * D::W1 + e];
-      const int a = e / D::R2, r = e - a * D::R2;
-      const int kappa = sl * D::P0 + a / D::N1, c = (a % D::N1) * D::R2 + r;
-      ST[c * SM::KP + kappa] = acc;
+    if (nsplit) {  // split slots: add the chunk partials in chunk order
+      for (int q = tid; q < nsplit * D::W1; q += kThreads) {
+        const int sl = splitl[q / D::W1], e = q % D::W1;
+        const int s0 = sstart[sl], s1 = sstart[sl + 1];
+        float acc = G2s[members[s0] * D::S2 + e];
+        for (int p = (s0 / GB::CHUNK + 1) * GB::CHUNK; p < s1; p += GB::CHUNK)
+          acc += G2s[members[p] * D::S2 + e];
+        const int a = e / D::R2, r = e - a * D::R2;
+        ST[((a % D::N1) * D::R2 + r) * KP + sl * D::P0 + a / D::N1] = acc;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // dG1 partial += Σ_kappa G0[kappa][r1] (x) S[kappa][c] (outer products)
-    if (lane_on) {
-      const int nk = nslots * D::P0;
-      for (int kap = 0; kap < nk; ++kap) {
-        float a[GB::RB];
+    // ---- dG1 partial += Σ_kappa G0s[kappa][r1] (x) S[kappa][c]
+    if (g1_on) {
+      for (int kq = 0; kq < nk4 / 4; ++kq) {
+        float4 b[GB::CB];
 #pragma unroll
-        for (int i = 0; i < GB::RB; ++i) a[i] = G0s[kap * D::R1 + r1b + i];
-        float bv[GB::CB];
+        for (int j = 0; j < GB::CB; ++j) b[j] = reinterpret_cast<const float4*>(ST + (cb0 + j) * KP)[kq];
 #pragma unroll
-        for (int j = 0; j < GB::CB; ++j) bv[j] = ST[(cb + j) * SM::KP + kap];
+        for (int kk = 0; kk < 4; ++kk) {
+          float a[GB::RB];
+          const float* ap = G0s + (4 * kq + kk) * D::R1 + r0;
+          if constexpr (GB::RB == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(ap);
+            a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+          } else {
+            const float2 v = *reinterpret_cast<const float2*>(ap);
+            a[0] = v.x; a[1] = v.y;
+          }
+#pragma unroll
+          for (int i = 0; i < GB::RB; ++i)
+#pragma unroll
+            for (int j = 0; j < GB::CB; ++j) {
+              const float bj = kk == 0 ? b[j].x : kk == 1 ? b[j].y : kk == 2 ? b[j].z : b[j].w;
+              acc1[i][j] = __fmaf_rn(a[i], bj, acc1[i][j]);
+            }
+        }
+      }
+    }
+    // ---- D0[kappa][r1] = Σ_c S[kappa][c] · G1[r1][c]  -> CTA D0 block
+    {
+      const int q = tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
+      if (q < nk4 / 4) {
+        float v[4][GB::RB0];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int i = 0; i < GB::RB0; ++i) v[kk][i] = 0.f;
+#pragma unroll 4
+        for (int c = 0; c < D::C1; ++c) {
+          const float4 s4 = reinterpret_cast<const float4*>(ST + c * KP)[q];
+          float gg[GB::RB0];
+          if constexpr (GB::RB0 == 4) {
+            const float4 w = *reinterpret_cast<const float4*>(G1t + c * SM::R1P + rb);
+            gg[0] = w.x; gg[1] = w.y; gg[2] = w.z; gg[3] = w.w;
+          } else {
+            const float2 w = *reinterpret_cast<const float2*>(G1t + c * SM::R1P + rb);
+            gg[0] = w.x; gg[1] = w.y;
+          }
+#pragma unroll
+          for (int i = 0; i < GB::RB0; ++i) {
+            v[0][i] = __fmaf_rn(s4.x, gg[i], v[0][i]);
+            v[1][i] = __fmaf_rn(s4.y, gg[i], v[1][i]);
+            v[2][i] = __fmaf_rn(s4.z, gg[i], v[2][i]);
+            v[3][i] = __fmaf_rn(s4.w, gg[i], v[3][i]);
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int kap = 4 * q + kk;
+          if (kap < nk) {
+            const int s = kap / D::P0, a0 = kap - s * D::P0;
+            float* dst = d0acc + slot_i0[s] * D::S0 + a0 * D::R1 + rb;
+            if (d0first[s]) {
+#pragma unroll
+              for (int i = 0; i < GB::RB0; ++i) dst[i] = v[kk][i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < GB::RB0; ++i) dst[i] += v[kk][i];
+            }
+          }
+        }
+      }
+    }
+    // ---- end of an i1 run (or of this CTA's range): flush the dG1 partial
+    if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
+    if (last || t + 1 == t_hi) {
+      float* dst = part1 + static_cast<int64_t>(run_start) * D::S1;
+      if (g1_on) {
 #pragma unroll
         for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
-          for (int j = 0; j < GB::CB; ++j) acc1[i][j] = __fmaf_rn(a[i], bv[j], acc1[i][j]);
+          for (int j = 0; j < GB::CB; j += 4)
+            *reinterpret_cast<float4*>(dst + (r0 + i) * D::C1 + cb0 + j) =
+                make_float4(acc1[i][j], acc1[i][j + 1], acc1[i][j + 2], acc1[i][j + 3]);
       }
-    }
-    // D0[kappa][r1] = Σ_c ST[c][kappa] · G1t[c][r1], 8 r1 per lane, rows
-    // distributed over warps; accumulated straight into the CTA's D0 block
-    {
-      constexpr int LR = D::R1 / 8;             // lanes per row
-      constexpr int RPW = 32 / LR;              // rows per warp pass
-      const int nk = nslots * D::P0;
-      const int rsub = lane / LR, rb = (lane % LR) * 8;
-      for (int k0 = wid * RPW; k0 < nk; k0 += NW * RPW) {
-        const int kap = k0 + rsub;
-        if (kap < nk) {
-          float v[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = 0.f;
-#pragma unroll 4
-          for (int c = 0; c < D::C1; ++c) {
-            const float sv = ST[c * SM::KP + kap];
-            const float4 g0 = reinterpret_cast<const float4*>(G1t + c * SM::R1P + rb)[0];
-            const float4 g1 = reinterpret_cast<const float4*>(G1t + c * SM::R1P + rb)[1];
-            v[0] = __fmaf_rn(sv, g0.x, v[0]);
-            v[1] = __fmaf_rn(sv, g0.y, v[1]);
-            v[2] = __fmaf_rn(sv, g0.z, v[2]);
-            v[3] = __fmaf_rn(sv, g0.w, v[3]);
-            v[4] = __fmaf_rn(sv, g1.x, v[4]);
-            v[5] = __fmaf_rn(sv, g1.y, v[5]);
-            v[6] = __fmaf_rn(sv, g1.z, v[6]);
-            v[7] = __fmaf_rn(sv, g1.w, v[7]);
-          }
-          const int s = kap / D::P0, a0 = kap - s * D::P0, i0 = slot_i0[s];
-          float4* dst = reinterpret_cast<float4*>(d0acc + i0 * D::S0 + a0 * D::R1 + rb);
-          float4 c0 = dst[0], c1 = dst[1];
-          c0.x += v[0];
-          c0.y += v[1];
-          c0.z += v[2];
-          c0.w += v[3];
-          c1.x += v[4];
-          c1.y += v[5];
-          c1.z += v[6];
-          c1.w += v[7];
-          dst[0] = c0;
-          dst[1] = c1;
-          if (a0 == 0 && rb == 0) d0m[i0] = 1;
-        }
-      }
-    }
-    // end of an i1 run (or of this CTA's range): flush the dG1 partial rows
-    const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
-    if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
-    if (last) {
-      float* dst = part1 + static_cast<int64_t>(run_start) * D::S1;
+      for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
-      for (int i = 0; i < GB::RB; ++i) {
-#pragma unroll
-        for (int j = 0; j < GB::CB; ++j) {
-          if (lane_on) dst[(r1b + i) * D::C1 + cb + j] = acc1[i][j];
-          acc1[i][j] = 0.f;
-        }
-      }
+        for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
       run_start = t + 1;
     }
-    __syncthreads();  // the next tile overwrites slot_i0 / lk_* still read above
+    if (wid == 0) {  // rotate the prefetched tile in; start fetching t+2's descriptor
+      c_d = n_d;
+      c_ns = n_ns;
+      c_l = n_l;
+      c_sl = n_sl;
+      c_i0 = n_i0;
+      c_i2 = n_i2;
+      c_al = n_al;
+      c_bag = n_bag;
+      if (t + 2 < t_hi) n_d = tiles[t + 2];
+    }
+    __syncthreads();  // the next tile overwrites the shared arrays read above
   }
 }
 

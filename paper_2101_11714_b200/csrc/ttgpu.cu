@@ -138,7 +138,11 @@ struct ttgpu_table {
   bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
   bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
   // optional phase timing (CUDA events between pipeline phases)
+  // Marks recorded while the stream is being captured become event-record nodes of
+  // the graph (cudaEventRecordExternal) and stay owned by it: every graph launch
+  // re-records them, so profile_read can be called after each launch.
   bool prof = false;
+  bool graph_marks = false;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
   std::vector<cudaEvent_t> ev_pool;
   void mark(const char* name) {
@@ -150,8 +154,18 @@ struct ttgpu_table {
       e = ev_pool.back();
       ev_pool.pop_back();
     }
-    cudaEventRecord(e, stream);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+      cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal);
+    else
+      cudaEventRecord(e, stream);
     marks.emplace_back(name, e);
+  }
+  void recycle_marks() {
+    for (auto& m : marks) ev_pool.push_back(m.second);
+    marks.clear();
+    graph_marks = false;
   }
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -916,6 +930,16 @@ int ttgpu_grad_buffer(ttgpu_table* t, void** ptr, int64_t* n) {
 int ttgpu_graph_begin(ttgpu_table* t) {
   return guarded([&] {
     require_arg(t->stream != nullptr, "graph capture needs a non-default stream (ttgpu_set_stream)");
+    CK(cudaStreamSynchronize(t->stream));
+    if (t->graph_exec) {
+      cudaGraphExecDestroy(t->graph_exec);
+      t->graph_exec = nullptr;
+    }
+    if (t->graph) {
+      cudaGraphDestroy(t->graph);
+      t->graph = nullptr;
+    }
+    t->recycle_marks();  // marks recorded from here on belong to the new graph
     CK(cudaStreamBeginCapture(t->stream, cudaStreamCaptureModeThreadLocal));
   });
 }
@@ -924,9 +948,8 @@ int ttgpu_graph_end(ttgpu_table* t, int* kernel_nodes, int* total_nodes) {
   return guarded([&] {
     cudaGraph_t g = nullptr;
     CK(cudaStreamEndCapture(t->stream, &g));
-    if (t->graph_exec) cudaGraphExecDestroy(t->graph_exec);
-    if (t->graph) cudaGraphDestroy(t->graph);
     t->graph = g;
+    t->graph_marks = !t->marks.empty();
     CK(cudaGraphInstantiate(&t->graph_exec, g, 0));
     size_t n = 0;
     CK(cudaGraphGetNodes(g, nullptr, &n));
@@ -1025,8 +1048,7 @@ int ttgpu_lookup_row(ttgpu_table* t, int64_t row, void* out) {
 int ttgpu_profile(ttgpu_table* t, int on) {
   return guarded([&] {
     CK(cudaStreamSynchronize(t->stream));
-    for (auto& m : t->marks) t->ev_pool.push_back(m.second);
-    t->marks.clear();
+    if (!t->graph_marks) t->recycle_marks();
     t->prof = on != 0;
   });
 }
@@ -1051,8 +1073,7 @@ int ttgpu_profile_read(ttgpu_table* t, char* names, int64_t names_len, float* ms
       names[names_len - 1] = 0;
     }
     *n_out = n;
-    for (auto& m : t->marks) t->ev_pool.push_back(m.second);
-    t->marks.clear();
+    if (!t->graph_marks) t->recycle_marks();
   });
 }
 

@@ -7,4 +7,4 @@ if [ "$1" != "nobench" ]; then
 fi
 timeout 300 python bench.py --steps 20 --warmup 5 --profile > gpurun_out/bench$TAG.log 2>&1; echo "bench rc=$?"; tail -c 3000 gpurun_out/bench$TAG.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-python tools_launches.py gpurun_out/launches$TAG.csv | tail -15
+python tools/launches.py gpurun_out/launches$TAG.csv | tail -15
