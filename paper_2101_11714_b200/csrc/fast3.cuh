@@ -21,6 +21,7 @@
 #pragma once
 
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_reduce.cuh>
 
 #include "tt_kernels.cuh"
 
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
                                                uint16_t* __restrict__ d2, int32_t* __restrict__ lk_bag,
                                                T* __restrict__ alpha, uint32_t* __restrict__ hist1,
                                                uint32_t* __restrict__ hist2,
+                                               uint32_t* __restrict__ tot1, uint32_t* __restrict__ tot2,
                                                unsigned long long* __restrict__ bad,
                                                int* __restrict__ errs) {
   extern __shared__ uint32_t shist[];  // m1 + m2
@@ -206,8 +208,16 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
   }
   __syncthreads();
   if (tile < NT) {
-    for (int k = threadIdx.x; k < g.m1; k += blockDim.x) hist1[static_cast<int64_t>(k) * NT + tile] = sh1[k];
-    for (int k = threadIdx.x; k < g.m2; k += blockDim.x) hist2[static_cast<int64_t>(k) * NT + tile] = sh2[k];
+    for (int k = threadIdx.x; k < g.m1; k += blockDim.x) {
+      const uint32_t c = sh1[k];
+      hist1[static_cast<int64_t>(k) * NT + tile] = c;
+      if (c) atomicAdd(tot1 + k, c);
+    }
+    for (int k = threadIdx.x; k < g.m2; k += blockDim.x) {
+      const uint32_t c = sh2[k];
+      hist2[static_cast<int64_t>(k) * NT + tile] = c;
+      if (c) atomicAdd(tot2 + k, c);
+    }
   }
   // bags (grid-stride over all CTAs): offsets checks, lookup->bag, backward alpha
   for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < B;
@@ -228,12 +238,15 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
 }
 
 // ------------------------------------------------------------- f3_scan ---
-// CTA 0 handles key 1 (K = m1), CTA 1 key 2 (K = m2).  The (K x NT,
-// key-major) histogram is staged in smem, scanned there and written back as
-// exclusive offsets; each bucket is cut into tiles of <= TT lookups, one
-// thread per tile finding its bucket by binary search.
+// One CTA per kScanKeys consecutive keys (CTAs [0, nb1) key 1, then key 2).
+// The hist kernel also summed every bucket into tot[k] (integer atomics:
+// exact), so each CTA derives its global bases -- lookups, tiles and combine
+// groups of all earlier keys -- from tot[] alone, scans its own keys'
+// (key-major, K x NT) histogram columns into absolute scatter offsets, and
+// cuts its buckets into tiles of <= TT lookups.
 struct ScanArgs {
   uint32_t* hist;
+  const uint32_t* tot;  // K bucket totals
   int32_t* tile_base;   // K + 1
   int32_t* group_base;  // K + 1: combine groups of <= kGroup tiles per bucket (>= 1 each)
   Tile* tiles;
@@ -241,83 +254,123 @@ struct ScanArgs {
   int K, TT;
 };
 
-constexpr int kGroup = 16;  // combine: candidate tiles per warp task
+constexpr int kGroup = 16;     // combine: candidate tiles per warp task
+constexpr int kScanKeys = 16;  // keys per f3_scan CTA
+constexpr int kScanThreads = 256;
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 5); }  // bank-conflict-free chunks
 
-__global__ void __launch_bounds__(1024) f3_scan(ScanArgs a1, ScanArgs a2, int NT, int64_t L) {
-  using Scan = cub::BlockScan<uint32_t, 1024>;
-  __shared__ typename Scan::TempStorage tmp;
-  extern __shared__ uint32_t sh[];  // spad(n) histogram entries, then K + 1 tile bases
-  const ScanArgs& A = blockIdx.x == 0 ? a1 : a2;
+__device__ __forceinline__ uint32_t n_groups(uint32_t tk) {
+  return tk > kGroup ? (tk + kGroup - 1) / kGroup : 1;
+}
+
+__global__ void __launch_bounds__(kScanThreads) f3_scan(ScanArgs a1, ScanArgs a2, int nb1, int NT,
+                                                        int64_t L) {
+  using Scan = cub::BlockScan<uint32_t, kScanThreads>;
+  using Red = cub::BlockReduce<uint32_t, kScanThreads>;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Red::TempStorage red;
+  } tmp;
+  __shared__ uint32_t kb[3][kScanKeys + 1];  // per-key lookup / tile / group starts
+  extern __shared__ uint32_t sh[];           // spad(kScanKeys * NT) histogram entries
+  const bool second = static_cast<int>(blockIdx.x) >= nb1;
+  const ScanArgs& A = second ? a2 : a1;
+  const int blk = second ? blockIdx.x - nb1 : blockIdx.x;
   const int K = A.K, TT = A.TT;
-  const int n = K * NT;
+  const int k0 = blk * kScanKeys, k1 = min(K, k0 + kScanKeys);
   const int tid = threadIdx.x;
-#pragma unroll 8
-  for (int i = tid; i < n; i += 1024) sh[spad(i)] = A.hist[i];
+  // global bases: all keys before k0
+  uint32_t p = 0, t = 0, gq = 0;
+  for (int k = tid; k < k0; k += kScanThreads) {
+    const uint32_t c = A.tot[k];
+    const uint32_t tk = (c + TT - 1) / TT;
+    p += c;
+    t += tk;
+    gq += n_groups(tk);
+  }
+  __shared__ uint32_t bases[3];
+  {
+    const uint32_t v0 = Red(tmp.red).Sum(p);  // aggregates are valid in thread 0 only
+    __syncthreads();
+    const uint32_t v1 = Red(tmp.red).Sum(t);
+    __syncthreads();
+    const uint32_t v2 = Red(tmp.red).Sum(gq);
+    if (tid == 0) {
+      bases[0] = v0;
+      bases[1] = v1;
+      bases[2] = v2;
+    }
+    __syncthreads();
+  }
+  const uint32_t pos_base = bases[0], tile_base = bases[1], group_base = bases[2];
+  if (tid < 32) {  // per-key starts within the CTA (one lane per key)
+    const int k = k0 + tid;
+    const uint32_t c = k < k1 ? A.tot[k] : 0u;
+    const uint32_t tk = (c + TT - 1) / TT;
+    const uint32_t gk = k < k1 ? n_groups(tk) : 0u;
+    uint32_t ic = c, it = tk, ig = gk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y0 = __shfl_up_sync(0xffffffffu, ic, o);
+      const uint32_t y1 = __shfl_up_sync(0xffffffffu, it, o);
+      const uint32_t y2 = __shfl_up_sync(0xffffffffu, ig, o);
+      if (tid >= o) {
+        ic += y0;
+        it += y1;
+        ig += y2;
+      }
+    }
+    if (tid <= kScanKeys) {
+      // exclusive starts for keys k0 .. k0 + kScanKeys (the last entry = CTA total)
+      kb[0][tid] = pos_base + ic - c;
+      kb[1][tid] = tile_base + it - tk;
+      kb[2][tid] = group_base + ig - gk;
+    }
+  }
+  // this CTA's histogram columns -> absolute scatter offsets
+  const int n = (k1 - k0) * NT;
+  uint32_t* hist = A.hist + static_cast<int64_t>(k0) * NT;
+#pragma unroll 4
+  for (int i = tid; i < n; i += kScanThreads) sh[spad(i)] = hist[i];
   __syncthreads();
-  const int per = (n + 1023) / 1024;
+  const int per = (n + kScanThreads - 1) / kScanThreads;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
-  uint32_t s = 0;
-  for (int i = lo; i < hi; ++i) s += sh[spad(i)];
+  uint32_t sacc = 0;
+  for (int i = lo; i < hi; ++i) sacc += sh[spad(i)];
   uint32_t ex;
-  Scan(tmp).ExclusiveSum(s, ex);
+  Scan(tmp.scan).ExclusiveSum(sacc, ex);
+  ex += pos_base;
   for (int i = lo; i < hi; ++i) {
     const uint32_t c = sh[spad(i)];
     sh[spad(i)] = ex;
     ex += c;
   }
   __syncthreads();
-#pragma unroll 8
-  for (int i = tid; i < n; i += 1024) A.hist[i] = sh[spad(i)];
-  const int perk = (K + 1023) / 1024;
-  const int klo = min(K, tid * perk), khi = min(K, klo + perk);
-  uint32_t nt = 0, ng = 0;
-  for (int k = klo; k < khi; ++k) {
-    const uint32_t bs = sh[spad(k * NT)];
-    const uint32_t be = k + 1 < K ? sh[spad((k + 1) * NT)] : static_cast<uint32_t>(L);
-    const uint32_t tk = (be - bs + TT - 1) / TT;
-    nt += tk;
-    ng += tk > kGroup ? (tk + kGroup - 1) / kGroup : 1;
+#pragma unroll 4
+  for (int i = tid; i < n; i += kScanThreads) hist[i] = sh[spad(i)];
+  // per-key tile / group bases and the tiles themselves
+  for (int k = k0 + tid; k < k1; k += kScanThreads) {
+    A.tile_base[k] = static_cast<int32_t>(kb[1][k - k0]);
+    A.group_base[k] = static_cast<int32_t>(kb[2][k - k0]);
   }
-  uint32_t tex, gex;
-  __syncthreads();
-  Scan(tmp).ExclusiveSum(nt, tex);
-  __syncthreads();
-  Scan(tmp).ExclusiveSum(ng, gex);
-  uint32_t* tb = sh + spad(n) + 1;  // K + 1 tile bases
-  for (int k = klo; k < khi; ++k) {
-    const uint32_t bs = sh[spad(k * NT)];
-    const uint32_t be = k + 1 < K ? sh[spad((k + 1) * NT)] : static_cast<uint32_t>(L);
-    const uint32_t tk = (be - bs + TT - 1) / TT;
-    tb[k] = tex;
-    A.tile_base[k] = static_cast<int32_t>(tex);
-    A.group_base[k] = static_cast<int32_t>(gex);
-    tex += tk;
-    gex += tk > kGroup ? (tk + kGroup - 1) / kGroup : 1;
+  if (k1 == K && tid == 0) {
+    const int j = k1 - k0;
+    A.tile_base[K] = static_cast<int32_t>(kb[1][j]);
+    A.group_base[K] = static_cast<int32_t>(kb[2][j]);
+    *A.ntiles = static_cast<int>(kb[1][j]);
   }
-  if (tid == 1023) {
-    tb[K] = tex;
-    A.tile_base[K] = static_cast<int32_t>(tex);
-    A.group_base[K] = static_cast<int32_t>(gex);
-    *A.ntiles = static_cast<int>(tex);
-  }
-  __syncthreads();
-  const uint32_t total = tb[K];
-  for (uint32_t t = tid; t < total; t += 1024) {
-    int lo2 = 0, hi2 = K;  // invariant: tb[lo2] <= t < tb[hi2]
-    while (hi2 - lo2 > 1) {
-      const int mid = (lo2 + hi2) >> 1;
-      if (tb[mid] <= t) lo2 = mid; else hi2 = mid;
+  for (int k = k0; k < k1; ++k) {
+    const uint32_t bs = kb[0][k - k0], be = kb[0][k - k0 + 1];
+    const uint32_t tb = kb[1][k - k0], tk = kb[1][k - k0 + 1] - tb;
+    for (uint32_t q = tid; q < tk; q += kScanThreads) {
+      Tile tl;
+      tl.key = k;
+      tl.start = static_cast<int>(bs + q * TT);
+      tl.end = static_cast<int>(min(be, bs + (q + 1) * TT));
+      tl.pad = 0;
+      A.tiles[tb + q] = tl;
     }
-    const uint32_t bs = sh[spad(lo2 * NT)];
-    const uint32_t be = lo2 + 1 < K ? sh[spad((lo2 + 1) * NT)] : static_cast<uint32_t>(L);
-    Tile tl;
-    tl.key = lo2;
-    tl.start = static_cast<int>(bs + (t - tb[lo2]) * TT);
-    tl.end = static_cast<int>(min(be, bs + (t - tb[lo2] + 1) * TT));
-    tl.pad = 0;
-    A.tiles[t] = tl;
   }
 }
 
@@ -391,8 +444,12 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
                                                   int TL, int NT, const uint32_t* __restrict__ hoff1,
                                                   const uint32_t* __restrict__ hoff2,
                                                   uint32_t* __restrict__ perm1,
-                                                  uint32_t* __restrict__ perm2) {
+                                                  uint32_t* __restrict__ perm2,
+                                                  uint32_t* __restrict__ tot) {
   extern __shared__ uint32_t wc[];  // 8 x max(m1, m2)
+  // f3_scan has consumed the bucket totals: clear them for the next batch
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.m1 + g.m2; k += gridDim.x * blockDim.x)
+    tot[k] = 0u;
   scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc);
   scatter_one(d2, g.m2, L, TL, NT, hoff2, perm2, wc);
 }

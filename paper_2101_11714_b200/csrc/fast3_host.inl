@@ -5,7 +5,7 @@ namespace ttgpu {
 struct F3Bufs {
   DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
-      group_base1, group_base2, gpart, gtouch, counters;
+      group_base1, group_base2, gpart, gtouch, counters, tot;
   f3::Geo geo{};
   int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
@@ -15,14 +15,14 @@ void f3_free(F3Bufs* f) { delete f; }
 
 namespace {
 
-constexpr int kF3MaxHist = 48 * 1024;  // (key x CTA) histogram entries the 1-CTA scan stages
+constexpr int kF3MaxHist = 48 * 1024;  // histogram entries one f3_scan CTA stages (kScanKeys x NT)
 
 // lookups per hist/scatter CTA: 512 * LPT, LPT in {1, 2, ..., 32}; 0 = infeasible.
 // The smallest LPT (most CTAs) whose histogram still fits the 1-CTA scan.
 int f3_lpt(int64_t L, int K) {
   for (int lpt = 1; lpt <= 32; lpt *= 2) {
     const int64_t nt = (L + 512 * lpt - 1) / (512 * lpt);
-    if (nt * K <= kF3MaxHist) return lpt;
+    if (nt * f3::kScanKeys <= kF3MaxHist && nt * K <= (int64_t{1} << 26)) return lpt;
   }
   return 0;
 }
@@ -48,7 +48,7 @@ void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const
   f3::f3_hist<float, LPT><<<grid, 512, smem, st>>>(
       g, idx, L, NT, off, B, w, pooling, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
       f.d2.as<uint16_t>(), lk_bag, alpha, f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
-      t->d_bad(), t->d_struct());
+      f.tot.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, t->d_bad(), t->d_struct());
 }
 
 template <class K>
@@ -78,6 +78,10 @@ struct F3Runner {
     f.d2.ensure(2 * L);
     f.hist1.ensure(4 * static_cast<size_t>(g.m1) * NT);
     f.hist2.ensure(4 * static_cast<size_t>(g.m2) * NT);
+    if (f.tot.cap < 4 * static_cast<size_t>(g.m1 + g.m2)) {  // kept zero between batches by f3_scatter
+      f.tot.ensure(4 * static_cast<size_t>(g.m1 + g.m2));
+      CK(cudaMemsetAsync(f.tot.p, 0, f.tot.cap, st));
+    }
     f.perm1.ensure(4 * L);
     f.perm2.ensure(4 * L);
     f.tiles1.ensure(sizeof(f3::Tile) * f.max_tiles1);
@@ -106,14 +110,18 @@ struct F3Runner {
     }
     t->mark("hist");
     {
-      f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tile_base1.as<int32_t>(), f.group_base1.as<int32_t>(),
-                      f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), g.m1, D::TT};
-      f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tile_base2.as<int32_t>(), f.group_base2.as<int32_t>(),
-                      f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, g.m2, D::TT2};
-      const size_t n = static_cast<size_t>(Kmax) * NT;
-      const size_t sm = 4 * (n + n / 32 + 2 + Kmax + 1);
+      f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tot.as<uint32_t>(), f.tile_base1.as<int32_t>(),
+                      f.group_base1.as<int32_t>(), f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
+                      g.m1, D::TT};
+      f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, f.tile_base2.as<int32_t>(),
+                      f.group_base2.as<int32_t>(), f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
+                      g.m2, D::TT2};
+      const size_t n = static_cast<size_t>(f3::kScanKeys) * NT;
+      const size_t sm = 4 * (n + n / 32 + 2);
       set_smem(f3::f3_scan, sm);
-      f3::f3_scan<<<2, 1024, sm, st>>>(a1, a2, NT, L);
+      const int nb1 = (g.m1 + f3::kScanKeys - 1) / f3::kScanKeys;
+      const int nb2 = (g.m2 + f3::kScanKeys - 1) / f3::kScanKeys;
+      f3::f3_scan<<<nb1 + nb2, f3::kScanThreads, sm, st>>>(a1, a2, nb1, NT, L);
     }
     t->mark("scan");
     {
@@ -121,7 +129,8 @@ struct F3Runner {
       set_smem(f3::f3_scatter, sm);
       f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.d1.as<uint16_t>(), f.d2.as<uint16_t>(), L, TL, NT,
                                           f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
-                                          f.perm1.as<uint32_t>(), f.perm2.as<uint32_t>());
+                                          f.perm1.as<uint32_t>(), f.perm2.as<uint32_t>(),
+                                          f.tot.as<uint32_t>());
     }
     t->mark("scatter");
     {

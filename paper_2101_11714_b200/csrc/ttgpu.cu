@@ -123,6 +123,8 @@ int bits_for(uint64_t n) {  // bits needed to represent values < n
 
 using namespace ttgpu;
 
+__global__ void k_noop() {}
+
 struct ttgpu_table {
   ShapePlan plan;
   std::string name;
@@ -156,8 +158,13 @@ struct ttgpu_table {
     }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(stream, &cs);
-    if (cs == cudaStreamCaptureStatusActive)
+    if (cs == cudaStreamCaptureStatusActive) {
+      // an event node at the graph's root fires as soon as the graph is
+      // launched, before earlier work on the stream has drained: anchor it
+      // behind an empty kernel
+      if (marks.empty()) k_noop<<<1, 32, 0, stream>>>();
       cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal);
+    }
     else
       cudaEventRecord(e, stream);
     marks.emplace_back(name, e);
