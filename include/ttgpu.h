@@ -153,6 +153,72 @@ int ttgpu_profile(ttgpu_table* t, int on);
 int ttgpu_profile_read(ttgpu_table* t, char* names, int64_t names_len, float* ms, int max_phases,
                        int* n_out);
 
+/* ---- LFU cache of hot uncompressed rows (lfu_cache.hpp:18-310,
+ * lfu_cache.cpp:15-126) and the cached EmbeddingLayer (model.hpp:195-284).
+ * Frequencies are dense per-row counters over [0, key_space) (the table's
+ * row count); a small GPU hash table (row -> slot) is probed for every lookup
+ * before any decompression.  Host entry points synchronise; the _device
+ * layer calls run on the table's stream (one host sync per forward reads the
+ * size of the chain part). --------------------------------------------- */
+int ttgpu_cache_create(int64_t capacity, int64_t emb_dim, int64_t refresh_period,
+                       int64_t key_space, int dtype, int device, void* stream, ttgpu_cache** out);
+int ttgpu_cache_destroy(ttgpu_cache* c);
+int ttgpu_cache_set_stream(ttgpu_cache* c, void* stream);
+int64_t ttgpu_cache_default_capacity(int64_t table_rows);              /* :146-148 */
+/* state() / resident_count() / active_accesses() / active_hits() (:150-160, 259-264) */
+int ttgpu_cache_info(ttgpu_cache* c, int* active, int64_t* resident, uint64_t* accesses,
+                     uint64_t* hits);
+int ttgpu_cache_record(ttgpu_cache* c, const int64_t* indices, int64_t L);   /* record (:180-183) */
+/* record_and_partition (:187-219): sizes of the two parts; fetch them with
+ * ttgpu_cache_last_partition (any output may be NULL; weights only if given) */
+int ttgpu_cache_record_and_partition(ttgpu_cache* c, const int64_t* indices, int64_t L,
+                                     const int64_t* offsets, int64_t B, const double* weights,
+                                     int pooling, int64_t* n_cached, int64_t* n_tt);
+int ttgpu_cache_last_partition(ttgpu_cache* c, int64_t* cached_slots, int64_t* cached_rows,
+                               int64_t* cached_offsets, double* cached_weights, int64_t* tt_indices,
+                               int64_t* tt_offsets, double* tt_weights);
+int ttgpu_cache_warmup_finalize(ttgpu_cache* c, ttgpu_table* t);           /* :223-229 */
+int ttgpu_cache_refresh(ttgpu_cache* c, ttgpu_table* t, double* drift);     /* :233-243 */
+int ttgpu_hot_set_drift(const int64_t* prev, int64_t n_prev, const int64_t* cur, int64_t n_cur,
+                        int64_t k, double* out);                            /* lfu_cache.cpp:113-126 */
+int ttgpu_cache_hot_rows(ttgpu_cache* c, int64_t* out, int64_t max, int64_t* n); /* :166-174 */
+int ttgpu_cache_slot_rows(ttgpu_cache* c, int64_t* out);   /* row_at(slot) for every slot */
+int ttgpu_cache_slot_of(ttgpu_cache* c, int64_t row, int64_t* slot);        /* :160-163 */
+int ttgpu_cache_get_rows(ttgpu_cache* c, void* host_out);  /* row_values, capacity x emb_dim */
+int ttgpu_cache_set_row(ttgpu_cache* c, int64_t slot, const void* host_in);
+int ttgpu_cache_store_device_ptr(ttgpu_cache* c, void** ptr);
+int ttgpu_cache_counts_device_ptr(ttgpu_cache* c, void** ptr, int64_t* n); /* for allreduce */
+/* FreqTable (lfu_cache.hpp:18-50): count / size / decay / clear / top_k */
+int ttgpu_cache_freq_count(ttgpu_cache* c, int64_t key, uint64_t* out);
+int ttgpu_cache_freq_size(ttgpu_cache* c, int64_t* out);
+int ttgpu_cache_freq_decay(ttgpu_cache* c, double factor);
+int ttgpu_cache_freq_clear(ttgpu_cache* c);
+int ttgpu_cache_top_k(ttgpu_cache* c, ttgpu_table* t, int64_t k, int64_t* rows, uint64_t* counts,
+                      int64_t* n);
+/* cached EmbeddingLayer::forward (model.hpp:210-223): partition, cached pooling,
+ * forward_bags on the chain part, combine_partition_outputs */
+int ttgpu_cache_forward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const int64_t* indices,
+                        int64_t L, const int64_t* offsets, int64_t B, const double* weights,
+                        int pooling, int save, void* out);
+int ttgpu_cache_forward_device(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx,
+                               const int64_t* d_indices, int64_t L, const int64_t* d_offsets,
+                               int64_t B, const double* d_weights, int pooling, int save,
+                               void* d_out);
+/* EmbeddingLayer::backward (model.hpp:237-262): chain gradients -> the table's
+ * gradient buffer, slot gradients -> the cache; EmbeddingLayer::step (:265-284) */
+int ttgpu_cache_backward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const void* grad_out,
+                         int64_t grad_len);
+int ttgpu_cache_backward_device(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx,
+                                const void* d_grad_out);
+int ttgpu_cache_step(ttgpu_cache* c, ttgpu_table* t, double lr);
+/* fused backward + step: SGD applied in both reductions' epilogues (async) */
+int ttgpu_cache_backward_step_device(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx,
+                                     const void* d_grad_out, double lr);
+int ttgpu_cache_slot_grads(ttgpu_cache* c, void* host_grads, uint8_t* touched);
+/* cached_sgd_update(SlotGradients, lr) with caller rows (:246-257) */
+int ttgpu_cache_sgd_update(ttgpu_cache* c, const int64_t* slots, int64_t n, const void* rows,
+                           double lr);
+
 /* ---- EmbeddingStats (embedding_stats.hpp:12-23) -------------------------- */
 void ttgpu_stats_reset(void);
 uint64_t ttgpu_stats_rows(void);            /* tt_rows_computed */

@@ -164,6 +164,8 @@ class RefImpl:
         L.ref_cache_freq.restype = C.c_uint64
         L.ref_cache_top_k.restype = C.c_int64
         L.ref_stats_rows.restype = C.c_uint64
+        L.ref_layer_freq.restype = C.c_uint64
+        L.ref_layer_cache_rows.restype = C.c_int64
 
     def check(self, st):
         if st:
@@ -190,6 +192,9 @@ class RefImpl:
     # ---- tables ----
     def table(self, plan: Plan, dtype=np.float32, name="tt-table"):
         return RefTable(self, plan, dtype, name)
+
+    def layer(self, plan: Plan, cache_capacity=-1, name="tt-layer"):
+        return RefLayer(self, plan, cache_capacity, name)
 
     # ---- streams (reference RNG, libstdc++-specific) ----
     def normal(self, seed, n):
@@ -415,3 +420,80 @@ class RefCache:
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+class RefLayer:
+    """EmbeddingLayer<float> over a TT table with an optional LFU cache
+    (model.hpp:148-284) from the reference build: the reference's own
+    composition of record_and_partition / forward_bags / backward_bags /
+    sgd_step / cached_sgd_update / warmup_finalize / refresh."""
+
+    def __init__(self, ref: RefImpl, plan: Plan, cache_capacity=-1, name="tt-layer"):
+        self.ref, self.plan = ref, plan
+        d = len(plan.row_factors)
+        h = C.c_void_p()
+        ref.check(ref.lib.ref_layer_create(
+            C.c_int64(plan.num_rows), C.c_int64(plan.emb_dim), C.c_int(d),
+            _p(np.asarray(plan.row_factors, np.int64)), _p(np.asarray(plan.col_factors, np.int64)),
+            _p(np.asarray(plan.ranks, np.int64)), C.c_int64(cache_capacity), name.encode(),
+            C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.ref.lib.ref_layer_destroy(self.h)
+        except Exception:
+            pass
+
+    def init(self, seed):
+        self.ref.check(self.ref.lib.ref_layer_init(self.h, C.c_uint64(seed)))
+
+    def forward(self, idx, off, w=None, pooling=0):
+        idx = np.ascontiguousarray(idx, np.int64)
+        off = np.ascontiguousarray(off, np.int64)
+        w = None if w is None else np.ascontiguousarray(w, np.float64)
+        B = len(off) - 1
+        out = np.zeros((B, self.plan.emb_dim), np.float32)
+        self.ref.check(self.ref.lib.ref_layer_forward(self.h, _p(idx), C.c_int64(len(idx)), _p(off),
+                                                      C.c_int64(B), _p(w), C.c_int(pooling), _p(out)))
+        return out
+
+    def backward(self, idx, off, grad, w=None, pooling=0):
+        idx = np.ascontiguousarray(idx, np.int64)
+        off = np.ascontiguousarray(off, np.int64)
+        w = None if w is None else np.ascontiguousarray(w, np.float64)
+        g = np.ascontiguousarray(grad, np.float32)
+        self.ref.check(self.ref.lib.ref_layer_backward(
+            self.h, _p(idx), C.c_int64(len(idx)), _p(off), C.c_int64(len(off) - 1), _p(w),
+            C.c_int(pooling), _p(g), C.c_int64(g.size)))
+
+    def step(self, lr):
+        self.ref.check(self.ref.lib.ref_layer_step(self.h, C.c_double(lr)))
+
+    def finalize_warmup(self):
+        self.ref.check(self.ref.lib.ref_layer_finalize_warmup(self.h))
+
+    def refresh(self):
+        d = C.c_double()
+        self.ref.check(self.ref.lib.ref_layer_refresh(self.h, C.byref(d)))
+        return d.value
+
+    def core(self, k):
+        rf, cf, rk = self.plan.row_factors, self.plan.col_factors, self.plan.ranks
+        out = np.zeros(rk[k] * rf[k] * cf[k] * rk[k + 1], np.float32)
+        self.ref.lib.ref_layer_get_core(self.h, C.c_int(k), _p(out))
+        return out
+
+    def cache_info(self):
+        r, a, h, act = C.c_int64(), C.c_uint64(), C.c_uint64(), C.c_int()
+        self.ref.lib.ref_layer_cache_info(self.h, C.byref(r), C.byref(a), C.byref(h), C.byref(act))
+        return dict(resident=r.value, accesses=a.value, hits=h.value, active=bool(act.value))
+
+    def cache_rows(self, capacity):
+        rows = np.zeros(capacity, np.int64)
+        vals = np.zeros((capacity, self.plan.emb_dim), np.float32)
+        self.ref.lib.ref_layer_cache_rows(self.h, _p(rows), _p(vals))
+        return rows, vals
+
+    def freq(self, row):
+        return int(self.ref.lib.ref_layer_freq(self.h, C.c_int64(row)))

@@ -27,6 +27,7 @@
 #include "ttrec/embedding_stats.hpp"
 #include "ttrec/initializer.hpp"
 #include "ttrec/lfu_cache.hpp"
+#include "ttrec/model.hpp"
 #include "ttrec/shape_plan.hpp"
 #include "ttrec/tt_table.hpp"
 
@@ -471,6 +472,94 @@ int64_t ref_cache_top_k(void* c, int64_t k, int64_t* out) {
   auto v = static_cast<RefCache*>(c)->c->freq().top_k(static_cast<size_t>(k));
   std::memcpy(out, v.data(), v.size() * 8);
   return (int64_t)v.size();
+}
+
+// ---- EmbeddingLayer<float> with a TT table + LFU cache (model.hpp:148-284) --
+// The reference's own composition of the cache with forward_bags /
+// backward_bags / sgd_step; used to record golden training trajectories.
+
+struct RefLayer {
+  std::unique_ptr<EmbeddingLayer<float>> l;
+};
+
+int ref_layer_create(int64_t rows, int64_t emb, int tt_dim, const int64_t* rf, const int64_t* cf,
+                     const int64_t* rk, int64_t cache_capacity, const char* name, void** out) {
+  return guarded([&] {
+    ShapePlan p;
+    p.num_rows = rows;
+    p.emb_dim = emb;
+    p.tt_dim = tt_dim;
+    p.row_factors.assign(rf, rf + tt_dim);
+    p.col_factors.assign(cf, cf + tt_dim);
+    p.ranks.assign(rk, rk + tt_dim + 1);
+    TableConfig cfg;
+    cfg.num_rows = rows;
+    cfg.use_tt = true;
+    cfg.tt_dim = tt_dim;
+    cfg.plan = p;
+    cfg.use_cache = cache_capacity >= 0;
+    cfg.cache_capacity = cache_capacity > 0 ? cache_capacity : 0;
+    auto* rl = new RefLayer;
+    rl->l = std::make_unique<EmbeddingLayer<float>>(cfg, emb, name);
+    *out = rl;
+  });
+}
+void ref_layer_destroy(void* l) { delete static_cast<RefLayer*>(l); }
+
+int ref_layer_init(void* l, uint64_t seed) {
+  return guarded([&] { static_cast<RefLayer*>(l)->l->init(InitSpec::sampled_gaussian(), seed); });
+}
+
+int ref_layer_forward(void* l, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                      const double* w, int pooling, float* out) {
+  return guarded([&] {
+    std::vector<float> o;
+    static_cast<RefLayer*>(l)->l->forward(make_batch(idx, L, off, B, w, pooling), o,
+                                          kDefaultMicroBatch, true);
+    std::memcpy(out, o.data(), o.size() * sizeof(float));
+  });
+}
+
+int ref_layer_backward(void* l, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                       const double* w, int pooling, const float* grad, int64_t n) {
+  return guarded([&] {
+    static_cast<RefLayer*>(l)->l->backward(make_batch(idx, L, off, B, w, pooling),
+                                           std::span<const float>(grad, static_cast<size_t>(n)));
+  });
+}
+
+int ref_layer_step(void* l, double lr) {
+  return guarded([&] { static_cast<RefLayer*>(l)->l->step(lr); });
+}
+int ref_layer_finalize_warmup(void* l) {
+  return guarded([&] { static_cast<RefLayer*>(l)->l->finalize_warmup(); });
+}
+int ref_layer_refresh(void* l, double* drift) {
+  return guarded([&] { *drift = static_cast<RefLayer*>(l)->l->refresh_cache(); });
+}
+void ref_layer_get_core(void* l, int k, float* out) {
+  const auto& c = static_cast<RefLayer*>(l)->l->tt()->core(k);
+  std::memcpy(out, c.data(), c.size() * sizeof(float));
+}
+void ref_layer_cache_info(void* l, int64_t* resident, uint64_t* accesses, uint64_t* hits,
+                          int* active) {
+  const auto* c = static_cast<RefLayer*>(l)->l->cache();
+  *resident = c->resident_count();
+  *accesses = c->active_accesses();
+  *hits = c->active_hits();
+  *active = c->state() == CacheState::Active ? 1 : 0;
+}
+int64_t ref_layer_cache_rows(void* l, int64_t* slot_rows, float* values) {
+  const auto* c = static_cast<RefLayer*>(l)->l->cache();
+  for (int64_t s = 0; s < c->capacity(); ++s) {
+    slot_rows[s] = c->row_at(s);
+    auto v = c->row_values(s);
+    std::memcpy(values + s * c->emb_dim(), v.data(), v.size() * sizeof(float));
+  }
+  return c->capacity();
+}
+uint64_t ref_layer_freq(void* l, int64_t row) {
+  return static_cast<RefLayer*>(l)->l->cache()->freq().count(row);
 }
 
 // ---- CPU baseline timing: the reference's own OpenMP path -----------------

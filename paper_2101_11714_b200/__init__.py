@@ -24,3 +24,12 @@ from .ttrec import (  # noqa: F401
     sgd_step,
     uniform_indices,
 )
+from . import lfu_cache  # noqa: F401,E402
+from .lfu_cache import (  # noqa: F401,E402
+    CachePartition,
+    CacheState,
+    EmbeddingLayer,
+    FreqTable,
+    LfuCache,
+    hot_set_drift,
+)

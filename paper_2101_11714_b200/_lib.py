@@ -60,6 +60,39 @@ _SIGS = {
                                      C.POINTER(C.c_int)]),
     "ttgpu_sync": (C.c_int, [vp]),
     "ttgpu_check": (C.c_int, [vp]),
+    # LFU cache (lfu_cache.hpp) + cached EmbeddingLayer (model.hpp:195-284)
+    "ttgpu_cache_create": (C.c_int, [i64, i64, i64, i64, C.c_int, C.c_int, vp, vpp]),
+    "ttgpu_cache_destroy": (C.c_int, [vp]),
+    "ttgpu_cache_set_stream": (C.c_int, [vp, vp]),
+    "ttgpu_cache_default_capacity": (i64, [i64]),
+    "ttgpu_cache_info": (C.c_int, [vp, vp, vp, vp, vp]),
+    "ttgpu_cache_record": (C.c_int, [vp, vp, i64]),
+    "ttgpu_cache_record_and_partition": (C.c_int, [vp, vp, i64, vp, i64, vp, C.c_int, vp, vp]),
+    "ttgpu_cache_last_partition": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ttgpu_cache_warmup_finalize": (C.c_int, [vp, vp]),
+    "ttgpu_cache_refresh": (C.c_int, [vp, vp, vp]),
+    "ttgpu_hot_set_drift": (C.c_int, [vp, i64, vp, i64, i64, vp]),
+    "ttgpu_cache_hot_rows": (C.c_int, [vp, vp, i64, vp]),
+    "ttgpu_cache_slot_rows": (C.c_int, [vp, vp]),
+    "ttgpu_cache_slot_of": (C.c_int, [vp, i64, vp]),
+    "ttgpu_cache_get_rows": (C.c_int, [vp, vp]),
+    "ttgpu_cache_set_row": (C.c_int, [vp, i64, vp]),
+    "ttgpu_cache_store_device_ptr": (C.c_int, [vp, vpp]),
+    "ttgpu_cache_counts_device_ptr": (C.c_int, [vp, vpp, vp]),
+    "ttgpu_cache_freq_count": (C.c_int, [vp, i64, vp]),
+    "ttgpu_cache_freq_size": (C.c_int, [vp, vp]),
+    "ttgpu_cache_freq_decay": (C.c_int, [vp, C.c_double]),
+    "ttgpu_cache_freq_clear": (C.c_int, [vp]),
+    "ttgpu_cache_top_k": (C.c_int, [vp, vp, i64, vp, vp, vp]),
+    "ttgpu_cache_forward": (C.c_int, [vp, vp, vp, vp, i64, vp, i64, vp, C.c_int, C.c_int, vp]),
+    "ttgpu_cache_forward_device": (C.c_int, [vp, vp, vp, vp, i64, vp, i64, vp, C.c_int, C.c_int,
+                                             vp]),
+    "ttgpu_cache_backward": (C.c_int, [vp, vp, vp, vp, i64]),
+    "ttgpu_cache_backward_device": (C.c_int, [vp, vp, vp, vp]),
+    "ttgpu_cache_step": (C.c_int, [vp, vp, C.c_double]),
+    "ttgpu_cache_backward_step_device": (C.c_int, [vp, vp, vp, vp, C.c_double]),
+    "ttgpu_cache_slot_grads": (C.c_int, [vp, vp, vp]),
+    "ttgpu_cache_sgd_update": (C.c_int, [vp, vp, i64, vp, C.c_double]),
     "ttgpu_stats_reset": (None, []),
     "ttgpu_stats_rows": (C.c_uint64, []),
     "ttgpu_stats_peak_workspace": (C.c_uint64, []),

@@ -1190,3 +1190,5 @@ int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
 }
 
 }  // extern "C"
+
+#include "lfu_cache_host.inl"

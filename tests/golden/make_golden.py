@@ -149,6 +149,62 @@ def cache_case(ref):
     return d
 
 
+CACHE_TRAIN = dict(rows=20000, cap=48, lr=0.002, steps=14, finalize_after=5, refresh_after=10,
+                   bags=128, pf=3, zipf=1.2)
+
+
+def cache_train_batches(ref, plan, c=CACHE_TRAIN):
+    """Per-step (idx, off, weights, pooling, grad) of the cached-layer trajectory."""
+    out = []
+    for s in range(c["steps"]):
+        idx, off = ref.zipf_batch(c["rows"], c["zipf"], 500 + s, c["bags"], c["pf"])
+        w = (0.5 + 0.5 * np.abs(ref.normal(700 + s, len(idx)))) if s % 2 else None
+        pooling = 1 if s % 3 == 2 else 0
+        grad = ref.normal(900 + s, c["bags"] * plan.emb_dim).astype(np.float32)
+        out.append((idx, off, w, pooling, grad))
+    return out
+
+
+def cache_train(ref, plan, c=CACHE_TRAIN):
+    """EmbeddingLayer with a TT table + LFU cache (model.hpp:195-284) trained on a
+    Zipf(1.2) multi-hot stream: warm-up steps, warmup_finalize, cached training
+    steps, one refresh.  Records every step's output, the cache counters, the
+    admitted rows/values, the drift and the final cores."""
+    layer = ref.layer(plan, c["cap"], "cached")
+    layer.init(5)
+    d = dict(rf=np.array(plan.row_factors, np.int64), cf=np.array(plan.col_factors, np.int64),
+             rk=np.array(plan.ranks, np.int64))
+    for k in range(len(plan.row_factors)):
+        d[f"init_core{k}"] = layer.core(k)
+    outs, acc, hits = [], [], []
+    for s, (idx, off, w, pooling, grad) in enumerate(cache_train_batches(ref, plan, c)):
+        d[f"idx{s}"], d[f"off{s}"], d[f"grad{s}"] = idx, off, grad
+        if w is not None:
+            d[f"w{s}"] = w
+        outs.append(layer.forward(idx, off, w, pooling))
+        layer.backward(idx, off, grad, w, pooling)
+        layer.step(c["lr"])
+        info = layer.cache_info()
+        acc.append(info["accesses"])
+        hits.append(info["hits"])
+        if s == c["finalize_after"]:
+            layer.finalize_warmup()
+            d["fin_rows"], d["fin_values"] = layer.cache_rows(c["cap"])
+        if s == c["refresh_after"]:
+            d["drift"] = np.array([layer.refresh()])
+            d["ref_rows"], d["ref_values"] = layer.cache_rows(c["cap"])
+    d["out"] = np.stack(outs)
+    d["accesses"] = np.array(acc, np.int64)
+    d["hits"] = np.array(hits, np.int64)
+    d["end_rows"], d["end_values"] = layer.cache_rows(c["cap"])
+    d["freq_end_rows"] = np.array([layer.freq(int(r)) for r in d["end_rows"]], np.int64)
+    for k in range(len(plan.row_factors)):
+        d[f"core{k}"] = layer.core(k)
+    for key, v in d.items():
+        assert np.all(np.isfinite(v)), f"cache_train: non-finite {key}"
+    return d
+
+
 def zipf_stream(ref):
     """First 4096 draws of the cfg2 index stream (Zipf 1.05 over 10,131,227 rows, seed 7)."""
     idx, off = ref.zipf_batch(10131227, 1.05, 7, 4096, 1)
@@ -163,6 +219,10 @@ def main():
     np.savez_compressed(os.path.join(HERE, "cfg1.npz"), **cfg1(ref))
     np.savez_compressed(os.path.join(HERE, "cache_case.npz"), **cache_case(ref))
     np.savez_compressed(os.path.join(HERE, "zipf_stream.npz"), **zipf_stream(ref))
+    p3, _ = ref.plan_shapes(CACHE_TRAIN["rows"], 16, 3, 16, [25, 28, 30], [2, 2, 4])
+    np.savez_compressed(os.path.join(HERE, "cache_train3.npz"), **cache_train(ref, p3))
+    p2, _ = ref.plan_shapes(CACHE_TRAIN["rows"], 8, 2, 4)
+    np.savez_compressed(os.path.join(HERE, "cache_train2.npz"), **cache_train(ref, p2))
     for fn in sorted(os.listdir(HERE)):
         print(fn, os.path.getsize(os.path.join(HERE, fn)))
 
