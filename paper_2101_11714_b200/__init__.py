@@ -33,3 +33,4 @@ from .lfu_cache import (  # noqa: F401,E402
     LfuCache,
     hot_set_drift,
 )
+from . import sharding  # noqa: F401,E402

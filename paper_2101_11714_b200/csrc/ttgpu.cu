@@ -5,6 +5,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
@@ -26,6 +29,25 @@ namespace ttgpu {
 namespace {
 
 thread_local std::string g_last_error;
+
+// TTGPU_TRACE=1: host-side stage timer for the host-pointer entry points
+// (synchronises the stream at every stage; diagnostics only).
+struct HostTrace {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostTrace(cudaStream_t s) : on(std::getenv("TTGPU_TRACE") != nullptr), st(s) {
+    t0 = std::chrono::steady_clock::now();
+  }
+  void operator()(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ttgpu trace] %-24s %9.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(t - t0).count());
+    t0 = t;
+  }
+};
 std::atomic<uint64_t> g_rows{0};
 std::atomic<uint64_t> g_ws_cur{0};
 std::atomic<uint64_t> g_ws_peak{0};
@@ -125,6 +147,7 @@ using namespace ttgpu;
 
 __global__ void k_noop() {}
 
+struct ttgpu_ctx;
 struct ttgpu_table {
   ShapePlan plan;
   std::string name;
@@ -136,6 +159,11 @@ struct ttgpu_table {
   DevPlan dp{};
   int64_t total = 0;         // total core elements (with alignment padding)
   DevBuf cores, grads, pair_tab, errs, lk_rows, lk_out;
+  // destroyed forward contexts keep their device workspace here for the next
+  // ttgpu_ctx_create (the reference returns a fresh ForwardContext from every
+  // forward_bags call; without recycling each would re-cudaMalloc its buffers)
+  std::vector<ttgpu_ctx*> ctx_pool;
+  unsigned long long* h_errs = nullptr;  // pinned host mirror of errs
   uint64_t generation = 0;
   bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
   bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
@@ -177,6 +205,7 @@ struct ttgpu_table {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   ~ttgpu_table() {
+    if (h_errs) cudaFreeHost(h_errs);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (auto& m : marks) cudaEventDestroy(m.second);
@@ -596,8 +625,10 @@ void check_ctx(ttgpu_table* t, ttgpu_ctx* c) {
 }
 
 void raise_latched(ttgpu_table* t, const int64_t* host_idx) {
-  unsigned long long h[3];
-  CK(cudaMemcpyAsync(h, t->errs.p, sizeof(h), cudaMemcpyDeviceToHost, t->stream));
+  if (!t->h_errs) CK(cudaHostAlloc(reinterpret_cast<void**>(&t->h_errs), 32, cudaHostAllocDefault));
+  unsigned long long* h = t->h_errs;  // pinned: the read rides the same sync as the caller's copies
+  CK(cudaMemcpyAsync(h, t->errs.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     t->stream));
   CK(cudaStreamSynchronize(t->stream));
   const int sflags = static_cast<int>(h[2] & 0xffffffffu);
   if (sflags == 0 && h[0] == ULLONG_MAX) return;
@@ -620,7 +651,9 @@ void raise_latched(ttgpu_table* t, const int64_t* host_idx) {
 // (index_batch.hpp:41-56); index range is checked on the device.
 void validate_host(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* off, int64_t B) {
   require_arg(off != nullptr && off[0] == 0, "offsets must start at 0");
-  for (int64_t b = 0; b < B; ++b) require_arg(off[b] <= off[b + 1], "offsets must be non-decreasing");
+  bool monotone = true;  // branch-free scan (no per-element message construction)
+  for (int64_t b = 0; b < B; ++b) monotone &= off[b] <= off[b + 1];
+  require_arg(monotone, "offsets must be non-decreasing");
   require_arg(off[B] == L, cat("offsets end at ", off[B], " but there are ", L, " indices"));
   (void)idx;
   (void)t;
@@ -723,6 +756,8 @@ int ttgpu_destroy(ttgpu_table* t) {
   return guarded([&] {
     if (t) {
       cudaStreamSynchronize(t->stream);
+      for (ttgpu_ctx* c : t->ctx_pool) delete c;
+      t->ctx_pool.clear();
       delete t;
     }
   });
@@ -794,7 +829,22 @@ int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out) {
 
 int ttgpu_ctx_create(ttgpu_table* t, ttgpu_ctx** out) {
   return guarded([&] {
-    auto* c = new ttgpu_ctx;
+    ttgpu_ctx* c;
+    if (t && !t->ctx_pool.empty()) {  // recycle a destroyed context's workspace
+      c = t->ctx_pool.back();
+      t->ctx_pool.pop_back();
+      c->fast = false;
+      c->snapshot = 0;
+      c->valid = false;
+      c->L = c->B = 0;
+      c->pooling = 0;
+      c->save = false;
+      c->has_w = false;
+      c->exact = true;
+      c->w_dev = nullptr;
+    } else {
+      c = new ttgpu_ctx;
+    }
     c->table = t;
     *out = c;
   });
@@ -802,7 +852,14 @@ int ttgpu_ctx_create(ttgpu_table* t, ttgpu_ctx** out) {
 
 int ttgpu_ctx_destroy(ttgpu_ctx* c) {
   return guarded([&] {
-    if (c && c->table) cudaStreamSynchronize(c->table->stream);
+    if (!c) return;
+    ttgpu_table* t = c->table;
+    if (t) cudaStreamSynchronize(t->stream);
+    if (t && t->ctx_pool.size() < 4) {
+      c->valid = false;
+      t->ctx_pool.push_back(c);
+      return;
+    }
     delete c;
   });
 }
@@ -813,7 +870,10 @@ int ttgpu_forward(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* 
   return guarded([&] {
     require_arg(c != nullptr, "forward needs a context");
     require_arg(L >= 0 && B >= 0, "negative batch size");
+    HostTrace tr(t->stream);
+    tr("enter");
     validate_host(t, idx, L, off, B);
+    tr("validate_host");
     require_arg(micro_batch >= 1, cat("micro_batch must be positive, got ", micro_batch));
     c->valid = false;
     c->h_idx.ensure(8 * std::max<int64_t>(L, 1));
@@ -827,17 +887,21 @@ int ttgpu_forward(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* 
       CK(cudaMemcpyAsync(c->h_w.p, w, 8 * L, cudaMemcpyHostToDevice, t->stream));
       dw = c->h_w.as<double>();
     }
+    tr("h2d");
     if (t->dtype == TTGPU_F64)
       forward_impl<double>(t, c, c->h_idx.as<int64_t>(), L, c->h_off.as<int64_t>(), B, dw,
                            pooling, save != 0, c->h_out.as<double>(), t->exact);
     else
       forward_impl<float>(t, c, c->h_idx.as<int64_t>(), L, c->h_off.as<int64_t>(), B, dw, pooling,
                           save != 0, c->h_out.as<float>(), t->exact);
+    tr("kernels");
     if (B > 0)
       CK(cudaMemcpyAsync(out, c->h_out.p, t->esz * B * t->plan.emb_dim, cudaMemcpyDeviceToHost,
                          t->stream));
+    tr("d2h");
     try {
       raise_latched(t, idx);
+      tr("raise_latched");
     } catch (...) {
       c->valid = false;
       throw;
@@ -915,13 +979,17 @@ int ttgpu_backward_sgd(ttgpu_table* t, ttgpu_ctx* c, int64_t L, int64_t B, const
                     B, ")"));
     require_arg(grad_len == B * t->plan.emb_dim,
                 cat("grad_output has ", grad_len, " elements, expected ", B * t->plan.emb_dim));
+    HostTrace tr(t->stream);
+    tr("enter");
     c->h_grad.ensure(t->esz * std::max<int64_t>(grad_len, 1));
     if (grad_len > 0)
       CK(cudaMemcpyAsync(c->h_grad.p, grad, t->esz * grad_len, cudaMemcpyHostToDevice, t->stream));
+    tr("h2d");
     if (t->dtype == TTGPU_F64)
       backward_impl<double>(t, c, c->h_grad.as<double>(), 1, lr);
     else
       backward_impl<float>(t, c, c->h_grad.as<float>(), 1, lr);
+    tr("kernels");
     ++t->generation;
     CK(cudaStreamSynchronize(t->stream));
   });

@@ -464,3 +464,63 @@ def test_fast_path_fused_sgd_equals_dense_then_sgd():
         assert np.array_equal(a.core(k), b_.core(k))
     with pytest.raises(tt.InvalidArgument, match="stale"):
         b_.backward_sgd(rb.context, batch, g, 0.01)
+
+
+def test_data_parallel_shards_sum_to_full_batch(orc):
+    """§8(e) on one GPU: the dense gradients of two bag shards (what two ranks
+    produce before the allreduce) sum to the full-batch gradient, and the
+    DataParallelTable step through a world-1 NCCL group equals the fused step."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2101_11714_b200.sharding import DataParallelTable, partition_bags, shard_batch, shard_rows
+
+    plan = tt.plan_shapes(CFG2.num_rows, 16, 3, 32, CFG2.row_factors, CFG2.col_factors)
+    rng = np.random.default_rng(5)
+    table, cores = make_table(plan, np.float32, 3, scale=0.3)
+    b = tt.generate_zipfian_batch(plan.num_rows, 1.05, 9, 4096, 2)
+    g = rng.standard_normal((b.num_bags(), 16)).astype(np.float32)
+    full = orc.backward(as_oplan(plan), cores, b.indices, b.offsets, g)
+    bounds = partition_bags(b.offsets, 2)
+    acc = [np.zeros_like(c) for c in cores]
+    for r in range(2):
+        sb = shard_batch(b, bounds, r)
+        res = tt.forward_bags(table, sb)
+        gr = tt.backward_bags(table, sb, res.context, shard_rows(g, bounds, r))
+        for k in range(3):
+            acc[k] += gr.cores[k]
+    for k in range(3):
+        assert scaled_max_err(acc[k], full[k]) <= GRAD_TOL
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        stream = torch.cuda.Stream()
+        t2 = tt.TtTable(plan, "dp", np.float32, stream=stream.cuda_stream)
+        t2.set_cores(cores)
+        dp = DataParallelTable(t2)
+        dp.broadcast_cores()
+        d_idx = torch.from_numpy(b.indices).to(dev)
+        d_off = torch.from_numpy(b.offsets).to(dev)
+        d_g = torch.from_numpy(g).to(dev)
+        d_out = torch.empty((b.num_bags(), 16), device=dev)
+        torch.cuda.synchronize()
+        dp.forward(d_idx.data_ptr(), b.num_lookups(), d_off.data_ptr(), b.num_bags(),
+                   d_out.data_ptr())
+        dp.backward_step(d_g.data_ptr(), 0.01, stream=stream)
+        t2.check()
+        want = [c.copy() for c in cores]
+        orc.sgd(as_oplan(plan), want, full, 0.01)
+        for k in range(3):
+            assert scaled_max_err(t2.core(k), want[k]) <= GRAD_TOL
+        assert np.array_equal(d_out.cpu().numpy(),
+                              orc.forward(as_oplan(plan), cores, b.indices, b.offsets))
+    finally:
+        dist.destroy_process_group()
