@@ -675,12 +675,168 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
   }
 }
 
+// ----------------------------------------------------------- f3_srows ----
+// One WARP per i1-tile (no block barriers): S(slot) = Σ_{lookups of the slot,
+// tile order} D1, D1 = D2·G2[i2]ᵀ, D2 = T(alpha)·grad[bag].  Lane owns the
+// elements e = lane + 32k of the (P1 x R2) row (a = e / R2, r = e % R2); the
+// members of a slot are walked in tile order, U of them with loads in flight.
+// S rows land at the slot's position (start + s), kappa-major: row s holds
+// S[a0][c] at a0*C1 + c == a*R2 + r, so f3_bwd1 can bulk-copy a tile's rows.
+template <class D>
+__global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cores, int64_t coff2,
+                                                const Tile* __restrict__ tiles,
+                                                const int* __restrict__ ntiles,
+                                                const uint32_t* __restrict__ perm,
+                                                const uint16_t* __restrict__ d2,
+                                                const int32_t* __restrict__ lk_bag,
+                                                const float* __restrict__ alpha,
+                                                const float* __restrict__ grad,
+                                                const uint16_t* __restrict__ slot_of_pos,
+                                                const int* __restrict__ tile_nslots,
+                                                float* __restrict__ Sbuf) {
+  constexpr int EPL = (D::W1 + 31) / 32;  // row elements per lane
+  // distinct G2 rows a lane reads per member: r = (lane + 32k) % R2 repeats with period NR
+  constexpr int NR = D::R2 > 32 ? D::R2 / 32 : 1;
+  static_assert(D::R2 <= 32 ? 32 % D::R2 == 0 : D::R2 % 32 == 0, "lane -> rank column map");
+  constexpr int U = 8;  // members with G2 loads in flight
+  const int lane = threadIdx.x & 31;
+  const int t = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
+  if (t >= *ntiles) return;
+  const float* G2 = cores + coff2;
+  const Tile tl = tiles[t];
+  const int ntl = tl.end - tl.start;
+  const int nslots = tile_nslots[t];
+  // each lane fetches its own lookup's D2 = T(alpha) * grad[bag] once (one
+  // round trip for the whole tile); members' values then move by shuffles
+  int my_sl = -1, my_i2 = 0;
+  float dmy[D::N];
+  if (lane < ntl) {
+    const int l = static_cast<int>(perm[tl.start + lane]);
+    my_sl = slot_of_pos[tl.start + lane];
+    my_i2 = d2[l];
+    const float al = alpha[l];
+    const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bag[l]) * D::N);
+#pragma unroll
+    for (int q = 0; q < D::N / 4; ++q) {
+      const float4 gq = __ldg(grow + q);
+      dmy[4 * q] = __fmul_rn(al, gq.x);
+      dmy[4 * q + 1] = __fmul_rn(al, gq.y);
+      dmy[4 * q + 2] = __fmul_rn(al, gq.z);
+      dmy[4 * q + 3] = __fmul_rn(al, gq.w);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < D::N; ++q) dmy[q] = 0.f;
+  }
+  // slot-sorted member order (stable: tile order within a slot), so the loads
+  // of U consecutive members stay in flight across slot boundaries
+  __shared__ int members_all[8][32];
+  __shared__ __align__(16) float d2s_all[8][32 * D::N];
+  int* members = members_all[(threadIdx.x >> 5) & 7];
+  float* d2s = d2s_all[(threadIdx.x >> 5) & 7];
+#pragma unroll
+  for (int q = 0; q < D::N / 4; ++q)
+    reinterpret_cast<float4*>(d2s + lane * D::N)[q] =
+        make_float4(dmy[4 * q], dmy[4 * q + 1], dmy[4 * q + 2], dmy[4 * q + 3]);
+  {
+    const unsigned peers = __match_any_sync(0xffffffffu, my_sl);
+    const int rank = __popc(peers & lanemask_lt());
+    const unsigned leaders = __ballot_sync(0xffffffffu, my_sl >= 0 && rank == 0);
+    // lane s (< nslots): size of slot s (slots are numbered by first occurrence)
+    const int lead_s = lane < nslots ? static_cast<int>(__fns(leaders, 0, lane + 1)) : 0;
+    const int cnt_s = __shfl_sync(0xffffffffu, __popc(peers), lead_s);
+    int inc = lane < nslots ? cnt_s : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int ex = inc - (lane < nslots ? cnt_s : 0);
+    const int base = __shfl_sync(0xffffffffu, ex, my_sl >= 0 ? my_sl : 0);
+    if (my_sl >= 0) members[base + rank] = lane;
+    __syncwarp();
+  }
+  float acc[EPL];
+  int cur = -1;
+  for (int j0 = 0; j0 < ntl; j0 += U) {
+    int m[U], sl[U];
+    float4 g2[U][NR];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      m[u] = j0 + u < ntl ? members[j0 + u] : 0;
+      sl[u] = __shfl_sync(0xffffffffu, my_sl, m[u]);
+      const int i2 = __shfl_sync(0xffffffffu, my_i2, m[u]);
+      if (j0 + u < ntl) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+          g2[u][k] = __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(i2) * D::S2) +
+                           (lane + 32 * k) % D::R2);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j0 + u >= ntl) break;
+      float dv[D::N];
+#pragma unroll
+      for (int q = 0; q < D::N / 4; ++q) {
+        const float4 x = reinterpret_cast<const float4*>(d2s + m[u] * D::N)[q];
+        dv[4 * q] = x.x;
+        dv[4 * q + 1] = x.y;
+        dv[4 * q + 2] = x.z;
+        dv[4 * q + 3] = x.w;
+      }
+      const bool first = sl[u] != cur;
+      if (first) {  // a new slot starts: flush the finished one
+        if (cur >= 0) {
+          float* dst = Sbuf + static_cast<int64_t>(tl.start + cur) * D::W1;
+#pragma unroll
+          for (int k = 0; k < EPL; ++k)
+            if (lane + 32 * k < D::W1) dst[lane + 32 * k] = acc[k];
+        }
+        cur = sl[u];
+      }
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) {
+        const int a = ((lane + 32 * k) % D::W1) / D::R2;
+        float d4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // dv[a*4 + j] with a lane-dependent a: select statically
+          float x = dv[j];
+#pragma unroll
+          for (int aa = 1; aa < D::P1; ++aa) x = (a == aa) ? dv[aa * 4 + j] : x;
+          d4[j] = x;
+        }
+        const float4 gk = g2[u][k % NR];
+        float v = __fmul_rn(d4[0], gk.x);
+        v = __fmaf_rn(d4[1], gk.y, v);
+        v = __fmaf_rn(d4[2], gk.z, v);
+        v = __fmaf_rn(d4[3], gk.w, v);
+        acc[k] = first ? v : __fadd_rn(acc[k], v);
+      }
+    }
+  }
+  if (cur >= 0) {
+    float* dst = Sbuf + static_cast<int64_t>(tl.start + cur) * D::W1;
+#pragma unroll
+    for (int k = 0; k < EPL; ++k)
+      if (lane + 32 * k < D::W1) dst[lane + 32 * k] = acc[k];
+  }
+}
+
 // ------------------------------------------------------------ f3_bwd1 ----
-// Register blocking of the two per-tile micro-GEMMs.  Both contract over the
-// tile's kappa = (slot, a0) rows, padded to a multiple of 4 so that the
-// transposed S (ST[c][kappa]) yields 4 kappas per float4 load:
-//   dG1 (R1 x C1) += G0sᵀ · S : thread = RB r1 x CB c, kappa in quads
-//   D0  (kappa x R1) = S · G1ᵀ : thread = 4 kappa x RB0 r1, c in sequence
+// Per i1-tile, from the S rows of f3_srows:
+//   dG1 (R1 x C1) += Σ_kappa G0[i0(kappa)]ᵀ (x) S[kappa]     kappa = (slot, a0)
+//   D0[kappa] (R1) = S[kappa] · G1[i1]ᵀ  -> CTA-private D0 block per i0
+// Each CTA owns a contiguous tile range.  A tile's S rows are contiguous
+// (positions start .. start+nslots) and arrive by one TMA bulk copy; its G0
+// rows by one bulk copy per slot; both are issued for tile t+1 as soon as the
+// GEMMs of tile t have consumed the buffers.  G1[i1] is staged transposed
+// (regular loads) when the tile's bucket differs from the previous one.
+// Consecutive tiles of the same i1 keep accumulating the dG1 partial in
+// registers; one partial per (CTA, i1 run) is flushed (has1 marks the run's
+// first tile).  D0 accumulates per (CTA, i0) in a CTA-private global block,
+// stored on first touch (d0mask marks it for f3_combine).  Slots of one tile
+// have distinct i0, tiles run in order: every sum has a fixed order.
 template <class D>
 struct G1Blk {
   static constexpr int RB = D::R1 >= 64 ? 4 : 2;
@@ -690,74 +846,43 @@ struct G1Blk {
   static constexpr int RB0 = D::R1 >= 64 ? 4 : 2;
   static constexpr int TR0 = D::R1 / RB0;  // D0 threads along r1
   static constexpr int KG = 1;             // dG1 partial rows per (CTA, i1 run)
-  static constexpr int CHUNK = D::TT / (kThreads / 32);  // slot-sorted positions per warp (D1)
-  static_assert(TR * TC <= kThreads && TR0 * (D::P0 * D::TT / 4) <= kThreads, "bad blocking");
-  static_assert(D::C1 % CB == 0 && D::R1 % RB == 0 && D::TT % (kThreads / 32) == 0, "bad blocking");
+  static_assert(TR * TC <= kThreads, "bad blocking");
+  static_assert(D::C1 % CB == 0 && D::R1 % RB == 0 && CB % 4 == 0, "bad blocking");
 };
 
 template <class D>
 struct Bwd1Smem {
-  // floats: G1t[C1*R1P] | ST[C1*KP] (S transposed, [c][kappa]) | G2s[TT*S2] (G2 rows;
-  //         then split-slot D1 partials in place) | D2s[TT*N] | G0s[KP*R1] ; then ints
+  // floats: S[TT*P0 x C1] (TMA) | G0s[TT*P0 x R1] (TMA) | G1t[C1 x R1P] ; then mbarrier, ints
   static constexpr int R1P = D::R1 + 4;
-  static constexpr int KP = D::P0 * D::TT + 4;
-  static constexpr int NI = 8 * D::TT + 16 + 256;  // + D0 first-touch bitmap (m0 <= 8192)
-  static_assert(D::S2 == D::W1, "D1 partials reuse the G2 row storage");
-  static_assert((D::P0 * D::TT) % 4 == 0, "kappa quads");
+  static constexpr int NI = 2 * D::TT + 16 + 256;  // slot i0 / first-touch flags / misc / bitmap
   static __host__ __device__ size_t floats() {
-    size_t f = static_cast<size_t>(D::C1) * (R1P + KP) +
-               static_cast<size_t>(D::TT) * (D::S2 + D::N) + static_cast<size_t>(KP) * D::R1;
+    size_t f = static_cast<size_t>(D::TT) * D::W1 + static_cast<size_t>(D::TT) * D::S0 +
+               static_cast<size_t>(D::C1) * R1P;
     return (f + 3) / 4 * 4;
   }
-  static __host__ __device__ size_t bytes() { return floats() * 4 + sizeof(int) * NI; }
+  static __host__ __device__ size_t bytes() { return floats() * 4 + 16 + sizeof(int) * NI; }
 };
 
-// Each CTA owns a contiguous range of i1-tiles.  Consecutive tiles of the same
-// i1 keep accumulating the dG1 partial in registers; one partial per (CTA, i1
-// run) is flushed at the run's first tile (has1 marks it).  D0 accumulates per
-// (CTA, i0) in a CTA-private global block (stored on first touch, d0mask marks
-// it for the combine).  Per tile:
-//   warp 0  publishes the tile's positions (prefetched during the previous
-//           tile), sorts them by slot (match_any) and marks the slots whose
-//           member range crosses a warp chunk;
-//   stage   D2 rows, G2 rows, G1 slice (transposed), G0 rows (kappa-major);
-//   D1      warp w walks the slot-sorted positions [w*CHUNK, (w+1)*CHUNK):
-//           D1 = D2·G2ᵀ per lookup, summed per slot in registers in tile
-//           order; whole slots go straight to ST, split slots leave one
-//           partial per chunk which a short fold adds in chunk order;
-//   GEMMs   dG1 += G0sᵀ·S and D0 = S·G1ᵀ.
-// Every sum has a fixed order: the result is bitwise reproducible.
 template <class D>
-__global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 4 : 1) f3_bwd1(
+__global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
-    const int* __restrict__ ntiles, const uint32_t* __restrict__ perm,
-    const uint16_t* __restrict__ d2, const int32_t* __restrict__ lk_bag,
-    const float* __restrict__ alpha, const float* __restrict__ grad,
-    const uint16_t* __restrict__ slot_of_pos, const uint16_t* __restrict__ tile_i0,
-    const int* __restrict__ tile_nslots, float* __restrict__ part1, int* __restrict__ has1,
-    float* __restrict__ D0acc, unsigned char* __restrict__ d0mask) {
+    const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
+    const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
+    float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
+    unsigned char* __restrict__ d0mask) {
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
-  constexpr int CH = (D::R2 + 31) / 32;  // rank columns per lane
-  constexpr int KP = SM::KP;
   extern __shared__ __align__(128) float sm[];
-  float* G1t = sm;                        // C1 x R1P
-  float* ST = G1t + D::C1 * SM::R1P;      // C1 x KP
-  float* G2s = ST + D::C1 * KP;           // TT x S2
-  float* D2s = G2s + D::TT * D::S2;       // TT x N (alpha * grad rows)
-  float* G0s = D2s + D::TT * D::N;        // KP x R1 (rows kappa)
-  int* lk_slot = reinterpret_cast<int*>(sm + SM::floats());
-  int* lk_i2 = lk_slot + D::TT;
-  int* slot_i0 = lk_i2 + D::TT;
-  int* members = slot_i0 + D::TT;  // tile positions sorted by slot (stable)
-  int* sstart = members + D::TT;   // TT + 1
-  int* d0first = sstart + D::TT + 1;
-  int* splitl = d0first + D::TT;
-  int* misc = splitl + D::TT;      // [0] nsplit [1] i1 [2] ntl [3] nslots [4] next i1
+  float* Ss = sm;                                 // [kappa][C1]
+  float* G0s = Ss + D::TT * D::W1;                // [kappa][R1]
+  float* G1t = G0s + D::TT * D::S0;               // [c][R1P]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());
+  int* slot_i0 = reinterpret_cast<int*>(bar + 2);  // TT
+  int* d0first = slot_i0 + D::TT;                  // TT
+  int* misc = d0first + D::TT;                     // 16
   unsigned* d0bits = reinterpret_cast<unsigned*>(misc + 16);
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
-  const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int t_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nt / gridDim.x);
@@ -766,27 +891,35 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 4 : 1) f3_bwd1(
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
   for (int e = tid; e < 256; e += kThreads) d0bits[e] = 0u;
-  // warp 0: the current tile's per-position indices, and the next tile's in flight
-  Tile c_d{}, n_d{};
-  int c_ns = 0, c_l = 0, c_sl = 0, c_i0 = 0, c_i2 = 0, c_bag = 0;
-  float c_al = 0.f;
-  int n_ns = 0, n_l = 0, n_sl = 0, n_i0 = 0, n_i2 = 0, n_bag = 0;
-  float n_al = 0.f;
-  if (wid == 0 && t_lo < t_hi) {
-    c_d = tiles[t_lo];
-    c_ns = tile_nslots[t_lo];
-    if (lane < c_d.end - c_d.start) {
-      c_l = static_cast<int>(perm[c_d.start + lane]);
-      c_sl = slot_of_pos[c_d.start + lane];
-      c_i0 = tile_i0[c_d.start + lane];
-      c_i2 = d2[c_l];
-      c_al = alpha[c_l];
-      c_bag = lk_bag[c_l];
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  // warp 0: descriptors of the next tile are fetched a tile ahead (registers),
+  // then its bulk copies -- S rows (one copy) + G0 rows (one per slot) -- are
+  // issued as soon as the buffers are free
+  Tile n_d{};
+  int n_ns = 0, n_i0 = 0;
+  auto fetch = [&](int t) {
+    n_d = tiles[t];
+    n_ns = tile_nslots[t];
+    n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
+  };
+  auto issue = [&]() {
+    if (lane < n_ns) slot_i0[lane] = n_i0;
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect(bar, static_cast<uint32_t>(n_ns) * (D::W1 + D::S0) * 4);
+      tma_load(Ss, Sbuf + static_cast<int64_t>(n_d.start) * D::W1, n_ns * D::W1 * 4, bar);
+      misc[1] = n_d.key;
+      misc[3] = n_ns;
     }
-    if (t_lo + 1 < t_hi) n_d = tiles[t_lo + 1];
+    __syncwarp();
+    if (lane < n_ns)
+      tma_load(G0s + lane * D::S0, G0 + static_cast<int64_t>(n_i0) * D::S0, D::S0 * 4, bar);
+  };
+  if (wid == 0 && t_lo < t_hi) {
+    fetch(t_lo);
+    issue();
   }
-  __syncthreads();  // d0bits / d0m cleared
-  // dG1 register block
   const int r0 = (tid % GB::TR) * GB::RB, cb0 = (tid / GB::TR) * GB::CB;
   const bool g1_on = tid < GB::TR * GB::TC;
   float acc1[GB::RB][GB::CB];
@@ -794,90 +927,17 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 4 : 1) f3_bwd1(
   for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
     for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
-  int run_start = t_lo;
-  for (int t = t_lo; t < t_hi; ++t) {
-    if (wid == 0) {
-      // publish tile t: positions, slot member lists, split slots, D0 first touches
-      const int ntl = c_d.end - c_d.start;
-      const bool on = lane < ntl;
-      const int sl = on ? c_sl : -1;
-      if (on) {
-        lk_slot[lane] = sl;
-        lk_i2[lane] = c_i2;
-      }
-      const unsigned peers = __match_any_sync(0xffffffffu, sl);
-      const unsigned lt = lanemask_lt();
-      if (sl >= 0 && (peers & lt) == 0) sstart[sl] = __popc(peers);  // slot leader: count
-      __syncwarp();
-      const int cnt = lane < c_ns ? sstart[lane] : 0;
-      int inc = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const int ex = inc - cnt;
-      const int base = __shfl_sync(0xffffffffu, ex, sl >= 0 ? sl : 0);
-      __syncwarp();
-      if (sl >= 0) members[base + __popc(peers & lt)] = lane;
-      bool split = false;
-      if (lane < c_ns) {
-        sstart[lane] = ex;
-        split = (ex / GB::CHUNK) != ((ex + cnt - 1) / GB::CHUNK);
-        slot_i0[lane] = c_i0;
-        const unsigned bit = 1u << (c_i0 & 31);
-        const unsigned old = atomicOr(d0bits + (c_i0 >> 5), bit);
-        d0first[lane] = (old & bit) ? 0 : 1;
-        if (!(old & bit)) d0m[c_i0] = 1;
-      }
-      const unsigned sb = __ballot_sync(0xffffffffu, split);
-      if (split) splitl[__popc(sb & lt)] = lane;
-      if (lane == 0) {
-        sstart[c_ns] = ntl;
-        misc[0] = __popc(sb);
-        misc[1] = c_d.key;
-        misc[2] = ntl;
-        misc[3] = c_ns;
-        misc[4] = (t + 1 < t_hi) ? n_d.key : -1;
-      }
-    }
-    __syncthreads();
-    const int i1 = misc[1], ntl = misc[2], nslots = misc[3], nsplit = misc[0];
-    const bool last = misc[4] != i1;
-    const int nk = nslots * D::P0, nk4 = (nk + 3) & ~3;
-    // ---- stage
-    if (wid == 0 && lane < ntl) {
-      const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(c_bag) * D::N);
-      float4 gv[D::N / 4];
-#pragma unroll
-      for (int k = 0; k < D::N / 4; ++k) gv[k] = __ldg(grow + k);
-#pragma unroll
-      for (int k = 0; k < D::N / 4; ++k)
-        reinterpret_cast<float4*>(D2s + lane * D::N)[k] =
-            make_float4(__fmul_rn(c_al, gv[k].x), __fmul_rn(c_al, gv[k].y),
-                        __fmul_rn(c_al, gv[k].z), __fmul_rn(c_al, gv[k].w));
-    }
-    {
-      constexpr int Q = D::S2 / 4;
-      for (int e0 = tid; e0 < ntl * Q; e0 += kThreads * 4) {
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + u * kThreads;
-          if (e < ntl * Q) {
-            const int i = e / Q;
-            v[u] = __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2) +
-                         (e - i * Q));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (e0 + u * kThreads < ntl * Q) reinterpret_cast<float4*>(G2s)[e0 + u * kThreads] = v[u];
-      }
-    }
-    {
+  int run_start = t_lo, cur_i1 = -1;
+  uint32_t phase = 0;
+  for (int t = t_lo; t < t_hi; ++t, phase ^= 1u) {
+    __syncthreads();  // misc / slot_i0 of tile t published
+    const int i1 = misc[1], nslots = misc[3];
+    const int nk = nslots * D::P0;
+    const int nxt_i1 = (t + 1 < t_hi) ? tiles[t + 1].key : -1;
+    if (wid == 0 && t + 1 < t_hi) fetch(t + 1);  // in flight during this tile's GEMMs
+    if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
-      constexpr int U = (D::S1 + kThreads - 1) / kThreads < 8 ? (D::S1 + kThreads - 1) / kThreads : 8;
+      constexpr int U = 8;
       for (int e0 = tid; e0 < D::S1; e0 += kThreads * U) {
         float v[U];
 #pragma unroll
@@ -891,167 +951,95 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 4 : 1) f3_bwd1(
           }
         }
       }
+      cur_i1 = i1;
     }
-    gather_to_smem<8>(G0s, nk * D::R1, [&](int e) {
-      const int s = e / D::S0;
-      return G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0);
-    });
-    for (int e = tid; e < (nk4 - nk) * D::R1; e += kThreads) G0s[nk * D::R1 + e] = 0.f;
-    for (int e = tid; e < (nk4 - nk) * D::C1; e += kThreads) {
-      const int c = e / (nk4 - nk);
-      ST[c * KP + nk + (e - c * (nk4 - nk))] = 0.f;
+    if (wid == 1 && lane < nslots) {  // D0 first touches of this CTA
+      const int i0 = slot_i0[lane];
+      const unsigned bit = 1u << (i0 & 31);
+      const unsigned old = atomicOr(d0bits + (i0 >> 5), bit);
+      d0first[lane] = (old & bit) ? 0 : 1;
+      if (!(old & bit)) d0m[i0] = 1;
     }
-    if (wid == 0 && t + 1 < t_hi) {  // prefetch tile t+1 (stage 1: positions)
-      n_ns = tile_nslots[t + 1];
-      if (lane < n_d.end - n_d.start) {
-        n_l = static_cast<int>(perm[n_d.start + lane]);
-        n_sl = slot_of_pos[n_d.start + lane];
-        n_i0 = tile_i0[n_d.start + lane];
-      }
-    }
-    __syncthreads();
-    // ---- D1 per lookup, summed per slot along the slot-sorted positions
-    {
-      const int j0 = wid * GB::CHUNK;
-      const int j1 = j0 + GB::CHUNK < ntl ? j0 + GB::CHUNK : ntl;
-      float acc[CH][D::P1];
-      int run_p = j0;
-      for (int j = j0; j < j1; ++j) {
-        const int m = members[j];
-        const int sl = lk_slot[m];
-        const bool first = j == j0 || lk_slot[members[j - 1]] != sl;
-        if (first) run_p = j;
-#pragma unroll
-        for (int rr = 0; rr < CH; ++rr) {
-          const int r = rr * 32 + lane;
-          if (r < D::R2) {
-            const float4 gv = reinterpret_cast<const float4*>(G2s + m * D::S2)[r];
-#pragma unroll
-            for (int a = 0; a < D::P1; ++a) {
-              const float4 dv = reinterpret_cast<const float4*>(D2s + m * D::N)[a];
-              float v = __fmul_rn(dv.x, gv.x);
-              v = __fmaf_rn(dv.y, gv.y, v);
-              v = __fmaf_rn(dv.z, gv.z, v);
-              v = __fmaf_rn(dv.w, gv.w, v);
-              acc[rr][a] = first ? v : acc[rr][a] + v;
-            }
-          }
-        }
-        const bool end = j + 1 == j1 || lk_slot[members[j + 1]] != sl;
-        if (end) {
-          const bool whole = sstart[sl] >= j0 && sstart[sl + 1] <= j1;
-          __syncwarp();  // the partial row (this warp's, already consumed) may be overwritten
-#pragma unroll
-          for (int rr = 0; rr < CH; ++rr) {
-            const int r = rr * 32 + lane;
-            if (r < D::R2) {
-#pragma unroll
-              for (int a = 0; a < D::P1; ++a) {
-                if (whole)
-                  ST[((a % D::N1) * D::R2 + r) * KP + sl * D::P0 + a / D::N1] = acc[rr][a];
-                else
-                  G2s[members[run_p] * D::S2 + a * D::R2 + r] = acc[rr][a];
-              }
-            }
-          }
-        }
-      }
-    }
-    if (wid == 0 && t + 1 < t_hi) {  // prefetch tile t+1 (stage 2: per-lookup data)
-      if (lane < n_d.end - n_d.start) {
-        n_i2 = d2[n_l];
-        n_al = alpha[n_l];
-        n_bag = lk_bag[n_l];
-      }
-    }
-    __syncthreads();
-    if (nsplit) {  // split slots: add the chunk partials in chunk order
-      for (int q = tid; q < nsplit * D::W1; q += kThreads) {
-        const int sl = splitl[q / D::W1], e = q % D::W1;
-        const int s0 = sstart[sl], s1 = sstart[sl + 1];
-        float acc = G2s[members[s0] * D::S2 + e];
-        for (int p = (s0 / GB::CHUNK + 1) * GB::CHUNK; p < s1; p += GB::CHUNK)
-          acc += G2s[members[p] * D::S2 + e];
-        const int a = e / D::R2, r = e - a * D::R2;
-        ST[((a % D::N1) * D::R2 + r) * KP + sl * D::P0 + a / D::N1] = acc;
-      }
-      __syncthreads();
-    }
+    mbar_wait(bar, phase);
+    __syncthreads();  // G1t staged, d0first set, bulk data visible
     // ---- dG1 partial += Σ_kappa G0s[kappa][r1] (x) S[kappa][c]
     if (g1_on) {
-      for (int kq = 0; kq < nk4 / 4; ++kq) {
-        float4 b[GB::CB];
+#pragma unroll 2
+      for (int k = 0; k < nk; ++k) {
+        float a[GB::RB], b[GB::CB];
+        const float* ap = G0s + k * D::R1 + r0;
 #pragma unroll
-        for (int j = 0; j < GB::CB; ++j) b[j] = reinterpret_cast<const float4*>(ST + (cb0 + j) * KP)[kq];
+        for (int i = 0; i < GB::RB; ++i) a[i] = ap[i];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          float a[GB::RB];
-          const float* ap = G0s + (4 * kq + kk) * D::R1 + r0;
-          if constexpr (GB::RB == 4) {
-            const float4 v = *reinterpret_cast<const float4*>(ap);
-            a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
-          } else {
-            const float2 v = *reinterpret_cast<const float2*>(ap);
-            a[0] = v.x; a[1] = v.y;
-          }
-#pragma unroll
-          for (int i = 0; i < GB::RB; ++i)
-#pragma unroll
-            for (int j = 0; j < GB::CB; ++j) {
-              const float bj = kk == 0 ? b[j].x : kk == 1 ? b[j].y : kk == 2 ? b[j].z : b[j].w;
-              acc1[i][j] = __fmaf_rn(a[i], bj, acc1[i][j]);
-            }
+        for (int j = 0; j < GB::CB; j += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(Ss + k * D::C1 + cb0 + j);
+          b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
         }
+#pragma unroll
+        for (int i = 0; i < GB::RB; ++i)
+#pragma unroll
+          for (int j = 0; j < GB::CB; ++j) acc1[i][j] = __fmaf_rn(a[i], b[j], acc1[i][j]);
       }
     }
-    // ---- D0[kappa][r1] = Σ_c S[kappa][c] · G1[r1][c]  -> CTA D0 block
-    {
-      const int q = tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
-      if (q < nk4 / 4) {
-        float v[4][GB::RB0];
+    // ---- D0[kappa][r1] = Σ_c S[kappa][c] · G1[r1][c]; thread = (kappa, RB0 r1)
+    constexpr int KPT = kThreads / GB::TR0;  // kappas in flight per pass
+    float dv[(D::P0 * D::TT + KPT - 1) / KPT][GB::RB0];
+    int npass = 0;
+    for (int kb = 0; kb < nk; kb += KPT, ++npass) {
+      const int k = kb + tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
+      float v[GB::RB0];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-          for (int i = 0; i < GB::RB0; ++i) v[kk][i] = 0.f;
+      for (int i = 0; i < GB::RB0; ++i) v[i] = 0.f;
+      if (k < nk) {
+        const float* srow = Ss + k * D::C1;
 #pragma unroll 4
-        for (int c = 0; c < D::C1; ++c) {
-          const float4 s4 = reinterpret_cast<const float4*>(ST + c * KP)[q];
-          float gg[GB::RB0];
-          if constexpr (GB::RB0 == 4) {
-            const float4 w = *reinterpret_cast<const float4*>(G1t + c * SM::R1P + rb);
-            gg[0] = w.x; gg[1] = w.y; gg[2] = w.z; gg[3] = w.w;
-          } else {
-            const float2 w = *reinterpret_cast<const float2*>(G1t + c * SM::R1P + rb);
-            gg[0] = w.x; gg[1] = w.y;
-          }
+        for (int c = 0; c < D::C1; c += 4) {
+          const float4 s4 = *reinterpret_cast<const float4*>(srow + c);
+          const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-          for (int i = 0; i < GB::RB0; ++i) {
-            v[0][i] = __fmaf_rn(s4.x, gg[i], v[0][i]);
-            v[1][i] = __fmaf_rn(s4.y, gg[i], v[1][i]);
-            v[2][i] = __fmaf_rn(s4.z, gg[i], v[2][i]);
-            v[3][i] = __fmaf_rn(s4.w, gg[i], v[3][i]);
+          for (int cc = 0; cc < 4; ++cc) {
+            const float* gp = G1t + (c + cc) * SM::R1P + rb;
+#pragma unroll
+            for (int i = 0; i < GB::RB0; ++i) v[i] = __fmaf_rn(sv[cc], gp[i], v[i]);
           }
         }
+      }
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int kap = 4 * q + kk;
-          if (kap < nk) {
-            const int s = kap / D::P0, a0 = kap - s * D::P0;
-            float* dst = d0acc + slot_i0[s] * D::S0 + a0 * D::R1 + rb;
-            if (d0first[s]) {
+      for (int q = 0; q < (D::P0 * D::TT + KPT - 1) / KPT; ++q)
+        if (q == npass)
 #pragma unroll
-              for (int i = 0; i < GB::RB0; ++i) dst[i] = v[kk][i];
-            } else {
+          for (int i = 0; i < GB::RB0; ++i) dv[q][i] = v[i];
+    }
+    // slot list of this tile -> registers before the buffers are handed to tile t+1
+    int my_i0[(D::P0 * D::TT + KPT - 1) / KPT];
+    int my_first[(D::P0 * D::TT + KPT - 1) / KPT];
 #pragma unroll
-              for (int i = 0; i < GB::RB0; ++i) dst[i] += v[kk][i];
-            }
-          }
+    for (int q = 0; q < (D::P0 * D::TT + KPT - 1) / KPT; ++q) {
+      const int k = q * KPT + tid / GB::TR0;
+      my_i0[q] = k < nk ? slot_i0[k / D::P0] : 0;
+      my_first[q] = k < nk ? d0first[k / D::P0] : 0;
+    }
+    __syncthreads();  // Ss / G0s / slot lists consumed
+    if (wid == 0 && t + 1 < t_hi) issue();
+    // ---- D0 into the CTA block (slots of one tile have distinct i0)
+#pragma unroll
+    for (int q = 0; q < (D::P0 * D::TT + KPT - 1) / KPT; ++q) {
+      const int k = q * KPT + tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
+      if (q < npass && k < nk) {
+        const int a0 = k % D::P0;
+        float* dst = d0acc + my_i0[q] * D::S0 + a0 * D::R1 + rb;
+        if (my_first[q]) {
+#pragma unroll
+          for (int i = 0; i < GB::RB0; ++i) dst[i] = dv[q][i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < GB::RB0; ++i) dst[i] += dv[q][i];
         }
       }
     }
     // ---- end of an i1 run (or of this CTA's range): flush the dG1 partial
     if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
-    if (last || t + 1 == t_hi) {
+    if (nxt_i1 != i1 || t + 1 == t_hi) {
       float* dst = part1 + static_cast<int64_t>(run_start) * D::S1;
       if (g1_on) {
 #pragma unroll
@@ -1067,18 +1055,6 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 4 : 1) f3_bwd1(
         for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
       run_start = t + 1;
     }
-    if (wid == 0) {  // rotate the prefetched tile in; start fetching t+2's descriptor
-      c_d = n_d;
-      c_ns = n_ns;
-      c_l = n_l;
-      c_sl = n_sl;
-      c_i0 = n_i0;
-      c_i2 = n_i2;
-      c_al = n_al;
-      c_bag = n_bag;
-      if (t + 2 < t_hi) n_d = tiles[t + 2];
-    }
-    __syncthreads();  // the next tile overwrites the shared arrays read above
   }
 }
 

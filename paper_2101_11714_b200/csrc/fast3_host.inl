@@ -5,7 +5,7 @@ namespace ttgpu {
 struct F3Bufs {
   DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
-      group_base1, group_base2, gpart, gtouch, counters, tot;
+      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf;
   f3::Geo geo{};
   int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
@@ -170,12 +170,18 @@ struct F3Runner {
     f.has2.ensure(4 * static_cast<size_t>(f.max_tiles2));
     f.D0acc.ensure(4 * static_cast<size_t>(grid1) * g.m0 * D::S0);
     f.d0mask.ensure(static_cast<size_t>(grid1) * g.m0);
+    f.Sbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
     t->mark("bwd_begin");
-    k1<<<grid1, f3::kThreads, sm1, st>>>(
-        g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.perm1.as<uint32_t>(),
-        f.d2.as<uint16_t>(), lk_bag, alpha, grad, f.slotpos.as<uint16_t>(),
-        f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(), f.part1.as<float>(), f.has1.as<int>(),
-        f.D0acc.as<float>(), f.d0mask.as<unsigned char>());
+    f3::f3_srows<D><<<(f.max_tiles1 * 32 + 255) / 256, 256, 0, st>>>(
+        t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
+        f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
+        f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>());
+    t->mark("f3_srows");
+    k1<<<grid1, f3::kThreads, sm1, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
+                                         f.ntiles.as<int>(), f.Sbuf.as<float>(),
+                                         f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(),
+                                         f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
+                                         f.d0mask.as<unsigned char>());
     t->mark("f3_bwd1");
     f3::f3_bwd2<D><<<grid2, 128, 0, st>>>(g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
                                           f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag,
