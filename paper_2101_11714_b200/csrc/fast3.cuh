@@ -852,12 +852,13 @@ struct G1Blk {
 
 template <class D>
 struct Bwd1Smem {
-  // floats: S[TT*P0 x C1] (TMA) | G0s[TT*P0 x R1] (TMA) | G1t[C1 x R1P] ; then mbarrier, ints
+  // floats: 2 stages x { S[TT*P0 x C1] (TMA) | G0s[TT*P0 x R1] (TMA) } | G1t[C1 x R1P] ;
+  // then 2 mbarriers, ints
   static constexpr int R1P = D::R1 + 4;
-  static constexpr int NI = 2 * D::TT + 16 + 256;  // slot i0 / first-touch flags / misc / bitmap
+  static constexpr int STAGE = D::TT * D::W1 + D::TT * D::S0;  // floats per stage
+  static constexpr int NI = 3 * D::TT + 16 + 256;  // 2 x slot i0 / first-touch flags / misc / bitmap
   static __host__ __device__ size_t floats() {
-    size_t f = static_cast<size_t>(D::TT) * D::W1 + static_cast<size_t>(D::TT) * D::S0 +
-               static_cast<size_t>(D::C1) * R1P;
+    size_t f = 2 * static_cast<size_t>(STAGE) + static_cast<size_t>(D::C1) * R1P;
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes() { return floats() * 4 + 16 + sizeof(int) * NI; }
@@ -873,29 +874,66 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
   extern __shared__ __align__(128) float sm[];
-  float* Ss = sm;                                 // [kappa][C1]
-  float* G0s = Ss + D::TT * D::W1;                // [kappa][R1]
-  float* G1t = G0s + D::TT * D::S0;               // [c][R1P]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());
-  int* slot_i0 = reinterpret_cast<int*>(bar + 2);  // TT
-  int* d0first = slot_i0 + D::TT;                  // TT
-  int* misc = d0first + D::TT;                     // 16
+  float* G1t = sm + 2 * SM::STAGE;                 // [c][R1P]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());  // 2 stages
+  int* slot_i0 = reinterpret_cast<int*>(bar + 2);  // 2 x TT
+  int* d0first = slot_i0 + 2 * D::TT;              // TT
+  int* misc = d0first + D::TT;                     // [2*stage + 0] key, [2*stage + 1] nslots
   unsigned* d0bits = reinterpret_cast<unsigned*>(misc + 16);
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const int nt = *ntiles;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const int t_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nt / gridDim.x);
-  const int t_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nt / gridDim.x);
+  int t_lo, t_hi;
+  // Contiguous tile ranges balanced by work, not by count: tile t weighs
+  // kTileCost + nslots(t) (its GEMMs scale with the slot count), and belongs
+  // to the CTA floor(E(t) * grid / W), E = exclusive prefix of the weights.
+  // Every CTA recomputes the (small) prefix; ranges partition the tiles.
+  {
+    constexpr int kTileCost = 4;
+    using Scan = cub::BlockScan<int, kThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int range[2];
+    const int per = (nt + kThreads - 1) / kThreads;
+    const int a0 = min(nt, tid * per), a1 = min(nt, a0 + per);
+    int wsum = 0;
+    for (int t = a0; t < a1; ++t) wsum += kTileCost + tile_nslots[t];
+    int ex, W;
+    Scan(scan_tmp).ExclusiveSum(wsum, ex, W);
+    if (tid == 0) {
+      range[0] = nt;
+      range[1] = 0;
+    }
+    __syncthreads();
+    int lo = nt, hi = -1;
+    for (int t = a0; t < a1; ++t) {
+      const int owner = static_cast<int>(static_cast<int64_t>(ex) * gridDim.x / max(W, 1));
+      if (owner == static_cast<int>(blockIdx.x)) {
+        lo = min(lo, t);
+        hi = max(hi, t);
+      }
+      ex += kTileCost + tile_nslots[t];
+    }
+    if (hi >= 0) {
+      atomicMin(&range[0], lo);
+      atomicMax(&range[1], hi + 1);
+    }
+    __syncthreads();
+    t_lo = range[0];
+    t_hi = range[1] > range[0] ? range[1] : range[0];
+  }
   float* d0acc = D0acc + static_cast<int64_t>(blockIdx.x) * g.m0 * D::S0;
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
   for (int e = tid; e < 256; e += kThreads) d0bits[e] = 0u;
-  if (tid == 0) mbar_init(bar, 1);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
   __syncthreads();
-  // warp 0: descriptors of the next tile are fetched a tile ahead (registers),
-  // then its bulk copies -- S rows (one copy) + G0 rows (one per slot) -- are
-  // issued as soon as the buffers are free
+  // warp 0 keeps two tiles of bulk copies in flight: the descriptors of tile
+  // t+2 are fetched during tile t, its S rows (one copy) and G0 rows (one per
+  // slot) are issued into tile t's stage as soon as tile t's GEMMs are done
   Tile n_d{};
   int n_ns = 0, n_i0 = 0;
   auto fetch = [&](int t) {
@@ -903,22 +941,30 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     n_ns = tile_nslots[t];
     n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
   };
-  auto issue = [&]() {
-    if (lane < n_ns) slot_i0[lane] = n_i0;
+  auto issue = [&](int st) {
+    float* Ss = sm + st * SM::STAGE;
+    float* G0s = Ss + D::TT * D::W1;
+    if (lane < n_ns) slot_i0[st * D::TT + lane] = n_i0;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect(bar, static_cast<uint32_t>(n_ns) * (D::W1 + D::S0) * 4);
-      tma_load(Ss, Sbuf + static_cast<int64_t>(n_d.start) * D::W1, n_ns * D::W1 * 4, bar);
-      misc[1] = n_d.key;
-      misc[3] = n_ns;
+      mbar_arrive_expect(bar + st, static_cast<uint32_t>(n_ns) * (D::W1 + D::S0) * 4);
+      tma_load(Ss, Sbuf + static_cast<int64_t>(n_d.start) * D::W1, n_ns * D::W1 * 4, bar + st);
+      misc[2 * st] = n_d.key;
+      misc[2 * st + 1] = n_ns;
     }
     __syncwarp();
     if (lane < n_ns)
-      tma_load(G0s + lane * D::S0, G0 + static_cast<int64_t>(n_i0) * D::S0, D::S0 * 4, bar);
+      tma_load(G0s + lane * D::S0, G0 + static_cast<int64_t>(n_i0) * D::S0, D::S0 * 4, bar + st);
   };
-  if (wid == 0 && t_lo < t_hi) {
-    fetch(t_lo);
-    issue();
+  if (wid == 0) {
+    if (t_lo < t_hi) {
+      fetch(t_lo);
+      issue(0);
+    }
+    if (t_lo + 1 < t_hi) {
+      fetch(t_lo + 1);
+      issue(1);
+    }
   }
   const int r0 = (tid % GB::TR) * GB::RB, cb0 = (tid / GB::TR) * GB::CB;
   const bool g1_on = tid < GB::TR * GB::TC;
@@ -928,13 +974,17 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
 #pragma unroll
     for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
   int run_start = t_lo, cur_i1 = -1;
-  uint32_t phase = 0;
-  for (int t = t_lo; t < t_hi; ++t, phase ^= 1u) {
+  for (int t = t_lo; t < t_hi; ++t) {
+    const int st = (t - t_lo) & 1;
+    const uint32_t parity = static_cast<uint32_t>(((t - t_lo) >> 1) & 1);
+    const float* Ss = sm + st * SM::STAGE;
+    const float* G0s = Ss + D::TT * D::W1;
+    const int* si0 = slot_i0 + st * D::TT;
     __syncthreads();  // misc / slot_i0 of tile t published
-    const int i1 = misc[1], nslots = misc[3];
+    const int i1 = misc[2 * st], nslots = misc[2 * st + 1];
     const int nk = nslots * D::P0;
-    const int nxt_i1 = (t + 1 < t_hi) ? tiles[t + 1].key : -1;
-    if (wid == 0 && t + 1 < t_hi) fetch(t + 1);  // in flight during this tile's GEMMs
+    const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * (st ^ 1)] : -1;
+    if (wid == 0 && t + 2 < t_hi) fetch(t + 2);  // in flight during this tile's GEMMs
     if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
       constexpr int U = 8;
@@ -954,13 +1004,13 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
       cur_i1 = i1;
     }
     if (wid == 1 && lane < nslots) {  // D0 first touches of this CTA
-      const int i0 = slot_i0[lane];
+      const int i0 = si0[lane];
       const unsigned bit = 1u << (i0 & 31);
       const unsigned old = atomicOr(d0bits + (i0 >> 5), bit);
       d0first[lane] = (old & bit) ? 0 : 1;
       if (!(old & bit)) d0m[i0] = 1;
     }
-    mbar_wait(bar, phase);
+    mbar_wait(bar + st, parity);
     __syncthreads();  // G1t staged, d0first set, bulk data visible
     // ---- dG1 partial += Σ_kappa G0s[kappa][r1] (x) S[kappa][c]
     if (g1_on) {
@@ -982,15 +1032,18 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
       }
     }
     // ---- D0[kappa][r1] = Σ_c S[kappa][c] · G1[r1][c]; thread = (kappa, RB0 r1)
-    constexpr int KPT = kThreads / GB::TR0;  // kappas in flight per pass
-    float dv[(D::P0 * D::TT + KPT - 1) / KPT][GB::RB0];
-    int npass = 0;
-    for (int kb = 0; kb < nk; kb += KPT, ++npass) {
-      const int k = kb + tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
-      float v[GB::RB0];
+    constexpr int KPT = kThreads / GB::TR0;  // kappas per pass
+    constexpr int NP = (D::P0 * D::TT + KPT - 1) / KPT;
+    float dv[NP][GB::RB0];
+    int my_i0[NP], my_first[NP];
 #pragma unroll
-      for (int i = 0; i < GB::RB0; ++i) v[i] = 0.f;
-      if (k < nk) {
+    for (int q = 0; q < NP; ++q) {
+      const int k = q * KPT + tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
+#pragma unroll
+      for (int i = 0; i < GB::RB0; ++i) dv[q][i] = 0.f;
+      my_i0[q] = k < nk ? si0[k / D::P0] : 0;
+      my_first[q] = k < nk ? d0first[k / D::P0] : 0;
+      if (q * KPT < nk && k < nk) {
         const float* srow = Ss + k * D::C1;
 #pragma unroll 4
         for (int c = 0; c < D::C1; c += 4) {
@@ -1000,32 +1053,18 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
           for (int cc = 0; cc < 4; ++cc) {
             const float* gp = G1t + (c + cc) * SM::R1P + rb;
 #pragma unroll
-            for (int i = 0; i < GB::RB0; ++i) v[i] = __fmaf_rn(sv[cc], gp[i], v[i]);
+            for (int i = 0; i < GB::RB0; ++i) dv[q][i] = __fmaf_rn(sv[cc], gp[i], dv[q][i]);
           }
         }
       }
-#pragma unroll
-      for (int q = 0; q < (D::P0 * D::TT + KPT - 1) / KPT; ++q)
-        if (q == npass)
-#pragma unroll
-          for (int i = 0; i < GB::RB0; ++i) dv[q][i] = v[i];
     }
-    // slot list of this tile -> registers before the buffers are handed to tile t+1
-    int my_i0[(D::P0 * D::TT + KPT - 1) / KPT];
-    int my_first[(D::P0 * D::TT + KPT - 1) / KPT];
-#pragma unroll
-    for (int q = 0; q < (D::P0 * D::TT + KPT - 1) / KPT; ++q) {
-      const int k = q * KPT + tid / GB::TR0;
-      my_i0[q] = k < nk ? slot_i0[k / D::P0] : 0;
-      my_first[q] = k < nk ? d0first[k / D::P0] : 0;
-    }
-    __syncthreads();  // Ss / G0s / slot lists consumed
-    if (wid == 0 && t + 1 < t_hi) issue();
+    __syncthreads();  // stage st / slot lists consumed
+    if (wid == 0 && t + 2 < t_hi) issue(st);
     // ---- D0 into the CTA block (slots of one tile have distinct i0)
 #pragma unroll
-    for (int q = 0; q < (D::P0 * D::TT + KPT - 1) / KPT; ++q) {
+    for (int q = 0; q < NP; ++q) {
       const int k = q * KPT + tid / GB::TR0, rb = (tid % GB::TR0) * GB::RB0;
-      if (q < npass && k < nk) {
+      if (k < nk) {
         const int a0 = k % D::P0;
         float* dst = d0acc + my_i0[q] * D::S0 + a0 * D::R1 + rb;
         if (my_first[q]) {
