@@ -189,6 +189,33 @@ class RefImpl:
         self.check(self.lib.ref_decompose_index(C.c_int64(flat), _p(r), C.c_int(len(r)), _p(out)))
         return out
 
+    # ---- checkpoints (checkpoint.hpp / src/checkpoint.cpp) ----
+    def checkpoint_save(self, path, tables, arrays=()):
+        """Checkpoint: put_table(t) for each RefTable, put_array<float>(name,
+        {len}, values) for each (name, values), save(path)."""
+        th = (C.c_void_p * max(1, len(tables)))(*[t.h for t in tables])
+        arrays = [(n, np.ascontiguousarray(v, np.float32)) for n, v in arrays]
+        names = (C.c_char_p * max(1, len(arrays)))(*[n.encode() for n, _ in arrays])
+        ptrs = (C.c_void_p * max(1, len(arrays)))(*[v.ctypes.data for _, v in arrays])
+        lens = np.array([v.size for _, v in arrays] or [0], np.int64)
+        self.check(self.lib.ref_checkpoint_save(th, C.c_int(len(tables)), names, ptrs, _p(lens),
+                                                C.c_int(len(arrays)), str(path).encode()))
+
+    def checkpoint_load_table(self, path, name, plan: Plan, dtype=np.float32):
+        h = C.c_void_p()
+        self.check(self.lib.ref_checkpoint_load_table(str(path).encode(), name.encode(),
+                                                      C.c_int(1 if np.dtype(dtype) == np.float64
+                                                              else 0), C.byref(h)))
+        t = RefTable.__new__(RefTable)
+        t.ref, t.plan, t.dtype, t.h = self, plan, np.dtype(dtype), h
+        return t
+
+    def checkpoint_load_array(self, path, name, n):
+        out = np.zeros(n, np.float32)
+        self.check(self.lib.ref_checkpoint_load_array(str(path).encode(), name.encode(), _p(out),
+                                                      C.c_int64(n)))
+        return out
+
     # ---- tables ----
     def table(self, plan: Plan, dtype=np.float32, name="tt-table"):
         return RefTable(self, plan, dtype, name)

@@ -22,6 +22,9 @@
 #include <string>
 #include <vector>
 
+#ifdef TTREF_CHECKPOINT
+#include "ttrec/checkpoint.hpp"
+#endif
 #include "ttrec/data.hpp"
 #include "ttrec/embedding_ops.hpp"
 #include "ttrec/embedding_stats.hpp"
@@ -587,5 +590,54 @@ double ref_time_step(void* h, const int64_t* idx, int64_t L, const int64_t* off,
   std::sort(ts.begin(), ts.end());
   return ts.empty() ? 0.0 : ts[ts.size() / 2];
 }
+
+#ifdef TTREF_CHECKPOINT
+// ---- checkpoint.hpp / src/checkpoint.cpp (TTRECV01) ------------------------
+// Checkpoint::put_table for every table (in order), optional f32 arrays
+// (name, 1-D length), then save(path).
+int ref_checkpoint_save(void* const* tables, int n, const char* const* array_names,
+                        const float* const* arrays, const int64_t* array_lens, int na,
+                        const char* path) {
+  return guarded([&] {
+    Checkpoint cp;
+    for (int i = 0; i < n; ++i) {
+      auto* t = static_cast<RefTable*>(tables[i]);
+      if (t->dtype)
+        cp.put_table(*t->d);
+      else
+        cp.put_table(*t->f);
+    }
+    for (int i = 0; i < na; ++i)
+      cp.put_array<float>(array_names[i], {array_lens[i]},
+                          std::span<const float>(arrays[i], static_cast<size_t>(array_lens[i])));
+    cp.save(path);
+  });
+}
+
+// Checkpoint::load(path).get_table<T>(name) -> a new RefTable
+int ref_checkpoint_load_table(const char* path, const char* name, int dtype, void** out) {
+  return guarded([&] {
+    Checkpoint cp = Checkpoint::load(path);
+    auto* t = new RefTable;
+    t->dtype = dtype;
+    if (dtype)
+      t->d = std::make_unique<TtTable<double>>(cp.get_table<double>(name));
+    else
+      t->f = std::make_unique<TtTable<float>>(cp.get_table<float>(name));
+    *out = t;
+  });
+}
+
+// Checkpoint::load(path).get_array<float>(name) into out (len elements)
+int ref_checkpoint_load_array(const char* path, const char* name, float* out, int64_t len) {
+  return guarded([&] {
+    Checkpoint cp = Checkpoint::load(path);
+    auto v = cp.get_array<float>(name);
+    require_arg(static_cast<int64_t>(v.size()) == len, "array length mismatch");
+    std::memcpy(out, v.data(), sizeof(float) * v.size());
+  });
+}
+
+#endif  // TTREF_CHECKPOINT
 
 }  // extern "C"

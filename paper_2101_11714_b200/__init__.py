@@ -34,3 +34,4 @@ from .lfu_cache import (  # noqa: F401,E402
     hot_set_drift,
 )
 from . import sharding  # noqa: F401,E402
+from . import checkpoint  # noqa: F401,E402

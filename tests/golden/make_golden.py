@@ -211,8 +211,32 @@ def zipf_stream(ref):
     return dict(idx=idx, off=off)
 
 
+CKPT_PLANS = {  # name -> (Plan args, dtype)
+    "emb0": ((5000, 16, [10, 20, 25], [2, 2, 4], [1, 6, 5, 1]), np.float32),
+    "emb1": ((300, 8, [15, 20], [2, 4], [1, 3, 1]), np.float64),
+}
+
+
+def checkpoint_golden(ref):
+    """A TTRECV01 file written by the reference's Checkpoint::save: two tables
+    (f32 3-core with init_tt_cores(sampled_gaussian, 3); f64 2-core with the
+    test helpers' fill_cores(seed 5)) and one f32 array."""
+    from pyoracle import Plan
+
+    t0 = ref.table(Plan(*CKPT_PLANS["emb0"][0]), CKPT_PLANS["emb0"][1], "emb0")
+    t0.init_sampled_gaussian(3)
+    t1 = ref.table(Plan(*CKPT_PLANS["emb1"][0]), CKPT_PLANS["emb1"][1], "emb1")
+    t1.fill_normal(5, 0.5)
+    w = ref.normal(11, 37).astype(np.float32)
+    ref.checkpoint_save(os.path.join(HERE, "ckpt_ref.ttrec"), [t0, t1], [("dense.w", w)])
+
+
 def main():
     ref = RefImpl()
+    if len(sys.argv) > 1 and sys.argv[1] == "ckpt":
+        checkpoint_golden(ref)
+        return
+    checkpoint_golden(ref)
     with open(os.path.join(HERE, "plans.json"), "w") as f:
         json.dump(plans(ref), f, indent=1)
     np.savez_compressed(os.path.join(HERE, "small_cases.npz"), **small_cases(ref))
