@@ -44,6 +44,10 @@ CONFIGS = {
                       "Zipf(1.05), fwd+bwd+SGD"),
     "cfg2u": dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32, bags=65536,
                   pf=1, zipf=0.0, desc="cfg2 shape with uniform indices"),
+    "cfg4": dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32, bags=65536,
+                 pf=1, zipf=1.2, cache=True,
+                 desc="cfg2 shape with the LFU hot-row cache (0.01% = 1,013 rows), Zipf(1.2), "
+                      "fwd+bwd+SGD, cache warmed on the same stream"),
     "cfg3": dict(rows=40000000, emb=64, rf=[200, 200, 1000], cf=[4, 4, 4], rank=64, bags=65536,
                  pf=32, zipf=0.0,
                  desc="40M rows (200x200x1000), dim 64 (4x4x4), R=64, 65,536 bags x 32, uniform"),
@@ -250,6 +254,13 @@ def main():
     stream.synchronize()
     ctx = tt.ForwardContext(table)
 
+    cache = None
+    if cfg.get("cache"):
+        # LFU cache of hot rows (lfu_cache.hpp; model.hpp:195-284): warm-up records
+        # frequencies on the same stream, then warmup_finalize admits the top 0.01%
+        cache = tt.LfuCache(tt.lfu_cache.default_capacity(cfg["rows"]), cfg["emb"],
+                            refresh_period=1 << 30, key_space=cfg["rows"], device=local,
+                            stream=stream.cuda_stream)
     gbuf = None
     if world > 1:
         gptr, gn = table.grad_buffer()
@@ -260,7 +271,23 @@ def main():
 
         gbuf = torch.as_tensor(_Arr(), device=dev)
 
+    from paper_2101_11714_b200._lib import lib as _L
+    import ctypes as _C
+
+    def cache_step():
+        st = _L().ttgpu_cache_forward_device(cache.handle, table.handle, ctx.handle,
+                                             _C.c_void_p(d_idx.data_ptr()), L,
+                                             _C.c_void_p(d_off.data_ptr()), B, None, 0, 1,
+                                             _C.c_void_p(d_out.data_ptr()))
+        assert st == 0, _L().ttgpu_last_error()
+        st = _L().ttgpu_cache_backward_step_device(cache.handle, table.handle, ctx.handle,
+                                                   _C.c_void_p(d_grad.data_ptr()), _C.c_double(LR))
+        assert st == 0, _L().ttgpu_last_error()
+
     def step():
+        if cache is not None:
+            cache_step()
+            return
         table.forward_device(ctx, d_idx.data_ptr(), L, d_off.data_ptr(), B, d_out.data_ptr(),
                              save=True)
         if world == 1:
@@ -275,7 +302,12 @@ def main():
     for _ in range(args.warmup):
         step()
     table.check()
-    use_graph = world == 1
+    if cache is not None:
+        cache.warmup_finalize(table)
+        for _ in range(2):
+            step()
+        table.check()
+    use_graph = world == 1 and cache is None  # the cached forward syncs once (chain-part size)
     kernels_per_step = None
     if use_graph:
         table.graph_begin()
@@ -360,6 +392,18 @@ def main():
     hctx = tt.ForwardContext(table)
 
     def e2e_step():
+        if cache is not None:  # EmbeddingLayer forward / backward / step (model.hpp:195-284)
+            st = lib().ttgpu_cache_forward(cache.handle, table.handle, hctx.handle,
+                                           h_idx.ctypes.data_as(C.c_void_p), L,
+                                           h_off.ctypes.data_as(C.c_void_p), B, None, 0, 1,
+                                           h_out.ctypes.data_as(C.c_void_p))
+            assert st == 0, lib().ttgpu_last_error()
+            st = lib().ttgpu_cache_backward(cache.handle, table.handle, hctx.handle,
+                                            h_grad.ctypes.data_as(C.c_void_p), B * N)
+            assert st == 0, lib().ttgpu_last_error()
+            st = lib().ttgpu_cache_step(cache.handle, table.handle, C.c_double(LR))
+            assert st == 0, lib().ttgpu_last_error()
+            return
         st = lib().ttgpu_forward(table.handle, h_idx.ctypes.data_as(C.c_void_p), L,
                                  h_off.ctypes.data_as(C.c_void_p), B, None, 0, 2048, 1,
                                  h_out.ctypes.data_as(C.c_void_p), hctx.handle)
@@ -464,6 +508,8 @@ def main():
                    "forward": "ffma" if args.fast_forward else "exact (bit-identical to reference)",
                    "graph": use_graph},
         "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
+        "cache": ({"capacity": cache.capacity(), "hit_rate": cache.hit_rate()}
+                  if cache is not None else None),
         "clocks": clk,
         "roofline": roofline,
         "roofline_hbm": roofline_hbm,

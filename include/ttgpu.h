@@ -236,6 +236,25 @@ int ttgpu_uniform_indices(int64_t rows, uint64_t seed, int64_t n, int64_t* indic
 /* init_tt_cores(table, InitSpec::sampled_gaussian(), seed) (initializer.hpp:143-154) */
 int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed);
 
+/* ---- device index streams -------------------------
+ * ZipfianSampler(population, s) (data.hpp:16-28, data.cpp:8-33) resident on
+ * the GPU: the CDF is built on the host with the reference's loop and
+ * inverted on the device (upper_bound); s = 0 is uniform.  Variates come from
+ * a counter-based SplitMix64 stream -- element i of a draw uses counter + i,
+ * so a stream splits across calls and ranks deterministically.  Same
+ * distribution as the reference, not the same bytes (its mt19937_64 stream
+ * is reproduced on the host by ttgpu_zipf_batch for parity runs). */
+typedef struct ttgpu_sampler ttgpu_sampler;
+int ttgpu_sampler_create(int64_t population, double exponent, int device, void* stream,
+                         ttgpu_sampler** out);
+int ttgpu_sampler_destroy(ttgpu_sampler* s);
+int ttgpu_sampler_set_stream(ttgpu_sampler* s, void* stream);
+int ttgpu_sampler_draw_device(ttgpu_sampler* s, uint64_t seed, uint64_t counter, int64_t n,
+                              int64_t* d_out);
+/* offsets of num_bags fixed-size bags: off[b] = b * pooling_factor (b <= bags) */
+int ttgpu_bag_offsets_device(int64_t bags, int64_t pooling_factor, int64_t* d_offsets,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1260,3 +1260,4 @@ int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
 }  // extern "C"
 
 #include "lfu_cache_host.inl"
+#include "sampler_host.inl"
