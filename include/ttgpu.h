@@ -233,6 +233,9 @@ int ttgpu_zipf_batch(int64_t population, double exponent, uint64_t seed, int64_t
                      int64_t pooling_factor, int64_t* indices, int64_t* offsets);
 /* Rng(seed).uniform_int(0, rows) x n (rng.hpp:47-51) */
 int ttgpu_uniform_indices(int64_t rows, uint64_t seed, int64_t n, int64_t* indices);
+/* Rng::derive(seed, stream).uniform_int(0, rows) x n (rng.hpp:25-29,47-51) */
+int ttgpu_derived_uniform_indices(int64_t rows, uint64_t seed, uint64_t stream, int64_t n,
+                                  int64_t* out);
 /* init_tt_cores(table, InitSpec::sampled_gaussian(), seed) (initializer.hpp:143-154) */
 int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed);
 

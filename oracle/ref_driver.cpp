@@ -360,6 +360,12 @@ void ref_rng_uniform_int(uint64_t seed, int64_t lo, int64_t hi, int64_t n, int64
 
 // oracle_helpers.hpp:65-77 random_batch; offsets has room for bags+1, indices/weights
 // for bags*max_size.  Returns the lookup count.
+// Rng::derive(seed, stream).uniform_int(0, rows) x n (bench.hpp:82-89)
+void ref_derived_uniform_int(uint64_t seed, uint64_t stream, int64_t rows, int64_t n, int64_t* out) {
+  Rng r = Rng::derive(seed, stream);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.uniform_int(0, rows);
+}
+
 int64_t ref_random_batch(uint64_t seed, int64_t rows, int64_t bags, int64_t min_size,
                          int64_t max_size, int weighted, int64_t* idx, int64_t* off,
                          double* w) {

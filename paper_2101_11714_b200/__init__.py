@@ -23,6 +23,7 @@ from .ttrec import (  # noqa: F401
     recompose_index,
     sgd_step,
     uniform_indices,
+    derived_uniform_indices,
 )
 from . import lfu_cache  # noqa: F401,E402
 from .lfu_cache import (  # noqa: F401,E402

@@ -99,6 +99,7 @@ _SIGS = {
     "ttgpu_stats_add_rows": (None, [C.c_uint64]),
     "ttgpu_zipf_batch": (C.c_int, [i64, C.c_double, C.c_uint64, i64, i64, vp, vp]),
     "ttgpu_uniform_indices": (C.c_int, [i64, C.c_uint64, i64, vp]),
+    "ttgpu_derived_uniform_indices": (C.c_int, [i64, C.c_uint64, C.c_uint64, i64, vp]),
     "ttgpu_init_sampled_gaussian": (C.c_int, [vp, C.c_uint64]),
     "ttgpu_sampler_create": (C.c_int, [i64, C.c_double, C.c_int, vp, vpp]),
     "ttgpu_sampler_destroy": (C.c_int, [vp]),

@@ -1221,6 +1221,18 @@ int ttgpu_uniform_indices(int64_t rows, uint64_t seed, int64_t n, int64_t* out) 
   });
 }
 
+int ttgpu_derived_uniform_indices(int64_t rows, uint64_t seed, uint64_t stream, int64_t n,
+                                  int64_t* out) {
+  return guarded([&] {
+    require_arg(rows >= 1, "rows must be positive");
+    std::mt19937_64 eng(0);  // Rng::derive(seed, stream) (rng.hpp:25-29)
+    eng.seed(splitmix(splitmix(seed) ^ splitmix(stream ^ 0xD1B54A32D192ED03ull)));
+    for (int64_t i = 0; i < n; ++i)
+      out[i] = static_cast<int64_t>(
+          std::uniform_int_distribution<uint64_t>(0, static_cast<uint64_t>(rows - 1))(eng));
+  });
+}
+
 int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
   return guarded([&] {
     // InitSpec::sampled_gaussian(): threshold 2, target 1/(3N), MomentMatched

@@ -502,3 +502,10 @@ def uniform_indices(rows: int, seed: int, n: int) -> np.ndarray:
     out = np.zeros(n, np.int64)
     _raise(lib().ttgpu_uniform_indices(rows, seed, n, _p(out)))
     return out
+
+
+def derived_uniform_indices(rows: int, seed: int, stream: int, n: int) -> np.ndarray:
+    """Rng::derive(seed, stream).uniform_int(0, rows) x n (rng.hpp:25-29,47-51)."""
+    out = np.zeros(n, np.int64)
+    _raise(lib().ttgpu_derived_uniform_indices(rows, seed, stream, n, _p(out)))
+    return out
