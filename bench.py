@@ -52,6 +52,11 @@ CONFIGS = {
                  pf=32, zipf=0.0,
                  desc="40M rows (200x200x1000), dim 64 (4x4x4), R=64, 65,536 bags x 32, uniform"),
 }
+CONFIGS["cfg5"] = dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32,
+                      bags=65536, pf=1, zipf=1.05, collection=True,
+                      desc="DLRM cfg5 TT part: the 7 largest Criteo-Kaggle tables (paper Table 2) "
+                           "at R=32, 65,536 bags x 1 per table, Zipf(1.05) (device sampler), "
+                           "one multi-stream CUDA graph per step")
 LR = 0.01
 
 
@@ -205,6 +210,100 @@ def run_reference(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_collection(args, cfg, rank, world, local):
+    """cfg5's TT part: 7 tables trained in one step, one CUDA graph with a
+    fork/join over the table streams (paper_2101_11714_b200/collection.py).
+    The same step with every table on one stream is timed beside it."""
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2101_11714_b200 as tt
+    from paper_2101_11714_b200.collection import TtEmbeddingCollection, kaggle_plans
+    from paper_2101_11714_b200.streams import DeviceZipfSampler, bag_offsets_device
+
+    plans = kaggle_plans(cfg["rank"], cfg["emb"])
+    col = TtEmbeddingCollection(plans, [f"kaggle{i}" for i in range(len(plans))], device=local)
+    B, N = cfg["bags"], cfg["emb"]
+    L = B * cfg["pf"]
+    inputs, keep = [], []
+    for i, p in enumerate(plans):
+        s = DeviceZipfSampler(p.num_rows, cfg["zipf"], device=local)
+        d_idx = torch.empty(L, dtype=torch.int64, device=dev)
+        d_off = torch.empty(B + 1, dtype=torch.int64, device=dev)
+        s.draw_device(7 + 131 * rank, i * L, L, d_idx.data_ptr())
+        bag_offsets_device(B, cfg["pf"], d_off.data_ptr())
+        d_out = torch.empty((B, N), dtype=torch.float32, device=dev)
+        d_g = torch.randn((B, N), dtype=torch.float32, device=dev,
+                          generator=torch.Generator(device=dev).manual_seed(100 + i))
+        keep += [s, d_idx, d_off, d_out, d_g]
+        inputs.append((d_idx.data_ptr(), L, d_off.data_ptr(), B, d_out.data_ptr(), d_g.data_ptr()))
+    torch.cuda.synchronize(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(run):
+        for _ in range(args.warmup):
+            run()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        with torch.cuda.stream(col.main):
+            for i in range(args.steps):
+                flush.fill_(i & 0xff)
+                ev[i][0].record(col.main)
+                run()
+                ev[i][1].record(col.main)
+        torch.cuda.synchronize(dev)
+        tot = float(sum(a.elapsed_time(b) for a, b in ev))
+        if world > 1:
+            t = torch.tensor([tot], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            tot = float(t.item())
+        return tot / args.steps
+
+    for _ in range(3):  # allocate every workspace before capture
+        col.step(inputs, LR)
+    col.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    col.capture(inputs, LR)
+    ms_par = timed(col.replay)
+    clk = clocks.stop()
+    # the same step with every table on the main stream (no overlap between tables)
+    for t in col.tables:
+        t.set_stream(col.main.cuda_stream)
+    saved = col.streams
+    col.streams = [col.main] * len(saved)
+    col.capture(inputs, LR)
+    ms_seq = timed(col.replay)
+    col.synchronize()
+    total = world * len(plans) * L
+    if rank == 0:
+        line = {"metric": METRIC + " [cfg5: 7-table TT step]", "value": total / (ms_par / 1e3),
+                "unit": "indices/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_par, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic: device Zipf(1.05) streams per table (reference CDF), "
+                        "sampled-Gaussian cores, N(0,1) grad_out",
+                "config": {"workload": cfg["desc"], "tables": len(plans),
+                           "lookups_per_step": total, "parallelism":
+                               f"dp{world}" if world > 1 else "single-gpu",
+                           "l2": "flushed (256 MiB write) before every timed step"},
+                "sequential_ms_per_step": ms_seq,
+                "multi_stream_speedup": ms_seq / ms_par,
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -225,6 +324,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, cfg, rank)
+        return
+    if cfg.get("collection"):
+        run_collection(args, cfg, rank, world, local)
         return
 
     import torch

@@ -37,3 +37,4 @@ from .lfu_cache import (  # noqa: F401,E402
 from . import sharding  # noqa: F401,E402
 from . import checkpoint  # noqa: F401,E402
 from . import streams  # noqa: F401,E402
+from . import collection  # noqa: F401,E402

@@ -1,0 +1,125 @@
+"""Multi-table TT embedding step (BASELINE cfg5's TT part).
+
+The 7 largest Criteo-Kaggle tables TT-compressed at rank 32 (paper Table 2,
+the reference's kRefTables, tools/ttrec.cpp:30-34), each one TtTable on its
+own CUDA stream.  One training step runs every table's forward_bags(save) +
+backward_bags + sgd_step; the per-table pipelines are independent, so they
+are captured into ONE CUDA graph with a fork/join over the table streams:
+each table's kernels are short latency-bound launches that leave most SMs
+idle, and the graph lets the 7 pipelines fill the GPU together.
+
+Multi-GPU (`world > 1`): batch-sharded like DataParallelTable; every table's
+dense core gradient goes into one coalesced NCCL allreduce(SUM) (a single
+collective group for all 7 buffers), then the identical SGD per replica.
+
+Not here: the 19 uncompressed DLRM features and the MLPs (SURVEY §2 rows
+8-14, out of scope) -- this is the TT-embedding part of the cfg5 step.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+import numpy as np
+
+from .ttrec import ForwardContext, ShapePlan, TtTable, plan_shapes
+
+# paper Table 2 / the reference's kRefTables (tools/ttrec.cpp:30-34): rows, row factors
+KAGGLE_TT_TABLES = [
+    (10131227, [200, 220, 250]), (8351593, [200, 200, 209]), (7046547, [200, 200, 200]),
+    (5461306, [166, 175, 188]), (2202608, [125, 130, 136]), (286181, [53, 72, 75]),
+    (142572, [50, 52, 55]),
+]
+
+
+def kaggle_plans(rank: int = 32, emb_dim: int = 16) -> List[ShapePlan]:
+    return [plan_shapes(n, emb_dim, 3, rank, rf, [2, 2, 4]) for n, rf in KAGGLE_TT_TABLES]
+
+
+class TtEmbeddingCollection:
+    """Several TtTables trained in one step; inputs are device pointers."""
+
+    def __init__(self, plans: Sequence[ShapePlan], names: Sequence[str] = (), device: int = 0,
+                 seed: int = 1, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch = torch
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.streams = [torch.cuda.Stream(device=self.dev) for _ in plans]
+        self.main = torch.cuda.Stream(device=self.dev)
+        self.tables: List[TtTable] = []
+        for i, p in enumerate(plans):
+            name = names[i] if i < len(names) else f"tt{i}"
+            t = TtTable(p, name, np.float32, device=device, stream=self.streams[i].cuda_stream)
+            t.init_sampled_gaussian(seed + i)
+            self.tables.append(t)
+        self.ctxs = [ForwardContext(t) for t in self.tables]
+        self.graph = None
+        self._grad_views = None
+        if self.world > 1:
+            from .sharding import _device_view
+
+            views = []
+            for t in self.tables:
+                ptr, n = t.grad_buffer()
+                views.append(_device_view(ptr, n, "<f4", device))
+            self._grad_views = views
+
+    def _table_step(self, i, idx_ptr, L, off_ptr, B, out_ptr, grad_ptr, lr):
+        t, c = self.tables[i], self.ctxs[i]
+        t.forward_device(c, idx_ptr, L, off_ptr, B, out_ptr, save=True)
+        if self.world == 1:
+            t.backward_sgd_device(c, grad_ptr, lr)
+        else:
+            t.backward_device(c, grad_ptr)
+
+    def step(self, inputs, lr: float):
+        """inputs: per table (idx_ptr, L, off_ptr, B, out_ptr, grad_ptr).  Forks the
+        table streams off `main`, joins them back; with world > 1 the 7 gradient
+        buffers are reduced in one coalesced NCCL call before the SGD."""
+        torch = self.torch
+        ev0 = torch.cuda.Event()
+        ev0.record(self.main)
+        for i, s in enumerate(self.streams):
+            s.wait_event(ev0)
+            self._table_step(i, *inputs[i], lr)
+        for s in self.streams:
+            e = torch.cuda.Event()
+            e.record(s)
+            self.main.wait_event(e)
+        if self.world > 1:
+            from .sharding import allreduce_sum_coalesced_
+
+            with torch.cuda.stream(self.main):
+                allreduce_sum_coalesced_(self._grad_views, self.group)
+            ev1 = torch.cuda.Event()
+            ev1.record(self.main)
+            for i, s in enumerate(self.streams):
+                s.wait_event(ev1)
+                self.tables[i].apply_grad(lr)
+            for s in self.streams:
+                e = torch.cuda.Event()
+                e.record(s)
+                self.main.wait_event(e)
+
+    def capture(self, inputs, lr: float):
+        """One CUDA graph of the whole multi-table step (fork/join over the
+        table streams).  Workspaces must already exist (run step() once)."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize(self.dev)
+        with torch.cuda.graph(g, stream=self.main):
+            self.step(inputs, lr)
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
+    def synchronize(self):
+        self.torch.cuda.synchronize(self.dev)
+        for t in self.tables:
+            t.check()

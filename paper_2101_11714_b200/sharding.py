@@ -78,6 +78,24 @@ def allreduce_sum_(tensor, group=None):
     return tensor
 
 
+def allreduce_sum_coalesced_(tensors, group=None):
+    """SUM-allreduce several buffers as ONE collective group (NCCL coalescing:
+    one launch for all of a multi-table step's core gradients); backends
+    without coalescing (gloo in the CPU tests) reduce them one by one."""
+    import torch.distributed as dist
+
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return tensors
+    if dist.get_backend(group) == "nccl":
+        with dist._coalescing_manager(group=group, device=tensors[0].device):
+            for t in tensors:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    else:
+        for t in tensors:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return tensors
+
+
 def _device_view(ptr: int, n: int, typestr: str, device: int):
     """Zero-copy torch view of a library-owned device buffer."""
     import torch
@@ -188,4 +206,5 @@ def cache_counts_view(cache, device: int = 0):
 
 
 __all__ = ["partition_bags", "equal_bag_bounds", "shard_batch", "shard_rows", "allreduce_sum_",
+           "allreduce_sum_coalesced_",
            "DataParallelTable", "replica_checksum", "FrequencySync", "cache_counts_view"]

@@ -209,3 +209,38 @@ def test_partition_bags_on_reference_batches():
         idx, off, w = ref.random_batch(seed, 1000, 50, 0, 7, True)
         for workers in (2, 3, 8):
             assert list(partition_bags(off, workers)) == _ref_partition(list(off), workers)
+
+
+def _coalesced_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2101_11714_b200.sharding import allreduce_sum_coalesced_
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bufs = [torch.full((n,), float(rank + 1) * (k + 1)) for k, n in enumerate((7, 3, 11))]
+        allreduce_sum_coalesced_(bufs)
+        q.put((rank, [b.numpy().copy() for b in bufs]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_coalesced_allreduce_of_table_gradients():
+    """The multi-table step reduces every table's gradient buffer in one group."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coalesced_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, bufs in res:
+        for k, b in enumerate(bufs):
+            assert np.all(b == 3.0 * (k + 1))
