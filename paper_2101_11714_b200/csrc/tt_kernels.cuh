@@ -514,8 +514,12 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
                            T* __restrict__ D0, T* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R1 = P.r[1], C1 = P.C1, P0 = P.n[0], s0 = P.slice[0], s1 = P.slice[1];
-  T* g1s = reinterpret_cast<T*>(smem_raw);  // R1 x C1
-  T* acc = g1s + s1;                        // R1 x C1
+  // G1[i1] staged transposed with an odd row pitch (C1 x (R1+1)): the D0
+  // loop's lanes walk r, so reads are conflict-free (row-major R1 x C1 with
+  // C1 a multiple of 32 put every lane of a warp in the same bank)
+  const int R1p = R1 + 1;
+  T* g1t = reinterpret_cast<T*>(smem_raw);              // C1 x R1p
+  T* acc = g1t + static_cast<int64_t>(C1) * R1p;        // R1 x C1
   const T* G0 = cores + P.coff[0];
   const T* G1 = cores + P.coff[1];
   const int U = counts[0];
@@ -531,7 +535,8 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
       while (hi < p1 && pair_key_u[hi] / m0 == i1) ++hi;
       __syncthreads();
       for (int e = threadIdx.x; e < s1; e += blockDim.x) {
-        g1s[e] = G1[static_cast<int64_t>(i1) * s1 + e];
+        const int rr = e / C1, c = e - rr * C1;
+        g1t[c * R1p + rr] = G1[static_cast<int64_t>(i1) * s1 + e];
         acc[e] = T(0);
       }
       __syncthreads();
@@ -543,7 +548,7 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
         for (int e = threadIdx.x; e < P0 * R1; e += blockDim.x) {
           const int a = e / R1, rr = e - a * R1;
           T v = T(0);
-          for (int c = 0; c < C1; ++c) v = madd<T, false>(Sp[a * C1 + c], g1s[rr * C1 + c], v);
+          for (int c = 0; c < C1; ++c) v = madd<T, false>(Sp[a * C1 + c], g1t[c * R1p + rr], v);
           D0[static_cast<int64_t>(p) * s0 + e] = v;
         }
         // acc[r][c] += sum_a G0[a][r] * S[a][c]

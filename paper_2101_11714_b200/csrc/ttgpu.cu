@@ -577,7 +577,8 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   t->mark("bwd_tail");
   // ---- head: D0 per pair, dG1 partials per i1 run
   {
-    const size_t smem = sizeof(T) * 2 * static_cast<size_t>(P.slice[1]);
+    const size_t smem = sizeof(T) * (static_cast<size_t>(P.slice[1]) +
+                                     static_cast<size_t>(P.C1) * (P.r[1] + 1));
     if (smem > 227 * 1024) fail(TTGPU_ERR_INVALID_ARGUMENT, "G1 slice too large for shared memory");
     auto kern = k_head_bwd<T>;
     set_smem(kern, smem);
