@@ -314,6 +314,8 @@ def main():
     ap.add_argument("--fast-forward", action="store_true",
                     help="FFMA forward instead of the bit-exact default")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl", action="store_true",
+                    help="N>1: NCCL allreduce + SGD kernel instead of the fused peer reduce+SGD")
     ap.add_argument("--profile", action="store_true", help="print per-phase times")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -394,22 +396,57 @@ def main():
                              save=True)
         if world == 1:
             table.backward_sgd_device(ctx, d_grad.data_ptr(), LR)
+        elif reducer is not None:  # one fused kernel: peers' gradients over NVLink + SGD
+            table.backward_device(ctx, d_grad.data_ptr())
+            reducer.reduce_sgd(LR)
         else:
             table.backward_device(ctx, d_grad.data_ptr())
             with torch.cuda.stream(stream):
                 dist.all_reduce(gbuf)
             table.apply_grad(LR)
 
+    # N>1: the fused peer reduce+SGD (ttgpu_peer_reduce_sgd) unless --nccl; it falls
+    # back to NCCL if P2P is unavailable, a peer wait times out, or replicas diverge
+    reducer, reduce_path = None, ("nccl-allreduce+sgd" if world > 1 else None)
+    if world > 1 and not args.nccl and cache is None:
+        try:
+            from paper_2101_11714_b200.sharding import PeerReducer
+
+            ok = all(torch.cuda.can_device_access_peer(local, j)
+                     for j in range(torch.cuda.device_count()) if j != local)
+            if ok:
+                reducer = PeerReducer(table)
+                reduce_path = "fused-peer-reduce+sgd"
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] peer reduce unavailable ({e}); using NCCL", file=sys.stderr)
+            reducer = None
+
     # warm-up (allocates every workspace), validation, then graph capture
     for _ in range(args.warmup):
         step()
     table.check()
+    if reducer is not None:
+        from paper_2101_11714_b200.sharding import replica_checksum
+
+        bad = torch.tensor([1 if reducer.timed_out() else 0], device=dev)
+        ck = torch.tensor(replica_checksum([table.core(k) for k in range(plan.tt_dim)]),
+                          dtype=torch.int64, device=dev)
+        allc = [torch.zeros_like(ck) for _ in range(world)]
+        dist.all_gather(allc, ck)
+        dist.all_reduce(bad)
+        if int(bad.item()) or not all(torch.equal(allc[0], c) for c in allc):
+            print("[bench] peer reduce failed validation; using NCCL", file=sys.stderr)
+            reducer, reduce_path = None, "nccl-allreduce+sgd (fused path failed validation)"
+            for _ in range(2):
+                step()
+            table.check()
     if cache is not None:
         cache.warmup_finalize(table)
         for _ in range(2):
             step()
         table.check()
-    use_graph = world == 1 and cache is None  # the cached forward syncs once (chain-part size)
+    # the cached forward syncs once (chain-part size); NCCL calls stay outside graphs
+    use_graph = cache is None and (world == 1 or reducer is not None)
     kernels_per_step = None
     if use_graph:
         table.graph_begin()
@@ -516,9 +553,12 @@ def main():
             st = lib().ttgpu_backward(table.handle, hctx.handle, L, B,
                                       h_grad.ctypes.data_as(C.c_void_p), B * N, None)
             assert st == 0
-            with torch.cuda.stream(stream):
-                dist.all_reduce(gbuf)
-            table.apply_grad(LR)
+            if reducer is not None:
+                reducer.reduce_sgd(LR)
+            else:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(gbuf)
+                table.apply_grad(LR)
             table.sync()
 
     for _ in range(3):
@@ -608,7 +648,7 @@ def main():
                    "parallelism": f"dp{world}" if world > 1 else "single-gpu",
                    "l2": "flushed (256 MiB write) before every timed step, outside the events",
                    "forward": "ffma" if args.fast_forward else "exact (bit-identical to reference)",
-                   "graph": use_graph},
+                   "graph": use_graph, "gradient_reduce": reduce_path},
         "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
         "cache": ({"capacity": cache.capacity(), "hit_rate": cache.hit_rate()}
                   if cache is not None else None),

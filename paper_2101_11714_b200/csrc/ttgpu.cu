@@ -148,7 +148,10 @@ using namespace ttgpu;
 __global__ void k_noop() {}
 
 struct ttgpu_ctx;
+struct ttgpu_peers;
+void ttgpu_destroy_peers(struct ttgpu_peers*);
 struct ttgpu_table {
+  void destroy_peers();
   ShapePlan plan;
   std::string name;
   int dtype = TTGPU_F32;
@@ -164,6 +167,8 @@ struct ttgpu_table {
   // forward_bags call; without recycling each would re-cudaMalloc its buffers)
   std::vector<ttgpu_ctx*> ctx_pool;
   unsigned long long* h_errs = nullptr;  // pinned host mirror of errs
+  DevBuf peer_flag_buf;                   // fused peer reduce: flag block (peer_host.inl)
+  struct ttgpu_peers* peers = nullptr;
   uint64_t generation = 0;
   bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
   bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
@@ -206,6 +211,7 @@ struct ttgpu_table {
   cudaGraphExec_t graph_exec = nullptr;
   ~ttgpu_table() {
     if (h_errs) cudaFreeHost(h_errs);
+    destroy_peers();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (auto& m : marks) cudaEventDestroy(m.second);
@@ -1274,3 +1280,7 @@ int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
 
 #include "lfu_cache_host.inl"
 #include "sampler_host.inl"
+#include "peer_host.inl"
+
+void ttgpu_destroy_peers(ttgpu_peers* p) { delete p; }
+void ttgpu_table::destroy_peers() { ttgpu_destroy_peers(peers); peers = nullptr; }

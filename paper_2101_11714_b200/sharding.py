@@ -160,6 +160,58 @@ class DataParallelTable:
         self.table.apply_grad(lr)
 
 
+class PeerReducer:
+    """Fused reduce + SGD over peer memory for one replicated table
+    (ttgpu_peer_reduce_sgd): every rank reads all ranks' dense gradient
+    buffers over NVLink, sums them in rank order and applies the SGD in one
+    kernel -- the NCCL allreduce and the separate SGD launch disappear.
+    Handles are exchanged once with an all_gather on `group`."""
+
+    def __init__(self, table: TtTable, group=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from ._lib import lib
+        from .ttrec import _raise
+
+        self.table = table
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        gh = (C.c_char * 64)()
+        fh = (C.c_char * 64)()
+        _raise(lib().ttgpu_peer_export(table.handle, gh, fh))
+        mine = torch.tensor(list(bytes(gh)) + list(bytes(fh)), dtype=torch.uint8)
+        if world > 1:
+            bufs = [torch.zeros_like(mine) for _ in range(world)]
+            dist.all_gather_object(bufs, mine, group=group)
+        else:
+            bufs = [mine]
+        allg = b"".join(bytes(b[:64].tolist()) for b in bufs)
+        allf = b"".join(bytes(b[64:].tolist()) for b in bufs)
+        self._g = C.create_string_buffer(allg, len(allg))
+        self._f = C.create_string_buffer(allf, len(allf))
+        _raise(lib().ttgpu_peer_attach(table.handle, world, rank, self._g, self._f))
+        self.world, self.rank = world, rank
+
+    def reduce_sgd(self, lr: float):
+        from ._lib import lib
+        from .ttrec import _raise
+
+        _raise(lib().ttgpu_peer_reduce_sgd(self.table.handle, float(lr)))
+
+    def timed_out(self) -> bool:
+        import ctypes as C
+
+        from ._lib import lib
+        from .ttrec import _raise
+
+        v = C.c_int()
+        _raise(lib().ttgpu_peer_status(self.table.handle, C.byref(v)))
+        return bool(v.value)
+
+
 def replica_checksum(cores: List[np.ndarray]) -> Tuple[int, ...]:
     """Bitwise fingerprint of a replica's cores (for cross-rank equality checks)."""
     import hashlib
@@ -206,5 +258,5 @@ def cache_counts_view(cache, device: int = 0):
 
 
 __all__ = ["partition_bags", "equal_bag_bounds", "shard_batch", "shard_rows", "allreduce_sum_",
-           "allreduce_sum_coalesced_",
+           "allreduce_sum_coalesced_", "PeerReducer",
            "DataParallelTable", "replica_checksum", "FrequencySync", "cache_counts_view"]
