@@ -477,6 +477,305 @@ __global__ void k_chunk_reduce(DevPlan P, const T* __restrict__ cores, const T* 
   }
 }
 
+// ------------------------------------- backward, d == 3: staged chunk sums --
+// Same contract as k_chunk_reduce (one chunk of C sorted positions per CTA
+// iteration, one partial per run, runs numbered from scan[c0] >> 32) and the
+// same per-element arithmetic, restructured for wide rows (cfg3: W1 = 1024):
+// the chunk's small per-lookup operands are staged once in shared memory and
+// every thread keeps ITS output elements of the running sum in registers, so
+// no per-lookup row is materialised or folded through shared memory.
+//   k_srun3  (S per pair run):   contrib[a][r] = Σ_j D2[a][j] · G2[i2][r][j]
+//   k_trun3  (dG2 per i2 run):   contrib[q][j] = Σ_a H[pair][a][q] · D2[a][j]
+// D2 = T(alpha) * grad[bag] (bwd_chain), products accumulated from zero with
+// FMA in the same order as warp_mm_abt / the MODE 1 loop of k_chunk_reduce.
+constexpr int kRun3MaxEPT = 8;   // output elements per thread (row width <= 8 x 256)
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ cores,
+                                               const uint32_t* __restrict__ tail_dig,
+                                               const int32_t* __restrict__ lk_bag,
+                                               const T* __restrict__ lk_alpha,
+                                               const T* __restrict__ grad,
+                                               const uint32_t* __restrict__ s_key,
+                                               const uint32_t* __restrict__ s_lk,
+                                               const unsigned long long* __restrict__ scan,
+                                               int64_t L, int C, T* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = P.N, R2 = P.r[2], n2 = P.n[2], S2 = P.slice[2], W = P.W1;
+  T* d2s = reinterpret_cast<T*>(smem_raw);               // C x N
+  T* g2s = d2s + static_cast<int64_t>(C) * N;            // C x S2
+  uint32_t* keys = reinterpret_cast<uint32_t*>(g2s + static_cast<int64_t>(C) * S2);  // C
+  const T* G2 = cores + P.coff[2];
+  const int64_t nchunks = (L + C - 1) / C;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = ch * C;
+    const int n = static_cast<int>(L - c0 < C ? L - c0 : C);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * N; e += blockDim.x) {
+      const int q = e / N, j = e - q * N;
+      const int64_t l = s_lk[c0 + q];
+      d2s[e] = mul_rn<T>(lk_alpha[l], grad[static_cast<int64_t>(lk_bag[l]) * N + j]);
+    }
+    for (int e = threadIdx.x; e < n * S2; e += blockDim.x) {
+      const int q = e / S2, j = e - q * S2;
+      const int64_t l = s_lk[c0 + q];
+      g2s[e] = G2[static_cast<int64_t>(tail_dig[l]) * S2 + j];
+    }
+    for (int q = threadIdx.x; q < n; q += blockDim.x) keys[q] = s_key[c0 + q];
+    __syncthreads();
+    const int run0 = static_cast<int>(scan[c0] >> 32) - 1;
+    T acc[kRun3MaxEPT];
+    int aoff[kRun3MaxEPT], roff[kRun3MaxEPT];  // element -> (a*n2, r*n2), hoisted
+#pragma unroll
+    for (int k = 0; k < kRun3MaxEPT; ++k) {
+      acc[k] = T(0);
+      const int e = threadIdx.x + k * blockDim.x;
+      const int a = e / R2;
+      aoff[k] = a * n2;
+      roff[k] = (e - a * R2) * n2;
+    }
+    int run = run0;
+    for (int q = 0; q < n; ++q) {
+      if (q > 0 && keys[q] != keys[q - 1]) {
+#pragma unroll
+        for (int k = 0; k < kRun3MaxEPT; ++k) {
+          const int e = threadIdx.x + k * blockDim.x;
+          if (e < W) partials[static_cast<int64_t>(run) * W + e] = acc[k];
+          acc[k] = T(0);
+        }
+        ++run;
+      }
+      const T* d = d2s + q * N;
+      const T* gg = g2s + q * S2;
+#pragma unroll
+      for (int k = 0; k < kRun3MaxEPT; ++k) {
+        const int e = threadIdx.x + k * blockDim.x;
+        if (e < W) {
+          T v = T(0);
+          if (n2 == 4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v = madd<T, false>(d[aoff[k] + j], gg[roff[k] + j], v);
+          } else {
+            for (int j = 0; j < n2; ++j) v = madd<T, false>(d[aoff[k] + j], gg[roff[k] + j], v);
+          }
+          acc[k] += v;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRun3MaxEPT; ++k) {
+      const int e = threadIdx.x + k * blockDim.x;
+      if (e < W) partials[static_cast<int64_t>(run) * W + e] = acc[k];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_trun3(DevPlan P, const T* __restrict__ H,
+                                               const int32_t* __restrict__ lk_pid,
+                                               const int32_t* __restrict__ lk_bag,
+                                               const T* __restrict__ lk_alpha,
+                                               const T* __restrict__ grad,
+                                               const uint32_t* __restrict__ s_key,
+                                               const uint32_t* __restrict__ s_lk,
+                                               const unsigned long long* __restrict__ scan,
+                                               int64_t L, int C, int sub, T* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = P.N, R2 = P.r[2], n2 = P.n[2], P1 = P.prefix[1], W1 = P.W1, Wc = P.slice[2];
+  T* hs = reinterpret_cast<T*>(smem_raw);                // sub x W1
+  T* d2s = hs + static_cast<int64_t>(sub) * W1;          // sub x N
+  uint32_t* keys = reinterpret_cast<uint32_t*>(d2s + static_cast<int64_t>(sub) * N);  // C
+  const int64_t nchunks = (L + C - 1) / C;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = ch * C;
+    const int n = static_cast<int>(L - c0 < C ? L - c0 : C);
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x) keys[q] = s_key[c0 + q];
+    const int run0 = static_cast<int>(scan[c0] >> 32) - 1;
+    T acc[kRun3MaxEPT];
+#pragma unroll
+    for (int k = 0; k < kRun3MaxEPT; ++k) acc[k] = T(0);
+    int run = run0;
+    for (int q0 = 0; q0 < n; q0 += sub) {
+      const int m = n - q0 < sub ? n - q0 : sub;
+      __syncthreads();  // previous sub-batch consumed (and keys staged)
+      for (int e = threadIdx.x; e < m * W1; e += blockDim.x) {
+        const int q = e / W1, x = e - q * W1;
+        const int64_t l = s_lk[c0 + q0 + q];
+        hs[e] = H[static_cast<int64_t>(lk_pid[l]) * W1 + x];
+      }
+      for (int e = threadIdx.x; e < m * N; e += blockDim.x) {
+        const int q = e / N, j = e - q * N;
+        const int64_t l = s_lk[c0 + q0 + q];
+        d2s[e] = mul_rn<T>(lk_alpha[l], grad[static_cast<int64_t>(lk_bag[l]) * N + j]);
+      }
+      __syncthreads();
+      for (int qq = 0; qq < m; ++qq) {
+        const int q = q0 + qq;
+        if (q > 0 && keys[q] != keys[q - 1]) {
+#pragma unroll
+          for (int k = 0; k < kRun3MaxEPT; ++k) {
+            const int e = threadIdx.x + k * blockDim.x;
+            if (e < Wc) partials[static_cast<int64_t>(run) * Wc + e] = acc[k];
+            acc[k] = T(0);
+          }
+          ++run;
+        }
+        const T* u = hs + qq * W1;
+        const T* d = d2s + qq * N;
+#pragma unroll
+        for (int k = 0; k < kRun3MaxEPT; ++k) {
+          const int e = threadIdx.x + k * blockDim.x;
+          if (e < Wc) {
+            const int qr = e / n2, j = e - qr * n2;
+            T v = T(0);
+            for (int i = 0; i < P1; ++i) v = madd<T, false>(u[i * R2 + qr], d[i * n2 + j], v);
+            acc[k] += v;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRun3MaxEPT; ++k) {
+      const int e = threadIdx.x + k * blockDim.x;
+      if (e < Wc) partials[static_cast<int64_t>(run) * Wc + e] = acc[k];
+    }
+  }
+}
+
+// ------------------------ d == 3, wide rows: work in pair order, H staged --
+// The tail contractions need the pair's head row H (P1 x R2; 4 KB at cfg3).
+// Walking lookups in i2 order re-reads H per lookup from HBM (H of all pairs
+// does not fit L2); walking them in PAIR order stages H once per pair run.
+// Per-lookup results go to a buffer (y rows for pooling; dG2 contributions
+// at the lookup's position in the i2 order), then a fixed-order segmented
+// sum / pooling pass produces the outputs -- deterministic.
+__global__ void k_inv_perm(const uint32_t* __restrict__ sorted_lk, int64_t L,
+                           uint32_t* __restrict__ pos_of) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < L;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    pos_of[sorted_lk[p]] = static_cast<uint32_t>(p);
+}
+
+// MODE 0: y[l][a*n2 + j] = Σ_r H[a][r] · G2[i2][r][j] (forward, kExact rounding)
+// MODE 1: C[pos2[l]][q*n2 + j] = Σ_a H[a][q] · D2[a][j]   (dG2 contribution)
+template <typename T, int MODE, bool kExact>
+__global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restrict__ cores,
+                                                   const T* __restrict__ H,
+                                                   const int32_t* __restrict__ lk_pid,
+                                                   const uint32_t* __restrict__ tail_dig,
+                                                   const int32_t* __restrict__ lk_bag,
+                                                   const T* __restrict__ lk_alpha,
+                                                   const T* __restrict__ grad,
+                                                   const uint32_t* __restrict__ s_lk,
+                                                   const uint32_t* __restrict__ pos2, int64_t L,
+                                                   int C, T* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = P.N, R2 = P.r[2], n2 = P.n[2], S2 = P.slice[2], W1 = P.W1, P1 = P.prefix[1];
+  const int OW = MODE == 0 ? N : S2;             // output row width per lookup
+  const int XW = MODE == 0 ? S2 : N;             // per-lookup operand (G2 slice / D2 row)
+  // H row staged with an odd pitch per a-row (R2 + 1): MODE 0 lanes read
+  // hs[a][r] for 8 different a at once, which would share one bank otherwise
+  const int R2p = R2 + 1;
+  T* hs = reinterpret_cast<T*>(smem_raw);        // P1 x R2p (current pair's H row)
+  T* xs = hs + P1 * R2p;                         // C x XW
+  __shared__ int cur_pid;
+  __shared__ int pids[64];                       // pair of each chunk position (C <= 64)
+  const int64_t nchunks = (L + C - 1) / C;
+  const int per = blockDim.x / OW > 0 ? blockDim.x / OW : 1;  // lookups in flight
+  const int e = threadIdx.x % OW, slot = threadIdx.x / OW;
+  const bool on_e = threadIdx.x < per * OW;
+  // element -> operand offsets (hoisted)
+  const int ra = MODE == 0 ? (e / n2) * R2p : e / n2;  // MODE0: a*R2p  MODE1: q
+  const int rj = e % n2;
+  if (threadIdx.x == 0) cur_pid = -1;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t c0 = ch * C;
+    const int n = static_cast<int>(L - c0 < C ? L - c0 : C);
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += blockDim.x) pids[q] = lk_pid[s_lk[c0 + q]];
+    for (int x = threadIdx.x; x < n * XW; x += blockDim.x) {
+      const int q = x / XW, j = x - q * XW;
+      const int64_t l = s_lk[c0 + q];
+      if (MODE == 0)
+        xs[x] = cores[P.coff[2] + static_cast<int64_t>(tail_dig[l]) * S2 + j];
+      else
+        xs[x] = mul_rn<T>(lk_alpha[l], grad[static_cast<int64_t>(lk_bag[l]) * N + j]);
+    }
+    __syncthreads();
+    // one pair run of this chunk at a time: stage its H row once, then every
+    // thread walks its lookups of the run (slot, slot + per, ...)
+    for (int q0 = 0; q0 < n;) {
+      const int pid0 = pids[q0];
+      int q1 = q0 + 1;
+      while (q1 < n && pids[q1] == pid0) ++q1;
+      if (cur_pid != pid0) {
+        __syncthreads();  // the previous run's readers are done with hs
+        for (int x = threadIdx.x; x < W1; x += blockDim.x)
+          hs[(x / R2) * R2p + x % R2] = H[static_cast<int64_t>(pid0) * W1 + x];
+        __syncthreads();
+        if (threadIdx.x == 0) cur_pid = pid0;
+      }
+      if (on_e) {
+        for (int q = q0 + slot; q < q1; q += per) {
+          const int64_t l = s_lk[c0 + q];
+          const T* x = xs + q * XW;
+          T v = T(0);
+          if (MODE == 0) {
+            for (int r = 0; r < R2; ++r) v = madd<T, kExact>(hs[ra + r], x[r * n2 + rj], v);
+            out[l * N + e] = v;
+          } else {
+            for (int i = 0; i < P1; ++i) v = madd<T, false>(hs[i * R2p + ra], x[i * n2 + rj], v);
+            out[static_cast<int64_t>(pos2[l]) * S2 + e] = v;
+          }
+        }
+      }
+      __syncthreads();  // cur_pid update visible; xs rows of this run consumed
+      q0 = q1;
+    }
+  }
+}
+
+// Σ over the sorted positions of each segment (i2 bucket) of the dG2
+// contributions, in position order; OUT_MODE 0 dense slice, 1 fused SGD.
+template <typename T, int OUT_MODE>
+__global__ void k_segsum3(const T* __restrict__ contrib, const int32_t* __restrict__ seg, int nseg,
+                          int Wc, T* __restrict__ out, T lr) {
+  for (int g = blockIdx.x; g < nseg; g += gridDim.x) {
+    const int first = seg[g], last = seg[g + 1];
+    if (last <= first) continue;
+    for (int e = threadIdx.x; e < Wc; e += blockDim.x) {
+      T sum = contrib[static_cast<int64_t>(first) * Wc + e];
+      for (int p = first + 1; p < last; ++p) sum += contrib[static_cast<int64_t>(p) * Wc + e];
+      if (OUT_MODE == 0)
+        out[static_cast<int64_t>(g) * Wc + e] = sum;
+      else
+        out[static_cast<int64_t>(g) * Wc + e] =
+            add_rn<T>(out[static_cast<int64_t>(g) * Wc + e], -mul_rn<T>(lr, sum));
+    }
+  }
+}
+
+// Pooling of per-lookup rows y (L x N) per bag in lookup order (reference
+// embedding_ops.hpp:232-249): out[b] = Σ T(w)·y, Mean rescale.
+template <typename T, bool kExact>
+__global__ void k_pool_rows(const T* __restrict__ y, const int64_t* __restrict__ off, int64_t B,
+                            int64_t L, int N, const double* __restrict__ w, int mean,
+                            T* __restrict__ out) {
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < B * N;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = q / N;
+    const int j = static_cast<int>(q - b * N);
+    const int64_t s = off[b], e = off[b + 1];
+    const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
+    T acc = T(0);
+    for (int64_t l = lo; l < hi; ++l)
+      acc = madd<T, kExact>(static_cast<T>(w ? w[l] : 1.0), y[l * N + j], acc);
+    if (mean && e - s > 1) acc = mul_rn<T>(acc, static_cast<T>(1.0 / static_cast<double>(e - s)));
+    out[b * N + j] = acc;
+  }
+}
+
 // Fold the partials of each segment in order.  Segment g spans sorted
 // positions [first, last]; its runs are run(first)..run(last).
 //   OUT_MODE 0: out[g*Wc + e] = sum      (S per pair; dense gradient slices)
@@ -520,6 +819,8 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
   const int R1p = R1 + 1;
   T* g1t = reinterpret_cast<T*>(smem_raw);              // C1 x R1p
   T* acc = g1t + static_cast<int64_t>(C1) * R1p;        // R1 x C1
+  T* sps = acc + s1;                                    // P0 x C1: S row of the pair
+  T* g0s = sps + P.W1;                                  // P0 x R1: G0[i0]
   const T* G0 = cores + P.coff[0];
   const T* G1 = cores + P.coff[1];
   const int U = counts[0];
@@ -542,22 +843,28 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
       __syncthreads();
       for (int p = lo; p < hi; ++p) {
         const uint32_t i0 = pair_key_u[p] % m0;
-        const T* Sp = S + static_cast<int64_t>(p) * P.W1;
-        const T* g0 = G0 + static_cast<int64_t>(i0) * s0;
+        // the pair's S row and G0[i0] staged once (every thread reads them)
+        for (int e = threadIdx.x; e < P.W1; e += blockDim.x)
+          sps[e] = S[static_cast<int64_t>(p) * P.W1 + e];
+        for (int e = threadIdx.x; e < s0; e += blockDim.x)
+          g0s[e] = G0[static_cast<int64_t>(i0) * s0 + e];
+        __syncthreads();
         // D0[p][a][r] = sum_c S[a][c] * G1[r][c]
         for (int e = threadIdx.x; e < P0 * R1; e += blockDim.x) {
           const int a = e / R1, rr = e - a * R1;
+          const T* sa = sps + a * C1;
           T v = T(0);
-          for (int c = 0; c < C1; ++c) v = madd<T, false>(Sp[a * C1 + c], g1t[c * R1p + rr], v);
+          for (int c = 0; c < C1; ++c) v = madd<T, false>(sa[c], g1t[c * R1p + rr], v);
           D0[static_cast<int64_t>(p) * s0 + e] = v;
         }
         // acc[r][c] += sum_a G0[a][r] * S[a][c]
         for (int e = threadIdx.x; e < s1; e += blockDim.x) {
           const int rr = e / C1, c = e - rr * C1;
           T v = acc[e];
-          for (int a = 0; a < P0; ++a) v = madd<T, false>(g0[a * R1 + rr], Sp[a * C1 + c], v);
+          for (int a = 0; a < P0; ++a) v = madd<T, false>(g0s[a * R1 + rr], sps[a * C1 + c], v);
           acc[e] = v;
         }
+        __syncthreads();  // sps / g0s are restaged for the next pair
       }
       __syncthreads();
       for (int e = threadIdx.x; e < s1; e += blockDim.x)

@@ -249,6 +249,8 @@ struct ttgpu_ctx {
   const double* w_dev = nullptr;
   // backward state
   DevBuf s_dkey, s_dlk, dscan, dseg, pair_i1, scan1, seg1, S, D0, partS, partK, part1;
+  // d == 3 wide-row path: per-lookup y rows, dG2 contributions, i2 positions
+  DevBuf ybuf, tcontrib, pos2;
   size_t cub_bytes = 0;
 };
 
@@ -437,6 +439,26 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
                                     c->counts.as<int>(), kHeadChunk, c->H.as<T>());
   }
   t->mark("head_fwd");
+  // d == 3 with wide rows: y per lookup walked in pair order (H staged once per
+  // pair run), then pooling in lookup order
+  if (d == 3 && sizeof(T) * (P.W1 + P.prefix[1] + static_cast<size_t>(kTailChunk) * P.slice[2]) <=
+                    96 * 1024 &&
+      P.W1 >= 32) {
+    c->ybuf.ensure(sizeof(T) * L * P.N);
+    const size_t smem =
+        sizeof(T) * (P.W1 + P.prefix[1] + static_cast<size_t>(kTailChunk) * P.slice[2]);
+    auto kern = exact ? k_pairwalk3<T, 0, true> : k_pairwalk3<T, 0, false>;
+    set_smem(kern, smem);
+    kern<<<grid_for((L + kTailChunk - 1) / kTailChunk, 1, t->num_sms, 8), 256, smem, st>>>(
+        P, t->cores.as<T>(), c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
+        nullptr, nullptr, nullptr, c->s_lk.as<uint32_t>(), nullptr, L, kTailChunk, c->ybuf.as<T>());
+    auto pk = exact ? k_pool_rows<T, true> : k_pool_rows<T, false>;
+    pk<<<grid_for(B * P.N, kThreads, t->num_sms), kThreads, 0, st>>>(
+        c->ybuf.as<T>(), off, B, L, P.N, w, pooling, out);
+    t->mark("tail_pool");
+    CK(cudaGetLastError());
+    return;
+  }
   // tail chain + pooling per bag
   {
     const size_t per_warp = sizeof(T) * (2 * P.maxw + P.N);
@@ -534,7 +556,20 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
 
   t->mark("bwd_prep");
   // ---- S(pair) = sum of D1 over the pair's lookups
-  {
+  const bool staged3 = d == 3 && P.W1 <= kRun3MaxEPT * 256 && P.slice[2] <= kRun3MaxEPT * 256 &&
+                       sizeof(T) * kTailChunk * (P.N + P.slice[2]) <= 96 * 1024 &&
+                       sizeof(T) * 8 * (P.W1 + P.N) <= 96 * 1024;
+  if (staged3) {
+    const size_t smem = sizeof(T) * kTailChunk * (P.N + P.slice[2]) + 4 * kTailChunk;
+    set_smem(k_srun3<T>, smem);
+    k_srun3<T><<<grid_for(nchunksL, 1, t->num_sms, 8), 256, smem, st>>>(
+        P, cores, c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad,
+        c->s_key.as<uint32_t>(), c->s_lk.as<uint32_t>(), c->pair_scan.as<unsigned long long>(), L,
+        kTailChunk, c->partS.as<T>());
+    k_combine<T, 0><<<grid_for(ucap, 1, t->num_sms, 8), 128, 0, st>>>(
+        c->partS.as<T>(), c->pair_scan.as<unsigned long long>(), c->pair_start.as<int32_t>(),
+        c->counts.as<int>(), 0, P.W1, c->S.as<T>(), T(0));
+  } else {
     const int Wc = P.W1;
     const size_t per_warp = sizeof(T) * (Wc + 4 * static_cast<size_t>(P.maxw));
     const int warps = warps_fitting(per_warp, sizeof(T) * Wc, 100 * 1024, 8);
@@ -558,17 +593,40 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   for (int k = 2; k < d; ++k) {
     const int j = k - 2;
     const int Wc = P.slice[k];
-    const size_t per_warp = sizeof(T) * (Wc + 4 * static_cast<size_t>(P.maxw));
-    const int warps = warps_fitting(per_warp, sizeof(T) * Wc, 100 * 1024, 8);
-    const size_t smem = sizeof(T) * Wc + per_warp * warps;
-    auto kern = k_chunk_reduce<T, 1>;
-    set_smem(kern, smem);
-    kern<<<grid_for(nchunksL, 1, t->num_sms, 4), warps * 32, smem, st>>>(
-        P, cores, c->H.as<T>(), c->save ? c->saved.as<T>() : nullptr, c->lk_pid.as<int32_t>(),
-        c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad,
-        c->s_dkey.as<uint32_t>() + j * L, c->s_dlk.as<uint32_t>() + j * L,
-        c->dscan.as<unsigned long long>() + j * L, L, kTailChunk, k, Wc, c->partK.as<T>(),
-        c->exact);
+    if (staged3) {
+      // contributions computed in pair order (H staged per pair run), stored at
+      // each lookup's i2-sorted position, then summed per i2 segment in order
+      c->pos2.ensure(4 * L);
+      c->tcontrib.ensure(sizeof(T) * L * Wc);
+      k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>() + j * L, L, c->pos2.as<uint32_t>());
+      const size_t smem = sizeof(T) * (P.W1 + P.prefix[1] + static_cast<size_t>(kTailChunk) * P.N);
+      set_smem(k_pairwalk3<T, 1, false>, smem);
+      k_pairwalk3<T, 1, false><<<grid_for(nchunksL, 1, t->num_sms, 8), 256, smem, st>>>(
+          P, cores, c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
+          c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad, c->s_lk.as<uint32_t>(),
+          c->pos2.as<uint32_t>(), L, kTailChunk, c->tcontrib.as<T>());
+      T* dst = fuse_tail ? cores + P.coff[k] : grads + P.coff[k];
+      if (fuse_tail)
+        k_segsum3<T, 1><<<grid_for(P.m[k], 1, t->num_sms, 16), 256, 0, st>>>(
+            c->tcontrib.as<T>(), c->dseg.as<int32_t>() + segoff, P.m[k], Wc, dst, tlr);
+      else
+        k_segsum3<T, 0><<<grid_for(P.m[k], 1, t->num_sms, 16), 256, 0, st>>>(
+            c->tcontrib.as<T>(), c->dseg.as<int32_t>() + segoff, P.m[k], Wc, dst, T(0));
+      segoff += P.m[k] + 1;
+      continue;
+    } else {
+      const size_t per_warp = sizeof(T) * (Wc + 4 * static_cast<size_t>(P.maxw));
+      const int warps = warps_fitting(per_warp, sizeof(T) * Wc, 100 * 1024, 8);
+      const size_t smem = sizeof(T) * Wc + per_warp * warps;
+      auto kern = k_chunk_reduce<T, 1>;
+      set_smem(kern, smem);
+      kern<<<grid_for(nchunksL, 1, t->num_sms, 4), warps * 32, smem, st>>>(
+          P, cores, c->H.as<T>(), c->save ? c->saved.as<T>() : nullptr, c->lk_pid.as<int32_t>(),
+          c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad,
+          c->s_dkey.as<uint32_t>() + j * L, c->s_dlk.as<uint32_t>() + j * L,
+          c->dscan.as<unsigned long long>() + j * L, L, kTailChunk, k, Wc, c->partK.as<T>(),
+          c->exact);
+    }
     T* dst = fuse_tail ? cores + P.coff[k] : grads + P.coff[k];
     if (fuse_tail)
       k_combine<T, 1><<<grid_for(P.m[k], 1, t->num_sms, 8), 128, 0, st>>>(
@@ -584,7 +642,8 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   // ---- head: D0 per pair, dG1 partials per i1 run
   {
     const size_t smem = sizeof(T) * (static_cast<size_t>(P.slice[1]) +
-                                     static_cast<size_t>(P.C1) * (P.r[1] + 1));
+                                     static_cast<size_t>(P.C1) * (P.r[1] + 1) + P.W1 +
+                                     P.slice[0]);
     if (smem > 227 * 1024) fail(TTGPU_ERR_INVALID_ARGUMENT, "G1 slice too large for shared memory");
     auto kern = k_head_bwd<T>;
     set_smem(kern, smem);

@@ -6,7 +6,7 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "--kernel-name", f"regex:{kern}", "--launch-count", "1"],
+                      "--kernel-name", f"regex:{kern}", "--launch-skip", sys.argv[4] if len(sys.argv) > 4 else "0", "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr = next(r for r in rows if r and r[0] == "Line No")
