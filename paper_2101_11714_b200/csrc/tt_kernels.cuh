@@ -552,6 +552,18 @@ __global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ 
         const int e = threadIdx.x + k * blockDim.x;
         if (e < W) {
           T v = T(0);
+          if constexpr (std::is_same_v<T, float>) {
+            if (n2 == 4) {  // rows of 4: one 16-byte load per operand
+              const float4 dv = *reinterpret_cast<const float4*>(d + aoff[k]);
+              const float4 gv = *reinterpret_cast<const float4*>(gg + roff[k]);
+              v = __fmaf_rn(dv.x, gv.x, v);
+              v = __fmaf_rn(dv.y, gv.y, v);
+              v = __fmaf_rn(dv.z, gv.z, v);
+              v = __fmaf_rn(dv.w, gv.w, v);
+              acc[k] += v;
+              continue;
+            }
+          }
           if (n2 == 4) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) v = madd<T, false>(d[aoff[k] + j], gg[roff[k] + j], v);
