@@ -26,6 +26,42 @@ for rank, generic in ((32, False), (8, True)):
     r = tt.forward_bags(t, b)
     gr = tt.backward_bags(t, b, r.context, g)
     tt.sgd_step(t, gr, 0.01)
+    r = tt.forward_bags(t, b, save_intermediates=True)
+    t.backward_sgd(r.context, b, g, 0.01)
+# generic d = 3 wide-row kernels (cfg3's factorisation at a smaller rank), multi-hot bags
+p = tt.plan_shapes(400000, 64, 3, 16, [50, 80, 100], [4, 4, 4])
+t = tt.TtTable(p, "wide")
+rng = np.random.default_rng(1)
+t.set_cores([(rng.standard_normal(p.core_size(k)) * 0.3).astype(np.float32) for k in range(3)])
+idx = rng.integers(0, p.num_rows, 4096 * 4)
+b = tt.IndexBatch(idx, np.arange(0, 4096 * 4 + 1, 4, dtype=np.int64))
+g = rng.standard_normal((4096, 64)).astype(np.float32)
+r = tt.forward_bags(t, b, save_intermediates=True)
+gr = tt.backward_bags(t, b, r.context, g)
+t.backward_sgd(r.context, b, g, 0.01)
+# fused peer reduce + SGD: two ranks' tables on two streams of this GPU (the sanitizer
+# serialises kernels, so the peer waits run into their bounded timeout here: this
+# exercises the timeout path's memory safety, the reduction itself is checked in
+# tests/test_peer_reduce_gpu.py)
+import ctypes as C, torch
+from paper_2101_11714_b200._lib import lib
+p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+ts = [tt.TtTable(p, "r" + str(r), stream=ss[r].cuda_stream) for r in range(2)]
+flags = []
+for q in ts:
+    q.set_cores([np.zeros(p.core_size(k), np.float32) for k in range(3)])
+    f = C.c_void_p(); assert lib().ttgpu_peer_flags_ptr(q.handle, C.byref(f)) == 0; flags.append(f.value)
+G = (C.c_void_p * 2)(*[q.grad_buffer()[0] for q in ts]); F = (C.c_void_p * 2)(*flags)
+for r, q in enumerate(ts):
+    assert lib().ttgpu_peer_attach_ptrs(q.handle, 2, r, G, F) == 0
+    b = tt.generate_zipfian_batch(p.num_rows, 1.05, 3 + r, 2048, 1)
+    res = tt.forward_bags(q, b, save_intermediates=True)
+    tt.backward_bags(q, b, res.context, rng.standard_normal((2048, 16)).astype(np.float32))
+for q in ts:
+    assert lib().ttgpu_peer_reduce_sgd(q.handle, C.c_double(0.01)) == 0
+for q in ts:
+    q.check()
 print("ok")
 """ % ROOT
 
