@@ -254,7 +254,11 @@ struct ScanArgs {
   int K, TT;
 };
 
-constexpr int kGroup = 16;     // combine: candidate tiles per warp task
+// combine: candidate tiles per warp task (dG1 / dG2).  Run partials are sparse
+// among a bucket's tiles (one per CTA run), so wide groups keep the number of
+// group partials -- and the last arriver's sequential fold -- small.
+constexpr int kGroup = 64;
+constexpr int kGroup0 = 16;    // combine: candidate CTA blocks per warp task (dG0; dense for hot i0)
 constexpr int kScanKeys = 16;  // keys per f3_scan CTA
 constexpr int kScanThreads = 256;
 
@@ -1352,14 +1356,14 @@ __global__ void __launch_bounds__(kThreads) f3_combine(Geo g, float* __restrict_
     return;
   }
   task -= A.maxg2 * C2c;
-  const int ng0 = (A.nbwd + kGroup - 1) / kGroup;
+  const int ng0 = (A.nbwd + kGroup0 - 1) / kGroup0;
   const int gidx = task / C0c, ch = task - gidx * C0c;
   if (gidx >= g.m0 * ng0) return;
   const int i0 = gidx / ng0, gi = gidx - i0 * ng0;
   const int col4 = ch * 32 + lane;
   const bool colok = col4 < D::S0 / 4;
   auto row = [&](int c) { return A.D0acc + (static_cast<int64_t>(c) * g.m0 + i0) * D::S0; };
-  const int c0 = gi * kGroup, c1 = min(A.nbwd, c0 + kGroup);
+  const int c0 = gi * kGroup0, c1 = min(A.nbwd, c0 + kGroup0);
   {
     const int c = c0 + lane;
     const unsigned live =

@@ -204,7 +204,7 @@ struct F3Runner {
       A.maxg1 = g.m1 + (f.max_tiles1 + f3::kGroup - 1) / f3::kGroup;
       A.maxg2 = g.m2 + (f.max_tiles2 + f3::kGroup - 1) / f3::kGroup;
       A.nbwd = grid1;
-      const int ng0 = (grid1 + f3::kGroup - 1) / f3::kGroup;
+      const int ng0 = (grid1 + f3::kGroup0 - 1) / f3::kGroup0;
       const int tasks = A.maxg1 * C1c + A.maxg2 * C2c + g.m0 * ng0 * C0c;  // one warp each
       const int ncnt = g.m1 * C1c + g.m2 * C2c + g.m0 * C0c;
       if (f.counters.cap < 4 * static_cast<size_t>(ncnt)) {
