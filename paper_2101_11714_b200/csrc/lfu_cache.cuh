@@ -241,61 +241,104 @@ __global__ void k_slot_chunks(int64_t n, int N, const int* __restrict__ skey,
                               const int* __restrict__ seg_lo, const int* __restrict__ seg_hi,
                               T* __restrict__ part, T* __restrict__ sg, T* __restrict__ store,
                               int fused, T lr) {
+  static_assert(kSlotChunk == 32, "one chunk position per lane");
   const int lane = threadIdx.x & 31;
   const int64_t nchunks = (n + kSlotChunk - 1) / kSlotChunk;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t ch = warp; ch < nchunks; ch += nwarps) {
     const int64_t p0 = ch * kSlotChunk;
-    const int64_t p1 = p0 + kSlotChunk < n ? p0 + kSlotChunk : n;
-    for (int j = lane; j < N; j += 32) {
+    const int m = static_cast<int>(p0 + kSlotChunk < n ? kSlotChunk : n - p0);
+    // lane q holds position p0 + q's slot / weight / bag: one round trip for the chunk
+    int my_s = -1, my_bag = 0;
+    T my_a = T(0);
+    // neighbours of the chunk: a run is final here iff it neither continues
+    // from the previous chunk nor into the next one
+    const int key_before = p0 > 0 ? skey[p0 - 1] : -1;
+    const int key_after = p0 + m < n ? skey[p0 + m] : -1;
+    if (lane < m) {
+      my_s = skey[p0 + lane];
+      const int pos = spos[p0 + lane];
+      my_bag = c_bag[pos];
+      my_a = c_w ? static_cast<T>(c_w[pos]) : T(1);
+    }
+    for (int j0 = 0; j0 < N; j0 += 32) {
+      const int j = j0 + lane;
+      // every position's value for this lane's column, loads issued together
+      T v[kSlotChunk];
+#pragma unroll
+      for (int q = 0; q < kSlotChunk; ++q) {
+        const int bag = __shfl_sync(0xffffffffu, my_bag, q);
+        const T a = __shfl_sync(0xffffffffu, my_a, q);
+        v[q] = (q < m && j < N) ? mul_rn(a, ge[static_cast<int64_t>(bag) * N + j]) : T(0);
+      }
       T acc = T(0);
-      int64_t run = p0;
-      for (int64_t p = p0; p < p1; ++p) {
-        const int s = skey[p];
-        const int pos = spos[p];
-        const T a = c_w ? static_cast<T>(c_w[pos]) : T(1);
-        const T v = mul_rn(a, ge[static_cast<int64_t>(c_bag[pos]) * N + j]);
-        const bool first = p == p0 || skey[p - 1] != s;
-        if (first) run = p;
-        acc = first ? v : add_rn(acc, v);
-        if (p + 1 == p1 || skey[p + 1] != s) {
-          if (seg_lo[s] >= p0 && seg_hi[s] <= p1) {
-            if (fused) {
-              T* r = store + static_cast<int64_t>(s) * N + j;
-              *r = sub_rn(*r, mul_rn(lr, acc));
+      int run = 0;
+#pragma unroll
+      for (int q = 0; q < kSlotChunk; ++q) {
+        if (q >= m) break;
+        const int s = __shfl_sync(0xffffffffu, my_s, q);
+        const int prev = __shfl_sync(0xffffffffu, my_s, q > 0 ? q - 1 : 0);
+        const int next = __shfl_sync(0xffffffffu, my_s, q + 1 < m ? q + 1 : q);
+        const bool first = q == 0 || prev != s;
+        if (first) run = q;
+        acc = first ? v[q] : add_rn(acc, v[q]);
+        if (q + 1 == m || next != s) {  // run ends
+          const int64_t p = p0 + q;
+          const bool whole = (run > 0 || key_before != s) && (q + 1 < m || key_after != s);
+          if (j < N) {
+            if (whole) {
+              if (fused) {
+                T* r = store + static_cast<int64_t>(s) * N + j;
+                *r = sub_rn(*r, mul_rn(lr, acc));
+              } else {
+                sg[static_cast<int64_t>(s) * N + j] = acc;
+              }
             } else {
-              sg[static_cast<int64_t>(s) * N + j] = acc;
+              part[(p0 + run) * N + j] = acc;
             }
-          } else {
-            part[run * N + j] = acc;
           }
+          (void)p;
         }
       }
     }
   }
 }
 
+
 // Slots whose sorted range spans chunks: add the chunk partials in order.
 template <typename T>
 __global__ void k_slot_fold(int64_t cap, int N, const int* __restrict__ seg_lo,
                             const int* __restrict__ seg_hi, const T* __restrict__ part,
                             T* __restrict__ sg, T* __restrict__ store, int fused, T lr) {
-  const int64_t n = cap * N;
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
-       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  // one warp per (slot, column): a hot slot's chunk partials (Zipf: the top
+  // row's run spans hundreds of chunks) are summed lane-strided, then by a
+  // fixed xor butterfly -- a fixed order for a given chunk count, so the
+  // result is deterministic, and the chain is ~n/32 + 5 adds long
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+       q < cap * N; q += nw) {
     const int64_t s = q / N;
     const int j = static_cast<int>(q - s * N);
     const int lo = seg_lo[s], hi = seg_hi[s];
     if (lo < 0 || lo / kSlotChunk == (hi - 1) / kSlotChunk) continue;
-    T acc = part[static_cast<int64_t>(lo) * N + j];
-    for (int p = (lo / kSlotChunk + 1) * kSlotChunk; p < hi; p += kSlotChunk)
+    // partial rows: the run's first position, then every later chunk start
+    const int c_lo = lo / kSlotChunk, c_hi = (hi - 1) / kSlotChunk;  // chunks c_lo..c_hi
+    T acc = T(0);
+    for (int c = c_lo + lane; c <= c_hi; c += 32) {
+      const int p = c == c_lo ? lo : c * kSlotChunk;
       acc = add_rn(acc, part[static_cast<int64_t>(p) * N + j]);
-    if (fused) {
-      T* r = store + s * N + j;
-      *r = sub_rn(*r, mul_rn(lr, acc));
-    } else {
-      sg[q] = acc;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) {
+      if (fused) {
+        T* r = store + s * N + j;
+        *r = sub_rn(*r, mul_rn(lr, acc));
+      } else {
+        sg[q] = acc;
+      }
     }
   }
 }

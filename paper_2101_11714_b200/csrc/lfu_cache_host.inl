@@ -329,7 +329,7 @@ void cache_backward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const T* gra
         n, N, c->skey.as<int>(), c->spos.as<int>(), c->has_w ? c->c_w.as<double>() : nullptr,
         c->c_bag.as<int32_t>(), ge, c->seg_lo.as<int>(), c->seg_hi.as<int>(), c->part.as<T>(),
         c->sg.as<T>(), c->now().store.as<T>(), fused ? 1 : 0, static_cast<T>(lr));
-    lfu::k_slot_fold<T><<<grid_for(c->capacity * N, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
+    lfu::k_slot_fold<T><<<grid_for(c->capacity * N * 32, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
         c->capacity, N, c->seg_lo.as<int>(), c->seg_hi.as<int>(), c->part.as<T>(), c->sg.as<T>(),
         c->now().store.as<T>(), fused ? 1 : 0, static_cast<T>(lr));
     CK(cudaGetLastError());
