@@ -818,6 +818,8 @@ __global__ void k_combine(const T* __restrict__ partials, const unsigned long lo
 // Over pairs in pid order (i1-major), chunks of CH pairs, runs by i1:
 //   D0[pid] = S[pid] (P0 x C1) · G1[i1]ᵀ (C1 x R1)
 //   partial(run) = Σ_pairs G0[i0]ᵀ (R1 x P0) · S[pid] (P0 x C1)
+constexpr int kHeadMaxR1 = 64, kHeadMaxP0 = 4;
+
 template <typename T>
 __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __restrict__ S,
                            const uint32_t* __restrict__ pair_key_u, const int* __restrict__ counts,
@@ -838,6 +840,12 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
   const int U = counts[0];
   const int nchunks = (U + CH - 1) / CH;
   const uint32_t m0 = static_cast<uint32_t>(P.m[0]);
+  // dG1 run accumulator in registers when one thread can own a whole column
+  // (C1 <= blockDim, R1 <= kHeadMaxR1, P0 <= kHeadMaxP0: cfg3's 4 x 64 x 256)
+  const bool reg_acc = C1 <= static_cast<int>(blockDim.x) && R1 <= kHeadMaxR1 && P0 <= kHeadMaxP0;
+  T racc[kHeadMaxR1];
+#pragma unroll
+  for (int rr = 0; rr < kHeadMaxR1; ++rr) racc[rr] = T(0);
   for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int p0 = ch * CH, p1 = min(U, p0 + CH);
     int run = static_cast<int>(scan1[p0] >> 32) - 1;
@@ -870,17 +878,47 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
           D0[static_cast<int64_t>(p) * s0 + e] = v;
         }
         // acc[r][c] += sum_a G0[a][r] * S[a][c]
-        for (int e = threadIdx.x; e < s1; e += blockDim.x) {
-          const int rr = e / C1, c = e - rr * C1;
-          T v = acc[e];
-          for (int a = 0; a < P0; ++a) v = madd<T, false>(g0s[a * R1 + rr], sps[a * C1 + c], v);
-          acc[e] = v;
+        if (reg_acc) {  // thread = column c, the whole r column in registers
+          const int c = threadIdx.x;
+          if (c < C1) {
+            T sv[kHeadMaxP0];
+#pragma unroll
+            for (int a = 0; a < kHeadMaxP0; ++a) sv[a] = a < P0 ? sps[a * C1 + c] : T(0);
+#pragma unroll
+            for (int rr = 0; rr < kHeadMaxR1; ++rr) {
+              if (rr < R1) {
+                T v = racc[rr];
+#pragma unroll
+                for (int a = 0; a < kHeadMaxP0; ++a)
+                  if (a < P0) v = madd<T, false>(g0s[a * R1 + rr], sv[a], v);
+                racc[rr] = v;
+              }
+            }
+          }
+        } else {
+          for (int e = threadIdx.x; e < s1; e += blockDim.x) {
+            const int rr = e / C1, c = e - rr * C1;
+            T v = acc[e];
+            for (int a = 0; a < P0; ++a) v = madd<T, false>(g0s[a * R1 + rr], sps[a * C1 + c], v);
+            acc[e] = v;
+          }
         }
         __syncthreads();  // sps / g0s are restaged for the next pair
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < s1; e += blockDim.x)
-        partials[static_cast<int64_t>(run) * s1 + e] = acc[e];
+      if (reg_acc) {
+        const int c = threadIdx.x;
+        if (c < C1) {
+#pragma unroll
+          for (int rr = 0; rr < kHeadMaxR1; ++rr) {
+            if (rr < R1) partials[static_cast<int64_t>(run) * s1 + rr * C1 + c] = racc[rr];
+            racc[rr] = T(0);
+          }
+        }
+      } else {
+        for (int e = threadIdx.x; e < s1; e += blockDim.x)
+          partials[static_cast<int64_t>(run) * s1 + e] = acc[e];
+      }
       ++run;
       lo = hi;
     }
