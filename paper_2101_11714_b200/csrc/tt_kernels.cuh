@@ -505,23 +505,47 @@ __global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ 
   T* d2s = reinterpret_cast<T*>(smem_raw);               // C x N
   T* g2s = d2s + static_cast<int64_t>(C) * N;            // C x S2
   uint32_t* keys = reinterpret_cast<uint32_t*>(g2s + static_cast<int64_t>(C) * S2);  // C
+  __shared__ int qbag[64], qi2[64];
+  __shared__ T qal[64];
   const T* G2 = cores + P.coff[2];
   const int64_t nchunks = (L + C - 1) / C;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t c0 = ch * C;
     const int n = static_cast<int>(L - c0 < C ? L - c0 : C);
     __syncthreads();
+    // per-position indices once (one round trip), then the row copies
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      const int64_t l = s_lk[c0 + q];
+      keys[q] = s_key[c0 + q];
+      qbag[q] = lk_bag[l];
+      qi2[q] = static_cast<int>(tail_dig[l]);
+      qal[q] = lk_alpha[l];
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < n * N; e += blockDim.x) {
       const int q = e / N, j = e - q * N;
-      const int64_t l = s_lk[c0 + q];
-      d2s[e] = mul_rn<T>(lk_alpha[l], grad[static_cast<int64_t>(lk_bag[l]) * N + j]);
+      d2s[e] = mul_rn<T>(qal[q], grad[static_cast<int64_t>(qbag[q]) * N + j]);
     }
-    for (int e = threadIdx.x; e < n * S2; e += blockDim.x) {
-      const int q = e / S2, j = e - q * S2;
-      const int64_t l = s_lk[c0 + q];
-      g2s[e] = G2[static_cast<int64_t>(tail_dig[l]) * S2 + j];
+    if constexpr (std::is_same_v<T, float>) {
+      if ((S2 & 3) == 0) {
+        const int S4 = S2 >> 2;
+        for (int e = threadIdx.x; e < n * S4; e += blockDim.x) {
+          const int q = e / S4, j = e - q * S4;
+          reinterpret_cast<float4*>(g2s)[e] =
+              __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(qi2[q]) * S2) + j);
+        }
+      } else {
+        for (int e = threadIdx.x; e < n * S2; e += blockDim.x) {
+          const int q = e / S2, j = e - q * S2;
+          g2s[e] = G2[static_cast<int64_t>(qi2[q]) * S2 + j];
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < n * S2; e += blockDim.x) {
+        const int q = e / S2, j = e - q * S2;
+        g2s[e] = G2[static_cast<int64_t>(qi2[q]) * S2 + j];
+      }
     }
-    for (int q = threadIdx.x; q < n; q += blockDim.x) keys[q] = s_key[c0 + q];
     __syncthreads();
     const int run0 = static_cast<int>(scan[c0] >> 32) - 1;
     T acc[kRun3MaxEPT];
@@ -693,6 +717,8 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
   T* xs = hs + P1 * R2p;                         // C x XW
   __shared__ int cur_pid;
   __shared__ int pids[64];                       // pair of each chunk position (C <= 64)
+  __shared__ int qlk[64], qrow[64];              // lookup, G2 slice (MODE 0) / bag (MODE 1)
+  __shared__ T qal[64];
   const int64_t nchunks = (L + C - 1) / C;
   const int per = blockDim.x / OW > 0 ? blockDim.x / OW : 1;  // lookups in flight
   const int e = threadIdx.x % OW, slot = threadIdx.x / OW;
@@ -705,14 +731,34 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
     const int64_t c0 = ch * C;
     const int n = static_cast<int>(L - c0 < C ? L - c0 : C);
     __syncthreads();
-    for (int q = threadIdx.x; q < n; q += blockDim.x) pids[q] = lk_pid[s_lk[c0 + q]];
-    for (int x = threadIdx.x; x < n * XW; x += blockDim.x) {
-      const int q = x / XW, j = x - q * XW;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {  // per-position indices, one round trip
       const int64_t l = s_lk[c0 + q];
-      if (MODE == 0)
-        xs[x] = cores[P.coff[2] + static_cast<int64_t>(tail_dig[l]) * S2 + j];
-      else
-        xs[x] = mul_rn<T>(lk_alpha[l], grad[static_cast<int64_t>(lk_bag[l]) * N + j]);
+      qlk[q] = static_cast<int>(l);
+      pids[q] = lk_pid[l];
+      qrow[q] = MODE == 0 ? static_cast<int>(tail_dig[l]) : lk_bag[l];
+      if (MODE == 1) qal[q] = lk_alpha[l];
+    }
+    __syncthreads();
+    const T* src = MODE == 0 ? cores + P.coff[2] : grad;
+    bool vec = false;
+    if constexpr (std::is_same_v<T, float>) vec = (XW & 3) == 0;
+    if (vec) {
+      const int X4 = XW >> 2;
+      for (int x = threadIdx.x; x < n * X4; x += blockDim.x) {
+        const int q = x / X4, j = x - q * X4;
+        float4 v = __ldg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(qrow[q]) * XW) + j);
+        if (MODE == 1) {
+          const float a = static_cast<float>(qal[q]);
+          v = make_float4(__fmul_rn(a, v.x), __fmul_rn(a, v.y), __fmul_rn(a, v.z), __fmul_rn(a, v.w));
+        }
+        reinterpret_cast<float4*>(xs)[x] = v;
+      }
+    } else {
+      for (int x = threadIdx.x; x < n * XW; x += blockDim.x) {
+        const int q = x / XW, j = x - q * XW;
+        const T v = src[static_cast<int64_t>(qrow[q]) * XW + j];
+        xs[x] = MODE == 0 ? v : mul_rn<T>(qal[q], v);
+      }
     }
     __syncthreads();
     // one pair run of this chunk at a time: stage its H row once, then every
@@ -730,7 +776,7 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
       }
       if (on_e) {
         for (int q = q0 + slot; q < q1; q += per) {
-          const int64_t l = s_lk[c0 + q];
+          const int64_t l = qlk[q];
           const T* x = xs + q * XW;
           T v = T(0);
           if (MODE == 0) {
