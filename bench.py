@@ -409,17 +409,31 @@ def main():
     # back to NCCL if P2P is unavailable, a peer wait times out, or replicas diverge
     reducer, reduce_path = None, ("nccl-allreduce+sgd" if world > 1 else None)
     if world > 1 and not args.nccl and cache is None:
-        try:
-            from paper_2101_11714_b200.sharding import PeerReducer
+        # every rank must take the same path: agree on P2P reachability first,
+        # then on the attach result (PeerReducer's handle exchange is collective)
+        def agree(flag):
+            t = torch.tensor([1 if flag else 0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return bool(t.item())
 
+        ok = True
+        try:
             ok = all(torch.cuda.can_device_access_peer(local, j)
                      for j in range(torch.cuda.device_count()) if j != local)
-            if ok:
+        except Exception:  # noqa: BLE001
+            ok = False
+        if agree(ok):
+            from paper_2101_11714_b200.sharding import PeerReducer
+
+            try:
                 reducer = PeerReducer(table)
+            except Exception as e:  # noqa: BLE001
+                print(f"[bench] peer attach failed ({e}); using NCCL", file=sys.stderr)
+                reducer = None
+            if agree(reducer is not None):
                 reduce_path = "fused-peer-reduce+sgd"
-        except Exception as e:  # noqa: BLE001
-            print(f"[bench] peer reduce unavailable ({e}); using NCCL", file=sys.stderr)
-            reducer = None
+            else:
+                reducer = None
 
     # warm-up (allocates every workspace), validation, then graph capture
     for _ in range(args.warmup):

@@ -181,15 +181,20 @@ class PeerReducer:
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         gh = (C.c_char * 64)()
         fh = (C.c_char * 64)()
-        _raise(lib().ttgpu_peer_export(table.handle, gh, fh))
-        mine = torch.tensor(list(bytes(gh)) + list(bytes(fh)), dtype=torch.uint8)
+        # a failed export still joins the (collective) exchange, flagged, so no
+        # rank is left waiting; every rank then raises together
+        exported = lib().ttgpu_peer_export(table.handle, gh, fh) == 0
+        mine = torch.tensor(list(bytes(gh)) + list(bytes(fh)) + [1 if exported else 0],
+                            dtype=torch.uint8)
         if world > 1:
             bufs = [torch.zeros_like(mine) for _ in range(world)]
             dist.all_gather_object(bufs, mine, group=group)
         else:
             bufs = [mine]
+        if not all(int(b[128]) for b in bufs):
+            raise RuntimeError("peer reduce: a rank could not export its buffers")
         allg = b"".join(bytes(b[:64].tolist()) for b in bufs)
-        allf = b"".join(bytes(b[64:].tolist()) for b in bufs)
+        allf = b"".join(bytes(b[64:128].tolist()) for b in bufs)
         self._g = C.create_string_buffer(allg, len(allg))
         self._f = C.create_string_buffer(allf, len(allf))
         _raise(lib().ttgpu_peer_attach(table.handle, world, rank, self._g, self._f))
