@@ -533,10 +533,10 @@ def main():
     dom = max(phase_ms, key=phase_ms.get)
 
     # e2e through the host C ABI: pinned host buffers, copies inside the region
-    h_idx = torch.from_numpy(idx).pin_memory().numpy()
-    h_off = torch.from_numpy(off).pin_memory().numpy()
-    h_grad = torch.from_numpy(grad).pin_memory().numpy()
-    h_out = torch.empty((B, N), dtype=torch.float32).pin_memory().numpy()
+    # page-locked host buffers; the torch tensors that own them stay referenced
+    pinned = [torch.from_numpy(a).pin_memory() for a in (idx, off, grad)]
+    pinned.append(torch.empty((B, N), dtype=torch.float32).pin_memory())
+    h_idx, h_off, h_grad, h_out = (t.numpy() for t in pinned)
     batch = tt.IndexBatch(h_idx, h_off)
     import ctypes as C
 
