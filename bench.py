@@ -333,13 +333,23 @@ def main():
 
     import torch
 
+    # test-only overrides: run an N-rank job on ONE GPU (every rank on device 0,
+    # gloo for the host-side collectives) to exercise the multi-GPU path where
+    # only one GPU exists; never set by the driver
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2101_11714_b200 as tt
 
     stream = torch.cuda.Stream(device=dev)
@@ -418,8 +428,8 @@ def main():
 
         ok = True
         try:
-            ok = all(torch.cuda.can_device_access_peer(local, j)
-                     for j in range(torch.cuda.device_count()) if j != local)
+            ok = share or all(torch.cuda.can_device_access_peer(local, j)
+                              for j in range(torch.cuda.device_count()) if j != local)
         except Exception:  # noqa: BLE001
             ok = False
         if agree(ok):
