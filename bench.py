@@ -216,12 +216,17 @@ def run_collection(args, cfg, rank, world, local):
     The same step with every table on one stream is timed beside it."""
     import torch
 
+    if os.environ.get("BENCH_SHARE_GPU") == "1":  # test-only, see main()
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("BENCH_BACKEND", "nccl") == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(os.environ["BENCH_BACKEND"])
     import paper_2101_11714_b200 as tt
     from paper_2101_11714_b200.collection import TtEmbeddingCollection, kaggle_plans
     from paper_2101_11714_b200.streams import DeviceZipfSampler, bag_offsets_device
@@ -273,16 +278,26 @@ def run_collection(args, cfg, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    col.capture(inputs, LR)
-    ms_par = timed(col.replay)
+    if col.capturable:
+        col.capture(inputs, LR)
+        run_par = col.replay
+    else:  # host-side collective in the step: eager launches
+        def run_par():
+            col.step(inputs, LR)
+    ms_par = timed(run_par)
     clk = clocks.stop()
     # the same step with every table on the main stream (no overlap between tables)
     for t in col.tables:
         t.set_stream(col.main.cuda_stream)
     saved = col.streams
     col.streams = [col.main] * len(saved)
-    col.capture(inputs, LR)
-    ms_seq = timed(col.replay)
+    if col.capturable:
+        col.capture(inputs, LR)
+        run_seq = col.replay
+    else:
+        def run_seq():
+            col.step(inputs, LR)
+    ms_seq = timed(run_seq)
     col.synchronize()
     total = world * len(plans) * L
     if rank == 0:
@@ -296,6 +311,8 @@ def run_collection(args, cfg, rank, world, local):
                            "lookups_per_step": total, "parallelism":
                                f"dp{world}" if world > 1 else "single-gpu",
                            "l2": "flushed (256 MiB write) before every timed step"},
+                "gradient_reduce": ("fused-peer-reduce+sgd" if col.reducers is not None else
+                                    "nccl-coalesced-allreduce+sgd") if world > 1 else None,
                 "sequential_ms_per_step": ms_seq,
                 "multi_stream_speedup": ms_seq / ms_par,
                 "clocks": clk}

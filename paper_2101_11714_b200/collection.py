@@ -59,20 +59,41 @@ class TtEmbeddingCollection:
         self.ctxs = [ForwardContext(t) for t in self.tables]
         self.graph = None
         self._grad_views = None
+        self.reducers = None
         if self.world > 1:
-            from .sharding import _device_view
+            from .sharding import PeerReducer, _device_view
 
             views = []
             for t in self.tables:
                 ptr, n = t.grad_buffer()
                 views.append(_device_view(ptr, n, "<f4", device))
             self._grad_views = views
+            # fused reduce+SGD over peer memory per table when every rank can
+            # attach (one kernel per table, graph-capturable); else NCCL
+            ok = 1
+            reducers = []
+            try:
+                for t in self.tables:
+                    reducers.append(PeerReducer(t, group))
+            except Exception:  # noqa: BLE001
+                ok = 0
+            flag = torch.tensor([ok], device=self.dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            self.reducers = reducers if int(flag.item()) else None
+
+    @property
+    def capturable(self) -> bool:
+        """The step can be captured as one CUDA graph (no host-side collective)."""
+        return self.world == 1 or self.reducers is not None
 
     def _table_step(self, i, idx_ptr, L, off_ptr, B, out_ptr, grad_ptr, lr):
         t, c = self.tables[i], self.ctxs[i]
         t.forward_device(c, idx_ptr, L, off_ptr, B, out_ptr, save=True)
         if self.world == 1:
             t.backward_sgd_device(c, grad_ptr, lr)
+        elif self.reducers is not None:
+            t.backward_device(c, grad_ptr)
+            self.reducers[i].reduce_sgd(lr)
         else:
             t.backward_device(c, grad_ptr)
 
@@ -90,7 +111,7 @@ class TtEmbeddingCollection:
             e = torch.cuda.Event()
             e.record(s)
             self.main.wait_event(e)
-        if self.world > 1:
+        if self.world > 1 and self.reducers is None:
             from .sharding import allreduce_sum_coalesced_
 
             with torch.cuda.stream(self.main):

@@ -37,3 +37,18 @@ def test_two_ranks_on_one_gpu(extra, want):
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
     assert d["config"]["gradient_reduce"] == want
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+def test_two_ranks_multitable_step():
+    """cfg5's 7-table step with the coalesced gradient reduction (allreduce over gloo here)."""
+    env = dict(os.environ, BENCH_SHARE_GPU="1", BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "cfg5", "--steps", "2",
+           "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["tables"] == 7 and d["value"] > 0
