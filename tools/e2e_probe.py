@@ -6,7 +6,8 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, ".")
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2101_11714_b200 as tt
 from paper_2101_11714_b200._lib import lib
 import bench

@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage: scratch/gpu_iter.sh TAG [pytest-args]   (runs on the GPU box)
+# usage: tools/gpu/gpu_iter.sh TAG [pytest-args]   (runs on the GPU box)
 TAG=$1; shift
 mkdir -p gpurun_out
 if [ "$1" != "nobench" ]; then
