@@ -35,6 +35,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "ttgpu.h"
@@ -51,61 +52,64 @@ inline void check(int st) {
   throw std::runtime_error(m);
 }
 
-/// One TT table resident on one GPU (cores + gradient buffer + workspace).
-class TtEmbeddingBagCuda {
+/// One TT table resident on one GPU (cores + gradient buffer + workspace);
+/// T = float or double (the reference instantiates both, common.hpp:13-15).
+template <typename T = float>
+class TtEmbeddingBagCudaT {
  public:
-  TtEmbeddingBagCuda(const ShapePlan& plan, std::string name, int device = 0,
-                     void* stream = nullptr)
+  TtEmbeddingBagCudaT(const ShapePlan& plan, std::string name, int device = 0,
+                      void* stream = nullptr)
       : plan_(plan), name_(std::move(name)) {
     check(ttgpu_create(plan.num_rows, plan.emb_dim, plan.tt_dim, plan.row_factors.data(),
-                       plan.col_factors.data(), plan.ranks.data(), TTGPU_F32, name_.c_str(),
+                       plan.col_factors.data(), plan.ranks.data(),
+                       std::is_same_v<T, double> ? TTGPU_F64 : TTGPU_F32, name_.c_str(),
                        device, stream, &h_));
     check(ttgpu_ctx_create(h_, &ctx_));
   }
-  ~TtEmbeddingBagCuda() {
+  ~TtEmbeddingBagCudaT() {
     if (ctx_) ttgpu_ctx_destroy(ctx_);
     if (h_) ttgpu_destroy(h_);
   }
-  TtEmbeddingBagCuda(const TtEmbeddingBagCuda&) = delete;
-  TtEmbeddingBagCuda& operator=(const TtEmbeddingBagCuda&) = delete;
+  TtEmbeddingBagCudaT(const TtEmbeddingBagCudaT&) = delete;
+  TtEmbeddingBagCudaT& operator=(const TtEmbeddingBagCudaT&) = delete;
 
   const ShapePlan& plan() const { return plan_; }
   const std::string& name() const { return name_; }
   ttgpu_table* handle() const { return h_; }
   ttgpu_ctx* context() const { return ctx_; }
 
-  void upload(const TtTable<float>& t) {
+  void upload(const TtTable<T>& t) {
     for (int k = 0; k < t.dim(); ++k) check(ttgpu_set_core(h_, k, t.core(k).data()));
   }
-  void download(TtTable<float>& t) const {
+  void download(TtTable<T>& t) const {
     for (int k = 0; k < t.dim(); ++k) check(ttgpu_get_core(h_, k, t.core(k).data()));
   }
 
   /// forward_bags into a host buffer (num_bags x emb_dim); the device context
   /// keeps what backward needs.
-  void forward(const IndexBatch& b, index_t micro_batch, bool save, float* out) {
+  void forward(const IndexBatch& b, index_t micro_batch, bool save, T* out) {
     check(ttgpu_forward(h_, b.indices.data(), b.num_lookups(), b.offsets.data(), b.num_bags(),
                         b.has_weights() ? b.weights.data() : nullptr,
                         b.pooling == Pooling::Mean ? TTGPU_MEAN : TTGPU_SUM, micro_batch,
                         save ? 1 : 0, out, ctx_));
   }
   /// backward_bags: dense gradients into per-core host buffers (may be null)
-  void backward(const IndexBatch& b, std::span<const float> grad, float* const* grads_out) {
+  void backward(const IndexBatch& b, std::span<const T> grad, T* const* grads_out) {
     check(ttgpu_backward(h_, ctx_, b.num_lookups(), b.num_bags(), grad.data(),
                          static_cast<int64_t>(grad.size()),
                          reinterpret_cast<void* const*>(grads_out)));
   }
   /// fused backward_bags + sgd_step on the device cores
-  void backward_sgd(const IndexBatch& b, std::span<const float> grad, double lr) {
+  void backward_sgd(const IndexBatch& b, std::span<const T> grad, double lr) {
     check(ttgpu_backward_sgd(h_, ctx_, b.num_lookups(), b.num_bags(), grad.data(),
                              static_cast<int64_t>(grad.size()), lr));
   }
-  void sgd(const CoreGradients<float>& g, double lr) {
+  void sgd(const CoreGradients<T>& g, double lr) {
     std::vector<const void*> p(g.cores.size());
     for (size_t k = 0; k < p.size(); ++k) p[k] = g.cores[k].data();
     check(ttgpu_sgd_step(h_, p.data(), lr));
   }
-  void lookup_row(index_t row, float* out) { check(ttgpu_lookup_row(h_, row, out)); }
+  void lookup_row(index_t row, T* out) { check(ttgpu_lookup_row(h_, row, out)); }
 
  private:
   ShapePlan plan_;
@@ -113,6 +117,7 @@ class TtEmbeddingBagCuda {
   ttgpu_table* h_ = nullptr;
   ttgpu_ctx* ctx_ = nullptr;
 };
+using TtEmbeddingBagCuda = TtEmbeddingBagCudaT<float>;
 
 namespace detail {
 
@@ -120,7 +125,8 @@ namespace detail {
 /// core buffer addresses and 64 sampled values per core.  A table destroyed
 /// and re-created at the same address (a loop-local TtTable) gets a new
 /// fingerprint unless it holds the same data.
-inline std::uint64_t fingerprint(const TtTable<float>& t) {
+template <typename T>
+inline std::uint64_t fingerprint(const TtTable<T>& t) {
   std::uint64_t h = 1469598103934665603ull;
   auto mix = [&](std::uint64_t v) { h = (h ^ v) * 1099511628211ull; };
   mix(t.mutation_counter());
@@ -136,17 +142,18 @@ inline std::uint64_t fingerprint(const TtTable<float>& t) {
     mix(reinterpret_cast<std::uintptr_t>(c.data()));
     const size_t n = c.size(), step = n > 64 ? n / 64 : 1;
     for (size_t i = 0; i < n; i += step) {
-      std::uint32_t bits;
-      std::memcpy(&bits, &c[i], 4);
+      std::uint64_t bits = 0;
+      std::memcpy(&bits, &c[i], sizeof(T));
       mix(bits);
     }
   }
   return h;
 }
 
-/// Device shadow of a host TtTable<float>, refreshed when its cores change.
+/// Device shadow of a host TtTable<T>, refreshed when its cores change.
+template <typename T>
 struct Shadow {
-  std::unique_ptr<TtEmbeddingBagCuda> dev;
+  std::unique_ptr<TtEmbeddingBagCudaT<T>> dev;
   std::uint64_t uploaded_at = ~std::uint64_t{0};  // fingerprint of the uploaded cores
   // identity of the forward the device context holds
   const void* idx_data = nullptr;
@@ -155,13 +162,15 @@ struct Shadow {
   bool fwd_saved = false;
 };
 
-inline std::map<const TtTable<float>*, Shadow>& registry() {
-  static std::map<const TtTable<float>*, Shadow> r;
+template <typename T>
+inline std::map<const TtTable<T>*, Shadow<T>>& registry() {
+  static std::map<const TtTable<T>*, Shadow<T>> r;
   return r;
 }
 
-inline Shadow& shadow_of(const TtTable<float>& t, int device = 0) {
-  Shadow& s = registry()[&t];
+template <typename T>
+inline Shadow<T>& shadow_of(const TtTable<T>& t, int device = 0) {
+  Shadow<T>& s = registry<T>()[&t];
   const std::uint64_t fp = fingerprint(t);
   if (s.dev && s.uploaded_at != fp) {
     const ShapePlan& a = s.dev->plan();
@@ -170,7 +179,7 @@ inline Shadow& shadow_of(const TtTable<float>& t, int device = 0) {
         a.col_factors != b.col_factors || a.ranks != b.ranks || s.dev->name() != t.name())
       s.dev.reset();  // another table now lives at this address
   }
-  if (!s.dev) s.dev = std::make_unique<TtEmbeddingBagCuda>(t.plan(), t.name(), device);
+  if (!s.dev) s.dev = std::make_unique<TtEmbeddingBagCudaT<T>>(t.plan(), t.name(), device);
   if (s.uploaded_at != fp) {
     s.dev->upload(t);
     s.uploaded_at = fp;
@@ -182,19 +191,26 @@ inline Shadow& shadow_of(const TtTable<float>& t, int device = 0) {
 }  // namespace detail
 
 /// Drop the device shadow of a table (e.g. before the table is destroyed).
-inline void release(const TtTable<float>& t) { detail::registry().erase(&t); }
+template <typename T>
+inline void release(const TtTable<T>& t) { detail::registry<T>().erase(&t); }
 
 /// embedding_ops.hpp:159-253 on the GPU; bit-identical output.
-inline ForwardResult<float> forward_bags(const TtTable<float>& table, const IndexBatch& batch,
-                                         index_t micro_batch = kDefaultMicroBatch,
-                                         bool save_intermediates = false) {
+template <typename T>
+inline ForwardResult<T> forward_bags(const TtTable<T>& table, const IndexBatch& batch,
+                                     index_t micro_batch = kDefaultMicroBatch,
+                                     bool save_intermediates = false) {
   batch.validate(table.rows(), table.name());
-  detail::Shadow& s = detail::shadow_of(table);
-  ForwardResult<float> r;
-  r.output.assign(static_cast<size_t>(batch.num_bags()) * table.cols(), 0.f);
+  detail::Shadow<T>& s = detail::shadow_of(table);
+  ForwardResult<T> r;
+  r.output.assign(static_cast<size_t>(batch.num_bags()) * table.cols(), T(0));
   const std::uint64_t before = ttgpu_stats_rows();
   s.dev->forward(batch, micro_batch, save_intermediates, r.output.data());
   EmbeddingStats::add_rows(ttgpu_stats_rows() - before);
+  // device workspace high-water mark into the reference's workspace counter
+  // (the GPU path does not chunk by micro_batch, so it does not scale with it)
+  const auto ws = static_cast<std::size_t>(ttgpu_stats_peak_workspace());
+  EmbeddingStats::workspace_add(ws);
+  EmbeddingStats::workspace_sub(ws);
   s.idx_data = batch.indices.data();
   s.L = batch.num_lookups();
   s.B = batch.num_bags();
@@ -211,9 +227,10 @@ inline ForwardResult<float> forward_bags(const TtTable<float>& table, const Inde
 
 /// embedding_ops.hpp:260-358 on the GPU: the reference's checks (:264-274),
 /// then dense CoreGradients in the core layout.
-inline CoreGradients<float> backward_bags(const TtTable<float>& table, const IndexBatch& batch,
-                                          const ForwardContext<float>& ctx,
-                                          std::span<const float> grad_output) {
+template <typename T>
+inline CoreGradients<T> backward_bags(const TtTable<T>& table, const IndexBatch& batch,
+                                      const ForwardContext<T>& ctx,
+                                      std::span<const T> grad_output) {
   const ShapePlan& plan = table.plan();
   batch.validate(plan.num_rows, table.name());
   require_arg(ctx.table == &table, "forward context belongs to a different table");
@@ -225,20 +242,20 @@ inline CoreGradients<float> backward_bags(const TtTable<float>& table, const Ind
   require_arg(static_cast<index_t>(grad_output.size()) == batch.num_bags() * plan.emb_dim,
               "grad_output has ", grad_output.size(), " elements, expected ",
               batch.num_bags() * plan.emb_dim);
-  detail::Shadow& s = detail::shadow_of(table);
+  detail::Shadow<T>& s = detail::shadow_of(table);
   if (s.idx_data != batch.indices.data() || s.L != batch.num_lookups() ||
       s.B != batch.num_bags() || s.fwd_snapshot != table.mutation_counter()) {
     // the device context holds another forward: rebuild it (not counted as
     // TT rows, like the reference's backward recompute, test_embedding_ops.cpp:341)
-    std::vector<float> scratch(static_cast<size_t>(batch.num_bags()) * table.cols());
+    std::vector<T> scratch(static_cast<size_t>(batch.num_bags()) * table.cols());
     s.dev->forward(batch, ctx.micro_batch, true, scratch.data());
     s.idx_data = batch.indices.data();
     s.L = batch.num_lookups();
     s.B = batch.num_bags();
     s.fwd_snapshot = table.mutation_counter();
   }
-  CoreGradients<float> g = CoreGradients<float>::zeros_like(table);
-  std::vector<float*> p(g.cores.size());
+  CoreGradients<T> g = CoreGradients<T>::zeros_like(table);
+  std::vector<T*> p(g.cores.size());
   for (size_t k = 0; k < p.size(); ++k) p[k] = g.cores[k].data();
   s.dev->backward(batch, grad_output, p.data());
   return g;
@@ -246,11 +263,12 @@ inline CoreGradients<float> backward_bags(const TtTable<float>& table, const Ind
 
 /// embedding_ops.hpp:361-376: core -= T(lr) * grad (separately rounded, like
 /// the reference), written back to the host table; invalidates contexts.
-inline void sgd_step(TtTable<float>& table, const CoreGradients<float>& grads, double lr) {
+template <typename T>
+inline void sgd_step(TtTable<T>& table, const CoreGradients<T>& grads, double lr) {
   require_arg(static_cast<int>(grads.cores.size()) == table.dim(), "gradient core count mismatch");
   for (int k = 0; k < table.dim(); ++k)
     require_arg(grads.cores[k].size() == table.core(k).size(), "gradient shape mismatch on core ", k);
-  detail::Shadow& s = detail::shadow_of(table);
+  detail::Shadow<T>& s = detail::shadow_of(table);
   s.dev->sgd(grads, lr);
   s.dev->download(table);
   table.mark_mutated();
@@ -259,20 +277,22 @@ inline void sgd_step(TtTable<float>& table, const CoreGradients<float>& grads, d
 }
 
 /// embedding_ops.hpp:120-152 (bit-identical; bumps the row counter by one)
-inline void lookup_row(const TtTable<float>& table, index_t row, std::span<float> out) {
+template <typename T>
+inline void lookup_row(const TtTable<T>& table, index_t row, std::span<T> out) {
   if (row < 0 || row >= table.plan().num_rows)
     throw std::out_of_range(concat("index ", row, " out of range [0, ", table.plan().num_rows,
                                    ") for table '", table.name(), "'"));
   require_arg(static_cast<index_t>(out.size()) == table.plan().emb_dim, "lookup_row: out has ",
               out.size(), " elements, expected ", table.plan().emb_dim);
-  detail::Shadow& s = detail::shadow_of(table);
+  detail::Shadow<T>& s = detail::shadow_of(table);
   s.dev->lookup_row(row, out.data());
   EmbeddingStats::add_rows(1);
 }
 
-inline std::vector<float> lookup_row(const TtTable<float>& table, index_t row) {
-  std::vector<float> out(table.cols());
-  lookup_row(table, row, std::span<float>(out));
+template <typename T>
+inline std::vector<T> lookup_row(const TtTable<T>& table, index_t row) {
+  std::vector<T> out(table.cols());
+  gpu::lookup_row(table, row, std::span<T>(out));
   return out;
 }
 
