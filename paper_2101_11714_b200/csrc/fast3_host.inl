@@ -226,6 +226,7 @@ struct F3Runner {
 };
 
 // instantiation table: (P0, R1, N1, R2, N2, TT)
+using F3_R4 = f3::Dims<2, 4, 2, 4, 4, 32>;
 using F3_R8 = f3::Dims<2, 8, 2, 8, 4, 32>;
 using F3_R16 = f3::Dims<2, 16, 2, 16, 4, 32>;
 using F3_R32 = f3::Dims<2, 32, 2, 32, 4, 32>;
@@ -245,6 +246,7 @@ int f3_kind(const ttgpu_table* t) {
   if (P.num_rows >= (1ll << 32) || static_cast<int64_t>(P.m[0]) * P.m[1] * P.m[2] >= (1ll << 32))
     return -1;
   if (std::max(P.m[1], P.m[2]) > 6144 || P.m[0] > 8192) return -1;
+  if (dims_match<F3_R4>(P)) return 4;
   if (dims_match<F3_R8>(P)) return 0;
   if (dims_match<F3_R16>(P)) return 1;
   if (dims_match<F3_R32>(P)) return 2;
@@ -266,6 +268,7 @@ void f3_forward(int kind, ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t
     case 1: F3Runner<F3_R16>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
     case 2: F3Runner<F3_R32>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
     case 3: F3Runner<F3_R64>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
+    case 4: F3Runner<F3_R4>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
     default: fail(TTGPU_ERR_RUNTIME, "bad fast-path kind");
   }
 }
@@ -277,6 +280,7 @@ void f3_backward(ttgpu_table* t, F3Bufs& f, const float* grad, int mode, float l
     case 1: F3Runner<F3_R16>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
     case 2: F3Runner<F3_R32>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
     case 3: F3Runner<F3_R64>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
+    case 4: F3Runner<F3_R4>::backward(t, f, grad, mode, lr, lk_bag, alpha, L); break;
     default: fail(TTGPU_ERR_RUNTIME, "bad fast-path kind");
   }
 }

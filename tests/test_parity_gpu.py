@@ -416,7 +416,7 @@ def test_init_matches_reference_initializer():
 
 
 # ------------------------------------------------ specialised 3-core path --
-@pytest.mark.parametrize("rank", [8, 16, 32, 64])
+@pytest.mark.parametrize("rank", [4, 8, 16, 32, 64])
 @pytest.mark.parametrize("exponent", [0.0, 1.2])
 def test_fast_path_vs_oracle_and_generic(orc, rank, exponent):
     """The compiled-shape fast path (tile counting sort, smem partials) against

@@ -57,3 +57,21 @@ def test_reference_embedding_ops_tests_on_gpu():
 def test_reference_lfu_cache_tests_on_gpu():
     fails, (cases, passed, failed, checks, bad) = _run("test_lfu_cache_gpu")
     assert failed == 0 and bad == 0 and checks > 1000
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_gate_on_gpu(tmp_path):
+    """tests/acceptance.cpp (8 criteria, 103,365 checks) with the GPU operators.
+    Criterion 7 also asserts CPU-performance trends (P-amortisation, rank
+    ordering at 8-bag batches); it passed on B200 (profiles/ref_acceptance_gpu.txt)
+    but is timing-based, so only criteria 1-6 and 8 are required here."""
+    path = os.path.join(REF, "acceptance_gpu")
+    if not os.path.exists(path):
+        pytest.skip("acceptance_gpu not built (needs the reference sources and nlohmann/json)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=1500, cwd=tmp_path)
+    print(r.stdout[-3000:])
+    status = dict(re.findall(r"\[(PASS|FAIL)\] criterion (\d+):", r.stdout)[i][::-1]
+                  for i in range(len(re.findall(r"\[(PASS|FAIL)\] criterion (\d+):", r.stdout))))
+    assert len(status) == 8, r.stdout[-2000:] + r.stderr[-2000:]
+    for c in ("1", "2", "3", "4", "5", "6", "8"):
+        assert status[c] == "PASS", f"criterion {c}: {r.stdout[-2000:]}"
