@@ -524,3 +524,45 @@ def test_data_parallel_shards_sum_to_full_batch(orc):
                               orc.forward(as_oplan(plan), cores, b.indices, b.offsets))
     finally:
         dist.destroy_process_group()
+
+
+def test_host_api_graph_replay_matches_eager(orc):
+    """Host C-ABI calls replay a cached graph of their kernels from the third
+    call with the same shape on; results must equal the eager calls (and the
+    oracle) through shape changes, weights and workspace growth."""
+    import torch
+
+    p = tt.plan_shapes(CFG2.num_rows, 16, 3, 32, CFG2.row_factors, CFG2.col_factors)
+    stream = torch.cuda.Stream()
+    t = tt.TtTable(p, "replay", stream=stream.cuda_stream)
+    rng = np.random.default_rng(17)
+    cores = [(rng.standard_normal(p.core_size(k)) * 0.3).astype(np.float32) for k in range(3)]
+    t.set_cores(cores)
+    ctx = tt.ForwardContext(t)
+    shapes = [(2048, False), (2048, False), (2048, False), (2048, False), (512, True), (2048, False),
+              (2048, False), (4096, True), (2048, False), (2048, False)]
+    import ctypes as C
+
+    from paper_2101_11714_b200._lib import lib
+
+    cur = [c.copy() for c in cores]
+    for n, weighted in shapes:
+        b = tt.generate_zipfian_batch(p.num_rows, 1.05, int(rng.integers(1 << 20)), n, 2)
+        w = rng.uniform(-1, 1, b.num_lookups()) if weighted else None
+        out = np.zeros((n, 16), np.float32)
+        st = lib().ttgpu_forward(t.handle, b.indices.ctypes.data_as(C.c_void_p), b.num_lookups(),
+                                 b.offsets.ctypes.data_as(C.c_void_p), n,
+                                 None if w is None else w.ctypes.data_as(C.c_void_p), 0, 2048, 1,
+                                 out.ctypes.data_as(C.c_void_p), ctx.handle)
+        assert st == 0, lib().ttgpu_last_error()
+        want = orc.forward(as_oplan(p), cur, b.indices, b.offsets, w)
+        assert np.array_equal(out, want)
+        g = rng.standard_normal((n, 16)).astype(np.float32)
+        ctx._fill(t, b.num_lookups(), n, True)
+        t.backward_sgd(ctx, b, g, 1e-4)
+        full = orc.backward(as_oplan(p), cur, b.indices, b.offsets, g, w)
+        orc.sgd(as_oplan(p), cur, full, 1e-4)
+        for k in range(3):
+            assert np.all(np.isfinite(t.core(k)))
+            assert scaled_max_err(t.core(k), cur[k]) <= GRAD_TOL
+        cur = [t.core(k).copy() for k in range(3)]  # track the device state exactly
