@@ -54,9 +54,10 @@ CONFIGS = {
 }
 CONFIGS["cfg5"] = dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32,
                       bags=65536, pf=1, zipf=1.05, collection=True,
-                      desc="DLRM cfg5 TT part: the 7 largest Criteo-Kaggle tables (paper Table 2) "
-                           "at R=32, 65,536 bags x 1 per table, Zipf(1.05) (device sampler), "
-                           "one multi-stream CUDA graph per step")
+                      desc="DLRM cfg5 embeddings: 26 Criteo-Kaggle sparse features, the 7 "
+                           "largest TT-compressed at R=32 (paper Table 2) + 19 uncompressed, "
+                           "65,536 bags x 1 per feature, Zipf(1.05) (device sampler), "
+                           "fwd+bwd+SGD in one multi-stream CUDA graph per step")
 LR = 0.01
 
 
@@ -231,8 +232,11 @@ def run_collection(args, cfg, rank, world, local):
     from paper_2101_11714_b200.collection import TtEmbeddingCollection, kaggle_plans
     from paper_2101_11714_b200.streams import DeviceZipfSampler, bag_offsets_device
 
+    from paper_2101_11714_b200.dense import KAGGLE_DENSE_ROWS
+
     plans = kaggle_plans(cfg["rank"], cfg["emb"])
-    col = TtEmbeddingCollection(plans, [f"kaggle{i}" for i in range(len(plans))], device=local)
+    col = TtEmbeddingCollection(plans, [f"kaggle{i}" for i in range(len(plans))], device=local,
+                                dense_rows=KAGGLE_DENSE_ROWS, dense_dim=cfg["emb"])
     B, N = cfg["bags"], cfg["emb"]
     L = B * cfg["pf"]
     inputs, keep = [], []
@@ -247,6 +251,20 @@ def run_collection(args, cfg, rank, world, local):
                           generator=torch.Generator(device=dev).manual_seed(100 + i))
         keep += [s, d_idx, d_off, d_out, d_g]
         inputs.append((d_idx.data_ptr(), L, d_off.data_ptr(), B, d_out.data_ptr(), d_g.data_ptr()))
+    # the 19 uncompressed features: one (n_dense x L) index block, shared offsets
+    nd = len(KAGGLE_DENSE_ROWS)
+    dd_idx = torch.empty((nd, L), dtype=torch.int64, device=dev)
+    for j, rows in enumerate(KAGGLE_DENSE_ROWS):
+        s = DeviceZipfSampler(rows, cfg["zipf"], device=local)
+        s.draw_device(11 + 131 * rank, (100 + j) * L, L, dd_idx[j].data_ptr())
+        keep.append(s)
+    dd_off = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    bag_offsets_device(B, cfg["pf"], dd_off.data_ptr())
+    dd_out = torch.empty((nd, B, N), dtype=torch.float32, device=dev)
+    dd_g = torch.randn((nd, B, N), dtype=torch.float32, device=dev,
+                       generator=torch.Generator(device=dev).manual_seed(99))
+    keep += [dd_idx, dd_off, dd_out, dd_g]
+    dense_inputs = (dd_idx.data_ptr(), L, dd_off.data_ptr(), B, dd_out.data_ptr(), dd_g.data_ptr())
     torch.cuda.synchronize(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -273,41 +291,44 @@ def run_collection(args, cfg, rank, world, local):
         return tot / args.steps
 
     for _ in range(3):  # allocate every workspace before capture
-        col.step(inputs, LR)
+        col.step(inputs, LR, dense_inputs)
     col.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     if col.capturable:
-        col.capture(inputs, LR)
+        col.capture(inputs, LR, dense_inputs)
         run_par = col.replay
     else:  # host-side collective in the step: eager launches
         def run_par():
-            col.step(inputs, LR)
+            col.step(inputs, LR, dense_inputs)
     ms_par = timed(run_par)
     clk = clocks.stop()
     # the same step with every table on the main stream (no overlap between tables)
     for t in col.tables:
         t.set_stream(col.main.cuda_stream)
+    col.dense.set_stream(col.main.cuda_stream)
     saved = col.streams
     col.streams = [col.main] * len(saved)
+    col.dense_stream = col.main
     if col.capturable:
-        col.capture(inputs, LR)
+        col.capture(inputs, LR, dense_inputs)
         run_seq = col.replay
     else:
         def run_seq():
-            col.step(inputs, LR)
+            col.step(inputs, LR, dense_inputs)
     ms_seq = timed(run_seq)
     col.synchronize()
-    total = world * len(plans) * L
+    total = world * (len(plans) + nd) * L
     if rank == 0:
-        line = {"metric": METRIC + " [cfg5: 7-table TT step]", "value": total / (ms_par / 1e3),
+        line = {"metric": METRIC + " [cfg5: 26-feature embedding step]", "value": total / (ms_par / 1e3),
                 "unit": "indices/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_par, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic: device Zipf(1.05) streams per table (reference CDF), "
                         "sampled-Gaussian cores, N(0,1) grad_out",
-                "config": {"workload": cfg["desc"], "tables": len(plans),
+                "config": {"workload": cfg["desc"], "tables": len(plans) + nd, "tt_tables": len(plans),
+                           "dense_tables": nd,
                            "lookups_per_step": total, "parallelism":
                                f"dp{world}" if world > 1 else "single-gpu",
                            "l2": "flushed (256 MiB write) before every timed step"},

@@ -260,6 +260,27 @@ int ttgpu_peer_reduce_sgd(ttgpu_table* t, double lr);
 /* synchronises; timed_out = 1 if a reduce gave up waiting for a rank */
 int ttgpu_peer_status(ttgpu_table* t, int* timed_out);
 
+/* ---- uncompressed embedding-bag tables (the DLRM
+ * features that are not TT-compressed).  A group of tables shares one row
+ * store and one bag structure: indices n_tables x L (table-major), offsets
+ * B + 1, outputs / gradients n_tables x B x dim.  Forward sums in lookup
+ * order (separately rounded); backward = stable sort by row + fixed-order
+ * segmented sums, fused with row -= lr * g (fused = 1) or into a dense gradient
+ * buffer for an allreduce (fused = 0, then ttgpu_dense_apply_grad). */
+typedef struct ttgpu_dense ttgpu_dense;
+int ttgpu_dense_create(int n_tables, const int64_t* rows, int64_t dim, int dtype, int device,
+                       void* stream, ttgpu_dense** out);
+int ttgpu_dense_destroy(ttgpu_dense* d);
+int ttgpu_dense_set_stream(ttgpu_dense* d, void* stream);
+int ttgpu_dense_set_table(ttgpu_dense* d, int t, const void* host);
+int ttgpu_dense_get_table(ttgpu_dense* d, int t, void* host);
+int ttgpu_dense_forward_device(ttgpu_dense* d, const int64_t* d_idx, int64_t L,
+                               const int64_t* d_off, int64_t B, void* d_out);
+int ttgpu_dense_backward_device(ttgpu_dense* d, const void* d_grad, int fused, double lr);
+int ttgpu_dense_grad_buffer(ttgpu_dense* d, void** ptr, int64_t* n_elems);
+int ttgpu_dense_apply_grad(ttgpu_dense* d, double lr);
+int ttgpu_dense_check(ttgpu_dense* d);
+
 /* ---- device index streams -------------------------
  * ZipfianSampler(population, s) (data.hpp:16-28, data.cpp:8-33) resident on
  * the GPU: the CDF is built on the host with the reference's loop and

@@ -38,3 +38,4 @@ from . import sharding  # noqa: F401,E402
 from . import checkpoint  # noqa: F401,E402
 from . import streams  # noqa: F401,E402
 from . import collection  # noqa: F401,E402
+from . import dense  # noqa: F401,E402

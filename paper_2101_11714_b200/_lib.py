@@ -112,6 +112,16 @@ _SIGS = {
     "ttgpu_peer_flags_ptr": (C.c_int, [vp, vpp]),
     "ttgpu_peer_reduce_sgd": (C.c_int, [vp, C.c_double]),
     "ttgpu_peer_status": (C.c_int, [vp, C.POINTER(C.c_int)]),
+    "ttgpu_dense_create": (C.c_int, [C.c_int, vp, i64, C.c_int, C.c_int, vp, vpp]),
+    "ttgpu_dense_destroy": (C.c_int, [vp]),
+    "ttgpu_dense_set_stream": (C.c_int, [vp, vp]),
+    "ttgpu_dense_set_table": (C.c_int, [vp, C.c_int, vp]),
+    "ttgpu_dense_get_table": (C.c_int, [vp, C.c_int, vp]),
+    "ttgpu_dense_forward_device": (C.c_int, [vp, vp, i64, vp, i64, vp]),
+    "ttgpu_dense_backward_device": (C.c_int, [vp, vp, C.c_int, C.c_double]),
+    "ttgpu_dense_grad_buffer": (C.c_int, [vp, vpp, i64p]),
+    "ttgpu_dense_apply_grad": (C.c_int, [vp, C.c_double]),
+    "ttgpu_dense_check": (C.c_int, [vp]),
 }
 
 

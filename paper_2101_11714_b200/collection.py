@@ -12,8 +12,10 @@ Multi-GPU (`world > 1`): batch-sharded like DataParallelTable; every table's
 dense core gradient goes into one coalesced NCCL allreduce(SUM) (a single
 collective group for all 7 buffers), then the identical SGD per replica.
 
-Not here: the 19 uncompressed DLRM features and the MLPs (SURVEY §2 rows
-8-14, out of scope) -- this is the TT-embedding part of the cfg5 step.
+The 19 uncompressed DLRM features run as one DenseEmbeddingBags group
+(dense.py) on its own stream of the same graph.  Not here: the MLPs and the
+interaction (out of scope) -- this is the embedding part
+of the cfg5 step.
 """
 from __future__ import annotations
 
@@ -39,7 +41,7 @@ class TtEmbeddingCollection:
     """Several TtTables trained in one step; inputs are device pointers."""
 
     def __init__(self, plans: Sequence[ShapePlan], names: Sequence[str] = (), device: int = 0,
-                 seed: int = 1, group=None):
+                 seed: int = 1, group=None, dense_rows: Sequence[int] = (), dense_dim: int = 16):
         import torch
         import torch.distributed as dist
 
@@ -57,6 +59,21 @@ class TtEmbeddingCollection:
             t.init_sampled_gaussian(seed + i)
             self.tables.append(t)
         self.ctxs = [ForwardContext(t) for t in self.tables]
+        # the uncompressed features (dense.py): one group on its own stream
+        self.dense = None
+        if dense_rows:
+            from .dense import DenseEmbeddingBags
+
+            self.dense_stream = torch.cuda.Stream(device=self.dev)
+            self.dense = DenseEmbeddingBags(dense_rows, dense_dim, device=device,
+                                            stream=self.dense_stream.cuda_stream)
+            self.dense.init_uniform(seed + 1000)
+            self._dense_grad = None
+            if self.world > 1:
+                from .sharding import _device_view
+
+                ptr, n = self.dense.grad_buffer()
+                self._dense_grad = _device_view(ptr, n, "<f4", device)
         self.graph = None
         self._grad_views = None
         self.reducers = None
@@ -84,7 +101,9 @@ class TtEmbeddingCollection:
     @property
     def capturable(self) -> bool:
         """The step can be captured as one CUDA graph (no host-side collective)."""
-        return self.world == 1 or self.reducers is not None
+        if self.world == 1:
+            return True
+        return self.reducers is not None and self.dense is None
 
     def _table_step(self, i, idx_ptr, L, off_ptr, B, out_ptr, grad_ptr, lr):
         t, c = self.tables[i], self.ctxs[i]
@@ -97,17 +116,33 @@ class TtEmbeddingCollection:
         else:
             t.backward_device(c, grad_ptr)
 
-    def step(self, inputs, lr: float):
-        """inputs: per table (idx_ptr, L, off_ptr, B, out_ptr, grad_ptr).  Forks the
-        table streams off `main`, joins them back; with world > 1 the 7 gradient
-        buffers are reduced in one coalesced NCCL call before the SGD."""
+    def step(self, inputs, lr: float, dense_inputs=None):
+        """inputs: per TT table (idx_ptr, L, off_ptr, B, out_ptr, grad_ptr);
+        dense_inputs: (idx_ptr [n_dense x L], L, off_ptr, B, out_ptr, grad_ptr) for
+        the uncompressed group.  Forks the table streams off `main`, joins them
+        back; with world > 1 the gradients are reduced before the SGD."""
         torch = self.torch
         ev0 = torch.cuda.Event()
         ev0.record(self.main)
         for i, s in enumerate(self.streams):
             s.wait_event(ev0)
             self._table_step(i, *inputs[i], lr)
-        for s in self.streams:
+        streams = list(self.streams)
+        if self.dense is not None and dense_inputs is not None:
+            di, dl, do, db, dout, dg = dense_inputs
+            self.dense_stream.wait_event(ev0)
+            self.dense.forward_device(di, dl, do, db, dout)
+            if self.world == 1:
+                self.dense.backward_device(dg, lr, fused=True)
+            else:
+                self.dense.backward_device(dg, 0.0, fused=False)
+                import torch.distributed as dist
+
+                with torch.cuda.stream(self.dense_stream):
+                    dist.all_reduce(self._dense_grad, op=dist.ReduceOp.SUM, group=self.group)
+                self.dense.apply_grad(lr)
+            streams.append(self.dense_stream)
+        for s in streams:
             e = torch.cuda.Event()
             e.record(s)
             self.main.wait_event(e)
@@ -126,14 +161,14 @@ class TtEmbeddingCollection:
                 e.record(s)
                 self.main.wait_event(e)
 
-    def capture(self, inputs, lr: float):
+    def capture(self, inputs, lr: float, dense_inputs=None):
         """One CUDA graph of the whole multi-table step (fork/join over the
         table streams).  Workspaces must already exist (run step() once)."""
         torch = self.torch
         g = torch.cuda.CUDAGraph()
         torch.cuda.synchronize(self.dev)
         with torch.cuda.graph(g, stream=self.main):
-            self.step(inputs, lr)
+            self.step(inputs, lr, dense_inputs)
         self.graph = g
         return g
 
@@ -144,3 +179,5 @@ class TtEmbeddingCollection:
         self.torch.cuda.synchronize(self.dev)
         for t in self.tables:
             t.check()
+        if self.dense is not None:
+            self.dense.check()

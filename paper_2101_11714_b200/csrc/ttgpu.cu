@@ -1464,3 +1464,4 @@ int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
 
 void ttgpu_destroy_peers(ttgpu_peers* p) { delete p; }
 void ttgpu_table::destroy_peers() { ttgpu_destroy_peers(peers); peers = nullptr; }
+#include "dense_host.inl"

@@ -51,4 +51,4 @@ def test_two_ranks_multitable_step():
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["config"]["tables"] == 7 and d["value"] > 0
+    assert d["n_gpus"] == 2 and d["config"]["tables"] == 26 and d["config"]["tt_tables"] == 7 and d["value"] > 0
