@@ -16,32 +16,38 @@ namespace ttgpu {
 namespace {
 
 template <typename T>
-__global__ void k_dense_fwd(int ntab, const int64_t* __restrict__ base,
-                            const int64_t* __restrict__ rows, const T* __restrict__ E, int N,
-                            const int64_t* __restrict__ idx, int64_t L,
-                            const int64_t* __restrict__ off, int64_t B, T* __restrict__ out,
-                            unsigned long long* __restrict__ bad) {
-  const int64_t n = static_cast<int64_t>(ntab) * B * N;
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n;
+__global__ void k_dense_fwd(const int64_t* __restrict__ base, const int64_t* __restrict__ rows,
+                            const T* __restrict__ E, int N, const int64_t* __restrict__ idx,
+                            int64_t L, const int64_t* __restrict__ off, int64_t B,
+                            T* __restrict__ out, unsigned long long* __restrict__ bad) {
+  // grid.y = table; threads over (bag, column quad): no 64-bit divisions, and
+  // a bag's lookups are read once per 4 columns
+  const int t = blockIdx.y;
+  const int Q = (N + 3) / 4;
+  const int64_t rt = rows[t], bt = base[t];
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < B * Q;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t tb = q / N;
-    const int j = static_cast<int>(q - tb * N);
-    const int t = static_cast<int>(tb / B);
-    const int64_t b = tb - static_cast<int64_t>(t) * B;
+    const int64_t b = q / Q;
+    const int c0 = static_cast<int>(q - b * Q) * 4;
     int64_t lo = off[b], hi = off[b + 1];
     lo = lo < 0 ? 0 : lo;
     hi = hi > L ? L : hi;
-    const int64_t rt = rows[t], bt = base[t];
-    T acc = T(0);
+    T acc[4] = {T(0), T(0), T(0), T(0)};
     for (int64_t l = lo; l < hi; ++l) {
       const int64_t r = idx[static_cast<int64_t>(t) * L + l];
       if (r < 0 || r >= rt) {
-        if (j == 0) atomicMin(bad, static_cast<unsigned long long>(static_cast<int64_t>(t) * L + l));
+        if (c0 == 0) atomicMin(bad, static_cast<unsigned long long>(static_cast<int64_t>(t) * L + l));
         continue;
       }
-      acc = lfu::add_rn(acc, E[(bt + r) * N + j]);
+      const T* row = E + (bt + r) * N + c0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u < N) acc[u] = lfu::add_rn(acc[u], row[u]);
     }
-    out[q] = acc;
+    T* o = out + (static_cast<int64_t>(t) * B + b) * N + c0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < N) o[u] = acc[u];
   }
 }
 
@@ -140,9 +146,9 @@ void dense_backward(ttgpu_dense* d, const T* grad, int fused, double lr) {
       n, N, d->key.as<int>(), d->pos.as<int>(), nullptr, d->cbag.as<int32_t>(), grad,
       d->seg_lo.as<int>(), d->seg_hi.as<int>(), d->part.as<T>(), d->sg.as<T>(), d->E.as<T>(), fused,
       static_cast<T>(lr));
-  lfu::k_slot_fold<T><<<grid_for(d->total * N * 32, kThreads, d->num_sms, 8), kThreads, 0, st>>>(
-      d->total, N, d->seg_lo.as<int>(), d->seg_hi.as<int>(), d->part.as<T>(), d->sg.as<T>(),
-      d->E.as<T>(), fused, static_cast<T>(lr));
+  lfu::k_slot_fold_runs<T><<<grid_for(chunks * N * 32, kThreads, d->num_sms, 8), kThreads, 0, st>>>(
+      n, N, d->key.as<int>(), d->seg_lo.as<int>(), d->seg_hi.as<int>(), d->part.as<T>(),
+      d->sg.as<T>(), d->E.as<T>(), fused, static_cast<T>(lr));
   CK(cudaGetLastError());
 }
 }  // namespace
@@ -156,6 +162,8 @@ int ttgpu_dense_create(int n_tables, const int64_t* rows, int64_t dim, int dtype
   return guarded([&] {
     require_arg(n_tables >= 1, cat("need at least one table, got ", n_tables));
     require_arg(dim >= 1, cat("emb_dim must be positive, got ", dim));
+    require_arg(dim <= lfu::kSlotMaxN,
+                cat("dense tables support emb_dim <= ", lfu::kSlotMaxN, ", got ", dim));
     require_arg(dtype == TTGPU_F32 || dtype == TTGPU_F64, "dtype must be TTGPU_F32 or TTGPU_F64");
     CK(cudaSetDevice(device));
     auto d = std::make_unique<ttgpu_dense>();
@@ -237,15 +245,19 @@ int ttgpu_dense_forward_device(ttgpu_dense* d, const int64_t* d_idx, int64_t L,
     d->B = B;
     d->valid = true;
     if (B == 0) return;
-    const int64_t outs = static_cast<int64_t>(d->ntab) * B * d->N;
+    const int64_t per_tab = B * ((d->N + 3) / 4);
+    const dim3 grid(static_cast<unsigned>(
+                        std::max<int64_t>(1, std::min<int64_t>((per_tab + kThreads - 1) / kThreads,
+                                                               int64_t{d->num_sms} * 2))),
+                    static_cast<unsigned>(d->ntab));
     if (d->dtype == TTGPU_F64)
-      k_dense_fwd<double><<<grid_for(outs, kThreads, d->num_sms, 8), kThreads, 0, st>>>(
-          d->ntab, d->d_base.as<int64_t>(), d->d_rows.as<int64_t>(), d->E.as<double>(),
+      k_dense_fwd<double><<<grid, kThreads, 0, st>>>(
+          d->d_base.as<int64_t>(), d->d_rows.as<int64_t>(), d->E.as<double>(),
           static_cast<int>(d->N), d->idx.as<int64_t>(), L, d->off.as<int64_t>(), B,
           static_cast<double*>(d_out), d->errs.as<unsigned long long>());
     else
-      k_dense_fwd<float><<<grid_for(outs, kThreads, d->num_sms, 8), kThreads, 0, st>>>(
-          d->ntab, d->d_base.as<int64_t>(), d->d_rows.as<int64_t>(), d->E.as<float>(),
+      k_dense_fwd<float><<<grid, kThreads, 0, st>>>(
+          d->d_base.as<int64_t>(), d->d_rows.as<int64_t>(), d->E.as<float>(),
           static_cast<int>(d->N), d->idx.as<int64_t>(), L, d->off.as<int64_t>(), B,
           static_cast<float*>(d_out), d->errs.as<unsigned long long>());
     k_dense_bags<<<grid_for(B, kThreads, d->num_sms, 8), kThreads, 0, st>>>(

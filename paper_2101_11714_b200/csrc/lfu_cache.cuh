@@ -25,6 +25,7 @@ namespace lfu {
 constexpr unsigned long long kEmptyKey = ~0ull;
 constexpr unsigned long long kFib = 0x9E3779B97F4A7C15ull;
 constexpr int kSlotChunk = 32;  // sorted cached lookups per slot-gradient chunk
+constexpr int kSlotMaxN = 64;   // row width the slot-gradient kernels handle in registers
 
 __device__ __forceinline__ int probe(const unsigned long long* __restrict__ keys,
                                      const int* __restrict__ vals, int shift,
@@ -305,6 +306,52 @@ __global__ void k_slot_chunks(int64_t n, int N, const int* __restrict__ skey,
   }
 }
 
+
+// Fold for the slots whose run spans chunk boundaries, found from the sorted
+// keys themselves: boundary c (position c * kSlotChunk) starts a fold task iff
+// the key there continues the previous chunk's last key and c is that key's
+// FIRST crossed boundary.  One warp per boundary; a candidate warp folds all
+// columns (lanes over the slot's chunk partials, fixed butterfly per column).
+// Work scales with the number of chunks, not with the row count -- what the
+// uncompressed tables (150k rows) need; the LFU cache uses it too.
+template <typename T>
+__global__ void k_slot_fold_runs(int64_t n, int N, const int* __restrict__ skey,
+                                 const int* __restrict__ seg_lo, const int* __restrict__ seg_hi,
+                                 const T* __restrict__ part, T* __restrict__ sg,
+                                 T* __restrict__ store, int fused, T lr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = (n + kSlotChunk - 1) / kSlotChunk;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  // task = (boundary c, column j): a hot slot's columns fold in parallel
+  for (int64_t task = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+       task < (nchunks - 1) * N; task += nw) {
+    const int64_t c = 1 + task / N;
+    const int j = static_cast<int>(task - (c - 1) * N);
+    const int64_t p = c * kSlotChunk;
+    const int s = skey[p];
+    if (skey[p - 1] != s) continue;
+    const int lo = seg_lo[s], hi = seg_hi[s];
+    if (lo / kSlotChunk != c - 1) continue;  // not the first boundary this slot crosses
+    const int c_lo = lo / kSlotChunk, c_hi = (hi - 1) / kSlotChunk;
+    {
+      T acc = T(0);
+      for (int cc = c_lo + lane; cc <= c_hi; cc += 32) {
+        const int pp = cc == c_lo ? lo : cc * kSlotChunk;
+        acc = add_rn(acc, part[static_cast<int64_t>(pp) * N + j]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      if (lane == 0) {
+        if (fused) {
+          T* r = store + static_cast<int64_t>(s) * N + j;
+          *r = sub_rn(*r, mul_rn(lr, acc));
+        } else {
+          sg[static_cast<int64_t>(s) * N + j] = acc;
+        }
+      }
+    }
+  }
+}
 
 // Slots whose sorted range spans chunks: add the chunk partials in order.
 template <typename T>

@@ -351,6 +351,8 @@ int ttgpu_cache_create(int64_t capacity, int64_t emb_dim, int64_t refresh_period
     require_arg(out != nullptr, "null output handle");
     require_arg(capacity >= 1, cat("cache capacity must be >= 1, got ", capacity));
     require_arg(emb_dim >= 1, cat("emb_dim must be >= 1, got ", emb_dim));
+    require_arg(emb_dim <= lfu::kSlotMaxN,
+                cat("the GPU cache supports emb_dim <= ", lfu::kSlotMaxN, ", got ", emb_dim));
     require_arg(refresh_period >= 1, cat("refresh_period must be >= 1, got ", refresh_period));
     require_arg(key_space >= 1, cat("cache key space must be >= 1, got ", key_space));
     require_arg(capacity < (int64_t{1} << 30), "cache capacity too large");
