@@ -904,23 +904,21 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     for (int t = a0; t < a1; ++t) wsum += kTileCost + tile_nslots[t];
     int ex, W;
     Scan(scan_tmp).ExclusiveSum(wsum, ex, W);
-    if (tid == 0) {
-      range[0] = nt;
-      range[1] = 0;
-    }
+    // owner(t) == b  <=>  E(t) in [ceil(b W / G), ceil((b+1) W / G)): the range
+    // ends are the first tiles reaching the two thresholds; only the (at most
+    // two) threads whose chunk holds a threshold walk their chunk
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t th[2] = {(b * W + G - 1) / G, ((b + 1) * W + G - 1) / G};
+    if (tid < 2) range[tid] = th[tid] <= 0 ? 0 : nt;
     __syncthreads();
-    int lo = nt, hi = -1;
-    for (int t = a0; t < a1; ++t) {
-      const int owner = static_cast<int>(static_cast<int64_t>(ex) * gridDim.x / max(W, 1));
-      if (owner == static_cast<int>(blockIdx.x)) {
-        lo = min(lo, t);
-        hi = max(hi, t);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (ex < th[q] && th[q] <= ex + wsum) {
+        int64_t e = ex;
+        int t = a0;
+        for (; t < a1 && e < th[q]; ++t) e += kTileCost + tile_nslots[t];
+        range[q] = t;
       }
-      ex += kTileCost + tile_nslots[t];
-    }
-    if (hi >= 0) {
-      atomicMin(&range[0], lo);
-      atomicMax(&range[1], hi + 1);
     }
     __syncthreads();
     t_lo = range[0];
