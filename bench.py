@@ -643,6 +643,26 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_med, e2e_mean = float(t[0].item()), float(t[1].item())
     e2e_value = world * L / e2e_med
+    # the PCIe rates this box gives the step's own pinned buffers (grad_out
+    # H2D, output D2H; explains e2e differences between boxes: H2D from
+    # CPU-written pages varies 26-51 GB/s, tools/pcie_probe.py), CUDA events
+    pcie = {}
+    try:
+        dbuf = torch.empty(h_out.size, dtype=torch.float32, device=dev)
+        for name, cp in (("h2d", lambda: dbuf.copy_(pinned[2].view(-1), non_blocking=True)),
+                         ("d2h", lambda: pinned[3].view(-1).copy_(dbuf, non_blocking=True))):
+            best = 1e9
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                cp()
+                e1.record()
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1) * 1e-3)
+            pcie[name + "_GBs"] = h_out.nbytes / best / 1e9
+        del dbuf
+    except Exception:  # noqa: BLE001 - diagnostic only
+        pcie = {}
 
     if rank != 0:
         if dist:
@@ -734,7 +754,8 @@ def main():
                 "d2h_bytes_per_step": int(h_out.nbytes),
                 "path": "ttgpu_forward + ttgpu_backward_sgd (host C ABI, pinned buffers)",
                 "statistic": "median step time over the timed steps",
-                "ms_per_step_median": e2e_med * 1e3, "ms_per_step_mean": e2e_mean * 1e3},
+                "ms_per_step_median": e2e_med * 1e3, "ms_per_step_mean": e2e_mean * 1e3,
+                "pcie_best_GBs": pcie},
     }
     if not args.no_cpu_baseline:
         cb = cpu_reference_time(cfg, idx, off, grad, budget_s=10.0)

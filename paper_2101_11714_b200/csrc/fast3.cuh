@@ -258,7 +258,7 @@ struct ScanArgs {
 // among a bucket's tiles (one per CTA run), so wide groups keep the number of
 // group partials -- and the last arriver's sequential fold -- small.
 constexpr int kGroup = 64;
-constexpr int kGroup0 = 16;    // combine: candidate CTA blocks per warp task (dG0; dense for hot i0)
+constexpr int kGroup0 = 32;    // combine: candidate CTA blocks per warp task (dG0; dense for hot i0)
 constexpr int kScanKeys = 16;  // keys per f3_scan CTA
 constexpr int kScanThreads = 256;
 
@@ -1211,22 +1211,23 @@ template <class RowFn>
 __device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, bool colok, RowFn row_of,
                                          float4& acc) {
   while (live) {
-    int idx[4];
+    int idx[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       idx[u] = -1;
       if (live) {
         idx[u] = cand0 + __ffs(live) - 1;
         live &= live - 1;
       }
     }
-    float4 v[4];
+    float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 8; ++u)
       v[u] = (idx[u] >= 0 && colok) ? __ldg(reinterpret_cast<const float4*>(row_of(idx[u])) + col4)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) add4(acc, v[u]);
+    for (int u = 0; u < 8; ++u)
+      if (idx[u] >= 0) add4(acc, v[u]);
   }
 }
 
@@ -1282,10 +1283,23 @@ __device__ __forceinline__ void finish_task(float4 acc, bool touched, int task_f
   __threadfence();
   float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
   bool any = false;
-  for (int q = 0; q < ng; ++q) {
-    const int tq = task_first + q * nch + ch;
-    add4(sum, __ldcg(reinterpret_cast<const float4*>(A.gpart + static_cast<int64_t>(tq) * 128) + lane));
-    any |= __ldcg(A.gtouch + tq) != 0;
+  // 8 group partials in flight per round, added in group order
+  for (int q0 = 0; q0 < ng; q0 += 8) {
+    float4 v[8];
+    int tch[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int tq = task_first + (q0 + u) * nch + ch;
+      const bool ok = q0 + u < ng;
+      v[u] = ok ? __ldcg(reinterpret_cast<const float4*>(A.gpart + static_cast<int64_t>(tq) * 128) + lane)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+      tch[u] = ok ? __ldcg(A.gtouch + tq) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (q0 + u < ng) add4(sum, v[u]);
+      any |= tch[u] != 0;
+    }
   }
   store_slice(sum, any, core, grad, col4, colok, mode, lr);
   if (lane == 0) *counter = 0;  // ready for the next launch
