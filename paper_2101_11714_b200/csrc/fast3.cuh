@@ -461,24 +461,30 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
 // ------------------------------------------------------------- f3_fwd ----
 template <class D>
 struct FwdSmem {
-  // floats: G1s[S1] (TMA) | Hs[TT*HSP] | G0s[TT*S0P] | G2s[TT*S2P] ; then mbarrier + ints
+  // floats: G1s[S1] (TMA) | Hs[TT*HSP] | G0s[TT*S0P] (TMA rows) | G2s[TT*S2P] (TMA rows);
+  // then mbarrier + ints
   static constexpr int R2P = D::R2 + 1;          // padded H rows: (slot, row) -> distinct banks
   static constexpr int HSP = D::P1 * R2P + 1;    // odd slot stride
-  static constexpr int S0P = D::S0 + 1;
+  static constexpr int HSP4 = (D::TT * HSP + 3) / 4 * 4;
+  static constexpr int S0P = D::S0 + 4;          // bulk-copy rows: 16-byte pitch, 2 slots per warp conflict-free
   static constexpr int S2P = D::S2 + 4;          // lookups' float4 rows in distinct bank groups
   static __host__ __device__ size_t floats() {
-    size_t f = D::S1 + static_cast<size_t>(D::TT) * (HSP + S0P + S2P);
+    size_t f = D::S1 + static_cast<size_t>(HSP4) + static_cast<size_t>(D::TT) * (S0P + S2P);
     return (f + 3) / 4 * 4;
   }
-  static __host__ __device__ size_t bytes(int m0) {
-    return floats() * 4 + 16 + sizeof(int) * (static_cast<size_t>(m0) + 6 * D::TT + 16);
+  static __host__ __device__ size_t bytes(int /*m0*/) {
+    return floats() * 4 + 16 + sizeof(int) * (2 * D::TT + 4);
   }
 };
 
-// Per i1-tile: TMA G1[i1] (issued first, overlaps the index gathers); slots =
-// distinct i0 numbered by first occurrence in the tile (warp ballots; the
-// numbering backward reuses); H(slot) = G0·G1; y = H·G2[i2] per lookup.
-// Saves H rows and, per lookup, the H row index (hloc) for f3_bwd2.
+// Per i1-tile (CTAs stride over the tiles).  Warp 0 owns the tile's lookups
+// (one per lane): slots = distinct i0 numbered by first occurrence (match_any;
+// the numbering backward reuses), then it issues every operand copy onto one
+// mbarrier -- G1[i1], one G0 row per slot, one G2 row per lookup -- and its
+// lane-0 arrive publishes the tile's metadata.  The next tile's descriptor,
+// positions and digits are loaded by warp 0 in stages during this tile's H and
+// y phases.  H(slot) = G0·G1; y = H·G2[i2] per lookup.  Saves H rows and, per
+// lookup, the H row index (hloc) for f3_bwd2.
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
@@ -492,122 +498,74 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots) {
   using SM = FwdSmem<D>;
-  constexpr int TW = (D::TT + 31) / 32;  // warps holding tile lookups
   extern __shared__ __align__(128) float sm[];
   float* G1s = sm;
   float* Hs = G1s + D::S1;
-  float* G0s = Hs + D::TT * SM::HSP;
+  float* G0s = Hs + SM::HSP4;
   float* G2s = G0s + D::TT * SM::S0P;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());
-  int* first = reinterpret_cast<int*>(bar + 2);  // m0: first tile position of each i0
-  int* lk_l = first + g.m0;
-  int* lk_i0 = lk_l + D::TT;
-  int* lk_i2 = lk_i0 + D::TT;
-  int* lk_slot = lk_i2 + D::TT;
-  int* slot_i0 = lk_slot + D::TT;
-  int* slot_at = slot_i0 + D::TT;  // slot id of a first-occurrence position
-  int* wcnt = slot_at + D::TT;     // 16
+  int* lk_l = reinterpret_cast<int*>(bar + 1);
+  int* lk_slot = lk_l + D::TT;
+  int* meta = lk_slot + D::TT;  // ntl, nslots, start
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) mbar_init(bar, 1);
-  for (int i = tid; i < g.m0; i += kThreads) first[i] = 0x7fffffff;
   __syncthreads();
+  // warp 0's pipeline registers for the next tile
+  Tile nd{};
+  int nl = 0, ni0 = 0, ni2 = 0;
+  if (wid == 0 && static_cast<int>(blockIdx.x) < nt) {
+    nd = tiles[blockIdx.x];
+    if (lane < nd.end - nd.start) {
+      nl = static_cast<int>(perm[nd.start + lane]);
+      ni0 = d0[nl];
+      ni2 = d2[nl];
+    }
+  }
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < nt; t += gridDim.x, phase ^= 1u) {
-    const Tile tl = tiles[t];
-    const int i1 = tl.key;
-    const int ntl = tl.end - tl.start;
-    if (tid == 0) {
-      // smem last touched by generic-proxy accesses; order them before the TMA write
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect(bar, D::S1 * 4);
-      tma_load(G1s, G1 + static_cast<int64_t>(i1) * D::S1, D::S1 * 4, bar);
-    }
-    int my_i0 = -1;
-    if (tid < ntl) {
-      const int l = static_cast<int>(perm[tl.start + tid]);
-      my_i0 = d0[l];
-      lk_l[tid] = l;
-      lk_i0[tid] = my_i0;
-      lk_i2[tid] = d2[l];
-      atomicMin(&first[my_i0], tid);
-    }
-    __syncthreads();
-    const bool is_first = tid < ntl && first[my_i0] == tid;
-    const unsigned fb = __ballot_sync(0xffffffffu, is_first);
-    if (wid < TW && lane == 0) wcnt[wid] = __popc(fb);
-    __syncthreads();
-    int base = 0, nslots = 0;
-#pragma unroll
-    for (int w = 0; w < TW; ++w) {
-      base += (w < wid) ? wcnt[w] : 0;
-      nslots += wcnt[w];
-    }
-    if (is_first) {
-      const int s = base + __popc(fb & lanemask_lt());
-      slot_i0[s] = my_i0;
-      slot_at[tid] = s;
-      tile_i0[tl.start + s] = static_cast<uint16_t>(my_i0);
-    }
-    __syncthreads();
-    if (tid < ntl) {
-      const int s = slot_at[first[my_i0]];
-      lk_slot[tid] = s;
-      slot_of_pos[tl.start + tid] = static_cast<uint16_t>(s);
-      hloc[lk_l[tid]] = static_cast<uint32_t>(tl.start + s);
-    }
-    if (tid == 0) tile_nslots[t] = nslots;
-    // G0 rows of the slots and G2 slices of the lookups (independent loads, batched)
-    {
-      constexpr int U = 8;
-      for (int e0 = tid; e0 < nslots * D::S0; e0 += kThreads * U) {
-        float v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * kThreads;
-          v[u] = 0.f;
-          if (e < nslots * D::S0) {
-            const int s = e / D::S0;
-            v[u] = __ldg(G0 + static_cast<int64_t>(slot_i0[s]) * D::S0 + (e - s * D::S0));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int e = e0 + u * kThreads;
-          if (e < nslots * D::S0) {
-            const int s = e / D::S0;
-            G0s[s * SM::S0P + (e - s * D::S0)] = v[u];
-          }
-        }
+    const int tn = t + static_cast<int>(gridDim.x);
+    if (wid == 0) {
+      const Tile tl = nd;
+      const int ntl = tl.end - tl.start;
+      const bool act = lane < ntl;
+      const int l = nl, i0 = ni0, i2 = ni2;
+      const unsigned peers = __match_any_sync(0xffffffffu, act ? i0 : -1);
+      const int leader = __ffs(peers) - 1;
+      const bool is_first = act && leader == lane;
+      const unsigned fb = __ballot_sync(0xffffffffu, is_first);
+      const int nslots = __popc(fb);
+      const int s = __shfl_sync(0xffffffffu, __popc(fb & lanemask_lt()), leader);
+      if (act) {
+        lk_l[lane] = l;
+        lk_slot[lane] = s;
+        slot_of_pos[tl.start + lane] = static_cast<uint16_t>(s);
+        hloc[l] = static_cast<uint32_t>(tl.start + s);
       }
-      constexpr int Q = D::S2 / 4;
-      for (int e0 = tid; e0 < ntl * Q; e0 += kThreads * 4) {
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + u * kThreads;
-          if (e < ntl * Q) {
-            const int i = e / Q;
-            v[u] = __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(lk_i2[i]) * D::S2) +
-                         (e - i * Q));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + u * kThreads;
-          if (e < ntl * Q) {
-            const int i = e / Q;
-            reinterpret_cast<float4*>(G2s + i * SM::S2P)[e - i * Q] = v[u];
-          }
-        }
+      if (is_first) tile_i0[tl.start + s] = static_cast<uint16_t>(i0);
+      if (lane == 0) {
+        tile_nslots[t] = nslots;
+        meta[0] = ntl;
+        meta[1] = nslots;
+        meta[2] = tl.start;
       }
+      __syncwarp();
+      if (lane == 0) {
+        // smem last touched by generic-proxy accesses; order them before the async writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect(bar, (D::S1 + nslots * D::S0 + ntl * D::S2) * 4);
+        tma_load(G1s, G1 + static_cast<int64_t>(tl.key) * D::S1, D::S1 * 4, bar);
+      }
+      __syncwarp();
+      if (is_first) tma_load(G0s + s * SM::S0P, G0 + static_cast<int64_t>(i0) * D::S0, D::S0 * 4, bar);
+      if (act) tma_load(G2s + lane * SM::S2P, G2 + static_cast<int64_t>(i2) * D::S2, D::S2 * 4, bar);
+      if (tn < nt) nd = tiles[tn];  // stage 1 of the next tile (consumed after H)
     }
-    __syncthreads();
-    if (tid < ntl && is_first) first[my_i0] = 0x7fffffff;  // ready for the next tile
     mbar_wait(bar, phase);
+    const int ntl = meta[0], nslots = meta[1], start = meta[2];
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
     for (int q = tid; q < nslots * D::C4; q += kThreads) {
       const int s = q / D::C4, c4 = q - s * D::C4;
@@ -622,7 +580,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         for (int a = 0; a < D::P0; ++a) acc[a] = madd4<float, kExact>(g0[a * D::R1 + p], b, acc[a]);
       }
       float* hs = Hs + s * SM::HSP;
-      float* hg = Hbuf + static_cast<int64_t>(tl.start + s) * D::W1;
+      float* hg = Hbuf + static_cast<int64_t>(start + s) * D::W1;
 #pragma unroll
       for (int a = 0; a < D::P0; ++a) {
         const int c = a * D::C1 + c4 * 4;  // = (row, r) in the (P1 x R2) view
@@ -635,6 +593,8 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         reinterpret_cast<float4*>(hg + c)[0] = acc[a];
       }
     }
+    if (wid == 0 && tn < nt && lane < nd.end - nd.start)
+      nl = static_cast<int>(perm[nd.start + lane]);  // stage 2 (consumed after y)
     __syncthreads();
     // y = H(slot) (P1 x R2) · G2[i2] (R2 x N2): thread -> (lookup, row a)
     for (int q = tid; q < ntl * D::P1; q += kThreads) {
@@ -646,7 +606,11 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
       for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
       reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
     }
-    __syncthreads();
+    if (wid == 0 && tn < nt && lane < nd.end - nd.start) {  // stage 3: digits of the next tile
+      ni0 = d0[nl];
+      ni2 = d2[nl];
+    }
+    __syncthreads();  // smem (operands, H, metadata) free for the next tile
   }
 }
 
