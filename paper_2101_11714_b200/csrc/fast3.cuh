@@ -383,7 +383,10 @@ __global__ void __launch_bounds__(kScanThreads) f3_scan(ScanArgs a1, ScanArgs a2
 // lookups, keys loaded 8 rounds at a time.  Run for key 1 then key 2.
 __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, int K, int64_t L,
                                             int TL, int NT, const uint32_t* __restrict__ hoff,
-                                            uint32_t* __restrict__ perm, uint32_t* wc) {
+                                            uint32_t* __restrict__ perm, uint32_t* wc,
+                                            const uint16_t* __restrict__ dg0 = nullptr,
+                                            const uint16_t* __restrict__ dg2 = nullptr,
+                                            uint2* __restrict__ rec = nullptr) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int per = TL / 8;
@@ -435,6 +438,8 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
       __syncwarp();
       if (k != 0xffffffffu) {
         perm[pos] = static_cast<uint32_t>(l);
+        // sorted record (position -> lookup, i0 | i2 << 16) for f3_fwd
+        if (rec) rec[pos] = make_uint2(static_cast<uint32_t>(l), dg0[l] | (static_cast<uint32_t>(dg2[l]) << 16));
         if (lane == __ffs(peers) - 1) my[k] += __popc(peers);
       }
       __syncwarp();
@@ -443,18 +448,20 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restrict__ d1,
+__global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restrict__ d0,
+                                                  const uint16_t* __restrict__ d1,
                                                   const uint16_t* __restrict__ d2, int64_t L,
                                                   int TL, int NT, const uint32_t* __restrict__ hoff1,
                                                   const uint32_t* __restrict__ hoff2,
                                                   uint32_t* __restrict__ perm1,
                                                   uint32_t* __restrict__ perm2,
-                                                  uint32_t* __restrict__ tot) {
+                                                  uint32_t* __restrict__ tot,
+                                                  uint2* __restrict__ rec1) {
   extern __shared__ uint32_t wc[];  // 8 x max(m1, m2)
   // f3_scan has consumed the bucket totals: clear them for the next batch
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.m1 + g.m2; k += gridDim.x * blockDim.x)
     tot[k] = 0u;
-  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc);
+  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc, d0, d2, rec1);
   scatter_one(d2, g.m2, L, TL, NT, hoff2, perm2, wc);
 }
 
@@ -481,17 +488,15 @@ struct FwdSmem {
 // (one per lane): slots = distinct i0 numbered by first occurrence (match_any;
 // the numbering backward reuses), then it issues every operand copy onto one
 // mbarrier -- G1[i1], one G0 row per slot, one G2 row per lookup -- and its
-// lane-0 arrive publishes the tile's metadata.  The next tile's descriptor,
-// positions and digits are loaded by warp 0 in stages during this tile's H and
-// y phases.  H(slot) = G0·G1; y = H·G2[i2] per lookup.  Saves H rows and, per
+// lane-0 arrive publishes the tile's metadata.  The next tile's descriptor and
+// its sorted records (lookup, digits; written by f3_scatter) are loaded by
+// warp 0 during this tile's H phase.  H(slot) = G0·G1; y = H·G2[i2] per lookup.  Saves H rows and, per
 // lookup, the H row index (hloc) for f3_bwd2.
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
                                                    const int* __restrict__ ntiles,
-                                                   const uint32_t* __restrict__ perm,
-                                                   const uint16_t* __restrict__ d0,
-                                                   const uint16_t* __restrict__ d2,
+                                                   const uint2* __restrict__ rec,
                                                    float* __restrict__ Hbuf, float* __restrict__ y,
                                                    uint32_t* __restrict__ hloc,
                                                    uint16_t* __restrict__ slot_of_pos,
@@ -516,14 +521,10 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   __syncthreads();
   // warp 0's pipeline registers for the next tile
   Tile nd{};
-  int nl = 0, ni0 = 0, ni2 = 0;
+  uint2 nr = make_uint2(0u, 0u);  // (lookup, i0 | i2 << 16) of this lane's next-tile position
   if (wid == 0 && static_cast<int>(blockIdx.x) < nt) {
     nd = tiles[blockIdx.x];
-    if (lane < nd.end - nd.start) {
-      nl = static_cast<int>(perm[nd.start + lane]);
-      ni0 = d0[nl];
-      ni2 = d2[nl];
-    }
+    if (lane < nd.end - nd.start) nr = rec[nd.start + lane];
   }
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < nt; t += gridDim.x, phase ^= 1u) {
@@ -532,7 +533,8 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
       const Tile tl = nd;
       const int ntl = tl.end - tl.start;
       const bool act = lane < ntl;
-      const int l = nl, i0 = ni0, i2 = ni2;
+      const int l = static_cast<int>(nr.x), i0 = static_cast<int>(nr.y & 0xffffu),
+                i2 = static_cast<int>(nr.y >> 16);
       const unsigned peers = __match_any_sync(0xffffffffu, act ? i0 : -1);
       const int leader = __ffs(peers) - 1;
       const bool is_first = act && leader == lane;
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
       }
     }
     if (wid == 0 && tn < nt && lane < nd.end - nd.start)
-      nl = static_cast<int>(perm[nd.start + lane]);  // stage 2 (consumed after y)
+      nr = rec[nd.start + lane];  // stage 2 (consumed at the next tile)
     __syncthreads();
     // y = H(slot) (P1 x R2) · G2[i2] (R2 x N2): thread -> (lookup, row a)
     for (int q = tid; q < ntl * D::P1; q += kThreads) {
@@ -605,10 +607,6 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
 #pragma unroll 8
       for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
       reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
-    }
-    if (wid == 0 && tn < nt && lane < nd.end - nd.start) {  // stage 3: digits of the next tile
-      ni0 = d0[nl];
-      ni2 = d2[nl];
     }
     __syncthreads();  // smem (operands, H, metadata) free for the next tile
   }

@@ -3,7 +3,7 @@
 namespace ttgpu {
 
 struct F3Bufs {
-  DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, tiles1, tiles2, tile_base1, tile_base2, ntiles,
+  DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, rec1, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
       group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf;
   f3::Geo geo{};
@@ -83,6 +83,7 @@ struct F3Runner {
       CK(cudaMemsetAsync(f.tot.p, 0, f.tot.cap, st));
     }
     f.perm1.ensure(4 * L);
+    f.rec1.ensure(8 * L);
     f.perm2.ensure(4 * L);
     f.tiles1.ensure(sizeof(f3::Tile) * f.max_tiles1);
     f.tiles2.ensure(sizeof(f3::Tile) * f.max_tiles2);
@@ -127,10 +128,11 @@ struct F3Runner {
     {
       const size_t sm = 4 * 8 * static_cast<size_t>(Kmax);
       set_smem(f3::f3_scatter, sm);
-      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.d1.as<uint16_t>(), f.d2.as<uint16_t>(), L, TL, NT,
-                                          f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
-                                          f.perm1.as<uint32_t>(), f.perm2.as<uint32_t>(),
-                                          f.tot.as<uint32_t>());
+      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
+                                          f.d2.as<uint16_t>(), L, TL, NT, f.hist1.as<uint32_t>(),
+                                          f.hist2.as<uint32_t>(), f.perm1.as<uint32_t>(),
+                                          f.perm2.as<uint32_t>(), f.tot.as<uint32_t>(),
+                                          f.rec1.as<uint2>());
     }
     t->mark("scatter");
     {
@@ -139,8 +141,7 @@ struct F3Runner {
       set_smem(kern, sm);
       const int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
       kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
-                                           f.ntiles.as<int>(), f.perm1.as<uint32_t>(),
-                                           f.d0.as<uint16_t>(), f.d2.as<uint16_t>(),
+                                           f.ntiles.as<int>(), f.rec1.as<uint2>(),
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
                                            f.tile_nslots.as<int>());
