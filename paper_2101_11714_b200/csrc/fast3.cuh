@@ -469,29 +469,32 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
 template <class D>
 struct FwdSmem {
   // floats: G1s[S1] (TMA) | Hs[TT*HSP] | G0s[TT*S0P] (TMA rows) | G2s[TT*S2P] (TMA rows);
-  // then mbarrier + ints
+  // then 2 mbarriers + ints (2 metadata buffers)
   static constexpr int R2P = D::R2 + 1;          // padded H rows: (slot, row) -> distinct banks
   static constexpr int HSP = D::P1 * R2P + 1;    // odd slot stride
   static constexpr int HSP4 = (D::TT * HSP + 3) / 4 * 4;
   static constexpr int S0P = D::S0 + 4;          // bulk-copy rows: 16-byte pitch, 2 slots per warp conflict-free
   static constexpr int S2P = D::S2 + 4;          // lookups' float4 rows in distinct bank groups
+  static constexpr int MI = 2 * D::TT + 4;       // ints per metadata buffer: lk_l, lk_slot, meta
   static __host__ __device__ size_t floats() {
     size_t f = D::S1 + static_cast<size_t>(HSP4) + static_cast<size_t>(D::TT) * (S0P + S2P);
     return (f + 3) / 4 * 4;
   }
   static __host__ __device__ size_t bytes(int /*m0*/) {
-    return floats() * 4 + 16 + sizeof(int) * (2 * D::TT + 4);
+    return floats() * 4 + 16 + sizeof(int) * 2 * MI;
   }
 };
 
-// Per i1-tile (CTAs stride over the tiles).  Warp 0 owns the tile's lookups
-// (one per lane): slots = distinct i0 numbered by first occurrence (match_any;
-// the numbering backward reuses), then it issues every operand copy onto one
-// mbarrier -- G1[i1], one G0 row per slot, one G2 row per lookup -- and its
-// lane-0 arrive publishes the tile's metadata.  The next tile's descriptor and
-// its sorted records (lookup, digits; written by f3_scatter) are loaded by
-// warp 0 during this tile's H phase.  H(slot) = G0·G1; y = H·G2[i2] per lookup.  Saves H rows and, per
-// lookup, the H row index (hloc) for f3_bwd2.
+// Per i1-tile (CTAs stride over the tiles), software-pipelined one tile ahead:
+//   wait A (G1[i1], G0 rows of the slots) -> H(slot) = G0·G1 (all warps)
+//   | warp 0: slots of the next tile (distinct i0 numbered by first
+//   |   occurrence, match_any; the numbering backward reuses) and its G1/G0
+//   |   bulk copies onto A, overlapping ...
+//   wait B (G2 rows of the lookups) -> y = H·G2[i2] (warps 1..)
+//   then warp 0 issues the next tile's G2 rows onto B (they land during its H).
+// Tile descriptors and sorted records (lookup, digits; f3_scatter) are loaded
+// two tiles ahead.  Saves H rows and, per lookup, the H row index (hloc) for
+// f3_bwd2.
 template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
@@ -508,64 +511,90 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   float* Hs = G1s + D::S1;
   float* G0s = Hs + SM::HSP4;
   float* G2s = G0s + D::TT * SM::S0P;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());
-  int* lk_l = reinterpret_cast<int*>(bar + 1);
-  int* lk_slot = lk_l + D::TT;
-  int* meta = lk_slot + D::TT;  // ntl, nslots, start
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());  // [0] G1+G0, [1] G2
+  int* mbuf = reinterpret_cast<int*>(bar + 2);                      // 2 x {lk_l, lk_slot, meta}
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
   const int nt = *ntiles;
+  const int G = static_cast<int>(gridDim.x);
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  if (tid == 0) mbar_init(bar, 1);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
   __syncthreads();
-  // warp 0's pipeline registers for the next tile
-  Tile nd{};
-  uint2 nr = make_uint2(0u, 0u);  // (lookup, i0 | i2 << 16) of this lane's next-tile position
-  if (wid == 0 && static_cast<int>(blockIdx.x) < nt) {
-    nd = tiles[blockIdx.x];
-    if (lane < nd.end - nd.start) nr = rec[nd.start + lane];
+  // warp 0 state: this lane's lookup of the staged tile (for its G2 copy), the
+  // next tile's descriptor + record, the tile after that's descriptor
+  bool g2_act = false;
+  int g2_i2 = 0, g2_ntl = 0;
+  Tile ndn{}, nd2{};
+  uint2 nrn = make_uint2(0u, 0u);
+  // slots + metadata of tile u into buffer m, G1/G0 copies onto bar[0]
+  auto stage = [&](int u, const Tile& tl, uint2 r, int m) {
+    int* lk_l = mbuf + m * SM::MI;
+    int* lk_slot = lk_l + D::TT;
+    int* meta = lk_slot + D::TT;
+    const int ntl = tl.end - tl.start;
+    const bool act = lane < ntl;
+    const int l = static_cast<int>(r.x), i0 = static_cast<int>(r.y & 0xffffu);
+    const unsigned peers = __match_any_sync(0xffffffffu, act ? i0 : -1);
+    const int leader = __ffs(peers) - 1;
+    const bool is_first = act && leader == lane;
+    const unsigned fb = __ballot_sync(0xffffffffu, is_first);
+    const int nslots = __popc(fb);
+    const int s = __shfl_sync(0xffffffffu, __popc(fb & lanemask_lt()), leader);
+    if (act) {
+      lk_l[lane] = l;
+      lk_slot[lane] = s;
+      slot_of_pos[tl.start + lane] = static_cast<uint16_t>(s);
+      hloc[l] = static_cast<uint32_t>(tl.start + s);
+    }
+    if (is_first) tile_i0[tl.start + s] = static_cast<uint16_t>(i0);
+    if (lane == 0) {
+      tile_nslots[u] = nslots;
+      meta[0] = ntl;
+      meta[1] = nslots;
+      meta[2] = tl.start;
+    }
+    g2_act = act;
+    g2_i2 = static_cast<int>(r.y >> 16);
+    g2_ntl = ntl;
+    __syncwarp();
+    if (lane == 0) {
+      // smem last touched by generic-proxy accesses; order them before the async writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect(bar, (D::S1 + nslots * D::S0) * 4);
+      tma_load(G1s, G1 + static_cast<int64_t>(tl.key) * D::S1, D::S1 * 4, bar);
+    }
+    __syncwarp();
+    if (is_first) tma_load(G0s + s * SM::S0P, G0 + static_cast<int64_t>(i0) * D::S0, D::S0 * 4, bar);
+  };
+  auto issue_g2 = [&]() {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect(bar + 1, g2_ntl * D::S2 * 4);
+    }
+    __syncwarp();
+    if (g2_act)
+      tma_load(G2s + lane * SM::S2P, G2 + static_cast<int64_t>(g2_i2) * D::S2, D::S2 * 4, bar + 1);
+  };
+  const int t0 = static_cast<int>(blockIdx.x);
+  if (wid == 0 && t0 < nt) {
+    const Tile tl = tiles[t0];
+    if (t0 + G < nt) ndn = tiles[t0 + G];
+    if (t0 + 2 * G < nt) nd2 = tiles[t0 + 2 * G];
+    const uint2 r = lane < tl.end - tl.start ? rec[tl.start + lane] : make_uint2(0u, 0u);
+    if (t0 + G < nt && lane < ndn.end - ndn.start) nrn = rec[ndn.start + lane];
+    stage(t0, tl, r, 0);
+    issue_g2();
   }
   uint32_t phase = 0;
-  for (int t = blockIdx.x; t < nt; t += gridDim.x, phase ^= 1u) {
-    const int tn = t + static_cast<int>(gridDim.x);
-    if (wid == 0) {
-      const Tile tl = nd;
-      const int ntl = tl.end - tl.start;
-      const bool act = lane < ntl;
-      const int l = static_cast<int>(nr.x), i0 = static_cast<int>(nr.y & 0xffffu),
-                i2 = static_cast<int>(nr.y >> 16);
-      const unsigned peers = __match_any_sync(0xffffffffu, act ? i0 : -1);
-      const int leader = __ffs(peers) - 1;
-      const bool is_first = act && leader == lane;
-      const unsigned fb = __ballot_sync(0xffffffffu, is_first);
-      const int nslots = __popc(fb);
-      const int s = __shfl_sync(0xffffffffu, __popc(fb & lanemask_lt()), leader);
-      if (act) {
-        lk_l[lane] = l;
-        lk_slot[lane] = s;
-        slot_of_pos[tl.start + lane] = static_cast<uint16_t>(s);
-        hloc[l] = static_cast<uint32_t>(tl.start + s);
-      }
-      if (is_first) tile_i0[tl.start + s] = static_cast<uint16_t>(i0);
-      if (lane == 0) {
-        tile_nslots[t] = nslots;
-        meta[0] = ntl;
-        meta[1] = nslots;
-        meta[2] = tl.start;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        // smem last touched by generic-proxy accesses; order them before the async writes
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect(bar, (D::S1 + nslots * D::S0 + ntl * D::S2) * 4);
-        tma_load(G1s, G1 + static_cast<int64_t>(tl.key) * D::S1, D::S1 * 4, bar);
-      }
-      __syncwarp();
-      if (is_first) tma_load(G0s + s * SM::S0P, G0 + static_cast<int64_t>(i0) * D::S0, D::S0 * 4, bar);
-      if (act) tma_load(G2s + lane * SM::S2P, G2 + static_cast<int64_t>(i2) * D::S2, D::S2 * 4, bar);
-      if (tn < nt) nd = tiles[tn];  // stage 1 of the next tile (consumed after H)
-    }
+  int m = 0;
+  for (int t = t0; t < nt; t += G, phase ^= 1u, m ^= 1) {
+    const int* lk_l = mbuf + m * SM::MI;
+    const int* lk_slot = lk_l + D::TT;
+    const int* meta = lk_slot + D::TT;
     mbar_wait(bar, phase);
     const int ntl = meta[0], nslots = meta[1], start = meta[2];
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
@@ -595,20 +624,29 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         reinterpret_cast<float4*>(hg + c)[0] = acc[a];
       }
     }
-    if (wid == 0 && tn < nt && lane < nd.end - nd.start)
-      nr = rec[nd.start + lane];  // stage 2 (consumed at the next tile)
-    __syncthreads();
-    // y = H(slot) (P1 x R2) · G2[i2] (R2 x N2): thread -> (lookup, row a)
-    for (int q = tid; q < ntl * D::P1; q += kThreads) {
-      const int i = q / D::P1, a = q - i * D::P1;
-      const float* hrow = Hs + lk_slot[i] * SM::HSP + a * SM::R2P;
-      const float4* g2 = reinterpret_cast<const float4*>(G2s + i * SM::S2P);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();  // H rows complete; G1s / G0s free
+    if (wid == 0) {
+      if (t + G < nt) {
+        stage(t + G, ndn, nrn, m ^ 1);  // lands during this tile's y phase
+        ndn = nd2;
+        if (t + 2 * G < nt && lane < ndn.end - ndn.start) nrn = rec[ndn.start + lane];
+        if (t + 3 * G < nt) nd2 = tiles[t + 3 * G];
+      }
+    } else {
+      // y = H(slot) (P1 x R2) · G2[i2] (R2 x N2): thread -> (lookup, row a), warps 1..
+      mbar_wait(bar + 1, phase);
+      for (int q = tid - 32; q < ntl * D::P1; q += kThreads - 32) {
+        const int i = q / D::P1, a = q - i * D::P1;
+        const float* hrow = Hs + lk_slot[i] * SM::HSP + a * SM::R2P;
+        const float4* g2 = reinterpret_cast<const float4*>(G2s + i * SM::S2P);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-      for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
-      reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
+        for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
+        reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
+      }
     }
-    __syncthreads();  // smem (operands, H, metadata) free for the next tile
+    __syncthreads();  // G2s / Hs free
+    if (wid == 0 && t + G < nt) issue_g2();
   }
 }
 
