@@ -52,12 +52,35 @@ struct Dims {
 
 constexpr int kThreads = 256;
 
+// acc += a * b per component.  Exact: separately rounded products and sums
+// (the reference's fp32 loop), products two at a time (mul.rn.f32x2 = FMUL2,
+// same IEEE result as two FMULs) and scalar adds.  (The adds stay scalar:
+// ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2.)
+__device__ __forceinline__ float2 fmul2_rn(float a, float2 b) {
+  unsigned long long aa, bb, m;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(aa), "l"(bb));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(m));
+  return r;
+}
+
 template <typename T, bool kExact>
 __device__ __forceinline__ float4 madd4(float a, float4 b, float4 acc) {
-  acc.x = madd<float, kExact>(a, b.x, acc.x);
-  acc.y = madd<float, kExact>(a, b.y, acc.y);
-  acc.z = madd<float, kExact>(a, b.z, acc.z);
-  acc.w = madd<float, kExact>(a, b.w, acc.w);
+  if constexpr (kExact) {
+    const float2 p01 = fmul2_rn(a, make_float2(b.x, b.y));
+    const float2 p23 = fmul2_rn(a, make_float2(b.z, b.w));
+    acc.x = __fadd_rn(acc.x, p01.x);
+    acc.y = __fadd_rn(acc.y, p01.y);
+    acc.z = __fadd_rn(acc.z, p23.x);
+    acc.w = __fadd_rn(acc.w, p23.y);
+  } else {
+    acc.x = madd<float, kExact>(a, b.x, acc.x);
+    acc.y = madd<float, kExact>(a, b.y, acc.y);
+    acc.z = madd<float, kExact>(a, b.z, acc.z);
+    acc.w = madd<float, kExact>(a, b.w, acc.w);
+  }
   return acc;
 }
 

@@ -139,7 +139,9 @@ struct F3Runner {
       const size_t sm = f3::FwdSmem<D>::bytes(g.m0);
       auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
       set_smem(kern, sm);
-      const int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
+      int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
+      static const int xocc = getenv("TTGPU_FWD_OCC") ? atoi(getenv("TTGPU_FWD_OCC")) : 0;
+      if (xocc > 0) grid = std::min(grid, t->num_sms * xocc);
       kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
                                            f.ntiles.as<int>(), f.rec1.as<uint2>(),
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
