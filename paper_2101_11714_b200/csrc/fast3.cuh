@@ -66,6 +66,17 @@ __device__ __forceinline__ float2 fmul2_rn(float a, float2 b) {
   return r;
 }
 
+// (c.x, c.y) += a * (b.x, b.y), one fma.rn.f32x2 (FFMA2): per lane the same
+// IEEE fma as __fmaf_rn, half the issue slots.
+__device__ __forceinline__ void ffma2(float a, float bx, float by, float& cx, float& cy) {
+  unsigned long long aa, bb, cc, d;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(bx), "f"(by));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(cx), "f"(cy));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(bb), "l"(cc));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(cx), "=f"(cy) : "l"(d));
+}
+
 template <typename T, bool kExact>
 __device__ __forceinline__ float4 madd4(float a, float4 b, float4 acc) {
   if constexpr (kExact) {
@@ -1053,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
 #pragma unroll
         for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
-          for (int j = 0; j < GB::CB; ++j) acc1[i][j] = __fmaf_rn(a[i], b[j], acc1[i][j]);
+          for (int j = 0; j < GB::CB; j += 2) ffma2(a[i], b[j], b[j + 1], acc1[i][j], acc1[i][j + 1]);
       }
     }
     // ---- D0[kappa][r1] = Σ_c S[kappa][c] · G1[r1][c]; thread = (kappa, RB0 r1)
@@ -1078,7 +1089,7 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
           for (int cc = 0; cc < 4; ++cc) {
             const float* gp = G1t + (c + cc) * SM::R1P + rb;
 #pragma unroll
-            for (int i = 0; i < GB::RB0; ++i) dv[q][i] = __fmaf_rn(sv[cc], gp[i], dv[q][i]);
+            for (int i = 0; i < GB::RB0; i += 2) ffma2(sv[cc], gp[i], gp[i + 1], dv[q][i], dv[q][i + 1]);
           }
         }
       }
@@ -1184,14 +1195,13 @@ __global__ void __launch_bounds__(128) f3_bwd2(
           const float a0 = al[i];
 #pragma unroll
           for (int a = 0; a < D::P1; ++a) {
-            const float4 dv = make_float4(__fmul_rn(a0, d[u][a].x), __fmul_rn(a0, d[u][a].y),
-                                          __fmul_rn(a0, d[u][a].z), __fmul_rn(a0, d[u][a].w));
+            const float2 d01 = fmul2_rn(a0, make_float2(d[u][a].x, d[u][a].y));
+            const float2 d23 = fmul2_rn(a0, make_float2(d[u][a].z, d[u][a].w));
+            const float4 dv = make_float4(d01.x, d01.y, d23.x, d23.y);
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-              acc[c].x = __fmaf_rn(h[u][c][a], dv.x, acc[c].x);
-              acc[c].y = __fmaf_rn(h[u][c][a], dv.y, acc[c].y);
-              acc[c].z = __fmaf_rn(h[u][c][a], dv.z, acc[c].z);
-              acc[c].w = __fmaf_rn(h[u][c][a], dv.w, acc[c].w);
+              ffma2(h[u][c][a], dv.x, dv.y, acc[c].x, acc[c].y);
+              ffma2(h[u][c][a], dv.z, dv.w, acc[c].z, acc[c].w);
             }
           }
         }
