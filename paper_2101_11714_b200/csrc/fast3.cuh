@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
                                                uint32_t* __restrict__ hist2,
                                                uint32_t* __restrict__ tot1, uint32_t* __restrict__ tot2,
                                                unsigned long long* __restrict__ bad,
-                                               int* __restrict__ errs) {
+                                               int* __restrict__ errs, int32_t* __restrict__ solo) {
   extern __shared__ uint32_t shist[];  // m1 + m2
   uint32_t* sh1 = shist;
   uint32_t* sh2 = shist + g.m1;
@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
     const double sz = static_cast<double>(e - s);
     for (int64_t l = lo; l < hi; ++l) {
       lk_bag[l] = static_cast<int32_t>(b);
+      solo[l] = e - s == 1 ? static_cast<int32_t>(b) : -1;  // pooled by f3_fwd directly
       double a = w ? w[l] : 1.0;
       if (mean) a /= sz;
       alpha[l] = static_cast<T>(a);
@@ -420,7 +421,8 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
                                             uint32_t* __restrict__ perm, uint32_t* wc,
                                             const uint16_t* __restrict__ dg0 = nullptr,
                                             const uint16_t* __restrict__ dg2 = nullptr,
-                                            uint2* __restrict__ rec = nullptr) {
+                                            const int32_t* __restrict__ solo = nullptr,
+                                            uint4* __restrict__ rec = nullptr) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int per = TL / 8;
@@ -472,8 +474,10 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
       __syncwarp();
       if (k != 0xffffffffu) {
         perm[pos] = static_cast<uint32_t>(l);
-        // sorted record (position -> lookup, i0 | i2 << 16) for f3_fwd
-        if (rec) rec[pos] = make_uint2(static_cast<uint32_t>(l), dg0[l] | (static_cast<uint32_t>(dg2[l]) << 16));
+        // sorted record (position -> lookup, i0 | i2 << 16, solo bag) for f3_fwd
+        if (rec)
+          rec[pos] = make_uint4(static_cast<uint32_t>(l), dg0[l] | (static_cast<uint32_t>(dg2[l]) << 16),
+                                static_cast<uint32_t>(solo[l]), 0u);
         if (lane == __ffs(peers) - 1) my[k] += __popc(peers);
       }
       __syncwarp();
@@ -490,12 +494,13 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
                                                   uint32_t* __restrict__ perm1,
                                                   uint32_t* __restrict__ perm2,
                                                   uint32_t* __restrict__ tot,
-                                                  uint2* __restrict__ rec1) {
+                                                  const int32_t* __restrict__ solo,
+                                                  uint4* __restrict__ rec1) {
   extern __shared__ uint32_t wc[];  // 8 x max(m1, m2)
   // f3_scan has consumed the bucket totals: clear them for the next batch
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.m1 + g.m2; k += gridDim.x * blockDim.x)
     tot[k] = 0u;
-  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc, d0, d2, rec1);
+  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc, d0, d2, solo, rec1);
   scatter_one(d2, g.m2, L, TL, NT, hoff2, perm2, wc);
 }
 
@@ -509,7 +514,7 @@ struct FwdSmem {
   static constexpr int HSP4 = (D::TT * HSP + 3) / 4 * 4;
   static constexpr int S0P = D::S0 + 4;          // bulk-copy rows: 16-byte pitch, 2 slots per warp conflict-free
   static constexpr int S2P = D::S2 + 4;          // lookups' float4 rows in distinct bank groups
-  static constexpr int MI = 2 * D::TT + 4;       // ints per metadata buffer: lk_l, lk_slot, meta
+  static constexpr int MI = 3 * D::TT + 4;       // ints per metadata buffer: lk_l, lk_slot, lk_solo, meta
   static __host__ __device__ size_t floats() {
     size_t f = D::S1 + static_cast<size_t>(HSP4) + static_cast<size_t>(D::TT) * (S0P + S2P);
     return (f + 3) / 4 * 4;
@@ -533,7 +538,9 @@ template <class D, bool kExact>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
                                                    const int* __restrict__ ntiles,
-                                                   const uint2* __restrict__ rec,
+                                                   const uint4* __restrict__ rec,
+                                                   const double* __restrict__ w,
+                                                   float* __restrict__ out,
                                                    float* __restrict__ Hbuf, float* __restrict__ y,
                                                    uint32_t* __restrict__ hloc,
                                                    uint16_t* __restrict__ slot_of_pos,
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   float* G0s = Hs + SM::HSP4;
   float* G2s = G0s + D::TT * SM::S0P;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());  // [0] G1+G0, [1] G2
-  int* mbuf = reinterpret_cast<int*>(bar + 2);                      // 2 x {lk_l, lk_slot, meta}
+  int* mbuf = reinterpret_cast<int*>(bar + 2);                      // 2 x {lk_l, lk_slot, lk_solo, meta}
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
   const float* G2 = cores + g.coff2;
@@ -563,12 +570,13 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   bool g2_act = false;
   int g2_i2 = 0, g2_ntl = 0;
   Tile ndn{}, nd2{};
-  uint2 nrn = make_uint2(0u, 0u);
+  uint4 nrn = make_uint4(0u, 0u, 0u, 0u);
   // slots + metadata of tile u into buffer m, G1/G0 copies onto bar[0]
-  auto stage = [&](int u, const Tile& tl, uint2 r, int m) {
+  auto stage = [&](int u, const Tile& tl, uint4 r, int m) {
     int* lk_l = mbuf + m * SM::MI;
     int* lk_slot = lk_l + D::TT;
-    int* meta = lk_slot + D::TT;
+    int* lk_solo = lk_slot + D::TT;
+    int* meta = lk_solo + D::TT;
     const int ntl = tl.end - tl.start;
     const bool act = lane < ntl;
     const int l = static_cast<int>(r.x), i0 = static_cast<int>(r.y & 0xffffu);
@@ -581,6 +589,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     if (act) {
       lk_l[lane] = l;
       lk_slot[lane] = s;
+      lk_solo[lane] = static_cast<int>(r.z);
       slot_of_pos[tl.start + lane] = static_cast<uint16_t>(s);
       hloc[l] = static_cast<uint32_t>(tl.start + s);
     }
@@ -618,7 +627,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     const Tile tl = tiles[t0];
     if (t0 + G < nt) ndn = tiles[t0 + G];
     if (t0 + 2 * G < nt) nd2 = tiles[t0 + 2 * G];
-    const uint2 r = lane < tl.end - tl.start ? rec[tl.start + lane] : make_uint2(0u, 0u);
+    const uint4 r = lane < tl.end - tl.start ? rec[tl.start + lane] : make_uint4(0u, 0u, 0u, 0u);
     if (t0 + G < nt && lane < ndn.end - ndn.start) nrn = rec[ndn.start + lane];
     stage(t0, tl, r, 0);
     issue_g2();
@@ -628,7 +637,8 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   for (int t = t0; t < nt; t += G, phase ^= 1u, m ^= 1) {
     const int* lk_l = mbuf + m * SM::MI;
     const int* lk_slot = lk_l + D::TT;
-    const int* meta = lk_slot + D::TT;
+    const int* lk_solo = lk_slot + D::TT;
+    const int* meta = lk_solo + D::TT;
     mbar_wait(bar, phase);
     const int ntl = meta[0], nslots = meta[1], start = meta[2];
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
@@ -676,7 +686,14 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
         for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
-        reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
+        const int solo = lk_solo[i];
+        if (solo >= 0) {  // the bag's only lookup: pooled here, as f3_pool would (0 + w·y)
+          const float wl = w ? static_cast<float>(w[lk_l[i]]) : 1.f;
+          reinterpret_cast<float4*>(out + static_cast<int64_t>(solo) * D::N)[a] =
+              madd4<float, kExact>(wl, acc, make_float4(0.f, 0.f, 0.f, 0.f));
+        } else {
+          reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
+        }
       }
     }
     __syncthreads();  // G2s / Hs free
@@ -686,6 +703,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
 
 // ------------------------------------------------------------- f3_pool ---
 // One thread per (bag, float4 column chunk); lookup-ascending accumulation.
+// Bags of exactly one lookup were written by f3_fwd (same arithmetic).
 template <int N, bool kExact>
 __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
                         const double* __restrict__ w, int mean, const float* __restrict__ y,
@@ -696,6 +714,7 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
     const int64_t b = q / Q;
     const int c = static_cast<int>(q - b * Q);
     const int64_t s = off[b], e = off[b + 1];
+    if (e - s == 1) continue;  // single-lookup bag: written by f3_fwd
     const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t l = lo; l < hi; ++l) {

@@ -3,7 +3,7 @@
 namespace ttgpu {
 
 struct F3Bufs {
-  DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, rec1, tiles1, tiles2, tile_base1, tile_base2, ntiles,
+  DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, rec1, solo, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
       group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf;
   f3::Geo geo{};
@@ -48,7 +48,8 @@ void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const
   f3::f3_hist<float, LPT><<<grid, 512, smem, st>>>(
       g, idx, L, NT, off, B, w, pooling, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
       f.d2.as<uint16_t>(), lk_bag, alpha, f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
-      f.tot.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, t->d_bad(), t->d_struct());
+      f.tot.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, t->d_bad(), t->d_struct(),
+      f.solo.as<int32_t>());
 }
 
 template <class K>
@@ -83,7 +84,8 @@ struct F3Runner {
       CK(cudaMemsetAsync(f.tot.p, 0, f.tot.cap, st));
     }
     f.perm1.ensure(4 * L);
-    f.rec1.ensure(8 * L);
+    f.rec1.ensure(16 * L);
+    f.solo.ensure(4 * L);
     f.perm2.ensure(4 * L);
     f.tiles1.ensure(sizeof(f3::Tile) * f.max_tiles1);
     f.tiles2.ensure(sizeof(f3::Tile) * f.max_tiles2);
@@ -132,18 +134,16 @@ struct F3Runner {
                                           f.d2.as<uint16_t>(), L, TL, NT, f.hist1.as<uint32_t>(),
                                           f.hist2.as<uint32_t>(), f.perm1.as<uint32_t>(),
                                           f.perm2.as<uint32_t>(), f.tot.as<uint32_t>(),
-                                          f.rec1.as<uint2>());
+                                          f.solo.as<int32_t>(), f.rec1.as<uint4>());
     }
     t->mark("scatter");
     {
       const size_t sm = f3::FwdSmem<D>::bytes(g.m0);
       auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
       set_smem(kern, sm);
-      int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
-      static const int xocc = getenv("TTGPU_FWD_OCC") ? atoi(getenv("TTGPU_FWD_OCC")) : 0;
-      if (xocc > 0) grid = std::min(grid, t->num_sms * xocc);
+      const int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
       kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
-                                           f.ntiles.as<int>(), f.rec1.as<uint2>(),
+                                           f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out,
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
                                            f.tile_nslots.as<int>());

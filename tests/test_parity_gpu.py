@@ -449,6 +449,31 @@ def test_fast_path_vs_oracle_and_generic(orc, rank, exponent):
         assert scaled_max_err(got.cores[k], got2.cores[k]) <= GRAD_TOL
 
 
+@pytest.mark.parametrize("nlook", [1, 2, 31, 32, 33, 65, 100])
+def test_fast_path_tiny_batches(orc, nlook):
+    """Batches with fewer tiles than CTAs (pipeline prologue only, ragged last
+    tile, one bucket, repeated rows) through the fast path against the oracle."""
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t, cores = make_table(p, np.float32, 32, "tiny", scale=0.3)
+    assert t.fast_path_kind() >= 0
+    rng = np.random.default_rng(nlook)
+    # half the lookups share bucket i1 = 0 (rows < 250), the rest anywhere
+    idx = np.where(rng.random(nlook) < 0.5, rng.integers(0, 250, nlook),
+                   rng.integers(0, p.num_rows, nlook)).astype(np.int64)
+    nb = max(1, nlook // 2)
+    cuts = np.sort(rng.integers(0, nlook + 1, nb - 1))
+    off = np.concatenate([[0], cuts, [nlook]]).astype(np.int64)
+    b = tt.IndexBatch(idx, off)
+    g = rng.standard_normal((nb, 16)).astype(np.float32)
+    op = as_oplan(p)
+    res = tt.forward_bags(t, b)
+    assert np.array_equal(res.output, orc.forward(op, cores, idx, off))
+    got = tt.backward_bags(t, b, res.context, g)
+    want = orc.backward(op, cores, idx, off, g)
+    for k in range(3):
+        assert scaled_max_err(got.cores[k], want[k]) <= GRAD_TOL
+
+
 def test_fast_path_fused_sgd_equals_dense_then_sgd():
     p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
     a, cores = make_table(p, np.float32, 9, "a", scale=0.3)
