@@ -48,8 +48,11 @@ def main():
             e["l2_bytes"] = mean["lts__t_bytes.sum"]
         if "sm__sass_thread_inst_executed_op_ffma_pred_on.sum" in mean:
             e["ffma_thread_inst"] = mean["sm__sass_thread_inst_executed_op_ffma_pred_on.sum"]
+            # FFMA2 (fma.rn.f32x2) is counted separately: 2 lanes x 2 flops
+            e["ffma2_thread_inst"] = mean.get("sm__sass_thread_inst_executed_op_ffma2_pred_on.sum", 0.0)
             if "us" in e:
-                e["executed_ffma_tflops"] = 2 * e["ffma_thread_inst"] / (e["us"] * 1e-6) / 1e12
+                fl = 2 * e["ffma_thread_inst"] + 4 * e["ffma2_thread_inst"]
+                e["executed_ffma_tflops"] = fl / (e["us"] * 1e-6) / 1e12
         res[name] = e
     for n, e in sorted(res.items(), key=lambda x: -x[1].get("us", 0)):
         print(f"{n:16s} " + " ".join(f"{k}={v:.4g}" for k, v in e.items()))
