@@ -1011,7 +1011,15 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     if (lane < n_ns)
       tma_load(G0s + lane * D::S0, G0 + static_cast<int64_t>(n_i0) * D::S0, D::S0 * 4, bar + st);
   };
+  // descriptor of the tile after the one being fetched (loaded a tile early,
+  // so the dependent slot-i0 load of a fetch never waits on it)
+  Tile q_d{};
+  int q_ns = 0;
   if (wid == 0) {
+    if (t_lo + 2 < t_hi) {
+      q_d = tiles[t_lo + 2];
+      q_ns = tile_nslots[t_lo + 2];
+    }
     if (t_lo < t_hi) {
       fetch(t_lo);
       issue(0);
@@ -1039,7 +1047,15 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     const int i1 = misc[2 * st], nslots = misc[2 * st + 1];
     const int nk = nslots * D::P0;
     const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * (st ^ 1)] : -1;
-    if (wid == 0 && t + 2 < t_hi) fetch(t + 2);  // in flight during this tile's GEMMs
+    if (wid == 0 && t + 2 < t_hi) {  // tile t+2's slot i0s in flight during this tile's GEMMs
+      n_d = q_d;
+      n_ns = q_ns;
+      n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
+      if (t + 3 < t_hi) {
+        q_d = tiles[t + 3];
+        q_ns = tile_nslots[t + 3];
+      }
+    }
     if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
       constexpr int U = 8;
