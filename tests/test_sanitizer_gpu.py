@@ -1,4 +1,4 @@
-"""GPU: compute-sanitizer racecheck + memcheck over one fast-path and one
+"""GPU: compute-sanitizer racecheck + memcheck + synccheck over one fast-path and one
 generic-path fwd+bwd+SGD step (the reference's determinism tests act as race
 canaries; on the GPU we check for races directly)."""
 import os
@@ -73,7 +73,7 @@ def _sanitizer():
     pytest.skip("compute-sanitizer not found")
 
 
-@pytest.mark.parametrize("tool", ["racecheck", "memcheck"])
+@pytest.mark.parametrize("tool", ["racecheck", "memcheck", "synccheck"])
 def test_sanitizer_clean(tool, tmp_path):
     script = tmp_path / "step.py"
     script.write_text(SCRIPT)
