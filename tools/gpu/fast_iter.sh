@@ -1,3 +1,4 @@
+# Fast-path iteration on the GPU box: the parity suite, cfg2 and cfg2u bench lines (phase times), ncu launch list.
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_parity_gpu.py -x -q > gpurun_out/pt_iter.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pt_iter.log
 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_iter.log 2>&1; echo "bench rc=$?"; python -c "
