@@ -953,8 +953,19 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     __shared__ int range[2];
     const int per = (nt + kThreads - 1) / kThreads;
     const int a0 = min(nt, tid * per), a1 = min(nt, a0 + per);
+    // up to kPer weights per thread are loaded all at once (independent loads,
+    // one round trip) and kept in registers for the threshold walk
+    constexpr int kPer = 16;
+    int wv[kPer];
     int wsum = 0;
-    for (int t = a0; t < a1; ++t) wsum += kTileCost + tile_nslots[t];
+    if (per <= kPer) {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) wv[j] = a0 + j < a1 ? kTileCost + tile_nslots[a0 + j] : 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) wsum += wv[j];
+    } else {
+      for (int t = a0; t < a1; ++t) wsum += kTileCost + tile_nslots[t];
+    }
     int ex, W;
     Scan(scan_tmp).ExclusiveSum(wsum, ex, W);
     // owner(t) == b  <=>  E(t) in [ceil(b W / G), ceil((b+1) W / G)): the range
@@ -969,7 +980,16 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
       if (ex < th[q] && th[q] <= ex + wsum) {
         int64_t e = ex;
         int t = a0;
-        for (; t < a1 && e < th[q]; ++t) e += kTileCost + tile_nslots[t];
+        if (per <= kPer) {
+#pragma unroll
+          for (int j = 0; j < kPer; ++j)
+            if (t < a1 && e < th[q]) {
+              e += wv[j];
+              ++t;
+            }
+        } else {
+          for (; t < a1 && e < th[q]; ++t) e += kTileCost + tile_nslots[t];
+        }
         range[q] = t;
       }
     }
