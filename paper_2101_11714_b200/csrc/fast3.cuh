@@ -907,18 +907,21 @@ struct G1Blk {
   static_assert(D::C1 % CB == 0 && D::R1 % RB == 0 && CB % 4 == 0, "bad blocking");
 };
 
+constexpr int kBwd1Stages = 2;  // tiles of bulk copies in flight per f3_bwd1 CTA (3: 2 CTAs/SM, slower)
+
 template <class D>
 struct Bwd1Smem {
-  // floats: 2 stages x { S[TT*P0 x C1] (TMA) | G0s[TT*P0 x R1] (TMA) } | G1t[C1 x R1P] ;
-  // then 2 mbarriers, ints
+  // floats: NS stages x { S[TT*P0 x C1] (TMA) | G0s[TT*P0 x R1] (TMA) } | G1t[C1 x R1P] ;
+  // then NS mbarriers, ints
+  static constexpr int NS = kBwd1Stages;
   static constexpr int R1P = D::R1 + 4;
   static constexpr int STAGE = D::TT * D::W1 + D::TT * D::S0;  // floats per stage
-  static constexpr int NI = 3 * D::TT + 16 + 256;  // 2 x slot i0 / first-touch flags / misc / bitmap
+  static constexpr int NI = (NS + 1) * D::TT + 16 + 256;  // NS x slot i0 / first-touch flags / misc / bitmap
   static __host__ __device__ size_t floats() {
-    size_t f = 2 * static_cast<size_t>(STAGE) + static_cast<size_t>(D::C1) * R1P;
+    size_t f = NS * static_cast<size_t>(STAGE) + static_cast<size_t>(D::C1) * R1P;
     return (f + 3) / 4 * 4;
   }
-  static __host__ __device__ size_t bytes() { return floats() * 4 + 16 + sizeof(int) * NI; }
+  static __host__ __device__ size_t bytes() { return floats() * 4 + 8 * NS + sizeof(int) * NI; }
 };
 
 template <class D>
@@ -931,11 +934,12 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
   extern __shared__ __align__(128) float sm[];
-  float* G1t = sm + 2 * SM::STAGE;                 // [c][R1P]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());  // 2 stages
-  int* slot_i0 = reinterpret_cast<int*>(bar + 2);  // 2 x TT
-  int* d0first = slot_i0 + 2 * D::TT;              // TT
-  int* misc = d0first + D::TT;                     // [2*stage + 0] key, [2*stage + 1] nslots
+  constexpr int NS = SM::NS;
+  float* G1t = sm + NS * SM::STAGE;                // [c][R1P]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());  // NS stages
+  int* slot_i0 = reinterpret_cast<int*>(bar + NS);  // NS x TT
+  int* d0first = slot_i0 + NS * D::TT;              // TT
+  int* misc = d0first + D::TT;                      // [2*stage + 0] key, [2*stage + 1] nslots
   unsigned* d0bits = reinterpret_cast<unsigned*>(misc + 16);
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
@@ -1001,13 +1005,11 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
   for (int e = tid; e < 256; e += kThreads) d0bits[e] = 0u;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-  }
+  if (tid == 0)
+    for (int q = 0; q < NS; ++q) mbar_init(bar + q, 1);
   __syncthreads();
-  // warp 0 keeps two tiles of bulk copies in flight: the descriptors of tile
-  // t+2 are fetched during tile t, its S rows (one copy) and G0 rows (one per
+  // warp 0 keeps NS tiles of bulk copies in flight: the descriptors of tile
+  // t+NS are fetched during tile t, its S rows (one copy) and G0 rows (one per
   // slot) are issued into tile t's stage as soon as tile t's GEMMs are done
   Tile n_d{};
   int n_ns = 0, n_i0 = 0;
@@ -1036,17 +1038,13 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
   Tile q_d{};
   int q_ns = 0;
   if (wid == 0) {
-    if (t_lo + 2 < t_hi) {
-      q_d = tiles[t_lo + 2];
-      q_ns = tile_nslots[t_lo + 2];
+    if (t_lo + NS < t_hi) {
+      q_d = tiles[t_lo + NS];
+      q_ns = tile_nslots[t_lo + NS];
     }
-    if (t_lo < t_hi) {
-      fetch(t_lo);
-      issue(0);
-    }
-    if (t_lo + 1 < t_hi) {
-      fetch(t_lo + 1);
-      issue(1);
+    for (int q = 0; q < NS && t_lo + q < t_hi; ++q) {
+      fetch(t_lo + q);
+      issue(q);
     }
   }
   const int r0 = (tid % GB::TR) * GB::RB, cb0 = (tid / GB::TR) * GB::CB;
@@ -1058,22 +1056,22 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
   int run_start = t_lo, cur_i1 = -1;
   for (int t = t_lo; t < t_hi; ++t) {
-    const int st = (t - t_lo) & 1;
-    const uint32_t parity = static_cast<uint32_t>(((t - t_lo) >> 1) & 1);
+    const int st = (t - t_lo) % NS;
+    const uint32_t parity = static_cast<uint32_t>(((t - t_lo) / NS) & 1);
     const float* Ss = sm + st * SM::STAGE;
     const float* G0s = Ss + D::TT * D::W1;
     const int* si0 = slot_i0 + st * D::TT;
     __syncthreads();  // misc / slot_i0 of tile t published
     const int i1 = misc[2 * st], nslots = misc[2 * st + 1];
     const int nk = nslots * D::P0;
-    const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * (st ^ 1)] : -1;
-    if (wid == 0 && t + 2 < t_hi) {  // tile t+2's slot i0s in flight during this tile's GEMMs
+    const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * ((st + 1) % NS)] : -1;
+    if (wid == 0 && t + NS < t_hi) {  // tile t+NS's slot i0s in flight during this tile's GEMMs
       n_d = q_d;
       n_ns = q_ns;
       n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
-      if (t + 3 < t_hi) {
-        q_d = tiles[t + 3];
-        q_ns = tile_nslots[t + 3];
+      if (t + NS + 1 < t_hi) {
+        q_d = tiles[t + NS + 1];
+        q_ns = tile_nslots[t + NS + 1];
       }
     }
     if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
@@ -1150,7 +1148,7 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
       }
     }
     __syncthreads();  // stage st / slot lists consumed
-    if (wid == 0 && t + 2 < t_hi) issue(st);
+    if (wid == 0 && t + NS < t_hi) issue(st);
     // ---- D0 into the CTA block (slots of one tile have distinct i0)
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
