@@ -155,9 +155,11 @@ def make_inputs(cfg, seed, tt):
     return idx, off, g.astype(np.float32)
 
 
-def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0):
+def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0, steps=None, warmup=0):
     """The reference's own OpenMP CPU step (oracle/_ref, compiled from the
-    reference sources) on this host's cores; falls back to the C restatement."""
+    reference sources) on this host's cores; falls back to the C restatement.
+    steps=None: as many steps as fit budget_s (3..50); else exactly `steps`
+    timed steps after `warmup` untimed ones."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
 
@@ -169,8 +171,13 @@ def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0):
         ref = pyoracle.RefImpl()
         t = ref.table(plan, np.float32, "cpu")
         t.init_sampled_gaussian(1)
-        first = t.time_step(idx, off, grad, LR, reps=1, threads=threads)
-        reps = int(max(3, min(50, budget_s / max(first, 1e-6))))
+        if steps is None:
+            first = t.time_step(idx, off, grad, LR, reps=1, threads=threads)
+            reps = int(max(3, min(50, budget_s / max(first, 1e-6))))
+        else:
+            if warmup > 0:
+                t.time_step(idx, off, grad, LR, reps=warmup, threads=threads)
+            reps = max(1, int(steps))
         sec = t.time_step(idx, off, grad, LR, reps=reps, threads=threads)
         kind = "reference"
     else:
@@ -178,8 +185,11 @@ def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0):
         rng = np.random.default_rng(0)
         cores = [rng.standard_normal(plan.core_size(k)).astype(np.float32) * 0.3
                  for k in range(plan.tt_dim)]
-        ts = [orc.time_step(plan, cores, idx, off, grad, LR, threads) for _ in range(3)]
-        sec, reps, kind = float(np.median(ts)), 3, "port"
+        reps = 3 if steps is None else max(1, int(steps))
+        for _ in range(warmup if steps is not None else 0):
+            orc.time_step(plan, cores, idx, off, grad, LR, threads)
+        ts = [orc.time_step(plan, cores, idx, off, grad, LR, threads) for _ in range(reps)]
+        sec, kind = float(np.median(ts)), "port"
     return {"value": L / sec, "unit": "indices/s", "cores": threads, "kind": kind,
             "sample": f"{L} lookups ({cfg['bags']} bags x {cfg['pf']}), median of {reps} steps "
                       f"(fwd save + bwd + sgd, fp32, OMP threads={threads})",
@@ -192,11 +202,9 @@ def run_reference(args, cfg, rank):
     import paper_2101_11714_b200 as tt  # host-only helpers: the reference's own streams
 
     idx, off, grad = make_inputs(cfg, 7, tt)
-    times = []
-    for _ in range(max(1, args.warmup)):
-        cpu_reference_time(cfg, idx, off, grad, budget_s=1.0)
-    base = cpu_reference_time(cfg, idx, off, grad, budget_s=10.0)
-    times.append(base["ms_per_step"])
+    # W untimed + K timed full-batch steps on all host threads (each step is one
+    # reference fwd(save) + bwd + sgd over the whole batch)
+    base = cpu_reference_time(cfg, idx, off, grad, steps=args.steps, warmup=args.warmup)
     v = base["value"]
     line = {"metric": METRIC, "value": v, "unit": "indices/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["ms_per_step"],
