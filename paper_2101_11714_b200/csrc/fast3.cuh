@@ -201,6 +201,13 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
   extern __shared__ uint32_t shist[];  // m1 + m2
   uint32_t* sh1 = shist;
   uint32_t* sh2 = shist + g.m1;
+  // this thread's first bag's offsets: loaded now, in flight during the digit phase
+  const int64_t b_first = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t s_first = 0, e_first = 0;
+  if (b_first < B) {
+    s_first = off[b_first];
+    e_first = off[b_first + 1];
+  }
   for (int k = threadIdx.x; k < g.m1 + g.m2; k += blockDim.x) shist[k] = 0;
   __syncthreads();
   const int tile = blockIdx.x;
@@ -254,9 +261,8 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
     }
   }
   // bags (grid-stride over all CTAs): offsets checks, lookup->bag, backward alpha
-  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < B;
-       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = off[b], e = off[b + 1];
+  for (int64_t b = b_first; b < B; b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = b == b_first ? s_first : off[b], e = b == b_first ? e_first : off[b + 1];
     if (b == 0 && s != 0) atomicOr(errs, 1);
     if (e < s) atomicOr(errs, 2);
     if (b == B - 1 && e != L) atomicOr(errs, 4);
