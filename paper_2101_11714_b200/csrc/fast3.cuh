@@ -325,6 +325,11 @@ __global__ void __launch_bounds__(kScanThreads) f3_scan(ScanArgs a1, ScanArgs a2
   const int K = A.K, TT = A.TT;
   const int k0 = blk * kScanKeys, k1 = min(K, k0 + kScanKeys);
   const int tid = threadIdx.x;
+  // this CTA's histogram columns: loads issued first, in flight during the bases
+  const int n = (k1 - k0) * NT;
+  uint32_t* hist = A.hist + static_cast<int64_t>(k0) * NT;
+#pragma unroll 4
+  for (int i = tid; i < n; i += kScanThreads) sh[spad(i)] = hist[i];
   // global bases: all keys before k0
   uint32_t p = 0, t = 0, gq = 0;
   for (int k = tid; k < k0; k += kScanThreads) {
@@ -374,10 +379,6 @@ __global__ void __launch_bounds__(kScanThreads) f3_scan(ScanArgs a1, ScanArgs a2
     }
   }
   // this CTA's histogram columns -> absolute scatter offsets
-  const int n = (k1 - k0) * NT;
-  uint32_t* hist = A.hist + static_cast<int64_t>(k0) * NT;
-#pragma unroll 4
-  for (int i = tid; i < n; i += kScanThreads) sh[spad(i)] = hist[i];
   __syncthreads();
   const int per = (n + kScanThreads - 1) / kScanThreads;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
