@@ -435,6 +435,14 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
   const int per = TL / 8;
   const int64_t base = static_cast<int64_t>(tile) * TL + static_cast<int64_t>(wid) * per;
   uint32_t* my = wc + static_cast<int64_t>(wid) * K;
+  // this CTA's scatter bases (f3_scan) for the first 4 * 256 keys: loads in
+  // flight during the counting phase
+  uint32_t hpre[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = threadIdx.x + j * 256;
+    hpre[j] = k < K ? hoff[static_cast<int64_t>(k) * NT + tile] : 0u;
+  }
   for (int k = lane; k < K; k += 32) my[k] = 0;
   __syncwarp();
   for (int r0 = 0; r0 < per; r0 += 256) {
@@ -453,15 +461,18 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    uint32_t run = hoff[static_cast<int64_t>(k) * NT + tile];
+  auto bases = [&](int k, uint32_t run) {  // per-warp starts of key k
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
       const uint32_t c = wc[static_cast<int64_t>(w) * K + k];
       wc[static_cast<int64_t>(w) * K + k] = run;
       run += c;
     }
-  }
+  };
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (threadIdx.x + j * 256 < K) bases(threadIdx.x + j * 256, hpre[j]);
+  for (int k = threadIdx.x + 1024; k < K; k += 256) bases(k, hoff[static_cast<int64_t>(k) * NT + tile]);
   __syncthreads();
   const unsigned lt = lanemask_lt();
   for (int r0 = 0; r0 < per; r0 += 256) {
