@@ -1231,15 +1231,20 @@ __global__ void __launch_bounds__(128) f3_bwd2(
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   int run_start = t_lo;
+  // the next tile's descriptor (loaded during this tile) and its lookups
+  // (loaded after this tile's loads): only the last hop is exposed per tile
+  Tile nx{};
+  int nl = 0;
   for (int t = t_lo; t < t_hi; ++t) {
-    const Tile tl = tiles[t];
+    const Tile tl = t == t_lo ? tiles[t] : nx;
     const int ntl = tl.end - tl.start;
     if (tid < ntl) {
-      const int l = static_cast<int>(perm[tl.start + tid]);
+      const int l = t == t_lo ? static_cast<int>(perm[tl.start + tid]) : nl;
       hl[tid] = static_cast<int>(hloc[l]);
       bg[tid] = lk_bag[l];
       al[tid] = alpha[l];
     }
+    if (t + 1 < t_hi) nx = tiles[t + 1];
     __syncthreads();
     for (int i0 = wid * U; i0 < ntl; i0 += NW * U) {
       float4 d[U][D::P1];
@@ -1278,7 +1283,8 @@ __global__ void __launch_bounds__(128) f3_bwd2(
         }
       }
     }
-    const bool last = (t + 1 == t_hi) || (tiles[t + 1].key != tl.key);
+    if (t + 1 < t_hi && tid < nx.end - nx.start) nl = static_cast<int>(perm[nx.start + tid]);
+    const bool last = (t + 1 == t_hi) || (nx.key != tl.key);
     if (tid == 0) has2[t] = (t == run_start) ? 1 : 0;
     if (last) {
 #pragma unroll
