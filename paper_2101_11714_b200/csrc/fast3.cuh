@@ -1425,7 +1425,7 @@ __device__ __forceinline__ int find_slice(const int32_t* base, int K, int x) {
 }
 
 template <class D, int MODE>
-__global__ void __launch_bounds__(kThreads) f3_combine(Geo g, float* __restrict__ cores,
+__global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restrict__ cores,
                                                        float* __restrict__ grads, CombineArgs A,
                                                        float lr) {
   const int lane = threadIdx.x & 31;
