@@ -52,31 +52,8 @@ struct Dims {
 
 constexpr int kThreads = 256;
 
-// acc += a * b per component.  Exact: separately rounded products and sums
-// (the reference's fp32 loop), products two at a time (mul.rn.f32x2 = FMUL2,
-// same IEEE result as two FMULs) and scalar adds.  (The adds stay scalar:
-// ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2.)
-__device__ __forceinline__ float2 fmul2_rn(float a, float2 b) {
-  unsigned long long aa, bb, m;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(aa), "l"(bb));
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(m));
-  return r;
-}
-
-// (c.x, c.y) += a * (b.x, b.y), one fma.rn.f32x2 (FFMA2): per lane the same
-// IEEE fma as __fmaf_rn, half the issue slots.
-__device__ __forceinline__ void ffma2(float a, float bx, float by, float& cx, float& cy) {
-  unsigned long long aa, bb, cc, d;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(bx), "f"(by));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(cx), "f"(cy));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(bb), "l"(cc));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(cx), "=f"(cy) : "l"(d));
-}
-
+// acc += a * b per component (fmul2_rn / ffma2: tt_kernels.cuh).  Exact: separately
+// rounded products and sums (the reference's fp32 loop), products two at a time.
 template <typename T, bool kExact>
 __device__ __forceinline__ float4 madd4(float a, float4 b, float4 acc) {
   if constexpr (kExact) {

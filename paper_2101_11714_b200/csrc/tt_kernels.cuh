@@ -48,6 +48,30 @@ struct DevPlan {
 };
 
 // ---------------------------------------------------------------- helpers --
+// Packed fp32 pairs (sm_100a).  fmul2_rn: mul.rn.f32x2 = FMUL2, the same IEEE
+// products as two FMULs; exact sums stay scalar (ptxas contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2, which would not be bit-exact).
+__device__ __forceinline__ float2 fmul2_rn(float a, float2 b) {
+  unsigned long long aa, bb, m;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(aa), "l"(bb));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(m));
+  return r;
+}
+
+// (c.x, c.y) += a * (b.x, b.y), one fma.rn.f32x2 (FFMA2): per lane the same
+// IEEE fma as __fmaf_rn, half the issue slots.
+__device__ __forceinline__ void ffma2(float a, float bx, float by, float& cx, float& cy) {
+  unsigned long long aa, bb, cc, d;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(bx), "f"(by));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(cx), "f"(cy));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(aa), "l"(bb), "l"(cc));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(cx), "=f"(cy) : "l"(d));
+}
+
 template <typename T, bool kExact>
 __device__ __forceinline__ T madd(T a, T b, T acc);
 template <>
@@ -695,7 +719,10 @@ __global__ void k_inv_perm(const uint32_t* __restrict__ sorted_lk, int64_t L,
 
 // MODE 0: y[l][a*n2 + j] = Σ_r H[a][r] · G2[i2][r][j] (forward, kExact rounding)
 // MODE 1: C[pos2[l]][q*n2 + j] = Σ_a H[a][q] · D2[a][j]   (dG2 contribution)
-template <typename T, int MODE, bool kExact>
+// PAIR (float, even n2): a thread owns two adjacent output columns (j, j+1)
+// and forms their products two at a time (FMUL2 / FFMA2), same per-element
+// arithmetic and order as the scalar form.
+template <typename T, int MODE, bool kExact, bool PAIR = false>
 __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restrict__ cores,
                                                    const T* __restrict__ H,
                                                    const int32_t* __restrict__ lk_pid,
@@ -714,15 +741,16 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
   // hs[a][r] for 8 different a at once, which would share one bank otherwise
   const int R2p = R2 + 1;
   T* hs = reinterpret_cast<T*>(smem_raw);        // P1 x R2p (current pair's H row)
-  T* xs = hs + P1 * R2p;                         // C x XW
+  T* xs = hs + (P1 * R2p + 3) / 4 * 4;           // C x XW, 16-byte aligned for the vector stores
   __shared__ int cur_pid;
   __shared__ int pids[64];                       // pair of each chunk position (C <= 64)
   __shared__ int qlk[64], qrow[64];              // lookup, G2 slice (MODE 0) / bag (MODE 1)
   __shared__ T qal[64];
   const int64_t nchunks = (L + C - 1) / C;
-  const int per = blockDim.x / OW > 0 ? blockDim.x / OW : 1;  // lookups in flight
-  const int e = threadIdx.x % OW, slot = threadIdx.x / OW;
-  const bool on_e = threadIdx.x < per * OW;
+  const int OWt = PAIR ? OW / 2 : OW;  // threads per lookup
+  const int per = blockDim.x / OWt > 0 ? blockDim.x / OWt : 1;  // lookups in flight
+  const int e = (threadIdx.x % OWt) * (PAIR ? 2 : 1), slot = threadIdx.x / OWt;
+  const bool on_e = threadIdx.x < per * OWt;
   // element -> operand offsets (hoisted)
   const int ra = MODE == 0 ? (e / n2) * R2p : e / n2;  // MODE0: a*R2p  MODE1: q
   const int rj = e % n2;
@@ -778,13 +806,37 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
         for (int q = q0 + slot; q < q1; q += per) {
           const int64_t l = qlk[q];
           const T* x = xs + q * XW;
-          T v = T(0);
-          if (MODE == 0) {
-            for (int r = 0; r < R2; ++r) v = madd<T, kExact>(hs[ra + r], x[r * n2 + rj], v);
-            out[l * N + e] = v;
+          if constexpr (PAIR) {
+            float v0 = 0.f, v1 = 0.f;
+            if (MODE == 0) {
+              for (int r = 0; r < R2; ++r) {
+                const float2 xv = *reinterpret_cast<const float2*>(x + r * n2 + rj);
+                if (kExact) {
+                  const float2 pr = fmul2_rn(hs[ra + r], xv);
+                  v0 = __fadd_rn(v0, pr.x);
+                  v1 = __fadd_rn(v1, pr.y);
+                } else {
+                  ffma2(hs[ra + r], xv.x, xv.y, v0, v1);
+                }
+              }
+              *reinterpret_cast<float2*>(out + l * N + e) = make_float2(v0, v1);
+            } else {
+              for (int i = 0; i < P1; ++i) {
+                const float2 xv = *reinterpret_cast<const float2*>(x + i * n2 + rj);
+                ffma2(hs[i * R2p + ra], xv.x, xv.y, v0, v1);
+              }
+              *reinterpret_cast<float2*>(out + static_cast<int64_t>(pos2[l]) * S2 + e) =
+                  make_float2(v0, v1);
+            }
           } else {
-            for (int i = 0; i < P1; ++i) v = madd<T, false>(hs[i * R2p + ra], x[i * n2 + rj], v);
-            out[static_cast<int64_t>(pos2[l]) * S2 + e] = v;
+            T v = T(0);
+            if (MODE == 0) {
+              for (int r = 0; r < R2; ++r) v = madd<T, kExact>(hs[ra + r], x[r * n2 + rj], v);
+              out[l * N + e] = v;
+            } else {
+              for (int i = 0; i < P1; ++i) v = madd<T, false>(hs[i * R2p + ra], x[i * n2 + rj], v);
+              out[static_cast<int64_t>(pos2[l]) * S2 + e] = v;
+            }
           }
         }
       }

@@ -462,13 +462,15 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
   t->mark("head_fwd");
   // d == 3 with wide rows: y per lookup walked in pair order (H staged once per
   // pair run), then pooling in lookup order
-  if (d == 3 && sizeof(T) * (P.W1 + P.prefix[1] + static_cast<size_t>(kTailChunk) * P.slice[2]) <=
+  if (d == 3 && sizeof(T) * (P.W1 + P.prefix[1] + 4 + static_cast<size_t>(kTailChunk) * P.slice[2]) <=
                     96 * 1024 &&
       P.W1 >= 32) {
     c->ybuf.ensure(sizeof(T) * L * P.N);
     const size_t smem =
-        sizeof(T) * (P.W1 + P.prefix[1] + static_cast<size_t>(kTailChunk) * P.slice[2]);
-    auto kern = exact ? k_pairwalk3<T, 0, true> : k_pairwalk3<T, 0, false>;
+        sizeof(T) * (P.W1 + P.prefix[1] + 4 + static_cast<size_t>(kTailChunk) * P.slice[2]);
+    const bool pair = std::is_same_v<T, float> && P.n[2] % 2 == 0;
+    auto kern = pair ? (exact ? k_pairwalk3<T, 0, true, true> : k_pairwalk3<T, 0, false, true>)
+                     : (exact ? k_pairwalk3<T, 0, true> : k_pairwalk3<T, 0, false>);
     set_smem(kern, smem);
     kern<<<grid_for((L + kTailChunk - 1) / kTailChunk, 1, t->num_sms, 8), 256, smem, st>>>(
         P, t->cores.as<T>(), c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
@@ -620,9 +622,12 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
       c->pos2.ensure(4 * L);
       c->tcontrib.ensure(sizeof(T) * L * Wc);
       k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>() + j * L, L, c->pos2.as<uint32_t>());
-      const size_t smem = sizeof(T) * (P.W1 + P.prefix[1] + static_cast<size_t>(kTailChunk) * P.N);
-      set_smem(k_pairwalk3<T, 1, false>, smem);
-      k_pairwalk3<T, 1, false><<<grid_for(nchunksL, 1, t->num_sms, 8), 256, smem, st>>>(
+      const size_t smem =
+          sizeof(T) * (P.W1 + P.prefix[1] + 4 + static_cast<size_t>(kTailChunk) * P.N);
+      auto kern1 = std::is_same_v<T, float> && P.n[2] % 2 == 0 ? k_pairwalk3<T, 1, false, true>
+                                                                : k_pairwalk3<T, 1, false>;
+      set_smem(kern1, smem);
+      kern1<<<grid_for(nchunksL, 1, t->num_sms, 8), 256, smem, st>>>(
           P, cores, c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
           c->lk_bag.as<int32_t>(), c->lk_alpha.as<T>(), grad, c->s_lk.as<uint32_t>(),
           c->pos2.as<uint32_t>(), L, kTailChunk, c->tcontrib.as<T>());
