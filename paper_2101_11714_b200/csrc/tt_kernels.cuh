@@ -513,6 +513,7 @@ __global__ void k_chunk_reduce(DevPlan P, const T* __restrict__ cores, const T* 
 // D2 = T(alpha) * grad[bag] (bwd_chain), products accumulated from zero with
 // FMA in the same order as warp_mm_abt / the MODE 1 loop of k_chunk_reduce.
 constexpr int kRun3MaxEPT = 8;   // output elements per thread (row width <= 8 x 256)
+constexpr int kQuadPT = 2;       // k_srun3 fp32 quad path: column quads per thread
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ cores,
@@ -533,6 +534,11 @@ __global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ 
   __shared__ T qal[64];
   const T* G2 = cores + P.coff[2];
   const int64_t nchunks = (L + C - 1) / C;
+  // quad path (fp32, n2 == 4): a thread owns quads (a, r..r+3); G2 slices are
+  // staged transposed ([j][r]) so a quad's 4 columns are one 16-byte load, and
+  // the products go two lanes at a time (FFMA2).  Per element the same fma
+  // chain over j, then acc += v, as the scalar form.
+  const bool quad = std::is_same_v<T, float> && n2 == 4 && (R2 & 3) == 0 && W <= 4 * kQuadPT * 256;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t c0 = ch * C;
     const int n = static_cast<int>(L - c0 < C ? L - c0 : C);
@@ -551,7 +557,18 @@ __global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ 
       d2s[e] = mul_rn<T>(qal[q], grad[static_cast<int64_t>(qbag[q]) * N + j]);
     }
     if constexpr (std::is_same_v<T, float>) {
-      if ((S2 & 3) == 0) {
+      if (quad) {  // row r of slice i2 -> column r of the [j][r] block
+        for (int e = threadIdx.x; e < n * R2; e += blockDim.x) {
+          const int q = e / R2, r = e - q * R2;
+          const float4 v =
+              __ldg(reinterpret_cast<const float4*>(G2 + static_cast<int64_t>(qi2[q]) * S2) + r);
+          float* gt = reinterpret_cast<float*>(g2s) + q * S2 + r;
+          gt[0] = v.x;
+          gt[R2] = v.y;
+          gt[2 * R2] = v.z;
+          gt[3 * R2] = v.w;
+        }
+      } else if ((S2 & 3) == 0) {
         const int S4 = S2 >> 2;
         for (int e = threadIdx.x; e < n * S4; e += blockDim.x) {
           const int q = e / S4, j = e - q * S4;
@@ -572,6 +589,59 @@ __global__ void __launch_bounds__(256) k_srun3(DevPlan P, const T* __restrict__ 
     }
     __syncthreads();
     const int run0 = static_cast<int>(scan[c0] >> 32) - 1;
+    if constexpr (std::is_same_v<T, float>) {
+      if (quad) {
+        const int R4 = R2 >> 2, NQ = W >> 2;
+        float4 qa[kQuadPT];
+        int doff[kQuadPT], goff[kQuadPT], ooff[kQuadPT];
+#pragma unroll
+        for (int k = 0; k < kQuadPT; ++k) {
+          qa[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          const int g = threadIdx.x + k * blockDim.x;
+          const int a = g / R4, r4 = g - a * R4;
+          doff[k] = a * 4;
+          goff[k] = r4 * 4;
+          ooff[k] = a * R2 + r4 * 4;
+        }
+        int run = run0;
+        for (int q = 0; q < n; ++q) {
+          if (q > 0 && keys[q] != keys[q - 1]) {
+#pragma unroll
+            for (int k = 0; k < kQuadPT; ++k) {
+              if (threadIdx.x + k * blockDim.x < NQ)
+                *reinterpret_cast<float4*>(partials + static_cast<int64_t>(run) * W + ooff[k]) = qa[k];
+              qa[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            ++run;
+          }
+          const float* d = reinterpret_cast<const float*>(d2s) + q * N;
+          const float* gt = reinterpret_cast<const float*>(g2s) + q * S2;
+#pragma unroll
+          for (int k = 0; k < kQuadPT; ++k) {
+            if (threadIdx.x + k * blockDim.x < NQ) {
+              const float4 dv = *reinterpret_cast<const float4*>(d + doff[k]);
+              const float dj[4] = {dv.x, dv.y, dv.z, dv.w};
+              float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 gv = *reinterpret_cast<const float4*>(gt + j * R2 + goff[k]);
+                ffma2(dj[j], gv.x, gv.y, v0, v1);
+                ffma2(dj[j], gv.z, gv.w, v2, v3);
+              }
+              qa[k].x += v0;
+              qa[k].y += v1;
+              qa[k].z += v2;
+              qa[k].w += v3;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kQuadPT; ++k)
+          if (threadIdx.x + k * blockDim.x < NQ)
+            *reinterpret_cast<float4*>(partials + static_cast<int64_t>(run) * W + ooff[k]) = qa[k];
+        continue;
+      }
+    }
     T acc[kRun3MaxEPT];
     int aoff[kRun3MaxEPT], roff[kRun3MaxEPT];  // element -> (a*n2, r*n2), hoisted
 #pragma unroll
