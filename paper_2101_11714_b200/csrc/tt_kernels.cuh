@@ -1000,9 +1000,9 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
   // C1 a multiple of 32 put every lane of a warp in the same bank)
   const int R1p = R1 + 1;
   T* g1t = reinterpret_cast<T*>(smem_raw);              // C1 x R1p
-  T* acc = g1t + static_cast<int64_t>(C1) * R1p;        // R1 x C1
-  T* sps = acc + s1;                                    // P0 x C1: S row of the pair
+  T* sps = g1t + static_cast<int64_t>(C1) * R1p;        // P0 x C1: S row of the pair
   T* g0s = sps + P.W1;                                  // P0 x R1: G0[i0]
+  T* acc = g0s + s0;                                    // R1 x C1 (only without reg_acc)
   const T* G0 = cores + P.coff[0];
   const T* G1 = cores + P.coff[1];
   const int U = counts[0];
@@ -1026,7 +1026,7 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
       for (int e = threadIdx.x; e < s1; e += blockDim.x) {
         const int rr = e / C1, c = e - rr * C1;
         g1t[c * R1p + rr] = G1[static_cast<int64_t>(i1) * s1 + e];
-        acc[e] = T(0);
+        if (!reg_acc) acc[e] = T(0);
       }
       __syncthreads();
       for (int p = lo; p < hi; ++p) {
@@ -1041,9 +1041,15 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
         for (int e = threadIdx.x; e < P0 * R1; e += blockDim.x) {
           const int a = e / R1, rr = e - a * R1;
           const T* sa = sps + a * C1;
-          T v = T(0);
-          for (int c = 0; c < C1; ++c) v = madd<T, false>(sa[c], g1t[c * R1p + rr], v);
-          D0[static_cast<int64_t>(p) * s0 + e] = v;
+          // four independent chains over c (c mod 4), folded in a fixed order
+          T v[4] = {T(0), T(0), T(0), T(0)};
+          int c = 0;
+          for (; c + 4 <= C1; c += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = madd<T, false>(sa[c + u], g1t[(c + u) * R1p + rr], v[u]);
+          }
+          for (; c < C1; ++c) v[0] = madd<T, false>(sa[c], g1t[c * R1p + rr], v[0]);
+          D0[static_cast<int64_t>(p) * s0 + e] = (v[0] + v[1]) + (v[2] + v[3]);
         }
         // acc[r][c] += sum_a G0[a][r] * S[a][c]
         if (reg_acc) {  // thread = column c, the whole r column in registers

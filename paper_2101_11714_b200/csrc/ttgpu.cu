@@ -667,7 +667,9 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   t->mark("bwd_tail");
   // ---- head: D0 per pair, dG1 partials per i1 run
   {
-    const size_t smem = sizeof(T) * (static_cast<size_t>(P.slice[1]) +
+    // the R1 x C1 accumulator lives in registers when a thread can own a column
+    const bool reg_acc = P.C1 <= kThreads && P.r[1] <= kHeadMaxR1 && P.n[0] <= kHeadMaxP0;
+    const size_t smem = sizeof(T) * ((reg_acc ? 0 : static_cast<size_t>(P.slice[1])) +
                                      static_cast<size_t>(P.C1) * (P.r[1] + 1) + P.W1 +
                                      P.slice[0]);
     if (smem > 227 * 1024) fail(TTGPU_ERR_INVALID_ARGUMENT, "G1 slice too large for shared memory");
