@@ -789,10 +789,10 @@ __global__ void k_inv_perm(const uint32_t* __restrict__ sorted_lk, int64_t L,
 
 // MODE 0: y[l][a*n2 + j] = Σ_r H[a][r] · G2[i2][r][j] (forward, kExact rounding)
 // MODE 1: C[pos2[l]][q*n2 + j] = Σ_a H[a][q] · D2[a][j]   (dG2 contribution)
-// PAIR (float, even n2): a thread owns two adjacent output columns (j, j+1)
+// CW (float, n2 % CW == 0): a thread owns CW = 2 or 4 adjacent output columns
 // and forms their products two at a time (FMUL2 / FFMA2), same per-element
-// arithmetic and order as the scalar form.
-template <typename T, int MODE, bool kExact, bool PAIR = false>
+// arithmetic and order as the scalar form (CW = 1).
+template <typename T, int MODE, bool kExact, int CW = 1>
 __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restrict__ cores,
                                                    const T* __restrict__ H,
                                                    const int32_t* __restrict__ lk_pid,
@@ -817,9 +817,9 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
   __shared__ int qlk[64], qrow[64];              // lookup, G2 slice (MODE 0) / bag (MODE 1)
   __shared__ T qal[64];
   const int64_t nchunks = (L + C - 1) / C;
-  const int OWt = PAIR ? OW / 2 : OW;  // threads per lookup
+  const int OWt = OW / CW;  // threads per lookup
   const int per = blockDim.x / OWt > 0 ? blockDim.x / OWt : 1;  // lookups in flight
-  const int e = (threadIdx.x % OWt) * (PAIR ? 2 : 1), slot = threadIdx.x / OWt;
+  const int e = (threadIdx.x % OWt) * CW, slot = threadIdx.x / OWt;
   const bool on_e = threadIdx.x < per * OWt;
   // element -> operand offsets (hoisted)
   const int ra = MODE == 0 ? (e / n2) * R2p : e / n2;  // MODE0: a*R2p  MODE1: q
@@ -876,7 +876,36 @@ __global__ void __launch_bounds__(256) k_pairwalk3(DevPlan P, const T* __restric
         for (int q = q0 + slot; q < q1; q += per) {
           const int64_t l = qlk[q];
           const T* x = xs + q * XW;
-          if constexpr (PAIR) {
+          if constexpr (CW == 4) {
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (MODE == 0) {
+              for (int r = 0; r < R2; ++r) {
+                const float4 xv = *reinterpret_cast<const float4*>(x + r * n2 + rj);
+                const float h = hs[ra + r];
+                if (kExact) {
+                  const float2 p01 = fmul2_rn(h, make_float2(xv.x, xv.y));
+                  const float2 p23 = fmul2_rn(h, make_float2(xv.z, xv.w));
+                  v[0] = __fadd_rn(v[0], p01.x);
+                  v[1] = __fadd_rn(v[1], p01.y);
+                  v[2] = __fadd_rn(v[2], p23.x);
+                  v[3] = __fadd_rn(v[3], p23.y);
+                } else {
+                  ffma2(h, xv.x, xv.y, v[0], v[1]);
+                  ffma2(h, xv.z, xv.w, v[2], v[3]);
+                }
+              }
+              *reinterpret_cast<float4*>(out + l * N + e) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+              for (int i = 0; i < P1; ++i) {
+                const float4 xv = *reinterpret_cast<const float4*>(x + i * n2 + rj);
+                const float h = hs[i * R2p + ra];
+                ffma2(h, xv.x, xv.y, v[0], v[1]);
+                ffma2(h, xv.z, xv.w, v[2], v[3]);
+              }
+              *reinterpret_cast<float4*>(out + static_cast<int64_t>(pos2[l]) * S2 + e) =
+                  make_float4(v[0], v[1], v[2], v[3]);
+            }
+          } else if constexpr (CW == 2) {
             float v0 = 0.f, v1 = 0.f;
             if (MODE == 0) {
               for (int r = 0; r < R2; ++r) {

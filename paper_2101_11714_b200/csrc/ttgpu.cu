@@ -468,9 +468,10 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
     c->ybuf.ensure(sizeof(T) * L * P.N);
     const size_t smem =
         sizeof(T) * (P.W1 + P.prefix[1] + 4 + static_cast<size_t>(kTailChunk) * P.slice[2]);
-    const bool pair = std::is_same_v<T, float> && P.n[2] % 2 == 0;
-    auto kern = pair ? (exact ? k_pairwalk3<T, 0, true, true> : k_pairwalk3<T, 0, false, true>)
-                     : (exact ? k_pairwalk3<T, 0, true> : k_pairwalk3<T, 0, false>);
+    const int cw = std::is_same_v<T, float> ? (P.n[2] % 4 == 0 ? 4 : P.n[2] % 2 == 0 ? 2 : 1) : 1;
+    auto kern = cw == 4 ? (exact ? k_pairwalk3<T, 0, true, 4> : k_pairwalk3<T, 0, false, 4>)
+              : cw == 2 ? (exact ? k_pairwalk3<T, 0, true, 2> : k_pairwalk3<T, 0, false, 2>)
+                        : (exact ? k_pairwalk3<T, 0, true> : k_pairwalk3<T, 0, false>);
     set_smem(kern, smem);
     kern<<<grid_for((L + kTailChunk - 1) / kTailChunk, 1, t->num_sms, 8), 256, smem, st>>>(
         P, t->cores.as<T>(), c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
@@ -624,8 +625,9 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
       k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>() + j * L, L, c->pos2.as<uint32_t>());
       const size_t smem =
           sizeof(T) * (P.W1 + P.prefix[1] + 4 + static_cast<size_t>(kTailChunk) * P.N);
-      auto kern1 = std::is_same_v<T, float> && P.n[2] % 2 == 0 ? k_pairwalk3<T, 1, false, true>
-                                                                : k_pairwalk3<T, 1, false>;
+      const int cw = std::is_same_v<T, float> ? (P.n[2] % 4 == 0 ? 4 : P.n[2] % 2 == 0 ? 2 : 1) : 1;
+      auto kern1 = cw == 4 ? k_pairwalk3<T, 1, false, 4>
+                 : cw == 2 ? k_pairwalk3<T, 1, false, 2> : k_pairwalk3<T, 1, false>;
       set_smem(kern1, smem);
       kern1<<<grid_for(nchunksL, 1, t->num_sms, 8), 256, smem, st>>>(
           P, cores, c->H.as<T>(), c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(),
