@@ -306,13 +306,45 @@ __global__ void k_head_fwd(DevPlan P, const T* __restrict__ cores,
       for (int e = threadIdx.x; e < s1; e += blockDim.x) g1s[e] = G1[(int64_t)i1 * s1 + e];
       __syncthreads();
       const int outs = P0 * C1;
-      for (int e = threadIdx.x; e < (run_hi - run_lo) * outs; e += blockDim.x) {
-        const int q = e / outs, rem = e - q * outs;
-        const int a = rem / C1, c = rem - a * C1;
-        const T* arow = g0s + (run_lo - p0 + q) * s0 + a * R1;
-        T acc = T(0);
-        for (int p = 0; p < R1; ++p) acc = madd<T, kExact>(arow[p], g1s[p * C1 + c], acc);
-        H[static_cast<int64_t>(run_lo + q) * P.W1 + rem] = acc;
+      bool quad_done = false;
+      if constexpr (std::is_same_v<T, float>) quad_done = (C1 & 3) == 0;
+      if (quad_done) {
+        // fp32: four adjacent columns per thread, products two at a time
+        // (FMUL2 / FFMA2), the same per-element p-ascending chain
+        const int outs4 = outs >> 2;
+        for (int e = threadIdx.x; e < (run_hi - run_lo) * outs4; e += blockDim.x) {
+          const int q = e / outs4, rem = (e - q * outs4) * 4;
+          const int a = rem / C1, c = rem - a * C1;
+          const float* arow = reinterpret_cast<const float*>(g0s) + (run_lo - p0 + q) * s0 + a * R1;
+          const float* gcol = reinterpret_cast<const float*>(g1s) + c;
+          float v[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int p = 0; p < R1; ++p) {
+            const float4 g = *reinterpret_cast<const float4*>(gcol + p * C1);
+            const float x = arow[p];
+            if (kExact) {
+              const float2 p01 = fmul2_rn(x, make_float2(g.x, g.y));
+              const float2 p23 = fmul2_rn(x, make_float2(g.z, g.w));
+              v[0] = __fadd_rn(v[0], p01.x);
+              v[1] = __fadd_rn(v[1], p01.y);
+              v[2] = __fadd_rn(v[2], p23.x);
+              v[3] = __fadd_rn(v[3], p23.y);
+            } else {
+              ffma2(x, g.x, g.y, v[0], v[1]);
+              ffma2(x, g.z, g.w, v[2], v[3]);
+            }
+          }
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(H) + static_cast<int64_t>(run_lo + q) * P.W1 +
+                                     rem) = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      } else {
+        for (int e = threadIdx.x; e < (run_hi - run_lo) * outs; e += blockDim.x) {
+          const int q = e / outs, rem = e - q * outs;
+          const int a = rem / C1, c = rem - a * C1;
+          const T* arow = g0s + (run_lo - p0 + q) * s0 + a * R1;
+          T acc = T(0);
+          for (int p = 0; p < R1; ++p) acc = madd<T, kExact>(arow[p], g1s[p * C1 + c], acc);
+          H[static_cast<int64_t>(run_lo + q) * P.W1 + rem] = acc;
+        }
       }
       run_lo = run_hi;
     }
