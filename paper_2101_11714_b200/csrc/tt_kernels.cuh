@@ -1119,14 +1119,33 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
             T sv[kHeadMaxP0];
 #pragma unroll
             for (int a = 0; a < kHeadMaxP0; ++a) sv[a] = a < P0 ? sps[a * C1 + c] : T(0);
+            bool paired = false;
+            if constexpr (std::is_same_v<T, float>)
+              paired = (R1 & 1) == 0 && ((C1 * R1p + P.W1) & 1) == 0;  // 8-byte aligned G0 pairs
+            if (paired) {  // (r, r+1) two lanes at a time: FFMA2, same per-element chain
+              if constexpr (std::is_same_v<T, float>) {
 #pragma unroll
-            for (int rr = 0; rr < kHeadMaxR1; ++rr) {
-              if (rr < R1) {
-                T v = racc[rr];
+                for (int rr = 0; rr < kHeadMaxR1; rr += 2) {
+                  if (rr < R1) {
 #pragma unroll
-                for (int a = 0; a < kHeadMaxP0; ++a)
-                  if (a < P0) v = madd<T, false>(g0s[a * R1 + rr], sv[a], v);
-                racc[rr] = v;
+                    for (int a = 0; a < kHeadMaxP0; ++a)
+                      if (a < P0) {
+                        const float2 g = *reinterpret_cast<const float2*>(g0s + a * R1 + rr);
+                        ffma2(sv[a], g.x, g.y, racc[rr], racc[rr + 1]);
+                      }
+                  }
+                }
+              }
+            } else {
+#pragma unroll
+              for (int rr = 0; rr < kHeadMaxR1; ++rr) {
+                if (rr < R1) {
+                  T v = racc[rr];
+#pragma unroll
+                  for (int a = 0; a < kHeadMaxP0; ++a)
+                    if (a < P0) v = madd<T, false>(g0s[a * R1 + rr], sv[a], v);
+                  racc[rr] = v;
+                }
               }
             }
           }
