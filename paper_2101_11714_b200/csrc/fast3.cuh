@@ -277,7 +277,7 @@ struct ScanArgs {
 // group partials -- and the last arriver's sequential fold -- small.
 constexpr int kGroup = 64;
 constexpr int kGroup0 = 32;    // combine: candidate CTA blocks per warp task (dG0; dense for hot i0)
-constexpr int kScanKeys = 16;  // keys per f3_scan CTA
+constexpr int kScanKeys = 8;   // keys per f3_scan CTA
 constexpr int kScanThreads = 256;
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 5); }  // bank-conflict-free chunks
