@@ -737,7 +737,7 @@ __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
 template <class D>
 __global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cores, int64_t coff2,
                                                 const Tile* __restrict__ tiles,
-                                                const int* __restrict__ ntiles,
+                                                const int* __restrict__ ntiles, int max_tiles,
                                                 const uint32_t* __restrict__ perm,
                                                 const uint16_t* __restrict__ d2,
                                                 const int32_t* __restrict__ lk_bag,
@@ -753,11 +753,15 @@ __global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cor
   constexpr int U = 8;  // members with G2 loads in flight
   const int lane = threadIdx.x & 31;
   const int t = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
-  if (t >= *ntiles) return;
-  const float* G2 = cores + coff2;
+  if (t >= max_tiles) return;
+  // the tile count and this tile's descriptor in one round trip (entries past
+  // the count are in bounds, just unused)
+  const int nt = *ntiles;
   const Tile tl = tiles[t];
-  const int ntl = tl.end - tl.start;
   const int nslots = tile_nslots[t];
+  if (t >= nt) return;
+  const float* G2 = cores + coff2;
+  const int ntl = tl.end - tl.start;
   // each lane fetches its own lookup's D2 = T(alpha) * grad[bag] once (one
   // round trip for the whole tile); members' values then move by shuffles
   int my_sl = -1, my_i2 = 0;

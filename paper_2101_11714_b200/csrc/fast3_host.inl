@@ -176,7 +176,7 @@ struct F3Runner {
     f.Sbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
     t->mark("bwd_begin");
     f3::f3_srows<D><<<(f.max_tiles1 * 32 + 255) / 256, 256, 0, st>>>(
-        t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
+        t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.max_tiles1,
         f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
         f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>());
     t->mark("f3_srows");
