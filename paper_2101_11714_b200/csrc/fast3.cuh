@@ -1,15 +1,18 @@
 // Fast path for 3-core tables (every BASELINE config): compile-time TT shape,
-// 8 kernels per fwd+bwd+SGD step, deterministic, no floating-point atomics.
+// 9 kernels per fwd+bwd+SGD step, deterministic, no floating-point atomics.
 //
 //   f3_hist     decode + validate; per-CTA histograms of two sort keys
-//               (k1 = i1, k2 = i2); lookup->bag map and backward alpha
-//   f3_scan     2 CTAs (one per key): exclusive scan of the (key, CTA)
-//               histogram; tile lists (each key bucket cut into tiles)
-//   f3_scatter  stable counting-sort scatter of both keys (warp match_any)
-//   f3_fwd      per i1-tile: G1[i1] staged in smem by TMA once; tile-local
-//               dedup of i0 ("slots"); H(slot) = G0[i0]·G1[i1]; y = H·G2[i2]
-//   f3_pool     per bag, lookup order: out = Σ T(w)·y (Mean rescale)
-//   f3_bwd1     per i1-tile: S(slot) = Σ D1, dG1 += Σ G0ᵀS, D0(slot) = S·G1ᵀ
+//               (k1 = i1, k2 = i2); lookup->bag map, backward alpha, solo bags
+//   f3_scan     one CTA per kScanKeys keys of either sort key: absolute
+//               scatter offsets; tile lists (each key bucket cut into tiles)
+//   f3_scatter  stable counting-sort scatter of both keys (warp match_any),
+//               plus sorted (lookup, digits, solo) records for f3_fwd
+//   f3_fwd      per i1-tile, pipelined one tile ahead: slots = distinct i0
+//               (match_any), operands by bulk copy onto mbarriers,
+//               H(slot) = G0[i0]·G1[i1], y = H·G2[i2]; single-lookup bags pooled here
+//   f3_pool     per multi-lookup bag, lookup order: out = Σ T(w)·y (Mean rescale)
+//   f3_srows    warp per i1-tile: S(slot) = Σ D1, D1 = D2·G2ᵀ
+//   f3_bwd1     per i1-tile (TMA-staged S and G0 rows): dG1 += Σ G0ᵀS, D0 = S·G1ᵀ
 //   f3_bwd2     per i2-tile: dG2 += Σ H(lookup)ᵀ D2 (H rows saved by f3_fwd)
 //   f3_combine  fixed-order folds of the partials per core slice, fused with
 //               the SGD update (or a dense gradient write)
