@@ -155,6 +155,34 @@ def make_inputs(cfg, seed, tt):
     return idx, off, g.astype(np.float32)
 
 
+def make_inputs_reference(cfg, seed):
+    """The same bytes as make_inputs, drawn by the REFERENCE's own generators
+    (oracle/_ref: ZipfianSampler + generate_zipfian_batch, Rng::uniform_int;
+    data.cpp:8-47, rng.hpp:47-51) -- the reference arm never loads this repo's
+    package or its libraries."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    ref = pyoracle.RefImpl()
+    if cfg["zipf"] > 0:
+        idx, off = ref.zipf_batch(cfg["rows"], cfg["zipf"], seed, cfg["bags"], cfg["pf"])
+    else:
+        idx = ref.uniform_int(seed, 0, cfg["rows"], cfg["bags"] * cfg["pf"])
+        off = np.arange(0, cfg["bags"] * cfg["pf"] + 1, cfg["pf"], dtype=np.int64)
+    g = np.random.default_rng(seed + 1000).standard_normal((cfg["bags"], cfg["emb"]))
+    return idx, off, g.astype(np.float32)
+
+
+def workload_config(cfg, world):
+    """The `config` object both arms print (identical for the same flags): the
+    workload only; how each arm executes it goes under `execution`."""
+    L = cfg["bags"] * cfg["pf"]
+    return {"workload": cfg["desc"], "global_batch": cfg["bags"] * world,
+            "lookups_per_step": L * world,
+            "parallelism": f"dp{world}" if world > 1 else "single-gpu",
+            "l2": "GPU arm: flushed (256 MiB write) before every timed step, outside the events"}
+
+
 def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0, steps=None, warmup=0):
     """The reference's own OpenMP CPU step (oracle/_ref, compiled from the
     reference sources) on this host's cores; falls back to the C restatement.
@@ -180,6 +208,17 @@ def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0, steps=None, warmup=0)
             reps = max(1, int(steps))
         sec = t.time_step(idx, off, grad, LR, reps=reps, threads=threads)
         kind = "reference"
+        # BASELINE.md §3.2 also asks for 1 thread and the serial ref:: pair
+        # (bounded: 1 warm-up + 3 steps each, skipped when one step > 20 s)
+        extra = {}
+        if sec * threads < 20.0:
+            s1 = t.time_step(idx, off, grad, LR, reps=3, threads=1)
+            ss = t.time_step_serial(idx, off, grad, LR, reps=3)
+            t.time_step(idx, off, grad, LR, reps=0, threads=threads)  # restore the thread count
+            extra = {"threads_1": {"value": L / s1, "ms_per_step": s1 * 1e3},
+                     "serial_ref": {"value": L / ss, "ms_per_step": ss * 1e3,
+                                    "what": "ref::forward_bags + ref::backward_bags (serial "
+                                            "oracle, embedding_ops.hpp:378-492) + sgd_step"}}
     else:
         orc = pyoracle.Oracle()
         rng = np.random.default_rng(0)
@@ -190,18 +229,17 @@ def cpu_reference_time(cfg, idx, off, grad, budget_s=10.0, steps=None, warmup=0)
             orc.time_step(plan, cores, idx, off, grad, LR, threads)
         ts = [orc.time_step(plan, cores, idx, off, grad, LR, threads) for _ in range(reps)]
         sec, kind = float(np.median(ts)), "port"
-    return {"value": L / sec, "unit": "indices/s", "cores": threads, "kind": kind,
+        extra = {}
+    return {"value": L / sec, "unit": "indices/s", "cores": threads, "kind": kind, **extra,
             "sample": f"{L} lookups ({cfg['bags']} bags x {cfg['pf']}), median of {reps} steps "
                       f"(fwd save + bwd + sgd, fp32, OMP threads={threads})",
             "ms_per_step": sec * 1e3}
 
 
-def run_reference(args, cfg, rank):
+def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    import paper_2101_11714_b200 as tt  # host-only helpers: the reference's own streams
-
-    idx, off, grad = make_inputs(cfg, 7, tt)
+    idx, off, grad = make_inputs_reference(cfg, 7)
     # W untimed + K timed full-batch steps on all host threads (each step is one
     # reference fwd(save) + bwd + sgd over the whole batch)
     base = cpu_reference_time(cfg, idx, off, grad, steps=args.steps, warmup=args.warmup)
@@ -211,9 +249,12 @@ def run_reference(args, cfg, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference Zipf/uniform streams, sampled-Gaussian cores)",
             "impl": "reference",
-            "config": {"workload": cfg["desc"], "global_batch": cfg["bags"],
-                       "lookups_per_step": len(idx), "parallelism": "cpu-openmp"},
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": workload_config(cfg, world),
+            "execution": {"device": "host CPU", "path": "oracle/_ref (reference sources, "
+                          "OpenMP): forward_bags(save) + backward_bags + sgd_step",
+                          "sample": f"rank 0 only, {len(idx)} lookups per step"},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                   "threads_1", "serial_ref") if k in base},
             "e2e": {"value": v, "unit": "indices/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -366,12 +407,26 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-exec this command under torch.distributed.run
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
-        run_reference(args, cfg, rank)
+        run_reference(args, cfg, rank, world)
         return
     if cfg.get("collection"):
         run_collection(args, cfg, rank, world, local)
@@ -707,12 +762,28 @@ def main():
         ncu = {}
     work = kernel_work(dom, cfg["rf"], cfg["cf"], ranks, L, B, N, params)
     dom_s = phase_ms[dom] / 1e3
-    traffic = ncu.get(args.config, {}).get(dom, {}).get("dram_bytes")
+    ncu_dom = ncu.get(args.config, {}).get(dom, {})
+    traffic = ncu_dom.get("dram_bytes")
+    executed = None
+    if ncu_dom.get("us"):
+        # ncu-executed FP32 work of the same kernel (dedup makes
+        # the algorithmic rate exceed what the FMA pipe actually ran):
+        # 2 flops per FFMA lane-op, 4 per FFMA2 thread instruction, over the ncu
+        # (cold, serialised) duration and over this run's event duration
+        ex_fl = 2.0 * ncu_dom.get("ffma_thread_inst", 0.0) + 4.0 * ncu_dom.get("ffma2_thread_inst", 0.0)
+        executed = {"flops_per_launch": ex_fl,
+                    "tflops_ncu_time": ex_fl / (ncu_dom["us"] * 1e-6) / 1e12,
+                    "frac_ncu_time": ex_fl / (ncu_dom["us"] * 1e-6) / 1e12 / fp32_peak_tf,
+                    "tflops_event_time": ex_fl / dom_s / 1e12,
+                    "frac_event_time": ex_fl / dom_s / 1e12 / fp32_peak_tf,
+                    "source": "profiles/ncu_kernels.json (sm__sass_thread_inst_executed_op_ffma"
+                              "/ffma2 counts of one ncu --set full capture)"}
     if work:
         fl, by = work
         roofline = {"bound": "fp32", "kernel": dom, "achieved": fl / dom_s / 1e12,
                     "peak": fp32_peak_tf, "unit": "TFLOP/s", "frac": fl / dom_s / 1e12 / fp32_peak_tf,
                     "traffic": traffic, "flops_per_launch": fl, "launch_ms": phase_ms[dom],
+                    "executed": executed,
                     "peak_source": fp32_src,
                     "note": "FP32 CUDA-core FFMA chain (no tensor-core path: the reference's fp32 "
                             "arithmetic order is kept); algorithmic flops, reference chain without "
@@ -740,11 +811,10 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: reference Zipf/uniform index streams (same bytes as data.cpp), "
                 "sampled-Gaussian cores (initializer.hpp), N(0,1) grad_out",
-        "config": {"workload": cfg["desc"], "global_batch": B * world, "lookups_per_step": L * world,
-                   "parallelism": f"dp{world}" if world > 1 else "single-gpu",
-                   "l2": "flushed (256 MiB write) before every timed step, outside the events",
-                   "forward": "ffma" if args.fast_forward else "exact (bit-identical to reference)",
-                   "graph": use_graph, "gradient_reduce": reduce_path},
+        "config": workload_config(cfg, world),
+        "execution": {"device": "B200", "forward": "ffma" if args.fast_forward else
+                      "exact (bit-identical to reference)", "graph": use_graph,
+                      "gradient_reduce": reduce_path},
         "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
         "cache": ({"capacity": cache.capacity(), "hit_rate": cache.hit_rate()}
                   if cache is not None else None),

@@ -121,10 +121,12 @@ using TtEmbeddingBagCuda = TtEmbeddingBagCudaT<float>;
 
 namespace detail {
 
-/// Cheap identity of a host table's contents: mutation counter, plan, name,
-/// core buffer addresses and 64 sampled values per core.  A table destroyed
-/// and re-created at the same address (a loop-local TtTable) gets a new
-/// fingerprint unless it holds the same data.
+/// Identity of a host table's contents: mutation counter, plan, name, core
+/// buffer addresses and a hash of EVERY core element.  The reference allows
+/// in-place writes through TtTable::core(k)[i] without mark_mutated() (its own
+/// tests do this), so a sampled fingerprint could miss an edit and leave a
+/// stale device shadow; the full hash (four independent 64-bit lanes, about
+/// 1 ns per 8 bytes) costs less than re-uploading the cores.
 template <typename T>
 inline std::uint64_t fingerprint(const TtTable<T>& t) {
   std::uint64_t h = 1469598103934665603ull;
@@ -140,12 +142,26 @@ inline std::uint64_t fingerprint(const TtTable<T>& t) {
     mix(static_cast<std::uint64_t>(p.ranks[k + 1]));
     auto c = t.core(k);
     mix(reinterpret_cast<std::uintptr_t>(c.data()));
-    const size_t n = c.size(), step = n > 64 ? n / 64 : 1;
-    for (size_t i = 0; i < n; i += step) {
-      std::uint64_t bits = 0;
-      std::memcpy(&bits, &c[i], sizeof(T));
-      mix(bits);
+    mix(static_cast<std::uint64_t>(c.size()));
+    const unsigned char* bytes = reinterpret_cast<const unsigned char*>(c.data());
+    const size_t nb = c.size() * sizeof(T), nw = nb / 8;
+    constexpr std::uint64_t kMul = 0x9E3779B97F4A7C15ull;
+    std::uint64_t lane[4] = {1, 2, 3, 4};
+    size_t i = 0;
+    for (; i + 4 <= nw; i += 4)
+      for (int j = 0; j < 4; ++j) {
+        std::uint64_t v;
+        std::memcpy(&v, bytes + 8 * (i + j), 8);
+        lane[j] = (lane[j] ^ v) * kMul;
+        lane[j] ^= lane[j] >> 29;
+      }
+    for (; i < nw; ++i) {
+      std::uint64_t v;
+      std::memcpy(&v, bytes + 8 * i, 8);
+      lane[0] = ((lane[0] ^ v) * kMul) ^ (lane[0] >> 31);
     }
+    for (size_t b = nw * 8; b < nb; ++b) lane[1] = (lane[1] ^ bytes[b]) * kMul;
+    for (int j = 0; j < 4; ++j) mix(lane[j]);
   }
   return h;
 }

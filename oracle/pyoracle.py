@@ -156,6 +156,7 @@ class RefImpl:
         L.ref_last_error.restype = C.c_char_p
         L.ref_core_size.restype = C.c_int64
         L.ref_time_step.restype = C.c_double
+        L.ref_time_step_serial.restype = C.c_double
         L.ref_random_batch.restype = C.c_int64
         L.ref_cache_default_capacity.restype = C.c_int64
         L.ref_cache_hot_rows.restype = C.c_int64
@@ -370,6 +371,15 @@ class RefTable:
         return self.ref.lib.ref_time_step(self.h, _p(idx), C.c_int64(len(idx)), _p(off),
                                           C.c_int64(len(off) - 1), _p(g), C.c_double(lr),
                                           C.c_int(reps), C.c_int(threads))
+
+    def time_step_serial(self, idx, off, grad_out, lr=0.01, reps=3):
+        """ref::forward_bags + ref::backward_bags + sgd_step (serial oracle)."""
+        idx = np.ascontiguousarray(idx, np.int64)
+        off = np.ascontiguousarray(off, np.int64)
+        g = np.ascontiguousarray(grad_out, np.float32)
+        return self.ref.lib.ref_time_step_serial(self.h, _p(idx), C.c_int64(len(idx)), _p(off),
+                                                 C.c_int64(len(off) - 1), _p(g), C.c_double(lr),
+                                                 C.c_int(reps))
 
 
 class RefCache:

@@ -597,6 +597,31 @@ double ref_time_step(void* h, const int64_t* idx, int64_t L, const int64_t* off,
   return ts.empty() ? 0.0 : ts[ts.size() / 2];
 }
 
+// The serial oracle step: ref::forward_bags + ref::backward_bags (always
+// recomputes, embedding_ops.hpp:378-492) + sgd_step -- BASELINE.md §3.2's
+// "serial ref::" figure.  Median seconds per step over `reps` after one warm-up.
+double ref_time_step_serial(void* h, const int64_t* idx, int64_t L, const int64_t* off, int64_t B,
+                            const float* grad, double lr, int reps) {
+  auto* t = static_cast<RefTable*>(h);
+  IndexBatch b = make_batch(idx, L, off, B, nullptr, 0);
+  std::span<const float> g(grad, static_cast<size_t>(B) * t->f->cols());
+  auto step = [&] {
+    auto o = ref::forward_bags(*t->f, b);
+    auto gr = ref::backward_bags(*t->f, b, g);
+    sgd_step(*t->f, gr, lr);
+    (void)o;
+  };
+  step();
+  std::vector<double> ts;
+  for (int i = 0; i < reps; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    step();
+    ts.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+  std::sort(ts.begin(), ts.end());
+  return ts.empty() ? 0.0 : ts[ts.size() / 2];
+}
+
 #ifdef TTREF_CHECKPOINT
 // ---- checkpoint.hpp / src/checkpoint.cpp (TTRECV01) ------------------------
 // Checkpoint::put_table for every table (in order), optional f32 arrays

@@ -13,6 +13,8 @@ struct ttgpu_cache {
   size_t esz = 4;
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t last = nullptr;  // stream of the last call that wrote cache state
+  bool last_set = false;
   int num_sms = 148;
   bool active = false;
   // frequencies (dense, one counter per row) and counters [accesses, hits]
@@ -54,7 +56,21 @@ int bits_for_slots(int64_t cap) {
 
 void cache_ensure_tmp(ttgpu_cache* c, size_t bytes) { c->tmp.ensure(std::max<size_t>(bytes, 256)); }
 
-cudaStream_t cache_stream(ttgpu_cache* c, ttgpu_table* t) { return t ? t->stream : c->stream; }
+// The stream a cache call runs on (the table's, when one is involved); it is
+// remembered so calls that only touch cache state order after it.
+cudaStream_t cache_stream(ttgpu_cache* c, ttgpu_table* t) {
+  cudaStream_t s = t ? t->stream : c->stream;
+  c->last = s;
+  c->last_set = true;
+  return s;
+}
+
+// Order c->stream after the last stream that wrote cache state (seg_lo, sg,
+// slot_rows, store are produced on the table's stream by forward / backward /
+// admit, which may differ from the cache's own stream).
+void cache_order_after_last(ttgpu_cache* c) {
+  if (c->last_set && c->last != c->stream) CK(cudaStreamSynchronize(c->last));
+}
 
 void cache_raise(ttgpu_cache* c, cudaStream_t st, const int64_t* host_idx, const char* what) {
   unsigned long long h[2];
@@ -703,7 +719,7 @@ int ttgpu_cache_forward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const in
       CK(cudaMemcpyAsync(out, ctx->h_out.p, t->esz * B * t->plan.emb_dim, cudaMemcpyDeviceToHost,
                          t->stream));
     CK(cudaStreamSynchronize(t->stream));
-    ttgpu::raise_latched(t, nullptr);
+    ttgpu::raise_latched(t, nullptr, 0);
   });
 }
 
@@ -774,6 +790,7 @@ int ttgpu_cache_backward_step_device(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* 
 int ttgpu_cache_slot_grads(ttgpu_cache* c, void* host_grads, uint8_t* touched) {
   return guarded([&] {
     require_arg(c->grads_valid, "no slot gradients (run ttgpu_cache_backward)");
+    ttgpu::cache_order_after_last(c);
     std::vector<int> lo(static_cast<size_t>(c->capacity));
     CK(cudaMemcpyAsync(lo.data(), c->seg_lo.p, 4 * c->capacity, cudaMemcpyDeviceToHost, c->stream));
     if (host_grads)
@@ -795,6 +812,7 @@ int ttgpu_cache_slot_grads(ttgpu_cache* c, void* host_grads, uint8_t* touched) {
 int ttgpu_cache_sgd_update(ttgpu_cache* c, const int64_t* slots, int64_t n, const void* rows,
                            double lr) {
   return guarded([&] {
+    ttgpu::cache_order_after_last(c);
     std::vector<int64_t> sr(static_cast<size_t>(c->capacity));
     CK(cudaMemcpyAsync(sr.data(), c->now().slot_rows.p, 8 * c->capacity, cudaMemcpyDeviceToHost,
                        c->stream));

@@ -516,6 +516,11 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
     }
   }
   if (mode == 0) CK(cudaMemsetAsync(grads, 0, sizeof(T) * t->total, st));
+  // fused mode, d >= 4: the tail cores k >= 2 go through the dense gradient
+  // buffer (k_combine<T,0> skips untouched slices, k_sgd applies every slice),
+  // so those slices must start at zero -- not at an earlier backward's values
+  if (mode == 1 && d >= 4)
+    CK(cudaMemsetAsync(grads + P.coff[2], 0, sizeof(T) * (t->total - P.coff[2]), st));
   if (L == 0 || c->B == 0) return;
   const int64_t m01 = static_cast<int64_t>(P.m[0]) * P.m[1];
   const int64_t ucap = std::min<int64_t>(L, m01);
@@ -720,7 +725,10 @@ void check_ctx(ttgpu_table* t, ttgpu_ctx* c) {
                   "': cores changed since the forward pass"));
 }
 
-void raise_latched(ttgpu_table* t, const int64_t* host_idx) {
+// host_idx / host_L: the caller's index array (nullptr for device-side calls).
+// The latch can hold a position set by an earlier asynchronous call on a larger
+// batch, so the position is bounds-checked before host_idx is read.
+void raise_latched(ttgpu_table* t, const int64_t* host_idx, int64_t host_L) {
   if (!t->h_errs) CK(cudaHostAlloc(reinterpret_cast<void**>(&t->h_errs), 32, cudaHostAllocDefault));
   unsigned long long* h = t->h_errs;  // pinned: the read rides the same sync as the caller's copies
   CK(cudaMemcpyAsync(h, t->errs.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -736,7 +744,7 @@ void raise_latched(ttgpu_table* t, const int64_t* host_idx) {
   if (sflags & 2) fail(TTGPU_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing");
   if (sflags & 4) fail(TTGPU_ERR_INVALID_ARGUMENT, "offsets end does not match the index count");
   const int64_t pos = static_cast<int64_t>(h[0]);
-  if (host_idx)
+  if (host_idx && pos >= 0 && pos < host_L)
     throw std::out_of_range(cat("index ", host_idx[pos], " out of range [0, ", t->plan.num_rows,
                                 ") for table '", t->name, "'"));
   throw std::out_of_range(cat("index at lookup ", pos, " out of range [0, ", t->plan.num_rows,
@@ -1085,7 +1093,7 @@ int ttgpu_forward(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* 
                          t->stream));
     tr("d2h");
     try {
-      raise_latched(t, idx);
+      raise_latched(t, idx, L);
       tr("raise_latched");
     } catch (...) {
       c->valid = false;
@@ -1353,7 +1361,7 @@ int ttgpu_sync(ttgpu_table* t) {
 }
 
 int ttgpu_check(ttgpu_table* t) {
-  return guarded([&] { raise_latched(t, nullptr); });
+  return guarded([&] { raise_latched(t, nullptr, 0); });
 }
 
 void ttgpu_stats_reset(void) {

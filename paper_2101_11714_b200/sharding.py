@@ -150,13 +150,23 @@ class DataParallelTable:
                                   save=True)
 
     def backward_step(self, grad_ptr: int, lr: float, stream=None):
+        """backward -> allreduce(SUM) -> SGD, all ordered on the table's stream.
+        With an explicit `stream` for the collective, events order it after the
+        backward and the SGD after it (no race on the gradient buffer)."""
         if self.world == 1:
             self.table.backward_sgd_device(self.ctx, grad_ptr, lr)
             return
+        torch = self._torch
         self.table.backward_device(self.ctx, grad_ptr)
-        s = stream if stream is not None else self._torch.cuda.current_stream(self.device)
-        with self._torch.cuda.stream(s):
+        ts = torch.cuda.ExternalStream(self.table.stream, device=self.device) \
+            if self.table.stream else torch.cuda.default_stream(self.device)
+        s = stream if stream is not None else ts
+        if s.cuda_stream != ts.cuda_stream:
+            s.wait_stream(ts)  # the collective reads the finished gradient
+        with torch.cuda.stream(s):
             allreduce_sum_(self.grad_view, self.group)
+        if s.cuda_stream != ts.cuda_stream:
+            ts.wait_stream(s)  # the SGD reads the reduced gradient
         self.table.apply_grad(lr)
 
 

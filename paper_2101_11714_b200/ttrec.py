@@ -209,6 +209,7 @@ class TtTable:
                                   C.c_void_p(stream), C.byref(h)))
         self.handle = h
         self.device = device
+        self.stream = stream  # raw cudaStream_t every call of this table is ordered on
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -331,6 +332,7 @@ class TtTable:
 
     def set_stream(self, stream: int):
         _raise(lib().ttgpu_set_stream(self.handle, C.c_void_p(stream or None)))
+        self.stream = stream or 0
 
     def graph_begin(self):
         _raise(lib().ttgpu_graph_begin(self.handle))

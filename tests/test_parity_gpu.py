@@ -491,6 +491,31 @@ def test_fast_path_fused_sgd_equals_dense_then_sgd():
         b_.backward_sgd(rb.context, batch, g, 0.01)
 
 
+@pytest.mark.parametrize("d", [3, 4, 5])
+def test_generic_fused_sgd_multistep_equals_dense_then_sgd(d):
+    """Several fused backward+SGD steps on DIFFERENT batches equal
+    backward_bags + sgd_step each step (generic path, d >= 4 included: the
+    tail cores' untouched slices must not re-apply an earlier step's gradient)."""
+    rows = 3000
+    emb = 32 if d == 5 else 16
+    p = tt.plan_shapes(rows, emb, d, 4, None, {4: [2, 2, 2, 2], 5: [2, 2, 2, 2, 2]}.get(d))
+    a, _ = make_table(p, np.float32, 21, "a", scale=0.5)
+    b_, _ = make_table(p, np.float32, 21, "b", scale=0.5)
+    a.set_generic_path(True)
+    b_.set_generic_path(True)
+    rng = np.random.default_rng(22)
+    for step in range(4):
+        # small batches over a few rows: most tail slices are untouched each step
+        batch = random_batch(rng, min(rows, 40 + 30 * step), 24, 1, 3, False, tt.Pooling.Sum)
+        g = rng.standard_normal((24, emb)).astype(np.float32)
+        ra = tt.forward_bags(a, batch)
+        tt.sgd_step(a, tt.backward_bags(a, batch, ra.context, g), 0.05)
+        rb = tt.forward_bags(b_, batch)
+        b_.backward_sgd(rb.context, batch, g, 0.05)
+        for k in range(d):
+            assert np.array_equal(a.core(k), b_.core(k)), f"step {step} core {k}"
+
+
 def test_data_parallel_shards_sum_to_full_batch(orc):
     """§8(e) on one GPU: the dense gradients of two bag shards (what two ranks
     produce before the allreduce) sum to the full-batch gradient, and the
