@@ -840,7 +840,8 @@ def main():
     }
     if not args.no_cpu_baseline:
         cb = cpu_reference_time(cfg, idx, off, grad, budget_s=10.0)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                   "threads_1", "serial_ref") if k in cb}
     if phases:
         line["profile_single_step"] = phases
     print(json.dumps(line), flush=True)
