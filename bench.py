@@ -401,6 +401,8 @@ def main():
     ap.add_argument("--fast-forward", action="store_true",
                     help="FFMA forward instead of the bit-exact default")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ffma-backward", action="store_true",
+                    help="backward head contraction on the FP32 FFMA path instead of tcgen05 3xTF32")
     ap.add_argument("--nccl", action="store_true",
                     help="N>1: NCCL allreduce + SGD kernel instead of the fused peer reduce+SGD")
     ap.add_argument("--profile", action="store_true", help="print per-phase times")
@@ -458,6 +460,7 @@ def main():
     table = tt.TtTable(plan, "bench", np.float32, device=local, stream=stream.cuda_stream)
     table.init_sampled_gaussian(1)
     table.set_exact_forward(not args.fast_forward)
+    table.set_tensor_path(not args.ffma_backward)
     idx, off, grad = make_inputs(cfg, 7 + rank, tt)
     L, B, N = len(idx), cfg["bags"], cfg["emb"]
     with torch.cuda.stream(stream):
@@ -814,6 +817,8 @@ def main():
         "config": workload_config(cfg, world),
         "execution": {"device": "B200", "forward": "ffma" if args.fast_forward else
                       "exact (bit-identical to reference)", "graph": use_graph,
+                      "backward_head": "ffma" if args.ffma_backward else
+                      "tcgen05 3xTF32 where eligible (cfg3 shape), else ffma",
                       "gradient_reduce": reduce_path},
         "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
         "cache": ({"capacity": cache.capacity(), "hit_rate": cache.hit_rate()}

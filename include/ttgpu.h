@@ -84,6 +84,12 @@ int ttgpu_set_exact_forward(ttgpu_table* t, int on);
 /* 3-core float tables with a compiled shape use the specialised fast path
  * (kind >= 0); on=1 forces the generic pipeline instead (used by tests to
  * cross-check the two implementations). */
+/* Backward contractions on the tcgen05 tensor cores (error-compensated
+ * 3xTF32, fp32 accumulation) where the shape allows it (1 = default) or on the
+ * FP32 FFMA path (0).  Forward results never depend on it; gradients differ
+ * within the 1e-4 tolerance.  No reference counterpart (the reference is CPU
+ * only, embedding_ops.hpp:335-347). */
+int ttgpu_set_tensor_path(ttgpu_table* t, int on);
 int ttgpu_set_generic_path(ttgpu_table* t, int on);
 int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind);
 int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out); /* tt_table.hpp:84 */

@@ -23,6 +23,7 @@
 #include "../../include/ttgpu.h"
 #include "shape_plan.hpp"
 #include "tt_kernels.cuh"
+#include "head_tc.cuh"
 #include "fast3.cuh"
 
 namespace ttgpu {
@@ -192,6 +193,7 @@ struct ttgpu_table {
   uint64_t generation = 0;
   bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
   bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
+  bool tensor_head = true;     // head backward on tcgen05 (3xTF32) where the shape allows it
   // optional phase timing (CUDA events between pipeline phases)
   // Marks recorded while the stream is being captured become event-record nodes of
   // the graph (cudaEventRecordExternal) and stay owned by it: every graph launch
@@ -680,11 +682,26 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
                                      static_cast<size_t>(P.C1) * (P.r[1] + 1) + P.W1 +
                                      P.slice[0]);
     if (smem > 227 * 1024) fail(TTGPU_ERR_INVALID_ARGUMENT, "G1 slice too large for shared memory");
-    auto kern = k_head_bwd<T>;
-    set_smem(kern, smem);
-    kern<<<grid_for(ucap, kHeadChunk, t->num_sms, 2), kThreads, smem, st>>>(
-        P, cores, c->S.as<T>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
-        c->scan1.as<unsigned long long>(), kHeadChunk, c->D0.as<T>(), c->part1.as<T>());
+    bool launched = false;
+    if constexpr (std::is_same_v<T, float>) {
+      // tensor-core head (head_tc.cuh): cfg3's shape class, P0 = 4, R1 = 64, C1 = 256
+      if (t->tensor_head && d == 3 && P.n[0] == tc::HeadTc::P0 && P.r[1] == tc::HeadTc::R1 &&
+          P.C1 == 256 && kHeadChunk <= tc::HeadTc::PAIRS) {
+        auto kt = tc::k_head_bwd_tc<256>;
+        set_smem(kt, tc::HeadTc::SMEM);
+        kt<<<grid_for(ucap, kHeadChunk, t->num_sms, 1), 256, tc::HeadTc::SMEM, st>>>(
+            P, cores, c->S.as<float>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
+            c->scan1.as<unsigned long long>(), kHeadChunk, c->D0.as<float>(), c->part1.as<float>());
+        launched = true;
+      }
+    }
+    if (!launched) {
+      auto kern = k_head_bwd<T>;
+      set_smem(kern, smem);
+      kern<<<grid_for(ucap, kHeadChunk, t->num_sms, 2), kThreads, smem, st>>>(
+          P, cores, c->S.as<T>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
+          c->scan1.as<unsigned long long>(), kHeadChunk, c->D0.as<T>(), c->part1.as<T>());
+    }
   }
   t->mark("bwd_head");
   const bool fuse_head = (mode == 1);
@@ -984,6 +1001,10 @@ int ttgpu_set_generic_path(ttgpu_table* t, int on) {
 
 int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind) {
   return guarded([&] { *kind = t->force_generic ? -1 : f3_kind(t); });
+}
+
+int ttgpu_set_tensor_path(ttgpu_table* t, int on) {
+  return guarded([&] { t->tensor_head = on != 0; });
 }
 
 int ttgpu_set_exact_forward(ttgpu_table* t, int on) {

@@ -280,6 +280,10 @@ class TtTable:
     def set_generic_path(self, on: bool):
         _raise(lib().ttgpu_set_generic_path(self.handle, int(bool(on))))
 
+    def set_tensor_path(self, on: bool):
+        """Backward head contraction on tcgen05 (3xTF32) where eligible (default on)."""
+        _raise(lib().ttgpu_set_tensor_path(self.handle, int(bool(on))))
+
     def fast_path_kind(self) -> int:
         k = C.c_int()
         _raise(lib().ttgpu_fast_path_kind(self.handle, C.byref(k)))

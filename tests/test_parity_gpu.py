@@ -368,10 +368,13 @@ def test_fused_device_step_matches_oracle(orc, exponent):
         assert err <= GRAD_TOL + ulp_slack / max(1.0, np.abs(want_g[k]).max())
 
 
-def test_cfg3_subsample(orc):
-    """configs[2] shape (40M rows, dim 64 = 4x4x4, R=64, P=32) on 256 bags."""
+@pytest.mark.parametrize("tensor", [True, False])
+def test_cfg3_subsample(orc, tensor):
+    """configs[2] shape (40M rows, dim 64 = 4x4x4, R=64, P=32) on 256 bags;
+    head backward on the tcgen05 3xTF32 path and on the FFMA path."""
     p = tt.plan_shapes(40000000, 64, 3, 64, [200, 200, 1000], [4, 4, 4])
     t, cores = make_table(p, np.float32, 5, "cfg3", scale=0.1)
+    t.set_tensor_path(tensor)
     rng = np.random.default_rng(8)
     idx = rng.integers(0, p.num_rows, 256 * 32).astype(np.int64)
     off = np.arange(0, 256 * 32 + 1, 32, dtype=np.int64)
@@ -616,3 +619,29 @@ def test_host_api_graph_replay_matches_eager(orc):
             assert np.all(np.isfinite(t.core(k)))
             assert scaled_max_err(t.core(k), cur[k]) <= GRAD_TOL
         cur = [t.core(k).copy() for k in range(3)]  # track the device state exactly
+
+
+@pytest.mark.parametrize("nbags", [1, 3, 40, 700])
+def test_tensor_head_ragged_runs(orc, nbags):
+    """tcgen05 head backward with runs of 1..32 pairs (padded operand rows),
+    many i1 values, Mean pooling and weights: gradients within 1e-4 of the
+    oracle and of the FFMA path."""
+    p = tt.plan_shapes(40000000, 64, 3, 64, [200, 200, 1000], [4, 4, 4])
+    rng = np.random.default_rng(nbags)
+    # few i0 per i1 for small batches, every i0 for the large one
+    rows = rng.integers(0, p.num_rows, nbags * 5).astype(np.int64)
+    off = np.arange(0, nbags * 5 + 1, 5, dtype=np.int64)
+    w = rng.uniform(0.5, 1.5, len(rows))
+    b = tt.IndexBatch(rows, off, w, tt.Pooling.Mean)
+    g = rng.standard_normal((nbags, 64)).astype(np.float32)
+    op = as_oplan(p)
+    got = {}
+    for tensor in (True, False):
+        t, cores = make_table(p, np.float32, 77, "tc", scale=0.1)
+        t.set_tensor_path(tensor)
+        res = tt.forward_bags(t, b)
+        got[tensor] = tt.backward_bags(t, b, res.context, g)
+    want = orc.backward(op, cores, rows, off, g, w, int(tt.Pooling.Mean))
+    for k in range(3):
+        assert scaled_max_err(got[True].cores[k], want[k]) <= GRAD_TOL
+        assert scaled_max_err(got[True].cores[k], got[False].cores[k]) <= GRAD_TOL
