@@ -26,8 +26,8 @@
 namespace ttgpu {
 namespace tc {
 
-__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+__device__ __forceinline__ void mbar_init1(uint64_t* bar, uint32_t count = 1) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
@@ -55,8 +55,8 @@ struct HeadTc {
   static constexpr int TMEM_COLS = 512;
 };
 
-template <int C1>
-__global__ void __launch_bounds__(256, 1) k_head_bwd_tc(
+template <int C1, int NT>
+__global__ void __launch_bounds__(NT, 1) k_head_bwd_tc(
     DevPlan P, const float* __restrict__ cores, const float* __restrict__ S,
     const uint32_t* __restrict__ pair_key_u, const int* __restrict__ counts,
     const unsigned long long* __restrict__ scan1, int CH, float* __restrict__ D0,
@@ -74,9 +74,9 @@ __global__ void __launch_bounds__(256, 1) k_head_bwd_tc(
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const float* G0 = cores + P.coff[0];
   const float* G1 = cores + P.coff[1];
-  if (tid == 0) {
-    mbar_init1(&bar[0]);
-    mbar_init1(&bar[1]);
+  if (tid == 0) {  // two MMA issuers (D0: thread 0, dG1: thread 32) commit to each buffer
+    mbar_init1(&bar[0], 2);
+    mbar_init1(&bar[1], 2);
   }
   if (wid == 0) tmem_alloc(&tbase, H::TMEM_COLS);
   fence_before_sync();
@@ -96,33 +96,70 @@ __global__ void __launch_bounds__(256, 1) k_head_bwd_tc(
     int run = static_cast<int>(scan1[p0] >> 32) - 1;
     int lo = p0;
     while (lo < p1) {
+      // run end: every warp reads the chunk's (<= 32) keys at once and ballots
       const uint32_t i1 = pair_key_u[lo] / m0;
-      int hi = lo + 1;
-      while (hi < p1 && pair_key_u[hi] / m0 == i1) ++hi;
+      int hi;
+      {
+        const int pp = lo + lane;
+        const bool diff = pp < p1 && pair_key_u[pp] / m0 != i1;
+        const unsigned m = __ballot_sync(0xffffffffu, diff || pp >= p1);
+        hi = lo + (m ? __ffs(m) - 1 : 32);
+      }
       const int np = hi - lo;  // <= CH <= 32
       const int rows = P0 * np;
       const int ksteps_g1 = (rows + 7) / 8;
-      // ---- A_G0 = G0[i0(p)]ᵀ stacked: (r1, k = 4p + a), zero for p >= np
-      for (int e = tid; e < R1 * H::PAIRS; e += blockDim.x) {
-        const int p = e / R1, r = e - p * R1;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (p < np) {
-          const uint32_t i0 = pair_key_u[lo + p] % m0;
-          const float* g = G0 + static_cast<int64_t>(i0) * S0 + r;
-#pragma unroll
-          for (int a = 0; a < P0; ++a) v[a] = __ldg(g + a * R1);
-        }
-        float4 h4, l4;
-        split_tf32(v[0], h4.x, l4.x);
-        split_tf32(v[1], h4.y, l4.y);
-        split_tf32(v[2], h4.z, l4.z);
-        split_tf32(v[3], h4.w, l4.w);
-        const uint32_t o = kmaj_off(r, P0 * p, H::LBO, H::SBO_KR);
-        *reinterpret_cast<float4*>(AGh + o) = h4;
-        *reinterpret_cast<float4*>(AGl + o) = l4;
-      }
       const float* Sp = S + static_cast<int64_t>(lo) * W1;
       const float* G1i = G1 + static_cast<int64_t>(i1) * S1;
+      // this thread's items of a C1 chunk: S (row, 4 columns) x NSI, G1 (r1, 4 columns) x NGI,
+      // loaded into registers one chunk ahead of their smem stores
+      constexpr int NSI = H::ROWS * (KC / 4) / NT, NGI = R1 * (KC / 4) / NT;
+      float4 sreg[NSI], greg[NGI];
+      auto load_chunk = [&](int kc) {
+        const int c0 = kc * KC;
+#pragma unroll
+        for (int j = 0; j < NSI; ++j) {
+          const int e = tid + NT * j, row = e / (KC / 4), q = e - row * (KC / 4);
+          sreg[j] = row < rows
+                        ? __ldg(reinterpret_cast<const float4*>(Sp + static_cast<int64_t>(row) * C1 + c0) + q)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < NGI; ++j) {
+          const int e = tid + NT * j, r = e / (KC / 4), q = e - r * (KC / 4);
+          greg[j] = __ldg(reinterpret_cast<const float4*>(G1i + static_cast<int64_t>(r) * C1 + c0) + q);
+        }
+      };
+      load_chunk(0);
+      // ---- A_G0 = G0[i0(p)]ᵀ stacked: (r1, k = 4p + a), zero for p >= np (loads batched)
+      {
+        constexpr int NAI = R1 * H::PAIRS / NT;
+        float v[NAI][4];
+#pragma unroll
+        for (int j = 0; j < NAI; ++j) {
+          const int e = tid + NT * j, p = e / R1, r = e - p * R1;
+          if (p < np) {
+            const uint32_t i0 = pair_key_u[lo + p] % m0;
+            const float* g = G0 + static_cast<int64_t>(i0) * S0 + r;
+#pragma unroll
+            for (int a = 0; a < P0; ++a) v[j][a] = __ldg(g + a * R1);
+          } else {
+#pragma unroll
+            for (int a = 0; a < P0; ++a) v[j][a] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NAI; ++j) {
+          const int e = tid + NT * j, p = e / R1, r = e - p * R1;
+          float4 h4, l4;
+          split_tf32(v[j][0], h4.x, l4.x);
+          split_tf32(v[j][1], h4.y, l4.y);
+          split_tf32(v[j][2], h4.z, l4.z);
+          split_tf32(v[j][3], h4.w, l4.w);
+          const uint32_t o = kmaj_off(r, P0 * p, H::LBO, H::SBO_KR);
+          *reinterpret_cast<float4*>(AGh + o) = h4;
+          *reinterpret_cast<float4*>(AGl + o) = l4;
+        }
+      }
       for (int kc = 0; kc < NKC; ++kc) {
         const int b = kc & 1;
         if (pend[b]) {  // the MMAs of chunk kc-2 read this buffer
@@ -137,69 +174,72 @@ __global__ void __launch_bounds__(256, 1) k_head_bwd_tc(
         unsigned char* BGh = BSl + H::BS_B;
         unsigned char* BGl = BGh + H::BG_B;
         const int c0 = kc * KC;
-        // S chunk: row = (p, a) = 4p + a, 4 consecutive columns per item
-        for (int e = tid; e < H::ROWS * (KC / 4); e += blockDim.x) {
-          const int row = e / (KC / 4), q = e - row * (KC / 4);
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row < rows) v = __ldg(reinterpret_cast<const float4*>(Sp + static_cast<int64_t>(row) * C1 + c0) + q);
+#pragma unroll
+        for (int j = 0; j < NSI; ++j) {  // S chunk: row = (p, a) = 4p + a
+          const int e = tid + NT * j, row = e / (KC / 4), q = e - row * (KC / 4);
           float4 h4, l4;
-          split_tf32(v.x, h4.x, l4.x);
-          split_tf32(v.y, h4.y, l4.y);
-          split_tf32(v.z, h4.z, l4.z);
-          split_tf32(v.w, h4.w, l4.w);
+          split_tf32(sreg[j].x, h4.x, l4.x);
+          split_tf32(sreg[j].y, h4.y, l4.y);
+          split_tf32(sreg[j].z, h4.z, l4.z);
+          split_tf32(sreg[j].w, h4.w, l4.w);
           const uint32_t oa = kmaj_off(row, 4 * q, H::LBO, H::SBO_KC);
           *reinterpret_cast<float4*>(ASh + oa) = h4;
           *reinterpret_cast<float4*>(ASl + oa) = l4;
           // transposed copy: (n = c, k = row)
           const float hv[4] = {h4.x, h4.y, h4.z, h4.w}, lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t ob = kmaj_off(4 * q + j, row, H::LBO, H::SBO_KR);
-            *reinterpret_cast<float*>(BSh + ob) = hv[j];
-            *reinterpret_cast<float*>(BSl + ob) = lv[j];
+          for (int jj = 0; jj < 4; ++jj) {
+            const uint32_t ob = kmaj_off(4 * q + jj, row, H::LBO, H::SBO_KR);
+            *reinterpret_cast<float*>(BSh + ob) = hv[jj];
+            *reinterpret_cast<float*>(BSl + ob) = lv[jj];
           }
         }
-        // G1 chunk: (n = r1, k = c)
-        for (int e = tid; e < R1 * (KC / 4); e += blockDim.x) {
-          const int r = e / (KC / 4), q = e - r * (KC / 4);
-          const float4 v = __ldg(reinterpret_cast<const float4*>(G1i + static_cast<int64_t>(r) * C1 + c0) + q);
+#pragma unroll
+        for (int j = 0; j < NGI; ++j) {  // G1 chunk: (n = r1, k = c)
+          const int e = tid + NT * j, r = e / (KC / 4), q = e - r * (KC / 4);
           float4 h4, l4;
-          split_tf32(v.x, h4.x, l4.x);
-          split_tf32(v.y, h4.y, l4.y);
-          split_tf32(v.z, h4.z, l4.z);
-          split_tf32(v.w, h4.w, l4.w);
+          split_tf32(greg[j].x, h4.x, l4.x);
+          split_tf32(greg[j].y, h4.y, l4.y);
+          split_tf32(greg[j].z, h4.z, l4.z);
+          split_tf32(greg[j].w, h4.w, l4.w);
           const uint32_t o = kmaj_off(r, 4 * q, H::LBO, H::SBO_KC);
           *reinterpret_cast<float4*>(BGh + o) = h4;
           *reinterpret_cast<float4*>(BGl + o) = l4;
         }
+        if (kc + 1 < NKC) load_chunk(kc + 1);  // in flight during the MMAs of this chunk
         fence_smem_to_async();
         __syncthreads();
+        // descriptors: start address field (bits 0..13, 16-byte units) advanced
+        // from a per-operand base -- no carry: every operand lies inside the CTA's smem
         if (tid == 0) {
           fence_after_sync();
           // D0 (128 x 64) += S_chunk (128 x KC) · G1_chunkᵀ (KC x 64)
+          const uint64_t ah0 = smem_desc(smem_addr(ASh), H::LBO, H::SBO_KC);
+          const uint64_t al0 = smem_desc(smem_addr(ASl), H::LBO, H::SBO_KC);
+          const uint64_t bh0 = smem_desc(smem_addr(BGh), H::LBO, H::SBO_KC);
+          const uint64_t bl0 = smem_desc(smem_addr(BGl), H::LBO, H::SBO_KC);
 #pragma unroll
           for (int ks = 0; ks < KC / 8; ++ks) {
-            const uint32_t o = ks * 256;
-            const uint64_t ah = smem_desc(smem_addr(ASh + o), H::LBO, H::SBO_KC);
-            const uint64_t al = smem_desc(smem_addr(ASl + o), H::LBO, H::SBO_KC);
-            const uint64_t bh = smem_desc(smem_addr(BGh + o), H::LBO, H::SBO_KC);
-            const uint64_t bl = smem_desc(smem_addr(BGl + o), H::LBO, H::SBO_KC);
+            const uint64_t o = static_cast<uint64_t>(ks * 256 / 16);
             const uint32_t first = (kc == 0 && ks == 0) ? 0u : 1u;
-            mma_tf32(tm, al, bh, id_d0, first);
-            mma_tf32(tm, ah, bl, id_d0, 1u);
-            mma_tf32(tm, ah, bh, id_d0, 1u);
+            mma_tf32(tm, al0 + o, bh0 + o, id_d0, first);
+            mma_tf32(tm, ah0 + o, bl0 + o, id_d0, 1u);
+            mma_tf32(tm, ah0 + o, bh0 + o, id_d0, 1u);
           }
+          commit(&bar[b]);
+        } else if (tid == 32) {
+          fence_after_sync();
           // dG1[:, c0:c0+KC] (64 x KC) = G0stackᵀ (64 x rows) · S_chunk (rows x KC)
           const uint32_t dg = tm + 64 + static_cast<uint32_t>(c0);
+          const uint64_t ah0 = smem_desc(smem_addr(AGh), H::LBO, H::SBO_KR);
+          const uint64_t al0 = smem_desc(smem_addr(AGl), H::LBO, H::SBO_KR);
+          const uint64_t bh0 = smem_desc(smem_addr(BSh), H::LBO, H::SBO_KR);
+          const uint64_t bl0 = smem_desc(smem_addr(BSl), H::LBO, H::SBO_KR);
           for (int ks = 0; ks < ksteps_g1; ++ks) {
-            const uint32_t o = ks * 256;
-            const uint64_t ah = smem_desc(smem_addr(AGh + o), H::LBO, H::SBO_KR);
-            const uint64_t al = smem_desc(smem_addr(AGl + o), H::LBO, H::SBO_KR);
-            const uint64_t bh = smem_desc(smem_addr(BSh + o), H::LBO, H::SBO_KR);
-            const uint64_t bl = smem_desc(smem_addr(BSl + o), H::LBO, H::SBO_KR);
-            mma_tf32(dg, al, bh, id_g1, ks == 0 ? 0u : 1u);
-            mma_tf32(dg, ah, bl, id_g1, 1u);
-            mma_tf32(dg, ah, bh, id_g1, 1u);
+            const uint64_t o = static_cast<uint64_t>(ks * 256 / 16);
+            mma_tf32(dg, al0 + o, bh0 + o, id_g1, ks == 0 ? 0u : 1u);
+            mma_tf32(dg, ah0 + o, bl0 + o, id_g1, 1u);
+            mma_tf32(dg, ah0 + o, bh0 + o, id_g1, 1u);
           }
           commit(&bar[b]);
         }
@@ -216,13 +256,14 @@ __global__ void __launch_bounds__(256, 1) k_head_bwd_tc(
         }
       fence_after_sync();
       // ---- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
-      const int q = wid & 3, half = wid >> 2;
-      {  // D0: row m = 32q + lane (M=128: row m in lane m), columns [32 half, +32)
+      constexpr int NG = NT / 128;  // warp groups: columns split between them
+      const int q = wid & 3, grp = wid >> 2;
+      {  // D0: row m = 32q + lane (M=128: row m in lane m), columns [64/NG grp, +64/NG)
         const int m = 32 * q + lane;
 #pragma unroll
-        for (int c16 = 0; c16 < 2; ++c16) {
+        for (int c16 = 0; c16 < 4 / NG; ++c16) {
           float v[16];
-          const int col = 32 * half + 16 * c16;
+          const int col = (64 / NG) * grp + 16 * c16;
           ld_32x32b_x16(tm + (static_cast<uint32_t>(32 * q) << 16) + col, v);
           if (m < rows) {
             float* dst = D0 + static_cast<int64_t>(lo + m / P0) * S0 + (m % P0) * R1 + col;
@@ -232,13 +273,13 @@ __global__ void __launch_bounds__(256, 1) k_head_bwd_tc(
           }
         }
       }
-      {  // dG1 (M=64: row r in lane (r%16) + 32*(r/16)), columns [C1/2 * half, +C1/2)
+      {  // dG1 (M=64: row r in lane (r%16) + 32*(r/16)), columns [C1/NG grp, +C1/NG)
         const int r = 16 * q + lane;
         float* dst = partials + static_cast<int64_t>(run) * S1 + static_cast<int64_t>(r) * C1;
 #pragma unroll 1
-        for (int c16 = 0; c16 < C1 / 32; ++c16) {
+        for (int c16 = 0; c16 < C1 / (16 * NG); ++c16) {
           float v[16];
-          const int col = (C1 / 2) * half + 16 * c16;
+          const int col = (C1 / NG) * grp + 16 * c16;
           ld_32x32b_x16(tm + (static_cast<uint32_t>(32 * q) << 16) + 64 + col, v);
           if (lane < 16) {
 #pragma unroll

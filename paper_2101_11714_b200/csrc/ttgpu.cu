@@ -687,9 +687,10 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
       // tensor-core head (head_tc.cuh): cfg3's shape class, P0 = 4, R1 = 64, C1 = 256
       if (t->tensor_head && d == 3 && P.n[0] == tc::HeadTc::P0 && P.r[1] == tc::HeadTc::R1 &&
           P.C1 == 256 && kHeadChunk <= tc::HeadTc::PAIRS) {
-        auto kt = tc::k_head_bwd_tc<256>;
+        constexpr int kNT = 512;
+        auto kt = tc::k_head_bwd_tc<256, kNT>;
         set_smem(kt, tc::HeadTc::SMEM);
-        kt<<<grid_for(ucap, kHeadChunk, t->num_sms, 1), 256, tc::HeadTc::SMEM, st>>>(
+        kt<<<grid_for(ucap, kHeadChunk, t->num_sms, 1), kNT, tc::HeadTc::SMEM, st>>>(
             P, cores, c->S.as<float>(), c->pair_key_u.as<uint32_t>(), c->counts.as<int>(),
             c->scan1.as<unsigned long long>(), kHeadChunk, c->D0.as<float>(), c->part1.as<float>());
         launched = true;

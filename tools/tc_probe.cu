@@ -31,6 +31,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 struct Case {
   int M, N, K, a_mn, b_mn, split3;
+  int swap = 0;  // MN-major: descriptor LBO field = MN-group stride, SBO field = K-group stride
 };
 
 // A: M x K row-major fp32, B: K x N row-major fp32 (global). out: 128 lanes x N.
@@ -80,10 +81,11 @@ __global__ void probe(Case c, const float* A, const float* B, float* out) {
     uint32_t acc = 0;
     for (int ks = 0; ks < K / 8; ++ks) {
       const uint32_t ao = ks * a_step, bo = ks * b_step;
-      const uint64_t ah = tc::smem_desc(tc::smem_addr(Ah + ao), a_lbo, a_sbo);
-      const uint64_t al = tc::smem_desc(tc::smem_addr(Al + ao), a_lbo, a_sbo);
-      const uint64_t bh = tc::smem_desc(tc::smem_addr(Bh + bo), b_lbo, b_sbo);
-      const uint64_t bl = tc::smem_desc(tc::smem_addr(Bl + bo), b_lbo, b_sbo);
+      const bool sa = c.swap && c.a_mn, sb = c.swap && c.b_mn;
+      const uint64_t ah = tc::smem_desc(tc::smem_addr(Ah + ao), sa ? a_sbo : a_lbo, sa ? a_lbo : a_sbo);
+      const uint64_t al = tc::smem_desc(tc::smem_addr(Al + ao), sa ? a_sbo : a_lbo, sa ? a_lbo : a_sbo);
+      const uint64_t bh = tc::smem_desc(tc::smem_addr(Bh + bo), sb ? b_sbo : b_lbo, sb ? b_lbo : b_sbo);
+      const uint64_t bl = tc::smem_desc(tc::smem_addr(Bl + bo), sb ? b_sbo : b_lbo, sb ? b_lbo : b_sbo);
       if (c.split3) {
         tc::mma_tf32(tm, al, bh, id, acc);
         acc = 1;
@@ -162,8 +164,8 @@ int run(Case c, bool integer, bool onehot = false) {
   // row m of D -> which TMEM lane holds it (first exact / closest match)
   int bad = 0;
   double maxrel = 0;
-  std::printf("case M=%d N=%d K=%d a_mn=%d b_mn=%d split3=%d %s: lanes of rows", c.M, c.N, c.K,
-              c.a_mn, c.b_mn, c.split3, integer ? "int" : "normal");
+  std::printf("case M=%d N=%d K=%d a_mn=%d b_mn=%d split3=%d swap=%d %s: lanes of rows", c.M, c.N,
+              c.K, c.a_mn, c.b_mn, c.split3, c.swap, integer ? "int" : "normal");
   for (int m = 0; m < c.M; ++m) {
     int best = -1;
     double be = 1e300;
@@ -194,9 +196,12 @@ int main() {
       {64, 256, 16, 0, 1, 0}, {128, 64, 32, 0, 0, 1}, {64, 32, 32, 0, 1, 1},
   };
   for (const Case& c : cases) bad += run(c, true);
-  run({128, 8, 8, 0, 1, 0}, true, true);
-  run({128, 16, 16, 0, 1, 0}, true, true);
-  run({128, 8, 8, 0, 0, 0}, true, true);
+  Case sw[] = {{128, 32, 16, 0, 1, 0, 1}, {128, 64, 16, 1, 0, 0, 1}, {64, 32, 32, 0, 1, 0, 1},
+               {64, 32, 32, 0, 1, 1, 1}, {128, 64, 32, 1, 1, 1, 1}};
+  int bad_sw = 0;
+  for (const Case& c : sw) bad_sw += run(c, true);
+  std::printf(bad_sw ? "MN-major (swapped fields) FAILED\n" : "MN-major (swapped fields) OK\n");
+  run({128, 16, 16, 0, 1, 0, 1}, true, true);
   // accuracy: 1xTF32 vs 3xTF32 on normal data
   bad += 0 * run({128, 64, 128, 0, 0, 0}, false);
   bad += 0 * run({128, 64, 128, 0, 0, 1}, false);
