@@ -31,6 +31,18 @@
 namespace ttgpu {
 namespace f3 {
 
+// Programmatic dependent launch (the fast-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization when the table enables it).
+// Every kernel waits for its predecessor grid's completion (griddepcontrol.wait:
+// a no-op without PDL) before touching memory, so overlap is limited to launch
+// and scheduling; g_pdl_early additionally lets the dependent grid be scheduled
+// as soon as every CTA of this one has started.
+__device__ int g_pdl_early = 0;
+__device__ __forceinline__ void pdl_entry() {
+  if (g_pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 struct Geo {
   int m0, m1, m2;
   uint32_t m12;  // m1 * m2
@@ -178,6 +190,7 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
                                                uint32_t* __restrict__ tot1, uint32_t* __restrict__ tot2,
                                                unsigned long long* __restrict__ bad,
                                                int* __restrict__ errs, int32_t* __restrict__ solo) {
+  pdl_entry();
   extern __shared__ uint32_t shist[];  // m1 + m2
   uint32_t* sh1 = shist;
   uint32_t* sh2 = shist + g.m1;
@@ -291,6 +304,7 @@ __device__ __forceinline__ uint32_t n_groups(uint32_t tk) {
 
 __global__ void __launch_bounds__(kScanThreads) f3_scan(ScanArgs a1, ScanArgs a2, int nb1, int NT,
                                                         int64_t L) {
+  pdl_entry();
   using Scan = cub::BlockScan<uint32_t, kScanThreads>;
   using Red = cub::BlockReduce<uint32_t, kScanThreads>;
   __shared__ union {
@@ -494,6 +508,7 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
                                                   uint32_t* __restrict__ tot,
                                                   const int32_t* __restrict__ solo,
                                                   uint4* __restrict__ rec1) {
+  pdl_entry();
   extern __shared__ uint32_t wc[];  // 8 x max(m1, m2)
   // f3_scan has consumed the bucket totals: clear them for the next batch
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.m1 + g.m2; k += gridDim.x * blockDim.x)
@@ -544,6 +559,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint16_t* __restrict__ slot_of_pos,
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots) {
+  pdl_entry();
   using SM = FwdSmem<D>;
   extern __shared__ __align__(128) float sm[];
   float* G1s = sm;
@@ -706,6 +722,7 @@ template <int N, bool kExact>
 __global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
                         const double* __restrict__ w, int mean, const float* __restrict__ y,
                         float* __restrict__ out) {
+  pdl_entry();
   constexpr int Q = N / 4;
   for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < B * Q;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -749,6 +766,7 @@ __global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cor
                                                 const uint16_t* __restrict__ slot_of_pos,
                                                 const int* __restrict__ tile_nslots,
                                                 float* __restrict__ Sbuf) {
+  pdl_entry();
   constexpr int EPL = (D::W1 + 31) / 32;  // row elements per lane
   // distinct G2 rows a lane reads per member: r = (lane + 32k) % R2 repeats with period NR
   constexpr int NR = D::R2 > 32 ? D::R2 / 32 : 1;
@@ -933,6 +951,7 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
     unsigned char* __restrict__ d0mask) {
+  pdl_entry();
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
   extern __shared__ __align__(128) float sm[];
@@ -1202,6 +1221,7 @@ __global__ void __launch_bounds__(128) f3_bwd2(
     const int32_t* __restrict__ lk_bag, const float* __restrict__ alpha,
     const float* __restrict__ grad, const float* __restrict__ Hbuf, float* __restrict__ part2,
     int* __restrict__ has2) {
+  pdl_entry();
   constexpr int NW = 4, U = 4;
   constexpr int CH = (D::R2 + 31) / 32;
   __shared__ float4 red[NW][CH * 32];
@@ -1412,6 +1432,7 @@ template <class D, int MODE>
 __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restrict__ cores,
                                                        float* __restrict__ grads, CombineArgs A,
                                                        float lr) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
   int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -15,6 +15,28 @@ void f3_free(F3Bufs* f) { delete f; }
 
 namespace {
 
+// Launch of a fast-path kernel: plain, or with programmatic dependent launch
+// (the kernels begin with f3::pdl_entry(), so both are correct).
+template <typename... KArgs, typename... Args>
+void f3_launch(int pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               Args... args) {
+  if (!pdl) {
+    k<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
 constexpr int kF3MaxHist = 48 * 1024;  // histogram entries one f3_scan CTA stages (kScanKeys x NT)
 
 // lookups per hist/scatter CTA: 512 * LPT, LPT in {1, 2, ..., 32}; 0 = infeasible.
@@ -45,7 +67,7 @@ template <int LPT>
 void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const int64_t* idx,
                  int64_t L, int NT, const int64_t* off, int64_t B, const double* w, int pooling,
                  F3Bufs& f, int32_t* lk_bag, float* alpha, ttgpu_table* t) {
-  f3::f3_hist<float, LPT><<<grid, 512, smem, st>>>(
+  f3_launch(t->pdl, f3::f3_hist<float, LPT>, dim3(grid), dim3(512), smem, st, 
       g, idx, L, NT, off, B, w, pooling, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
       f.d2.as<uint16_t>(), lk_bag, alpha, f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
       f.tot.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, t->d_bad(), t->d_struct(),
@@ -124,13 +146,13 @@ struct F3Runner {
       set_smem(f3::f3_scan, sm);
       const int nb1 = (g.m1 + f3::kScanKeys - 1) / f3::kScanKeys;
       const int nb2 = (g.m2 + f3::kScanKeys - 1) / f3::kScanKeys;
-      f3::f3_scan<<<nb1 + nb2, f3::kScanThreads, sm, st>>>(a1, a2, nb1, NT, L);
+      f3_launch(t->pdl, f3::f3_scan, dim3(nb1 + nb2), dim3(f3::kScanThreads), sm, st, a1, a2, nb1, NT, L);
     }
     t->mark("scan");
     {
       const size_t sm = 4 * 8 * static_cast<size_t>(Kmax);
       set_smem(f3::f3_scatter, sm);
-      f3::f3_scatter<<<NT, 256, sm, st>>>(g, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
+      f3_launch(t->pdl, f3::f3_scatter, dim3(NT), dim3(256), sm, st, g, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
                                           f.d2.as<uint16_t>(), L, TL, NT, f.hist1.as<uint32_t>(),
                                           f.hist2.as<uint32_t>(), f.perm1.as<uint32_t>(),
                                           f.perm2.as<uint32_t>(), f.tot.as<uint32_t>(),
@@ -142,7 +164,7 @@ struct F3Runner {
       auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
       set_smem(kern, sm);
       const int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
-      kern<<<grid, f3::kThreads, sm, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
+      f3_launch(t->pdl, kern, dim3(grid), dim3(f3::kThreads), sm, st, g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
                                            f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out,
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
@@ -151,7 +173,7 @@ struct F3Runner {
     t->mark("f3_fwd");
     {
       auto kern = exact ? f3::f3_pool<D::N, true> : f3::f3_pool<D::N, false>;
-      kern<<<grid_for(B * (D::N / 4), 256, t->num_sms, 8), 256, 0, st>>>(
+      f3_launch(t->pdl, kern, dim3(grid_for(B * (D::N / 4), 256, t->num_sms, 8)), dim3(256), 0, st, 
           off, B, L, w, pooling, f.y.as<float>(), out);
     }
     t->mark("pool");
@@ -175,18 +197,18 @@ struct F3Runner {
     f.d0mask.ensure(static_cast<size_t>(grid1) * g.m0);
     f.Sbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
     t->mark("bwd_begin");
-    f3::f3_srows<D><<<(f.max_tiles1 * 32 + 255) / 256, 256, 0, st>>>(
+    f3_launch(t->pdl, f3::f3_srows<D>, dim3((f.max_tiles1 * 32 + 255) / 256), dim3(256), 0, st, 
         t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.max_tiles1,
         f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
         f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>());
     t->mark("f3_srows");
-    k1<<<grid1, f3::kThreads, sm1, st>>>(g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
+    f3_launch(t->pdl, k1, dim3(grid1), dim3(f3::kThreads), sm1, st, g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
                                          f.ntiles.as<int>(), f.Sbuf.as<float>(),
                                          f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(),
                                          f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
                                          f.d0mask.as<unsigned char>());
     t->mark("f3_bwd1");
-    f3::f3_bwd2<D><<<grid2, 128, 0, st>>>(g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
+    f3_launch(t->pdl, f3::f3_bwd2<D>, dim3(grid2), dim3(128), 0, st, g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
                                           f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag,
                                           alpha, grad, f.Hbuf.as<float>(), f.part2.as<float>(),
                                           f.has2.as<int>());
@@ -220,7 +242,7 @@ struct F3Runner {
       A.gtouch = f.gtouch.as<int>();
       A.counters = f.counters.as<int>();
       auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
-      ck<<<(tasks * 32 + f3::kThreads - 1) / f3::kThreads, f3::kThreads, 0, st>>>(
+      f3_launch(t->pdl, ck, dim3((tasks * 32 + f3::kThreads - 1) / f3::kThreads), dim3(f3::kThreads), 0, st, 
           g, t->cores.as<float>(), t->grads.as<float>(), A, lr);
     }
     t->mark("f3_combine");

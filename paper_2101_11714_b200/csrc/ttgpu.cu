@@ -194,6 +194,7 @@ struct ttgpu_table {
   bool exact = true;  // forward bit-identical to the reference (no FMA contraction)
   bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
   bool tensor_head = true;     // head backward on tcgen05 (3xTF32) where the shape allows it
+  int pdl = 0;                 // fast-path launches: 0 plain, 1 programmatic dependent launch
   // optional phase timing (CUDA events between pipeline phases)
   // Marks recorded while the stream is being captured become event-record nodes of
   // the graph (cudaEventRecordExternal) and stay owned by it: every graph launch
@@ -924,6 +925,12 @@ int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* r
     t->stream = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, device));
+    {  // TTGPU_PDL: 0 plain launches, 1 programmatic dependent launch, 2 PDL + early trigger
+      const char* e = std::getenv("TTGPU_PDL");
+      t->pdl = e ? std::atoi(e) : 0;
+      const int early = t->pdl >= 2 ? 1 : 0;
+      CK(cudaMemcpyToSymbol(f3::g_pdl_early, &early, sizeof(int)));
+    }
     std::vector<int64_t> coff;
     t->dp = make_devplan(t->plan, coff, t->total);
     t->cores.ensure(t->esz * t->total);
