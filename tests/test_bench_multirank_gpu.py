@@ -35,7 +35,7 @@ def test_two_ranks_on_one_gpu(extra, want):
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
-    assert d["config"]["gradient_reduce"] == want
+    assert d["execution"]["gradient_reduce"] == want
     assert d["value"] > 0 and d["e2e"]["value"] > 0
 
 
