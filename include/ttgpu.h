@@ -90,6 +90,15 @@ int ttgpu_set_exact_forward(ttgpu_table* t, int on);
  * within the 1e-4 tolerance.  No reference counterpart (the reference is CPU
  * only, embedding_ops.hpp:335-347). */
 int ttgpu_set_tensor_path(ttgpu_table* t, int on);
+/* Fast path: sort the batch with the one-kernel cooperative sort (gsort.cuh) (1 = default,
+ * used when the batch fits one co-resident grid) or with the three-kernel
+ * histogram / scan / scatter sort (0).  Results never depend on it. */
+int ttgpu_set_grid_sort(ttgpu_table* t, int on);
+/* Fast path: chunked kernels (1: per-bucket chunks of 64 lookups, CTA-wide
+ * i0 dedup, fused S / dG1 / D0 backward; fastc.cuh) or the one-warp
+ * 32-lookup tile kernels (0 = default; measured faster at cfg2).  Forward
+ * outputs are bit-identical either way; gradients agree within 1e-4. */
+int ttgpu_set_chunked(ttgpu_table* t, int on);
 int ttgpu_set_generic_path(ttgpu_table* t, int on);
 int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind);
 int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out); /* tt_table.hpp:84 */

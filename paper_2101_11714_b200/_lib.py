@@ -37,6 +37,8 @@ _SIGS = {
     "ttgpu_set_exact_forward": (C.c_int, [vp, C.c_int]),
     "ttgpu_set_generic_path": (C.c_int, [vp, C.c_int]),
     "ttgpu_set_tensor_path": (C.c_int, [vp, C.c_int]),
+    "ttgpu_set_grid_sort": (C.c_int, [vp, C.c_int]),
+    "ttgpu_set_chunked": (C.c_int, [vp, C.c_int]),
     "ttgpu_fast_path_kind": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "ttgpu_mutation_counter": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "ttgpu_ctx_create": (C.c_int, [vp, vpp]),

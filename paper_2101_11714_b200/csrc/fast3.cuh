@@ -1,5 +1,7 @@
 // Fast path for 3-core tables (every BASELINE config): compile-time TT shape,
-// 9 kernels per fwd+bwd+SGD step, deterministic, no floating-point atomics.
+// 6 kernels per fwd+bwd+SGD step (f3_gsort, gsort.cuh, replaces the first
+// three below when the batch fits one co-resident grid), deterministic, no
+// floating-point atomics.
 //
 //   f3_hist     decode + validate; per-CTA histograms of two sort keys
 //               (k1 = i1, k2 = i2); lookup->bag map, backward alpha, solo bags
@@ -9,8 +11,8 @@
 //               plus sorted (lookup, digits, solo) records for f3_fwd
 //   f3_fwd      per i1-tile, pipelined one tile ahead: slots = distinct i0
 //               (match_any), operands by bulk copy onto mbarriers,
-//               H(slot) = G0[i0]·G1[i1], y = H·G2[i2]; single-lookup bags pooled here
-//   f3_pool     per multi-lookup bag, lookup order: out = Σ T(w)·y (Mean rescale)
+//               H(slot) = G0[i0]·G1[i1], y = H·G2[i2]; bags pooled by their last
+//               finished lookup (pool_if_last), single-lookup bags directly
 //   f3_srows    warp per i1-tile: S(slot) = Σ D1, D1 = D2·G2ᵀ
 //   f3_bwd1     per i1-tile (TMA-staged S and G0 rows): dG1 += Σ G0ᵀS, D0 = S·G1ᵀ
 //   f3_bwd2     per i2-tile: dG2 += Σ H(lookup)ᵀ D2 (H rows saved by f3_fwd)
@@ -94,6 +96,39 @@ __device__ __forceinline__ void add4(float4& a, const float4 b) {
   a.w += b.w;
 }
 
+// Pooling of a multi-lookup bag by its last finished (lookup, row) task: every
+// task of a bag's lookups counts itself in bag_cnt[bag] after storing its y row
+// (fenced); the task completing the count sums the bag's y rows in lookup
+// order -- f3_pool's arithmetic (embedding_ops.hpp:232-249) -- and stores the
+// pooled row.  The sort kernel zeroes bag_cnt for every bag of the batch and
+// writes the (zero) rows of empty bags, so no separate pooling pass runs.
+template <int N, bool kExact>
+__device__ __forceinline__ void pool_if_last(int bag, int parts, const int64_t* __restrict__ off,
+                                             int64_t L, const double* __restrict__ w, int mean,
+                                             const float* y, float* __restrict__ out, int* bag_cnt) {
+  __threadfence();  // this task's y row before its count
+  const int64_t s = off[bag], e = off[bag + 1];
+  if (atomicAdd(bag_cnt + bag, 1) != static_cast<int>(e - s) * parts - 1) return;
+  __threadfence();  // every other task's row is visible past the count
+  const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
+  const float inv = static_cast<float>(1.0 / static_cast<double>(e - s));
+#pragma unroll
+  for (int c = 0; c < N / 4; ++c) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t l = lo; l < hi; ++l) {
+      const float a = static_cast<float>(w ? w[l] : 1.0);
+      acc = madd4<float, kExact>(a, __ldcg(reinterpret_cast<const float4*>(y + l * N) + c), acc);
+    }
+    if (mean && e - s > 1) {
+      acc.x = __fmul_rn(acc.x, inv);
+      acc.y = __fmul_rn(acc.y, inv);
+      acc.z = __fmul_rn(acc.z, inv);
+      acc.w = __fmul_rn(acc.w, inv);
+    }
+    reinterpret_cast<float4*>(out + static_cast<int64_t>(bag) * N)[c] = acc;
+  }
+}
+
 // ---- TMA bulk copies (cp.async.bulk, sm_90+/sm_100a) with mbarrier completion
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -124,6 +159,16 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Sorted record of key 1 (lookup order within an i1 bucket):
+//   x = lookup, y = i0 | i2 << 16, z = bag | (single-lookup bag) << 31, w = alpha bits
+__device__ __forceinline__ uint4 make_rec(uint32_t l, uint32_t d02, int32_t solo, int32_t bag, float alpha) {
+  return make_uint4(l, d02, static_cast<uint32_t>(bag) | (solo >= 0 ? 0x80000000u : 0u), __float_as_uint(alpha));
+}
+// the bag a record's lookup is pooled into directly (its only lookup), else -1
+__device__ __forceinline__ int rec_solo(const uint4& r) {
+  return (r.z >> 31) ? static_cast<int>(r.z & 0x7fffffffu) : -1;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -189,7 +234,8 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
                                                uint32_t* __restrict__ hist2,
                                                uint32_t* __restrict__ tot1, uint32_t* __restrict__ tot2,
                                                unsigned long long* __restrict__ bad,
-                                               int* __restrict__ errs, int32_t* __restrict__ solo) {
+                                               int* __restrict__ errs, int32_t* __restrict__ solo,
+                                               float* __restrict__ out, int N, int* __restrict__ bag_cnt) {
   pdl_entry();
   extern __shared__ uint32_t shist[];  // m1 + m2
   uint32_t* sh1 = shist;
@@ -261,6 +307,9 @@ __global__ void __launch_bounds__(512) f3_hist(Geo g, const int64_t* __restrict_
     if (b == B - 1 && e != L) atomicOr(errs, 4);
     const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
     const double sz = static_cast<double>(e - s);
+    bag_cnt[b] = 0;
+    if (e == s)  // an empty bag pools to zeros (no lookup will)
+      for (int c = 0; c < N; c += 4) reinterpret_cast<float4*>(out + b * N + c)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t l = lo; l < hi; ++l) {
       lk_bag[l] = static_cast<int32_t>(b);
       solo[l] = e - s == 1 ? static_cast<int32_t>(b) : -1;  // pooled by f3_fwd directly
@@ -423,7 +472,9 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
                                             const uint16_t* __restrict__ dg0 = nullptr,
                                             const uint16_t* __restrict__ dg2 = nullptr,
                                             const int32_t* __restrict__ solo = nullptr,
-                                            uint4* __restrict__ rec = nullptr) {
+                                            uint4* __restrict__ rec = nullptr,
+                                            const int32_t* __restrict__ lk_bag = nullptr,
+                                            const float* __restrict__ alpha = nullptr) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int per = TL / 8;
@@ -488,8 +539,8 @@ __device__ __forceinline__ void scatter_one(const uint16_t* __restrict__ key, in
         perm[pos] = static_cast<uint32_t>(l);
         // sorted record (position -> lookup, i0 | i2 << 16, solo bag) for f3_fwd
         if (rec)
-          rec[pos] = make_uint4(static_cast<uint32_t>(l), dg0[l] | (static_cast<uint32_t>(dg2[l]) << 16),
-                                static_cast<uint32_t>(solo[l]), 0u);
+          rec[pos] = make_rec(static_cast<uint32_t>(l), dg0[l] | (static_cast<uint32_t>(dg2[l]) << 16),
+                              solo[l], lk_bag[l], alpha[l]);
         if (lane == __ffs(peers) - 1) my[k] += __popc(peers);
       }
       __syncwarp();
@@ -507,13 +558,15 @@ __global__ void __launch_bounds__(256) f3_scatter(Geo g, const uint16_t* __restr
                                                   uint32_t* __restrict__ perm2,
                                                   uint32_t* __restrict__ tot,
                                                   const int32_t* __restrict__ solo,
-                                                  uint4* __restrict__ rec1) {
+                                                  uint4* __restrict__ rec1,
+                                                  const int32_t* __restrict__ lk_bag,
+                                                  const float* __restrict__ alpha) {
   pdl_entry();
   extern __shared__ uint32_t wc[];  // 8 x max(m1, m2)
   // f3_scan has consumed the bucket totals: clear them for the next batch
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.m1 + g.m2; k += gridDim.x * blockDim.x)
     tot[k] = 0u;
-  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc, d0, d2, solo, rec1);
+  scatter_one(d1, g.m1, L, TL, NT, hoff1, perm1, wc, d0, d2, solo, rec1, lk_bag, alpha);
   scatter_one(d2, g.m2, L, TL, NT, hoff2, perm2, wc);
 }
 
@@ -558,7 +611,9 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint32_t* __restrict__ hloc,
                                                    uint16_t* __restrict__ slot_of_pos,
                                                    uint16_t* __restrict__ tile_i0,
-                                                   int* __restrict__ tile_nslots) {
+                                                   int* __restrict__ tile_nslots,
+                                                   const int64_t* __restrict__ off, int64_t L, int mean,
+                                                   int* __restrict__ bag_cnt) {
   pdl_entry();
   using SM = FwdSmem<D>;
   extern __shared__ __align__(128) float sm[];
@@ -603,7 +658,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     if (act) {
       lk_l[lane] = l;
       lk_slot[lane] = s;
-      lk_solo[lane] = static_cast<int>(r.z);
+      lk_solo[lane] = static_cast<int>(r.z);  // bag | single-lookup bit (make_rec)
       slot_of_pos[tl.start + lane] = static_cast<uint16_t>(s);
       hloc[l] = static_cast<uint32_t>(tl.start + s);
     }
@@ -700,50 +755,19 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
         for (int r = 0; r < D::R2; ++r) acc = madd4<float, kExact>(hrow[r], g2[r], acc);
-        const int solo = lk_solo[i];
-        if (solo >= 0) {  // the bag's only lookup: pooled here, as f3_pool would (0 + w·y)
+        const int z = lk_solo[i];
+        if (z < 0) {  // the bag's only lookup: pooled here, (0 + w·y, the pooling arithmetic)
           const float wl = w ? static_cast<float>(w[lk_l[i]]) : 1.f;
-          reinterpret_cast<float4*>(out + static_cast<int64_t>(solo) * D::N)[a] =
+          reinterpret_cast<float4*>(out + static_cast<int64_t>(z & 0x7fffffff) * D::N)[a] =
               madd4<float, kExact>(wl, acc, make_float4(0.f, 0.f, 0.f, 0.f));
         } else {
           reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
+          pool_if_last<D::N, kExact>(z, D::P1, off, L, w, mean, y, out, bag_cnt);
         }
       }
     }
     __syncthreads();  // G2s / Hs free
     if (wid == 0 && t + G < nt) issue_g2();
-  }
-}
-
-// ------------------------------------------------------------- f3_pool ---
-// One thread per (bag, float4 column chunk); lookup-ascending accumulation.
-// Bags of exactly one lookup were written by f3_fwd (same arithmetic).
-template <int N, bool kExact>
-__global__ void f3_pool(const int64_t* __restrict__ off, int64_t B, int64_t L,
-                        const double* __restrict__ w, int mean, const float* __restrict__ y,
-                        float* __restrict__ out) {
-  pdl_entry();
-  constexpr int Q = N / 4;
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < B * Q;
-       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t b = q / Q;
-    const int c = static_cast<int>(q - b * Q);
-    const int64_t s = off[b], e = off[b + 1];
-    if (e - s == 1) continue;  // single-lookup bag: written by f3_fwd
-    const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t l = lo; l < hi; ++l) {
-      const float a = static_cast<float>(w ? w[l] : 1.0);
-      acc = madd4<float, kExact>(a, reinterpret_cast<const float4*>(y + l * N)[c], acc);
-    }
-    if (mean && e - s > 1) {
-      const float inv = static_cast<float>(1.0 / static_cast<double>(e - s));
-      acc.x = __fmul_rn(acc.x, inv);
-      acc.y = __fmul_rn(acc.y, inv);
-      acc.z = __fmul_rn(acc.z, inv);
-      acc.w = __fmul_rn(acc.w, inv);
-    }
-    reinterpret_cast<float4*>(out + b * N)[c] = acc;
   }
 }
 
@@ -1506,3 +1530,5 @@ __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restri
 
 }  // namespace f3
 }  // namespace ttgpu
+#include "gsort.cuh"
+#include "fastc.cuh"

@@ -5,10 +5,11 @@ namespace ttgpu {
 struct F3Bufs {
   DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, rec1, solo, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
-      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf;
+      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf, gs_hist, gs_tot, bag_cnt;
   f3::Geo geo{};
   int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
+  bool chunked = false;  // forward ran the chunked kernels (fastc.cuh); backward follows it
 };
 
 void f3_free(F3Bufs* f) { delete f; }
@@ -66,12 +67,27 @@ f3::Geo make_geo(const ttgpu_table* t) {
 template <int LPT>
 void launch_hist(int grid, size_t smem, cudaStream_t st, const f3::Geo& g, const int64_t* idx,
                  int64_t L, int NT, const int64_t* off, int64_t B, const double* w, int pooling,
-                 F3Bufs& f, int32_t* lk_bag, float* alpha, ttgpu_table* t) {
+                 F3Bufs& f, int32_t* lk_bag, float* alpha, float* out, ttgpu_table* t) {
   f3_launch(t->pdl, f3::f3_hist<float, LPT>, dim3(grid), dim3(512), smem, st, 
       g, idx, L, NT, off, B, w, pooling, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
       f.d2.as<uint16_t>(), lk_bag, alpha, f.hist1.as<uint32_t>(), f.hist2.as<uint32_t>(),
       f.tot.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, t->d_bad(), t->d_struct(),
-      f.solo.as<int32_t>());
+      f.solo.as<int32_t>(), out, static_cast<int>(t->dp.N), f.bag_cnt.as<int>());
+}
+
+// Cooperative launch of the one-kernel sort (gsort.cuh): all CTAs co-resident.
+void launch_gsort(const ttgpu_table* t, int G, size_t smem, const f3::GsortArgs& a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(f3::kGsThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = t->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort, a));
 }
 
 template <class K>
@@ -80,6 +96,8 @@ int grid_occ(K kern, int threads, size_t smem, int num_sms, int cap) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   return std::max(1, std::min(cap, num_sms * std::max(occ, 1)));
 }
+
+constexpr int kChunk = 64;  // lookups per chunk of the chunked path (fastc.cuh)
 
 template <class D>
 struct F3Runner {
@@ -90,11 +108,29 @@ struct F3Runner {
     f3::Geo& g = f.geo;
     g = make_geo(t);
     const int Kmax = std::max(g.m1, g.m2);
+    // one-kernel sort when the batch fits one co-resident grid (gsort.cuh)
+    const size_t gs_smem = f3::gsort_smem_bytes(g.m1, g.m2);
+    int GS = 0, PW = 0;
+    if (t->grid_sort && g.m1 + g.m2 <= 4 * f3::kGsThreads && gs_smem <= 160 * 1024) {
+      set_smem(f3::f3_gsort, gs_smem);
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort, f3::kGsThreads, gs_smem));
+      const int64_t cap = std::min<int64_t>(32 * f3::kGsMaxGridChunks,
+                                            static_cast<int64_t>(t->num_sms) * std::max(occ, 0));
+      const int64_t per = 16 * 32;  // lookups per CTA round
+      const int64_t rounds = (L + cap * per - 1) / std::max<int64_t>(1, cap * per);
+      if (cap > 0 && rounds <= f3::kGsMaxRounds) {
+        PW = static_cast<int>(32 * std::max<int64_t>(1, rounds));
+        GS = static_cast<int>((L + 16 * PW - 1) / (16 * PW));
+      }
+    }
     const int lpt = f3_lpt(L, Kmax);
     if (lpt == 0) fail(TTGPU_ERR_RUNTIME, "batch too large for the fast path histogram");
     const int TL = 512 * lpt;
     const int NT = static_cast<int>((L + TL - 1) / TL);
-    f.max_tiles1 = static_cast<int>((L + D::TT - 1) / D::TT) + g.m1;
+    f.chunked = t->chunked;
+    const int TT1 = f.chunked ? kChunk : D::TT;  // i1-bucket tile (chunk) length
+    f.max_tiles1 = static_cast<int>((L + TT1 - 1) / TT1) + g.m1;
     f.max_tiles2 = static_cast<int>((L + D::TT2 - 1) / D::TT2) + g.m2;
     f.d0.ensure(2 * L);
     f.d1.ensure(2 * L);
@@ -122,44 +158,95 @@ struct F3Runner {
     f.slotpos.ensure(2 * L);
     f.tile_i0.ensure(2 * L);
     f.tile_nslots.ensure(4 * f.max_tiles1);
+    f.bag_cnt.ensure(4 * static_cast<size_t>(B));
     const int gb = std::max(NT, grid_for(B, 512, t->num_sms, 4));
     t->mark("fwd_begin");
-    const size_t hs = 4 * static_cast<size_t>(g.m1 + g.m2);
-    switch (lpt) {
-      case 1: launch_hist<1>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      case 2: launch_hist<2>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      case 4: launch_hist<4>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      case 8: launch_hist<8>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      case 16: launch_hist<16>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
-      default: launch_hist<32>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, t); break;
+    if (GS) {
+      const int K = g.m1 + g.m2;
+      f.gs_hist.ensure(4 * static_cast<size_t>(K) * GS);
+      f.gs_tot.ensure(4 * static_cast<size_t>(K));
+      f3::GsortArgs a{};
+      a.g = g;
+      a.idx = idx;
+      a.L = L;
+      a.off = off;
+      a.B = B;
+      a.w = w;
+      a.mean = pooling;
+      a.PW = PW;
+      a.TT1 = TT1;
+      a.TT2 = D::TT2;
+      a.inv_m12 = 1.0 / static_cast<double>(g.m12);
+      a.inv_m2 = 1.0 / static_cast<double>(g.m2);
+      a.d2 = f.d2.as<uint16_t>();
+      a.lk_bag = lk_bag;
+      a.alpha = alpha;
+      a.solo = f.solo.as<int32_t>();
+      a.hist = f.gs_hist.as<uint32_t>();
+      a.tot = f.gs_tot.as<uint32_t>();
+      a.perm1 = f.perm1.as<uint32_t>();
+      a.perm2 = f.perm2.as<uint32_t>();
+      a.rec1 = f.rec1.as<uint4>();
+      a.tiles1 = f.tiles1.as<f3::Tile>();
+      a.tiles2 = f.tiles2.as<f3::Tile>();
+      a.tile_base1 = f.tile_base1.as<int32_t>();
+      a.tile_base2 = f.tile_base2.as<int32_t>();
+      a.group_base1 = f.group_base1.as<int32_t>();
+      a.group_base2 = f.group_base2.as<int32_t>();
+      a.ntiles = f.ntiles.as<int>();
+      a.bad = t->d_bad();
+      a.errs = t->d_struct();
+      a.out = out;
+      a.N = static_cast<int>(t->dp.N);
+      a.bag_cnt = f.bag_cnt.as<int>();
+      launch_gsort(t, GS, gs_smem, a);
+      t->mark("gsort");
+    } else {
+      const size_t hs = 4 * static_cast<size_t>(g.m1 + g.m2);
+      switch (lpt) {
+        case 1: launch_hist<1>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, out, t); break;
+        case 2: launch_hist<2>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, out, t); break;
+        case 4: launch_hist<4>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, out, t); break;
+        case 8: launch_hist<8>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, out, t); break;
+        case 16: launch_hist<16>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, out, t); break;
+        default: launch_hist<32>(gb, hs, st, g, idx, L, NT, off, B, w, pooling, f, lk_bag, alpha, out, t); break;
+      }
+      t->mark("hist");
+      {
+        f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tot.as<uint32_t>(), f.tile_base1.as<int32_t>(),
+                        f.group_base1.as<int32_t>(), f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
+                        g.m1, TT1};
+        f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, f.tile_base2.as<int32_t>(),
+                        f.group_base2.as<int32_t>(), f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
+                        g.m2, D::TT2};
+        const size_t n = static_cast<size_t>(f3::kScanKeys) * NT;
+        const size_t sm = 4 * (n + n / 32 + 2);
+        set_smem(f3::f3_scan, sm);
+        const int nb1 = (g.m1 + f3::kScanKeys - 1) / f3::kScanKeys;
+        const int nb2 = (g.m2 + f3::kScanKeys - 1) / f3::kScanKeys;
+        f3_launch(t->pdl, f3::f3_scan, dim3(nb1 + nb2), dim3(f3::kScanThreads), sm, st, a1, a2, nb1, NT, L);
+      }
+      t->mark("scan");
+      {
+        const size_t sm = 4 * 8 * static_cast<size_t>(Kmax);
+        set_smem(f3::f3_scatter, sm);
+        f3_launch(t->pdl, f3::f3_scatter, dim3(NT), dim3(256), sm, st, g, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
+                                            f.d2.as<uint16_t>(), L, TL, NT, f.hist1.as<uint32_t>(),
+                                            f.hist2.as<uint32_t>(), f.perm1.as<uint32_t>(),
+                                            f.perm2.as<uint32_t>(), f.tot.as<uint32_t>(),
+                                            f.solo.as<int32_t>(), f.rec1.as<uint4>(), lk_bag, alpha);
+      }
+      t->mark("scatter");
     }
-    t->mark("hist");
-    {
-      f3::ScanArgs a1{f.hist1.as<uint32_t>(), f.tot.as<uint32_t>(), f.tile_base1.as<int32_t>(),
-                      f.group_base1.as<int32_t>(), f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
-                      g.m1, D::TT};
-      f3::ScanArgs a2{f.hist2.as<uint32_t>(), f.tot.as<uint32_t>() + g.m1, f.tile_base2.as<int32_t>(),
-                      f.group_base2.as<int32_t>(), f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
-                      g.m2, D::TT2};
-      const size_t n = static_cast<size_t>(f3::kScanKeys) * NT;
-      const size_t sm = 4 * (n + n / 32 + 2);
-      set_smem(f3::f3_scan, sm);
-      const int nb1 = (g.m1 + f3::kScanKeys - 1) / f3::kScanKeys;
-      const int nb2 = (g.m2 + f3::kScanKeys - 1) / f3::kScanKeys;
-      f3_launch(t->pdl, f3::f3_scan, dim3(nb1 + nb2), dim3(f3::kScanThreads), sm, st, a1, a2, nb1, NT, L);
-    }
-    t->mark("scan");
-    {
-      const size_t sm = 4 * 8 * static_cast<size_t>(Kmax);
-      set_smem(f3::f3_scatter, sm);
-      f3_launch(t->pdl, f3::f3_scatter, dim3(NT), dim3(256), sm, st, g, f.d0.as<uint16_t>(), f.d1.as<uint16_t>(),
-                                          f.d2.as<uint16_t>(), L, TL, NT, f.hist1.as<uint32_t>(),
-                                          f.hist2.as<uint32_t>(), f.perm1.as<uint32_t>(),
-                                          f.perm2.as<uint32_t>(), f.tot.as<uint32_t>(),
-                                          f.solo.as<int32_t>(), f.rec1.as<uint4>());
-    }
-    t->mark("scatter");
-    {
+    if (f.chunked) {
+      const size_t sm = f3::FcFwdSmem<D, kChunk>::bytes(g.m0);
+      auto kern = exact ? f3::f3c_fwd<D, true, kChunk> : f3::f3c_fwd<D, false, kChunk>;
+      set_smem(kern, sm);
+      f3_launch(t->pdl, kern, dim3(f.max_tiles1), dim3(f3::kFcThreads), sm, st, g, t->cores.as<float>(),
+                f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out, f.Hbuf.as<float>(),
+                f.y.as<float>(), f.hloc.as<uint32_t>(), f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
+                f.tile_nslots.as<int>(), off, L, pooling, f.bag_cnt.as<int>());
+    } else {
       const size_t sm = f3::FwdSmem<D>::bytes(g.m0);
       auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
       set_smem(kern, sm);
@@ -168,15 +255,9 @@ struct F3Runner {
                                            f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out,
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
-                                           f.tile_nslots.as<int>());
+                                           f.tile_nslots.as<int>(), off, L, pooling, f.bag_cnt.as<int>());
     }
     t->mark("f3_fwd");
-    {
-      auto kern = exact ? f3::f3_pool<D::N, true> : f3::f3_pool<D::N, false>;
-      f3_launch(t->pdl, kern, dim3(grid_for(B * (D::N / 4), 256, t->num_sms, 8)), dim3(256), 0, st, 
-          off, B, L, w, pooling, f.y.as<float>(), out);
-    }
-    t->mark("pool");
     CK(cudaGetLastError());
   }
 
@@ -184,10 +265,17 @@ struct F3Runner {
                        const int32_t* lk_bag, const float* alpha, int64_t L) {
     cudaStream_t st = t->stream;
     const f3::Geo& g = f.geo;
-    const size_t sm1 = f3::Bwd1Smem<D>::bytes();
+    const size_t sm1 = f.chunked ? f3::FcBwdSmem<D, kChunk>::bytes() : f3::Bwd1Smem<D>::bytes();
     auto k1 = f3::f3_bwd1<D>;
-    set_smem(k1, sm1);
-    const int grid1 = grid_occ(k1, f3::kThreads, sm1, t->num_sms, f.max_tiles1);
+    auto kc = f3::f3c_bwd<D, kChunk>;
+    int grid1;
+    if (f.chunked) {
+      set_smem(kc, sm1);
+      grid1 = grid_occ(kc, f3::kFcThreads, sm1, t->num_sms, f.max_tiles1);
+    } else {
+      set_smem(k1, sm1);
+      grid1 = grid_occ(k1, f3::kThreads, sm1, t->num_sms, f.max_tiles1);
+    }
     const int grid2 = grid_occ(f3::f3_bwd2<D>, 128, 0, t->num_sms, f.max_tiles2);
     f.part1.ensure(4 * static_cast<size_t>(f.max_tiles1) * f3::G1Blk<D>::KG * D::S1);
     f.has1.ensure(4 * static_cast<size_t>(f.max_tiles1));
@@ -197,6 +285,13 @@ struct F3Runner {
     f.d0mask.ensure(static_cast<size_t>(grid1) * g.m0);
     f.Sbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
     t->mark("bwd_begin");
+    if (f.chunked) {
+      f3_launch(t->pdl, kc, dim3(grid1), dim3(f3::kFcThreads), sm1, st, g, t->cores.as<float>(),
+                f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.rec1.as<uint4>(), f.slotpos.as<uint16_t>(),
+                f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(), grad, f.part1.as<float>(),
+                f.has1.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>());
+      t->mark("f3c_bwd");
+    } else {
     f3_launch(t->pdl, f3::f3_srows<D>, dim3((f.max_tiles1 * 32 + 255) / 256), dim3(256), 0, st, 
         t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.max_tiles1,
         f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
@@ -208,6 +303,7 @@ struct F3Runner {
                                          f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
                                          f.d0mask.as<unsigned char>());
     t->mark("f3_bwd1");
+    }
     f3_launch(t->pdl, f3::f3_bwd2<D>, dim3(grid2), dim3(128), 0, st, g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
                                           f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag,
                                           alpha, grad, f.Hbuf.as<float>(), f.part2.as<float>(),

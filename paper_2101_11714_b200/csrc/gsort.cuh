@@ -1,0 +1,405 @@
+// One-kernel two-key stable counting sort for the 3-core fast path (replaces
+// f3_hist + f3_scan + f3_scatter when the batch fits one co-resident grid).
+//
+// A cooperative grid of G <= #SMs CTAs x 512 threads; CTA c owns the lookups
+// [c*16*PW, (c+1)*16*PW), warp w of it a run of PW consecutive lookups walked
+// 32 at a time, so (CTA, warp, round, lane) is lookup order.  Phases:
+//   A  decode + range check (d2 digits), per-warp key counts (match_any
+//      leaders, warp-private smem counters); the CTA's count of every key
+//      into hist[k][c] (key-major); bags: offsets checks, lookup->bag, alpha,
+//      solo flags, pooling counters zeroed, empty bags' rows zeroed
+//   -- grid barrier --
+//   B1 one warp per key (keys spread over the grid): exclusive scan of the
+//      key's G CTA counts in place, key total into tot[k]
+//   -- grid barrier --
+//   B2 every CTA scans the K key totals (lookups, tiles, combine groups) into
+//      the bucket / tile / group bases (CTA 0 publishes them, every CTA
+//      writes its share of the tile lists) and adds its own CTA prefix
+//   C  stable scatter of both keys from the per-warp starts, plus the sorted
+//      (lookup, i0 | i2 << 16, bag | solo, alpha) records of key 1 (make_rec)
+// Keys and digits stay in registers between A and C; no memsets, so the
+// kernel replays from a CUDA graph.  Outputs are
+// exactly those of f3_hist + f3_scan + f3_scatter, so the kernels after the
+// sort are unchanged.  Reference semantics: decompose_row
+// (embedding_ops.hpp:98-108), offsets checks (index_batch.hpp:33-55),
+// backward alpha (embedding_ops.hpp:283-296).
+#pragma once
+
+#include <cooperative_groups.h>
+
+namespace ttgpu {
+namespace f3 {
+
+constexpr int kGsThreads = 512;
+constexpr int kGsWarps = kGsThreads / 32;
+constexpr int kGsMaxRounds = 8;  // lookups per thread (PW <= 256)
+constexpr int kGsMaxGridChunks = 5;  // G <= 160 CTAs
+
+struct GsortArgs {
+  Geo g;
+  const int64_t* idx;
+  int64_t L;
+  const int64_t* off;
+  int64_t B;
+  const double* w;
+  int mean;
+  int PW;  // lookups per warp, multiple of 32, <= 32 * kGsMaxRounds
+  int TT1, TT2;
+  double inv_m12, inv_m2;  // 1 / m12, 1 / m2 (decode by multiply + correction)
+  uint16_t* d2;
+  int32_t* lk_bag;
+  float* alpha;
+  int32_t* solo;
+  uint32_t* hist;  // [K][G] CTA counts -> exclusive CTA prefixes
+  uint32_t* tot;   // [K] key totals
+  uint32_t* perm1;
+  uint32_t* perm2;
+  uint4* rec1;
+  Tile* tiles1;
+  Tile* tiles2;
+  int32_t *tile_base1, *tile_base2, *group_base1, *group_base2;
+  int* ntiles;
+  unsigned long long* bad;
+  int* errs;
+  float* out;    // pooled rows: empty bags are written here (zeros)
+  int N;         // embedding dim
+  int* bag_cnt;  // [B] pooling counters (pool_if_last), zeroed here
+};
+
+// dynamic shared memory: wc[16][K] | ctot[K] | base[K] | gb1 tb1 [K1+1] | gb2 tb2 [K2+1]
+__host__ __device__ constexpr size_t gsort_smem_bytes(int K1, int K2) {
+  return 4 * (static_cast<size_t>(kGsWarps + 2) * (K1 + K2) + 2 * (K1 + 1) + 2 * (K2 + 1));
+}
+
+// largest i in [0, n) with a[i] <= x (a ascending, a[0] <= x)
+__device__ __forceinline__ int upper_slot(const uint32_t* a, int n, uint32_t x) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// q = x / d, r = x % d for x, d < 2^32 (inv = 1.0 / d): the double product is
+// within one of the quotient; one correction step makes it exact.
+__device__ __forceinline__ uint32_t div_fix(uint32_t x, uint32_t d, double inv, uint32_t& r) {
+  uint32_t q = static_cast<uint32_t>(static_cast<double>(x) * inv);
+  int64_t rr = static_cast<int64_t>(x) - static_cast<int64_t>(q) * d;
+  if (rr < 0) {
+    --q;
+    rr += d;
+  } else if (rr >= d) {
+    ++q;
+    rr -= d;
+  }
+  r = static_cast<uint32_t>(rr);
+  return q;
+}
+
+__global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
+  namespace cg = cooperative_groups;
+  const int c = blockIdx.x, G = gridDim.x;
+  const int K1 = a.g.m1, K2 = a.g.m2, K = K1 + K2;
+  extern __shared__ __align__(16) uint32_t gs_sm[];
+  uint32_t* wc = gs_sm;                  // [16][K] per-warp counts -> per-warp starts
+  uint32_t* ctot = wc + kGsWarps * K;    // [K] this CTA's count per key
+  uint32_t* base = ctot + K;             // [K] this CTA's absolute start per key
+  uint32_t* gb1 = base + K;              // [K1+1] bucket starts, key 1
+  uint32_t* tb1 = gb1 + K1 + 1;          // [K1+1] tile starts, key 1
+  uint32_t* gb2 = tb1 + K1 + 1;          // [K2+1]
+  uint32_t* tb2 = gb2 + K2 + 1;          // [K2+1]
+  __shared__ uint32_t wsum[32][3];
+  __shared__ uint32_t k1tot[3];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int R = a.PW >> 5;
+  const int64_t wbase = (static_cast<int64_t>(c) * kGsWarps + wid) * a.PW;
+
+  // ---- phase A: keys (loads of 4 rounds in flight), counts, bags
+  // this thread's first bag's offsets: in flight during the key phase
+  const int64_t b_first = static_cast<int64_t>(c) * kGsThreads + tid;
+  int64_t s_first = 0, e_first = 0;
+  if (b_first < a.B) {
+    s_first = a.off[b_first];
+    e_first = a.off[b_first + 1];
+  }
+  for (int i = tid; i < kGsWarps * K; i += kGsThreads) wc[i] = 0u;
+  // per round: k1 = i1 (0xffffffff: no lookup), d02 = i0 | i2 << 16
+  uint32_t k1[kGsMaxRounds], d02[kGsMaxRounds];
+  uint32_t* mywc = wc + wid * K;
+#pragma unroll
+  for (int q0 = 0; q0 < kGsMaxRounds; q0 += 4) {
+    int64_t rows[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t l = wbase + (q0 + u) * 32 + lane;
+      rows[u] = (q0 + u < R && l < a.L) ? a.idx[l] : 0;
+    }
+    if (q0 == 0) __syncthreads();  // counters zeroed
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u;
+      k1[q] = 0xffffffffu;
+      d02[q] = 0u;
+      if (q < R) {  // warp-uniform
+        const int64_t l = wbase + q * 32 + lane;
+        if (l < a.L) {
+          int64_t row = rows[u];
+          if (row < 0 || row >= a.g.num_rows) {
+            atomicMin(a.bad, static_cast<unsigned long long>(l));
+            row = 0;
+          }
+          uint32_t rem, i2;
+          const uint32_t i0 = div_fix(static_cast<uint32_t>(row), a.g.m12, a.inv_m12, rem);
+          const uint32_t i1 = div_fix(rem, static_cast<uint32_t>(a.g.m2), a.inv_m2, i2);
+          a.d2[l] = static_cast<uint16_t>(i2);
+          k1[q] = i1;
+          d02[q] = i0 | (i2 << 16);
+        }
+        const uint32_t x2 = k1[q] != 0xffffffffu ? d02[q] >> 16 : 0xffffffffu;
+        unsigned p = __match_any_sync(0xffffffffu, k1[q]);
+        if (k1[q] != 0xffffffffu && lane == __ffs(p) - 1) mywc[k1[q]] += __popc(p);
+        p = __match_any_sync(0xffffffffu, x2);
+        if (x2 != 0xffffffffu && lane == __ffs(p) - 1) mywc[K1 + x2] += __popc(p);
+        __syncwarp();
+      }
+    }
+  }
+  // bags (grid-stride over the whole grid)
+  for (int64_t b = b_first; b < a.B; b += static_cast<int64_t>(G) * kGsThreads) {
+    const int64_t s = b == b_first ? s_first : a.off[b], e = b == b_first ? e_first : a.off[b + 1];
+    if (b == 0 && s != 0) atomicOr(a.errs, 1);
+    if (e < s) atomicOr(a.errs, 2);
+    if (b == a.B - 1 && e != a.L) atomicOr(a.errs, 4);
+    const int64_t lo = s < 0 ? 0 : s, hi = e > a.L ? a.L : e;
+    a.bag_cnt[b] = 0;
+    if (e == s)  // an empty bag pools to zeros (no lookup will)
+      for (int c = 0; c < a.N; c += 4)
+        reinterpret_cast<float4*>(a.out + b * a.N + c)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e - s == 1 && hi - lo == 1) {  // the common single-lookup bag
+      a.lk_bag[lo] = static_cast<int32_t>(b);
+      a.solo[lo] = static_cast<int32_t>(b);
+      a.alpha[lo] = a.w ? static_cast<float>(a.w[lo]) : 1.f;
+      continue;
+    }
+    const double sz = static_cast<double>(e - s);
+    for (int64_t l = lo; l < hi; ++l) {
+      a.lk_bag[l] = static_cast<int32_t>(b);
+      a.solo[l] = -1;
+      double al = a.w ? a.w[l] : 1.0;
+      if (a.mean) al /= sz;
+      a.alpha[l] = static_cast<float>(al);
+    }
+  }
+  __syncthreads();
+  // per-warp exclusive starts within the CTA; CTA counts out
+  for (int k = tid; k < K; k += kGsThreads) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kGsWarps; ++w) {
+      const uint32_t v = wc[w * K + k];
+      wc[w * K + k] = run;
+      run += v;
+    }
+    ctot[k] = run;
+    a.hist[static_cast<int64_t>(k) * G + c] = run;
+  }
+  cg::grid_group grid = cg::this_grid();
+  grid.sync();
+
+  // ---- phase B1: per key, exclusive scan over the CTAs (warp per key)
+  for (int k = c * kGsWarps + wid; k < K; k += G * kGsWarps) {
+    uint32_t* row = a.hist + static_cast<int64_t>(k) * G;
+    uint32_t v[kGsMaxGridChunks];  // all loads first: one round trip
+#pragma unroll
+    for (int j = 0; j < kGsMaxGridChunks; ++j) v[j] = j * 32 + lane < G ? __ldcg(row + j * 32 + lane) : 0u;
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < kGsMaxGridChunks; ++j) {
+      uint32_t x = v[j];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (j * 32 + lane < G) row[j * 32 + lane] = run + x - v[j];
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) a.tot[k] = run;
+  }
+  grid.sync();
+
+  // ---- phase B2: bases from the totals plus this CTA's prefix.  Block scan
+  // of (lookups, tiles, groups) over [key 1 | key 2], IPT consecutive keys
+  // per thread.
+  const int IPT = (K + kGsThreads - 1) / kGsThreads;
+  const int k_lo = min(K, tid * IPT), k_hi = min(K, k_lo + IPT);
+  uint32_t t0 = 0, t1 = 0, t2 = 0;
+  for (int k = k_lo; k < k_hi; ++k) {
+    const uint32_t T = __ldcg(a.tot + k);
+    const uint32_t TT = k >= K1 ? a.TT2 : a.TT1;
+    const uint32_t tk = (T + TT - 1) / TT;
+    t0 += T;
+    t1 += tk;
+    t2 += n_groups(tk);
+    // the key total, until the scan is done; this CTA's prefix (B1) in flight
+    base[k] = T;
+  }
+  uint32_t pre[4];  // IPT <= 4 (K <= 2048)
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    pre[j] = k_lo + j < k_hi && ctot[k_lo + j] ? __ldcg(a.hist + static_cast<int64_t>(k_lo + j) * G + c) : 0u;
+  uint32_t s0 = t0, s1 = t1, s2 = t2;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y0 = __shfl_up_sync(0xffffffffu, s0, o);
+    const uint32_t y1 = __shfl_up_sync(0xffffffffu, s1, o);
+    const uint32_t y2 = __shfl_up_sync(0xffffffffu, s2, o);
+    if (lane >= o) {
+      s0 += y0;
+      s1 += y1;
+      s2 += y2;
+    }
+  }
+  if (lane == 31) {
+    wsum[wid][0] = s0;
+    wsum[wid][1] = s1;
+    wsum[wid][2] = s2;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t v[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v[j] = lane < kGsWarps ? wsum[lane][j] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v[j], o);
+        if (lane >= o) v[j] += y;
+      }
+    }
+    __syncwarp();
+    if (lane < kGsWarps)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) wsum[lane][j] = v[j];
+  }
+  __syncthreads();
+  // exclusive running values at this thread's first key
+  uint32_t e0 = s0 - t0, e1 = s1 - t1, e2 = s2 - t2;
+  if (wid > 0) {
+    e0 += wsum[wid - 1][0];
+    e1 += wsum[wid - 1][1];
+    e2 += wsum[wid - 1][2];
+  }
+  // key-2 entries restart at zero: key 1's totals are the running values at
+  // k = K1, found by the thread whose key range holds K1 (K2 >= 1)
+  if (k_lo <= K1 && K1 < k_hi) {
+    uint32_t r0 = e0, r1 = e1, r2 = e2;
+    for (int k = k_lo; k < K1; ++k) {
+      const uint32_t T = base[k];
+      const uint32_t tk = (T + a.TT1 - 1) / a.TT1;
+      r0 += T;
+      r1 += tk;
+      r2 += n_groups(tk);
+    }
+    k1tot[0] = r0;
+    k1tot[1] = r1;
+    k1tot[2] = r2;
+  }
+  __syncthreads();
+  for (int k = k_lo; k < k_hi; ++k) {
+    const bool second = k >= K1;
+    const uint32_t T = base[k];
+    const uint32_t TT = second ? a.TT2 : a.TT1;
+    const uint32_t tk = (T + TT - 1) / TT;
+    const uint32_t b0 = second ? e0 - k1tot[0] : e0;
+    const uint32_t b1 = second ? e1 - k1tot[1] : e1;
+    const uint32_t b2 = second ? e2 - k1tot[2] : e2;
+    if (!second) {
+      gb1[k] = b0;
+      tb1[k] = b1;
+    } else {
+      gb2[k - K1] = b0;
+      tb2[k - K1] = b1;
+    }
+    if (c == 0) {
+      (second ? a.tile_base2 : a.tile_base1)[second ? k - K1 : k] = static_cast<int32_t>(b1);
+      (second ? a.group_base2 : a.group_base1)[second ? k - K1 : k] = static_cast<int32_t>(b2);
+    }
+    base[k] = b0 + pre[k - k_lo];  // this CTA's start of the key
+    e0 += T;
+    e1 += tk;
+    e2 += n_groups(tk);
+    if (k == K1 - 1) {
+      gb1[K1] = e0;
+      tb1[K1] = e1;
+      if (c == 0) {
+        a.tile_base1[K1] = static_cast<int32_t>(e1);
+        a.group_base1[K1] = static_cast<int32_t>(e2);
+        a.ntiles[0] = static_cast<int>(e1);
+      }
+    }
+    if (k == K - 1) {
+      gb2[K2] = e0 - k1tot[0];
+      tb2[K2] = e1 - k1tot[1];
+      if (c == 0) {
+        a.tile_base2[K2] = static_cast<int32_t>(e1 - k1tot[1]);
+        a.group_base2[K2] = static_cast<int32_t>(e2 - k1tot[2]);
+        a.ntiles[1] = static_cast<int>(e1 - k1tot[1]);
+      }
+    }
+  }
+  __syncthreads();
+  // tile lists, split over the grid; the key of a tile by binary search
+  {
+    const uint32_t nt1 = tb1[K1], nt2 = tb2[K2];
+    for (uint32_t t = static_cast<uint32_t>(c) * kGsThreads + tid; t < nt1 + nt2;
+         t += static_cast<uint32_t>(G) * kGsThreads) {
+      const bool s = t >= nt1;
+      const uint32_t tt = s ? t - nt1 : t;
+      const uint32_t* tb = s ? tb2 : tb1;
+      const uint32_t* gb = s ? gb2 : gb1;
+      const int kk = upper_slot(tb, s ? K2 : K1, tt);
+      const uint32_t TTk = s ? a.TT2 : a.TT1;
+      Tile tl;
+      tl.key = kk;
+      tl.start = static_cast<int>(gb[kk] + (tt - tb[kk]) * TTk);
+      tl.end = static_cast<int>(min(gb[kk + 1], gb[kk] + (tt - tb[kk] + 1) * TTk));
+      tl.pad = 0;
+      (s ? a.tiles2 : a.tiles1)[tt] = tl;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase C: stable scatter of both keys
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int q = 0; q < kGsMaxRounds; ++q) {
+    if (q < R) {
+      const int64_t l = wbase + q * 32 + lane;
+      const uint32_t x = k1[q];
+      unsigned p = __match_any_sync(0xffffffffu, x);
+      if (x != 0xffffffffu) {
+        const uint32_t pos = base[x] + mywc[x] + __popc(p & lt);
+        a.perm1[pos] = static_cast<uint32_t>(l);
+        a.rec1[pos] = make_rec(static_cast<uint32_t>(l), d02[q], __ldcg(a.solo + l), __ldcg(a.lk_bag + l),
+                               __ldcg(a.alpha + l));
+      }
+      __syncwarp();
+      if (x != 0xffffffffu && lane == __ffs(p) - 1) mywc[x] += __popc(p);
+      const uint32_t y = x != 0xffffffffu ? d02[q] >> 16 : 0xffffffffu;
+      p = __match_any_sync(0xffffffffu, y);
+      if (y != 0xffffffffu) {
+        const uint32_t pos = base[K1 + y] + mywc[K1 + y] + __popc(p & lt);
+        a.perm2[pos] = static_cast<uint32_t>(l);
+      }
+      __syncwarp();
+      if (y != 0xffffffffu && lane == __ffs(p) - 1) mywc[K1 + y] += __popc(p);
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace f3
+}  // namespace ttgpu

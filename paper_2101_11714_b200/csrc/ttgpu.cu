@@ -195,6 +195,8 @@ struct ttgpu_table {
   bool force_generic = false;  // route 3-core tables through the generic pipeline (testing)
   bool tensor_head = true;     // head backward on tcgen05 (3xTF32) where the shape allows it
   int pdl = 0;                 // fast-path launches: 0 plain, 1 programmatic dependent launch
+  bool grid_sort = true;       // fast path: one-kernel cooperative sort (gsort.cuh) where the batch fits
+  bool chunked = false;        // fast path: chunked forward / S+dG1+D0 backward (fastc.cuh; slower, off)
   // optional phase timing (CUDA events between pipeline phases)
   // Marks recorded while the stream is being captured become event-record nodes of
   // the graph (cudaEventRecordExternal) and stay owned by it: every graph launch
@@ -337,7 +339,8 @@ int grid_for(int64_t work, int per_block, int num_sms, int waves = 8) {
 
 template <class K>
 void set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024)
+  // dynamic + static shared memory above 48 KB needs the opt-in (static is <= 8 KB here)
+  if (bytes > 40 * 1024)
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(bytes)));
 }
@@ -930,6 +933,10 @@ int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* r
       t->pdl = e ? std::atoi(e) : 0;
       const int early = t->pdl >= 2 ? 1 : 0;
       CK(cudaMemcpyToSymbol(f3::g_pdl_early, &early, sizeof(int)));
+      const char* cs = std::getenv("TTGPU_GRID_SORT");
+      t->grid_sort = !(cs && std::atoi(cs) == 0);
+      const char* ch = std::getenv("TTGPU_CHUNKED");
+      t->chunked = ch && std::atoi(ch) != 0;
     }
     std::vector<int64_t> coff;
     t->dp = make_devplan(t->plan, coff, t->total);
@@ -1009,6 +1016,14 @@ int ttgpu_set_generic_path(ttgpu_table* t, int on) {
 
 int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind) {
   return guarded([&] { *kind = t->force_generic ? -1 : f3_kind(t); });
+}
+
+int ttgpu_set_chunked(ttgpu_table* t, int on) {
+  return guarded([&] { t->chunked = on != 0; });
+}
+
+int ttgpu_set_grid_sort(ttgpu_table* t, int on) {
+  return guarded([&] { t->grid_sort = on != 0; });
 }
 
 int ttgpu_set_tensor_path(ttgpu_table* t, int on) {
@@ -1091,7 +1106,9 @@ int ttgpu_forward(ttgpu_table* t, const int64_t* idx, int64_t L, const int64_t* 
     const uint64_t key = mix_key({static_cast<uint64_t>(L), static_cast<uint64_t>(B),
                                   static_cast<uint64_t>(pooling), dw != nullptr ? 1u : 0u,
                                   save != 0 ? 1u : 0u, t->exact ? 1u : 0u,
-                                  t->force_generic ? 1u : 0u, static_cast<uint64_t>(t->dtype)});
+                                  (t->force_generic ? 1u : 0u) | (t->grid_sort ? 2u : 0u) |
+                                      (t->chunked ? 4u : 0u),
+                                  static_cast<uint64_t>(t->dtype)});
     const bool replay = c->gfwd.exec && c->gfwd.key == key && c->gfwd.epoch == g_alloc_epoch.load();
     run_cached(t, c->gfwd, key, [&] {
       if (t->dtype == TTGPU_F64)

@@ -284,6 +284,14 @@ class TtTable:
         """Backward head contraction on tcgen05 (3xTF32) where eligible (default on)."""
         _raise(lib().ttgpu_set_tensor_path(self.handle, int(bool(on))))
 
+    def set_grid_sort(self, on: bool):
+        """Fast path: one-kernel cooperative sort (gsort.cuh) (default on) or the three-kernel sort."""
+        _raise(lib().ttgpu_set_grid_sort(self.handle, int(bool(on))))
+
+    def set_chunked(self, on: bool):
+        """Fast path: chunked kernels (fastc.cuh) or the 32-lookup tile kernels (default)."""
+        _raise(lib().ttgpu_set_chunked(self.handle, int(bool(on))))
+
     def fast_path_kind(self) -> int:
         k = C.c_int()
         _raise(lib().ttgpu_fast_path_kind(self.handle, C.byref(k)))

@@ -645,3 +645,74 @@ def test_tensor_head_ragged_runs(orc, nbags):
     for k in range(3):
         assert scaled_max_err(got[True].cores[k], want[k]) <= GRAD_TOL
         assert scaled_max_err(got[True].cores[k], got[False].cores[k]) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("nlook", [1, 45, 4096, 65536, 131072, 131073])
+def test_grid_sort_equals_three_kernel_sort(orc, nlook):
+    """The one-kernel cooperative sort (gsort.cuh) produces the same permutations, tiles and
+    bag data as f3_hist + f3_scan + f3_scatter, so forward outputs and gradients
+    are BITWISE equal between the two paths (131,073 lookups exceeds one
+    cluster: both runs take the three-kernel sort).  Multi-hot weighted Mean
+    bags with empties; checked against the oracle too."""
+    p = tt.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
+    t, cores = make_table(p, np.float32, 5, "csort", scale=0.3)
+    rng = np.random.default_rng(nlook)
+    base = tt.generate_zipfian_batch(p.num_rows, 1.05, 11, nlook, 1)
+    idx = base.indices.astype(np.int64)
+    nb = max(1, nlook // 3)
+    cuts = np.sort(rng.integers(0, nlook + 1, nb - 1))
+    off = np.concatenate([[0], cuts, [nlook]]).astype(np.int64)
+    w = rng.uniform(-2, 2, nlook)
+    b = tt.IndexBatch(idx, off, w, tt.Pooling.Mean)
+    g = rng.standard_normal((nb, 16)).astype(np.float32)
+    outs, grads = [], []
+    for on in (True, False):
+        t.set_grid_sort(on)
+        res = tt.forward_bags(t, b)
+        outs.append(res.output)
+        grads.append(tt.backward_bags(t, b, res.context, g).cores)
+    assert np.array_equal(outs[0], outs[1])
+    for k in range(3):
+        assert np.array_equal(grads[0][k], grads[1][k])
+    op = as_oplan(p)
+    assert np.array_equal(outs[0], orc.forward(op, cores, idx, off, w, 1))
+    if nlook <= 4096:
+        want = orc.backward(op, cores, idx, off, g, w, 1)
+        for k in range(3):
+            assert scaled_max_err(grads[0][k], want[k]) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("rank", [8, 32, 64])
+@pytest.mark.parametrize("exponent", [0.0, 1.05])
+def test_chunked_vs_tile_kernels(orc, rank, exponent):
+    """The chunked kernels (fastc.cuh: 64-lookup bucket chunks, CTA-wide i0
+    dedup, fused S/dG1/D0 backward) against the 32-lookup tile kernels and the
+    oracle: forward bit-identical, gradients within tolerance, fused SGD
+    deterministic across repeats."""
+    p = tt.plan_shapes(10131227, 16, 3, rank, [200, 220, 250], [2, 2, 4])
+    t, cores = make_table(p, np.float32, rank + 1, "chunk", scale=0.3)
+    rng = np.random.default_rng(rank)
+    nb = 5000
+    base = tt.generate_zipfian_batch(p.num_rows, exponent, 5, nb, 2)
+    sizes = rng.integers(0, 4, nb)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    idx = np.resize(base.indices, int(off[-1])).astype(np.int64)
+    w = rng.uniform(-2, 2, len(idx))
+    b = tt.IndexBatch(idx, off, w, tt.Pooling.Mean)
+    g = rng.standard_normal((nb, 16)).astype(np.float32)
+    op = as_oplan(p)
+    want_out = orc.forward(op, cores, idx, off, w, 1)
+    want = orc.backward(op, cores, idx, off, g, w, 1)
+    got = {}
+    for on in (True, False):
+        t.set_chunked(on)
+        res = tt.forward_bags(t, b)
+        assert np.array_equal(res.output, want_out)
+        got[on] = tt.backward_bags(t, b, res.context, g).cores
+        for k in range(3):
+            assert scaled_max_err(got[on][k], want[k]) <= GRAD_TOL
+    t.set_chunked(True)
+    res = tt.forward_bags(t, b)
+    again = tt.backward_bags(t, b, res.context, g).cores
+    for k in range(3):
+        assert np.array_equal(again[k], got[True][k])

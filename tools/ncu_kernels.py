@@ -10,7 +10,7 @@ import re
 import sys
 
 PHASE = {"f3_hist": "hist", "f3_scan": "scan", "f3_scatter": "scatter", "f3_fwd": "f3_fwd",
-         "f3_pool": "pool", "f3_bwd1": "f3_bwd1", "f3_bwd2": "f3_bwd2", "f3_combine": "f3_combine"}
+         "f3_bwd1": "f3_bwd1", "f3_bwd2": "f3_bwd2", "f3_combine": "f3_combine"}
 SCALE = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3, "ms": 1e3,
          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
