@@ -573,7 +573,7 @@ def main():
         for _ in range(2):
             step()
         table.check()
-    # the cached forward syncs once (chain-part size); NCCL calls stay outside graphs
+    # the cached forward syncs once (chain-part size), so it runs eagerly
     use_graph = cache is None and (world == 1 or reducer is not None)
     kernels_per_step = None
     if use_graph:
@@ -583,6 +583,21 @@ def main():
         run = table.graph_launch
         for _ in range(2):
             run()
+    elif cache is None and world > 1 and backend == "nccl":
+        # NCCL fallback: the whole step, allreduce included, in one torch-managed
+        # CUDA graph on the table's stream (NCCL kernels are capturable)
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step()
+            run = g.replay
+            for _ in range(2):
+                run()
+            use_graph = True
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] NCCL step capture failed ({e}); running eagerly", file=sys.stderr)
+            torch.cuda.synchronize()
+            run = step
     else:
         run = step
     stream.synchronize()

@@ -256,20 +256,22 @@ int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed);
 
 /* ---- fused cross-GPU gradient reduction + SGD over peer memory (§8(e)) ----
  * Replaces allreduce(SUM) of the dense core gradients + sgd_step on every
- * replica (embedding_ops.hpp:355-376) with ONE kernel per rank: it reads
- * every rank's gradient buffer over NVLink (CUDA IPC mappings), sums in rank
- * order (identical bits on every replica) and applies core -= lr * g.
+ * replica (embedding_ops.hpp:355-376) with ONE kernel per rank, a
+ * reduce-scatter + all-gather over NVLink: rank q reduces its 1/W shard of
+ * every rank's gradient buffer in rank order, applies core -= lr * g and
+ * stores the result into every replica's cores (CUDA IPC mappings), so the
+ * replicas stay bitwise equal.
  * Usage: after ttgpu_backward_device on each rank's bag shard,
  * ttgpu_peer_reduce_sgd(t, lr) on every rank (asynchronous, graph-capturable).
  * Handles are cudaIpcMemHandle_t (64 bytes) per rank, exchanged by the caller
  * (e.g. an all_gather over torch.distributed). */
-int ttgpu_peer_export(ttgpu_table* t, void* grad_handle, void* flags_handle);
+int ttgpu_peer_export(ttgpu_table* t, void* grad_handle, void* core_handle, void* flags_handle);
 int ttgpu_peer_attach(ttgpu_table* t, int world, int rank, const void* grad_handles,
-                      const void* flags_handles);
+                      const void* core_handles, const void* flags_handles);
 /* peers addressable from this process (one process driving several GPUs with
  * P2P enabled, or several ranks' tables on one GPU in tests) */
 int ttgpu_peer_attach_ptrs(ttgpu_table* t, int world, int rank, void* const* grad_ptrs,
-                           void* const* flag_ptrs);
+                           void* const* core_ptrs, void* const* flag_ptrs);
 int ttgpu_peer_flags_ptr(ttgpu_table* t, void** out);
 int ttgpu_peer_reduce_sgd(ttgpu_table* t, double lr);
 /* synchronises; timed_out = 1 if a reduce gave up waiting for a rank */

@@ -109,9 +109,9 @@ _SIGS = {
     "ttgpu_sampler_set_stream": (C.c_int, [vp, vp]),
     "ttgpu_sampler_draw_device": (C.c_int, [vp, C.c_uint64, C.c_uint64, i64, vp]),
     "ttgpu_bag_offsets_device": (C.c_int, [i64, i64, vp, vp]),
-    "ttgpu_peer_export": (C.c_int, [vp, vp, vp]),
-    "ttgpu_peer_attach": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
-    "ttgpu_peer_attach_ptrs": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
+    "ttgpu_peer_export": (C.c_int, [vp, vp, vp, vp]),
+    "ttgpu_peer_attach": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp]),
+    "ttgpu_peer_attach_ptrs": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp]),
     "ttgpu_peer_flags_ptr": (C.c_int, [vp, vpp]),
     "ttgpu_peer_reduce_sgd": (C.c_int, [vp, C.c_double]),
     "ttgpu_peer_status": (C.c_int, [vp, C.POINTER(C.c_int)]),

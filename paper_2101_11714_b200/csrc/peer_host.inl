@@ -3,21 +3,30 @@
 // The multi-GPU step is: per-rank backward_bags on its bag shard (dense core
 // gradient in the table's buffer) -> allreduce(SUM) -> identical sgd_step on
 // every replica (embedding_ops.hpp:355-376).  ttgpu_peer_reduce_sgd does the
-// last two in ONE kernel: each rank reads every rank's gradient buffer
-// directly (NVLink P2P loads through CUDA IPC mappings), sums them in rank
-// order -- the same order on every rank, so the replicas stay bitwise equal
-// -- and applies core -= T(lr) * g in the same pass.  No NCCL launch, no
-// separate SGD kernel, no intermediate reduced buffer.
+// last two in ONE kernel, as a reduce-scatter + all-gather over NVLink:
+//   rank q owns the shard [q*per, (q+1)*per) of the flat core vector; it reads
+//   that shard of every rank's gradient buffer (16-byte P2P loads, all ranks'
+//   loads in flight at once), sums them in rank order, applies
+//   core -= T(lr) * g, and stores the new values into its own cores AND every
+//   peer's cores (P2P stores through the CUDA IPC mappings).
+// Each element is reduced by exactly one rank in a fixed order and the result
+// is copied everywhere, so the replicas stay bitwise equal.  Per rank and call
+// the NVLink traffic is 2 (W-1)/W of the core bytes (about 3.5 MB at W = 8 for
+// the 1.98 MB cfg2 table) instead of (W-1) times them for all-to-all reads.
+// No NCCL launch, no separate SGD kernel, no intermediate reduced buffer.
 //
 // Synchronisation, per call (epoch e = previous + 1, kept on the device so the
 // kernel is CUDA-graph replayable):
 //   start   CTA 0 of rank q writes ready[q] = e into every rank's flag block
 //           (release, system scope); every CTA waits until its own block has
-//           ready[r] >= e for all r (acquire) -- all gradients are final;
-//   body    grid-stride reduce-in-rank-order + SGD;
-//   finish  the last CTA to finish writes done[q] = e everywhere, then waits
-//           for done[r] >= e from all ranks, so no rank's next backward can
-//           overwrite a gradient buffer a peer is still reading; it commits e.
+//           ready[r] >= e for all r (acquire) -- all gradients are final and
+//           no rank still reads its cores for this step's backward;
+//   body    the shard: reduce in rank order + SGD + push to every replica;
+//   finish  every CTA fences its P2P stores (system scope); the last CTA to
+//           finish writes done[q] = e everywhere, then waits for done[r] >= e
+//           from all ranks -- every replica's cores are complete and no
+//           rank's next backward can overwrite a gradient a peer still reads;
+//           it commits e.
 // Spins are bounded (~seconds): a missing peer latches an error that the next
 // ttgpu_check() reports instead of hanging the GPU.
 namespace ttgpu {
@@ -31,8 +40,27 @@ constexpr int kFlagWords = 64;
 template <typename T>
 struct PeerPtrs {
   const T* grads[kMaxPeers];
+  T* cores[kMaxPeers];
   unsigned* flags[kMaxPeers];
 };
+
+template <typename T> struct Vec;
+template <> struct Vec<float> { using V = float4; static constexpr int n = 4; };
+template <> struct Vec<double> { using V = double2; static constexpr int n = 2; };
+
+__device__ __forceinline__ void vadd(float4& a, const float4& b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+__device__ __forceinline__ void vadd(double2& a, const double2& b) {
+  a.x += b.x; a.y += b.y;
+}
+__device__ __forceinline__ float4 vsgd(float4 c, float4 g, float step) {
+  return make_float4(__fadd_rn(c.x, -__fmul_rn(step, g.x)), __fadd_rn(c.y, -__fmul_rn(step, g.y)),
+                     __fadd_rn(c.z, -__fmul_rn(step, g.z)), __fadd_rn(c.w, -__fmul_rn(step, g.w)));
+}
+__device__ __forceinline__ double2 vsgd(double2 c, double2 g, double step) {
+  return make_double2(__dadd_rn(c.x, -__dmul_rn(step, g.x)), __dadd_rn(c.y, -__dmul_rn(step, g.y)));
+}
 
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -54,10 +82,16 @@ __device__ __forceinline__ bool wait_all(const unsigned* own, int slot0, int wor
   return true;
 }
 
+// shard of rank q: [q * per, min(n, (q + 1) * per)), per a multiple of 4 elements
+__host__ __device__ inline int64_t peer_shard(int64_t n, int world) {
+  return ((n + world - 1) / world + 3) / 4 * 4;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_peer_reduce_sgd(PeerPtrs<T> pp, int world, int rank,
-                                                         T* __restrict__ cores, int64_t n, T step,
-                                                         unsigned* own) {
+__global__ void __launch_bounds__(256) k_peer_reduce_sgd(PeerPtrs<T> pp, int world, int rank, int64_t n,
+                                                         T step, unsigned* own) {
+  using V = typename Vec<T>::V;
+  constexpr int NV = Vec<T>::n;
   __shared__ unsigned epoch_s;
   __shared__ int ok_s;
   if (threadIdx.x == 0) {
@@ -74,16 +108,27 @@ __global__ void __launch_bounds__(256) k_peer_reduce_sgd(PeerPtrs<T> pp, int wor
   __syncthreads();
   const unsigned epoch = epoch_s;
   if (ok_s) {
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-      T g = __ldcg(pp.grads[0] + e);
-      for (int r = 1; r < world; ++r) g += __ldcg(pp.grads[r] + e);  // rank order everywhere
-      cores[e] = add_rn<T>(cores[e], -mul_rn<T>(step, g));
+    const int64_t per = peer_shard(n, world);
+    const int64_t lo = rank * per, hi = lo + per < n ? lo + per : n;
+    for (int64_t e = lo + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * NV; e < hi;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x * NV) {
+      V g[kMaxPeers];
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r)  // every rank's load in flight
+        if (r < world) g[r] = __ldcg(reinterpret_cast<const V*>(pp.grads[r] + e));
+      V sum = g[0];
+#pragma unroll
+      for (int r = 1; r < kMaxPeers; ++r)
+        if (r < world) vadd(sum, g[r]);  // rank order everywhere
+      const V c = vsgd(*reinterpret_cast<const V*>(pp.cores[rank] + e), sum, step);
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r)
+        if (r < world) __stcg(reinterpret_cast<V*>(pp.cores[r] + e), c);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    __threadfence_system();  // this CTA's P2P core stores before it counts as done
     const unsigned prev = atomicAdd(own + 17, 1u);
     if (prev == gridDim.x - 1) {  // last CTA of this rank
       own[17] = 0u;
@@ -100,7 +145,7 @@ __global__ void __launch_bounds__(256) k_peer_reduce_sgd(PeerPtrs<T> pp, int wor
 
 struct ttgpu_peers {
   int world = 0, rank = 0;
-  std::vector<void*> grads, flags;  // per rank (own entries are the table's buffers)
+  std::vector<void*> grads, cores, flags;  // per rank (own entries are the table's buffers)
   std::vector<void*> opened;        // IPC mappings to close
   ~ttgpu_peers() {
     for (void* p : opened) cudaIpcCloseMemHandle(p);
@@ -125,10 +170,11 @@ int ttgpu_peer_flags_ptr(ttgpu_table* t, void** out) {
   return guarded([&] { *out = ttgpu::peer_flags(t); });
 }
 
-int ttgpu_peer_export(ttgpu_table* t, void* grad_handle, void* flags_handle) {
+int ttgpu_peer_export(ttgpu_table* t, void* grad_handle, void* core_handle, void* flags_handle) {
   return guarded([&] {
     ttgpu::peer_flags(t);
     CK(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(grad_handle), t->grads.p));
+    CK(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(core_handle), t->cores.p));
     CK(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(flags_handle), t->peer_flag_buf.p));
   });
 }
@@ -143,41 +189,50 @@ static void attach_common(ttgpu_table* t, int world, int rank) {
   t->peers->world = world;
   t->peers->rank = rank;
   t->peers->grads.assign(world, nullptr);
+  t->peers->cores.assign(world, nullptr);
   t->peers->flags.assign(world, nullptr);
 }
 
 int ttgpu_peer_attach(ttgpu_table* t, int world, int rank, const void* grad_handles,
-                      const void* flags_handles) {
+                      const void* core_handles, const void* flags_handles) {
   return guarded([&] {
     attach_common(t, world, rank);
     const auto* gh = static_cast<const cudaIpcMemHandle_t*>(grad_handles);
+    const auto* ch = static_cast<const cudaIpcMemHandle_t*>(core_handles);
     const auto* fh = static_cast<const cudaIpcMemHandle_t*>(flags_handles);
     for (int r = 0; r < world; ++r) {
       if (r == rank) {
         t->peers->grads[r] = t->grads.p;
+        t->peers->cores[r] = t->cores.p;
         t->peers->flags[r] = ttgpu::peer_flags(t);
         continue;
       }
       void* g = nullptr;
+      void* c = nullptr;
       void* f = nullptr;
       CK(cudaIpcOpenMemHandle(&g, gh[r], cudaIpcMemLazyEnablePeerAccess));
       t->peers->opened.push_back(g);
+      CK(cudaIpcOpenMemHandle(&c, ch[r], cudaIpcMemLazyEnablePeerAccess));
+      t->peers->opened.push_back(c);
       CK(cudaIpcOpenMemHandle(&f, fh[r], cudaIpcMemLazyEnablePeerAccess));
       t->peers->opened.push_back(f);
       t->peers->grads[r] = g;
+      t->peers->cores[r] = c;
       t->peers->flags[r] = f;
     }
   });
 }
 
 int ttgpu_peer_attach_ptrs(ttgpu_table* t, int world, int rank, void* const* grad_ptrs,
-                           void* const* flag_ptrs) {
+                           void* const* core_ptrs, void* const* flag_ptrs) {
   return guarded([&] {
     attach_common(t, world, rank);
     for (int r = 0; r < world; ++r) {
       t->peers->grads[r] = r == rank ? t->grads.p : grad_ptrs[r];
+      t->peers->cores[r] = r == rank ? t->cores.p : core_ptrs[r];
       t->peers->flags[r] = r == rank ? static_cast<void*>(ttgpu::peer_flags(t)) : flag_ptrs[r];
-      require_arg(t->peers->grads[r] && t->peers->flags[r], cat("missing buffers of rank ", r));
+      require_arg(t->peers->grads[r] && t->peers->cores[r] && t->peers->flags[r],
+                  cat("missing buffers of rank ", r));
     }
   });
 }
@@ -189,25 +244,25 @@ int ttgpu_peer_reduce_sgd(ttgpu_table* t, double lr) {
     const ttgpu_peers& P = *t->peers;
     // at most half the SMs: two ranks sharing one GPU (tests) must be co-resident
     const int64_t n = t->total;
+    const int64_t shard = peer_shard(n, P.world);
     const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>((n + 1023) / 1024, std::max(1, t->num_sms / 2))));
+        1, std::min<int64_t>((shard + 1023) / 1024, std::max(1, t->num_sms / 2))));
     if (t->dtype == TTGPU_F64) {
       PeerPtrs<double> pp{};
       for (int r = 0; r < P.world; ++r) {
         pp.grads[r] = static_cast<const double*>(P.grads[r]);
+        pp.cores[r] = static_cast<double*>(P.cores[r]);
         pp.flags[r] = static_cast<unsigned*>(P.flags[r]);
       }
-      k_peer_reduce_sgd<double><<<grid, 256, 0, t->stream>>>(pp, P.world, P.rank,
-                                                              t->cores.as<double>(), n, lr,
-                                                              peer_flags(t));
+      k_peer_reduce_sgd<double><<<grid, 256, 0, t->stream>>>(pp, P.world, P.rank, n, lr, peer_flags(t));
     } else {
       PeerPtrs<float> pp{};
       for (int r = 0; r < P.world; ++r) {
         pp.grads[r] = static_cast<const float*>(P.grads[r]);
+        pp.cores[r] = static_cast<float*>(P.cores[r]);
         pp.flags[r] = static_cast<unsigned*>(P.flags[r]);
       }
-      k_peer_reduce_sgd<float><<<grid, 256, 0, t->stream>>>(pp, P.world, P.rank,
-                                                             t->cores.as<float>(), n,
+      k_peer_reduce_sgd<float><<<grid, 256, 0, t->stream>>>(pp, P.world, P.rank, n,
                                                              static_cast<float>(lr), peer_flags(t));
     }
     CK(cudaGetLastError());

@@ -172,10 +172,12 @@ class DataParallelTable:
 
 class PeerReducer:
     """Fused reduce + SGD over peer memory for one replicated table
-    (ttgpu_peer_reduce_sgd): every rank reads all ranks' dense gradient
-    buffers over NVLink, sums them in rank order and applies the SGD in one
-    kernel -- the NCCL allreduce and the separate SGD launch disappear.
-    Handles are exchanged once with an all_gather on `group`."""
+    (ttgpu_peer_reduce_sgd): a reduce-scatter + all-gather over NVLink in
+    one kernel -- each rank sums its 1/W shard of every rank's dense gradient
+    in rank order, applies the SGD and stores the result into every replica's
+    cores.  The NCCL allreduce and the separate SGD launch disappear.
+    Handles (gradients, cores, flags) are exchanged once with an all_gather
+    on `group`."""
 
     def __init__(self, table: TtTable, group=None):
         import ctypes as C
@@ -190,24 +192,27 @@ class PeerReducer:
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         gh = (C.c_char * 64)()
+        ch = (C.c_char * 64)()
         fh = (C.c_char * 64)()
         # a failed export still joins the (collective) exchange, flagged, so no
         # rank is left waiting; every rank then raises together
-        exported = lib().ttgpu_peer_export(table.handle, gh, fh) == 0
-        mine = torch.tensor(list(bytes(gh)) + list(bytes(fh)) + [1 if exported else 0],
-                            dtype=torch.uint8)
+        exported = lib().ttgpu_peer_export(table.handle, gh, ch, fh) == 0
+        mine = torch.tensor(list(bytes(gh)) + list(bytes(ch)) + list(bytes(fh)) +
+                            [1 if exported else 0], dtype=torch.uint8)
         if world > 1:
             bufs = [torch.zeros_like(mine) for _ in range(world)]
             dist.all_gather_object(bufs, mine, group=group)
         else:
             bufs = [mine]
-        if not all(int(b[128]) for b in bufs):
+        if not all(int(b[192]) for b in bufs):
             raise RuntimeError("peer reduce: a rank could not export its buffers")
         allg = b"".join(bytes(b[:64].tolist()) for b in bufs)
-        allf = b"".join(bytes(b[64:128].tolist()) for b in bufs)
+        allc = b"".join(bytes(b[64:128].tolist()) for b in bufs)
+        allf = b"".join(bytes(b[128:192].tolist()) for b in bufs)
         self._g = C.create_string_buffer(allg, len(allg))
+        self._c = C.create_string_buffer(allc, len(allc))
         self._f = C.create_string_buffer(allf, len(allf))
-        _raise(lib().ttgpu_peer_attach(table.handle, world, rank, self._g, self._f))
+        _raise(lib().ttgpu_peer_attach(table.handle, world, rank, self._g, self._c, self._f))
         self.world, self.rank = world, rank
 
     def reduce_sgd(self, lr: float):

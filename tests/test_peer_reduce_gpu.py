@@ -1,11 +1,12 @@
 """Fused cross-GPU reduce + SGD over peer memory (ttgpu_peer_reduce_sgd).
 
-One B200 is available, so ranks share it: (1) two tables in one process whose
-peer pointers are each other's buffers (ttgpu_peer_attach_ptrs), the two
-kernels running concurrently on two streams; (2) two processes exchanging
-CUDA IPC handles (the production path) over a gloo group.  Checks: replicas
-bitwise equal, equal to the oracle's full-batch SGD within 1e-4, and equal to
-NCCL-free host arithmetic (core - lr*(g0+g1)) bit for bit."""
+One B200 is available, so ranks share it: (1) two or three tables in one
+process whose peer pointers are each other's buffers
+(ttgpu_peer_attach_ptrs), the kernels running concurrently on separate
+streams; (2) two processes exchanging CUDA IPC handles (the production path)
+over a gloo group.  Checks: replicas bitwise equal, equal to the oracle's
+full-batch SGD within 1e-4, and equal to NCCL-free host arithmetic
+(core - lr*(g0+g1+...)) bit for bit."""
 import ctypes as C
 import os
 import socket
@@ -35,17 +36,20 @@ def _oplan(p):
     return Plan(p.num_rows, p.emb_dim, p.row_factors, p.col_factors, p.ranks)
 
 
-def test_two_ranks_in_one_process_concurrent_streams():
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_in_one_process_concurrent_streams(world):
+    """W tables on W streams of this GPU act as the ranks: every rank reduces
+    its 1/W shard (W = 3: uneven shards) and pushes it into every replica."""
     import torch
 
     from paper_2101_11714_b200._lib import lib
     from paper_2101_11714_b200.sharding import partition_bags, shard_batch, shard_rows
 
     plan, cores, b, g = _case()
-    bounds = partition_bags(b.offsets, 2)
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-    tabs, ctxs, keep = [], [], []
-    for r in range(2):
+    bounds = partition_bags(b.offsets, world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    tabs = []
+    for r in range(world):
         t = tt.TtTable(plan, f"rank{r}", stream=streams[r].cuda_stream)
         t.set_cores(cores)
         tabs.append(t)
@@ -54,32 +58,32 @@ def test_two_ranks_in_one_process_concurrent_streams():
         p = C.c_void_p()
         assert lib().ttgpu_peer_flags_ptr(t.handle, C.byref(p)) == 0
         flags.append(p.value)
-    grads = [t.grad_buffer()[0] for t in tabs]
-    G = (C.c_void_p * 2)(*grads)
-    F = (C.c_void_p * 2)(*flags)
+    G = (C.c_void_p * world)(*[t.grad_buffer()[0] for t in tabs])
+    Cp = (C.c_void_p * world)(*[t.core_device_ptr(0) for t in tabs])
+    F = (C.c_void_p * world)(*flags)
     for r, t in enumerate(tabs):
-        assert lib().ttgpu_peer_attach_ptrs(t.handle, 2, r, G, F) == 0, lib().ttgpu_last_error()
-    host_g = []
+        assert lib().ttgpu_peer_attach_ptrs(t.handle, world, r, G, Cp, F) == 0, lib().ttgpu_last_error()
     for step in range(2):
+        host_g = []
         for r, t in enumerate(tabs):
             sb = shard_batch(b, bounds, r)
             res = tt.forward_bags(t, sb, save_intermediates=True)
-            gr = tt.backward_bags(t, sb, res.context, shard_rows(g, bounds, r))
-            host_g.append(gr)
-        before = [t.core(k) for k in range(3) for t in tabs[:1]]
+            host_g.append(tt.backward_bags(t, sb, res.context, shard_rows(g, bounds, r)))
+        before = [tabs[0].core(k) for k in range(3)]
         for t in tabs:
             assert lib().ttgpu_peer_reduce_sgd(t.handle, C.c_double(0.01)) == 0
         for t in tabs:
             t.check()
             st = C.c_int()
             assert lib().ttgpu_peer_status(t.handle, C.byref(st)) == 0 and st.value == 0
-        # replicas bitwise equal, and equal to core - lr*(g0 + g1) in rank order
+        # replicas bitwise equal, and equal to core - lr*(g0 + g1 + ...) in rank order
         for k in range(3):
-            a, c = tabs[0].core(k), tabs[1].core(k)
-            assert np.array_equal(a, c)
-            gsum = host_g[-2].cores[k] + host_g[-1].cores[k]
+            gsum = host_g[0].cores[k].copy()
+            for r in range(1, world):
+                gsum = (gsum + host_g[r].cores[k]).astype(np.float32)
             want = (before[k] - np.float32(0.01) * gsum).astype(np.float32)
-            assert np.array_equal(a, want), k
+            for t in tabs:
+                assert np.array_equal(t.core(k), want), k
         if step == 0:
             full = Oracle().backward(_oplan(plan), cores, b.indices, b.offsets, g)
             ref = [c.copy() for c in cores]

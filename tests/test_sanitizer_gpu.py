@@ -53,8 +53,9 @@ for q in ts:
     q.set_cores([np.zeros(p.core_size(k), np.float32) for k in range(3)])
     f = C.c_void_p(); assert lib().ttgpu_peer_flags_ptr(q.handle, C.byref(f)) == 0; flags.append(f.value)
 G = (C.c_void_p * 2)(*[q.grad_buffer()[0] for q in ts]); F = (C.c_void_p * 2)(*flags)
+Cp = (C.c_void_p * 2)(*[q.core_device_ptr(0) for q in ts])
 for r, q in enumerate(ts):
-    assert lib().ttgpu_peer_attach_ptrs(q.handle, 2, r, G, F) == 0
+    assert lib().ttgpu_peer_attach_ptrs(q.handle, 2, r, G, Cp, F) == 0
     b = tt.generate_zipfian_batch(p.num_rows, 1.05, 3 + r, 2048, 1)
     res = tt.forward_bags(q, b, save_intermediates=True)
     tt.backward_bags(q, b, res.context, rng.standard_normal((2048, 16)).astype(np.float32))
