@@ -47,7 +47,12 @@ CONFIGS = {
     "cfg4": dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32, bags=65536,
                  pf=1, zipf=1.2, cache=True,
                  desc="cfg2 shape with the LFU hot-row cache (0.01% = 1,013 rows), Zipf(1.2), "
-                      "fwd+bwd+SGD, cache warmed on the same stream"),
+                      "fwd+bwd+SGD; the cache is warmed on W other Zipf(1.2) batches (not the "
+                      "timed one), then admits the top 1,013 rows"),
+    "cfg2z12": dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32, bags=65536,
+                    pf=1, zipf=1.2,
+                    desc="cfg4 without the cache: cfg2 shape, Zipf(1.2), fwd+bwd+SGD "
+                         "(the like-for-like uncached step beside cfg4)"),
     "cfg3": dict(rows=40000000, emb=64, rf=[200, 200, 1000], cf=[4, 4, 4], rank=64, bags=65536,
                  pf=32, zipf=0.0,
                  desc="40M rows (200x200x1000), dim 64 (4x4x4), R=64, 65,536 bags x 32, uniform"),
@@ -406,6 +411,8 @@ def main():
     ap.add_argument("--nccl", action="store_true",
                     help="N>1: NCCL allreduce + SGD kernel instead of the fused peer reduce+SGD")
     ap.add_argument("--profile", action="store_true", help="print per-phase times")
+    ap.add_argument("--cache-partition", action="store_true",
+                    help="cfg4: the explicit partition path (eager) instead of the cache fast path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -479,6 +486,7 @@ def main():
         cache = tt.LfuCache(tt.lfu_cache.default_capacity(cfg["rows"]), cfg["emb"],
                             refresh_period=1 << 30, key_space=cfg["rows"], device=local,
                             stream=stream.cuda_stream)
+        cache.set_fast(not args.cache_partition)
     gbuf = None
     if world > 1:
         gptr, gn = table.grad_buffer()
@@ -549,9 +557,18 @@ def main():
             else:
                 reducer = None
 
-    # warm-up (allocates every workspace), validation, then graph capture
-    for _ in range(args.warmup):
+    # warm-up (allocates every workspace), validation, then graph capture.  The
+    # cache warms on W different batches of the same stream (seeds 7 + rank +
+    # 101 * (i + 1)); the timed batch is restored afterwards.
+    for i in range(args.warmup):
+        if cache is not None:
+            widx = make_inputs(cfg, 7 + rank + 101 * (i + 1), tt)[0]
+            with torch.cuda.stream(stream):
+                d_idx.copy_(torch.from_numpy(widx))
         step()
+    if cache is not None:
+        with torch.cuda.stream(stream):
+            d_idx.copy_(torch.from_numpy(idx))
     table.check()
     if reducer is not None:
         from paper_2101_11714_b200.sharding import replica_checksum
@@ -573,8 +590,9 @@ def main():
         for _ in range(2):
             step()
         table.check()
-    # the cached forward syncs once (chain-part size), so it runs eagerly
-    use_graph = cache is None and (world == 1 or reducer is not None)
+    # the cached step is graph-captured on the cache fast path (no host sync);
+    # the partition path (--cache-partition) syncs once per forward and runs eagerly
+    use_graph = (cache is None or not args.cache_partition) and (world == 1 or reducer is not None)
     kernels_per_step = None
     if use_graph:
         table.graph_begin()
@@ -836,7 +854,10 @@ def main():
                       "tcgen05 3xTF32 where eligible (cfg3 shape), else ffma",
                       "gradient_reduce": reduce_path},
         "gpu_launches": (kernels_per_step * args.steps) if kernels_per_step else None,
-        "cache": ({"capacity": cache.capacity(), "hit_rate": cache.hit_rate()}
+        "cache": ({"capacity": cache.capacity(), "hit_rate": cache.hit_rate(),
+                   "path": ("partition (record_and_partition + forward_bags(part.tt) + combine, eager)"
+                            if args.cache_partition else
+                            "fast (cache probed inside f3_gsort; one CUDA graph per step)")}
                   if cache is not None else None),
         "clocks": clk,
         "roofline": roofline,

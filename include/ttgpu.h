@@ -74,6 +74,9 @@ int ttgpu_core_size(const ttgpu_table* t, int k, int64_t* n);
 /* TtTable::core(k) read / write as raw bytes (tt_table.hpp:43-44).  A write
  * bumps the mutation counter (tt_table.hpp:82-85) like init / sgd_step. */
 int ttgpu_get_core(ttgpu_table* t, int k, void* host_dst);
+/* copy of core k's slice of the table's dense gradient buffer (the last
+ * non-fused backward's CoreGradients::core(k)) */
+int ttgpu_get_grad(ttgpu_table* t, int k, void* host_dst);
 int ttgpu_set_core(ttgpu_table* t, int k, const void* host_src);
 int ttgpu_core_device_ptr(ttgpu_table* t, int k, void** dptr);
 int ttgpu_mark_mutated(ttgpu_table* t);                        /* tt_table.hpp:85 */
@@ -100,6 +103,11 @@ int ttgpu_set_grid_sort(ttgpu_table* t, int on);
  * outputs are bit-identical either way; gradients agree within 1e-4. */
 int ttgpu_set_chunked(ttgpu_table* t, int on);
 int ttgpu_set_generic_path(ttgpu_table* t, int on);
+/* d == 3 wide-row tables (cfg3's shape class: fp32, n0·n1 = 16, R2 = 64,
+ * n2 = 4): warp-per-chunk tail kernels with register-resident operands
+ * (1 = default, wide3.cuh) or the shared-memory staged kernels (0).  Forward
+ * outputs are bit-identical either way; gradients agree within 1e-4. */
+int ttgpu_set_wide3(ttgpu_table* t, int on);
 int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind);
 int ttgpu_mutation_counter(const ttgpu_table* t, uint64_t* out); /* tt_table.hpp:84 */
 
@@ -179,6 +187,16 @@ int ttgpu_cache_create(int64_t capacity, int64_t emb_dim, int64_t refresh_period
                        int64_t key_space, int dtype, int device, void* stream, ttgpu_cache** out);
 int ttgpu_cache_destroy(ttgpu_cache* c);
 int ttgpu_cache_set_stream(ttgpu_cache* c, void* stream);
+/* Fast path (default on): for fp32 3-core tables with a compiled fast-path
+ * shape, the cached forward consults the cache inside the fast-path sort
+ * (record + probe + slot counting sort in one kernel, no host sync, CUDA-graph
+ * capturable).  enable = 0 forces the partition path (record_and_partition +
+ * forward_bags(part.tt) + combine, lfu_cache.hpp:187-219 / model.hpp:210-223). */
+int ttgpu_cache_set_fast(ttgpu_cache* c, int enable);
+/* sizes of the last cached forward's partition (syncs on the fast path), its
+ * bag count, whether it had weights and its original pooling (any may be NULL) */
+int ttgpu_cache_last_counts(ttgpu_cache* c, int64_t* n_cached, int64_t* n_tt, int64_t* bags,
+                            int* has_weights, int* pooling);
 int64_t ttgpu_cache_default_capacity(int64_t table_rows);              /* :146-148 */
 /* state() / resident_count() / active_accesses() / active_hits() (:150-160, 259-264) */
 int ttgpu_cache_info(ttgpu_cache* c, int* active, int64_t* resident, uint64_t* accesses,

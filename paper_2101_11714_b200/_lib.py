@@ -31,6 +31,7 @@ _SIGS = {
     "ttgpu_set_stream": (C.c_int, [vp, vp]),
     "ttgpu_core_size": (C.c_int, [vp, C.c_int, i64p]),
     "ttgpu_get_core": (C.c_int, [vp, C.c_int, vp]),
+    "ttgpu_get_grad": (C.c_int, [vp, C.c_int, vp]),
     "ttgpu_set_core": (C.c_int, [vp, C.c_int, vp]),
     "ttgpu_core_device_ptr": (C.c_int, [vp, C.c_int, vpp]),
     "ttgpu_mark_mutated": (C.c_int, [vp]),
@@ -39,6 +40,7 @@ _SIGS = {
     "ttgpu_set_tensor_path": (C.c_int, [vp, C.c_int]),
     "ttgpu_set_grid_sort": (C.c_int, [vp, C.c_int]),
     "ttgpu_set_chunked": (C.c_int, [vp, C.c_int]),
+    "ttgpu_set_wide3": (C.c_int, [vp, C.c_int]),
     "ttgpu_fast_path_kind": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "ttgpu_mutation_counter": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
     "ttgpu_ctx_create": (C.c_int, [vp, vpp]),
@@ -67,6 +69,8 @@ _SIGS = {
     "ttgpu_cache_create": (C.c_int, [i64, i64, i64, i64, C.c_int, C.c_int, vp, vpp]),
     "ttgpu_cache_destroy": (C.c_int, [vp]),
     "ttgpu_cache_set_stream": (C.c_int, [vp, vp]),
+    "ttgpu_cache_set_fast": (C.c_int, [vp, C.c_int]),
+    "ttgpu_cache_last_counts": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "ttgpu_cache_default_capacity": (i64, [i64]),
     "ttgpu_cache_info": (C.c_int, [vp, vp, vp, vp, vp]),
     "ttgpu_cache_record": (C.c_int, [vp, vp, i64]),

@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
               madd4<float, kExact>(wl, acc, make_float4(0.f, 0.f, 0.f, 0.f));
         } else {
           reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
-          pool_if_last<D::N, kExact>(z, D::P1, off, L, w, mean, y, out, bag_cnt);
+          if (bag_cnt) pool_if_last<D::N, kExact>(z, D::P1, off, L, w, mean, y, out, bag_cnt);
         }
       }
     }

@@ -99,36 +99,71 @@ int grid_occ(K kern, int threads, size_t smem, int num_sms, int cap) {
 
 constexpr int kChunk = 64;  // lookups per chunk of the chunked path (fastc.cuh)
 
+// Cache mode of the fast path (lfu_cache_host.inl): the LFU cache is consulted
+// inside f3_gsort; its hits leave the chain.
+struct F3Cache {
+  int K3 = 0;
+  unsigned long long* counts = nullptr;
+  const unsigned long long* hkeys = nullptr;
+  const int* hvals = nullptr;
+  int hshift = 63;
+  unsigned long long hmask = 0;
+  int active = 0;
+  unsigned long long* hits = nullptr;
+  unsigned long long* hits2 = nullptr;
+  unsigned long long* accesses = nullptr;
+  const int64_t* slot_rows = nullptr;
+  int* lk_slot = nullptr;
+  uint32_t* perm3 = nullptr;
+  int* skey3 = nullptr;
+  int* seg_lo3 = nullptr;
+  int* seg_hi3 = nullptr;
+  int* ncached = nullptr;
+  const float* store = nullptr;
+};
+
+// Grid of the one-kernel sort for L lookups (0: infeasible): G CTAs, PW lookups per warp.
+void gsort_grid(const ttgpu_table* t, const f3::Geo& g, int64_t L, int K3, int* GS, int* PW) {
+  *GS = 0;
+  *PW = 0;
+  const size_t gs_smem = f3::gsort_smem_bytes(g.m1, g.m2, K3);
+  if (!t->grid_sort || g.m1 + g.m2 > 4 * f3::kGsThreads || K3 > 8 * f3::kGsThreads ||
+      gs_smem > 160 * 1024)
+    return;
+  set_smem(f3::f3_gsort, std::max<size_t>(gs_smem, f3::gsort_smem_bytes(g.m1, g.m2)));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort, f3::kGsThreads, gs_smem));
+  const int64_t cap = std::min<int64_t>(32 * f3::kGsMaxGridChunks,
+                                        static_cast<int64_t>(t->num_sms) * std::max(occ, 0));
+  const int64_t per = 16 * 32;  // lookups per CTA round
+  const int64_t rounds = (L + cap * per - 1) / std::max<int64_t>(1, cap * per);
+  if (cap > 0 && rounds <= f3::kGsMaxRounds) {
+    *PW = static_cast<int>(32 * std::max<int64_t>(1, rounds));
+    *GS = static_cast<int>((L + 16 * *PW - 1) / (16 * *PW));
+  }
+}
+
 template <class D>
 struct F3Runner {
   static void forward(ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L, const int64_t* off,
                       int64_t B, const double* w, int pooling, float* out, bool exact,
-                      int32_t* lk_bag, float* alpha) {
+                      int32_t* lk_bag, float* alpha, const F3Cache* cache = nullptr) {
     cudaStream_t st = t->stream;
     f3::Geo& g = f.geo;
     g = make_geo(t);
     const int Kmax = std::max(g.m1, g.m2);
     // one-kernel sort when the batch fits one co-resident grid (gsort.cuh)
-    const size_t gs_smem = f3::gsort_smem_bytes(g.m1, g.m2);
+    const int K3 = cache ? cache->K3 : 0;
+    const size_t gs_smem = f3::gsort_smem_bytes(g.m1, g.m2, K3);
     int GS = 0, PW = 0;
-    if (t->grid_sort && g.m1 + g.m2 <= 4 * f3::kGsThreads && gs_smem <= 160 * 1024) {
-      set_smem(f3::f3_gsort, gs_smem);
-      int occ = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort, f3::kGsThreads, gs_smem));
-      const int64_t cap = std::min<int64_t>(32 * f3::kGsMaxGridChunks,
-                                            static_cast<int64_t>(t->num_sms) * std::max(occ, 0));
-      const int64_t per = 16 * 32;  // lookups per CTA round
-      const int64_t rounds = (L + cap * per - 1) / std::max<int64_t>(1, cap * per);
-      if (cap > 0 && rounds <= f3::kGsMaxRounds) {
-        PW = static_cast<int>(32 * std::max<int64_t>(1, rounds));
-        GS = static_cast<int>((L + 16 * PW - 1) / (16 * PW));
-      }
-    }
+    gsort_grid(t, g, L, K3, &GS, &PW);
+    if (cache && !GS) fail(TTGPU_ERR_RUNTIME, "cache fast path needs the one-kernel sort");
+    if (cache) f.chunked = false;
     const int lpt = f3_lpt(L, Kmax);
     if (lpt == 0) fail(TTGPU_ERR_RUNTIME, "batch too large for the fast path histogram");
     const int TL = 512 * lpt;
     const int NT = static_cast<int>((L + TL - 1) / TL);
-    f.chunked = t->chunked;
+    f.chunked = t->chunked && !cache;
     const int TT1 = f.chunked ? kChunk : D::TT;  // i1-bucket tile (chunk) length
     f.max_tiles1 = static_cast<int>((L + TT1 - 1) / TT1) + g.m1;
     f.max_tiles2 = static_cast<int>((L + D::TT2 - 1) / D::TT2) + g.m2;
@@ -162,7 +197,7 @@ struct F3Runner {
     const int gb = std::max(NT, grid_for(B, 512, t->num_sms, 4));
     t->mark("fwd_begin");
     if (GS) {
-      const int K = g.m1 + g.m2;
+      const int K = g.m1 + g.m2 + K3;  // key 3 = cache slots
       f.gs_hist.ensure(4 * static_cast<size_t>(K) * GS);
       f.gs_tot.ensure(4 * static_cast<size_t>(K));
       f3::GsortArgs a{};
@@ -199,6 +234,27 @@ struct F3Runner {
       a.out = out;
       a.N = static_cast<int>(t->dp.N);
       a.bag_cnt = f.bag_cnt.as<int>();
+      if (cache) {
+        a.mean = 0;  // both partition parts are Sum-pooled (the Mean rescale is the combine's)
+        a.K3 = cache->K3;
+        a.counts = cache->counts;
+        a.hkeys = cache->hkeys;
+        a.hvals = cache->hvals;
+        a.hshift = cache->hshift;
+        a.hmask = cache->hmask;
+        a.active = cache->active;
+        a.hits = cache->hits;
+        a.hits2 = cache->hits2;
+        a.accesses = cache->accesses;
+        a.lk_slot = cache->lk_slot;
+        a.slot_rows = cache->slot_rows;
+        a.perm3 = cache->perm3;
+        a.skey3 = cache->skey3;
+        a.seg_lo3 = cache->seg_lo3;
+        a.seg_hi3 = cache->seg_hi3;
+        a.ncached = cache->ncached;
+        a.store = cache->store;
+      }
       launch_gsort(t, GS, gs_smem, a);
       t->mark("gsort");
     } else {
@@ -255,7 +311,8 @@ struct F3Runner {
                                            f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out,
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
-                                           f.tile_nslots.as<int>(), off, L, pooling, f.bag_cnt.as<int>());
+                                           f.tile_nslots.as<int>(), off, L, pooling,
+                                           cache ? nullptr : f.bag_cnt.as<int>());
     }
     t->mark("f3_fwd");
     CK(cudaGetLastError());
@@ -382,14 +439,14 @@ bool f3_feasible(const ttgpu_table* t, int64_t L) {
 
 void f3_forward(int kind, ttgpu_table* t, F3Bufs& f, const int64_t* idx, int64_t L,
                 const int64_t* off, int64_t B, const double* w, int pooling, float* out, bool exact,
-                int32_t* lk_bag, float* alpha) {
+                int32_t* lk_bag, float* alpha, const F3Cache* cache = nullptr) {
   f.kind = kind;
   switch (kind) {
-    case 0: F3Runner<F3_R8>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
-    case 1: F3Runner<F3_R16>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
-    case 2: F3Runner<F3_R32>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
-    case 3: F3Runner<F3_R64>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
-    case 4: F3Runner<F3_R4>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha); break;
+    case 0: F3Runner<F3_R8>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha, cache); break;
+    case 1: F3Runner<F3_R16>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha, cache); break;
+    case 2: F3Runner<F3_R32>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha, cache); break;
+    case 3: F3Runner<F3_R64>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha, cache); break;
+    case 4: F3Runner<F3_R4>::forward(t, f, idx, L, off, B, w, pooling, out, exact, lk_bag, alpha, cache); break;
     default: fail(TTGPU_ERR_RUNTIME, "bad fast-path kind");
   }
 }

@@ -27,6 +27,8 @@
 
 #include <cooperative_groups.h>
 
+#include "lfu_cache.cuh"
+
 namespace ttgpu {
 namespace f3 {
 
@@ -64,11 +66,34 @@ struct GsortArgs {
   float* out;    // pooled rows: empty bags are written here (zeros)
   int N;         // embedding dim
   int* bag_cnt;  // [B] pooling counters (pool_if_last), zeroed here
+  // LFU cache consulted before decompression (cache mode; K3 == 0 and
+  // counts == nullptr: no cache).  record_and_partition (lfu_cache.hpp:187-219)
+  // happens here: every valid lookup counts its row, an Active cache's hash is
+  // probed, and a hit becomes a key-3 (slot) record instead of a TT lookup.
+  int K3;                            // cache capacity (key-3 buckets); 0 = no cache
+  unsigned long long* counts;        // [rows] frequencies (record), or nullptr
+  const unsigned long long* hkeys;   // residency hash (lfu_cache.cuh probe)
+  const int* hvals;
+  int hshift;
+  unsigned long long hmask;
+  int active;                        // probe the hash (CacheState::Active)
+  unsigned long long* hits;          // += hits of this batch
+  unsigned long long* hits2;         // += hits (the chain rows not computed: EmbeddingStats)
+  unsigned long long* accesses;      // += L (Active accesses), or nullptr
+  const int64_t* slot_rows;          // [K3] row of each slot (frequency of cached rows)
+  int* lk_slot;                      // [L] slot of a cached lookup, -1 for the chain
+  uint32_t* perm3;                   // cached lookups, stable by slot
+  int* skey3;                        // their slots
+  int* seg_lo3;                      // [K3] first sorted position of a slot, -1 if none
+  int* seg_hi3;                      // [K3] one past the last
+  int* ncached;                      // [1] cached lookups in the batch
+  const float* store;                // [K3][N] cached rows (single-lookup bags pooled here)
 };
 
 // dynamic shared memory: wc[16][K] | ctot[K] | base[K] | gb1 tb1 [K1+1] | gb2 tb2 [K2+1]
-__host__ __device__ constexpr size_t gsort_smem_bytes(int K1, int K2) {
-  return 4 * (static_cast<size_t>(kGsWarps + 2) * (K1 + K2) + 2 * (K1 + 1) + 2 * (K2 + 1));
+// (K = K1 + K2 + K3; key 3 = cache slots)
+__host__ __device__ constexpr size_t gsort_smem_bytes(int K1, int K2, int K3 = 0) {
+  return 4 * (static_cast<size_t>(kGsWarps + 2) * (K1 + K2 + K3) + 2 * (K1 + 1) + 2 * (K2 + 1));
 }
 
 // largest i in [0, n) with a[i] <= x (a ascending, a[0] <= x)
@@ -100,7 +125,7 @@ __device__ __forceinline__ uint32_t div_fix(uint32_t x, uint32_t d, double inv, 
 __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   namespace cg = cooperative_groups;
   const int c = blockIdx.x, G = gridDim.x;
-  const int K1 = a.g.m1, K2 = a.g.m2, K = K1 + K2;
+  const int K1 = a.g.m1, K2 = a.g.m2, K12 = K1 + K2, K3 = a.K3, K = K12 + K3;
   extern __shared__ __align__(16) uint32_t gs_sm[];
   uint32_t* wc = gs_sm;                  // [16][K] per-warp counts -> per-warp starts
   uint32_t* ctot = wc + kGsWarps * K;    // [K] this CTA's count per key
@@ -125,8 +150,12 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   }
   for (int i = tid; i < kGsWarps * K; i += kGsThreads) wc[i] = 0u;
   // per round: k1 = i1 (0xffffffff: no lookup), d02 = i0 | i2 << 16
+  // cached lookups: k1 = 0x80000000 | slot
   uint32_t k1[kGsMaxRounds], d02[kGsMaxRounds];
   uint32_t* mywc = wc + wid * K;
+  unsigned my_hits = 0;
+  __shared__ unsigned cta_hits;
+  if (tid == 0) cta_hits = 0u;
 #pragma unroll
   for (int q0 = 0; q0 < kGsMaxRounds; q0 += 4) {
     int64_t rows[4];
@@ -143,24 +172,52 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       d02[q] = 0u;
       if (q < R) {  // warp-uniform
         const int64_t l = wbase + q * 32 + lane;
-        if (l < a.L) {
-          int64_t row = rows[u];
-          if (row < 0 || row >= a.g.num_rows) {
-            atomicMin(a.bad, static_cast<unsigned long long>(l));
-            row = 0;
-          }
-          uint32_t rem, i2;
-          const uint32_t i0 = div_fix(static_cast<uint32_t>(row), a.g.m12, a.inv_m12, rem);
-          const uint32_t i1 = div_fix(rem, static_cast<uint32_t>(a.g.m2), a.inv_m2, i2);
-          a.d2[l] = static_cast<uint16_t>(i2);
-          k1[q] = i1;
-          d02[q] = i0 | (i2 << 16);
+        const bool in = l < a.L;
+        int64_t row = rows[u];
+        bool ok = in;
+        if (in && (row < 0 || row >= a.g.num_rows)) {
+          atomicMin(a.bad, static_cast<unsigned long long>(l));
+          ok = false;
         }
-        const uint32_t x2 = k1[q] != 0xffffffffu ? d02[q] >> 16 : 0xffffffffu;
-        unsigned p = __match_any_sync(0xffffffffu, k1[q]);
-        if (k1[q] != 0xffffffffu && lane == __ffs(p) - 1) mywc[k1[q]] += __popc(p);
+        if (!ok) row = 0;
+        int slot = -1;
+        if (a.active && ok)
+          slot = lfu::probe(a.hkeys, a.hvals, a.hshift, a.hmask, static_cast<unsigned long long>(row));
+        // FreqTable::increment: chain rows warp-aggregated here; the cached (hot)
+        // rows once per CTA from the slot counts below (no same-address storm)
+        if (a.counts) {
+          const unsigned long long key = ok && slot < 0 ? static_cast<unsigned long long>(row) : ~0ull;
+          const unsigned pr = __match_any_sync(0xffffffffu, key);
+          if (key != ~0ull && lane == __ffs(pr) - 1)
+            atomicAdd(a.counts + row, static_cast<unsigned long long>(__popc(pr)));
+        }
+        if (in) {
+          if (a.lk_slot) a.lk_slot[l] = slot;
+          if (slot >= 0) {
+            k1[q] = 0x80000000u | static_cast<uint32_t>(slot);
+            ++my_hits;
+          } else {
+            uint32_t rem, i2;
+            const uint32_t i0 = div_fix(static_cast<uint32_t>(row), a.g.m12, a.inv_m12, rem);
+            const uint32_t i1 = div_fix(rem, static_cast<uint32_t>(a.g.m2), a.inv_m2, i2);
+            a.d2[l] = static_cast<uint16_t>(i2);
+            k1[q] = i1;
+            d02[q] = i0 | (i2 << 16);
+          }
+        }
+        const bool tt = k1[q] < 0x80000000u;
+        const uint32_t x1 = tt ? k1[q] : 0xffffffffu;
+        const uint32_t x2 = tt ? d02[q] >> 16 : 0xffffffffu;
+        unsigned p = __match_any_sync(0xffffffffu, x1);
+        if (tt && lane == __ffs(p) - 1) mywc[x1] += __popc(p);
         p = __match_any_sync(0xffffffffu, x2);
-        if (x2 != 0xffffffffu && lane == __ffs(p) - 1) mywc[K1 + x2] += __popc(p);
+        if (tt && lane == __ffs(p) - 1) mywc[K1 + x2] += __popc(p);
+        if (K3) {
+          const bool ca = k1[q] != 0xffffffffu && !tt;
+          const uint32_t x3 = ca ? (k1[q] & 0x7fffffffu) : 0xffffffffu;
+          p = __match_any_sync(0xffffffffu, x3);
+          if (ca && lane == __ffs(p) - 1) mywc[K12 + x3] += __popc(p);
+        }
         __syncwarp();
       }
     }
@@ -191,7 +248,18 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       a.alpha[l] = static_cast<float>(al);
     }
   }
+  if (a.hits) {
+    unsigned h = my_hits;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0 && h) atomicAdd(&cta_hits, h);
+  }
   __syncthreads();
+  if (a.accesses && c == 0 && tid == 0) atomicAdd(a.accesses, static_cast<unsigned long long>(a.L));
+  if (a.hits && tid == 0 && cta_hits) {
+    atomicAdd(a.hits, static_cast<unsigned long long>(cta_hits));
+    if (a.hits2) atomicAdd(a.hits2, static_cast<unsigned long long>(cta_hits));
+  }
   // per-warp exclusive starts within the CTA; CTA counts out
   for (int k = tid; k < K; k += kGsThreads) {
     uint32_t run = 0;
@@ -203,6 +271,8 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
     }
     ctot[k] = run;
     a.hist[static_cast<int64_t>(k) * G + c] = run;
+    if (k >= K12 && run && a.counts)  // this CTA's hits of slot k - K12
+      atomicAdd(a.counts + a.slot_rows[k - K12], static_cast<unsigned long long>(run));
   }
   cg::grid_group grid = cg::this_grid();
   grid.sync();
@@ -232,8 +302,8 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   // ---- phase B2: bases from the totals plus this CTA's prefix.  Block scan
   // of (lookups, tiles, groups) over [key 1 | key 2], IPT consecutive keys
   // per thread.
-  const int IPT = (K + kGsThreads - 1) / kGsThreads;
-  const int k_lo = min(K, tid * IPT), k_hi = min(K, k_lo + IPT);
+  const int IPT = (K12 + kGsThreads - 1) / kGsThreads;
+  const int k_lo = min(K12, tid * IPT), k_hi = min(K12, k_lo + IPT);
   uint32_t t0 = 0, t1 = 0, t2 = 0;
   for (int k = k_lo; k < k_hi; ++k) {
     const uint32_t T = __ldcg(a.tot + k);
@@ -245,7 +315,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
     // the key total, until the scan is done; this CTA's prefix (B1) in flight
     base[k] = T;
   }
-  uint32_t pre[4];  // IPT <= 4 (K <= 2048)
+  uint32_t pre[4];  // IPT <= 4 (K1 + K2 <= 2048)
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     pre[j] = k_lo + j < k_hi && ctot[k_lo + j] ? __ldcg(a.hist + static_cast<int64_t>(k_lo + j) * G + c) : 0u;
@@ -340,7 +410,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
         a.ntiles[0] = static_cast<int>(e1);
       }
     }
-    if (k == K - 1) {
+    if (k == K12 - 1) {
       gb2[K2] = e0 - k1tot[0];
       tb2[K2] = e1 - k1tot[1];
       if (c == 0) {
@@ -371,6 +441,49 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
     }
   }
   __syncthreads();
+  // key 3 (cache slots): bucket bases by a block scan of the slot totals, IPT3
+  // consecutive slots per thread; CTA 0 publishes the per-slot segments
+  if (K3) {
+    const int IPT3 = (K3 + kGsThreads - 1) / kGsThreads;
+    const int s_lo = min(K3, tid * IPT3), s_hi = min(K3, s_lo + IPT3);
+    uint32_t sum = 0;
+    for (int s = s_lo; s < s_hi; ++s) {
+      const uint32_t T = __ldcg(a.tot + K12 + s);
+      base[K12 + s] = T;
+      sum += T;
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid][0] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t v = lane < kGsWarps ? wsum[lane][0] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      __syncwarp();
+      if (lane < kGsWarps) wsum[lane][1] = v;
+    }
+    __syncthreads();
+    uint32_t e = x - sum + (wid > 0 ? wsum[wid - 1][1] : 0u);
+    for (int s = s_lo; s < s_hi; ++s) {
+      const uint32_t T = base[K12 + s];
+      if (c == 0) {
+        a.seg_lo3[s] = T ? static_cast<int>(e) : -1;
+        a.seg_hi3[s] = static_cast<int>(e + T);
+      }
+      base[K12 + s] = e + (ctot[K12 + s] ? __ldcg(a.hist + static_cast<int64_t>(K12 + s) * G + c) : 0u);
+      e += T;
+    }
+    if (c == 0 && tid == kGsThreads - 1) *a.ncached = static_cast<int>(wsum[kGsWarps - 1][1]);
+    __syncthreads();
+  }
 
   // ---- phase C: stable scatter of both keys
   const unsigned lt = lanemask_lt();
@@ -378,25 +491,59 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   for (int q = 0; q < kGsMaxRounds; ++q) {
     if (q < R) {
       const int64_t l = wbase + q * 32 + lane;
-      const uint32_t x = k1[q];
+      const bool tt = k1[q] < 0x80000000u;
+      const uint32_t x = tt ? k1[q] : 0xffffffffu;
       unsigned p = __match_any_sync(0xffffffffu, x);
-      if (x != 0xffffffffu) {
+      if (tt) {
         const uint32_t pos = base[x] + mywc[x] + __popc(p & lt);
         a.perm1[pos] = static_cast<uint32_t>(l);
         a.rec1[pos] = make_rec(static_cast<uint32_t>(l), d02[q], __ldcg(a.solo + l), __ldcg(a.lk_bag + l),
                                __ldcg(a.alpha + l));
       }
       __syncwarp();
-      if (x != 0xffffffffu && lane == __ffs(p) - 1) mywc[x] += __popc(p);
-      const uint32_t y = x != 0xffffffffu ? d02[q] >> 16 : 0xffffffffu;
+      if (tt && lane == __ffs(p) - 1) mywc[x] += __popc(p);
+      const uint32_t y = tt ? d02[q] >> 16 : 0xffffffffu;
       p = __match_any_sync(0xffffffffu, y);
-      if (y != 0xffffffffu) {
+      if (tt) {
         const uint32_t pos = base[K1 + y] + mywc[K1 + y] + __popc(p & lt);
         a.perm2[pos] = static_cast<uint32_t>(l);
       }
       __syncwarp();
-      if (y != 0xffffffffu && lane == __ffs(p) - 1) mywc[K1 + y] += __popc(p);
+      if (tt && lane == __ffs(p) - 1) mywc[K1 + y] += __popc(p);
       __syncwarp();
+      if (K3) {
+        const bool ca = k1[q] != 0xffffffffu && !tt;
+        const uint32_t z = ca ? (k1[q] & 0x7fffffffu) : 0xffffffffu;
+        p = __match_any_sync(0xffffffffu, z);
+        if (ca) {
+          const uint32_t pos = base[K12 + z] + mywc[K12 + z] + __popc(p & lt);
+          a.perm3[pos] = static_cast<uint32_t>(l);
+          a.skey3[pos] = static_cast<int>(z);
+        }
+        __syncwarp();
+        if (ca && lane == __ffs(p) - 1) mywc[K12 + z] += __popc(p);
+        __syncwarp();
+      }
+    }
+  }
+  // cache mode: a single-lookup bag whose lookup hit the cache pools here
+  // (cached_out = 0 + w·row, out = cached_out + 0: model.hpp:210-223 with an
+  // empty chain part); multi-lookup bags are combined after the forward
+  if (a.store) {
+    for (int64_t b = static_cast<int64_t>(c) * kGsThreads + tid; b < a.B;
+         b += static_cast<int64_t>(G) * kGsThreads) {
+      const int64_t s = a.off[b], e = a.off[b + 1];
+      if (e - s != 1 || s < 0 || s >= a.L) continue;
+      const int slot = __ldcg(a.lk_slot + s);
+      if (slot < 0) continue;
+      const float wl = a.w ? static_cast<float>(a.w[s]) : 1.f;
+      const float4* src = reinterpret_cast<const float4*>(a.store + static_cast<int64_t>(slot) * a.N);
+      float4* dst = reinterpret_cast<float4*>(a.out + b * a.N);
+      for (int j = 0; j < a.N / 4; ++j) {
+        const float4 v = src[j];
+        dst[j] = make_float4(__fadd_rn(0.f, __fmul_rn(wl, v.x)), __fadd_rn(0.f, __fmul_rn(wl, v.y)),
+                             __fadd_rn(0.f, __fmul_rn(wl, v.z)), __fadd_rn(0.f, __fmul_rn(wl, v.w)));
+      }
     }
   }
 }

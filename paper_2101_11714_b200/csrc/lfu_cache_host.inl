@@ -19,7 +19,7 @@ struct ttgpu_cache {
   bool active = false;
   // frequencies (dense, one counter per row) and counters [accesses, hits]
   DevBuf counts, counters, errs;
-  uint64_t accesses = 0;  // host-side (known L)
+  uint64_t accesses = 0;  // partition path: host-side (known L); fast path: counters[0]
   // residency: hash (row -> slot) + slot rows + values; double-buffered for admit
   struct Res {
     DevBuf hkeys, hvals, slot_rows, store;
@@ -42,6 +42,14 @@ struct ttgpu_cache {
   DevBuf sel_rows, sel_n, sel_cnt, top_cnt, top_rows, old_slot, fresh, fpos, new_rows, chain;
   // host-API staging
   DevBuf h_idx_stage, h_off_stage, h_w_stage;
+  // fast path: the cache consulted inside the fast-path sort (f3_gsort), no
+  // host sync; the partition exists only as per-lookup slots on the device
+  bool fast_enabled = true;
+  bool fast_part = false;  // the last partition came from the fast path
+  DevBuf f_slot, f_perm3, f_skey3, f_ncached;
+  const int64_t* f_idx = nullptr;  // the last fast forward's device batch (last_partition)
+  const int64_t* f_off = nullptr;
+  const double* f_w = nullptr;
   Res& now() { return res[cur]; }
 };
 
@@ -138,6 +146,7 @@ void cache_partition(ttgpu_cache* c, cudaStream_t st, const int64_t* idx, int64_
   CK(cudaMemcpyAsync(&nc, c->hpos.as<int>() + L, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   c->part_valid = false;
+  c->fast_part = false;
   cache_raise(c, st, host_idx, what);
   if (c->active) c->accesses += static_cast<uint64_t>(L);
   c->L = L;
@@ -272,6 +281,160 @@ void check_layer(ttgpu_cache* c, ttgpu_table* t) {
               cat("cache key space ", c->key_space, " does not match table rows ", t->plan.num_rows));
 }
 
+// ---- cache fast path: record_and_partition inside f3_gsort ---------------
+__device__ unsigned long long g_dev_cached_rows = 0;  // chain rows the fast path did not compute
+std::mutex g_fast_dev_mu;
+std::vector<int> g_fast_devs;  // devices whose g_dev_cached_rows may be non-zero
+
+}  // namespace
+
+// hits of the cache fast path so far (EmbeddingStats: chain rows it did not
+// compute), summed over the devices that ran it; reset zeroes them.  Reads
+// after the device work (the legacy-stream copy orders it on blocking streams).
+uint64_t cache_fast_rows(bool reset) {
+  std::lock_guard<std::mutex> lk(g_fast_dev_mu);
+  uint64_t total = 0;
+  int cur = 0;
+  if (g_fast_devs.empty()) return 0;
+  cudaGetDevice(&cur);
+  for (int dev : g_fast_devs) {
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    unsigned long long v = 0;
+    if (reset)
+      cudaMemcpyToSymbol(g_dev_cached_rows, &v, sizeof(v));
+    else if (cudaMemcpyFromSymbol(&v, g_dev_cached_rows, sizeof(v)) == cudaSuccess)
+      total += v;
+  }
+  cudaSetDevice(cur);
+  return total;
+}
+
+namespace {
+
+bool cache_fast_ok(ttgpu_cache* c, ttgpu_table* t, int64_t L, int64_t B) {
+  if (!c->fast_enabled || t->dtype != TTGPU_F32 || c->dtype != TTGPU_F32 || t->force_generic ||
+      t->chunked)
+    return false;
+  if (L <= 0 || B <= 0 || c->emb_dim % 4 != 0 || c->capacity < 1 || c->capacity > 4096) return false;
+  if (f3_kind(t) < 0 || !f3_feasible(t, L)) return false;
+  int GS = 0, PW = 0;
+  gsort_grid(t, make_geo(t), L, static_cast<int>(c->capacity), &GS, &PW);
+  return GS > 0;
+}
+
+void cache_forward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const int64_t* idx, int64_t L,
+                        const int64_t* off, int64_t B, const double* w, int pooling, bool save,
+                        float* out) {
+  cudaStream_t st = t->stream;
+  cache_stream(c, t);
+  const int K3 = static_cast<int>(c->capacity);
+  c->f_slot.ensure(4 * L);
+  c->f_perm3.ensure(4 * L);
+  c->f_skey3.ensure(4 * L);
+  c->f_ncached.ensure(16);
+  c->seg_lo.ensure(4 * c->capacity);
+  c->seg_hi.ensure(4 * c->capacity);
+  {
+    std::lock_guard<std::mutex> lk(g_fast_dev_mu);
+    if (std::find(g_fast_devs.begin(), g_fast_devs.end(), t->device) == g_fast_devs.end())
+      g_fast_devs.push_back(t->device);
+  }
+  unsigned long long* dev_rows = nullptr;
+  CK(cudaGetSymbolAddress(reinterpret_cast<void**>(&dev_rows), g_dev_cached_rows));
+  F3Cache fc;
+  fc.K3 = K3;
+  fc.counts = c->counts.as<unsigned long long>();
+  auto& R = c->now();
+  fc.hkeys = R.hkeys.as<unsigned long long>();
+  fc.hvals = R.hvals.as<int>();
+  fc.hshift = R.hshift;
+  fc.hmask = R.hmask;
+  fc.active = c->active && R.resident > 0 ? 1 : 0;
+  fc.hits = c->counters.as<unsigned long long>() + 1;
+  fc.accesses = fc.active ? c->counters.as<unsigned long long>() : nullptr;  // device-side: graph replays count
+  fc.hits2 = dev_rows;
+  fc.lk_slot = c->f_slot.as<int>();
+  fc.slot_rows = R.slot_rows.as<int64_t>();
+  fc.perm3 = c->f_perm3.as<uint32_t>();
+  fc.skey3 = c->f_skey3.as<int>();
+  fc.seg_lo3 = c->seg_lo.as<int>();
+  fc.seg_hi3 = c->seg_hi.as<int>();
+  fc.ncached = c->f_ncached.as<int>();
+  fc.store = fc.active ? R.store.as<float>() : nullptr;
+  // ForwardContext bookkeeping of forward_bags(part.tt): the chain part is
+  // Sum-pooled with the batch's weights; its size is known on the device only
+  ctx->table = t;
+  ctx->snapshot = t->generation;
+  ctx->L = L;
+  ctx->B = B;
+  ctx->pooling = TTGPU_SUM;
+  ctx->save = false;
+  ctx->exact = t->exact;
+  ctx->has_w = w != nullptr;
+  ctx->w_dev = w;
+  ctx->valid = true;
+  ctx->fast = true;
+  (void)save;
+  g_rows.fetch_add(static_cast<uint64_t>(L));  // less the hits, counted on the device
+  if (!ctx->f3) ctx->f3 = new F3Bufs;
+  ctx->lk_bag.ensure(4 * L);
+  ctx->lk_alpha.ensure(4 * L);
+  f3_forward(f3_kind(t), t, *ctx->f3, idx, L, off, B, w, pooling, out, t->exact,
+             ctx->lk_bag.as<int32_t>(), ctx->lk_alpha.as<float>(), &fc);
+  lfu::k_cache_pool<<<grid_for(B, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
+      B, static_cast<int>(c->emb_dim), off, L, w, c->f_slot.as<int>(),
+      fc.active ? R.store.as<float>() : nullptr, ctx->f3->y.as<float>(),
+      pooling == TTGPU_MEAN ? 1 : 0, out);
+  CK(cudaGetLastError());
+  t->mark("cache_pool");
+  c->L = L;
+  c->B = B;
+  c->pooling = pooling;
+  c->has_w = w != nullptr;
+  c->f_idx = idx;
+  c->f_off = off;
+  c->f_w = w;
+  c->fast_part = true;
+  c->part_valid = true;
+  c->grads_valid = false;
+}
+
+void cache_backward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const float* grad, bool fused,
+                         double lr) {
+  cudaStream_t st = t->stream;
+  cache_stream(c, t);
+  const int64_t B = c->B, L = c->L;
+  const int N = static_cast<int>(c->emb_dim);
+  const float* ge = grad;
+  if (c->pooling == TTGPU_MEAN) {
+    c->grad_eff.ensure(4 * B * N);
+    lfu::k_grad_eff_off<<<grid_for(B * N, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
+        B, N, c->f_off, grad, c->grad_eff.as<float>());
+    ge = c->grad_eff.as<float>();
+  }
+  // chain part: the fast-path backward over the chain lookups' tiles (the
+  // dense gradient, or fused with the SGD)
+  f3_backward(t, *ctx->f3, ge, fused ? 1 : 0, static_cast<float>(lr), ctx->lk_bag.as<int32_t>(),
+              ctx->lk_alpha.as<float>(), L);
+  if (fused) ++t->generation;
+  // slot gradients: the cached lookups sorted by slot (f3_gsort's key 3)
+  c->sg.ensure(4 * c->capacity * N);
+  c->part.ensure(4 * L * N);
+  const int64_t chunks = (L + lfu::kSlotChunk - 1) / lfu::kSlotChunk;
+  lfu::k_slot_chunks<float><<<grid_for(chunks * 32, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
+      L, N, c->f_skey3.as<int>(), reinterpret_cast<const int*>(c->f_perm3.as<uint32_t>()), c->f_w,
+      ctx->lk_bag.as<int32_t>(), ge, c->seg_lo.as<int>(), c->seg_hi.as<int>(), c->part.as<float>(),
+      c->sg.as<float>(), c->now().store.as<float>(), fused ? 1 : 0, static_cast<float>(lr),
+      c->f_ncached.as<int>());
+  lfu::k_slot_fold<float><<<grid_for(c->capacity * N * 32, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
+      c->capacity, N, c->seg_lo.as<int>(), c->seg_hi.as<int>(), c->part.as<float>(), c->sg.as<float>(),
+      c->now().store.as<float>(), fused ? 1 : 0, static_cast<float>(lr));
+  CK(cudaGetLastError());
+  t->mark("cache_slots");
+  c->grads_valid = !fused;
+}
+
 // EmbeddingLayer::forward with a cache (model.hpp:210-223), device pointers
 template <typename T>
 void cache_forward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const int64_t* idx, int64_t L,
@@ -280,6 +443,13 @@ void cache_forward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const int64_t
   check_layer(c, t);
   require_arg(ctx != nullptr, "forward needs a context");
   cudaStream_t st = t->stream;
+  if constexpr (std::is_same_v<T, float>) {
+    if (cache_fast_ok(c, t, L, B)) {
+      cache_forward_fast(c, t, ctx, idx, L, off, B, w, pooling, save, out);
+      return;
+    }
+  }
+  c->fast_part = false;
   cache_partition(c, st, idx, L, off, B, w, pooling, host_idx,
                   cat("table '", t->name, "'").c_str());
   const int N = static_cast<int>(c->emb_dim);
@@ -302,6 +472,12 @@ void cache_backward(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const T* gra
   check_layer(c, t);
   require_arg(c->part_valid, "cache backward needs the partition of a cached forward");
   check_ctx(t, ctx);
+  if constexpr (std::is_same_v<T, float>) {
+    if (c->fast_part) {
+      cache_backward_fast(c, t, ctx, grad, fused, lr);
+      return;
+    }
+  }
   cudaStream_t st = t->stream;
   const int64_t B = c->B;
   const int N = static_cast<int>(c->emb_dim);
@@ -407,6 +583,30 @@ int ttgpu_cache_create(int64_t capacity, int64_t emb_dim, int64_t refresh_period
   });
 }
 
+int ttgpu_cache_set_fast(ttgpu_cache* c, int enable) {
+  return guarded([&] { c->fast_enabled = enable != 0; });
+}
+
+int ttgpu_cache_last_counts(ttgpu_cache* c, int64_t* n_cached, int64_t* n_tt, int64_t* bags,
+                            int* has_weights, int* pooling) {
+  return guarded([&] {
+    require_arg(c->part_valid, "no partition recorded");
+    int64_t nc = c->n_cached;
+    if (c->fast_part) {
+      ttgpu::cache_order_after_last(c);
+      int v = 0;
+      CK(cudaMemcpyAsync(&v, c->f_ncached.p, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      nc = v;
+    }
+    if (n_cached) *n_cached = nc;
+    if (n_tt) *n_tt = c->L - nc;
+    if (bags) *bags = c->B;
+    if (has_weights) *has_weights = c->has_w ? 1 : 0;
+    if (pooling) *pooling = c->pooling;
+  });
+}
+
 int ttgpu_cache_destroy(ttgpu_cache* c) {
   return guarded([&] {
     if (!c) return;
@@ -431,7 +631,7 @@ int ttgpu_cache_info(ttgpu_cache* c, int* active, int64_t* resident, uint64_t* a
     CK(cudaStreamSynchronize(c->stream));
     if (active) *active = c->active ? 1 : 0;
     if (resident) *resident = c->now().resident;
-    if (accesses) *accesses = c->accesses;
+    if (accesses) *accesses = c->accesses + h[0];  // partition path (host) + fast path (device)
     if (hits) *hits = h[1];
   });
 }
@@ -486,6 +686,40 @@ int ttgpu_cache_last_partition(ttgpu_cache* c, int64_t* cached_slots, int64_t* c
   return guarded([&] {
     require_arg(c->part_valid, "no partition recorded");
     cudaStream_t st = c->stream;
+    if (c->fast_part) {
+      // fast path: rebuild CachePartition (lfu_cache.hpp:187-219) from the
+      // per-lookup slots and the forward's device batch (still alive)
+      cache_order_after_last(c);
+      const int64_t L = c->L, B = c->B;
+      std::vector<int> slot(static_cast<size_t>(L));
+      std::vector<int64_t> idx(static_cast<size_t>(L)), off(static_cast<size_t>(B + 1));
+      std::vector<double> w(c->has_w ? static_cast<size_t>(L) : 0);
+      CK(cudaMemcpyAsync(slot.data(), c->f_slot.p, 4 * L, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(idx.data(), c->f_idx, 8 * L, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(off.data(), c->f_off, 8 * (B + 1), cudaMemcpyDeviceToHost, st));
+      if (c->has_w) CK(cudaMemcpyAsync(w.data(), c->f_w, 8 * L, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      int64_t nc = 0, nt = 0;
+      for (int64_t b = 0; b < B; ++b) {
+        if (cached_off) cached_off[b] = nc;
+        if (tt_off) tt_off[b] = nt;
+        for (int64_t l = off[b]; l < off[b + 1]; ++l) {
+          if (slot[l] >= 0) {
+            if (cached_slots) cached_slots[nc] = slot[l];
+            if (cached_rows) cached_rows[nc] = idx[l];
+            if (cached_w && c->has_w) cached_w[nc] = w[l];
+            ++nc;
+          } else {
+            if (tt_idx) tt_idx[nt] = idx[l];
+            if (tt_w && c->has_w) tt_w[nt] = w[l];
+            ++nt;
+          }
+        }
+      }
+      if (cached_off) cached_off[B] = nc;
+      if (tt_off) tt_off[B] = nt;
+      return;
+    }
     auto cp = [&](void* dst, const DevBuf& src, size_t bytes) {
       if (dst && bytes) CK(cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDeviceToHost, st));
     };

@@ -306,9 +306,50 @@ __global__ void k_head_fwd(DevPlan P, const T* __restrict__ cores,
       for (int e = threadIdx.x; e < s1; e += blockDim.x) g1s[e] = G1[(int64_t)i1 * s1 + e];
       __syncthreads();
       const int outs = P0 * C1;
-      bool quad_done = false;
-      if constexpr (std::is_same_v<T, float>) quad_done = (C1 & 3) == 0;
-      if (quad_done) {
+      bool quad_done = false, block4 = false;
+      if constexpr (std::is_same_v<T, float>) {
+        quad_done = (C1 & 3) == 0;
+        block4 = quad_done && P0 == 4;
+      }
+      if (block4) {
+        // fp32, P0 == 4 (cfg3): a thread owns all 4 rows x 4 adjacent columns
+        // of one pair; per p one 16-byte G1 load and the 4 G0 values (read as
+        // broadcasts) feed 16 products -- the same per-element p-ascending chain
+        const int C4 = C1 >> 2;
+        for (int e = threadIdx.x; e < (run_hi - run_lo) * C4; e += blockDim.x) {
+          const int q = e / C4, c = (e - q * C4) * 4;
+          const float* arow = reinterpret_cast<const float*>(g0s) + (run_lo - p0 + q) * s0;
+          const float* gcol = reinterpret_cast<const float*>(g1s) + c;
+          float v[4][4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[a][u] = 0.f;
+#pragma unroll 4
+          for (int p = 0; p < R1; ++p) {
+            const float4 g = *reinterpret_cast<const float4*>(gcol + p * C1);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const float x = arow[a * R1 + p];
+              if (kExact) {
+                const float2 p01 = fmul2_rn(x, make_float2(g.x, g.y));
+                const float2 p23 = fmul2_rn(x, make_float2(g.z, g.w));
+                v[a][0] = __fadd_rn(v[a][0], p01.x);
+                v[a][1] = __fadd_rn(v[a][1], p01.y);
+                v[a][2] = __fadd_rn(v[a][2], p23.x);
+                v[a][3] = __fadd_rn(v[a][3], p23.y);
+              } else {
+                ffma2(x, g.x, g.y, v[a][0], v[a][1]);
+                ffma2(x, g.z, g.w, v[a][2], v[a][3]);
+              }
+            }
+          }
+          float* hrow = reinterpret_cast<float*>(H) + static_cast<int64_t>(run_lo + q) * P.W1 + c;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            *reinterpret_cast<float4*>(hrow + a * C1) = make_float4(v[a][0], v[a][1], v[a][2], v[a][3]);
+        }
+      } else if (quad_done) {
         // fp32: four adjacent columns per thread, products two at a time
         // (FMUL2 / FFMA2), the same per-element p-ascending chain
         const int outs4 = outs >> 2;
@@ -1026,12 +1067,13 @@ __global__ void k_combine(const T* __restrict__ partials, const unsigned long lo
                           const int32_t* __restrict__ seg, const int* __restrict__ nseg_dev,
                           int nseg_host, int Wc, T* __restrict__ out, T lr) {
   const int nseg = nseg_dev ? *nseg_dev : nseg_host;
+  // gridDim.y > 1 splits a wide row's elements over several CTAs
   for (int g = blockIdx.x; g < nseg; g += gridDim.x) {
     const int first = seg[g], last = seg[g + 1] - 1;
     if (last < first) continue;  // empty segment: untouched slice
     const int r0 = static_cast<int>(scan[first] >> 32) - 1;
     const int r1 = static_cast<int>(scan[last] >> 32) - 1;
-    for (int e = threadIdx.x; e < Wc; e += blockDim.x) {
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < Wc; e += blockDim.x * gridDim.y) {
       T sum = partials[static_cast<int64_t>(r0) * Wc + e];
       for (int r = r0 + 1; r <= r1; ++r) sum += partials[static_cast<int64_t>(r) * Wc + e];
       if (OUT_MODE == 0)
@@ -1183,27 +1225,55 @@ __global__ void k_head_bwd(DevPlan P, const T* __restrict__ cores, const T* __re
 // from earlier batches are rejected by checking the pair key back.
 // OUT_MODE 0 writes the dense slice, 1 applies SGD to touched slices.
 template <typename T, int OUT_MODE>
-__global__ void k_head_g0(DevPlan P, const T* __restrict__ D0, const int32_t* __restrict__ pair_tab,
-                          const uint32_t* __restrict__ pair_key_u, const int* __restrict__ counts,
-                          T* __restrict__ out, T lr) {
+__global__ void __launch_bounds__(128) k_head_g0(DevPlan P, const T* __restrict__ D0,
+                                                 const int32_t* __restrict__ pair_tab,
+                                                 const uint32_t* __restrict__ pair_key_u,
+                                                 const int* __restrict__ counts, T* __restrict__ out,
+                                                 T lr) {
+  // the pair ids of a tile of i1 values are resolved by all threads at once
+  // (one round trip), then every thread sums its elements over them in i1
+  // order -- the D0 loads of consecutive i1 are independent and pipeline
+  constexpr int kTile = 1024, kEPT = 4;
+  __shared__ int pids[kTile];
   const int U = counts[0];
   const int s0 = P.slice[0], m0 = P.m[0], m1 = P.m[1];
   for (int i0 = blockIdx.x; i0 < m0; i0 += gridDim.x) {
-    for (int e = threadIdx.x; e < s0; e += blockDim.x) {
-      T sum = T(0);
+    for (int e0 = 0; e0 < s0; e0 += kEPT * blockDim.x) {
+      T sum[kEPT];
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k) sum[k] = T(0);
       bool touched = false;
-      for (int i1 = 0; i1 < m1; ++i1) {
-        const uint32_t key = static_cast<uint32_t>(i1) * static_cast<uint32_t>(m0) + i0;
-        const int pid = pair_tab[key];
-        if (pid < 0 || pid >= U || pair_key_u[pid] != key) continue;
-        sum += D0[static_cast<int64_t>(pid) * s0 + e];
-        touched = true;
+      for (int b = 0; b < m1; b += kTile) {
+        const int nb = m1 - b < kTile ? m1 - b : kTile;
+        __syncthreads();
+        for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+          const uint32_t key = static_cast<uint32_t>(b + j) * static_cast<uint32_t>(m0) + i0;
+          const int pid = pair_tab[key];
+          pids[j] = (pid < 0 || pid >= U || pair_key_u[pid] != key) ? -1 : pid;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int j = 0; j < nb; ++j) {
+          const int pid = pids[j];
+          if (pid < 0) continue;
+          touched = true;
+#pragma unroll
+          for (int k = 0; k < kEPT; ++k) {
+            const int e = e0 + k * blockDim.x + threadIdx.x;
+            if (e < s0) sum[k] += D0[static_cast<int64_t>(pid) * s0 + e];
+          }
+        }
       }
-      if (OUT_MODE == 0)
-        out[static_cast<int64_t>(i0) * s0 + e] = sum;
-      else if (touched)
-        out[static_cast<int64_t>(i0) * s0 + e] =
-            add_rn<T>(out[static_cast<int64_t>(i0) * s0 + e], -mul_rn<T>(lr, sum));
+#pragma unroll
+      for (int k = 0; k < kEPT; ++k) {
+        const int e = e0 + k * blockDim.x + threadIdx.x;
+        if (e >= s0) continue;
+        if (OUT_MODE == 0)
+          out[static_cast<int64_t>(i0) * s0 + e] = sum[k];
+        else if (touched)
+          out[static_cast<int64_t>(i0) * s0 + e] =
+              add_rn<T>(out[static_cast<int64_t>(i0) * s0 + e], -mul_rn<T>(lr, sum[k]));
+      }
     }
   }
 }

@@ -25,6 +25,7 @@
 #include "tt_kernels.cuh"
 #include "head_tc.cuh"
 #include "fast3.cuh"
+#include "wide3.cuh"
 
 namespace ttgpu {
 namespace {
@@ -197,6 +198,7 @@ struct ttgpu_table {
   int pdl = 0;                 // fast-path launches: 0 plain, 1 programmatic dependent launch
   bool grid_sort = true;       // fast path: one-kernel cooperative sort (gsort.cuh) where the batch fits
   bool chunked = false;        // fast path: chunked forward / S+dG1+D0 backward (fastc.cuh; slower, off)
+  bool wide3 = true;           // d == 3 wide rows: warp-per-chunk tail kernels (wide3.cuh)
   // optional phase timing (CUDA events between pipeline phases)
   // Marks recorded while the stream is being captured become event-record nodes of
   // the graph (cudaEventRecordExternal) and stay owned by it: every graph launch
@@ -276,6 +278,7 @@ struct ttgpu_ctx {
   DevBuf s_dkey, s_dlk, dscan, dseg, pair_i1, scan1, seg1, S, D0, partS, partK, part1;
   // d == 3 wide-row path: per-lookup y rows, dG2 contributions, i2 positions
   DevBuf ybuf, tcontrib, pos2;
+  DevBuf w3_slab_base, w3_slab_part, w3_cnt;  // wide3.cuh segsum slabs
   CachedGraph gfwd, gbwd;  // host-API kernel sequences
   size_t cub_bytes = 0;
 };
@@ -364,6 +367,14 @@ T* core_ptr(ttgpu_table* t, int k) {
 
 namespace ttgpu {
 namespace {
+
+// The warp-per-chunk wide-row tail kernels (wide3.cuh) serve fp32 3-core
+// tables of cfg3's shape class.
+bool wide3_ok(const ttgpu_table* t) {
+  const DevPlan& P = t->dp;
+  return t->dtype == TTGPU_F32 && t->wide3 && P.d == 3 && P.prefix[1] == w3::P1 &&
+         P.r[2] == w3::R2 && P.n[2] == w3::N2 && P.r[3] == 1 && P.m[2] <= 1024 * 64;
+}
 
 // ------------------------------------------------------------- forward ---
 template <typename T>
@@ -472,6 +483,22 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
                     96 * 1024 &&
       P.W1 >= 32) {
     c->ybuf.ensure(sizeof(T) * L * P.N);
+    if (wide3_ok(t)) {  // warp-per-chunk tail (wide3.cuh)
+      const int64_t nch = (L + kTailChunk - 1) / kTailChunk;
+      const int g = static_cast<int>(std::min<int64_t>((nch + w3::kWarps - 1) / w3::kWarps,
+                                                       static_cast<int64_t>(t->num_sms) * 8));
+      auto kern = exact ? w3::k_w3_fwd<true> : w3::k_w3_fwd<false>;
+      kern<<<g, w3::kWarps * 32, 0, st>>>(
+          reinterpret_cast<const float*>(t->cores.as<T>() + P.coff[2]),
+          reinterpret_cast<const float*>(c->H.as<T>()), c->lk_pid.as<int32_t>(),
+          c->tail_dig.as<uint32_t>(), c->s_lk.as<uint32_t>(), L, reinterpret_cast<float*>(c->ybuf.as<T>()));
+      auto pk = exact ? k_pool_rows<T, true> : k_pool_rows<T, false>;
+      pk<<<grid_for(B * P.N, kThreads, t->num_sms), kThreads, 0, st>>>(
+          c->ybuf.as<T>(), off, B, L, P.N, w, pooling, out);
+      t->mark("tail_pool");
+      CK(cudaGetLastError());
+      return;
+    }
     const size_t smem =
         sizeof(T) * (P.W1 + P.prefix[1] + 4 + static_cast<size_t>(kTailChunk) * P.slice[2]);
     const int cw = std::is_same_v<T, float> ? (P.n[2] % 4 == 0 ? 4 : P.n[2] % 2 == 0 ? 2 : 1) : 1;
@@ -594,7 +621,25 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   const bool staged3 = d == 3 && P.W1 <= kRun3MaxEPT * 256 && P.slice[2] <= kRun3MaxEPT * 256 &&
                        sizeof(T) * kTailChunk * (P.N + P.slice[2]) <= 96 * 1024 &&
                        sizeof(T) * 8 * (P.W1 + P.N) <= 96 * 1024;
-  if (staged3) {
+  const bool w3path = staged3 && wide3_ok(t);
+  if (w3path) {
+    // S partials and the dG2 contributions in one warp-per-chunk pass (wide3.cuh)
+    c->pos2.ensure(4 * L);
+    c->tcontrib.ensure(sizeof(T) * L * P.slice[2]);
+    k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>(), L, c->pos2.as<uint32_t>());
+    set_smem(w3::k_w3_bwd, w3::kBwdSmem);
+    const int g = static_cast<int>(std::min<int64_t>((nchunksL + w3::kWarps - 1) / w3::kWarps,
+                                                     static_cast<int64_t>(t->num_sms) * 2));
+    w3::k_w3_bwd<<<g, w3::kWarps * 32, w3::kBwdSmem, st>>>(
+        reinterpret_cast<const float*>(cores + P.coff[2]), reinterpret_cast<const float*>(c->H.as<T>()),
+        c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(),
+        reinterpret_cast<const float*>(c->lk_alpha.as<T>()), reinterpret_cast<const float*>(grad),
+        c->s_lk.as<uint32_t>(), c->pair_scan.as<unsigned long long>(), c->pos2.as<uint32_t>(), L,
+        reinterpret_cast<float*>(c->partS.as<T>()), reinterpret_cast<float*>(c->tcontrib.as<T>()));
+    k_combine<T, 0><<<grid_for(ucap, 1, t->num_sms, 8), 128, 0, st>>>(
+        c->partS.as<T>(), c->pair_scan.as<unsigned long long>(), c->pair_start.as<int32_t>(),
+        c->counts.as<int>(), 0, P.W1, c->S.as<T>(), T(0));
+  } else if (staged3) {
     const size_t smem = sizeof(T) * kTailChunk * (P.N + P.slice[2]) + 4 * kTailChunk;
     set_smem(k_srun3<T>, smem);
     k_srun3<T><<<grid_for(nchunksL, 1, t->num_sms, 8), 256, smem, st>>>(
@@ -628,7 +673,27 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   for (int k = 2; k < d; ++k) {
     const int j = k - 2;
     const int Wc = P.slice[k];
-    if (staged3) {
+    if (w3path) {
+      // contributions already at their i2-sorted positions (k_w3_bwd): slab sums
+      const int nseg = P.m[k];
+      const int64_t max_slabs = (L + w3::kW3Slab - 1) / w3::kW3Slab + nseg;
+      c->w3_slab_base.ensure(4 * (nseg + 1));
+      c->w3_slab_part.ensure(sizeof(float) * max_slabs * w3::S2);
+      if (c->w3_cnt.cap < 4 * static_cast<size_t>(nseg)) {
+        c->w3_cnt.ensure(4 * static_cast<size_t>(nseg));
+        CK(cudaMemsetAsync(c->w3_cnt.p, 0, c->w3_cnt.cap, st));
+      }
+      const int32_t* seg = c->dseg.as<int32_t>() + segoff;
+      w3::k_w3_slabs<<<1, 1024, 0, st>>>(seg, nseg, c->w3_slab_base.as<int32_t>());
+      T* dst = fuse_tail ? cores + P.coff[k] : grads + P.coff[k];
+      auto sk = fuse_tail ? w3::k_w3_segsum<1> : w3::k_w3_segsum<0>;
+      sk<<<static_cast<int>(max_slabs), 64, 0, st>>>(
+          reinterpret_cast<const float*>(c->tcontrib.as<T>()), seg, nseg, c->w3_slab_base.as<int32_t>(),
+          c->w3_slab_part.as<float>(), c->w3_cnt.as<int>(), reinterpret_cast<float*>(dst),
+          static_cast<float>(lr));
+      segoff += P.m[k] + 1;
+      continue;
+    } else if (staged3) {
       // contributions computed in pair order (H staged per pair run), stored at
       // each lookup's i2-sorted position, then summed per i2 segment in order
       c->pos2.ensure(4 * L);
@@ -710,12 +775,15 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
   }
   t->mark("bwd_head");
   const bool fuse_head = (mode == 1);
+  // wide G1 slices (cfg3: 16,384 floats) are split over CTAs along y
+  const dim3 gh(grid_for(P.m[1], 1, t->num_sms, 8),
+                static_cast<unsigned>(std::max(1, std::min(16, P.slice[1] / 1024))));
   if (fuse_head)
-    k_combine<T, 1><<<grid_for(P.m[1], 1, t->num_sms, 8), 256, 0, st>>>(
+    k_combine<T, 1><<<gh, 256, 0, st>>>(
         c->part1.as<T>(), c->scan1.as<unsigned long long>(), c->seg1.as<int32_t>(), nullptr, P.m[1],
         P.slice[1], cores + P.coff[1], tlr);
   else
-    k_combine<T, 0><<<grid_for(P.m[1], 1, t->num_sms, 8), 256, 0, st>>>(
+    k_combine<T, 0><<<gh, 256, 0, st>>>(
         c->part1.as<T>(), c->scan1.as<unsigned long long>(), c->seg1.as<int32_t>(), nullptr, P.m[1],
         P.slice[1], grads + P.coff[1], T(0));
   t->mark("bwd_head_combine");
@@ -986,6 +1054,15 @@ int ttgpu_get_core(ttgpu_table* t, int k, void* dst) {
   });
 }
 
+int ttgpu_get_grad(ttgpu_table* t, int k, void* dst) {
+  return guarded([&] {
+    require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
+    CK(cudaMemcpyAsync(dst, static_cast<char*>(t->grads.p) + t->esz * t->dp.coff[k],
+                       t->esz * t->plan.core_size(k), cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
 int ttgpu_set_core(ttgpu_table* t, int k, const void* src) {
   return guarded([&] {
     require_arg(k >= 0 && k < t->plan.tt_dim, cat("core index ", k, " out of range"));
@@ -1020,6 +1097,10 @@ int ttgpu_fast_path_kind(const ttgpu_table* t, int* kind) {
 
 int ttgpu_set_chunked(ttgpu_table* t, int on) {
   return guarded([&] { t->chunked = on != 0; });
+}
+
+int ttgpu_set_wide3(ttgpu_table* t, int on) {
+  return guarded([&] { t->wide3 = on != 0; });
 }
 
 int ttgpu_set_grid_sort(ttgpu_table* t, int on) {
@@ -1410,11 +1491,16 @@ int ttgpu_check(ttgpu_table* t) {
   return guarded([&] { raise_latched(t, nullptr, 0); });
 }
 
+namespace ttgpu {
+uint64_t cache_fast_rows(bool reset);  // lfu_cache_host.inl
+}
 void ttgpu_stats_reset(void) {
+  ttgpu::cache_fast_rows(true);
   g_rows.store(0);
   g_ws_peak.store(g_ws_cur.load());
 }
-uint64_t ttgpu_stats_rows(void) { return g_rows.load(); }
+// the cache fast path counts every lookup here and its hits on the device
+uint64_t ttgpu_stats_rows(void) { return g_rows.load() - ttgpu::cache_fast_rows(false); }
 uint64_t ttgpu_stats_peak_workspace(void) { return g_ws_peak.load(); }
 void ttgpu_stats_add_rows(uint64_t n) { g_rows.fetch_add(n); }
 

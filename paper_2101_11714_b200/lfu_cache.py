@@ -124,6 +124,26 @@ class LfuCache:
 
     default_capacity = staticmethod(default_capacity)
 
+    def set_fast(self, enable: bool):
+        """Cached forward through the fast-path sort (default; no host sync,
+        graph-capturable) or through the explicit partition (False)."""
+        _raise(lib().ttgpu_cache_set_fast(self.handle, 1 if enable else 0))
+
+    def _last(self):
+        nc, nt, b, hw, pl = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+        _raise(lib().ttgpu_cache_last_counts(self.handle, C.byref(nc), C.byref(nt), C.byref(b),
+                                             C.byref(hw), C.byref(pl)))
+        return nc.value, nt.value, b.value, bool(hw.value), pl.value
+
+    def last_counts(self):
+        """(cached, chain) lookup counts of the last cached forward."""
+        return self._last()[:2]
+
+    def last_partition(self) -> "CachePartition":
+        """The partition of the last cached forward (record_and_partition's
+        result; the fast path rebuilds it from its per-lookup slots)."""
+        return self._fetch_partition(*self._last())
+
     # ---- accessors (lfu_cache.hpp:150-175) ----
     def _info(self):
         a, r, acc, hits = C.c_int(), C.c_int64(), C.c_uint64(), C.c_uint64()
@@ -202,18 +222,21 @@ class LfuCache:
         _raise(lib().ttgpu_cache_record_and_partition(
             self.handle, _p(batch.indices), L, _p(batch.offsets), B, _p(w), int(batch.pooling),
             C.byref(nc), C.byref(nt)))
-        cs = np.zeros(max(nc.value, 1), np.int64)
-        cr = np.zeros(max(nc.value, 1), np.int64)
+        return self._fetch_partition(nc.value, nt.value, B, w is not None, int(batch.pooling))
+
+    def _fetch_partition(self, nc: int, nt: int, B: int, has_w: bool, pooling: int) -> "CachePartition":
+        cs = np.zeros(max(nc, 1), np.int64)
+        cr = np.zeros(max(nc, 1), np.int64)
         co = np.zeros(B + 1, np.int64)
-        ti = np.zeros(max(nt.value, 1), np.int64)
+        ti = np.zeros(max(nt, 1), np.int64)
         to = np.zeros(B + 1, np.int64)
-        cw = np.zeros(max(nc.value, 1), np.float64) if w is not None else None
-        tw = np.zeros(max(nt.value, 1), np.float64) if w is not None else None
+        cw = np.zeros(max(nc, 1), np.float64) if has_w else None
+        tw = np.zeros(max(nt, 1), np.float64) if has_w else None
         _raise(lib().ttgpu_cache_last_partition(self.handle, _p(cs), _p(cr), _p(co), _p(cw), _p(ti),
                                                 _p(to), _p(tw)))
-        cached = IndexBatch(cs[: nc.value], co, None if cw is None else cw[: nc.value], Pooling.Sum)
-        tt = IndexBatch(ti[: nt.value], to, None if tw is None else tw[: nt.value], Pooling.Sum)
-        return CachePartition(cached, cr[: nc.value], tt, Pooling(batch.pooling))
+        cached = IndexBatch(cs[:nc], co, None if cw is None else cw[:nc], Pooling.Sum)
+        tt = IndexBatch(ti[:nt], to, None if tw is None else tw[:nt], Pooling.Sum)
+        return CachePartition(cached, cr[:nc], tt, Pooling(pooling))
 
     # ---- admission (lfu_cache.hpp:223-243) ----
     def warmup_finalize(self, table: TtTable):

@@ -246,6 +246,12 @@ class TtTable:
         _raise(lib().ttgpu_get_core(self.handle, k, _p(out)))
         return out
 
+    def grad(self, k: int) -> np.ndarray:
+        """Copy of core k's slice of the table's dense gradient buffer."""
+        out = np.zeros(self._plan.core_size(k), self.dtype)
+        _raise(lib().ttgpu_get_grad(self.handle, k, _p(out)))
+        return out
+
     def cores(self) -> List[np.ndarray]:
         return [self.core(k) for k in range(self.dim())]
 
@@ -287,6 +293,10 @@ class TtTable:
     def set_grid_sort(self, on: bool):
         """Fast path: one-kernel cooperative sort (gsort.cuh) (default on) or the three-kernel sort."""
         _raise(lib().ttgpu_set_grid_sort(self.handle, int(bool(on))))
+
+    def set_wide3(self, on: bool):
+        """d == 3 wide rows (cfg3 class): warp-per-chunk tail kernels (default on)."""
+        _raise(lib().ttgpu_set_wide3(self.handle, int(bool(on))))
 
     def set_chunked(self, on: bool):
         """Fast path: chunked kernels (fastc.cuh) or the 32-lookup tile kernels (default)."""
