@@ -50,6 +50,15 @@ struct ttgpu_cache {
   const int64_t* f_idx = nullptr;  // the last fast forward's device batch (last_partition)
   const int64_t* f_off = nullptr;
   const double* f_w = nullptr;
+  // side stream for the slot gradients (forked from / joined to the table's
+  // stream: they overlap the chain backward, also inside a captured graph)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~ttgpu_cache() {
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
   Res& now() { return res[cur]; }
 };
 
@@ -413,14 +422,19 @@ void cache_backward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const f
         B, N, c->f_off, grad, c->grad_eff.as<float>());
     ge = c->grad_eff.as<float>();
   }
-  // chain part: the fast-path backward over the chain lookups' tiles (the
-  // dense gradient, or fused with the SGD)
-  f3_backward(t, *ctx->f3, ge, fused ? 1 : 0, static_cast<float>(lr), ctx->lk_bag.as<int32_t>(),
-              ctx->lk_alpha.as<float>(), L);
-  if (fused) ++t->generation;
-  // slot gradients: the cached lookups sorted by slot (f3_gsort's key 3)
+  // slot gradients (the cached lookups sorted by slot: f3_gsort's key 3) on a
+  // side stream, concurrent with the chain part's backward
+  if (!c->side) {
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
   c->sg.ensure(4 * c->capacity * N);
   c->part.ensure(4 * L * N);
+  CK(cudaEventRecord(c->ev_fork, st));
+  CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  const cudaStream_t st_main = st;
+  st = c->side;
   const int64_t chunks = (L + lfu::kSlotChunk - 1) / lfu::kSlotChunk;
   lfu::k_slot_chunks<float><<<grid_for(chunks * 32, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
       L, N, c->f_skey3.as<int>(), reinterpret_cast<const int*>(c->f_perm3.as<uint32_t>()), c->f_w,
@@ -431,7 +445,15 @@ void cache_backward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const f
       c->capacity, N, c->seg_lo.as<int>(), c->seg_hi.as<int>(), c->part.as<float>(), c->sg.as<float>(),
       c->now().store.as<float>(), fused ? 1 : 0, static_cast<float>(lr));
   CK(cudaGetLastError());
-  t->mark("cache_slots");
+  CK(cudaEventRecord(c->ev_join, st));
+  st = st_main;
+  // chain part: the fast-path backward over the chain lookups' tiles (the
+  // dense gradient, or fused with the SGD)
+  f3_backward(t, *ctx->f3, ge, fused ? 1 : 0, static_cast<float>(lr), ctx->lk_bag.as<int32_t>(),
+              ctx->lk_alpha.as<float>(), L);
+  if (fused) ++t->generation;
+  CK(cudaStreamWaitEvent(st, c->ev_join, 0));
+  t->mark("cache_bwd");
   c->grads_valid = !fused;
 }
 

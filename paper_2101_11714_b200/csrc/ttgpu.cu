@@ -488,7 +488,8 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
       const int g = static_cast<int>(std::min<int64_t>((nch + w3::kWarps - 1) / w3::kWarps,
                                                        static_cast<int64_t>(t->num_sms) * 8));
       auto kern = exact ? w3::k_w3_fwd<true> : w3::k_w3_fwd<false>;
-      kern<<<g, w3::kWarps * 32, 0, st>>>(
+      set_smem(kern, w3::kFwdSmem);
+      kern<<<g, w3::kWarps * 32, w3::kFwdSmem, st>>>(
           reinterpret_cast<const float*>(t->cores.as<T>() + P.coff[2]),
           reinterpret_cast<const float*>(c->H.as<T>()), c->lk_pid.as<int32_t>(),
           c->tail_dig.as<uint32_t>(), c->s_lk.as<uint32_t>(), L, reinterpret_cast<float*>(c->ybuf.as<T>()));
@@ -628,9 +629,9 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
     c->tcontrib.ensure(sizeof(T) * L * P.slice[2]);
     k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>(), L, c->pos2.as<uint32_t>());
     set_smem(w3::k_w3_bwd, w3::kBwdSmem);
-    const int g = static_cast<int>(std::min<int64_t>((nchunksL + w3::kWarps - 1) / w3::kWarps,
-                                                     static_cast<int64_t>(t->num_sms) * 2));
-    w3::k_w3_bwd<<<g, w3::kWarps * 32, w3::kBwdSmem, st>>>(
+    const int g = static_cast<int>(std::min<int64_t>((nchunksL + w3::kWarpsB - 1) / w3::kWarpsB,
+                                                     static_cast<int64_t>(t->num_sms) * 3));
+    w3::k_w3_bwd<<<g, w3::kWarpsB * 32, w3::kBwdSmem, st>>>(
         reinterpret_cast<const float*>(cores + P.coff[2]), reinterpret_cast<const float*>(c->H.as<T>()),
         c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(),
         reinterpret_cast<const float*>(c->lk_alpha.as<T>()), reinterpret_cast<const float*>(grad),

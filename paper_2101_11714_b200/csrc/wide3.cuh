@@ -45,21 +45,53 @@ constexpr int P1 = 16, R2 = 64, N2 = 4, N = P1 * N2, W1 = P1 * R2, S2 = R2 * N2;
 constexpr int kWarps = 8;      // warps per CTA
 constexpr int kChunk = 32;     // lookups per warp work unit (== kTailChunk)
 constexpr int kW3Slab = 64;    // rows of C per segsum slab
-constexpr size_t kBwdSmem = sizeof(float) * kWarps * kChunk * N;  // 64 KB
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+// Packed fp32 pairs held in 64-bit registers (sm_100a f32x2 ops).
+__device__ __forceinline__ unsigned long long pk(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 upk(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b,
+                                                   unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 // ---------------------------------------------------------------- forward --
+// Up to kRunsPerPass pair runs of a chunk are staged at once (H transposed,
+// [r][a]), so every lane of the chunk computes in the same pass.
+constexpr int kRunsPerPass = 2;
+constexpr int kRB = 8;          // G2 rows per staged block
+constexpr int kGsStride = 9;    // float4 per staged lookup block (8 rows + 1 pad: no bank conflicts)
+constexpr size_t kFwdSmem =
+    sizeof(float) * kWarps * (kRunsPerPass * W1 + kChunk * kGsStride * 4);  // 64 + 36 KB
+
 template <bool kExact>
-__global__ void __launch_bounds__(kWarps * 32) k_w3_fwd(const float* __restrict__ G2,
+__global__ void __launch_bounds__(kWarps * 32, 2) k_w3_fwd(const float* __restrict__ G2,
                                                         const float* __restrict__ H,
                                                         const int32_t* __restrict__ lk_pid,
                                                         const uint32_t* __restrict__ tail_dig,
                                                         const uint32_t* __restrict__ s_lk, int64_t L,
                                                         float* __restrict__ y) {
-  __shared__ __align__(16) float hs_all[kWarps][R2 * P1];  // H staged transposed: [r][a]
+  // per warp: [kRunsPerPass][R2][P1] H rows (transposed) | [kChunk][kGsStride] float4 G2 block
+  extern __shared__ __align__(16) float w3f_dyn[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* hs = hs_all[wid];
+  float* hs_w = w3f_dyn + wid * (kRunsPerPass * W1 + kChunk * kGsStride * 4);
+  float4* gs = reinterpret_cast<float4*>(hs_w + kRunsPerPass * W1);
   const int64_t nchunks = (L + kChunk - 1) / kChunk;
   for (int64_t ch = static_cast<int64_t>(blockIdx.x) * kWarps + wid; ch < nchunks;
        ch += static_cast<int64_t>(gridDim.x) * kWarps) {
@@ -71,82 +103,111 @@ __global__ void __launch_bounds__(kWarps * 32) k_w3_fwd(const float* __restrict_
       pid = lk_pid[l];
       i2 = static_cast<int>(tail_dig[l]);
     }
-    const float* g2 = G2 + static_cast<int64_t>(i2) * S2;
-    for (int q0 = 0; q0 < n;) {
-      const int p = __shfl_sync(0xffffffffu, pid, q0);
-      const unsigned same = __ballot_sync(0xffffffffu, lane < n && pid == p);
-      const int q1 = 32 - __clz(same);  // runs are contiguous: last member + 1
+    // run starts: lane q starts a run iff its pair differs from lane q - 1's
+    const int prev = __shfl_up_sync(0xffffffffu, pid, 1);
+    const unsigned starts = __ballot_sync(0xffffffffu, lane < n && (lane == 0 || prev != pid));
+    const int my_run = __popc(starts & ((2u << lane) - 1u)) - 1;  // this lane's run ordinal
+    const int nruns = __popc(starts);
+    for (int r0 = 0; r0 < nruns; r0 += kRunsPerPass) {
+      const int rn = min(kRunsPerPass, nruns - r0);
       __syncwarp();
-      // H[p] (P1 x R2, a-major) -> hs[r][a]
-      const float* hp = H + static_cast<int64_t>(p) * W1;
+      for (int k = 0; k < rn; ++k) {
+        // the k-th run's pair: the lane at the (r0 + k)-th set bit of starts
+        unsigned m = starts;
+        for (int z = 0; z < r0 + k; ++z) m &= m - 1;
+        const int p = __shfl_sync(0xffffffffu, pid, __ffs(m) - 1);
+        const float* hp = H + static_cast<int64_t>(p) * W1;
+        float* hs = hs_w + k * W1;
+        // column r = it % 2 * 32 + lane, a-group g = it / 2: 4 coalesced loads,
+        // one 16-byte store into the [r][a] layout
 #pragma unroll
-      for (int k = 0; k < W1 / 32 / 4; ++k) {
-        const int e = (k * 32 + lane) * 4;  // 4 consecutive r of one a
-        const float4 v = ld4(hp + e);
-        const int a = e / R2, r = e - a * R2;
-        hs[(r + 0) * P1 + a] = v.x;
-        hs[(r + 1) * P1 + a] = v.y;
-        hs[(r + 2) * P1 + a] = v.z;
-        hs[(r + 3) * P1 + a] = v.w;
+        for (int it = 0; it < 2 * (P1 / 4); ++it) {
+          const int r = (it & 1) * 32 + lane, g = it >> 1;
+          const float4 v = make_float4(__ldg(hp + (4 * g + 0) * R2 + r), __ldg(hp + (4 * g + 1) * R2 + r),
+                                       __ldg(hp + (4 * g + 2) * R2 + r), __ldg(hp + (4 * g + 3) * R2 + r));
+          *reinterpret_cast<float4*>(hs + r * P1 + 4 * g) = v;
+        }
       }
-      __syncwarp();
-      if (lane >= q0 && lane < q1) {
-        float4 acc[P1];
+      const int k = my_run - r0;
+      const bool act = lane < n && k >= 0 && k < rn;
+      const float* hs = hs_w + (act ? k : 0) * W1;
+      float4 acc[P1];
 #pragma unroll
-        for (int a = 0; a < P1; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-        for (int r = 0; r < R2; ++r) {
-          const float4 g = ld4(g2 + r * N2);
-          const float4* h4 = reinterpret_cast<const float4*>(hs + r * P1);
+      for (int a = 0; a < P1; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int rb = 0; rb < R2; rb += kRB) {
+        // G2 rows [rb, rb + kRB) of every lookup of the chunk: 4 lookups x 128 B
+        // per warp load (coalesced), lane q then reads its own block
+        __syncwarp();
 #pragma unroll
-          for (int a4 = 0; a4 < P1 / 4; ++a4) {
-            const float4 h = h4[a4];
-            const float hv[4] = {h.x, h.y, h.z, h.w};
+        for (int it = 0; it < kChunk / 4; ++it) {
+          const int qq = it * 4 + (lane >> 3), piece = lane & 7;
+          const int iq = __shfl_sync(0xffffffffu, i2, qq);
+          if (qq < n) gs[qq * kGsStride + piece] = ld4(G2 + static_cast<int64_t>(iq) * S2 + (rb + piece) * N2);
+        }
+        __syncwarp();
+        if (act) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              float4& c = acc[a4 * 4 + u];
-              if constexpr (kExact) {
-                const float2 p01 = fmul2_rn(hv[u], make_float2(g.x, g.y));
-                const float2 p23 = fmul2_rn(hv[u], make_float2(g.z, g.w));
-                c.x = __fadd_rn(c.x, p01.x);
-                c.y = __fadd_rn(c.y, p01.y);
-                c.z = __fadd_rn(c.z, p23.x);
-                c.w = __fadd_rn(c.w, p23.y);
-              } else {
-                ffma2(hv[u], g.x, g.y, c.x, c.y);
-                ffma2(hv[u], g.z, g.w, c.z, c.w);
+          for (int rr = 0; rr < kRB; ++rr) {
+            const float4 g = gs[lane * kGsStride + rr];
+            const float4* h4 = reinterpret_cast<const float4*>(hs + (rb + rr) * P1);
+#pragma unroll
+            for (int a4 = 0; a4 < P1 / 4; ++a4) {
+              const float4 h = h4[a4];
+              const float hv[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                float4& c = acc[a4 * 4 + u];
+                if constexpr (kExact) {
+                  const float2 p01 = fmul2_rn(hv[u], make_float2(g.x, g.y));
+                  const float2 p23 = fmul2_rn(hv[u], make_float2(g.z, g.w));
+                  c.x = __fadd_rn(c.x, p01.x);
+                  c.y = __fadd_rn(c.y, p01.y);
+                  c.z = __fadd_rn(c.z, p23.x);
+                  c.w = __fadd_rn(c.w, p23.y);
+                } else {
+                  ffma2(hv[u], g.x, g.y, c.x, c.y);
+                  ffma2(hv[u], g.z, g.w, c.z, c.w);
+                }
               }
             }
           }
         }
+      }
+      if (act) {
         float4* yo = reinterpret_cast<float4*>(y + static_cast<int64_t>(l) * N);
 #pragma unroll
         for (int a = 0; a < P1; ++a) yo[a] = acc[a];
       }
-      q0 = q1;
     }
   }
 }
 
 // --------------------------------------------------------------- backward --
-__global__ void __launch_bounds__(kWarps * 32, 2) k_w3_bwd(
+// D2 is staged as DUPLICATED pairs (d, d), so every f32x2 operand is a natural
+// register pair: no packing moves in the inner loop.
+constexpr int kWarpsB = 4;
+constexpr int kDdStride = N + 2;  // pairs per staged lookup (+16 B: conflict-free 16-byte stores)
+constexpr size_t kBwdSmem = sizeof(unsigned long long) * kWarpsB * kChunk * kDdStride;  // 66 KB
+
+__global__ void __launch_bounds__(kWarpsB * 32, 3) k_w3_bwd(
     const float* __restrict__ G2, const float* __restrict__ H, const int32_t* __restrict__ lk_pid,
     const uint32_t* __restrict__ tail_dig, const int32_t* __restrict__ lk_bag,
     const float* __restrict__ lk_alpha, const float* __restrict__ grad,
     const uint32_t* __restrict__ s_lk, const unsigned long long* __restrict__ scan,
     const uint32_t* __restrict__ pos2, int64_t L, float* __restrict__ partS,
     float* __restrict__ contrib) {
-  extern __shared__ __align__(16) float w3_dyn[];  // [kWarps][kChunk * N]: the chunk's D2 rows
+  extern __shared__ __align__(16) float w3b_dyn[];  // [kWarpsB][kChunk][P1][N2] (d, d) pairs
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* d2s = w3_dyn + wid * kChunk * N;
+  unsigned long long* dd = reinterpret_cast<unsigned long long*>(w3b_dyn) + wid * kChunk * kDdStride;
   const int r0 = 2 * lane;  // this lane's two columns r0, r0 + 1
   const int64_t nchunks = (L + kChunk - 1) / kChunk;
-  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * kWarps + wid; ch < nchunks;
-       ch += static_cast<int64_t>(gridDim.x) * kWarps) {
+  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * kWarpsB + wid; ch < nchunks;
+       ch += static_cast<int64_t>(gridDim.x) * kWarpsB) {
     const int64_t c0 = ch * kChunk;
     const int n = static_cast<int>(L - c0 < kChunk ? L - c0 : kChunk);
-    int pid = -1, i2 = 0, run = 0;
+    int pid = -1, i2 = 0, run = 0, bag = 0;
     uint32_t p2 = 0;
+    float al = 0.f;
     __syncwarp();
     if (lane < n) {
       const int l = static_cast<int>(s_lk[c0 + lane]);
@@ -154,21 +215,28 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_bwd(
       i2 = static_cast<int>(tail_dig[l]);
       run = static_cast<int>(scan[c0 + lane] >> 32) - 1;
       p2 = pos2[l];
-      // D2 = T(alpha)·grad[bag], one row per lane
-      const float al = lk_alpha[l];
-      const float4* gr = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bag[l]) * N);
-      float4* dst = reinterpret_cast<float4*>(d2s + lane * N);
-#pragma unroll
-      for (int k = 0; k < N / 4; ++k) {
-        const float4 v = __ldg(gr + k);
-        dst[k] = make_float4(__fmul_rn(al, v.x), __fmul_rn(al, v.y), __fmul_rn(al, v.z),
-                             __fmul_rn(al, v.w));
+      bag = lk_bag[l];
+      al = lk_alpha[l];
+    }
+    // D2 = T(alpha)·grad[bag] as (d, d) pairs: two lookups' rows (2 x 256 B)
+    // per warp load, lanes 16 B apart (coalesced and conflict-free)
+#pragma unroll 4
+    for (int it = 0; it < kChunk / 2; ++it) {
+      const int qq = it * 2 + (lane >> 4), k4 = lane & 15;
+      const int bq = __shfl_sync(0xffffffffu, bag, qq);
+      const float aq = __shfl_sync(0xffffffffu, al, qq);
+      if (qq < n) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bq) * N) + k4);
+        const float x = __fmul_rn(aq, v.x), yv = __fmul_rn(aq, v.y), z = __fmul_rn(aq, v.z),
+                    w = __fmul_rn(aq, v.w);
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(dd + qq * kDdStride + 4 * k4);
+        dst[0] = make_ulonglong2(pk(x, x), pk(yv, yv));
+        dst[1] = make_ulonglong2(pk(z, z), pk(w, w));
       }
     }
     __syncwarp();
-    float2 h[P1], s[P1];
+    unsigned long long h[P1], s[P1];
     int cur = -1;
-    // G2 rows of the first lookup; later ones are loaded one lookup ahead
     int i2n = __shfl_sync(0xffffffffu, i2, 0);
     float4 ga = ld4(G2 + static_cast<int64_t>(i2n) * S2 + r0 * N2);
     float4 gb = ld4(G2 + static_cast<int64_t>(i2n) * S2 + (r0 + 1) * N2);
@@ -176,52 +244,51 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_bwd(
       const int p = __shfl_sync(0xffffffffu, pid, q);
       const int rq = __shfl_sync(0xffffffffu, run, q);
       const uint32_t pq = __shfl_sync(0xffffffffu, p2, q);
-      const float4 g0 = ga, g1 = gb;
+      // G2 column pairs (G2[r0][j], G2[r0+1][j]) of this lookup
+      const unsigned long long gp0 = pk(ga.x, gb.x), gp1 = pk(ga.y, gb.y), gp2 = pk(ga.z, gb.z),
+                               gp3 = pk(ga.w, gb.w);
       if (q + 1 < n) {
         i2n = __shfl_sync(0xffffffffu, i2, q + 1);
         ga = ld4(G2 + static_cast<int64_t>(i2n) * S2 + r0 * N2);
         gb = ld4(G2 + static_cast<int64_t>(i2n) * S2 + (r0 + 1) * N2);
       }
-      if (p != cur) {  // a new pair run: its H columns into registers, S from zero
+      if (p != cur) {  // a new pair run: its H column pairs into registers, S from zero
         const float* hp = H + static_cast<int64_t>(p) * W1 + r0;
 #pragma unroll
         for (int a = 0; a < P1; ++a) {
-          h[a] = __ldg(reinterpret_cast<const float2*>(hp + a * R2));
-          s[a] = make_float2(0.f, 0.f);
+          h[a] = __ldg(reinterpret_cast<const unsigned long long*>(hp + a * R2));
+          s[a] = 0ull;
         }
         cur = p;
       }
-      float2 c[N2];
-#pragma unroll
-      for (int j = 0; j < N2; ++j) c[j] = make_float2(0.f, 0.f);
-      const float4* d4 = reinterpret_cast<const float4*>(d2s + q * N);
+      unsigned long long c0v = 0ull, c1v = 0ull, c2v = 0ull, c3v = 0ull;
+      const ulonglong2* d2 = reinterpret_cast<const ulonglong2*>(dd + q * kDdStride);
 #pragma unroll
       for (int a = 0; a < P1; ++a) {
-        const float4 d = d4[a];  // D2[a][0..3] (broadcast)
+        const ulonglong2 d01 = d2[2 * a], d23 = d2[2 * a + 1];  // (D2[a][j], D2[a][j]) pairs
         // S: v = Σ_j D2[a][j]·G2[r][j] (fma chain from zero), S += v
-        float v0 = 0.f, v1 = 0.f;
-        ffma2(d.x, g0.x, g1.x, v0, v1);
-        ffma2(d.y, g0.y, g1.y, v0, v1);
-        ffma2(d.z, g0.z, g1.z, v0, v1);
-        ffma2(d.w, g0.w, g1.w, v0, v1);
-        s[a].x += v0;
-        s[a].y += v1;
+        unsigned long long v = fma2(d01.x, gp0, 0ull);
+        v = fma2(d01.y, gp1, v);
+        v = fma2(d23.x, gp2, v);
+        v = fma2(d23.y, gp3, v);
+        s[a] = add2(s[a], v);
         // C[r][j] += H[a][r]·D2[a][j] (a ascending from zero)
-        ffma2(d.x, h[a].x, h[a].y, c[0].x, c[0].y);
-        ffma2(d.y, h[a].x, h[a].y, c[1].x, c[1].y);
-        ffma2(d.z, h[a].x, h[a].y, c[2].x, c[2].y);
-        ffma2(d.w, h[a].x, h[a].y, c[3].x, c[3].y);
+        c0v = fma2(h[a], d01.x, c0v);
+        c1v = fma2(h[a], d01.y, c1v);
+        c2v = fma2(h[a], d23.x, c2v);
+        c3v = fma2(h[a], d23.y, c3v);
       }
       // C rows r0, r0 + 1 (4 columns each) at the lookup's i2-sorted position
+      const float2 e0 = upk(c0v), e1 = upk(c1v), e2 = upk(c2v), e3 = upk(c3v);
       float4* co = reinterpret_cast<float4*>(contrib + static_cast<int64_t>(pq) * S2 + r0 * N2);
-      co[0] = make_float4(c[0].x, c[1].x, c[2].x, c[3].x);
-      co[1] = make_float4(c[0].y, c[1].y, c[2].y, c[3].y);
+      co[0] = make_float4(e0.x, e1.x, e2.x, e3.x);
+      co[1] = make_float4(e0.y, e1.y, e2.y, e3.y);
       // the run ends here: its S partial row (a-major, [a][r])
       const int pn = q + 1 < n ? __shfl_sync(0xffffffffu, pid, q + 1) : -2;
       if (pn != p) {
         float* so = partS + static_cast<int64_t>(rq) * W1 + r0;
 #pragma unroll
-        for (int a = 0; a < P1; ++a) *reinterpret_cast<float2*>(so + a * R2) = s[a];
+        for (int a = 0; a < P1; ++a) *reinterpret_cast<unsigned long long*>(so + a * R2) = s[a];
       }
     }
   }
