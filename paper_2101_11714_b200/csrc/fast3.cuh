@@ -102,10 +102,16 @@ __device__ __forceinline__ void add4(float4& a, const float4 b) {
 // order -- f3_pool's arithmetic (embedding_ops.hpp:232-249) -- and stores the
 // pooled row.  The sort kernel zeroes bag_cnt for every bag of the batch and
 // writes the (zero) rows of empty bags, so no separate pooling pass runs.
+// Cache mode (lk_slot != nullptr, lfu_cache_host.inl): the bag's cached
+// lookups count as already done (f3_gsort presets bag_cnt), and the pooled row
+// is cached_out + tt_out, each summed in lookup order (model.hpp:210-223,
+// combine_partition_outputs lfu_cache.hpp:106-126).
 template <int N, bool kExact>
 __device__ __forceinline__ void pool_if_last(int bag, int parts, const int64_t* __restrict__ off,
                                              int64_t L, const double* __restrict__ w, int mean,
-                                             const float* y, float* __restrict__ out, int* bag_cnt) {
+                                             const float* y, float* __restrict__ out, int* bag_cnt,
+                                             const int* __restrict__ lk_slot = nullptr,
+                                             const float* __restrict__ store = nullptr) {
   __threadfence();  // this task's y row before its count
   const int64_t s = off[bag], e = off[bag + 1];
   if (atomicAdd(bag_cnt + bag, 1) != static_cast<int>(e - s) * parts - 1) return;
@@ -114,11 +120,21 @@ __device__ __forceinline__ void pool_if_last(int bag, int parts, const int64_t* 
   const float inv = static_cast<float>(1.0 / static_cast<double>(e - s));
 #pragma unroll
   for (int c = 0; c < N / 4; ++c) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), cac = acc;
     for (int64_t l = lo; l < hi; ++l) {
       const float a = static_cast<float>(w ? w[l] : 1.0);
-      acc = madd4<float, kExact>(a, __ldcg(reinterpret_cast<const float4*>(y + l * N) + c), acc);
+      const int slot = lk_slot ? __ldcg(lk_slot + l) : -1;
+      if (slot >= 0) {
+        const float4 v = reinterpret_cast<const float4*>(store + static_cast<int64_t>(slot) * N)[c];
+        cac = make_float4(__fadd_rn(cac.x, __fmul_rn(a, v.x)), __fadd_rn(cac.y, __fmul_rn(a, v.y)),
+                          __fadd_rn(cac.z, __fmul_rn(a, v.z)), __fadd_rn(cac.w, __fmul_rn(a, v.w)));
+      } else {
+        acc = madd4<float, kExact>(a, __ldcg(reinterpret_cast<const float4*>(y + l * N) + c), acc);
+      }
     }
+    if (lk_slot)
+      acc = make_float4(__fadd_rn(cac.x, acc.x), __fadd_rn(cac.y, acc.y), __fadd_rn(cac.z, acc.z),
+                        __fadd_rn(cac.w, acc.w));
     if (mean && e - s > 1) {
       acc.x = __fmul_rn(acc.x, inv);
       acc.y = __fmul_rn(acc.y, inv);
@@ -600,7 +616,7 @@ struct FwdSmem {
 // Tile descriptors and sorted records (lookup, digits; f3_scatter) are loaded
 // two tiles ahead.  Saves H rows and, per lookup, the H row index (hloc) for
 // f3_bwd2.
-template <class D, bool kExact>
+template <class D, bool kExact, bool kCache = false>
 __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restrict__ cores,
                                                    const Tile* __restrict__ tiles,
                                                    const int* __restrict__ ntiles,
@@ -613,7 +629,9 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots,
                                                    const int64_t* __restrict__ off, int64_t L, int mean,
-                                                   int* __restrict__ bag_cnt) {
+                                                   int* __restrict__ bag_cnt,
+                                                   const int* __restrict__ cache_slot,
+                                                   const float* __restrict__ store) {
   pdl_entry();
   using SM = FwdSmem<D>;
   extern __shared__ __align__(128) float sm[];
@@ -762,7 +780,10 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
               madd4<float, kExact>(wl, acc, make_float4(0.f, 0.f, 0.f, 0.f));
         } else {
           reinterpret_cast<float4*>(y + static_cast<int64_t>(lk_l[i]) * D::N)[a] = acc;
-          if (bag_cnt) pool_if_last<D::N, kExact>(z, D::P1, off, L, w, mean, y, out, bag_cnt);
+          if constexpr (kCache)
+            pool_if_last<D::N, kExact>(z, D::P1, off, L, w, mean, y, out, bag_cnt, cache_slot, store);
+          else
+            pool_if_last<D::N, kExact>(z, D::P1, off, L, w, mean, y, out, bag_cnt);
         }
       }
     }

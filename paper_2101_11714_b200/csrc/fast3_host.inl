@@ -236,6 +236,8 @@ struct F3Runner {
       a.bag_cnt = f.bag_cnt.as<int>();
       if (cache) {
         a.mean = 0;  // both partition parts are Sum-pooled (the Mean rescale is the combine's)
+        a.pool_mean = pooling;
+        a.parts = D::P1;
         a.K3 = cache->K3;
         a.counts = cache->counts;
         a.hkeys = cache->hkeys;
@@ -304,15 +306,17 @@ struct F3Runner {
                 f.tile_nslots.as<int>(), off, L, pooling, f.bag_cnt.as<int>());
     } else {
       const size_t sm = f3::FwdSmem<D>::bytes(g.m0);
-      auto kern = exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>;
+      auto kern = cache ? (exact ? f3::f3_fwd<D, true, true> : f3::f3_fwd<D, false, true>)
+                        : (exact ? f3::f3_fwd<D, true> : f3::f3_fwd<D, false>);
       set_smem(kern, sm);
       const int grid = grid_occ(kern, f3::kThreads, sm, t->num_sms, f.max_tiles1);
       f3_launch(t->pdl, kern, dim3(grid), dim3(f3::kThreads), sm, st, g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
                                            f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out,
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
-                                           f.tile_nslots.as<int>(), off, L, pooling,
-                                           cache ? nullptr : f.bag_cnt.as<int>());
+                                           f.tile_nslots.as<int>(), off, L, pooling, f.bag_cnt.as<int>(),
+                                           cache ? cache->lk_slot : nullptr,
+                                           cache ? cache->store : nullptr);
     }
     t->mark("f3_fwd");
     CK(cudaGetLastError());

@@ -88,6 +88,8 @@ struct GsortArgs {
   int* seg_hi3;                      // [K3] one past the last
   int* ncached;                      // [1] cached lookups in the batch
   const float* store;                // [K3][N] cached rows (single-lookup bags pooled here)
+  int pool_mean;                     // the batch's Mean pooling (cache mode: all-cached bags)
+  int parts;                         // pool_if_last tasks per lookup (f3_fwd: P1)
 };
 
 // dynamic shared memory: wc[16][K] | ctot[K] | base[K] | gb1 tb1 [K1+1] | gb2 tb2 [K2+1]
@@ -526,23 +528,37 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       }
     }
   }
-  // cache mode: a single-lookup bag whose lookup hit the cache pools here
-  // (cached_out = 0 + w·row, out = cached_out + 0: model.hpp:210-223 with an
-  // empty chain part); multi-lookup bags are combined after the forward
-  if (a.store) {
+  // cache mode: a bag whose lookups ALL hit the cache pools here (cached_out =
+  // Σ w·row in lookup order, out = cached_out + 0, the Mean rescale:
+  // model.hpp:210-223 with an empty chain part); a bag with chain lookups
+  // presets its pooling counter with its cached lookups, so its last chain
+  // lookup pools it in f3_fwd (pool_if_last)
+  if (a.K3) {
     for (int64_t b = static_cast<int64_t>(c) * kGsThreads + tid; b < a.B;
          b += static_cast<int64_t>(G) * kGsThreads) {
       const int64_t s = a.off[b], e = a.off[b + 1];
-      if (e - s != 1 || s < 0 || s >= a.L) continue;
-      const int slot = __ldcg(a.lk_slot + s);
-      if (slot < 0) continue;
-      const float wl = a.w ? static_cast<float>(a.w[s]) : 1.f;
-      const float4* src = reinterpret_cast<const float4*>(a.store + static_cast<int64_t>(slot) * a.N);
-      float4* dst = reinterpret_cast<float4*>(a.out + b * a.N);
+      if (e - s < 1 || s < 0 || e > a.L) continue;
+      int nc = 0;
+      for (int64_t l = s; l < e; ++l) nc += __ldcg(a.lk_slot + l) >= 0 ? 1 : 0;
+      if (nc < e - s) {
+        if (e - s > 1) a.bag_cnt[b] = nc * a.parts;
+        continue;
+      }
+      const float inv = static_cast<float>(1.0 / static_cast<double>(e - s));
       for (int j = 0; j < a.N / 4; ++j) {
-        const float4 v = src[j];
-        dst[j] = make_float4(__fadd_rn(0.f, __fmul_rn(wl, v.x)), __fadd_rn(0.f, __fmul_rn(wl, v.y)),
-                             __fadd_rn(0.f, __fmul_rn(wl, v.z)), __fadd_rn(0.f, __fmul_rn(wl, v.w)));
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t l = s; l < e; ++l) {
+          const float wl = a.w ? static_cast<float>(a.w[l]) : 1.f;
+          const float4 v = reinterpret_cast<const float4*>(a.store + static_cast<int64_t>(__ldcg(a.lk_slot + l)) * a.N)[j];
+          acc = make_float4(__fadd_rn(acc.x, __fmul_rn(wl, v.x)), __fadd_rn(acc.y, __fmul_rn(wl, v.y)),
+                            __fadd_rn(acc.z, __fmul_rn(wl, v.z)), __fadd_rn(acc.w, __fmul_rn(wl, v.w)));
+        }
+        acc = make_float4(__fadd_rn(acc.x, 0.f), __fadd_rn(acc.y, 0.f), __fadd_rn(acc.z, 0.f),
+                          __fadd_rn(acc.w, 0.f));  // + tt_out (zero)
+        if (a.pool_mean && e - s > 1)
+          acc = make_float4(__fmul_rn(acc.x, inv), __fmul_rn(acc.y, inv), __fmul_rn(acc.z, inv),
+                            __fmul_rn(acc.w, inv));
+        reinterpret_cast<float4*>(a.out + b * a.N)[j] = acc;
       }
     }
   }

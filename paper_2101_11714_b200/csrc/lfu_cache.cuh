@@ -192,50 +192,6 @@ __global__ void k_combine(int64_t B, int N, const int64_t* __restrict__ c_off,
   }
 }
 
-// Cache fast path (the cache consulted inside f3_gsort): bags of more than one
-// lookup, after the forward.  cached_out = Σ T(w)·store[slot] over the bag's
-// cached lookups and tt_out = Σ T(w)·y over its chain lookups, each in lookup
-// order with separately rounded products and sums (axpy, gemm.hpp:64-66; the
-// Sum pooling of forward_bags), out = cached_out + tt_out, then the original
-// Mean rescale (combine_partition_outputs, lfu_cache.hpp:106-126).  Empty and
-// single-lookup bags were written by f3_gsort / f3_fwd.  Thread per bag (most
-// bags exit at once), 4 columns at a time.
-__global__ void k_cache_pool(int64_t B, int N, const int64_t* __restrict__ off, int64_t L,
-                             const double* __restrict__ w, const int* __restrict__ lk_slot,
-                             const float* __restrict__ store, const float* __restrict__ y, int mean,
-                             float* __restrict__ out) {
-  const int N4 = N / 4;
-  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < B;
-       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = off[b], e = off[b + 1];
-    if (e - s <= 1) continue;
-    const int64_t lo = s < 0 ? 0 : s, hi = e > L ? L : e;
-    for (int j = 0; j < N4; ++j) {
-      float4 c = make_float4(0.f, 0.f, 0.f, 0.f), t = c;
-      for (int64_t l = lo; l < hi; ++l) {
-        const float a = w ? static_cast<float>(w[l]) : 1.f;
-        const int slot = lk_slot[l];
-        const float4 v = slot >= 0
-                             ? reinterpret_cast<const float4*>(store + static_cast<int64_t>(slot) * N)[j]
-                             : __ldcg(reinterpret_cast<const float4*>(y + l * N) + j);
-        float4& acc = slot >= 0 ? c : t;
-        acc.x = __fadd_rn(acc.x, __fmul_rn(a, v.x));
-        acc.y = __fadd_rn(acc.y, __fmul_rn(a, v.y));
-        acc.z = __fadd_rn(acc.z, __fmul_rn(a, v.z));
-        acc.w = __fadd_rn(acc.w, __fmul_rn(a, v.w));
-      }
-      float4 v = make_float4(__fadd_rn(c.x, t.x), __fadd_rn(c.y, t.y), __fadd_rn(c.z, t.z),
-                             __fadd_rn(c.w, t.w));
-      if (mean) {
-        const float inv = static_cast<float>(1.0 / static_cast<double>(e - s));
-        v = make_float4(__fmul_rn(v.x, inv), __fmul_rn(v.y, inv), __fmul_rn(v.z, inv),
-                        __fmul_rn(v.w, inv));
-      }
-      reinterpret_cast<float4*>(out + b * N)[j] = v;
-    }
-  }
-}
-
 // grad_eff for a Mean batch on the cache fast path: the original bag size from
 // the batch's own offsets (model.hpp:242-252).
 __global__ void k_grad_eff_off(int64_t B, int N, const int64_t* __restrict__ off,

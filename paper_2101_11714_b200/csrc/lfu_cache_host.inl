@@ -370,7 +370,7 @@ void cache_forward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const in
   fc.seg_lo3 = c->seg_lo.as<int>();
   fc.seg_hi3 = c->seg_hi.as<int>();
   fc.ncached = c->f_ncached.as<int>();
-  fc.store = fc.active ? R.store.as<float>() : nullptr;
+  fc.store = R.store.as<float>();  // read only for hits (none while warming up)
   // ForwardContext bookkeeping of forward_bags(part.tt): the chain part is
   // Sum-pooled with the batch's weights; its size is known on the device only
   ctx->table = t;
@@ -391,12 +391,8 @@ void cache_forward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const in
   ctx->lk_alpha.ensure(4 * L);
   f3_forward(f3_kind(t), t, *ctx->f3, idx, L, off, B, w, pooling, out, t->exact,
              ctx->lk_bag.as<int32_t>(), ctx->lk_alpha.as<float>(), &fc);
-  lfu::k_cache_pool<<<grid_for(B, kThreads, c->num_sms, 8), kThreads, 0, st>>>(
-      B, static_cast<int>(c->emb_dim), off, L, w, c->f_slot.as<int>(),
-      fc.active ? R.store.as<float>() : nullptr, ctx->f3->y.as<float>(),
-      pooling == TTGPU_MEAN ? 1 : 0, out);
-  CK(cudaGetLastError());
-  t->mark("cache_pool");
+  // every bag was pooled by f3_gsort (all lookups cached) or by the last
+  // chain lookup in f3_fwd (pool_if_last with the cached rows): no combine pass
   c->L = L;
   c->B = B;
   c->pooling = pooling;
@@ -425,7 +421,9 @@ void cache_backward_fast(ttgpu_cache* c, ttgpu_table* t, ttgpu_ctx* ctx, const f
   // slot gradients (the cached lookups sorted by slot: f3_gsort's key 3) on a
   // side stream, concurrent with the chain part's backward
   if (!c->side) {
-    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;  // lowest priority: the chain backward is the critical path
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   }

@@ -485,8 +485,8 @@ void forward_impl(ttgpu_table* t, ttgpu_ctx* c, const int64_t* idx, int64_t L, c
     c->ybuf.ensure(sizeof(T) * L * P.N);
     if (wide3_ok(t)) {  // warp-per-chunk tail (wide3.cuh)
       const int64_t nch = (L + kTailChunk - 1) / kTailChunk;
-      const int g = static_cast<int>(std::min<int64_t>((nch + w3::kWarps - 1) / w3::kWarps,
-                                                       static_cast<int64_t>(t->num_sms) * 8));
+      const int g = static_cast<int>(std::min<int64_t>((nch + w3::kWarps / 2 - 1) / (w3::kWarps / 2),
+                                                       static_cast<int64_t>(t->num_sms) * 3));
       auto kern = exact ? w3::k_w3_fwd<true> : w3::k_w3_fwd<false>;
       set_smem(kern, w3::kFwdSmem);
       kern<<<g, w3::kWarps * 32, w3::kFwdSmem, st>>>(
@@ -629,7 +629,7 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
     c->tcontrib.ensure(sizeof(T) * L * P.slice[2]);
     k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>(), L, c->pos2.as<uint32_t>());
     set_smem(w3::k_w3_bwd, w3::kBwdSmem);
-    const int g = static_cast<int>(std::min<int64_t>((nchunksL + w3::kWarpsB - 1) / w3::kWarpsB,
+    const int g = static_cast<int>(std::min<int64_t>((nchunksL + w3::kWarpsB / 2 - 1) / (w3::kWarpsB / 2),
                                                      static_cast<int64_t>(t->num_sms) * 3));
     w3::k_w3_bwd<<<g, w3::kWarpsB * 32, w3::kBwdSmem, st>>>(
         reinterpret_cast<const float*>(cores + P.coff[2]), reinterpret_cast<const float*>(c->H.as<T>()),

@@ -77,24 +77,39 @@ __device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigne
 constexpr int kRunsPerPass = 2;
 constexpr int kRB = 8;          // G2 rows per staged block
 constexpr int kGsStride = 9;    // float4 per staged lookup block (8 rows + 1 pad: no bank conflicts)
-constexpr size_t kFwdSmem =
-    sizeof(float) * kWarps * (kRunsPerPass * W1 + kChunk * kGsStride * 4);  // 64 + 36 KB
+constexpr int kAH = P1 / 2;     // output rows a per warp (two warps per chunk)
+constexpr size_t kFwdWarpFloats = kRunsPerPass * R2 * kAH + 2 * kChunk * kGsStride * 4;
+constexpr size_t kFwdSmem = sizeof(float) * kWarps * kFwdWarpFloats;  // 104 KB
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N_>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_) : "memory"); }
+
+// Two warps per chunk: warp half h computes rows a in [8h, 8h + 8) of every
+// lookup's y (lane = lookup), so a lane keeps 8 x 4 accumulators.
 template <bool kExact>
 __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_fwd(const float* __restrict__ G2,
-                                                        const float* __restrict__ H,
-                                                        const int32_t* __restrict__ lk_pid,
-                                                        const uint32_t* __restrict__ tail_dig,
-                                                        const uint32_t* __restrict__ s_lk, int64_t L,
-                                                        float* __restrict__ y) {
-  // per warp: [kRunsPerPass][R2][P1] H rows (transposed) | [kChunk][kGsStride] float4 G2 block
+                                                           const float* __restrict__ H,
+                                                           const int32_t* __restrict__ lk_pid,
+                                                           const uint32_t* __restrict__ tail_dig,
+                                                           const uint32_t* __restrict__ s_lk,
+                                                           int64_t L, float* __restrict__ y) {
+  // per warp: [kRunsPerPass][R2][kAH] H rows (transposed) | 2 x [kChunk][kGsStride] float4 G2
+  // blocks (double-buffered: block rb + 1 lands by cp.async while block rb is used)
   extern __shared__ __align__(16) float w3f_dyn[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* hs_w = w3f_dyn + wid * (kRunsPerPass * W1 + kChunk * kGsStride * 4);
-  float4* gs = reinterpret_cast<float4*>(hs_w + kRunsPerPass * W1);
+  const int half = wid & 1, a0 = half * kAH;
+  float* hs_w = w3f_dyn + wid * kFwdWarpFloats;
+  float4* gs = reinterpret_cast<float4*>(hs_w + kRunsPerPass * R2 * kAH);
   const int64_t nchunks = (L + kChunk - 1) / kChunk;
-  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * kWarps + wid; ch < nchunks;
-       ch += static_cast<int64_t>(gridDim.x) * kWarps) {
+  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * (kWarps / 2) + (wid >> 1); ch < nchunks;
+       ch += static_cast<int64_t>(gridDim.x) * (kWarps / 2)) {
     const int64_t c0 = ch * kChunk;
     const int n = static_cast<int>(L - c0 < kChunk ? L - c0 : kChunk);
     int l = 0, pid = -1, i2 = 0;
@@ -116,42 +131,55 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_fwd(const float* __restri
         unsigned m = starts;
         for (int z = 0; z < r0 + k; ++z) m &= m - 1;
         const int p = __shfl_sync(0xffffffffu, pid, __ffs(m) - 1);
-        const float* hp = H + static_cast<int64_t>(p) * W1;
-        float* hs = hs_w + k * W1;
-        // column r = it % 2 * 32 + lane, a-group g = it / 2: 4 coalesced loads,
-        // one 16-byte store into the [r][a] layout
+        const float* hp = H + static_cast<int64_t>(p) * W1 + a0 * R2;
+        float* hs = hs_w + k * R2 * kAH;
+        // column r = it % 2 * 32 + lane, a-group g = it / 2 (of this warp's 8 rows):
+        // 4 coalesced loads, one 16-byte store into the [r][a] layout
 #pragma unroll
-        for (int it = 0; it < 2 * (P1 / 4); ++it) {
+        for (int it = 0; it < 2 * (kAH / 4); ++it) {
           const int r = (it & 1) * 32 + lane, g = it >> 1;
           const float4 v = make_float4(__ldg(hp + (4 * g + 0) * R2 + r), __ldg(hp + (4 * g + 1) * R2 + r),
                                        __ldg(hp + (4 * g + 2) * R2 + r), __ldg(hp + (4 * g + 3) * R2 + r));
-          *reinterpret_cast<float4*>(hs + r * P1 + 4 * g) = v;
+          *reinterpret_cast<float4*>(hs + r * kAH + 4 * g) = v;
         }
       }
       const int k = my_run - r0;
       const bool act = lane < n && k >= 0 && k < rn;
-      const float* hs = hs_w + (act ? k : 0) * W1;
-      float4 acc[P1];
+      const float* hs = hs_w + (act ? k : 0) * R2 * kAH;
+      float4 acc[kAH];
 #pragma unroll
-      for (int a = 0; a < P1; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int rb = 0; rb < R2; rb += kRB) {
-        // G2 rows [rb, rb + kRB) of every lookup of the chunk: 4 lookups x 128 B
-        // per warp load (coalesced), lane q then reads its own block
-        __syncwarp();
+      for (int a = 0; a < kAH; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      // G2 rows [rb, rb + kRB) of every lookup of the chunk: 4 lookups x 128 B per
+      // warp copy (coalesced), lane q then reads its own block
+      auto stage = [&](int rb, int buf) {
+        float4* gb = gs + buf * kChunk * kGsStride;
 #pragma unroll
         for (int it = 0; it < kChunk / 4; ++it) {
           const int qq = it * 4 + (lane >> 3), piece = lane & 7;
           const int iq = __shfl_sync(0xffffffffu, i2, qq);
-          if (qq < n) gs[qq * kGsStride + piece] = ld4(G2 + static_cast<int64_t>(iq) * S2 + (rb + piece) * N2);
+          if (qq < n) cp_async16(gb + qq * kGsStride + piece, G2 + static_cast<int64_t>(iq) * S2 + (rb + piece) * N2);
+        }
+        cp_async_commit();
+      };
+      __syncwarp();
+      stage(0, 0);
+      for (int rb = 0; rb < R2; rb += kRB) {
+        const int buf = (rb / kRB) & 1;
+        if (rb + kRB < R2) {
+          stage(rb + kRB, buf ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
         }
         __syncwarp();
+        const float4* gb = gs + buf * kChunk * kGsStride;
         if (act) {
 #pragma unroll
           for (int rr = 0; rr < kRB; ++rr) {
-            const float4 g = gs[lane * kGsStride + rr];
-            const float4* h4 = reinterpret_cast<const float4*>(hs + (rb + rr) * P1);
+            const float4 g = gb[lane * kGsStride + rr];
+            const float4* h4 = reinterpret_cast<const float4*>(hs + (rb + rr) * kAH);
 #pragma unroll
-            for (int a4 = 0; a4 < P1 / 4; ++a4) {
+            for (int a4 = 0; a4 < kAH / 4; ++a4) {
               const float4 h = h4[a4];
               const float hv[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
@@ -172,37 +200,43 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_fwd(const float* __restri
             }
           }
         }
+        __syncwarp();  // every lane is done with this buffer before it is restaged
       }
       if (act) {
-        float4* yo = reinterpret_cast<float4*>(y + static_cast<int64_t>(l) * N);
+        float4* yo = reinterpret_cast<float4*>(y + static_cast<int64_t>(l) * N) + a0;
 #pragma unroll
-        for (int a = 0; a < P1; ++a) yo[a] = acc[a];
+        for (int a = 0; a < kAH; ++a) yo[a] = acc[a];
       }
     }
   }
 }
 
 // --------------------------------------------------------------- backward --
-// D2 is staged as DUPLICATED pairs (d, d), so every f32x2 operand is a natural
-// register pair: no packing moves in the inner loop.
-constexpr int kWarpsB = 4;
-constexpr int kDdStride = N + 2;  // pairs per staged lookup (+16 B: conflict-free 16-byte stores)
-constexpr size_t kBwdSmem = sizeof(unsigned long long) * kWarpsB * kChunk * kDdStride;  // 66 KB
+// Two warps per chunk, each owning 32 of the 64 columns r (lane = one column):
+// per pair run the lane holds H[a][r] and the running S[a][r] for the 16 a in
+// registers as (a, a+1) pairs.  D2 is staged per warp as [a/2][j][a%2], so
+// (D2[a][j], D2[a+1][j]) is a natural f32x2 operand (8-byte loads); the only packed value is
+// the lane's G2 row duplicated per j, once per lookup.  Per lookup:
+//   S[a][r]  += Σ_j D2[a][j]·G2[i2][r][j]       (fma chain over j from zero)
+//   C[r][j]   = Σ_a H[a][r]·D2[a][j]            (even / odd a accumulated apart)
+constexpr int kWarpsB = 8;                              // 4 chunks x 2 column halves
+constexpr size_t kBwdSmem = sizeof(float) * kWarpsB * kChunk * N;  // 64 KB: [warp][q][j][a]
 
-__global__ void __launch_bounds__(kWarpsB * 32, 3) k_w3_bwd(
+__global__ void __launch_bounds__(kWarpsB * 32, 2) k_w3_bwd(
     const float* __restrict__ G2, const float* __restrict__ H, const int32_t* __restrict__ lk_pid,
     const uint32_t* __restrict__ tail_dig, const int32_t* __restrict__ lk_bag,
     const float* __restrict__ lk_alpha, const float* __restrict__ grad,
     const uint32_t* __restrict__ s_lk, const unsigned long long* __restrict__ scan,
     const uint32_t* __restrict__ pos2, int64_t L, float* __restrict__ partS,
     float* __restrict__ contrib) {
-  extern __shared__ __align__(16) float w3b_dyn[];  // [kWarpsB][kChunk][P1][N2] (d, d) pairs
+  extern __shared__ __align__(16) float w3b_dyn[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned long long* dd = reinterpret_cast<unsigned long long*>(w3b_dyn) + wid * kChunk * kDdStride;
-  const int r0 = 2 * lane;  // this lane's two columns r0, r0 + 1
+  float* d2s = w3b_dyn + wid * kChunk * N;  // this warp's [q][j][a]
+  const int half = wid & 1;
+  const int r = half * 32 + lane;  // this lane's column
   const int64_t nchunks = (L + kChunk - 1) / kChunk;
-  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * kWarpsB + wid; ch < nchunks;
-       ch += static_cast<int64_t>(gridDim.x) * kWarpsB) {
+  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * (kWarpsB / 2) + (wid >> 1); ch < nchunks;
+       ch += static_cast<int64_t>(gridDim.x) * (kWarpsB / 2)) {
     const int64_t c0 = ch * kChunk;
     const int n = static_cast<int>(L - c0 < kChunk ? L - c0 : kChunk);
     int pid = -1, i2 = 0, run = 0, bag = 0;
@@ -218,77 +252,80 @@ __global__ void __launch_bounds__(kWarpsB * 32, 3) k_w3_bwd(
       bag = lk_bag[l];
       al = lk_alpha[l];
     }
-    // D2 = T(alpha)·grad[bag] as (d, d) pairs: two lookups' rows (2 x 256 B)
-    // per warp load, lanes 16 B apart (coalesced and conflict-free)
+    // D2 = T(alpha)·grad[bag] as [a/2][j][a%2]: two lookups (2 x 256 B) per
+    // warp load; lane (q, a4 = lane & 15 -> a = a4 / 4 * 4.., j...) writes 4 floats
 #pragma unroll 4
     for (int it = 0; it < kChunk / 2; ++it) {
-      const int qq = it * 2 + (lane >> 4), k4 = lane & 15;
+      const int qq = it * 2 + (lane >> 4), k4 = lane & 15;  // float4 k4 of row qq = D2[a = k4][0..3]
       const int bq = __shfl_sync(0xffffffffu, bag, qq);
       const float aq = __shfl_sync(0xffffffffu, al, qq);
       if (qq < n) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bq) * N) + k4);
-        const float x = __fmul_rn(aq, v.x), yv = __fmul_rn(aq, v.y), z = __fmul_rn(aq, v.z),
-                    w = __fmul_rn(aq, v.w);
-        ulonglong2* dst = reinterpret_cast<ulonglong2*>(dd + qq * kDdStride + 4 * k4);
-        dst[0] = make_ulonglong2(pk(x, x), pk(yv, yv));
-        dst[1] = make_ulonglong2(pk(z, z), pk(w, w));
+        // [a / 2][j][a % 2]: (D2[a][j], D2[a+1][j]) adjacent, j = 0..3 in 32 bytes
+        float* dq = d2s + qq * N + (k4 >> 1) * 8 + (k4 & 1);
+        dq[0] = __fmul_rn(aq, v.x);
+        dq[2] = __fmul_rn(aq, v.y);
+        dq[4] = __fmul_rn(aq, v.z);
+        dq[6] = __fmul_rn(aq, v.w);
       }
     }
     __syncwarp();
-    unsigned long long h[P1], s[P1];
+    unsigned long long h[P1 / 2], s[P1 / 2];
     int cur = -1;
-    int i2n = __shfl_sync(0xffffffffu, i2, 0);
-    float4 ga = ld4(G2 + static_cast<int64_t>(i2n) * S2 + r0 * N2);
-    float4 gb = ld4(G2 + static_cast<int64_t>(i2n) * S2 + (r0 + 1) * N2);
+    // the lane's G2 row of lookups q + 1 and q + 2 in flight
+    float4 gn = ld4(G2 + static_cast<int64_t>(__shfl_sync(0xffffffffu, i2, 0)) * S2 + r * N2);
+    float4 gnn = ld4(G2 + static_cast<int64_t>(__shfl_sync(0xffffffffu, i2, 1)) * S2 + r * N2);
     for (int q = 0; q < n; ++q) {
       const int p = __shfl_sync(0xffffffffu, pid, q);
       const int rq = __shfl_sync(0xffffffffu, run, q);
       const uint32_t pq = __shfl_sync(0xffffffffu, p2, q);
-      // G2 column pairs (G2[r0][j], G2[r0+1][j]) of this lookup
-      const unsigned long long gp0 = pk(ga.x, gb.x), gp1 = pk(ga.y, gb.y), gp2 = pk(ga.z, gb.z),
-                               gp3 = pk(ga.w, gb.w);
-      if (q + 1 < n) {
-        i2n = __shfl_sync(0xffffffffu, i2, q + 1);
-        ga = ld4(G2 + static_cast<int64_t>(i2n) * S2 + r0 * N2);
-        gb = ld4(G2 + static_cast<int64_t>(i2n) * S2 + (r0 + 1) * N2);
+      const float4 g = gn;
+      gn = gnn;
+      {
+        const int i2q = __shfl_sync(0xffffffffu, i2, (q + 2) & 31);
+        if (q + 2 < n) gnn = ld4(G2 + static_cast<int64_t>(i2q) * S2 + r * N2);
       }
-      if (p != cur) {  // a new pair run: its H column pairs into registers, S from zero
-        const float* hp = H + static_cast<int64_t>(p) * W1 + r0;
+      const unsigned long long g0 = pk(g.x, g.x), g1 = pk(g.y, g.y), g2 = pk(g.z, g.z), g3 = pk(g.w, g.w);
+      if (p != cur) {  // a new pair run: H[a][r] pairs into registers, S from zero
+        const float* hp = H + static_cast<int64_t>(p) * W1 + r;
 #pragma unroll
-        for (int a = 0; a < P1; ++a) {
-          h[a] = __ldg(reinterpret_cast<const unsigned long long*>(hp + a * R2));
-          s[a] = 0ull;
+        for (int a2 = 0; a2 < P1 / 2; ++a2) {
+          h[a2] = pk(__ldg(hp + (2 * a2) * R2), __ldg(hp + (2 * a2 + 1) * R2));
+          s[a2] = 0ull;
         }
         cur = p;
       }
       unsigned long long c0v = 0ull, c1v = 0ull, c2v = 0ull, c3v = 0ull;
-      const ulonglong2* d2 = reinterpret_cast<const ulonglong2*>(dd + q * kDdStride);
+      const float* dq = d2s + q * N;
 #pragma unroll
-      for (int a = 0; a < P1; ++a) {
-        const ulonglong2 d01 = d2[2 * a], d23 = d2[2 * a + 1];  // (D2[a][j], D2[a][j]) pairs
-        // S: v = Σ_j D2[a][j]·G2[r][j] (fma chain from zero), S += v
-        unsigned long long v = fma2(d01.x, gp0, 0ull);
-        v = fma2(d01.y, gp1, v);
-        v = fma2(d23.x, gp2, v);
-        v = fma2(d23.y, gp3, v);
-        s[a] = add2(s[a], v);
-        // C[r][j] += H[a][r]·D2[a][j] (a ascending from zero)
-        c0v = fma2(h[a], d01.x, c0v);
-        c1v = fma2(h[a], d01.y, c1v);
-        c2v = fma2(h[a], d23.x, c2v);
-        c3v = fma2(h[a], d23.y, c3v);
+      for (int a2 = 0; a2 < P1 / 2; ++a2) {
+        // (D2[a][j], D2[a+1][j]) for j = 0..3, a = 2 a2 (broadcast reads)
+        const unsigned long long* dp = reinterpret_cast<const unsigned long long*>(dq + a2 * 8);
+        const unsigned long long d0 = dp[0], d1 = dp[1], d2 = dp[2], d3 = dp[3];
+        unsigned long long v = fma2(d0, g0, 0ull);
+        v = fma2(d1, g1, v);
+        v = fma2(d2, g2, v);
+        v = fma2(d3, g3, v);
+        s[a2] = add2(s[a2], v);
+        c0v = fma2(h[a2], d0, c0v);
+        c1v = fma2(h[a2], d1, c1v);
+        c2v = fma2(h[a2], d2, c2v);
+        c3v = fma2(h[a2], d3, c3v);
       }
-      // C rows r0, r0 + 1 (4 columns each) at the lookup's i2-sorted position
+      // C[r][j] = even-a sum + odd-a sum, at the lookup's i2-sorted position
       const float2 e0 = upk(c0v), e1 = upk(c1v), e2 = upk(c2v), e3 = upk(c3v);
-      float4* co = reinterpret_cast<float4*>(contrib + static_cast<int64_t>(pq) * S2 + r0 * N2);
-      co[0] = make_float4(e0.x, e1.x, e2.x, e3.x);
-      co[1] = make_float4(e0.y, e1.y, e2.y, e3.y);
+      *reinterpret_cast<float4*>(contrib + static_cast<int64_t>(pq) * S2 + r * N2) =
+          make_float4(e0.x + e0.y, e1.x + e1.y, e2.x + e2.y, e3.x + e3.y);
       // the run ends here: its S partial row (a-major, [a][r])
       const int pn = q + 1 < n ? __shfl_sync(0xffffffffu, pid, q + 1) : -2;
       if (pn != p) {
-        float* so = partS + static_cast<int64_t>(rq) * W1 + r0;
+        float* so = partS + static_cast<int64_t>(rq) * W1 + r;
 #pragma unroll
-        for (int a = 0; a < P1; ++a) *reinterpret_cast<unsigned long long*>(so + a * R2) = s[a];
+        for (int a2 = 0; a2 < P1 / 2; ++a2) {
+          const float2 sv = upk(s[a2]);
+          so[(2 * a2) * R2] = sv.x;
+          so[(2 * a2 + 1) * R2] = sv.y;
+        }
       }
     }
   }

@@ -1,5 +1,6 @@
 """GPU: compute-sanitizer racecheck + memcheck + synccheck over one fast-path and one
-generic-path fwd+bwd+SGD step (the reference's determinism tests act as race
+generic-path fwd+bwd+SGD step, the wide3 tail kernels, the cache fast path and the
+peer reduce (the reference's determinism tests act as race
 canaries; on the GPU we check for races directly)."""
 import os
 import shutil
@@ -39,6 +40,34 @@ g = rng.standard_normal((4096, 64)).astype(np.float32)
 r = tt.forward_bags(t, b, save_intermediates=True)
 gr = tt.backward_bags(t, b, r.context, g)
 t.backward_sgd(r.context, b, g, 0.01)
+# wide3 warp-per-chunk tail kernels (cfg3's shape class: n = 4x4x4, R = 64)
+p = tt.ShapePlan(30000, 64, 3, [20, 30, 50], [4, 4, 4], [1, 64, 64, 1])
+t = tt.TtTable(p, "w3")
+t.set_cores([(rng.standard_normal(p.core_size(k)) * 0.1).astype(np.float32) for k in range(3)])
+sizes = rng.integers(0, 40, 200)
+off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+b = tt.IndexBatch(rng.integers(0, p.num_rows, int(off[-1])).astype(np.int64), off)
+g = rng.standard_normal((200, 64)).astype(np.float32)
+r = tt.forward_bags(t, b)
+gr = tt.backward_bags(t, b, r.context, g)
+t.backward_sgd(r.context, b, g, 0.01)
+# LFU cache on the fast path (probe inside f3_gsort, pool_if_last with cached
+# rows, slot gradients on the side stream): warm-up, finalize, active steps
+from paper_2101_11714_b200.lfu_cache import EmbeddingLayer, LfuCache
+p = tt.ShapePlan(40000, 16, 3, [30, 34, 40], [2, 2, 4], [1, 16, 16, 1])
+t = tt.TtTable(p, "cache")
+t.init_sampled_gaussian(3)
+lay = EmbeddingLayer(t, LfuCache(48, 16, key_space=40000))
+zs = tt.generate_zipfian_batch(40000, 1.2, 11, 30000, 1).indices
+for s_ in range(4):
+    sizes = rng.integers(0, 6, 2000)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    b = tt.IndexBatch(zs[s_ * 7000: s_ * 7000 + int(off[-1])].copy(), off, None, tt.Pooling(s_ % 2))
+    lay.forward(b)
+    lay.backward(b, rng.standard_normal((2000, 16)).astype(np.float32))
+    lay.step(0.01)
+    if s_ == 1:
+        lay.finalize_warmup()
 # fused peer reduce + SGD: two ranks' tables on two streams of this GPU (the sanitizer
 # serialises kernels, so the peer waits run into their bounded timeout here: this
 # exercises the timeout path's memory safety, the reduction itself is checked in
