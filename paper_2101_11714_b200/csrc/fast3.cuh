@@ -800,25 +800,24 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
 // S rows land at the slot's position (start + s), kappa-major: row s holds
 // S[a0][c] at a0*C1 + c == a*R2 + r, so f3_bwd1 can bulk-copy a tile's rows.
 template <class D>
-__global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cores, int64_t coff2,
-                                                const Tile* __restrict__ tiles,
-                                                const int* __restrict__ ntiles, int max_tiles,
-                                                const uint32_t* __restrict__ perm,
-                                                const uint16_t* __restrict__ d2,
-                                                const int32_t* __restrict__ lk_bag,
-                                                const float* __restrict__ alpha,
-                                                const float* __restrict__ grad,
-                                                const uint16_t* __restrict__ slot_of_pos,
-                                                const int* __restrict__ tile_nslots,
-                                                float* __restrict__ Sbuf) {
-  pdl_entry();
+__device__ __forceinline__ void srows_body(int vblock, const float* __restrict__ cores, int64_t coff2,
+                                           const Tile* __restrict__ tiles,
+                                           const int* __restrict__ ntiles, int max_tiles,
+                                           const uint32_t* __restrict__ perm,
+                                           const uint16_t* __restrict__ d2,
+                                           const int32_t* __restrict__ lk_bag,
+                                           const float* __restrict__ alpha,
+                                           const float* __restrict__ grad,
+                                           const uint16_t* __restrict__ slot_of_pos,
+                                           const int* __restrict__ tile_nslots,
+                                           float* __restrict__ Sbuf) {
   constexpr int EPL = (D::W1 + 31) / 32;  // row elements per lane
   // distinct G2 rows a lane reads per member: r = (lane + 32k) % R2 repeats with period NR
   constexpr int NR = D::R2 > 32 ? D::R2 / 32 : 1;
   static_assert(D::R2 <= 32 ? 32 % D::R2 == 0 : D::R2 % 32 == 0, "lane -> rank column map");
   constexpr int U = 8;  // members with G2 loads in flight
   const int lane = threadIdx.x & 31;
-  const int t = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
+  const int t = static_cast<int>((vblock * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
   if (t >= max_tiles) return;
   // the tile count and this tile's descriptor in one round trip (entries past
   // the count are in bounds, just unused)
@@ -1260,13 +1259,12 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
 // tiles of the same i2 in a CTA's range accumulate; one partial per run
 // (has2 marks its first tile).
 template <class D>
-__global__ void __launch_bounds__(128) f3_bwd2(
-    Geo g, const Tile* __restrict__ tiles, const int* __restrict__ ntiles,
+__device__ __forceinline__ void bwd2_body(
+    int vblock, int vgrid, Geo g, const Tile* __restrict__ tiles, const int* __restrict__ ntiles,
     const uint32_t* __restrict__ perm, const uint32_t* __restrict__ hloc,
     const int32_t* __restrict__ lk_bag, const float* __restrict__ alpha,
     const float* __restrict__ grad, const float* __restrict__ Hbuf, float* __restrict__ part2,
     int* __restrict__ has2) {
-  pdl_entry();
   constexpr int NW = 4, U = 4;
   constexpr int CH = (D::R2 + 31) / 32;
   __shared__ float4 red[NW][CH * 32];
@@ -1274,8 +1272,8 @@ __global__ void __launch_bounds__(128) f3_bwd2(
   __shared__ float al[D::TT2];
   const int nt = *ntiles;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const int t_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nt / gridDim.x);
-  const int t_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nt / gridDim.x);
+  const int t_lo = static_cast<int>(static_cast<int64_t>(vblock) * nt / vgrid);
+  const int t_hi = static_cast<int>(static_cast<int64_t>(vblock + 1) * nt / vgrid);
   float4 acc[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1388,6 +1386,87 @@ __device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, boo
     for (int u = 0; u < 8; ++u)
       if (idx[u] >= 0) add4(acc, v[u]);
   }
+}
+
+// ---- kernel wrappers of the two independent backward stages, and their
+// horizontal fusion: f3_srows (per i1-tile) and f3_bwd2 (per i2-tile) read
+// only the forward's outputs and grad_out, so one launch runs both -- the first
+// nb2 CTAs as f3_bwd2, the rest as f3_srows warps -- and their tails overlap.
+template <class D>
+__global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cores, int64_t coff2,
+                                                const Tile* __restrict__ tiles,
+                                                const int* __restrict__ ntiles, int max_tiles,
+                                                const uint32_t* __restrict__ perm,
+                                                const uint16_t* __restrict__ d2,
+                                                const int32_t* __restrict__ lk_bag,
+                                                const float* __restrict__ alpha,
+                                                const float* __restrict__ grad,
+                                                const uint16_t* __restrict__ slot_of_pos,
+                                                const int* __restrict__ tile_nslots,
+                                                float* __restrict__ Sbuf) {
+  pdl_entry();
+  srows_body<D>(blockIdx.x, cores, coff2, tiles, ntiles, max_tiles, perm, d2, lk_bag, alpha, grad,
+                slot_of_pos, tile_nslots, Sbuf);
+}
+
+template <class D>
+__global__ void __launch_bounds__(128) f3_bwd2(
+    Geo g, const Tile* __restrict__ tiles, const int* __restrict__ ntiles,
+    const uint32_t* __restrict__ perm, const uint32_t* __restrict__ hloc,
+    const int32_t* __restrict__ lk_bag, const float* __restrict__ alpha,
+    const float* __restrict__ grad, const float* __restrict__ Hbuf, float* __restrict__ part2,
+    int* __restrict__ has2) {
+  pdl_entry();
+  bwd2_body<D>(blockIdx.x, gridDim.x, g, tiles, ntiles, perm, hloc, lk_bag, alpha, grad, Hbuf, part2,
+               has2);
+}
+
+struct SrowsArgs {
+  const float* cores;
+  int64_t coff2;
+  const Tile* tiles;
+  const int* ntiles;
+  int max_tiles;
+  const uint32_t* perm;
+  const uint16_t* d2;
+  const uint16_t* slot_of_pos;
+  const int* tile_nslots;
+  float* Sbuf;
+};
+struct Bwd2Args {
+  const Tile* tiles;
+  const int* ntiles;
+  const uint32_t* perm;
+  const uint32_t* hloc;
+  const float* Hbuf;
+  float* part2;
+  int* has2;
+};
+
+// CTA roles interleave (even: f3_bwd2 CTA, odd: 4 f3_srows warps) while both
+// have work left, so both stages spread over every SM from the first wave.
+template <class D>
+__global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Args ba, int nb2, int nbs,
+                                                    const int32_t* __restrict__ lk_bag,
+                                                    const float* __restrict__ alpha,
+                                                    const float* __restrict__ grad) {
+  pdl_entry();
+  const int b = static_cast<int>(blockIdx.x), m = min(nb2, nbs);
+  bool is_b2;
+  int idx;
+  if (b < 2 * m) {
+    is_b2 = (b & 1) == 0;
+    idx = b >> 1;
+  } else {
+    is_b2 = nb2 > nbs;
+    idx = m + (b - 2 * m);
+  }
+  if (is_b2)
+    bwd2_body<D>(idx, nb2, g, ba.tiles, ba.ntiles, ba.perm, ba.hloc, lk_bag, alpha, grad, ba.Hbuf,
+                 ba.part2, ba.has2);
+  else
+    srows_body<D>(idx, sa.cores, sa.coff2, sa.tiles, sa.ntiles, sa.max_tiles, sa.perm, sa.d2, lk_bag,
+                  alpha, grad, sa.slot_of_pos, sa.tile_nslots, sa.Sbuf);
 }
 
 __device__ __forceinline__ void store_slice(float4 s, bool touched, float* out_core, float* out_grad,

@@ -353,11 +353,24 @@ struct F3Runner {
                 f.has1.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>());
       t->mark("f3c_bwd");
     } else {
+    if (t->fuse_sb) {
+      // f3_srows and f3_bwd2 in one launch (they are independent)
+      f3::SrowsArgs sa{t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
+                       f.max_tiles1, f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(),
+                       f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>()};
+      f3::Bwd2Args ba{f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, f.perm2.as<uint32_t>(),
+                      f.hloc.as<uint32_t>(), f.Hbuf.as<float>(), f.part2.as<float>(), f.has2.as<int>()};
+      const int nbs = (f.max_tiles1 * 32 + 127) / 128;
+      f3_launch(t->pdl, f3::f3_srows_bwd2<D>, dim3(grid2 + nbs), dim3(128), 0, st, g, sa, ba, grid2, nbs,
+                lk_bag, alpha, grad);
+      t->mark("f3_srows_bwd2");
+    } else {
     f3_launch(t->pdl, f3::f3_srows<D>, dim3((f.max_tiles1 * 32 + 255) / 256), dim3(256), 0, st, 
         t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.max_tiles1,
         f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
         f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>());
     t->mark("f3_srows");
+    }
     f3_launch(t->pdl, k1, dim3(grid1), dim3(f3::kThreads), sm1, st, g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
                                          f.ntiles.as<int>(), f.Sbuf.as<float>(),
                                          f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(),
@@ -365,11 +378,13 @@ struct F3Runner {
                                          f.d0mask.as<unsigned char>());
     t->mark("f3_bwd1");
     }
+    if (!t->fuse_sb || f.chunked) {
     f3_launch(t->pdl, f3::f3_bwd2<D>, dim3(grid2), dim3(128), 0, st, g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
                                           f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag,
                                           alpha, grad, f.Hbuf.as<float>(), f.part2.as<float>(),
                                           f.has2.as<int>());
     t->mark("f3_bwd2");
+    }
     {
       constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
       f3::CombineArgs A{};

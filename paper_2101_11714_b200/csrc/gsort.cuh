@@ -224,7 +224,12 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       }
     }
   }
-  // bags (grid-stride over the whole grid)
+  // bags (grid-stride over the whole grid).  Cache mode: a single-lookup bag
+  // whose lookup this very thread decoded (every bag when bags are singles and
+  // the batch is laid out one lookup per thread) knows its slot already and is
+  // pooled here; any other bag sets need_c and is handled after the grid
+  // barriers, when every lookup's slot is visible
+  bool need_c = false;
   for (int64_t b = b_first; b < a.B; b += static_cast<int64_t>(G) * kGsThreads) {
     const int64_t s = b == b_first ? s_first : a.off[b], e = b == b_first ? e_first : a.off[b + 1];
     if (b == 0 && s != 0) atomicOr(a.errs, 1);
@@ -238,9 +243,29 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
     if (e - s == 1 && hi - lo == 1) {  // the common single-lookup bag
       a.lk_bag[lo] = static_cast<int32_t>(b);
       a.solo[lo] = static_cast<int32_t>(b);
-      a.alpha[lo] = a.w ? static_cast<float>(a.w[lo]) : 1.f;
+      const float wl = a.w ? static_cast<float>(a.w[lo]) : 1.f;
+      a.alpha[lo] = wl;
+      if (K3) {
+        if (lo == wbase + lane && k1[0] != 0xffffffffu) {
+          if (k1[0] >= 0x80000000u) {  // cached: out = (0 + w·row) + 0
+            const float4* src =
+                reinterpret_cast<const float4*>(a.store + static_cast<int64_t>(k1[0] & 0x7fffffffu) * a.N);
+            float4* dst = reinterpret_cast<float4*>(a.out + b * a.N);
+            for (int j = 0; j < a.N / 4; ++j) {
+              const float4 v = src[j];
+              dst[j] = make_float4(__fadd_rn(__fadd_rn(0.f, __fmul_rn(wl, v.x)), 0.f),
+                                   __fadd_rn(__fadd_rn(0.f, __fmul_rn(wl, v.y)), 0.f),
+                                   __fadd_rn(__fadd_rn(0.f, __fmul_rn(wl, v.z)), 0.f),
+                                   __fadd_rn(__fadd_rn(0.f, __fmul_rn(wl, v.w)), 0.f));
+            }
+          }
+        } else {
+          need_c = true;
+        }
+      }
       continue;
     }
+    if (K3) need_c = true;
     const double sz = static_cast<double>(e - s);
     for (int64_t l = lo; l < hi; ++l) {
       a.lk_bag[l] = static_cast<int32_t>(b);
@@ -533,11 +558,12 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   // model.hpp:210-223 with an empty chain part); a bag with chain lookups
   // presets its pooling counter with its cached lookups, so its last chain
   // lookup pools it in f3_fwd (pool_if_last)
-  if (a.K3) {
+  if (a.K3 && need_c) {
     for (int64_t b = static_cast<int64_t>(c) * kGsThreads + tid; b < a.B;
          b += static_cast<int64_t>(G) * kGsThreads) {
       const int64_t s = a.off[b], e = a.off[b + 1];
       if (e - s < 1 || s < 0 || e > a.L) continue;
+      if (e - s == 1 && s == wbase + lane) continue;  // pooled in phase A
       int nc = 0;
       for (int64_t l = s; l < e; ++l) nc += __ldcg(a.lk_slot + l) >= 0 ? 1 : 0;
       if (nc < e - s) {

@@ -214,15 +214,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_fwd(const float* __restri
 // --------------------------------------------------------------- backward --
 // Two warps per chunk, each owning 32 of the 64 columns r (lane = one column):
 // per pair run the lane holds H[a][r] and the running S[a][r] for the 16 a in
-// registers as (a, a+1) pairs.  D2 is staged per warp as [a/2][j][a%2], so
-// (D2[a][j], D2[a+1][j]) is a natural f32x2 operand (8-byte loads); the only packed value is
+// registers as (a, a+1) pairs.  D2 is staged per warp as [j][a], so
+// (D2[a][j], D2[a+1][j]) is a natural f32x2 operand; the only packed value is
 // the lane's G2 row duplicated per j, once per lookup.  Per lookup:
 //   S[a][r]  += Σ_j D2[a][j]·G2[i2][r][j]       (fma chain over j from zero)
 //   C[r][j]   = Σ_a H[a][r]·D2[a][j]            (even / odd a accumulated apart)
 constexpr int kWarpsB = 8;                              // 4 chunks x 2 column halves
 constexpr size_t kBwdSmem = sizeof(float) * kWarpsB * kChunk * N;  // 64 KB: [warp][q][j][a]
 
-__global__ void __launch_bounds__(kWarpsB * 32, 2) k_w3_bwd(
+__global__ void __launch_bounds__(kWarpsB * 32, 3) k_w3_bwd(
     const float* __restrict__ G2, const float* __restrict__ H, const int32_t* __restrict__ lk_pid,
     const uint32_t* __restrict__ tail_dig, const int32_t* __restrict__ lk_bag,
     const float* __restrict__ lk_alpha, const float* __restrict__ grad,
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kWarpsB * 32, 2) k_w3_bwd(
       bag = lk_bag[l];
       al = lk_alpha[l];
     }
-    // D2 = T(alpha)·grad[bag] as [a/2][j][a%2]: two lookups (2 x 256 B) per
+    // D2 = T(alpha)·grad[bag] transposed to [j][a]: two lookups (2 x 256 B) per
     // warp load; lane (q, a4 = lane & 15 -> a = a4 / 4 * 4.., j...) writes 4 floats
 #pragma unroll 4
     for (int it = 0; it < kChunk / 2; ++it) {
@@ -261,12 +261,11 @@ __global__ void __launch_bounds__(kWarpsB * 32, 2) k_w3_bwd(
       const float aq = __shfl_sync(0xffffffffu, al, qq);
       if (qq < n) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bq) * N) + k4);
-        // [a / 2][j][a % 2]: (D2[a][j], D2[a+1][j]) adjacent, j = 0..3 in 32 bytes
-        float* dq = d2s + qq * N + (k4 >> 1) * 8 + (k4 & 1);
-        dq[0] = __fmul_rn(aq, v.x);
-        dq[2] = __fmul_rn(aq, v.y);
-        dq[4] = __fmul_rn(aq, v.z);
-        dq[6] = __fmul_rn(aq, v.w);
+        float* dq = d2s + qq * N + k4;  // [j][a]: j * 16 + a
+        dq[0 * P1] = __fmul_rn(aq, v.x);
+        dq[1 * P1] = __fmul_rn(aq, v.y);
+        dq[2 * P1] = __fmul_rn(aq, v.z);
+        dq[3 * P1] = __fmul_rn(aq, v.w);
       }
     }
     __syncwarp();
@@ -300,8 +299,10 @@ __global__ void __launch_bounds__(kWarpsB * 32, 2) k_w3_bwd(
 #pragma unroll
       for (int a2 = 0; a2 < P1 / 2; ++a2) {
         // (D2[a][j], D2[a+1][j]) for j = 0..3, a = 2 a2 (broadcast reads)
-        const unsigned long long* dp = reinterpret_cast<const unsigned long long*>(dq + a2 * 8);
-        const unsigned long long d0 = dp[0], d1 = dp[1], d2 = dp[2], d3 = dp[3];
+        const unsigned long long d0 = *reinterpret_cast<const unsigned long long*>(dq + 0 * P1 + 2 * a2);
+        const unsigned long long d1 = *reinterpret_cast<const unsigned long long*>(dq + 1 * P1 + 2 * a2);
+        const unsigned long long d2 = *reinterpret_cast<const unsigned long long*>(dq + 2 * P1 + 2 * a2);
+        const unsigned long long d3 = *reinterpret_cast<const unsigned long long*>(dq + 3 * P1 + 2 * a2);
         unsigned long long v = fma2(d0, g0, 0ull);
         v = fma2(d1, g1, v);
         v = fma2(d2, g2, v);

@@ -62,7 +62,7 @@ zs = tt.generate_zipfian_batch(40000, 1.2, 11, 30000, 1).indices
 for s_ in range(4):
     sizes = rng.integers(0, 6, 2000)
     off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    b = tt.IndexBatch(zs[s_ * 7000: s_ * 7000 + int(off[-1])].copy(), off, None, tt.Pooling(s_ % 2))
+    b = tt.IndexBatch(zs[s_ * 7000: s_ * 7000 + int(off[-1])].copy(), off, None, tt.Pooling(s_ & 1))
     lay.forward(b)
     lay.backward(b, rng.standard_normal((2000, 16)).astype(np.float32))
     lay.step(0.01)
