@@ -63,6 +63,12 @@ CONFIGS["cfg5"] = dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], 
                            "largest TT-compressed at R=32 (paper Table 2) + 19 uncompressed, "
                            "65,536 bags x 1 per feature, Zipf(1.05) (device sampler), "
                            "fwd+bwd+SGD in one multi-stream CUDA graph per step")
+CONFIGS["cfg5m"] = dict(rows=10131227, emb=16, rf=[200, 220, 250], cf=[2, 2, 4], rank=32,
+                       bags=65536, pf=1, zipf=1.05, model=True,
+                       desc="DLRM cfg5 full training step (DlrmModel, model.hpp:355-538): 13 dense "
+                            "features, bottom MLP 512-256-64-16, 26 Criteo-Kaggle sparse features "
+                            "(7 TT at R=32 + 19 uncompressed), Dot interaction, top MLP 512-256-1, "
+                            "BCE, SGD; 65,536 samples per step")
 LR = 0.01
 
 
@@ -396,6 +402,92 @@ def run_collection(args, cfg, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
+def run_model(args, cfg, rank, world, local):
+    """cfg5m: the whole DLRM training step on one GPU (paper_2101_11714_b200/dlrm.py):
+    forward + BCE + backward + SGD of both MLPs and all 26 embedding tables."""
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2101_11714_b200 as tt
+    from paper_2101_11714_b200.dense import KAGGLE_CARDINALITIES
+    from paper_2101_11714_b200.dlrm import DlrmModel
+
+    tables = [(n, n >= 142572, cfg["rank"]) for n in KAGGLE_CARDINALITIES]
+    m = DlrmModel(13, cfg["emb"], tables, [512, 256, 64, 16], [512, 256, 1], dot=True, device=local)
+    m.init(1)
+    B = cfg["bags"]
+    rng = np.random.default_rng(7)
+    host = {"dense": rng.standard_normal((B, 13)).astype(np.float32),
+            "labels": rng.integers(0, 2, B).astype(np.float64),
+            "idx": [tt.generate_zipfian_batch(n, cfg["zipf"], 100 + t, B, 1).indices
+                    for t, (n, _, _) in enumerate(tables)],
+            "off": [np.arange(B + 1, dtype=np.int64) for _ in tables]}
+    mb = m.to_device(host)
+    pinned = {"dense": torch.from_numpy(host["dense"]).pin_memory(),
+              "labels": torch.from_numpy(host["labels"]).pin_memory(),
+              "idx": [torch.from_numpy(i).pin_memory() for i in host["idx"]],
+              "off": [torch.from_numpy(o).pin_memory() for o in host["off"]]}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        m.train_step(mb, LR)
+    for t in m.tables:
+        t.check()
+    st = m.stream
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(st):
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)
+            starts[i].record(st)
+            m.train_step(mb, LR)
+            ends[i].record(st)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in zip(starts, ends)]))
+    # e2e: host minibatch copied in (pinned), loss read back, every step
+    h2d = host["dense"].nbytes + host["labels"].nbytes + sum(i.nbytes for i in host["idx"]) + \
+        sum(o.nbytes for o in host["off"])
+    e2e = []
+    for i in range(args.steps):
+        flush.fill_(3)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(st):
+            mb["dense"].copy_(pinned["dense"], non_blocking=True)
+            mb["labels"].copy_(pinned["labels"], non_blocking=True)
+            for d, h in zip(mb["idx"], pinned["idx"]):
+                d.copy_(h, non_blocking=True)
+            for d, h in zip(mb["off"], pinned["off"]):
+                d.copy_(h, non_blocking=True)
+        _, loss = m.train_step(mb, LR)
+        float(loss.item())
+        e2e.append(time.perf_counter() - t0)
+    lookups = len(tables) * B
+    if rank == 0:
+        e2e_med = float(np.median(e2e))
+        line = {"metric": METRIC + " [cfg5m: full DLRM training step]", "value": lookups / (ms / 1e3),
+                "unit": "indices/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "samples_per_s": B / (ms / 1e3),
+                "data": "synthetic: host Zipf(1.05) streams per table (reference generator), N(0,1) "
+                        "dense features, random labels, model init (reference distributions)",
+                "config": {"workload": cfg["desc"], "tables": len(tables), "tt_tables": 7,
+                           "dense_tables": len(tables) - 7, "lookups_per_step": lookups,
+                           "parallelism": "single-gpu",
+                           "l2": "flushed (256 MiB write) before every timed step"},
+                "e2e": {"value": lookups / e2e_med, "unit": "indices/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": 8, "statistic": "median step time",
+                        "path": "DlrmModel.train_step with the minibatch copied from pinned host memory "
+                                "and the loss read back"},
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -439,6 +531,9 @@ def main():
         return
     if cfg.get("collection"):
         run_collection(args, cfg, rank, world, local)
+        return
+    if cfg.get("model"):
+        run_model(args, cfg, rank, world, local)
         return
 
     import torch

@@ -167,6 +167,7 @@ class RefImpl:
         L.ref_stats_rows.restype = C.c_uint64
         L.ref_layer_freq.restype = C.c_uint64
         L.ref_layer_cache_rows.restype = C.c_int64
+        L.ref_model_param.restype = C.c_int64
 
     def check(self, st):
         if st:
@@ -534,3 +535,87 @@ class RefLayer:
 
     def freq(self, row):
         return int(self.ref.lib.ref_layer_freq(self.h, C.c_int64(row)))
+
+
+class RefModel:
+    """DlrmModel<float> (model.hpp:355-538) from the reference build: the
+    checker of the GPU DlrmModel (paper_2101_11714_b200/dlrm.py)."""
+
+    def __init__(self, ref: RefImpl, dense_features, emb_dim, tables, bottom, top, dot=True):
+        """tables: list of (rows, use_tt, rank)."""
+        self.ref = ref
+        self.ntables = len(tables)
+        rows = np.asarray([t[0] for t in tables], np.int64)
+        use_tt = np.asarray([1 if t[1] else 0 for t in tables], np.int32)
+        ranks = np.asarray([t[2] for t in tables], np.int64)
+        bot = np.asarray(bottom, np.int64)
+        tp = np.asarray(top, np.int64)
+        h = C.c_void_p()
+        ref.check(ref.lib.ref_model_create(
+            C.c_int64(dense_features), C.c_int64(emb_dim), C.c_int(len(tables)), _p(rows), _p(use_tt),
+            _p(ranks), C.c_int(len(bot)), _p(bot), C.c_int(len(tp)), _p(tp), C.c_int(1 if dot else 0),
+            C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.ref.lib.ref_model_destroy(self.h)
+        except Exception:
+            pass
+
+    def init(self, seed):
+        self.ref.check(self.ref.lib.ref_model_init(self.h, C.c_uint64(seed)))
+
+    def param(self, which, index, k=0):
+        """which: 0 bottom.w, 1 bottom.b, 2 top.w, 3 top.b, 4 TT core k of table, 5 dense table."""
+        n = self.ref.lib.ref_model_param(self.h, C.c_int(which), C.c_int(index), C.c_int(k), None)
+        if n < 0:
+            raise RefError(1, self.ref.lib.ref_last_error().decode())
+        out = np.zeros(n, np.float32)
+        self.ref.lib.ref_model_param(self.h, C.c_int(which), C.c_int(index), C.c_int(k), _p(out))
+        return out
+
+    def step(self, mb, lr):
+        """One train() iteration on a minibatch dict (dense, labels, idx, off); returns (logits, loss)."""
+        bs = len(mb["labels"])
+        idx = np.concatenate(mb["idx"]).astype(np.int64)
+        lk = np.concatenate([[0], np.cumsum([len(i) for i in mb["idx"]])]).astype(np.int64)
+        off = np.concatenate(mb["off"]).astype(np.int64)
+        logits = np.zeros(bs, np.float32)
+        loss = C.c_double()
+        self.ref.check(self.ref.lib.ref_model_step(
+            self.h, C.c_int64(bs), _p(np.ascontiguousarray(mb["dense"], np.float64)),
+            _p(np.ascontiguousarray(mb["labels"], np.float64)), C.c_int(len(mb["idx"])), _p(idx), _p(lk),
+            _p(off), C.c_double(lr), _p(logits), C.byref(loss)))
+        return logits, loss.value
+
+
+class RefSource:
+    """SyntheticDataSource (data.hpp:54-90) of the reference: minibatches."""
+
+    def __init__(self, ref: RefImpl, dense_features, rows, zipf, bs, pf, seed):
+        self.ref, self.df, self.rows, self.bs, self.pf = ref, dense_features, list(rows), bs, pf
+        h = C.c_void_p()
+        r = np.asarray(rows, np.int64)
+        ref.check(ref.lib.ref_source_create(C.c_int64(dense_features), C.c_int(len(rows)), _p(r),
+                                            C.c_double(zipf), C.c_int64(bs), C.c_int64(pf),
+                                            C.c_uint64(seed), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.ref.lib.ref_source_destroy(self.h)
+        except Exception:
+            pass
+
+    def next(self, it):
+        T, bs, pf = len(self.rows), self.bs, self.pf
+        dense = np.zeros(bs * self.df, np.float64)
+        labels = np.zeros(bs, np.float64)
+        idx = np.zeros(T * bs * pf, np.int64)
+        off = np.zeros(T * (bs + 1), np.int64)
+        self.ref.check(self.ref.lib.ref_source_next(self.h, C.c_int64(it), _p(dense), _p(labels), _p(idx),
+                                                    _p(off)))
+        return {"dense": dense.reshape(bs, self.df), "labels": labels,
+                "idx": [idx[t * bs * pf:(t + 1) * bs * pf] for t in range(T)],
+                "off": [off[t * (bs + 1):(t + 1) * (bs + 1)] for t in range(T)]}

@@ -671,4 +671,127 @@ int ref_checkpoint_load_array(const char* path, const char* name, float* out, in
 
 #endif  // TTREF_CHECKPOINT
 
+
+// ---- DlrmModel<float> + SyntheticDataSource (model.hpp:355-538, data.cpp:49-130) ----
+// The reference model, used by tests/test_dlrm_gpu.py as the checker of the GPU
+// DlrmModel (paper_2101_11714_b200/dlrm.py): the same minibatches, the
+// reference's parameters copied over, then train steps on both.
+struct RefModel {
+  std::unique_ptr<DlrmModel<float>> m;
+};
+
+int ref_model_create(int64_t dense_features, int64_t emb_dim, int ntables, const int64_t* rows,
+                     const int* use_tt, const int64_t* ranks, int nbottom, const int64_t* bottom,
+                     int ntop, const int64_t* top, int interaction_dot, void** out) {
+  return guarded([&] {
+    ModelConfig cfg;
+    cfg.dense_features = dense_features;
+    cfg.emb_dim = emb_dim;
+    for (int t = 0; t < ntables; ++t) {
+      TableConfig tc;
+      tc.num_rows = rows[t];
+      tc.use_tt = use_tt[t] != 0;
+      tc.tt_dim = 3;
+      tc.rank = ranks[t];
+      cfg.tables.push_back(tc);
+    }
+    cfg.bottom_layers.assign(bottom, bottom + nbottom);
+    cfg.top_layers.assign(top, top + ntop);
+    cfg.interaction = interaction_dot ? InteractionKind::Dot : InteractionKind::Concat;
+    auto* rm = new RefModel;
+    rm->m = std::make_unique<DlrmModel<float>>(cfg);
+    *out = rm;
+  });
+}
+void ref_model_destroy(void* m) { delete static_cast<RefModel*>(m); }
+
+int ref_model_init(void* m, uint64_t seed) {
+  return guarded([&] { static_cast<RefModel*>(m)->m->init(seed, InitSpec::sampled_gaussian()); });
+}
+
+// parameters through the reference's own checkpoint writer (EmbeddingLayer::put,
+// Mlp::put): which 0 bottom.w, 1 bottom.b, 2 top.w, 3 top.b (index = layer),
+// 4 TT core k of table index, 5 dense table index (k ignored); returns count
+int64_t ref_model_param(void* m, int which, int index, int k, float* out) {
+  int64_t n = -1;
+  guarded([&] {
+    Checkpoint cp;
+    static_cast<RefModel*>(m)->m->save_checkpoint(cp);
+    std::vector<float> v;
+    if (which <= 3) {
+      const char* pre = which < 2 ? "bottom" : "top";
+      v = cp.get_array<float>(concat(pre, which % 2 == 0 ? ".w" : ".b", index));
+    } else if (which == 4) {
+      const auto tab = cp.get_table<float>(concat("table", index));
+      v.assign(tab.core(k).begin(), tab.core(k).end());
+    } else {
+      v = cp.get_array<float>(concat("table", index));
+    }
+    if (out) std::memcpy(out, v.data(), v.size() * sizeof(float));
+    n = static_cast<int64_t>(v.size());
+  });
+  return n;
+}
+
+// one training step (train(), model.hpp:566-573): forward, bce_with_logits,
+// backward, step.  idx / off: per table, concatenated (table t's lookups at
+// lk_off[t], its bs + 1 offsets at t * (bs + 1)).
+int ref_model_step(void* m, int64_t bs, const double* dense, const double* labels, int ntables,
+                   const int64_t* idx, const int64_t* lk_off, const int64_t* off, double lr,
+                   float* logits_out, double* loss_out) {
+  return guarded([&] {
+    auto& model = *static_cast<RefModel*>(m)->m;
+    MiniBatch mb;
+    mb.batch_size = bs;
+    mb.dense.assign(dense, dense + bs * model.config().dense_features);
+    mb.labels.assign(labels, labels + bs);
+    for (int t = 0; t < ntables; ++t)
+      mb.tables.push_back(make_batch(idx + lk_off[t], lk_off[t + 1] - lk_off[t], off + t * (bs + 1), bs,
+                                     nullptr, 0));
+    auto logits = model.forward(mb, kDefaultMicroBatch, true);
+    std::vector<float> dlogits;
+    *loss_out = bce_with_logits<float>(logits, mb.labels, &dlogits);
+    if (logits_out) std::memcpy(logits_out, logits.data(), logits.size() * sizeof(float));
+    model.backward(mb, dlogits);
+    model.step(lr);
+  });
+}
+
+// SyntheticDataSource minibatches (data.cpp): dense (bs x df), labels (bs),
+// per-table lookups (pooling factor pf, so table t's lookups are at t * bs * pf)
+// and offsets (t * (bs + 1))
+struct RefSource {
+  std::unique_ptr<SyntheticDataSource> s;
+};
+int ref_source_create(int64_t dense_features, int ntables, const int64_t* rows, double zipf,
+                      int64_t bs, int64_t pf, uint64_t seed, void** out) {
+  return guarded([&] {
+    SyntheticConfig c;
+    c.dense_features = dense_features;
+    c.table_rows.assign(rows, rows + ntables);
+    c.zipf_exponent = zipf;
+    c.batch_size = bs;
+    c.pooling_factor = pf;
+    auto* rs = new RefSource;
+    rs->s = std::make_unique<SyntheticDataSource>(c, seed);
+    *out = rs;
+  });
+}
+void ref_source_destroy(void* s) { delete static_cast<RefSource*>(s); }
+int ref_source_next(void* s, int64_t iteration, double* dense, double* labels, int64_t* idx,
+                    int64_t* off) {
+  return guarded([&] {
+    MiniBatch mb = static_cast<RefSource*>(s)->s->next(iteration);
+    std::memcpy(dense, mb.dense.data(), mb.dense.size() * sizeof(double));
+    std::memcpy(labels, mb.labels.data(), mb.labels.size() * sizeof(double));
+    int64_t li = 0;
+    for (size_t t = 0; t < mb.tables.size(); ++t) {
+      const auto& b = mb.tables[t];
+      std::memcpy(idx + li, b.indices.data(), b.indices.size() * 8);
+      std::memcpy(off + t * b.offsets.size(), b.offsets.data(), b.offsets.size() * 8);
+      li += static_cast<int64_t>(b.indices.size());
+    }
+  });
+}
+
 }  // extern "C"

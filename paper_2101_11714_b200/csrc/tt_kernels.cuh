@@ -1231,12 +1231,14 @@ __global__ void __launch_bounds__(128) k_head_g0(DevPlan P, const T* __restrict_
                                                  const int* __restrict__ counts, T* __restrict__ out,
                                                  T lr) {
   // the pair ids of a tile of i1 values are resolved by all threads at once
-  // (one round trip), then every thread sums its elements over them in i1
-  // order -- the D0 loads of consecutive i1 are independent and pipeline
-  constexpr int kTile = 1024, kEPT = 4;
+  // (one round trip) and compacted in i1 order; every thread then sums its
+  // elements over them with kU independent D0 loads in flight
+  constexpr int kTile = 1024, kEPT = 4, kU = 16;
   __shared__ int pids[kTile];
+  __shared__ int wcnt[4];
   const int U = counts[0];
   const int s0 = P.slice[0], m0 = P.m[0], m1 = P.m[1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int i0 = blockIdx.x; i0 < m0; i0 += gridDim.x) {
     for (int e0 = 0; e0 < s0; e0 += kEPT * blockDim.x) {
       T sum[kEPT];
@@ -1246,22 +1248,45 @@ __global__ void __launch_bounds__(128) k_head_g0(DevPlan P, const T* __restrict_
       for (int b = 0; b < m1; b += kTile) {
         const int nb = m1 - b < kTile ? m1 - b : kTile;
         __syncthreads();
-        for (int j = threadIdx.x; j < nb; j += blockDim.x) {
-          const uint32_t key = static_cast<uint32_t>(b + j) * static_cast<uint32_t>(m0) + i0;
-          const int pid = pair_tab[key];
-          pids[j] = (pid < 0 || pid >= U || pair_key_u[pid] != key) ? -1 : pid;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int j = 0; j < nb; ++j) {
-          const int pid = pids[j];
-          if (pid < 0) continue;
-          touched = true;
-#pragma unroll
-          for (int k = 0; k < kEPT; ++k) {
-            const int e = e0 + k * blockDim.x + threadIdx.x;
-            if (e < s0) sum[k] += D0[static_cast<int64_t>(pid) * s0 + e];
+        // thread j resolves i1 = b + j.. (blockDim-strided chunks, each chunk
+        // compacted in order by a ballot prefix)
+        int nvalid = 0;
+        for (int j0 = 0; j0 < nb; j0 += blockDim.x) {
+          const int j = j0 + threadIdx.x;
+          int pid = -1;
+          if (j < nb) {
+            const uint32_t key = static_cast<uint32_t>(b + j) * static_cast<uint32_t>(m0) + i0;
+            pid = pair_tab[key];
+            if (pid < 0 || pid >= U || pair_key_u[pid] != key) pid = -1;
           }
+          const unsigned bal = __ballot_sync(0xffffffffu, pid >= 0);
+          if (lane == 0) wcnt[wid] = __popc(bal);
+          __syncthreads();
+          int before = nvalid;
+          for (int w = 0; w < wid; ++w) before += wcnt[w];
+          int total = nvalid;
+          for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += wcnt[w];
+          if (pid >= 0) pids[before + __popc(bal & ((1u << lane) - 1u))] = pid;
+          nvalid = total;
+          __syncthreads();
+        }
+        if (nvalid) touched = true;
+        for (int j = 0; j < nvalid; j += kU) {
+          T v[kU][kEPT];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int pid = j + u < nvalid ? pids[j + u] : -1;
+#pragma unroll
+            for (int k = 0; k < kEPT; ++k) {
+              const int e = e0 + k * blockDim.x + threadIdx.x;
+              v[u][k] = (pid >= 0 && e < s0) ? D0[static_cast<int64_t>(pid) * s0 + e] : T(0);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (j + u < nvalid)
+#pragma unroll
+              for (int k = 0; k < kEPT; ++k) sum[k] += v[u][k];
         }
       }
 #pragma unroll

@@ -120,3 +120,25 @@ def test_reference_plan_goldens():
     # acceptance.cpp:72-80 / tests/golden/table2_r32.txt:1
     _, info = ref.plan_shapes(10131227, 16, 3, 32, [200, 220, 250], [2, 2, 4])
     assert info["params"] == 495360 and info["reduction"] == 327
+
+
+@pytest.mark.skipif(not ref_available(), reason="reference build missing")
+def test_reference_model_driver():
+    """The reference DlrmModel / SyntheticDataSource wrappers the GPU DLRM test
+    checks against (oracle/ref_driver.cpp): parameter shapes follow the config
+    and a few training steps give finite, decreasing-ish losses."""
+    from pyoracle import RefModel, RefSource
+
+    ref = RefImpl()
+    tables = [(5000, True, 8), (300, False, 0)]
+    m = RefModel(ref, 3, 16, tables, [16], [8, 1])
+    m.init(2)
+    assert m.param(0, 0).size == 16 * 3 and m.param(1, 0).size == 16
+    assert m.param(2, 0).size == 8 * (16 + 3) and m.param(2, 1).size == 8
+    assert m.param(5, 1).size == 300 * 16
+    src = RefSource(ref, 3, [t[0] for t in tables], 1.05, 64, 1, 3)
+    mb = src.next(0)
+    assert mb["dense"].shape == (64, 3) and set(np.unique(mb["labels"])) <= {0.0, 1.0}
+    assert all(len(o) == 65 for o in mb["off"])
+    losses = [m.step(src.next(i), 0.05)[1] for i in range(6)]
+    assert all(np.isfinite(losses))
