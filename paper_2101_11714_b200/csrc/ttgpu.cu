@@ -629,18 +629,16 @@ void backward_impl(ttgpu_table* t, ttgpu_ctx* c, const T* grad, int mode, double
     c->pos2.ensure(4 * L);
     c->tcontrib.ensure(sizeof(T) * L * P.slice[2]);
     k_inv_perm<<<gL, kThreads, 0, st>>>(c->s_dlk.as<uint32_t>(), L, c->pos2.as<uint32_t>());
-    set_smem(w3::k_w3_bwd, w3::kBwdSmem);
-    const int g = static_cast<int>(std::min<int64_t>((nchunksL + w3::kWarpsB / 2 - 1) / (w3::kWarpsB / 2),
+    // pair-aligned warps: S(pair) complete at the end of its walk, no fold
+    set_smem(w3::k_w3_bwd_pairs, w3::kBwdSmem);
+    const int g = static_cast<int>(std::min<int64_t>((ucap + w3::kWarpsB / 2 - 1) / (w3::kWarpsB / 2),
                                                      static_cast<int64_t>(t->num_sms) * 3));
-    w3::k_w3_bwd<<<g, w3::kWarpsB * 32, w3::kBwdSmem, st>>>(
+    w3::k_w3_bwd_pairs<<<g, w3::kWarpsB * 32, w3::kBwdSmem, st>>>(
         reinterpret_cast<const float*>(cores + P.coff[2]), reinterpret_cast<const float*>(c->H.as<T>()),
-        c->lk_pid.as<int32_t>(), c->tail_dig.as<uint32_t>(), c->lk_bag.as<int32_t>(),
-        reinterpret_cast<const float*>(c->lk_alpha.as<T>()), reinterpret_cast<const float*>(grad),
-        c->s_lk.as<uint32_t>(), c->pair_scan.as<unsigned long long>(), c->pos2.as<uint32_t>(), L,
-        reinterpret_cast<float*>(c->partS.as<T>()), reinterpret_cast<float*>(c->tcontrib.as<T>()));
-    k_combine<T, 0><<<grid_for(ucap, 1, t->num_sms, 8), 128, 0, st>>>(
-        c->partS.as<T>(), c->pair_scan.as<unsigned long long>(), c->pair_start.as<int32_t>(),
-        c->counts.as<int>(), 0, P.W1, c->S.as<T>(), T(0));
+        c->counts.as<int>(), c->pair_start.as<int32_t>(), c->tail_dig.as<uint32_t>(),
+        c->lk_bag.as<int32_t>(), reinterpret_cast<const float*>(c->lk_alpha.as<T>()),
+        reinterpret_cast<const float*>(grad), c->s_lk.as<uint32_t>(), c->pos2.as<uint32_t>(),
+        reinterpret_cast<float*>(c->S.as<T>()), reinterpret_cast<float*>(c->tcontrib.as<T>()));
   } else if (staged3) {
     const size_t smem = sizeof(T) * kTailChunk * (P.N + P.slice[2]) + 4 * kTailChunk;
     set_smem(k_srun3<T>, smem);

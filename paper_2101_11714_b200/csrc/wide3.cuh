@@ -16,17 +16,14 @@
 //             Exact mode keeps the reference's per-element order (r ascending,
 //             separately rounded products and sums: gemm.hpp:15-31), so the
 //             pooled output stays bit-identical.
-//   k_w3_bwd  (backward tail) lane = 2 columns r of the 64.  Per pair run the
-//             lane holds H[a][r] (16 x 2) and the running S[a][r] (16 x 2) in
-//             registers; per lookup (D2 = T(alpha)·grad[bag] staged once per
-//             chunk in shared memory, read as broadcasts):
+//   k_w3_bwd_pairs (backward tail) two warps per PAIR, lane = one column r
+//             of the 64.  The lane holds H[a][r] and the running S[a][r] (16 a)
+//             in registers as f32x2 pairs; per lookup (D2 = T(alpha)·grad[bag]
+//             staged per 32-lookup chunk in shared memory, read as broadcasts):
 //               S[a][r]  += Σ_j D2[a][j]·G2[i2][r][j]     (S = Σ D1, D1 = D2·G2ᵀ)
 //               C[r][j]   = Σ_a H[a][r]·D2[a][j]          (dG2 contribution)
-//             S is written once per run (partial row, folded by k_combine as
-//             before); C goes to the lookup's i2-sorted position, summed per i2
-//             by k_w3_segsum.  Per element the same fma chains as k_srun3 /
-//             k_pairwalk3 MODE 1, so gradients are bitwise those of the generic
-//             kernels.
+//             S(pair) is written once, complete; C goes to the lookup's
+//             i2-sorted position, summed per i2 by k_w3_segsum.
 //   k_w3_segsum  dG2[i2] = Σ C over the i2 segment in position order, split
 //             into slabs of kW3Slab rows so every SM streams (the generic
 //             k_segsum3 runs one CTA per i2 with 2,000-long dependent chains);
@@ -222,112 +219,102 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_w3_fwd(const float* __restri
 constexpr int kWarpsB = 8;                              // 4 chunks x 2 column halves
 constexpr size_t kBwdSmem = sizeof(float) * kWarpsB * kChunk * N;  // 64 KB: [warp][q][j][a]
 
-__global__ void __launch_bounds__(kWarpsB * 32, 3) k_w3_bwd(
-    const float* __restrict__ G2, const float* __restrict__ H, const int32_t* __restrict__ lk_pid,
-    const uint32_t* __restrict__ tail_dig, const int32_t* __restrict__ lk_bag,
-    const float* __restrict__ lk_alpha, const float* __restrict__ grad,
-    const uint32_t* __restrict__ s_lk, const unsigned long long* __restrict__ scan,
-    const uint32_t* __restrict__ pos2, int64_t L, float* __restrict__ partS,
-    float* __restrict__ contrib) {
-  extern __shared__ __align__(16) float w3b_dyn[];
+// A warp pair owns whole PAIRS (grid-stride over the unique pairs, positions
+// pair_start[p] .. pair_start[p + 1]), walked in chunks of kChunk lookups, so
+// S(p) is complete when its walk ends and is written straight to S[p] -- no
+// partial rows and no separate fold.  S sums over the pair's lookups in sorted
+// order.
+__global__ void __launch_bounds__(kWarpsB * 32, 3) k_w3_bwd_pairs(
+    const float* __restrict__ G2, const float* __restrict__ H, const int* __restrict__ counts,
+    const int32_t* __restrict__ pair_start, const uint32_t* __restrict__ tail_dig,
+    const int32_t* __restrict__ lk_bag, const float* __restrict__ lk_alpha,
+    const float* __restrict__ grad, const uint32_t* __restrict__ s_lk,
+    const uint32_t* __restrict__ pos2, float* __restrict__ S, float* __restrict__ contrib) {
+  extern __shared__ __align__(16) float w3p_dyn[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* d2s = w3b_dyn + wid * kChunk * N;  // this warp's [q][j][a]
+  float* d2s = w3p_dyn + wid * kChunk * N;  // this warp's [q][j][a]
   const int half = wid & 1;
   const int r = half * 32 + lane;  // this lane's column
-  const int64_t nchunks = (L + kChunk - 1) / kChunk;
-  for (int64_t ch = static_cast<int64_t>(blockIdx.x) * (kWarpsB / 2) + (wid >> 1); ch < nchunks;
-       ch += static_cast<int64_t>(gridDim.x) * (kWarpsB / 2)) {
-    const int64_t c0 = ch * kChunk;
-    const int n = static_cast<int>(L - c0 < kChunk ? L - c0 : kChunk);
-    int pid = -1, i2 = 0, run = 0, bag = 0;
-    uint32_t p2 = 0;
-    float al = 0.f;
-    __syncwarp();
-    if (lane < n) {
-      const int l = static_cast<int>(s_lk[c0 + lane]);
-      pid = lk_pid[l];
-      i2 = static_cast<int>(tail_dig[l]);
-      run = static_cast<int>(scan[c0 + lane] >> 32) - 1;
-      p2 = pos2[l];
-      bag = lk_bag[l];
-      al = lk_alpha[l];
-    }
-    // D2 = T(alpha)·grad[bag] transposed to [j][a]: two lookups (2 x 256 B) per
-    // warp load; lane (q, a4 = lane & 15 -> a = a4 / 4 * 4.., j...) writes 4 floats
-#pragma unroll 4
-    for (int it = 0; it < kChunk / 2; ++it) {
-      const int qq = it * 2 + (lane >> 4), k4 = lane & 15;  // float4 k4 of row qq = D2[a = k4][0..3]
-      const int bq = __shfl_sync(0xffffffffu, bag, qq);
-      const float aq = __shfl_sync(0xffffffffu, al, qq);
-      if (qq < n) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bq) * N) + k4);
-        float* dq = d2s + qq * N + k4;  // [j][a]: j * 16 + a
-        dq[0 * P1] = __fmul_rn(aq, v.x);
-        dq[1 * P1] = __fmul_rn(aq, v.y);
-        dq[2 * P1] = __fmul_rn(aq, v.z);
-        dq[3 * P1] = __fmul_rn(aq, v.w);
-      }
-    }
-    __syncwarp();
+  const int U = counts[0];
+  for (int p = blockIdx.x * (kWarpsB / 2) + (wid >> 1); p < U; p += gridDim.x * (kWarpsB / 2)) {
+    const int ps = pair_start[p], pe = pair_start[p + 1];
     unsigned long long h[P1 / 2], s[P1 / 2];
-    int cur = -1;
-    // the lane's G2 row of lookups q + 1 and q + 2 in flight
-    float4 gn = ld4(G2 + static_cast<int64_t>(__shfl_sync(0xffffffffu, i2, 0)) * S2 + r * N2);
-    float4 gnn = ld4(G2 + static_cast<int64_t>(__shfl_sync(0xffffffffu, i2, 1)) * S2 + r * N2);
-    for (int q = 0; q < n; ++q) {
-      const int p = __shfl_sync(0xffffffffu, pid, q);
-      const int rq = __shfl_sync(0xffffffffu, run, q);
-      const uint32_t pq = __shfl_sync(0xffffffffu, p2, q);
-      const float4 g = gn;
-      gn = gnn;
-      {
-        const int i2q = __shfl_sync(0xffffffffu, i2, (q + 2) & 31);
-        if (q + 2 < n) gnn = ld4(G2 + static_cast<int64_t>(i2q) * S2 + r * N2);
-      }
-      const unsigned long long g0 = pk(g.x, g.x), g1 = pk(g.y, g.y), g2 = pk(g.z, g.z), g3 = pk(g.w, g.w);
-      if (p != cur) {  // a new pair run: H[a][r] pairs into registers, S from zero
-        const float* hp = H + static_cast<int64_t>(p) * W1 + r;
-#pragma unroll
-        for (int a2 = 0; a2 < P1 / 2; ++a2) {
-          h[a2] = pk(__ldg(hp + (2 * a2) * R2), __ldg(hp + (2 * a2 + 1) * R2));
-          s[a2] = 0ull;
-        }
-        cur = p;
-      }
-      unsigned long long c0v = 0ull, c1v = 0ull, c2v = 0ull, c3v = 0ull;
-      const float* dq = d2s + q * N;
+    {
+      const float* hp = H + static_cast<int64_t>(p) * W1 + r;
 #pragma unroll
       for (int a2 = 0; a2 < P1 / 2; ++a2) {
-        // (D2[a][j], D2[a+1][j]) for j = 0..3, a = 2 a2 (broadcast reads)
-        const unsigned long long d0 = *reinterpret_cast<const unsigned long long*>(dq + 0 * P1 + 2 * a2);
-        const unsigned long long d1 = *reinterpret_cast<const unsigned long long*>(dq + 1 * P1 + 2 * a2);
-        const unsigned long long d2 = *reinterpret_cast<const unsigned long long*>(dq + 2 * P1 + 2 * a2);
-        const unsigned long long d3 = *reinterpret_cast<const unsigned long long*>(dq + 3 * P1 + 2 * a2);
-        unsigned long long v = fma2(d0, g0, 0ull);
-        v = fma2(d1, g1, v);
-        v = fma2(d2, g2, v);
-        v = fma2(d3, g3, v);
-        s[a2] = add2(s[a2], v);
-        c0v = fma2(h[a2], d0, c0v);
-        c1v = fma2(h[a2], d1, c1v);
-        c2v = fma2(h[a2], d2, c2v);
-        c3v = fma2(h[a2], d3, c3v);
+        h[a2] = pk(__ldg(hp + (2 * a2) * R2), __ldg(hp + (2 * a2 + 1) * R2));
+        s[a2] = 0ull;
       }
-      // C[r][j] = even-a sum + odd-a sum, at the lookup's i2-sorted position
-      const float2 e0 = upk(c0v), e1 = upk(c1v), e2 = upk(c2v), e3 = upk(c3v);
-      *reinterpret_cast<float4*>(contrib + static_cast<int64_t>(pq) * S2 + r * N2) =
-          make_float4(e0.x + e0.y, e1.x + e1.y, e2.x + e2.y, e3.x + e3.y);
-      // the run ends here: its S partial row (a-major, [a][r])
-      const int pn = q + 1 < n ? __shfl_sync(0xffffffffu, pid, q + 1) : -2;
-      if (pn != p) {
-        float* so = partS + static_cast<int64_t>(rq) * W1 + r;
-#pragma unroll
-        for (int a2 = 0; a2 < P1 / 2; ++a2) {
-          const float2 sv = upk(s[a2]);
-          so[(2 * a2) * R2] = sv.x;
-          so[(2 * a2 + 1) * R2] = sv.y;
+    }
+    for (int c0 = ps; c0 < pe; c0 += kChunk) {
+      const int n = pe - c0 < kChunk ? pe - c0 : kChunk;
+      int i2 = 0, bag = 0;
+      uint32_t p2 = 0;
+      float al = 0.f;
+      __syncwarp();
+      if (lane < n) {
+        const int l = static_cast<int>(s_lk[c0 + lane]);
+        i2 = static_cast<int>(tail_dig[l]);
+        p2 = pos2[l];
+        bag = lk_bag[l];
+        al = lk_alpha[l];
+      }
+#pragma unroll 4
+      for (int it = 0; it < kChunk / 2; ++it) {
+        const int qq = it * 2 + (lane >> 4), k4 = lane & 15;
+        const int bq = __shfl_sync(0xffffffffu, bag, qq);
+        const float aq = __shfl_sync(0xffffffffu, al, qq);
+        if (qq < n) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bq) * N) + k4);
+          float* dq = d2s + qq * N + k4;  // [j][a]: j * 16 + a
+          dq[0 * P1] = __fmul_rn(aq, v.x);
+          dq[1 * P1] = __fmul_rn(aq, v.y);
+          dq[2 * P1] = __fmul_rn(aq, v.z);
+          dq[3 * P1] = __fmul_rn(aq, v.w);
         }
       }
+      __syncwarp();
+      float4 gn = ld4(G2 + static_cast<int64_t>(__shfl_sync(0xffffffffu, i2, 0)) * S2 + r * N2);
+      float4 gnn = ld4(G2 + static_cast<int64_t>(__shfl_sync(0xffffffffu, i2, 1)) * S2 + r * N2);
+      for (int q = 0; q < n; ++q) {
+        const uint32_t pq = __shfl_sync(0xffffffffu, p2, q);
+        const float4 g = gn;
+        gn = gnn;
+        {
+          const int i2q = __shfl_sync(0xffffffffu, i2, (q + 2) & 31);
+          if (q + 2 < n) gnn = ld4(G2 + static_cast<int64_t>(i2q) * S2 + r * N2);
+        }
+        const unsigned long long g0 = pk(g.x, g.x), g1 = pk(g.y, g.y), g2 = pk(g.z, g.z), g3 = pk(g.w, g.w);
+        unsigned long long c0v = 0ull, c1v = 0ull, c2v = 0ull, c3v = 0ull;
+        const float* dq = d2s + q * N;
+#pragma unroll
+        for (int a2 = 0; a2 < P1 / 2; ++a2) {
+          const unsigned long long d0 = *reinterpret_cast<const unsigned long long*>(dq + 0 * P1 + 2 * a2);
+          const unsigned long long d1 = *reinterpret_cast<const unsigned long long*>(dq + 1 * P1 + 2 * a2);
+          const unsigned long long d2 = *reinterpret_cast<const unsigned long long*>(dq + 2 * P1 + 2 * a2);
+          const unsigned long long d3 = *reinterpret_cast<const unsigned long long*>(dq + 3 * P1 + 2 * a2);
+          unsigned long long v = fma2(d0, g0, 0ull);
+          v = fma2(d1, g1, v);
+          v = fma2(d2, g2, v);
+          v = fma2(d3, g3, v);
+          s[a2] = add2(s[a2], v);
+          c0v = fma2(h[a2], d0, c0v);
+          c1v = fma2(h[a2], d1, c1v);
+          c2v = fma2(h[a2], d2, c2v);
+          c3v = fma2(h[a2], d3, c3v);
+        }
+        const float2 e0 = upk(c0v), e1 = upk(c1v), e2 = upk(c2v), e3 = upk(c3v);
+        *reinterpret_cast<float4*>(contrib + static_cast<int64_t>(pq) * S2 + r * N2) =
+            make_float4(e0.x + e0.y, e1.x + e1.y, e2.x + e2.y, e3.x + e3.y);
+      }
+    }
+    float* so = S + static_cast<int64_t>(p) * W1 + r;
+#pragma unroll
+    for (int a2 = 0; a2 < P1 / 2; ++a2) {
+      const float2 sv = upk(s[a2]);
+      so[(2 * a2) * R2] = sv.x;
+      so[(2 * a2 + 1) * R2] = sv.y;
     }
   }
 }
