@@ -37,13 +37,10 @@ namespace f3 {
 // cudaLaunchAttributeProgrammaticStreamSerialization when the table enables it).
 // Every kernel waits for its predecessor grid's completion (griddepcontrol.wait:
 // a no-op without PDL) before touching memory, so overlap is limited to launch
-// and scheduling; g_pdl_early additionally lets the dependent grid be scheduled
+// and scheduling.  (An early launch_dependents trigger measured slower and was
+// dropped: it also cost every kernel a dependent global load at entry.)
 // as soon as every CTA of this one has started.
-__device__ int g_pdl_early = 0;
-__device__ __forceinline__ void pdl_entry() {
-  if (g_pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
+__device__ __forceinline__ void pdl_entry() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 struct Geo {
   int m0, m1, m2;
@@ -1559,14 +1556,22 @@ __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restri
   pdl_entry();
   const int lane = threadIdx.x & 31;
   constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
+  // the group bases of both keys in shared memory: a warp's slice lookup is a
+  // binary search there instead of ~8 dependent global loads
+  extern __shared__ int cb_sm[];
+  int* gb1 = cb_sm;
+  int* gb2 = cb_sm + g.m1 + 1;
+  for (int e = threadIdx.x; e < g.m1 + 1; e += blockDim.x) gb1[e] = A.group_base1[e];
+  for (int e = threadIdx.x; e < g.m2 + 1; e += blockDim.x) gb2[e] = A.group_base2[e];
+  __syncthreads();
   int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   bool touched = false;
   if (task < A.maxg1 * C1c) {
     const int gidx = task / C1c, ch = task - gidx * C1c;
-    if (gidx >= A.group_base1[g.m1]) return;
-    const int i1 = find_slice(A.group_base1, g.m1, gidx);
-    const int gfirst = A.group_base1[i1], ng = A.group_base1[i1 + 1] - gfirst, gi = gidx - gfirst;
+    if (gidx >= gb1[g.m1]) return;
+    const int i1 = find_slice(gb1, g.m1, gidx);
+    const int gfirst = gb1[i1], ng = gb1[i1 + 1] - gfirst, gi = gidx - gfirst;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S1 / 4;
     auto row = [&](int t) { return A.part1 + static_cast<int64_t>(t) * D::S1; };
@@ -1586,9 +1591,9 @@ __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restri
   task -= A.maxg1 * C1c;
   if (task < A.maxg2 * C2c) {
     const int gidx = task / C2c, ch = task - gidx * C2c;
-    if (gidx >= A.group_base2[g.m2]) return;
-    const int i2 = find_slice(A.group_base2, g.m2, gidx);
-    const int gfirst = A.group_base2[i2], ng = A.group_base2[i2 + 1] - gfirst, gi = gidx - gfirst;
+    if (gidx >= gb2[g.m2]) return;
+    const int i2 = find_slice(gb2, g.m2, gidx);
+    const int gfirst = gb2[i2], ng = gb2[i2 + 1] - gfirst, gi = gidx - gfirst;
     const int col4 = ch * 32 + lane;
     const bool colok = col4 < D::S2 / 4;
     auto row = [&](int t) { return A.part2 + static_cast<int64_t>(t) * D::S2; };

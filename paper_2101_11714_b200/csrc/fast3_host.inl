@@ -414,7 +414,9 @@ struct F3Runner {
       A.gtouch = f.gtouch.as<int>();
       A.counters = f.counters.as<int>();
       auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
-      f3_launch(t->pdl, ck, dim3((tasks * 32 + f3::kThreads - 1) / f3::kThreads), dim3(f3::kThreads), 0, st, 
+      const size_t csm = 4 * static_cast<size_t>(g.m1 + 1 + g.m2 + 1);
+      set_smem(ck, csm);
+      f3_launch(t->pdl, ck, dim3((tasks * 32 + f3::kThreads - 1) / f3::kThreads), dim3(f3::kThreads), csm, st, 
           g, t->cores.as<float>(), t->grads.as<float>(), A, lr);
     }
     t->mark("f3_combine");

@@ -996,11 +996,9 @@ int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* r
     t->stream = static_cast<cudaStream_t>(stream);
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, device));
-    {  // TTGPU_PDL: 0 plain launches, 1 programmatic dependent launch, 2 PDL + early trigger
+    {  // TTGPU_PDL: 0 plain launches, nonzero programmatic dependent launch
       const char* e = std::getenv("TTGPU_PDL");
       t->pdl = e ? std::atoi(e) : 0;
-      const int early = t->pdl >= 2 ? 1 : 0;
-      CK(cudaMemcpyToSymbol(f3::g_pdl_early, &early, sizeof(int)));
       const char* cs = std::getenv("TTGPU_GRID_SORT");
       t->grid_sort = !(cs && std::atoi(cs) == 0);
       const char* ch = std::getenv("TTGPU_CHUNKED");
