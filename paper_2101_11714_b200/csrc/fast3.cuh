@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   // next tile's descriptor + record, the tile after that's descriptor
   bool g2_act = false;
   int g2_i2 = 0, g2_ntl = 0;
+  int g1_key = -1;  // the i1 whose G1 slice is in G1s (warp 0)
   Tile ndn{}, nd2{};
   uint4 nrn = make_uint4(0u, 0u, 0u, 0u);
   // slots + metadata of tile u into buffer m, G1/G0 copies onto bar[0]
@@ -688,11 +689,15 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     g2_i2 = static_cast<int>(r.y >> 16);
     g2_ntl = ntl;
     __syncwarp();
+    // G1[i1] stays staged across consecutive tiles of the same bucket (hot
+    // buckets under Zipf): only a new i1 is copied
+    const bool need_g1 = tl.key != g1_key;
+    g1_key = tl.key;
     if (lane == 0) {
       // smem last touched by generic-proxy accesses; order them before the async writes
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect(bar, (D::S1 + nslots * D::S0) * 4);
-      tma_load(G1s, G1 + static_cast<int64_t>(tl.key) * D::S1, D::S1 * 4, bar);
+      mbar_arrive_expect(bar, ((need_g1 ? D::S1 : 0) + nslots * D::S0) * 4);
+      if (need_g1) tma_load(G1s, G1 + static_cast<int64_t>(tl.key) * D::S1, D::S1 * 4, bar);
     }
     __syncwarp();
     if (is_first) tma_load(G0s + s * SM::S0P, G0 + static_cast<int64_t>(i0) * D::S0, D::S0 * 4, bar);
