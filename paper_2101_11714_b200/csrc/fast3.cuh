@@ -25,6 +25,7 @@
 // bit-identical to ttrec::forward_bags.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 #include <cub/block/block_reduce.cuh>
 
@@ -991,13 +992,12 @@ struct Bwd1Smem {
 };
 
 template <class D>
-__global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
+__device__ __forceinline__ void bwd1_body(
     Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
     const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
     unsigned char* __restrict__ d0mask) {
-  pdl_entry();
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
   extern __shared__ __align__(128) float sm[];
@@ -1382,7 +1382,7 @@ __device__ __forceinline__ void sum_live(unsigned live, int cand0, int col4, boo
     float4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      v[u] = (idx[u] >= 0 && colok) ? __ldg(reinterpret_cast<const float4*>(row_of(idx[u])) + col4)
+      v[u] = (idx[u] >= 0 && colok) ? __ldcg(reinterpret_cast<const float4*>(row_of(idx[u])) + col4)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int u = 0; u < 8; ++u)
@@ -1554,22 +1554,14 @@ __device__ __forceinline__ int find_slice(const int32_t* base, int K, int x) {
   return lo;
 }
 
-template <class D, int MODE>
-__global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restrict__ cores,
-                                                       float* __restrict__ grads, CombineArgs A,
-                                                       float lr) {
-  pdl_entry();
+// One combine warp task (task = slice group x 128-column chunk of dG1, dG2 or
+// dG0).  gb1 / gb2: the group bases of both keys (shared memory copies).
+template <class D>
+__device__ __forceinline__ void combine_task(int task, const int* gb1, const int* gb2, Geo g,
+                                             float* __restrict__ cores, float* __restrict__ grads,
+                                             const CombineArgs& A, float lr, int MODE) {
   const int lane = threadIdx.x & 31;
   constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
-  // the group bases of both keys in shared memory: a warp's slice lookup is a
-  // binary search there instead of ~8 dependent global loads
-  extern __shared__ int cb_sm[];
-  int* gb1 = cb_sm;
-  int* gb2 = cb_sm + g.m1 + 1;
-  for (int e = threadIdx.x; e < g.m1 + 1; e += blockDim.x) gb1[e] = A.group_base1[e];
-  for (int e = threadIdx.x; e < g.m2 + 1; e += blockDim.x) gb2[e] = A.group_base2[e];
-  __syncthreads();
-  int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   bool touched = false;
   if (task < A.maxg1 * C1c) {
@@ -1636,6 +1628,59 @@ __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restri
                      A.counters + g.m1 * C1c + g.m2 * C2c + i0 * C0c + ch, A,
                      cores + g.coff0 + static_cast<int64_t>(i0) * D::S0,
                      grads + g.coff0 + static_cast<int64_t>(i0) * D::S0, MODE, lr);
+}
+
+template <class D>
+__global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
+    Geo g, const float* __restrict__ cores, const Tile* __restrict__ tiles,
+    const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
+    const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
+    float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
+    unsigned char* __restrict__ d0mask) {
+  pdl_entry();
+  bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask);
+}
+
+// f3_bwd1 and f3_combine in ONE cooperative launch (the bwd1 grid is exactly
+// the co-resident CTAs): after its tiles every CTA meets a grid barrier, then
+// its warps take the combine tasks (grid-stride).  Saves the combine launch
+// and its ramp; the combine's partial loads are L2-coherent (__ldcg).
+template <class D>
+__global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1_comb(
+    Geo g, float* __restrict__ cores, const Tile* __restrict__ tiles,
+    const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
+    const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
+    float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
+    unsigned char* __restrict__ d0mask, float* __restrict__ grads, CombineArgs A, float lr, int mode,
+    int ntasks) {
+  pdl_entry();
+  bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask);
+  cooperative_groups::this_grid().sync();
+  extern __shared__ __align__(128) float sm[];
+  int* gb1 = reinterpret_cast<int*>(sm);
+  int* gb2 = gb1 + g.m1 + 1;
+  for (int e = threadIdx.x; e < g.m1 + 1; e += blockDim.x) gb1[e] = __ldcg(A.group_base1 + e);
+  for (int e = threadIdx.x; e < g.m2 + 1; e += blockDim.x) gb2[e] = __ldcg(A.group_base2 + e);
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  for (int task = blockIdx.x * nw + (threadIdx.x >> 5); task < ntasks; task += gridDim.x * nw)
+    combine_task<D>(task, gb1, gb2, g, cores, grads, A, lr, mode);
+}
+
+template <class D, int MODE>
+__global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restrict__ cores,
+                                                       float* __restrict__ grads, CombineArgs A,
+                                                       float lr) {
+  pdl_entry();
+  // the group bases of both keys in shared memory: a warp's slice lookup is a
+  // binary search there instead of ~8 dependent global loads
+  extern __shared__ int cb_sm[];
+  int* gb1 = cb_sm;
+  int* gb2 = cb_sm + g.m1 + 1;
+  for (int e = threadIdx.x; e < g.m1 + 1; e += blockDim.x) gb1[e] = A.group_base1[e];
+  for (int e = threadIdx.x; e < g.m2 + 1; e += blockDim.x) gb2[e] = A.group_base2[e];
+  __syncthreads();
+  combine_task<D>((blockIdx.x * blockDim.x + threadIdx.x) >> 5, gb1, gb2, g, cores, grads, A, lr, MODE);
 }
 
 }  // namespace f3

@@ -336,6 +336,10 @@ struct F3Runner {
     } else {
       set_smem(k1, sm1);
       grid1 = grid_occ(k1, f3::kThreads, sm1, t->num_sms, f.max_tiles1);
+      if (t->fuse_comb) {  // the cooperative variant must fit co-resident
+        set_smem(f3::f3_bwd1_comb<D>, sm1);
+        grid1 = std::min(grid1, grid_occ(f3::f3_bwd1_comb<D>, f3::kThreads, sm1, t->num_sms, f.max_tiles1));
+      }
     }
     const int grid2 = grid_occ(f3::f3_bwd2<D>, 128, 0, t->num_sms, f.max_tiles2);
     f.part1.ensure(4 * static_cast<size_t>(f.max_tiles1) * f3::G1Blk<D>::KG * D::S1);
@@ -345,6 +349,37 @@ struct F3Runner {
     f.D0acc.ensure(4 * static_cast<size_t>(grid1) * g.m0 * D::S0);
     f.d0mask.ensure(static_cast<size_t>(grid1) * g.m0);
     f.Sbuf.ensure(4 * static_cast<size_t>(L) * D::W1);
+    // combine arguments (f3_combine, or the combine phase of f3_bwd1_comb)
+    constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
+    f3::CombineArgs A{};
+    A.tile_base1 = f.tile_base1.as<int32_t>();
+    A.tile_base2 = f.tile_base2.as<int32_t>();
+    A.group_base1 = f.group_base1.as<int32_t>();
+    A.group_base2 = f.group_base2.as<int32_t>();
+    A.part1 = f.part1.as<float>();
+    A.part2 = f.part2.as<float>();
+    A.D0acc = f.D0acc.as<float>();
+    A.has1 = f.has1.as<int>();
+    A.has2 = f.has2.as<int>();
+    A.d0mask = f.d0mask.as<unsigned char>();
+    A.maxg1 = g.m1 + (f.max_tiles1 + f3::kGroup - 1) / f3::kGroup;
+    A.maxg2 = g.m2 + (f.max_tiles2 + f3::kGroup - 1) / f3::kGroup;
+    A.nbwd = grid1;
+    const int ng0 = (grid1 + f3::kGroup0 - 1) / f3::kGroup0;
+    const int tasks = A.maxg1 * C1c + A.maxg2 * C2c + g.m0 * ng0 * C0c;  // one warp each
+    const int ncnt = g.m1 * C1c + g.m2 * C2c + g.m0 * C0c;
+    if (f.counters.cap < 4 * static_cast<size_t>(ncnt)) {
+      f.counters.ensure(4 * static_cast<size_t>(ncnt));
+      CK(cudaMemsetAsync(f.counters.p, 0, f.counters.cap, st));
+    }
+    f.gpart.ensure(4 * 128 * static_cast<size_t>(tasks));
+    f.gtouch.ensure(4 * static_cast<size_t>(tasks));
+    A.gpart = f.gpart.as<float>();
+    A.gtouch = f.gtouch.as<int>();
+    A.counters = f.counters.as<int>();
+    // bwd1 + combine in one cooperative launch when the bwd1 grid is co-resident
+    const bool fuse_comb = !f.chunked && t->fuse_comb &&
+                           4 * static_cast<size_t>(g.m1 + g.m2 + 2) <= sm1;
     t->mark("bwd_begin");
     if (f.chunked) {
       f3_launch(t->pdl, kc, dim3(grid1), dim3(f3::kFcThreads), sm1, st, g, t->cores.as<float>(),
@@ -352,8 +387,7 @@ struct F3Runner {
                 f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(), grad, f.part1.as<float>(),
                 f.has1.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>());
       t->mark("f3c_bwd");
-    } else {
-    if (t->fuse_sb) {
+    } else if (t->fuse_sb) {
       // f3_srows and f3_bwd2 in one launch (they are independent)
       f3::SrowsArgs sa{t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
                        f.max_tiles1, f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(),
@@ -365,59 +399,56 @@ struct F3Runner {
                 lk_bag, alpha, grad);
       t->mark("f3_srows_bwd2");
     } else {
-    f3_launch(t->pdl, f3::f3_srows<D>, dim3((f.max_tiles1 * 32 + 255) / 256), dim3(256), 0, st, 
-        t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.max_tiles1,
-        f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
-        f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>());
-    t->mark("f3_srows");
+      f3_launch(t->pdl, f3::f3_srows<D>, dim3((f.max_tiles1 * 32 + 255) / 256), dim3(256), 0, st,
+                t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.max_tiles1,
+                f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(), lk_bag, alpha, grad,
+                f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>());
+      t->mark("f3_srows");
     }
-    f3_launch(t->pdl, k1, dim3(grid1), dim3(f3::kThreads), sm1, st, g, t->cores.as<float>(), f.tiles1.as<f3::Tile>(),
-                                         f.ntiles.as<int>(), f.Sbuf.as<float>(),
-                                         f.tile_i0.as<uint16_t>(), f.tile_nslots.as<int>(),
-                                         f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
-                                         f.d0mask.as<unsigned char>());
-    t->mark("f3_bwd1");
+    auto launch_bwd2 = [&] {
+      f3_launch(t->pdl, f3::f3_bwd2<D>, dim3(grid2), dim3(128), 0, st, g, f.tiles2.as<f3::Tile>(),
+                f.ntiles.as<int>() + 1, f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag, alpha, grad,
+                f.Hbuf.as<float>(), f.part2.as<float>(), f.has2.as<int>());
+      t->mark("f3_bwd2");
+    };
+    if (fuse_comb) {
+      if (!t->fuse_sb) launch_bwd2();  // the combine phase reads its partials
+      auto kf = f3::f3_bwd1_comb<D>;
+      set_smem(kf, sm1);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid1);
+      cfg.blockDim = dim3(f3::kThreads);
+      cfg.dynamicSmemBytes = sm1;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, kf, g, t->cores.as<float>(), static_cast<const f3::Tile*>(f.tiles1.as<f3::Tile>()),
+                            static_cast<const int*>(f.ntiles.as<int>()), static_cast<const float*>(f.Sbuf.as<float>()),
+                            static_cast<const uint16_t*>(f.tile_i0.as<uint16_t>()),
+                            static_cast<const int*>(f.tile_nslots.as<int>()), f.part1.as<float>(),
+                            f.has1.as<int>(), f.D0acc.as<float>(), f.d0mask.as<unsigned char>(),
+                            t->grads.as<float>(), A, lr, mode, tasks));
+      t->mark("f3_bwd1_comb");
+      CK(cudaGetLastError());
+      return;
     }
-    if (!t->fuse_sb || f.chunked) {
-    f3_launch(t->pdl, f3::f3_bwd2<D>, dim3(grid2), dim3(128), 0, st, g, f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1,
-                                          f.perm2.as<uint32_t>(), f.hloc.as<uint32_t>(), lk_bag,
-                                          alpha, grad, f.Hbuf.as<float>(), f.part2.as<float>(),
-                                          f.has2.as<int>());
-    t->mark("f3_bwd2");
+    if (!f.chunked) {
+      f3_launch(t->pdl, k1, dim3(grid1), dim3(f3::kThreads), sm1, st, g, t->cores.as<float>(),
+                f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.Sbuf.as<float>(), f.tile_i0.as<uint16_t>(),
+                f.tile_nslots.as<int>(), f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
+                f.d0mask.as<unsigned char>());
+      t->mark("f3_bwd1");
     }
+    if (!t->fuse_sb || f.chunked) launch_bwd2();
     {
-      constexpr int C1c = (D::S1 + 127) / 128, C2c = (D::S2 + 127) / 128, C0c = (D::S0 + 127) / 128;
-      f3::CombineArgs A{};
-      A.tile_base1 = f.tile_base1.as<int32_t>();
-      A.tile_base2 = f.tile_base2.as<int32_t>();
-      A.group_base1 = f.group_base1.as<int32_t>();
-      A.group_base2 = f.group_base2.as<int32_t>();
-      A.part1 = f.part1.as<float>();
-      A.part2 = f.part2.as<float>();
-      A.D0acc = f.D0acc.as<float>();
-      A.has1 = f.has1.as<int>();
-      A.has2 = f.has2.as<int>();
-      A.d0mask = f.d0mask.as<unsigned char>();
-      A.maxg1 = g.m1 + (f.max_tiles1 + f3::kGroup - 1) / f3::kGroup;
-      A.maxg2 = g.m2 + (f.max_tiles2 + f3::kGroup - 1) / f3::kGroup;
-      A.nbwd = grid1;
-      const int ng0 = (grid1 + f3::kGroup0 - 1) / f3::kGroup0;
-      const int tasks = A.maxg1 * C1c + A.maxg2 * C2c + g.m0 * ng0 * C0c;  // one warp each
-      const int ncnt = g.m1 * C1c + g.m2 * C2c + g.m0 * C0c;
-      if (f.counters.cap < 4 * static_cast<size_t>(ncnt)) {
-        f.counters.ensure(4 * static_cast<size_t>(ncnt));
-        CK(cudaMemsetAsync(f.counters.p, 0, f.counters.cap, st));
-      }
-      f.gpart.ensure(4 * 128 * static_cast<size_t>(tasks));
-      f.gtouch.ensure(4 * static_cast<size_t>(tasks));
-      A.gpart = f.gpart.as<float>();
-      A.gtouch = f.gtouch.as<int>();
-      A.counters = f.counters.as<int>();
       auto ck = mode == 1 ? f3::f3_combine<D, 1> : f3::f3_combine<D, 0>;
       const size_t csm = 4 * static_cast<size_t>(g.m1 + 1 + g.m2 + 1);
       set_smem(ck, csm);
-      f3_launch(t->pdl, ck, dim3((tasks * 32 + f3::kThreads - 1) / f3::kThreads), dim3(f3::kThreads), csm, st, 
-          g, t->cores.as<float>(), t->grads.as<float>(), A, lr);
+      f3_launch(t->pdl, ck, dim3((tasks * 32 + f3::kThreads - 1) / f3::kThreads), dim3(f3::kThreads), csm, st,
+                g, t->cores.as<float>(), t->grads.as<float>(), A, lr);
     }
     t->mark("f3_combine");
     CK(cudaGetLastError());
