@@ -97,6 +97,12 @@ def kernel_work(name, rf, cf, ranks, L, B, N, params):
         "f3_bwd2": (L * tail, idx_b + 4 * B * N),
         "f3_combine": (2 * params, 3 * 4 * params),
         "pool": (2 * L * N, 4 * L * N + 8 * (B + 1) + 4 * B * N),
+        # cfg3's wide-row phases (wide3.cuh; per-lookup tail work, no dedup):
+        # bwd_S = k_w3_bwd_pairs: D1 (S) and the dG2 contribution per lookup;
+        # bytes: grad row in, contribution row out, indices
+        "bwd_S": (L * 2 * tail, idx_b + 4 * L * N + 4 * L * R2 * n2),
+        # tail_pool = k_w3_fwd + pooling: y per lookup, y rows out and back, pooled rows
+        "tail_pool": (L * tail + 2 * L * N, idx_b + 2 * 4 * L * N + 4 * B * N),
     }
     return table.get(name)
 
