@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
 // S rows land at the slot's position (start + s), kappa-major: row s holds
 // S[a0][c] at a0*C1 + c == a*R2 + r, so f3_bwd1 can bulk-copy a tile's rows.
 template <class D>
-__device__ __forceinline__ void srows_body(int vblock, const float* __restrict__ cores, int64_t coff2,
+__device__ __forceinline__ void srows_tile(int t, const float* __restrict__ cores, int64_t coff2,
                                            const Tile* __restrict__ tiles,
                                            const int* __restrict__ ntiles, int max_tiles,
                                            const uint32_t* __restrict__ perm,
@@ -820,7 +820,6 @@ __device__ __forceinline__ void srows_body(int vblock, const float* __restrict__
   static_assert(D::R2 <= 32 ? 32 % D::R2 == 0 : D::R2 % 32 == 0, "lane -> rank column map");
   constexpr int U = 8;  // members with G2 loads in flight
   const int lane = threadIdx.x & 31;
-  const int t = static_cast<int>((vblock * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
   if (t >= max_tiles) return;
   // the tile count and this tile's descriptor in one round trip (entries past
   // the count are in bounds, just unused)
@@ -944,6 +943,28 @@ __device__ __forceinline__ void srows_body(int vblock, const float* __restrict__
 #pragma unroll
     for (int k = 0; k < EPL; ++k)
       if (lane + 32 * k < D::W1) dst[lane + 32 * k] = acc[k];
+  }
+}
+
+// warps of virtual CTAs [vblock, ...) walk the i1-tiles grid-stride (vgrid
+// virtual CTAs in all); the per-warp shared rows are reused tile to tile
+template <class D>
+__device__ __forceinline__ void srows_body(int vblock, int vgrid, const float* __restrict__ cores,
+                                           int64_t coff2, const Tile* __restrict__ tiles,
+                                           const int* __restrict__ ntiles, int max_tiles,
+                                           const uint32_t* __restrict__ perm,
+                                           const uint16_t* __restrict__ d2,
+                                           const int32_t* __restrict__ lk_bag,
+                                           const float* __restrict__ alpha,
+                                           const float* __restrict__ grad,
+                                           const uint16_t* __restrict__ slot_of_pos,
+                                           const int* __restrict__ tile_nslots,
+                                           float* __restrict__ Sbuf) {
+  const int nw = blockDim.x >> 5;
+  for (int t = vblock * nw + (threadIdx.x >> 5); t < max_tiles; t += vgrid * nw) {
+    srows_tile<D>(t, cores, coff2, tiles, ntiles, max_tiles, perm, d2, lk_bag, alpha, grad, slot_of_pos,
+                  tile_nslots, Sbuf);
+    __syncwarp();
   }
 }
 
@@ -1407,8 +1428,8 @@ __global__ void __launch_bounds__(256, 2) f3_srows(const float* __restrict__ cor
                                                 const int* __restrict__ tile_nslots,
                                                 float* __restrict__ Sbuf) {
   pdl_entry();
-  srows_body<D>(blockIdx.x, cores, coff2, tiles, ntiles, max_tiles, perm, d2, lk_bag, alpha, grad,
-                slot_of_pos, tile_nslots, Sbuf);
+  srows_body<D>(blockIdx.x, gridDim.x, cores, coff2, tiles, ntiles, max_tiles, perm, d2, lk_bag, alpha,
+                grad, slot_of_pos, tile_nslots, Sbuf);
 }
 
 template <class D>
@@ -1467,7 +1488,7 @@ __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Ar
     bwd2_body<D>(idx, nb2, g, ba.tiles, ba.ntiles, ba.perm, ba.hloc, lk_bag, alpha, grad, ba.Hbuf,
                  ba.part2, ba.has2);
   else
-    srows_body<D>(idx, sa.cores, sa.coff2, sa.tiles, sa.ntiles, sa.max_tiles, sa.perm, sa.d2, lk_bag,
+    srows_body<D>(idx, nbs, sa.cores, sa.coff2, sa.tiles, sa.ntiles, sa.max_tiles, sa.perm, sa.d2, lk_bag,
                   alpha, grad, sa.slot_of_pos, sa.tile_nslots, sa.Sbuf);
 }
 

@@ -394,7 +394,14 @@ struct F3Runner {
                        f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>()};
       f3::Bwd2Args ba{f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, f.perm2.as<uint32_t>(),
                       f.hloc.as<uint32_t>(), f.Hbuf.as<float>(), f.part2.as<float>(), f.has2.as<int>()};
-      const int nbs = (f.max_tiles1 * 32 + 127) / 128;
+      // srows warps walk the tiles grid-stride: TTGPU_SROWS_CTAS_PER_SM virtual
+      // CTAs per SM (0 = one warp per tile)
+      static const int srows_per_sm = [] {
+        const char* e = std::getenv("TTGPU_SROWS_CTAS_PER_SM");
+        return e ? std::atoi(e) : 0;
+      }();
+      const int nbs_all = (f.max_tiles1 * 32 + 127) / 128;
+      const int nbs = srows_per_sm > 0 ? std::min(nbs_all, t->num_sms * srows_per_sm) : nbs_all;
       f3_launch(t->pdl, f3::f3_srows_bwd2<D>, dim3(grid2 + nbs), dim3(128), 0, st, g, sa, ba, grid2, nbs,
                 lk_bag, alpha, grad);
       t->mark("f3_srows_bwd2");
