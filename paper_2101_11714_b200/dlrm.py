@@ -21,7 +21,14 @@ Shapes and semantics follow the reference:
 
 Parameters can be loaded from (and compared with) the reference model through
 the `set_*` / getter methods; `init` draws fresh parameters with the
-reference's distributions (not its RNG streams)."""
+reference's distributions (not its RNG streams).
+
+Data parallel (`group` with world > 1): every rank trains its
+shard of the batch with replicated parameters.  dlogits are scaled by the
+GLOBAL batch size, every gradient -- both MLPs, every TT table's dense core
+gradient, every uncompressed table's row gradient -- goes into ONE flat buffer
+and one allreduce(SUM), then the identical SGD on every replica: the update of
+the full-batch step."""
 from __future__ import annotations
 
 from typing import List, Sequence, Tuple
@@ -34,7 +41,8 @@ from .ttrec import ForwardContext, TtTable, plan_shapes
 
 class DlrmModel:
     def __init__(self, dense_features: int, emb_dim: int, tables: Sequence[Tuple[int, bool, int]],
-                 bottom: Sequence[int], top: Sequence[int], dot: bool = True, device: int = 0):
+                 bottom: Sequence[int], top: Sequence[int], dot: bool = True, device: int = 0,
+                 group=None, data_parallel: bool = True):
         """tables: (rows, use_tt, rank) per categorical feature (TableConfig,
         model.hpp:23-31; a TT table gets plan_shapes(rows, emb_dim, 3, rank))."""
         import torch
@@ -47,6 +55,11 @@ class DlrmModel:
             raise ValueError("top MLP must end in a single logit")
         torch.backends.cuda.matmul.allow_tf32 = False
         self.torch = torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = (dist.get_world_size(group)
+                      if data_parallel and dist.is_available() and dist.is_initialized() else 1)
         self.dev = torch.device("cuda", device)
         self.stream = torch.cuda.Stream(device=self.dev)
         self.df, self.emb, self.dot = int(dense_features), int(emb_dim), bool(dot)
@@ -175,15 +188,16 @@ class DlrmModel:
             return logits.reshape(bs)
 
     @staticmethod
-    def bce_with_logits(logits, labels):
-        """model.hpp:82-103 in float64: (mean loss, dlogits as float32)."""
+    def bce_with_logits(logits, labels, n=None):
+        """model.hpp:82-103 in float64: (mean loss, dlogits as float32); n is the
+        batch the mean is over (the global batch under data parallelism)."""
         import torch
 
         x = logits.double()
         y = labels
         total = torch.clamp(x, min=0) - x * y + torch.log1p(torch.exp(-x.abs()))
         sig = torch.where(x >= 0, 1.0 / (1.0 + torch.exp(-x)), torch.exp(x) / (1.0 + torch.exp(x)))
-        n = x.numel()
+        n = x.numel() if n is None else n
         return total.sum() / n, ((sig - y) / n).float()
 
     def backward(self, mb, dlogits, fused_lr: float = None):
@@ -228,12 +242,56 @@ class DlrmModel:
                 for t, tab in enumerate(self.tables):
                     tab.apply_grad(lr)
 
+    def _grad_tensors(self):
+        """Every gradient buffer (device tensors / views), in a fixed order."""
+        torch = self.torch
+        out = []
+        for layers in (self.bottom, self.top):
+            for L in layers:
+                out += [L["gw"], L["gb"]]
+        for t, tab in enumerate(self.tables):
+            ptr, n = tab.grad_buffer()
+
+            class _Arr:
+                __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                            "version": 3, "strides": None}
+
+            out.append(torch.as_tensor(_Arr(), device=self.dev))
+        return out
+
+    def allreduce_grads(self):
+        """One flat allreduce(SUM) of every gradient (data parallel)."""
+        import torch.distributed as dist
+
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            gs = self._grad_tensors()
+            flat = torch.cat([g.reshape(-1) for g in gs])
+            dist.all_reduce(flat, group=self.group)
+            o = 0
+            for g in gs:
+                n = g.numel()
+                g.copy_(flat[o:o + n].view_as(g))
+                o += n
+
     def train_step(self, mb, lr: float, fused: bool = True):
         """One train() iteration: forward, BCE, backward, step.  Returns the
-        logits (device) and the loss (device float64 scalar)."""
+        logits (device) and the loss (device float64 scalar; the global mean
+        under data parallelism)."""
+        torch = self.torch
         logits = self.forward(mb)
-        with self.torch.cuda.stream(self.stream):
-            loss, dlogits = self.bce_with_logits(logits, mb["labels"])
+        n = logits.numel() * self.world
+        with torch.cuda.stream(self.stream):
+            loss, dlogits = self.bce_with_logits(logits, mb["labels"], n)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            self.backward(mb, dlogits)  # dense gradients (every table's buffer)
+            self.allreduce_grads()
+            self.step(lr)
+            with torch.cuda.stream(self.stream):
+                dist.all_reduce(loss, group=self.group)
+            return logits, loss
         self.backward(mb, dlogits, fused_lr=lr if fused else None)
         self.step(lr, tables_done=fused)
         return logits, loss
