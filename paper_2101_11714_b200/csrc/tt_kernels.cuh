@@ -276,6 +276,16 @@ __global__ void k_pair_i1(const uint32_t* __restrict__ pair_key_u, const int* __
 // H[pid] = G0[i0] (P0 x R1) · G1[i1] (R1 x C1) for every unique pair.  Pairs
 // are processed in chunks of CH; G1[i1] is staged in shared memory once per
 // i1 run inside the chunk (pairs are i1-major, so runs are long).
+__device__ __forceinline__ void cp_async16_g(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 template <typename T, bool kExact>
 __global__ void k_head_fwd(DevPlan P, const T* __restrict__ cores,
                            const uint32_t* __restrict__ pair_key_u,
@@ -289,13 +299,30 @@ __global__ void k_head_fwd(DevPlan P, const T* __restrict__ cores,
   const T* G0 = cores + P.coff[0];
   const T* G1 = cores + P.coff[1];
   const int nchunks = (U + CH - 1) / CH;
-  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  // contiguous chunk ranges per CTA: consecutive chunks usually share i1 (pairs
+  // are i1-major), so the staged G1[i1] is reused across them
+  const int ch_lo = static_cast<int>(static_cast<int64_t>(blockIdx.x) * nchunks / gridDim.x);
+  const int ch_hi = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * nchunks / gridDim.x);
+  // fp32 operands with 16-byte rows are staged by cp.async (no register round trip)
+  bool async16 = false;
+  if constexpr (std::is_same_v<T, float>) async16 = (s0 % 4) == 0 && (s1 % 4) == 0;
+  uint32_t staged_i1 = 0xffffffffu;
+  for (int ch = ch_lo; ch < ch_hi; ++ch) {
     const int p0 = ch * CH, p1 = min(U, p0 + CH);
     __syncthreads();
-    for (int e = threadIdx.x; e < (p1 - p0) * s0; e += blockDim.x) {
-      const int q = e / s0;
-      const uint32_t i0 = pair_key_u[p0 + q] % static_cast<uint32_t>(P.m[0]);
-      g0s[e] = G0[i0 * s0 + (e - q * s0)];
+    if (async16) {
+      const int q4 = s0 / 4;
+      for (int e = threadIdx.x; e < (p1 - p0) * q4; e += blockDim.x) {
+        const int q = e / q4;
+        const uint32_t i0 = pair_key_u[p0 + q] % static_cast<uint32_t>(P.m[0]);
+        cp_async16_g(g0s + 4 * e, G0 + static_cast<int64_t>(i0) * s0 + 4 * (e - q * q4));
+      }
+    } else {
+      for (int e = threadIdx.x; e < (p1 - p0) * s0; e += blockDim.x) {
+        const int q = e / s0;
+        const uint32_t i0 = pair_key_u[p0 + q] % static_cast<uint32_t>(P.m[0]);
+        g0s[e] = G0[i0 * s0 + (e - q * s0)];
+      }
     }
     int run_lo = p0;
     while (run_lo < p1) {
@@ -303,7 +330,16 @@ __global__ void k_head_fwd(DevPlan P, const T* __restrict__ cores,
       int run_hi = run_lo + 1;
       while (run_hi < p1 && pair_key_u[run_hi] / static_cast<uint32_t>(P.m[0]) == i1) ++run_hi;
       __syncthreads();
-      for (int e = threadIdx.x; e < s1; e += blockDim.x) g1s[e] = G1[(int64_t)i1 * s1 + e];
+      if (i1 != staged_i1) {
+        if (async16) {
+          for (int e = threadIdx.x; e < s1 / 4; e += blockDim.x)
+            cp_async16_g(g1s + 4 * e, G1 + static_cast<int64_t>(i1) * s1 + 4 * e);
+        } else {
+          for (int e = threadIdx.x; e < s1; e += blockDim.x) g1s[e] = G1[(int64_t)i1 * s1 + e];
+        }
+        staged_i1 = i1;
+      }
+      if (async16) cp_async_wait_all();
       __syncthreads();
       const int outs = P0 * C1;
       bool quad_done = false, block4 = false;
