@@ -87,7 +87,15 @@ void launch_gsort(const ttgpu_table* t, int G, size_t smem, const f3::GsortArgs&
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort, a));
+  const int rounds = a.PW / 32;
+  if (rounds <= 1)
+    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<1>, a));
+  else if (rounds <= 2)
+    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<2>, a));
+  else if (rounds <= 4)
+    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<4>, a));
+  else
+    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<8>, a));
 }
 
 template <class K>
@@ -130,9 +138,13 @@ void gsort_grid(const ttgpu_table* t, const f3::Geo& g, int64_t L, int K3, int* 
   if (!t->grid_sort || g.m1 + g.m2 > 4 * f3::kGsThreads || K3 > 8 * f3::kGsThreads ||
       gs_smem > 160 * 1024)
     return;
-  set_smem(f3::f3_gsort, std::max<size_t>(gs_smem, f3::gsort_smem_bytes(g.m1, g.m2)));
-  int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort, f3::kGsThreads, gs_smem));
+  const size_t gsm = std::max<size_t>(gs_smem, f3::gsort_smem_bytes(g.m1, g.m2));
+  set_smem(f3::f3_gsort<1>, gsm);
+  set_smem(f3::f3_gsort<2>, gsm);
+  set_smem(f3::f3_gsort<4>, gsm);
+  set_smem(f3::f3_gsort<8>, gsm);
+  int occ = 0;  // the widest variant bounds the co-resident grid
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort<8>, f3::kGsThreads, gs_smem));
   const int64_t cap = std::min<int64_t>(32 * f3::kGsMaxGridChunks,
                                         static_cast<int64_t>(t->num_sms) * std::max(occ, 0));
   const int64_t per = 16 * 32;  // lookups per CTA round

@@ -124,7 +124,12 @@ __device__ __forceinline__ uint32_t div_fix(uint32_t x, uint32_t d, double inv, 
   return q;
 }
 
+// RMAX: rounds (lookups per thread) compiled in -- the host picks the smallest
+// power of two >= the batch's rounds, so a one-round batch (cfg2) runs a
+// kernel without the unrolled code of eight (instruction-cache pressure)
+template <int RMAX>
 __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
+  constexpr int QC = RMAX < 4 ? RMAX : 4;  // rounds whose index loads are batched
   namespace cg = cooperative_groups;
   const int c = blockIdx.x, G = gridDim.x;
   const int K1 = a.g.m1, K2 = a.g.m2, K12 = K1 + K2, K3 = a.K3, K = K12 + K3;
@@ -153,22 +158,22 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   for (int i = tid; i < kGsWarps * K; i += kGsThreads) wc[i] = 0u;
   // per round: k1 = i1 (0xffffffff: no lookup), d02 = i0 | i2 << 16
   // cached lookups: k1 = 0x80000000 | slot
-  uint32_t k1[kGsMaxRounds], d02[kGsMaxRounds];
+  uint32_t k1[RMAX], d02[RMAX];
   uint32_t* mywc = wc + wid * K;
   unsigned my_hits = 0;
   __shared__ unsigned cta_hits;
   if (tid == 0) cta_hits = 0u;
 #pragma unroll
-  for (int q0 = 0; q0 < kGsMaxRounds; q0 += 4) {
-    int64_t rows[4];
+  for (int q0 = 0; q0 < RMAX; q0 += QC) {
+    int64_t rows[QC];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < QC; ++u) {
       const int64_t l = wbase + (q0 + u) * 32 + lane;
       rows[u] = (q0 + u < R && l < a.L) ? a.idx[l] : 0;
     }
     if (q0 == 0) __syncthreads();  // counters zeroed
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < QC; ++u) {
       const int q = q0 + u;
       k1[q] = 0xffffffffu;
       d02[q] = 0u;
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   // ---- phase C: stable scatter of both keys
   const unsigned lt = lanemask_lt();
 #pragma unroll
-  for (int q = 0; q < kGsMaxRounds; ++q) {
+  for (int q = 0; q < RMAX; ++q) {
     if (q < R) {
       const int64_t l = wbase + q * 32 + lane;
       const bool tt = k1[q] < 0x80000000u;
