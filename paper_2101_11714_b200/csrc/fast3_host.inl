@@ -88,14 +88,12 @@ void launch_gsort(const ttgpu_table* t, int G, size_t smem, const f3::GsortArgs&
   cfg.attrs = at;
   cfg.numAttrs = 1;
   const int rounds = a.PW / 32;
-  if (rounds <= 1)
-    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<1>, a));
-  else if (rounds <= 2)
-    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<2>, a));
-  else if (rounds <= 4)
-    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<4>, a));
-  else
-    CK(cudaLaunchKernelEx(&cfg, f3::f3_gsort<8>, a));
+  const bool cache = a.K3 > 0 || a.counts != nullptr;
+  auto kern = rounds <= 1 ? (cache ? f3::f3_gsort<1, true> : f3::f3_gsort<1, false>)
+            : rounds <= 2 ? (cache ? f3::f3_gsort<2, true> : f3::f3_gsort<2, false>)
+            : rounds <= 4 ? (cache ? f3::f3_gsort<4, true> : f3::f3_gsort<4, false>)
+                          : (cache ? f3::f3_gsort<8, true> : f3::f3_gsort<8, false>);
+  CK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
 template <class K>
@@ -139,12 +137,16 @@ void gsort_grid(const ttgpu_table* t, const f3::Geo& g, int64_t L, int K3, int* 
       gs_smem > 160 * 1024)
     return;
   const size_t gsm = std::max<size_t>(gs_smem, f3::gsort_smem_bytes(g.m1, g.m2));
-  set_smem(f3::f3_gsort<1>, gsm);
-  set_smem(f3::f3_gsort<2>, gsm);
-  set_smem(f3::f3_gsort<4>, gsm);
-  set_smem(f3::f3_gsort<8>, gsm);
+  set_smem(f3::f3_gsort<1, false>, gsm);
+  set_smem(f3::f3_gsort<2, false>, gsm);
+  set_smem(f3::f3_gsort<4, false>, gsm);
+  set_smem(f3::f3_gsort<8, false>, gsm);
+  set_smem(f3::f3_gsort<1, true>, gsm);
+  set_smem(f3::f3_gsort<2, true>, gsm);
+  set_smem(f3::f3_gsort<4, true>, gsm);
+  set_smem(f3::f3_gsort<8, true>, gsm);
   int occ = 0;  // the widest variant bounds the co-resident grid
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort<8>, f3::kGsThreads, gs_smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f3::f3_gsort<8, true>, f3::kGsThreads, gs_smem));
   const int64_t cap = std::min<int64_t>(32 * f3::kGsMaxGridChunks,
                                         static_cast<int64_t>(t->num_sms) * std::max(occ, 0));
   const int64_t per = 16 * 32;  // lookups per CTA round

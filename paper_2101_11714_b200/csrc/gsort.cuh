@@ -126,13 +126,14 @@ __device__ __forceinline__ uint32_t div_fix(uint32_t x, uint32_t d, double inv, 
 
 // RMAX: rounds (lookups per thread) compiled in -- the host picks the smallest
 // power of two >= the batch's rounds, so a one-round batch (cfg2) runs a
-// kernel without the unrolled code of eight (instruction-cache pressure)
-template <int RMAX>
+// kernel without the unrolled code of eight (instruction-cache pressure);
+// kCache: the LFU cache code (key 3) compiled in only where a cache is used
+template <int RMAX, bool kCache>
 __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   constexpr int QC = RMAX < 4 ? RMAX : 4;  // rounds whose index loads are batched
   namespace cg = cooperative_groups;
   const int c = blockIdx.x, G = gridDim.x;
-  const int K1 = a.g.m1, K2 = a.g.m2, K12 = K1 + K2, K3 = a.K3, K = K12 + K3;
+  const int K1 = a.g.m1, K2 = a.g.m2, K12 = K1 + K2, K3 = kCache ? a.K3 : 0, K = K12 + K3;
   extern __shared__ __align__(16) uint32_t gs_sm[];
   uint32_t* wc = gs_sm;                  // [16][K] per-warp counts -> per-warp starts
   uint32_t* ctot = wc + kGsWarps * K;    // [K] this CTA's count per key
@@ -188,18 +189,18 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
         }
         if (!ok) row = 0;
         int slot = -1;
-        if (a.active && ok)
+        if (kCache && a.active && ok)
           slot = lfu::probe(a.hkeys, a.hvals, a.hshift, a.hmask, static_cast<unsigned long long>(row));
         // FreqTable::increment: chain rows warp-aggregated here; the cached (hot)
         // rows once per CTA from the slot counts below (no same-address storm)
-        if (a.counts) {
+        if (kCache && a.counts) {
           const unsigned long long key = ok && slot < 0 ? static_cast<unsigned long long>(row) : ~0ull;
           const unsigned pr = __match_any_sync(0xffffffffu, key);
           if (key != ~0ull && lane == __ffs(pr) - 1)
             atomicAdd(a.counts + row, static_cast<unsigned long long>(__popc(pr)));
         }
         if (in) {
-          if (a.lk_slot) a.lk_slot[l] = slot;
+          if (kCache && a.lk_slot) a.lk_slot[l] = slot;
           if (slot >= 0) {
             k1[q] = 0x80000000u | static_cast<uint32_t>(slot);
             ++my_hits;
@@ -280,15 +281,15 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       a.alpha[l] = static_cast<float>(al);
     }
   }
-  if (a.hits) {
+  if (kCache && a.hits) {
     unsigned h = my_hits;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
     if (lane == 0 && h) atomicAdd(&cta_hits, h);
   }
   __syncthreads();
-  if (a.accesses && c == 0 && tid == 0) atomicAdd(a.accesses, static_cast<unsigned long long>(a.L));
-  if (a.hits && tid == 0 && cta_hits) {
+  if (kCache && a.accesses && c == 0 && tid == 0) atomicAdd(a.accesses, static_cast<unsigned long long>(a.L));
+  if (kCache && a.hits && tid == 0 && cta_hits) {
     atomicAdd(a.hits, static_cast<unsigned long long>(cta_hits));
     if (a.hits2) atomicAdd(a.hits2, static_cast<unsigned long long>(cta_hits));
   }
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   // model.hpp:210-223 with an empty chain part); a bag with chain lookups
   // presets its pooling counter with its cached lookups, so its last chain
   // lookup pools it in f3_fwd (pool_if_last)
-  if (a.K3 && need_c) {
+  if (kCache && K3 && need_c) {
     for (int64_t b = static_cast<int64_t>(c) * kGsThreads + tid; b < a.B;
          b += static_cast<int64_t>(G) * kGsThreads) {
       const int64_t s = a.off[b], e = a.off[b + 1];
