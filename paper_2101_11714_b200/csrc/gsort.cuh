@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
   // pooled here; any other bag sets need_c and is handled after the grid
   // barriers, when every lookup's slot is visible
   bool need_c = false;
+  int32_t loc_bag = -1;  // bag of this thread's first-round lookup when it is a single-lookup bag
+  float loc_alpha = 0.f;
   for (int64_t b = b_first; b < a.B; b += static_cast<int64_t>(G) * kGsThreads) {
     const int64_t s = b == b_first ? s_first : a.off[b], e = b == b_first ? e_first : a.off[b + 1];
     if (b == 0 && s != 0) atomicOr(a.errs, 1);
@@ -251,6 +253,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       a.solo[lo] = static_cast<int32_t>(b);
       const float wl = a.w ? static_cast<float>(a.w[lo]) : 1.f;
       a.alpha[lo] = wl;
+      if (lo == wbase + lane) {  // this thread's own first-round lookup: keep it for phase C
+        loc_bag = static_cast<int32_t>(b);
+        loc_alpha = wl;
+      }
       if (K3) {
         if (lo == wbase + lane && k1[0] != 0xffffffffu) {
           if (k1[0] >= 0x80000000u) {  // cached: out = (0 + w·row) + 0
@@ -530,8 +536,12 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       if (tt) {
         const uint32_t pos = base[x] + mywc[x] + __popc(p & lt);
         a.perm1[pos] = static_cast<uint32_t>(l);
-        a.rec1[pos] = make_rec(static_cast<uint32_t>(l), d02[q], __ldcg(a.solo + l), __ldcg(a.lk_bag + l),
-                               __ldcg(a.alpha + l));
+        // the bag fields of a lookup whose single-lookup bag this thread set
+        // up are in registers; others were written by another thread (phase A)
+        a.rec1[pos] = q == 0 && loc_bag >= 0
+                          ? make_rec(static_cast<uint32_t>(l), d02[q], loc_bag, loc_bag, loc_alpha)
+                          : make_rec(static_cast<uint32_t>(l), d02[q], __ldcg(a.solo + l),
+                                     __ldcg(a.lk_bag + l), __ldcg(a.alpha + l));
       }
       __syncwarp();
       if (tt && lane == __ffs(p) - 1) mywc[x] += __popc(p);
