@@ -207,6 +207,9 @@ int ttgpu_cache_record(ttgpu_cache* c, const int64_t* indices, int64_t L);   /* 
 int ttgpu_cache_record_and_partition(ttgpu_cache* c, const int64_t* indices, int64_t L,
                                      const int64_t* offsets, int64_t B, const double* weights,
                                      int pooling, int64_t* n_cached, int64_t* n_tt);
+/* After a fast-path cached forward (ttgpu_cache_set_fast) the partition is rebuilt
+ * from the per-lookup slots and the forward's own index / offset / weight arrays:
+ * for ttgpu_cache_forward_device those device arrays must still be alive. */
 int ttgpu_cache_last_partition(ttgpu_cache* c, int64_t* cached_slots, int64_t* cached_rows,
                                int64_t* cached_offsets, double* cached_weights, int64_t* tt_indices,
                                int64_t* tt_offsets, double* tt_weights);
