@@ -1,7 +1,8 @@
 // Fast path for 3-core tables (every BASELINE config): compile-time TT shape,
-// 6 kernels per fwd+bwd+SGD step (f3_gsort, gsort.cuh, replaces the first
-// three below when the batch fits one co-resident grid), deterministic, no
-// floating-point atomics.
+// 5 kernels per fwd+bwd+SGD step -- f3_gsort (gsort.cuh, replaces the first
+// three below when the batch fits one co-resident grid), f3_fwd,
+// f3_srows_bwd2 (f3_srows and f3_bwd2 in one launch), f3_bwd1, f3_combine --
+// deterministic, no floating-point atomics.
 //
 //   f3_hist     decode + validate; per-CTA histograms of two sort keys
 //               (k1 = i1, k2 = i2); lookup->bag map, backward alpha, solo bags
