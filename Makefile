@@ -10,10 +10,19 @@ NVFLAGS  := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -shared -Xptxas -v
 SRCS     := $(CSRC)/ttgpu.cu $(CSRC)/shape_plan.cpp
 HDRS     := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) $(wildcard $(CSRC)/*.inl) include/ttgpu.h
 
-.PHONY: all lib oracle clean
+DIAG     := $(PKG)/lib/libttgpu_diag.so
+
+.PHONY: all lib lib-diag oracle clean
 all: lib oracle
 
 lib: $(LIB)
+
+# diagnostics build: per-CTA timelines (bench.py --cta-times, TTGPU_LIB=$(DIAG))
+lib-diag: $(DIAG)
+
+$(DIAG): $(SRCS) $(HDRS)
+	mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -DTTGPU_CTA_TIMES -o $@ $(SRCS) 2> $(PKG)/lib/ptxas_diag.log || (cat $(PKG)/lib/ptxas_diag.log; false)
 
 $(LIB): $(SRCS) $(HDRS)
 	mkdir -p $(PKG)/lib
@@ -23,5 +32,5 @@ oracle:
 	$(MAKE) -C oracle all
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(DIAG)
 	$(MAKE) -C oracle clean

@@ -161,6 +161,47 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def cta_timeline(path, run, flush, stream):
+    """Diagnostic (outside every timed region): one graph replay with the
+    per-CTA entry / exit timers of the five fast-path kernels enabled
+    (ttgpu_debug_cta_times), saved raw to `path` and summarised on stderr."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2101_11714_b200._lib import lib
+
+    names = ["f3_gsort", "f3_fwd", "f3_srows_bwd2", "f3_bwd1", "f3_combine"]
+    bufs = [torch.zeros(8 * 8192, dtype=torch.int64, device="cuda") for _ in names]
+    for k, b in enumerate(bufs):
+        assert lib().ttgpu_debug_cta_times(k, C.c_void_p(b.data_ptr())) == 0
+    with torch.cuda.stream(stream):
+        flush.fill_(3)
+        run()
+    stream.synchronize()
+    for k in range(len(names)):
+        lib().ttgpu_debug_cta_times(k, None)
+    out = {}
+    t0 = None
+    for name, b in zip(names, bufs):
+        a = b.view(-1, 8).cpu().numpy()
+        a = a[a[:, 0] > 0]
+        out[name] = a
+        if len(a) and (t0 is None or a[:, 0].min() < t0):
+            t0 = a[:, 0].min()
+    np.savez(path, **out)
+    for name in names:
+        a = out[name]
+        if not len(a):
+            continue
+        st, en = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3
+        d = en - st
+        print(f"[cta] {name:14s} ctas {len(a):5d} span {st.min():7.2f}..{en.max():7.2f} us  "
+              f"dur mean {d.mean():6.2f} p50 {np.median(d):6.2f} p90 {np.percentile(d, 90):6.2f} "
+              f"max {d.max():6.2f}  last-start {st.max():7.2f}  end p50 {np.median(en):7.2f}",
+              file=sys.stderr)
+
+
 def make_inputs(cfg, seed, tt):
     if cfg["zipf"] > 0:
         b = tt.generate_zipfian_batch(cfg["rows"], cfg["zipf"], seed, cfg["bags"], cfg["pf"])
@@ -509,6 +550,10 @@ def main():
     ap.add_argument("--nccl", action="store_true",
                     help="N>1: NCCL allreduce + SGD kernel instead of the fused peer reduce+SGD")
     ap.add_argument("--profile", action="store_true", help="print per-phase times")
+    ap.add_argument("--cta-times", default=None,
+                    help="diagnostic: after the timed region, record one step's per-CTA "
+                         "timeline of the fast-path kernels into this .npz (needs the "
+                         "diagnostics build: make lib-diag, TTGPU_LIB=.../libttgpu_diag.so)")
     ap.add_argument("--cache-partition", action="store_true",
                     help="cfg4: the explicit partition path (eager) instead of the cache fast path")
     args = ap.parse_args()
@@ -778,6 +823,8 @@ def main():
                 agg.setdefault(name, []).append(ms)
     table.profile(False)
     phase_ms = {k: float(np.mean(v)) for k, v in agg.items()}
+    if args.cta_times and rank == 0:
+        cta_timeline(args.cta_times, run, flush, stream)
     dom = max(phase_ms, key=phase_ms.get)
 
     # e2e through the host C ABI: pinned host buffers, copies inside the region

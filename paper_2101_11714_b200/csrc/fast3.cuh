@@ -44,6 +44,51 @@ namespace f3 {
 // as soon as every CTA of this one has started.
 __device__ __forceinline__ void pdl_entry() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Diagnostics: per-CTA timeline of the fast-path kernels (ttgpu_debug_cta_times),
+// compiled in only with -DTTGPU_CTA_TIMES (`make lib-diag`: the reads of the
+// pointer table at CTA entry would otherwise cost every kernel a dependent
+// global load).  When g_cta_times[kid] is set, thread 0 of every CTA records
+// the global timer at entry and at its own exit, the SM id, a kernel-specific
+// work note and up to four intermediate marks: u64 [blockIdx][8].
+__device__ unsigned long long* g_cta_times[8];
+#ifdef TTGPU_CTA_TIMES
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct CtaClock {
+  unsigned long long* p;
+  __device__ __forceinline__ explicit CtaClock(int kid) {
+    p = threadIdx.x == 0 ? g_cta_times[kid] : nullptr;
+    if (p) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p += 8 * static_cast<size_t>(blockIdx.x);
+      p[0] = gtimer();
+      p[2] = smid;
+    }
+  }
+  __device__ __forceinline__ ~CtaClock() {
+    if (p) p[1] = gtimer();
+  }
+};
+__device__ __forceinline__ void cta_note(int kid, unsigned long long v) {
+  unsigned long long* p = threadIdx.x == 0 ? g_cta_times[kid] : nullptr;
+  if (p) p[8 * static_cast<size_t>(blockIdx.x) + 3] = v;
+}
+__device__ __forceinline__ void cta_mark(int kid, int m) {  // m in 0..3
+  unsigned long long* p = threadIdx.x == 0 ? g_cta_times[kid] : nullptr;
+  if (p) p[8 * static_cast<size_t>(blockIdx.x) + 4 + m] = gtimer();
+}
+#else
+struct CtaClock {
+  __device__ __forceinline__ explicit CtaClock(int) {}
+};
+__device__ __forceinline__ void cta_note(int, unsigned long long) {}
+__device__ __forceinline__ void cta_mark(int, int) {}
+#endif
+
 struct Geo {
   int m0, m1, m2;
   uint32_t m12;  // m1 * m2
@@ -631,6 +676,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    int* __restrict__ bag_cnt,
                                                    const int* __restrict__ cache_slot,
                                                    const float* __restrict__ store) {
+  CtaClock clk_(1);
   pdl_entry();
   using SM = FwdSmem<D>;
   extern __shared__ __align__(128) float sm[];
@@ -1090,6 +1136,8 @@ __device__ __forceinline__ void bwd1_body(
     t_lo = range[0];
     t_hi = range[1] > range[0] ? range[1] : range[0];
   }
+  unsigned long long note_ns = 0, note_runs = 0;  // diagnostics (cta_note)
+  cta_mark(3, 0);
   float* d0acc = D0acc + static_cast<int64_t>(blockIdx.x) * g.m0 * D::S0;
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
@@ -1163,6 +1211,10 @@ __device__ __forceinline__ void bwd1_body(
         q_ns = tile_nslots[t + NS + 1];
       }
     }
+#ifdef TTGPU_CTA_TIMES
+    note_ns += nslots;
+    note_runs += i1 != cur_i1;
+#endif
     if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
       constexpr int U = 8;
@@ -1189,6 +1241,7 @@ __device__ __forceinline__ void bwd1_body(
       if (!(old & bit)) d0m[i0] = 1;
     }
     mbar_wait(bar + st, parity);
+    if (t == t_lo) cta_mark(3, 1);
     __syncthreads();  // G1t staged, d0first set, bulk data visible
     // ---- dG1 partial += Σ_kappa G0s[kappa][r1] (x) S[kappa][c]
     if (g1_on) {
@@ -1273,6 +1326,8 @@ __device__ __forceinline__ void bwd1_body(
       run_start = t + 1;
     }
   }
+  cta_mark(3, 2);
+  cta_note(3, static_cast<unsigned long long>(t_hi - t_lo) | (note_ns << 16) | (note_runs << 40));
 }
 
 // ------------------------------------------------------------ f3_bwd2 ----
@@ -1474,6 +1529,7 @@ __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Ar
                                                     const int32_t* __restrict__ lk_bag,
                                                     const float* __restrict__ alpha,
                                                     const float* __restrict__ grad) {
+  CtaClock clk_(2);
   pdl_entry();
   const int b = static_cast<int>(blockIdx.x), m = min(nb2, nbs);
   bool is_b2;
@@ -1659,6 +1715,7 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
     unsigned char* __restrict__ d0mask) {
+  CtaClock clk_(3);
   pdl_entry();
   bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask);
 }
@@ -1693,6 +1750,7 @@ template <class D, int MODE>
 __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restrict__ cores,
                                                        float* __restrict__ grads, CombineArgs A,
                                                        float lr) {
+  CtaClock clk_(4);
   pdl_entry();
   // the group bases of both keys in shared memory: a warp's slice lookup is a
   // binary search there instead of ~8 dependent global loads
@@ -1702,6 +1760,7 @@ __global__ void __launch_bounds__(kThreads, 6) f3_combine(Geo g, float* __restri
   for (int e = threadIdx.x; e < g.m1 + 1; e += blockDim.x) gb1[e] = A.group_base1[e];
   for (int e = threadIdx.x; e < g.m2 + 1; e += blockDim.x) gb2[e] = A.group_base2[e];
   __syncthreads();
+  cta_mark(4, 0);
   combine_task<D>((blockIdx.x * blockDim.x + threadIdx.x) >> 5, gb1, gb2, g, cores, grads, A, lr, MODE);
 }
 

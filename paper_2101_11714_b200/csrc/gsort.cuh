@@ -130,6 +130,7 @@ __device__ __forceinline__ uint32_t div_fix(uint32_t x, uint32_t d, double inv, 
 // kCache: the LFU cache code (key 3) compiled in only where a cache is used
 template <int RMAX, bool kCache>
 __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
+  CtaClock clk_(0);
   constexpr int QC = RMAX < 4 ? RMAX : 4;  // rounds whose index loads are batched
   namespace cg = cooperative_groups;
   const int c = blockIdx.x, G = gridDim.x;
@@ -314,7 +315,9 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
       atomicAdd(a.counts + a.slot_rows[k - K12], static_cast<unsigned long long>(run));
   }
   cg::grid_group grid = cg::this_grid();
+  cta_mark(0, 0);
   grid.sync();
+  cta_mark(0, 1);
 
   // ---- phase B1: per key, exclusive scan over the CTAs (warp per key)
   for (int k = c * kGsWarps + wid; k < K; k += G * kGsWarps) {
@@ -337,6 +340,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
     if (lane == 0) a.tot[k] = run;
   }
   grid.sync();
+  cta_mark(0, 2);
 
   // ---- phase B2: bases from the totals plus this CTA's prefix.  Block scan
   // of (lookups, tiles, groups) over [key 1 | key 2], IPT consecutive keys
@@ -524,6 +528,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) f3_gsort(GsortArgs a) {
     __syncthreads();
   }
 
+  cta_mark(0, 3);
   // ---- phase C: stable scatter of both keys
   const unsigned lt = lanemask_lt();
 #pragma unroll

@@ -1609,6 +1609,18 @@ int ttgpu_init_sampled_gaussian(ttgpu_table* t, uint64_t seed) {
   });
 }
 
+// Diagnostics (not part of the reference interface): per-CTA timeline of the
+// fast-path kernel `kid` (0 f3_gsort, 1 f3_fwd, 2 f3_srows_bwd2, 3 f3_bwd1,
+// 4 f3_combine) into the device buffer `dev` (u64 [grid][8]: entry and exit
+// global-timer ns, SM id, work note, four marks), or off with dev = NULL.
+int ttgpu_debug_cta_times(int kid, void* dev) {
+  return guarded([&] {
+    require_arg(kid >= 0 && kid < 8, "kernel id out of range");
+    unsigned long long* p = static_cast<unsigned long long*>(dev);
+    CK(cudaMemcpyToSymbol(f3::g_cta_times, &p, sizeof(p), sizeof(p) * kid));
+  });
+}
+
 }  // extern "C"
 
 #include "lfu_cache_host.inl"
