@@ -1042,6 +1042,7 @@ struct G1Blk {
   static_assert(D::C1 % CB == 0 && D::R1 % RB == 0 && CB % 4 == 0, "bad blocking");
 };
 
+constexpr int kBwd1TileCost = 4;  // f3_bwd1 range weight of a tile: kBwd1TileCost + nslots
 constexpr int kBwd1Stages = 2;  // tiles of bulk copies in flight per f3_bwd1 CTA (3: 2 CTAs/SM, slower)
 
 template <class D>
@@ -1065,7 +1066,7 @@ __device__ __forceinline__ void bwd1_body(
     const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
-    unsigned char* __restrict__ d0mask) {
+    unsigned char* __restrict__ d0mask, const int* __restrict__ plan = nullptr) {
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
   extern __shared__ __align__(128) float sm[];
@@ -1084,9 +1085,13 @@ __device__ __forceinline__ void bwd1_body(
   // Contiguous tile ranges balanced by work, not by count: tile t weighs
   // kTileCost + nslots(t) (its GEMMs scale with the slot count), and belongs
   // to the CTA floor(E(t) * grid / W), E = exclusive prefix of the weights.
-  // Every CTA recomputes the (small) prefix; ranges partition the tiles.
-  {
-    constexpr int kTileCost = 4;
+  // Planned ahead by f3_srows_bwd2's last CTA (plan_bwd1), or else recomputed
+  // here by every CTA (the prefix is small); ranges partition the tiles.
+  if (plan) {
+    t_lo = __ldcg(plan + blockIdx.x);
+    t_hi = max(t_lo, __ldcg(plan + blockIdx.x + 1));
+  } else {
+    constexpr int kTileCost = kBwd1TileCost;
     using Scan = cub::BlockScan<int, kThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int range[2];
@@ -1511,6 +1516,8 @@ struct SrowsArgs {
   const uint16_t* slot_of_pos;
   const int* tile_nslots;
   float* Sbuf;
+  int* b1range;  // f3_bwd1's tile ranges, planned by the last CTA (nullptr: bwd1 plans itself)
+  int b1grid;
 };
 struct Bwd2Args {
   const Tile* tiles;
@@ -1522,8 +1529,60 @@ struct Bwd2Args {
   int* has2;
 };
 
+// f3_bwd1's contiguous tile ranges, balanced by weight kBwd1TileCost + nslots
+// (tile t belongs to CTA b iff its exclusive weight prefix E(t) lies in
+// [ceil(bW/G), ceil((b+1)W/G))): range[b] = first tile with E >= ceil(bW/G),
+// range[G] = nt.  One 128-thread CTA; each thread walks its chunk of tiles
+// once for every threshold that falls inside it.  Same partition as the
+// in-kernel planning of bwd1_body (used when no plan is given).
+__device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
+                                          const int* __restrict__ tile_nslots, int* __restrict__ range,
+                                          int G) {
+  using Scan = cub::BlockScan<int, 128>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  const int nt = *ntiles;
+  const int tid = threadIdx.x;
+  const int per = (nt + 127) / 128;
+  const int a0 = min(nt, tid * per), a1 = min(nt, a0 + per);
+  constexpr int kPer = 32;
+  int wv[kPer];
+  int wsum = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) wv[j] = a0 + j < a1 ? kBwd1TileCost + tile_nslots[a0 + j] : 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) wsum += wv[j];
+  if (per > kPer)
+    for (int t = a0 + kPer; t < a1; ++t) wsum += kBwd1TileCost + tile_nslots[t];
+  int ex, W;
+  Scan(scan_tmp).ExclusiveSum(wsum, ex, W);
+  if (tid == 0) {
+    range[0] = 0;
+    range[G] = nt;
+  }
+  if (W == 0) {
+    for (int b = tid + 1; b < G; b += 128) range[b] = nt;
+    return;
+  }
+  // thresholds th_b = ceil(b W / G) with ex < th_b <= ex + wsum (b in 1 .. G-1)
+  const int64_t Wl = W, Gl = G;
+  int64_t b = static_cast<int64_t>(ex) * Gl / Wl + 1;
+  const int64_t b_end = min(Gl - 1, (static_cast<int64_t>(ex) + wsum) * Gl / Wl);
+  int64_t e = ex;
+  int t = a0, j = 0;
+  for (; b <= b_end; ++b) {
+    const int64_t th = (b * Wl + Gl - 1) / Gl;
+    while (t < a1 && e < th) {
+      e += j < kPer ? wv[j] : kBwd1TileCost + tile_nslots[t];
+      ++t;
+      ++j;
+    }
+    range[b] = t;
+  }
+}
+
 // CTA roles interleave (even: f3_bwd2 CTA, odd: 4 f3_srows warps) while both
 // have work left, so both stages spread over every SM from the first wave.
+// With sa.b1range, the grid's last CTA plans f3_bwd1's tile ranges instead.
 template <class D>
 __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Args ba, int nb2, int nbs,
                                                     const int32_t* __restrict__ lk_bag,
@@ -1531,6 +1590,10 @@ __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Ar
                                                     const float* __restrict__ grad) {
   CtaClock clk_(2);
   pdl_entry();
+  if (sa.b1range && blockIdx.x == gridDim.x - 1) {
+    plan_bwd1(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid);
+    return;
+  }
   const int b = static_cast<int>(blockIdx.x), m = min(nb2, nbs);
   bool is_b2;
   int idx;
@@ -1714,10 +1777,10 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
-    unsigned char* __restrict__ d0mask) {
+    unsigned char* __restrict__ d0mask, const int* __restrict__ plan) {
   CtaClock clk_(3);
   pdl_entry();
-  bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask);
+  bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask, plan);
 }
 
 // f3_bwd1 and f3_combine in ONE cooperative launch (the bwd1 grid is exactly

@@ -5,7 +5,7 @@ namespace ttgpu {
 struct F3Bufs {
   DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, rec1, solo, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
-      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf, gs_hist, gs_tot, bag_cnt;
+      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf, gs_hist, gs_tot, bag_cnt, b1plan;
   f3::Geo geo{};
   int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
@@ -394,6 +394,7 @@ struct F3Runner {
     // bwd1 + combine in one cooperative launch when the bwd1 grid is co-resident
     const bool fuse_comb = !f.chunked && t->fuse_comb &&
                            4 * static_cast<size_t>(g.m1 + g.m2 + 2) <= sm1;
+    int* b1plan_ptr = nullptr;  // f3_bwd1 ranges planned by f3_srows_bwd2 (fused path)
     t->mark("bwd_begin");
     if (f.chunked) {
       f3_launch(t->pdl, kc, dim3(grid1), dim3(f3::kFcThreads), sm1, st, g, t->cores.as<float>(),
@@ -403,9 +404,18 @@ struct F3Runner {
       t->mark("f3c_bwd");
     } else if (t->fuse_sb) {
       // f3_srows and f3_bwd2 in one launch (they are independent)
+      // the launch's last CTA plans f3_bwd1's tile ranges (unless the
+      // cooperative bwd1+combine variant runs, which plans them itself)
+      int* plan = nullptr;
+      if (!fuse_comb && t->plan_bwd1) {
+        f.b1plan.ensure(4 * (static_cast<size_t>(grid1) + 1));
+        plan = f.b1plan.as<int>();
+      }
       f3::SrowsArgs sa{t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
                        f.max_tiles1, f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(),
-                       f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>()};
+                       f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>(),
+                       plan, grid1};
+      b1plan_ptr = plan;
       f3::Bwd2Args ba{f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, f.perm2.as<uint32_t>(),
                       f.hloc.as<uint32_t>(), f.Hbuf.as<float>(), f.part2.as<float>(), f.has2.as<int>()};
       // srows warps walk the tiles grid-stride: TTGPU_SROWS_CTAS_PER_SM virtual
@@ -416,8 +426,8 @@ struct F3Runner {
       }();
       const int nbs_all = (f.max_tiles1 * 32 + 127) / 128;
       const int nbs = srows_per_sm > 0 ? std::min(nbs_all, t->num_sms * srows_per_sm) : nbs_all;
-      f3_launch(t->pdl, f3::f3_srows_bwd2<D>, dim3(grid2 + nbs), dim3(128), 0, st, g, sa, ba, grid2, nbs,
-                lk_bag, alpha, grad);
+      f3_launch(t->pdl, f3::f3_srows_bwd2<D>, dim3(grid2 + nbs + (plan ? 1 : 0)), dim3(128), 0, st, g, sa,
+                ba, grid2, nbs, lk_bag, alpha, grad);
       t->mark("f3_srows_bwd2");
     } else {
       f3_launch(t->pdl, f3::f3_srows<D>, dim3((f.max_tiles1 * 32 + 255) / 256), dim3(256), 0, st,
@@ -460,7 +470,7 @@ struct F3Runner {
       f3_launch(t->pdl, k1, dim3(grid1), dim3(f3::kThreads), sm1, st, g, t->cores.as<float>(),
                 f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.Sbuf.as<float>(), f.tile_i0.as<uint16_t>(),
                 f.tile_nslots.as<int>(), f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
-                f.d0mask.as<unsigned char>());
+                f.d0mask.as<unsigned char>(), static_cast<const int*>(b1plan_ptr));
       t->mark("f3_bwd1");
     }
     if (!t->fuse_sb || f.chunked) launch_bwd2();
