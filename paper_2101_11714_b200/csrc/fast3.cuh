@@ -1143,6 +1143,31 @@ __device__ __forceinline__ void bwd1_body(
   }
   unsigned long long note_ns = 0, note_runs = 0;  // diagnostics (cta_note)
   cta_mark(3, 0);
+  // prologue loads, all in flight together: warp 0 the descriptors and slot
+  // i0s of the first NS + 1 tiles; every thread G1[i1] of the first tile (its
+  // transposed staging needs no global round trip at the first tile)
+  constexpr int kG1U = 8;
+  constexpr bool kG1Pre = D::S1 <= kThreads * kG1U;
+  Tile p_d[NS];
+  int p_ns[NS], p_i0[NS];
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      p_d[q] = t_lo + q < t_hi ? tiles[t_lo + q] : Tile{};
+      p_ns[q] = t_lo + q < t_hi ? tile_nslots[t_lo + q] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < NS; ++q)
+      p_i0[q] = lane < p_ns[q] ? static_cast<int>(tile_i0[p_d[q].start + lane]) : 0;
+  }
+  float g1pre[kG1U];
+  int pre_i1 = -1;
+  if (kG1Pre && t_lo < t_hi) {
+    pre_i1 = __ldg(&tiles[t_lo].key);
+    const float* src = G1 + static_cast<int64_t>(pre_i1) * D::S1;
+#pragma unroll
+    for (int u = 0; u < kG1U; ++u) g1pre[u] = tid + u * kThreads < D::S1 ? __ldg(src + tid + u * kThreads) : 0.f;
+  }
   float* d0acc = D0acc + static_cast<int64_t>(blockIdx.x) * g.m0 * D::S0;
   unsigned char* d0m = d0mask + static_cast<int64_t>(blockIdx.x) * g.m0;
   for (int e = tid; e < g.m0; e += kThreads) d0m[e] = 0;
@@ -1184,9 +1209,14 @@ __device__ __forceinline__ void bwd1_body(
       q_d = tiles[t_lo + NS];
       q_ns = tile_nslots[t_lo + NS];
     }
-    for (int q = 0; q < NS && t_lo + q < t_hi; ++q) {
-      fetch(t_lo + q);
-      issue(q);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      if (t_lo + q < t_hi) {
+        n_d = p_d[q];
+        n_ns = p_ns[q];
+        n_i0 = p_i0[q];
+        issue(q);
+      }
     }
   }
   const int r0 = (tid % GB::TR) * GB::RB, cb0 = (tid / GB::TR) * GB::CB;
@@ -1220,7 +1250,17 @@ __device__ __forceinline__ void bwd1_body(
     note_ns += nslots;
     note_runs += i1 != cur_i1;
 #endif
-    if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
+    if (kG1Pre && t == t_lo && i1 == pre_i1) {  // the first tile's G1, loaded in the prologue
+#pragma unroll
+      for (int u = 0; u < kG1U; ++u) {
+        const int e = tid + u * kThreads;
+        if (e < D::S1) {
+          const int r = e / D::C1, c = e - r * D::C1;
+          G1t[c * SM::R1P + r] = g1pre[u];
+        }
+      }
+      cur_i1 = i1;
+    } else if (i1 != cur_i1) {  // stage G1[i1] transposed (once per bucket run)
       const float* src = G1 + static_cast<int64_t>(i1) * D::S1;
       constexpr int U = 8;
       for (int e0 = tid; e0 < D::S1; e0 += kThreads * U) {
