@@ -771,6 +771,9 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
   }
   uint32_t phase = 0;
   int m = 0;
+#ifdef TTGPU_CTA_TIMES
+  unsigned long long note_t = 0, note_l = 0, note_s = 0;
+#endif
   for (int t = t0; t < nt; t += G, phase ^= 1u, m ^= 1) {
     const int* lk_l = mbuf + m * SM::MI;
     const int* lk_slot = lk_l + D::TT;
@@ -778,6 +781,12 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     const int* meta = lk_solo + D::TT;
     mbar_wait(bar, phase);
     const int ntl = meta[0], nslots = meta[1], start = meta[2];
+#ifdef TTGPU_CTA_TIMES
+    if (t == t0) cta_mark(1, 0);
+    note_t += 1;
+    note_l += ntl;
+    note_s += nslots;
+#endif
     // H(slot) = G0[i0] (P0 x R1) · G1[i1] (R1 x C1): thread -> (slot, 4 columns), all P0 rows
     for (int q = tid; q < nslots * D::C4; q += kThreads) {
       const int s = q / D::C4, c4 = q - s * D::C4;
@@ -840,6 +849,9 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     __syncthreads();  // G2s / Hs free
     if (wid == 0 && t + G < nt) issue_g2();
   }
+#ifdef TTGPU_CTA_TIMES
+  cta_note(1, note_t | (note_l << 16) | (note_s << 40));
+#endif
 }
 
 // ----------------------------------------------------------- f3_srows ----
