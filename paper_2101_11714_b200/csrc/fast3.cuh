@@ -872,7 +872,8 @@ __device__ __forceinline__ void srows_tile(int t, const float* __restrict__ core
                                            const float* __restrict__ grad,
                                            const uint16_t* __restrict__ slot_of_pos,
                                            const int* __restrict__ tile_nslots,
-                                           float* __restrict__ Sbuf) {
+                                           float* __restrict__ Sbuf,
+                                           const uint4* __restrict__ rec = nullptr) {
   constexpr int EPL = (D::W1 + 31) / 32;  // row elements per lane
   // distinct G2 rows a lane reads per member: r = (lane + 32k) % R2 repeats with period NR
   constexpr int NR = D::R2 > 32 ? D::R2 / 32 : 1;
@@ -893,11 +894,23 @@ __device__ __forceinline__ void srows_tile(int t, const float* __restrict__ core
   int my_sl = -1, my_i2 = 0;
   float dmy[D::N];
   if (lane < ntl) {
-    const int l = static_cast<int>(perm[tl.start + lane]);
+    // the sorted record (f3_gsort / f3_scatter: lookup, i0 | i2 << 16, bag, alpha)
+    // gives i2, bag and alpha in one load; else through the lookup index
+    int bag;
+    float al;
     my_sl = slot_of_pos[tl.start + lane];
-    my_i2 = d2[l];
-    const float al = alpha[l];
-    const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(lk_bag[l]) * D::N);
+    if (rec) {
+      const uint4 r = rec[tl.start + lane];
+      my_i2 = static_cast<int>(r.y >> 16);
+      bag = static_cast<int>(r.z & 0x7fffffffu);
+      al = __uint_as_float(r.w);
+    } else {
+      const int l = static_cast<int>(perm[tl.start + lane]);
+      my_i2 = d2[l];
+      bag = lk_bag[l];
+      al = alpha[l];
+    }
+    const float4* grow = reinterpret_cast<const float4*>(grad + static_cast<int64_t>(bag) * D::N);
 #pragma unroll
     for (int q = 0; q < D::N / 4; ++q) {
       const float4 gq = __ldg(grow + q);
@@ -1018,11 +1031,12 @@ __device__ __forceinline__ void srows_body(int vblock, int vgrid, const float* _
                                            const float* __restrict__ grad,
                                            const uint16_t* __restrict__ slot_of_pos,
                                            const int* __restrict__ tile_nslots,
-                                           float* __restrict__ Sbuf) {
+                                           float* __restrict__ Sbuf,
+                                           const uint4* __restrict__ rec = nullptr) {
   const int nw = blockDim.x >> 5;
   for (int t = vblock * nw + (threadIdx.x >> 5); t < max_tiles; t += vgrid * nw) {
     srows_tile<D>(t, cores, coff2, tiles, ntiles, max_tiles, perm, d2, lk_bag, alpha, grad, slot_of_pos,
-                  tile_nslots, Sbuf);
+                  tile_nslots, Sbuf, rec);
     __syncwarp();
   }
 }
@@ -1570,6 +1584,7 @@ struct SrowsArgs {
   float* Sbuf;
   int* b1range;  // f3_bwd1's tile ranges, planned by the last CTA (nullptr: bwd1 plans itself)
   int b1grid;
+  const uint4* rec;  // sorted key-1 records (nullptr: through perm / d2 / lk_bag / alpha)
 };
 struct Bwd2Args {
   const Tile* tiles;
@@ -1661,7 +1676,7 @@ __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Ar
                  ba.part2, ba.has2);
   else
     srows_body<D>(idx, nbs, sa.cores, sa.coff2, sa.tiles, sa.ntiles, sa.max_tiles, sa.perm, sa.d2, lk_bag,
-                  alpha, grad, sa.slot_of_pos, sa.tile_nslots, sa.Sbuf);
+                  alpha, grad, sa.slot_of_pos, sa.tile_nslots, sa.Sbuf, sa.rec);
 }
 
 __device__ __forceinline__ void store_slice(float4 s, bool touched, float* out_core, float* out_grad,
