@@ -1111,7 +1111,7 @@ __device__ __forceinline__ void bwd1_body(
   // Contiguous tile ranges balanced by work, not by count: tile t weighs
   // kTileCost + nslots(t) (its GEMMs scale with the slot count), and belongs
   // to the CTA floor(E(t) * grid / W), E = exclusive prefix of the weights.
-  // Planned ahead by f3_srows_bwd2's last CTA (plan_bwd1), or else recomputed
+  // Planned ahead by f3_srows_bwd2's first CTA (plan_bwd1), or else recomputed
   // here by every CTA (the prefix is small); ranges partition the tiles.
   if (plan) {
     t_lo = __ldcg(plan + blockIdx.x);
@@ -1582,7 +1582,7 @@ struct SrowsArgs {
   const uint16_t* slot_of_pos;
   const int* tile_nslots;
   float* Sbuf;
-  int* b1range;  // f3_bwd1's tile ranges, planned by the last CTA (nullptr: bwd1 plans itself)
+  int* b1range;  // f3_bwd1's tile ranges, planned by CTA 0 (nullptr: bwd1 plans itself)
   int b1grid;
   const uint4* rec;  // sorted key-1 records (nullptr: through perm / d2 / lk_bag / alpha)
 };
@@ -1649,7 +1649,7 @@ __device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
 
 // CTA roles interleave (even: f3_bwd2 CTA, odd: 4 f3_srows warps) while both
 // have work left, so both stages spread over every SM from the first wave.
-// With sa.b1range, the grid's last CTA plans f3_bwd1's tile ranges instead.
+// With sa.b1range, the grid's first CTA plans f3_bwd1's tile ranges instead.
 template <class D>
 __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Args ba, int nb2, int nbs,
                                                     const int32_t* __restrict__ lk_bag,
@@ -1657,11 +1657,15 @@ __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Ar
                                                     const float* __restrict__ grad) {
   CtaClock clk_(2);
   pdl_entry();
-  if (sa.b1range && blockIdx.x == gridDim.x - 1) {
-    plan_bwd1(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid);
-    return;
+  int b = static_cast<int>(blockIdx.x);
+  if (sa.b1range) {  // CTA 0 (first wave) plans f3_bwd1; the roles start at CTA 1
+    if (b == 0) {
+      plan_bwd1(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid);
+      return;
+    }
+    --b;
   }
-  const int b = static_cast<int>(blockIdx.x), m = min(nb2, nbs);
+  const int m = min(nb2, nbs);
   bool is_b2;
   int idx;
   if (b < 2 * m) {

@@ -404,7 +404,7 @@ struct F3Runner {
       t->mark("f3c_bwd");
     } else if (t->fuse_sb) {
       // f3_srows and f3_bwd2 in one launch (they are independent)
-      // the launch's last CTA plans f3_bwd1's tile ranges (unless the
+      // the launch's first CTA plans f3_bwd1's tile ranges (unless the
       // cooperative bwd1+combine variant runs, which plans them itself)
       int* plan = nullptr;
       if (!fuse_comb && t->plan_bwd1) {
