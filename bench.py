@@ -161,6 +161,33 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def gpu_local_cpus(dev_index):
+    """The host CPUs of the GPU's own NUMA node (sysfs local_cpulist) that this
+    process may run on, or None.  The e2e section runs there, so its pinned
+    buffers are allocated (first-touched) in the GPU's node: H2D DMA reads from
+    a remote node's pages measured 11-18 GB/s on some boxes against ~50 GB/s
+    local (tools/numa_probe.py)."""
+    import torch
+
+    if os.environ.get("TTGPU_BENCH_NUMA", "1") == "0":
+        return None
+    try:
+        p = torch.cuda.get_device_properties(dev_index)
+        pci = "%04x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+        text = open(f"/sys/bus/pci/devices/{pci}/local_cpulist").read().strip()
+    except Exception:  # noqa: BLE001 - no sysfs entry: leave the affinity alone
+        return None
+    cpus = set()
+    for part in text.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        elif part:
+            cpus.add(int(part))
+    cpus &= os.sched_getaffinity(0)
+    return cpus or None
+
+
 def cta_timeline(path, run, flush, stream):
     """Diagnostic (outside every timed region): one graph replay with the
     per-CTA entry / exit timers of the five fast-path kernels enabled
@@ -829,6 +856,11 @@ def main():
 
     # e2e through the host C ABI: pinned host buffers, copies inside the region
     # page-locked host buffers; the torch tensors that own them stay referenced
+    # the e2e section runs on the GPU's NUMA node, its pinned pages allocated there
+    affinity0 = os.sched_getaffinity(0)
+    local_cpus = gpu_local_cpus(local)
+    if local_cpus:
+        os.sched_setaffinity(0, local_cpus)
     pinned = [torch.from_numpy(a).pin_memory() for a in (idx, off, grad)]
     pinned.append(torch.empty((B, N), dtype=torch.float32).pin_memory())
     h_idx, h_off, h_grad, h_out = (t.numpy() for t in pinned)
@@ -891,8 +923,11 @@ def main():
         e2e_med, e2e_mean = float(t[0].item()), float(t[1].item())
     e2e_value = world * L / e2e_med
     # the PCIe rates this box gives the step's own pinned buffers (grad_out
-    # H2D, output D2H; explains e2e differences between boxes: H2D from
-    # CPU-written pages varies 26-51 GB/s, tools/pcie_probe.py), CUDA events
+    # H2D, output D2H), CUDA events, measured right after the e2e steps: they
+    # explain e2e differences between runs.  The H2D rate of one and the same
+    # pinned buffer varies over time on these shared hosts (51 GB/s when
+    # allocated, 11-41 GB/s a few seconds later, single-NUMA-node VMs), while
+    # D2H stays at ~52 GB/s
     pcie = {}
     try:
         dbuf = torch.empty(h_out.size, dtype=torch.float32, device=dev)
@@ -910,6 +945,7 @@ def main():
         del dbuf
     except Exception:  # noqa: BLE001 - diagnostic only
         pcie = {}
+    os.sched_setaffinity(0, affinity0)
 
     if rank != 0:
         if dist:
@@ -1025,7 +1061,9 @@ def main():
                 "path": "ttgpu_forward + ttgpu_backward_sgd (host C ABI, pinned buffers)",
                 "statistic": "median step time over the timed steps",
                 "ms_per_step_median": e2e_med * 1e3, "ms_per_step_mean": e2e_mean * 1e3,
-                "pcie_best_GBs": pcie},
+                "pcie_best_GBs": pcie,
+                "host_cpus": (f"GPU-local NUMA node ({len(local_cpus)} CPUs, sysfs local_cpulist)"
+                              if local_cpus else "process default")},
     }
     if not args.no_cpu_baseline:
         cb = cpu_reference_time(cfg, idx, off, grad, budget_s=10.0)
