@@ -716,3 +716,33 @@ def test_chunked_vs_tile_kernels(orc, rank, exponent):
     again = tt.backward_bags(t, b, res.context, g).cores
     for k in range(3):
         assert np.array_equal(again[k], got[True][k])
+
+
+@pytest.mark.parametrize("rank,nlook", [(32, 1), (32, 45), (32, 4096), (32, 65536), (8, 4096), (64, 4096)])
+def test_bwd1_planned_ranges_bitwise(orc, monkeypatch, rank, nlook):
+    """f3_bwd1's tile ranges planned once by f3_srows_bwd2's first CTA
+    (plan_bwd1) are the ranges every bwd1 CTA derives itself
+    (TTGPU_PLAN_BWD1=0): same partition, so the gradients are BITWISE equal;
+    tiny, multi-hot weighted Mean batches with empty bags."""
+    p = tt.plan_shapes(10131227, 16, 3, rank, [200, 220, 250], [2, 2, 4])
+    rng = np.random.default_rng(nlook + rank)
+    base = tt.generate_zipfian_batch(p.num_rows, 1.05, 3, nlook, 1)
+    nb = max(1, nlook // 3)
+    cuts = np.sort(rng.integers(0, nlook + 1, nb - 1))
+    off = np.concatenate([[0], cuts, [nlook]]).astype(np.int64)
+    b = tt.IndexBatch(base.indices.astype(np.int64), off, rng.uniform(-2, 2, nlook), tt.Pooling.Mean)
+    g = rng.standard_normal((nb, 16)).astype(np.float32)
+    outs, grads = [], []
+    for plan in ("1", "0"):
+        monkeypatch.setenv("TTGPU_PLAN_BWD1", plan)
+        t, cores = make_table(p, np.float32, 9, "plan" + plan, scale=0.3)
+        res = tt.forward_bags(t, b)
+        outs.append(res.output)
+        grads.append(tt.backward_bags(t, b, res.context, g).cores)
+    assert np.array_equal(outs[0], outs[1])
+    for k in range(3):
+        assert np.array_equal(grads[0][k], grads[1][k]), k
+    if nlook <= 4096:
+        want = orc.backward(as_oplan(p), cores, b.indices, b.offsets, g, b.weights, 1)
+        for k in range(3):
+            assert scaled_max_err(grads[0][k], want[k]) <= GRAD_TOL
