@@ -1253,16 +1253,20 @@ __device__ __forceinline__ void bwd1_body(
 #pragma unroll
     for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
   int run_start = t_lo, cur_i1 = -1;
+  __syncthreads();  // the prologue's misc / slot_i0 published
   for (int t = t_lo; t < t_hi; ++t) {
     const int st = (t - t_lo) % NS;
     const uint32_t parity = static_cast<uint32_t>(((t - t_lo) / NS) & 1);
     const float* Ss = sm + st * SM::STAGE;
     const float* G0s = Ss + D::TT * D::W1;
     const int* si0 = slot_i0 + st * D::TT;
-    __syncthreads();  // misc / slot_i0 of tile t published
+    // misc / slot_i0 of stage st were written by issue() at the end of tile
+    // t - NS (or in the prologue): every thread has passed tile t - 1's
+    // barriers since, so no barrier is needed here.  Stage st + 1's misc
+    // (the next tile's key) was written at the end of tile t - 1 and is read
+    // after this tile's post-wait barrier.
     const int i1 = misc[2 * st], nslots = misc[2 * st + 1];
     const int nk = nslots * D::P0;
-    const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * ((st + 1) % NS)] : -1;
     if (wid == 0 && t + NS < t_hi) {  // tile t+NS's slot i0s in flight during this tile's GEMMs
       n_d = q_d;
       n_ns = q_ns;
@@ -1314,6 +1318,7 @@ __device__ __forceinline__ void bwd1_body(
     mbar_wait(bar + st, parity);
     if (t == t_lo) cta_mark(3, 1);
     __syncthreads();  // G1t staged, d0first set, bulk data visible
+    const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * ((st + 1) % NS)] : -1;
     // ---- dG1 partial += Σ_kappa G0s[kappa][r1] (x) S[kappa][c]
     if (g1_on) {
 #pragma unroll 2
