@@ -672,6 +672,7 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
                                                    uint16_t* __restrict__ slot_of_pos,
                                                    uint16_t* __restrict__ tile_i0,
                                                    int* __restrict__ tile_nslots,
+                                                   int* __restrict__ tile_one,
                                                    const int64_t* __restrict__ off, int64_t L, int mean,
                                                    int* __restrict__ bag_cnt,
                                                    const int* __restrict__ cache_slot,
@@ -729,6 +730,8 @@ __global__ void __launch_bounds__(kThreads) f3_fwd(Geo g, const float* __restric
     if (is_first) tile_i0[tl.start + s] = static_cast<uint16_t>(i0);
     if (lane == 0) {
       tile_nslots[u] = nslots;
+      // (i1, i0) of a one-slot tile, for f3_bwd1's merge units (plan_bwd1)
+      tile_one[u] = nslots == 1 ? (tl.key << 16) | i0 : -1;
       meta[0] = ntl;
       meta[1] = nslots;
       meta[2] = tl.start;
@@ -1092,7 +1095,8 @@ __device__ __forceinline__ void bwd1_body(
     const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
-    unsigned char* __restrict__ d0mask, const int* __restrict__ plan = nullptr) {
+    unsigned char* __restrict__ d0mask, const int* __restrict__ plan = nullptr,
+    const uint8_t* __restrict__ ulen = nullptr) {
   using SM = Bwd1Smem<D>;
   using GB = G1Blk<D>;
   extern __shared__ __align__(128) float sm[];
@@ -1101,7 +1105,7 @@ __device__ __forceinline__ void bwd1_body(
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + SM::floats());  // NS stages
   int* slot_i0 = reinterpret_cast<int*>(bar + NS);  // NS x TT
   int* d0first = slot_i0 + NS * D::TT;              // TT
-  int* misc = d0first + D::TT;                      // [2*stage + 0] key, [2*stage + 1] nslots
+  int* misc = d0first + D::TT;  // [2*stage + 0] key, [2*stage + 1] nslots, [8 + stage] unit tiles
   unsigned* d0bits = reinterpret_cast<unsigned*>(misc + 16);
   const float* G0 = cores + g.coff0;
   const float* G1 = cores + g.coff1;
@@ -1175,16 +1179,31 @@ __device__ __forceinline__ void bwd1_body(
   constexpr int kG1U = 8;
   constexpr bool kG1Pre = D::S1 <= kThreads * kG1U;
   Tile p_d[NS];
-  int p_ns[NS], p_i0[NS];
+  int p_ns[NS], p_i0[NS], p_K[NS];
+  int nx_t = t_lo + NS;  // warp 0: first tile of the next unit to fetch
   if (wid == 0) {
+    if (ulen) {  // merge units: unit q starts where unit q - 1 ends
+      int tq = t_lo;
 #pragma unroll
-    for (int q = 0; q < NS; ++q) {
-      p_d[q] = t_lo + q < t_hi ? tiles[t_lo + q] : Tile{};
-      p_ns[q] = t_lo + q < t_hi ? tile_nslots[t_lo + q] : 0;
+      for (int q = 0; q < NS; ++q) {
+        p_K[q] = tq < t_hi ? min(static_cast<int>(ulen[tq]), t_hi - tq) : 0;
+        p_d[q] = tq < t_hi ? tiles[tq] : Tile{};
+        p_ns[q] = tq < t_hi ? tile_nslots[tq] : 0;
+        p_i0[q] = lane < p_ns[q] ? static_cast<int>(tile_i0[p_d[q].start + lane]) : 0;
+        tq += p_K[q];
+      }
+      nx_t = tq;
+    } else {
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        p_d[q] = t_lo + q < t_hi ? tiles[t_lo + q] : Tile{};
+        p_ns[q] = t_lo + q < t_hi ? tile_nslots[t_lo + q] : 0;
+        p_K[q] = t_lo + q < t_hi ? 1 : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < NS; ++q)
+        p_i0[q] = lane < p_ns[q] ? static_cast<int>(tile_i0[p_d[q].start + lane]) : 0;
     }
-#pragma unroll
-    for (int q = 0; q < NS; ++q)
-      p_i0[q] = lane < p_ns[q] ? static_cast<int>(tile_i0[p_d[q].start + lane]) : 0;
   }
   float g1pre[kG1U];
   int pre_i1 = -1;
@@ -1204,25 +1223,28 @@ __device__ __forceinline__ void bwd1_body(
   // warp 0 keeps NS tiles of bulk copies in flight: the descriptors of tile
   // t+NS are fetched during tile t, its S rows (one copy) and G0 rows (one per
   // slot) are issued into tile t's stage as soon as tile t's GEMMs are done
+  // A merged unit (n_K > 1 one-slot tiles of one i0) copies the S row of each
+  // of its tiles (tile q's rows start at its first lookup position, q * TT
+  // after the unit's first) and the one G0 row.
   Tile n_d{};
-  int n_ns = 0, n_i0 = 0;
-  auto fetch = [&](int t) {
-    n_d = tiles[t];
-    n_ns = tile_nslots[t];
-    n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
-  };
+  int n_ns = 0, n_i0 = 0, n_K = 1;
   auto issue = [&](int st) {
     float* Ss = sm + st * SM::STAGE;
     float* G0s = Ss + D::TT * D::W1;
+    const int rows = n_K > 1 ? n_K : n_ns;
     if (lane < n_ns) slot_i0[st * D::TT + lane] = n_i0;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect(bar + st, static_cast<uint32_t>(n_ns) * (D::W1 + D::S0) * 4);
-      tma_load(Ss, Sbuf + static_cast<int64_t>(n_d.start) * D::W1, n_ns * D::W1 * 4, bar + st);
+      mbar_arrive_expect(bar + st, static_cast<uint32_t>(rows * D::W1 + n_ns * D::S0) * 4);
+      if (n_K == 1) tma_load(Ss, Sbuf + static_cast<int64_t>(n_d.start) * D::W1, rows * D::W1 * 4, bar + st);
       misc[2 * st] = n_d.key;
       misc[2 * st + 1] = n_ns;
+      misc[8 + st] = n_K;
     }
     __syncwarp();
+    if (n_K > 1 && lane < n_K)
+      tma_load(Ss + lane * D::W1, Sbuf + static_cast<int64_t>(n_d.start + lane * D::TT) * D::W1, D::W1 * 4,
+               bar + st);
     if (lane < n_ns)
       tma_load(G0s + lane * D::S0, G0 + static_cast<int64_t>(n_i0) * D::S0, D::S0 * 4, bar + st);
   };
@@ -1231,16 +1253,17 @@ __device__ __forceinline__ void bwd1_body(
   Tile q_d{};
   int q_ns = 0;
   if (wid == 0) {
-    if (t_lo + NS < t_hi) {
+    if (!ulen && t_lo + NS < t_hi) {
       q_d = tiles[t_lo + NS];
       q_ns = tile_nslots[t_lo + NS];
     }
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
-      if (t_lo + q < t_hi) {
+      if (p_K[q] > 0) {
         n_d = p_d[q];
         n_ns = p_ns[q];
         n_i0 = p_i0[q];
+        n_K = p_K[q];
         issue(q);
       }
     }
@@ -1254,9 +1277,9 @@ __device__ __forceinline__ void bwd1_body(
     for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
   int run_start = t_lo, cur_i1 = -1;
   __syncthreads();  // the prologue's misc / slot_i0 published
-  for (int t = t_lo; t < t_hi; ++t) {
-    const int st = (t - t_lo) % NS;
-    const uint32_t parity = static_cast<uint32_t>(((t - t_lo) / NS) & 1);
+  for (int t = t_lo, u = 0; t < t_hi; ++u) {  // unit u: tiles t .. t + K - 1
+    const int st = u % NS;
+    const uint32_t parity = static_cast<uint32_t>((u / NS) & 1);
     const float* Ss = sm + st * SM::STAGE;
     const float* G0s = Ss + D::TT * D::W1;
     const int* si0 = slot_i0 + st * D::TT;
@@ -1265,16 +1288,22 @@ __device__ __forceinline__ void bwd1_body(
     // barriers since, so no barrier is needed here.  Stage st + 1's misc
     // (the next tile's key) was written at the end of tile t - 1 and is read
     // after this tile's post-wait barrier.
-    const int i1 = misc[2 * st], nslots = misc[2 * st + 1];
+    const int i1 = misc[2 * st], nslots = misc[2 * st + 1], K = misc[8 + st];
     const int nk = nslots * D::P0;
-    if (wid == 0 && t + NS < t_hi) {  // tile t+NS's slot i0s in flight during this tile's GEMMs
-      n_d = q_d;
-      n_ns = q_ns;
-      n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
-      if (t + NS + 1 < t_hi) {
-        q_d = tiles[t + NS + 1];
-        q_ns = tile_nslots[t + NS + 1];
+    if (wid == 0 && nx_t < t_hi) {  // unit u+NS's slot i0s in flight during this unit's GEMMs
+      if (ulen) {
+        n_K = min(static_cast<int>(ulen[nx_t]), t_hi - nx_t);
+        n_d = tiles[nx_t];
+        n_ns = tile_nslots[nx_t];
+      } else {
+        n_d = q_d;
+        n_ns = q_ns;
+        if (nx_t + 1 < t_hi) {
+          q_d = tiles[nx_t + 1];
+          q_ns = tile_nslots[nx_t + 1];
+        }
       }
+      n_i0 = lane < n_ns ? static_cast<int>(tile_i0[n_d.start + lane]) : 0;
     }
 #ifdef TTGPU_CTA_TIMES
     note_ns += nslots;
@@ -1318,7 +1347,22 @@ __device__ __forceinline__ void bwd1_body(
     mbar_wait(bar + st, parity);
     if (t == t_lo) cta_mark(3, 1);
     __syncthreads();  // G1t staged, d0first set, bulk data visible
-    const int nxt_i1 = (t + 1 < t_hi) ? misc[2 * ((st + 1) % NS)] : -1;
+    const int nxt_i1 = (t + K < t_hi) ? misc[2 * ((st + 1) % NS)] : -1;
+    if (K > 1) {  // merged unit: S row 0 = the sum of its K rows (fixed order), then one-slot GEMMs
+      static_assert(kThreads % D::W1 == 0, "merge groups");
+      constexpr int NG = kThreads / D::W1;
+      float* Sw = const_cast<float*>(Ss);
+      const int gq = tid / D::W1, e = tid - gq * D::W1;
+      float p = 0.f;
+      for (int j = gq; j < K; j += NG) p += Sw[j * D::W1 + e];
+      if (gq < K) Sw[gq * D::W1 + e] = p;  // row gq is read by this thread only
+      __syncthreads();
+      if (gq == 0) {
+        for (int q = 1; q < min(NG, K); ++q) p += Sw[q * D::W1 + e];
+        Sw[e] = p;
+      }
+      __syncthreads();
+    }
     // ---- dG1 partial += Σ_kappa G0s[kappa][r1] (x) S[kappa][c]
     if (g1_on) {
 #pragma unroll 2
@@ -1366,7 +1410,10 @@ __device__ __forceinline__ void bwd1_body(
       }
     }
     __syncthreads();  // stage st / slot lists consumed
-    if (wid == 0 && t + NS < t_hi) issue(st);
+    if (wid == 0 && nx_t < t_hi) {
+      issue(st);
+      nx_t += n_K;
+    }
     // ---- D0 into the CTA block (slots of one tile have distinct i0)
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
@@ -1384,8 +1431,8 @@ __device__ __forceinline__ void bwd1_body(
       }
     }
     // ---- end of an i1 run (or of this CTA's range): flush the dG1 partial
-    if (tid == 0) has1[t] = (t == run_start) ? 1 : 0;
-    if (nxt_i1 != i1 || t + 1 == t_hi) {
+    if (tid < K) has1[t + tid] = (t + tid == run_start) ? 1 : 0;
+    if (nxt_i1 != i1 || t + K == t_hi) {
       float* dst = part1 + static_cast<int64_t>(run_start) * D::S1;
       if (g1_on) {
 #pragma unroll
@@ -1399,8 +1446,9 @@ __device__ __forceinline__ void bwd1_body(
       for (int i = 0; i < GB::RB; ++i)
 #pragma unroll
         for (int j = 0; j < GB::CB; ++j) acc1[i][j] = 0.f;
-      run_start = t + 1;
+      run_start = t + K;
     }
+    t += K;
   }
   cta_mark(3, 2);
   cta_note(3, static_cast<unsigned long long>(t_hi - t_lo) | (note_ns << 16) | (note_runs << 40));
@@ -1590,6 +1638,8 @@ struct SrowsArgs {
   int* b1range;  // f3_bwd1's tile ranges, planned by CTA 0 (nullptr: bwd1 plans itself)
   int b1grid;
   const uint4* rec;  // sorted key-1 records (nullptr: through perm / d2 / lk_bag / alpha)
+  uint8_t* b1ulen;   // f3_bwd1 merge units planned with the ranges (nullptr: one tile per unit)
+  const int* tile_one;  // (i1 << 16 | i0) of one-slot tiles, else -1 (f3_fwd)
 };
 struct Bwd2Args {
   const Tile* tiles;
@@ -1606,21 +1656,65 @@ struct Bwd2Args {
 // [ceil(bW/G), ceil((b+1)W/G))): range[b] = first tile with E >= ceil(bW/G),
 // range[G] = nt.  One 128-thread CTA; each thread walks its chunk of tiles
 // once for every threshold that falls inside it.  Same partition as the
-// in-kernel planning of bwd1_body (used when no plan is given).
+// in-kernel planning of bwd1_body (used when no plan is given) unless ulen
+// is given:
+//
+// Merge units (ulen != nullptr).  Under Zipf most i1-tiles of a hot (i0, i1)
+// pair hold that single slot (cfg2: 939 of 2,157 tiles are pair (0, 0)), and
+// f3_bwd1 pays its per-tile pipeline (bulk copies, barriers, the D0
+// read-modify-write) for each.  By linearity their GEMMs can run once on the
+// sum of their S rows: tile t CONTINUES tile t - 1 when both hold one slot of
+// the same i1 and i0 (bwd1 copies the K S rows of a unit one by one: a
+// tile's rows start at its first lookup position).  A run of continuing
+// tiles is cut into units of <= kCap tiles (counted from the run's first
+// tile); ulen[t] = tiles from t to the end of its unit, so a CTA whose range
+// starts inside a unit starts a shorter one there.  A continuing tile weighs
+// kBwd1ContCost instead of kBwd1TileCost + 1.
+constexpr int kBwd1ContCost = 1;
+
+template <int kCap>
 __device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
                                           const int* __restrict__ tile_nslots, int* __restrict__ range,
-                                          int G) {
+                                          int G, const int* __restrict__ tile_one,
+                                          uint8_t* __restrict__ ulen) {
   using Scan = cub::BlockScan<int, 128>;
   __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int run_first[128], run_last[128];
   const int nt = *ntiles;
   const int tid = threadIdx.x;
   const int per = (nt + 127) / 128;
   const int a0 = min(nt, tid * per), a1 = min(nt, a0 + per);
   constexpr int kPer = 32;
+  const bool merge = ulen != nullptr && per <= kPer;
   int wv[kPer];
   int wsum = 0;
+  unsigned cont = 0;  // bit j: tile a0 + j continues tile a0 + j - 1
+  if (merge) {
+    // tile_one: (i1 << 16 | i0) of a one-slot tile, else -1; all loads of a
+    // batch of 16 tiles (and tile a0 - 1) in one round trip
+    int prev = a0 > 0 && a0 < a1 ? tile_one[a0 - 1] : -1;
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) wv[j] = a0 + j < a1 ? kBwd1TileCost + tile_nslots[a0 + j] : 0;
+    for (int b0 = 0; b0 < kPer; b0 += 16) {
+      int ns[16], on[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = a0 + b0 + j;
+        ns[j] = t < a1 ? tile_nslots[t] : 0;
+        on[j] = t < a1 ? tile_one[t] : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int jj = b0 + j;
+        const bool c = on[j] >= 0 && on[j] == prev;
+        if (c) cont |= 1u << jj;
+        wv[jj] = a0 + jj < a1 ? (c ? kBwd1ContCost : kBwd1TileCost + ns[j]) : 0;
+        prev = on[j];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) wv[j] = a0 + j < a1 ? kBwd1TileCost + tile_nslots[a0 + j] : 0;
+  }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) wsum += wv[j];
   if (per > kPer)
@@ -1633,22 +1727,55 @@ __device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
   }
   if (W == 0) {
     for (int b = tid + 1; b < G; b += 128) range[b] = nt;
+  } else {
+    // thresholds th_b = ceil(b W / G) with ex < th_b <= ex + wsum (b in 1 .. G-1)
+    const int64_t Wl = W, Gl = G;
+    int64_t b = static_cast<int64_t>(ex) * Gl / Wl + 1;
+    const int64_t b_end = min(Gl - 1, (static_cast<int64_t>(ex) + wsum) * Gl / Wl);
+    int64_t e = ex;
+    int t = a0, j = 0;
+    // With merge units the boundary is placed by tile MIDPOINTS (a tile goes
+    // to the CTA holding E(t) + w(t)/2): once the hot one-slot runs are cheap,
+    // the big multi-slot tiles set the longest CTA, and the first-tile rule
+    // lets one overshoot its CTA's share by up to a whole tile weight.
+    const bool mid = ulen != nullptr;
+    for (; b <= b_end; ++b) {
+      const int64_t th = (b * Wl + Gl - 1) / Gl;
+      while (t < a1) {
+        const int w = j < kPer ? wv[j] : kBwd1TileCost + tile_nslots[t];
+        if (mid ? 2 * e + w >= 2 * th : e >= th) break;
+        e += w;
+        ++t;
+        ++j;
+      }
+      range[b] = t;
+    }
+  }
+  if (ulen == nullptr) return;
+  // unit lengths: a tile's run starts at the last non-continuing tile <= t and
+  // ends before the first non-continuing tile > t (searched across chunks)
+  const int n = a1 - a0;
+  const unsigned live = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+  const unsigned starts = merge ? (~cont & live) : live;  // non-continuing tiles of the chunk
+  run_last[tid] = starts ? a0 + 31 - __clz(starts) : -1;
+  run_first[tid] = starts ? a0 + __ffs(starts) - 1 : INT_MAX;
+  __syncthreads();
+  if (!merge) {
+    for (int t = a0; t < a1; ++t) ulen[t] = 1;
     return;
   }
-  // thresholds th_b = ceil(b W / G) with ex < th_b <= ex + wsum (b in 1 .. G-1)
-  const int64_t Wl = W, Gl = G;
-  int64_t b = static_cast<int64_t>(ex) * Gl / Wl + 1;
-  const int64_t b_end = min(Gl - 1, (static_cast<int64_t>(ex) + wsum) * Gl / Wl);
-  int64_t e = ex;
-  int t = a0, j = 0;
-  for (; b <= b_end; ++b) {
-    const int64_t th = (b * Wl + Gl - 1) / Gl;
-    while (t < a1 && e < th) {
-      e += j < kPer ? wv[j] : kBwd1TileCost + tile_nslots[t];
-      ++t;
-      ++j;
-    }
-    range[b] = t;
+  int rs = -1;  // run start carried into the chunk
+  for (int q = tid - 1; q >= 0 && rs < 0; --q) rs = run_last[q];
+  int re_after = nt;  // first run start after the chunk
+  for (int q = tid + 1; q < 128 && re_after == nt; ++q)
+    if (run_first[q] != INT_MAX) re_after = run_first[q];
+  for (int j = 0; j < n; ++j) {
+    const int t = a0 + j;
+    if (!((cont >> j) & 1u)) rs = t;
+    const unsigned later = j + 1 < 32 ? (starts >> (j + 1)) : 0u;
+    const int re = later ? t + __ffs(later) : re_after;
+    const int ce = rs + kCap * ((t - rs) / kCap + 1);
+    ulen[t] = static_cast<uint8_t>(min(ce, re) - t);
   }
 }
 
@@ -1656,7 +1783,7 @@ __device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
 // have work left, so both stages spread over every SM from the first wave.
 // With sa.b1range, the grid's first CTA plans f3_bwd1's tile ranges instead.
 template <class D>
-__global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Args ba, int nb2, int nbs,
+__global__ void __launch_bounds__(128, 4) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Args ba, int nb2, int nbs,
                                                     const int32_t* __restrict__ lk_bag,
                                                     const float* __restrict__ alpha,
                                                     const float* __restrict__ grad) {
@@ -1665,7 +1792,7 @@ __global__ void __launch_bounds__(128) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd2Ar
   int b = static_cast<int>(blockIdx.x);
   if (sa.b1range) {  // CTA 0 (first wave) plans f3_bwd1; the roles start at CTA 1
     if (b == 0) {
-      plan_bwd1(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid);
+      plan_bwd1<D::TT>(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid, sa.tile_one, sa.b1ulen);
       return;
     }
     --b;
@@ -1853,10 +1980,10 @@ __global__ void __launch_bounds__(kThreads, D::R1 <= 32 ? 3 : 1) f3_bwd1(
     const int* __restrict__ ntiles, const float* __restrict__ Sbuf,
     const uint16_t* __restrict__ tile_i0, const int* __restrict__ tile_nslots,
     float* __restrict__ part1, int* __restrict__ has1, float* __restrict__ D0acc,
-    unsigned char* __restrict__ d0mask, const int* __restrict__ plan) {
+    unsigned char* __restrict__ d0mask, const int* __restrict__ plan, const uint8_t* __restrict__ ulen) {
   CtaClock clk_(3);
   pdl_entry();
-  bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask, plan);
+  bwd1_body<D>(g, cores, tiles, ntiles, Sbuf, tile_i0, tile_nslots, part1, has1, D0acc, d0mask, plan, ulen);
 }
 
 // f3_bwd1 and f3_combine in ONE cooperative launch (the bwd1 grid is exactly

@@ -5,7 +5,8 @@ namespace ttgpu {
 struct F3Bufs {
   DevBuf d0, d1, d2, hist1, hist2, perm1, perm2, rec1, solo, tiles1, tiles2, tile_base1, tile_base2, ntiles,
       Hbuf, y, hloc, slotpos, tile_i0, tile_nslots, part1, has1, part2, has2, D0acc, d0mask,
-      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf, gs_hist, gs_tot, bag_cnt, b1plan;
+      group_base1, group_base2, gpart, gtouch, counters, tot, Sbuf, gs_hist, gs_tot, bag_cnt, b1plan,
+      b1ulen, tile_one;
   f3::Geo geo{};
   int max_tiles1 = 0, max_tiles2 = 0;
   int kind = -1;  // instantiation index
@@ -207,6 +208,7 @@ struct F3Runner {
     f.slotpos.ensure(2 * L);
     f.tile_i0.ensure(2 * L);
     f.tile_nslots.ensure(4 * f.max_tiles1);
+    f.tile_one.ensure(4 * f.max_tiles1);
     f.bag_cnt.ensure(4 * static_cast<size_t>(B));
     const int gb = std::max(NT, grid_for(B, 512, t->num_sms, 4));
     t->mark("fwd_begin");
@@ -328,7 +330,8 @@ struct F3Runner {
                                            f.ntiles.as<int>(), f.rec1.as<uint4>(), w, out,
                                            f.Hbuf.as<float>(), f.y.as<float>(), f.hloc.as<uint32_t>(),
                                            f.slotpos.as<uint16_t>(), f.tile_i0.as<uint16_t>(),
-                                           f.tile_nslots.as<int>(), off, L, pooling, f.bag_cnt.as<int>(),
+                                           f.tile_nslots.as<int>(), f.tile_one.as<int>(), off, L, pooling,
+                                           f.bag_cnt.as<int>(),
                                            cache ? cache->lk_slot : nullptr,
                                            cache ? cache->store : nullptr);
     }
@@ -395,6 +398,7 @@ struct F3Runner {
     const bool fuse_comb = !f.chunked && t->fuse_comb &&
                            4 * static_cast<size_t>(g.m1 + g.m2 + 2) <= sm1;
     int* b1plan_ptr = nullptr;  // f3_bwd1 ranges planned by f3_srows_bwd2 (fused path)
+    uint8_t* b1ulen_ptr = nullptr;  // and its merge units
     t->mark("bwd_begin");
     if (f.chunked) {
       f3_launch(t->pdl, kc, dim3(grid1), dim3(f3::kFcThreads), sm1, st, g, t->cores.as<float>(),
@@ -407,15 +411,21 @@ struct F3Runner {
       // the launch's first CTA plans f3_bwd1's tile ranges (unless the
       // cooperative bwd1+combine variant runs, which plans them itself)
       int* plan = nullptr;
+      uint8_t* ulen = nullptr;
       if (!fuse_comb && t->plan_bwd1) {
         f.b1plan.ensure(4 * (static_cast<size_t>(grid1) + 1));
         plan = f.b1plan.as<int>();
+        if (t->merge1) {
+          f.b1ulen.ensure(static_cast<size_t>(f.max_tiles1) + 16);
+          ulen = f.b1ulen.as<uint8_t>();
+        }
       }
       f3::SrowsArgs sa{t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
                        f.max_tiles1, f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(),
                        f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>(),
-                       plan, grid1, f.rec1.as<uint4>()};
+                       plan, grid1, f.rec1.as<uint4>(), ulen, f.tile_one.as<int>()};
       b1plan_ptr = plan;
+      b1ulen_ptr = ulen;
       f3::Bwd2Args ba{f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, f.perm2.as<uint32_t>(),
                       f.hloc.as<uint32_t>(), f.Hbuf.as<float>(), f.part2.as<float>(), f.has2.as<int>()};
       // srows warps walk the tiles grid-stride: TTGPU_SROWS_CTAS_PER_SM virtual
@@ -470,7 +480,8 @@ struct F3Runner {
       f3_launch(t->pdl, k1, dim3(grid1), dim3(f3::kThreads), sm1, st, g, t->cores.as<float>(),
                 f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(), f.Sbuf.as<float>(), f.tile_i0.as<uint16_t>(),
                 f.tile_nslots.as<int>(), f.part1.as<float>(), f.has1.as<int>(), f.D0acc.as<float>(),
-                f.d0mask.as<unsigned char>(), static_cast<const int*>(b1plan_ptr));
+                f.d0mask.as<unsigned char>(), static_cast<const int*>(b1plan_ptr),
+                static_cast<const uint8_t*>(b1ulen_ptr));
       t->mark("f3_bwd1");
     }
     if (!t->fuse_sb || f.chunked) launch_bwd2();

@@ -202,6 +202,7 @@ struct ttgpu_table {
   bool fuse_sb = true;         // fast path: f3_srows + f3_bwd2 in one launch (TTGPU_FUSE_SB=0: two)
   bool fuse_comb = false;      // fast path: f3_bwd1 + f3_combine in one cooperative launch
   bool plan_bwd1 = true;       // fast path: f3_bwd1's ranges planned by f3_srows_bwd2 (TTGPU_PLAN_BWD1=0: in bwd1)
+  bool merge1 = true;          // planned f3_bwd1: runs of one-slot tiles of the same (i1, i0) as one unit (TTGPU_MERGE1=0: off)
                                // (TTGPU_FUSE_COMB=1; measured slower: the combine tasks get half the warps)
   // optional phase timing (CUDA events between pipeline phases)
   // Marks recorded while the stream is being captured become event-record nodes of
@@ -1012,6 +1013,8 @@ int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* r
       t->fuse_comb = fc && std::atoi(fc) != 0;
       const char* pb = std::getenv("TTGPU_PLAN_BWD1");
       t->plan_bwd1 = !(pb && std::atoi(pb) == 0);
+      const char* mg = std::getenv("TTGPU_MERGE1");
+      t->merge1 = !(mg && std::atoi(mg) == 0);
     }
     std::vector<int64_t> coff;
     t->dp = make_devplan(t->plan, coff, t->total);

@@ -733,6 +733,9 @@ def test_bwd1_planned_ranges_bitwise(orc, monkeypatch, rank, nlook):
     b = tt.IndexBatch(base.indices.astype(np.int64), off, rng.uniform(-2, 2, nlook), tt.Pooling.Mean)
     g = rng.standard_normal((nb, 16)).astype(np.float32)
     outs, grads = [], []
+    # merge units off: the planned ranges alone must reproduce the in-kernel
+    # planning bit for bit
+    monkeypatch.setenv("TTGPU_MERGE1", "0")
     for plan in ("1", "0"):
         monkeypatch.setenv("TTGPU_PLAN_BWD1", plan)
         t, cores = make_table(p, np.float32, 9, "plan" + plan, scale=0.3)
@@ -746,3 +749,44 @@ def test_bwd1_planned_ranges_bitwise(orc, monkeypatch, rank, nlook):
         want = orc.backward(as_oplan(p), cores, b.indices, b.offsets, g, b.weights, 1)
         for k in range(3):
             assert scaled_max_err(grads[0][k], want[k]) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("rank,nlook,s", [(32, 1, 1.05), (32, 45, 1.05), (32, 4096, 1.05), (32, 4096, 1.2),
+                                          (32, 65536, 1.05), (8, 4096, 1.2), (64, 4096, 1.05),
+                                          (16, 20000, 1.5)])
+def test_bwd1_merge_units(orc, monkeypatch, rank, nlook, s):
+    """Planned f3_bwd1 merge units (runs of one-slot tiles of one (i1, i0) pair
+    whose GEMMs run once on the summed S rows; the default): gradients within
+    the tolerance of the unmerged path and of the oracle, deterministic
+    (two tables, bitwise equal), and the post-SGD cores of the fused step
+    within tolerance; Zipf 1.05 / 1.2 / 1.5 (long runs of hot-pair tiles)."""
+    p = tt.plan_shapes(10131227, 16, 3, rank, [200, 220, 250], [2, 2, 4])
+    rng = np.random.default_rng(nlook + rank + int(10 * s))
+    base = tt.generate_zipfian_batch(p.num_rows, s, 5, nlook, 1)
+    nb = max(1, nlook // 2)
+    cuts = np.sort(rng.integers(0, nlook + 1, nb - 1))
+    off = np.concatenate([[0], cuts, [nlook]]).astype(np.int64)
+    b = tt.IndexBatch(base.indices.astype(np.int64), off, rng.uniform(-2, 2, nlook), tt.Pooling.Sum)
+    g = rng.standard_normal((nb, 16)).astype(np.float32)
+    grads = []
+    for merge, name in (("1", "m1a"), ("1", "m1b"), ("0", "m0")):
+        monkeypatch.setenv("TTGPU_MERGE1", merge)
+        t, cores = make_table(p, np.float32, 9, name, scale=0.3)
+        res = tt.forward_bags(t, b)
+        grads.append(tt.backward_bags(t, b, res.context, g).cores)
+    for k in range(3):
+        assert np.array_equal(grads[0][k], grads[1][k]), k
+        assert scaled_max_err(grads[0][k], grads[2][k]) <= GRAD_TOL, k
+    if nlook <= 4096:
+        want = orc.backward(as_oplan(p), cores, b.indices, b.offsets, g, b.weights, 0)
+        for k in range(3):
+            assert scaled_max_err(grads[0][k], want[k]) <= GRAD_TOL
+    # the fused backward + SGD step through the same units equals
+    # backward_bags + sgd_step bit for bit
+    monkeypatch.setenv("TTGPU_MERGE1", "1")
+    a, _ = make_table(p, np.float32, 9, "m1s", scale=0.3)
+    c, _ = make_table(p, np.float32, 9, "m1t", scale=0.3)
+    tt.sgd_step(a, tt.backward_bags(a, b, tt.forward_bags(a, b).context, g), 0.05)
+    c.backward_sgd(tt.forward_bags(c, b).context, b, g, 0.05)
+    for k in range(3):
+        assert np.array_equal(a.core(k), c.core(k)), k
