@@ -1640,6 +1640,7 @@ struct SrowsArgs {
   const uint4* rec;  // sorted key-1 records (nullptr: through perm / d2 / lk_bag / alpha)
   uint8_t* b1ulen;   // f3_bwd1 merge units planned with the ranges (nullptr: one tile per unit)
   const int* tile_one;  // (i1 << 16 | i0) of one-slot tiles, else -1 (f3_fwd)
+  int b1tile, b1cont;   // merge-unit range weights: a tile b1tile + nslots, a continuing tile b1cont
 };
 struct Bwd2Args {
   const Tile* tiles;
@@ -1669,14 +1670,14 @@ struct Bwd2Args {
 // tiles is cut into units of <= kCap tiles (counted from the run's first
 // tile); ulen[t] = tiles from t to the end of its unit, so a CTA whose range
 // starts inside a unit starts a shorter one there.  A continuing tile weighs
-// kBwd1ContCost instead of kBwd1TileCost + 1.
+// wcont (default kBwd1ContCost) instead of wtile + 1 (default kBwd1TileCost + 1).
 constexpr int kBwd1ContCost = 1;
 
 template <int kCap>
 __device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
                                           const int* __restrict__ tile_nslots, int* __restrict__ range,
                                           int G, const int* __restrict__ tile_one,
-                                          uint8_t* __restrict__ ulen) {
+                                          uint8_t* __restrict__ ulen, int wtile, int wcont) {
   using Scan = cub::BlockScan<int, 128>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int run_first[128], run_last[128];
@@ -1707,7 +1708,7 @@ __device__ __forceinline__ void plan_bwd1(const int* __restrict__ ntiles,
         const int jj = b0 + j;
         const bool c = on[j] >= 0 && on[j] == prev;
         if (c) cont |= 1u << jj;
-        wv[jj] = a0 + jj < a1 ? (c ? kBwd1ContCost : kBwd1TileCost + ns[j]) : 0;
+        wv[jj] = a0 + jj < a1 ? (c ? wcont : wtile + ns[j]) : 0;
         prev = on[j];
       }
     }
@@ -1792,7 +1793,8 @@ __global__ void __launch_bounds__(128, 4) f3_srows_bwd2(Geo g, SrowsArgs sa, Bwd
   int b = static_cast<int>(blockIdx.x);
   if (sa.b1range) {  // CTA 0 (first wave) plans f3_bwd1; the roles start at CTA 1
     if (b == 0) {
-      plan_bwd1<D::TT>(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid, sa.tile_one, sa.b1ulen);
+      plan_bwd1<D::TT>(sa.ntiles, sa.tile_nslots, sa.b1range, sa.b1grid, sa.tile_one, sa.b1ulen, sa.b1tile,
+                       sa.b1cont);
       return;
     }
     --b;

@@ -423,7 +423,8 @@ struct F3Runner {
       f3::SrowsArgs sa{t->cores.as<float>(), g.coff2, f.tiles1.as<f3::Tile>(), f.ntiles.as<int>(),
                        f.max_tiles1, f.perm1.as<uint32_t>(), f.d2.as<uint16_t>(),
                        f.slotpos.as<uint16_t>(), f.tile_nslots.as<int>(), f.Sbuf.as<float>(),
-                       plan, grid1, f.rec1.as<uint4>(), ulen, f.tile_one.as<int>()};
+                       plan, grid1, f.rec1.as<uint4>(), ulen, f.tile_one.as<int>(),
+                       t->b1tile, t->b1cont};
       b1plan_ptr = plan;
       b1ulen_ptr = ulen;
       f3::Bwd2Args ba{f.tiles2.as<f3::Tile>(), f.ntiles.as<int>() + 1, f.perm2.as<uint32_t>(),

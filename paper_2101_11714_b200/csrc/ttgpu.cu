@@ -203,6 +203,7 @@ struct ttgpu_table {
   bool fuse_comb = false;      // fast path: f3_bwd1 + f3_combine in one cooperative launch
   bool plan_bwd1 = true;       // fast path: f3_bwd1's ranges planned by f3_srows_bwd2 (TTGPU_PLAN_BWD1=0: in bwd1)
   bool merge1 = true;          // planned f3_bwd1: runs of one-slot tiles of the same (i1, i0) as one unit (TTGPU_MERGE1=0: off)
+  int b1tile = 3, b1cont = 1;  // merge-unit range weights (TTGPU_B1COST=tile,cont; swept: 3,1 best at cfg2)
                                // (TTGPU_FUSE_COMB=1; measured slower: the combine tasks get half the warps)
   // optional phase timing (CUDA events between pipeline phases)
   // Marks recorded while the stream is being captured become event-record nodes of
@@ -1015,6 +1016,7 @@ int ttgpu_create(int64_t num_rows, int64_t emb_dim, int tt_dim, const int64_t* r
       t->plan_bwd1 = !(pb && std::atoi(pb) == 0);
       const char* mg = std::getenv("TTGPU_MERGE1");
       t->merge1 = !(mg && std::atoi(mg) == 0);
+      if (const char* bc = std::getenv("TTGPU_B1COST")) std::sscanf(bc, "%d,%d", &t->b1tile, &t->b1cont);
     }
     std::vector<int64_t> coff;
     t->dp = make_devplan(t->plan, coff, t->total);
