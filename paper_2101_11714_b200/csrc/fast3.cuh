@@ -15,7 +15,9 @@
 //               H(slot) = G0[i0]·G1[i1], y = H·G2[i2]; bags pooled by their last
 //               finished lookup (pool_if_last), single-lookup bags directly
 //   f3_srows    warp per i1-tile: S(slot) = Σ D1, D1 = D2·G2ᵀ
-//   f3_bwd1     per i1-tile (TMA-staged S and G0 rows): dG1 += Σ G0ᵀS, D0 = S·G1ᵀ
+//   f3_bwd1     per i1-tile (TMA-staged S and G0 rows): dG1 += Σ G0ᵀS, D0 = S·G1ᵀ;
+//               runs of one-slot tiles of one (i1, i0) as one unit on their
+//               summed S rows (merge units, planned by plan_bwd1)
 //   f3_bwd2     per i2-tile: dG2 += Σ H(lookup)ᵀ D2 (H rows saved by f3_fwd)
 //   f3_combine  fixed-order folds of the partials per core slice, fused with
 //               the SGD update (or a dense gradient write)
