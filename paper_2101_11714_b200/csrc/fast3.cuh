@@ -404,6 +404,7 @@ struct ScanArgs {
 // group partials -- and the last arriver's sequential fold -- small.
 constexpr int kGroup = 64;
 constexpr int kGroup0 = 32;    // combine: candidate CTA blocks per warp task (dG0; dense for hot i0)
+static_assert(kGroup0 <= 32, "a dG0 combine task takes its candidates in one 32-lane ballot");
 constexpr int kScanKeys = 8;   // keys per f3_scan CTA
 constexpr int kScanThreads = 256;
 
